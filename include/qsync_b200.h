@@ -1,0 +1,176 @@
+/*
+ * qsync_b200.h -- C ABI of the B200-native QSync quantized-operator hot path.
+ *
+ * Every entry point:
+ *   - is extern "C", takes plain pointers/sizes, never throws;
+ *   - returns an int status: QSYNC_OK (0) or (qsync::ErrorKind + 1), the kinds of
+ *     reference errors.hpp:11-26, so a C++ caller re-raises with
+ *     qsync::fail(ErrorKind(status - 1), qsync_last_error()) (errors.hpp:42-44);
+ *     CUDA failures map to QSYNC_ERR_INTERNAL;
+ *   - works on caller-owned DEVICE buffers, stream-ordered on `stream`
+ *     (a cudaStream_t; NULL = legacy default stream), and allocates nothing;
+ *   - is reentrant per stream.
+ *
+ * The reference (/root/reference/proj) has no tensor-level API: its hot path is
+ * consumed as measured costs.  Each entry cites the reference
+ * semantics it implements or the reference interface it replaces.
+ *
+ * GEMM convention for every GEMM entry:  C[m,n] = sum_k A[m,k] * B[n,k]
+ * (row-major, both operands K-contiguous), i.e. Y = X W^T for X [M,K], W [N,K].
+ */
+#ifndef QSYNC_B200_H
+#define QSYNC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* qsync_stream_t; /* cudaStream_t */
+
+/* Status codes: ErrorKind (errors.hpp:11-26) + 1. */
+enum qsync_status {
+    QSYNC_OK = 0,
+    QSYNC_ERR_GRAPH_CYCLE = 1,
+    QSYNC_ERR_VALIDATION = 2,
+    QSYNC_ERR_REFERENCE = 3,
+    QSYNC_ERR_DOMAIN = 4,
+    QSYNC_ERR_MISSING_PROFILE = 5,
+    QSYNC_ERR_MISSING_MODEL = 6,
+    QSYNC_ERR_DEGENERATE_FIT = 7,
+    QSYNC_ERR_STATS_INCOMPLETE = 8,
+    QSYNC_ERR_KIND_MISMATCH = 9,
+    QSYNC_ERR_TOPOLOGY = 10,
+    QSYNC_ERR_ENUMERATION_LIMIT = 11,
+    QSYNC_ERR_INFEASIBLE = 12,
+    QSYNC_ERR_IO = 13,
+    QSYNC_ERR_INTERNAL = 14
+};
+
+/* Element types for the typed entries. */
+enum qsync_dtype { QSYNC_F32 = 0, QSYNC_F16 = 1, QSYNC_BF16 = 2, QSYNC_I8 = 3, QSYNC_I32 = 4 };
+
+/* "<kind>: message" of the last failure on this host thread (errors.hpp:33). */
+const char* qsync_last_error(void);
+/* Kind tag of a status, as error_kind_name (errors.cpp:5-23). */
+const char* qsync_status_name(int status);
+int qsync_abi_version(void);
+/* Number of SMs of the current device (grid sizing), or -1. */
+int qsync_device_sm_count(void);
+
+/* ---------------------------------------------------------------------------
+ * K1  absmax -> scale.  The paper's two-step minmax; the
+ * scale rule s = absmax/127 (s = 1 for an all-zero tensor) is the symmetric
+ * fixed-point grid x_bar = (x - z)/q of PAPER.md:342 with z = 0.
+ * ------------------------------------------------------------------------- */
+/* absmax over n FP32/FP16/BF16 values into *absmax (device float). */
+int qsync_absmax(const void* x, int dtype, int64_t n, float* absmax, qsync_stream_t stream);
+/* absmax of every row of a [rows, cols] matrix (per-channel). */
+int qsync_absmax_rows(const void* x, int dtype, int64_t rows, int64_t cols, float* absmax_rows,
+                      qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K2  quantize to INT8 (round-to-nearest-even, saturating to +-127).
+ * q = sat(rint(x / s)), s derived from absmax as above, FP32 IEEE division.
+ * ------------------------------------------------------------------------- */
+/* Per-tensor: absmax + scale + quantize of a [rows, cols] matrix.  `scale` is a
+ * device float[2]: scale[0] receives s, scale[1] the absmax.  If q_t_f16 != NULL the same quantized values are
+ * also written transposed as FP16 integers, [cols, rows] (the saved activation
+ * operand of the FP16 wgrad GEMM, cost_mapper.cpp:13-15). */
+int qsync_quantize_per_tensor(const void* x, int dtype, int64_t rows, int64_t cols, int8_t* q,
+                              float* scale, uint16_t* q_t_f16, qsync_stream_t stream);
+/* Quantize with a scale already on the device (e.g. delayed / shared scale). */
+int qsync_quantize_with_scale(const void* x, int dtype, int64_t n, const float* scale, int8_t* q,
+                              qsync_stream_t stream);
+/* Per-channel over rows of W [rows, cols] (PAPER.md:426-427 channel-wise
+ * weight).  scales[rows] receives s_r.  If w_t_f16 != NULL, W itself (not the
+ * quantized copy) is also cast to FP16 transposed [cols, rows] -- the dgrad
+ * weight operand of the FP16 backward. */
+int qsync_quantize_per_channel(const float* w, int64_t rows, int64_t cols, int8_t* q,
+                               float* scales, uint16_t* w_t_f16, qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K9  stochastic rounding on the reference RNG stream.
+ * Element i consumes draw i of std::mt19937_64(seed) (indicator.cpp:179-187,
+ * rng.hpp:12-14), reproduced on the device by GF(2) jump-ahead.
+ * ------------------------------------------------------------------------- */
+/* Exact device restatement of qsync::stochastic_round (indicator.cpp:176-193):
+ * FP64 in, int64 rounded + FP64 dequantized out, no clamp.  Domain if q <= 0. */
+int qsync_stochastic_round_f64(const double* x, int64_t n, double q, double zp, uint64_t seed,
+                               int64_t* rounded, double* dequantized, qsync_stream_t stream);
+/* qsync::stochastic_round_float (indicator.cpp:195-200): spacing 2^(e-k). */
+int qsync_stochastic_round_float_f64(const double* x, int64_t n, int e, int k, uint64_t seed,
+                                     double* out, qsync_stream_t stream);
+/* FP32 -> INT8 SR quantization with a device scale (promoted to FP64 as the
+ * reference does), saturated to +-127. */
+int qsync_quantize_sr(const float* x, int64_t n, const float* scale, uint64_t seed, int8_t* q,
+                      qsync_stream_t stream);
+/* Raw stream: out[i] = draw (offset + i) of mt19937_64(seed). */
+int qsync_mt64_draws(uint64_t seed, uint64_t offset, int64_t n, uint64_t* out,
+                     qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K3  dequantize: out = float(q) * s.
+ * ------------------------------------------------------------------------- */
+int qsync_dequantize_per_tensor(const int8_t* q, int64_t n, const float* scale, float* out,
+                                qsync_stream_t stream);
+int qsync_dequantize_per_channel(const int8_t* q, int64_t rows, int64_t cols, const float* scales,
+                                 float* out, qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K4  float casts (CastScheme::FloatToFloat, profile.hpp:19).  RNE.
+ * ------------------------------------------------------------------------- */
+int qsync_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64_t n,
+               qsync_stream_t stream);
+/* [rows, cols] FP32/FP16 -> FP16 copy (optional), FP16 transposed [cols, rows]
+ * (optional) and FP32 column sums (optional; the bias gradient of a Linear).
+ * This is the backward entry of an INT8/FP16 op: the incoming gradient is cast
+ * to the FP16 backward format (cost_mapper.cpp:13-15) for dgrad and wgrad. */
+int qsync_cast_transpose(const void* x, int dtype, int64_t rows, int64_t cols, uint16_t* out,
+                         uint16_t* out_t, float* colsum, qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K5  fused tensor statistics for OpStats (profile.hpp:95-108).
+ * out[0] = ||x||^2 (FP64 accumulation)   -> norm_*_sq
+ * out[1] = absmax
+ * out[2] = q = absmax/127                -> q_act / q_w
+ * out[3] = e = floor(log2(absmax))       -> e_act / e_w / e_grad
+ * out[4] = numel                         -> d_act / d_w / d_grad
+ * `out` is a device double[5]; `workspace` a device buffer of
+ * qsync_stats_workspace_bytes() bytes.
+ * ------------------------------------------------------------------------- */
+size_t qsync_stats_workspace_bytes(void);
+int qsync_tensor_stats(const void* x, int dtype, int64_t n, double* out, void* workspace,
+                       qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K6  INT8 GEMM on tcgen05 (kind::i8, int32 accumulators in TMEM, TMA-fed).
+ * A [M,K] int8, B [N,K] int8, K % 16 == 0.
+ *   c_i32 != NULL : raw int32 accumulators [M,N] (bit-exact parity output);
+ *   c_f32 != NULL : fused dequant epilogue (graph.hpp:38-40: INT8 emits FP32)
+ *                   c = float(acc) * (scale_a[0] * scale_b[n]) (+ bias[n]).
+ *   scale_b may be per-row (b_per_channel=1, [N]) or a device scalar.
+ * ------------------------------------------------------------------------- */
+int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k,
+                  int32_t* c_i32, float* c_f32, const float* scale_a, const float* scale_b,
+                  int b_per_channel, const float* bias, qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K7  FP16/BF16 GEMM on tcgen05 (kind::f16, FP32 accumulators in TMEM).
+ * A [M,K], B [N,K] of ab_dtype (QSYNC_F16 / QSYNC_BF16), K % 8 == 0.
+ * c = alpha * (alpha_dev ? *alpha_dev : 1) * acc (+ bias[n]) (+ c if accumulate)
+ * written as c_dtype (QSYNC_F32 or QSYNC_F16 / QSYNC_BF16).
+ * Used for FP16 forward, dgrad (FP16 out) and wgrad (FP32 out, alpha_dev = the
+ * activation scale of an INT8 op; cost_mapper.cpp:48-50).
+ * ------------------------------------------------------------------------- */
+int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,
+                   void* c, int c_dtype, float alpha, const float* alpha_dev, const float* bias,
+                   int accumulate, qsync_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSYNC_B200_H */

@@ -1,0 +1,82 @@
+// common.cuh -- shared helpers of the qsync_b200 device library (sm_100a only).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "qsync_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "qsync_b200 is written for sm_100a (B200) only"
+#endif
+
+namespace qsb {
+
+// ---- error plumbing (status = ErrorKind + 1, errors.hpp:11-26) -------------
+int set_error(int status, const std::string& msg);
+int check_launch(const char* what);  // cudaGetLastError -> status
+inline int cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return QSYNC_OK;
+    return set_error(QSYNC_ERR_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define QSB_TRY(expr)                      \
+    do {                                   \
+        int _st = (expr);                  \
+        if (_st != QSYNC_OK) return _st;   \
+    } while (0)
+#define QSB_REQUIRE(cond, status, msg)                   \
+    do {                                                 \
+        if (!(cond)) return ::qsb::set_error(status, msg); \
+    } while (0)
+
+inline cudaStream_t to_stream(qsync_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// ---- typed loads ----------------------------------------------------------
+template <int DT>
+struct Elem;
+template <>
+struct Elem<QSYNC_F32> {
+    using T = float;
+    __device__ static float f(T v) { return v; }
+};
+template <>
+struct Elem<QSYNC_F16> {
+    using T = __half;
+    __device__ static float f(T v) { return __half2float(v); }
+};
+template <>
+struct Elem<QSYNC_BF16> {
+    using T = __nv_bfloat16;
+    __device__ static float f(T v) { return __bfloat162float(v); }
+};
+
+// Scale rule shared by every quantizer: s = absmax / 127 (IEEE), 1 if all-zero.
+__device__ __forceinline__ float scale_from_absmax(float a) {
+    return a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
+}
+// RNE, saturating to the symmetric INT8 grid [-127, 127].
+__device__ __forceinline__ int quant_rne(float x, float s) {
+    float r = rintf(__fdiv_rn(x, s));
+    r = fminf(fmaxf(r, -127.0f), 127.0f);
+    return static_cast<int>(r);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace qsb

@@ -1,0 +1,669 @@
+// quant.cu -- K1 absmax, K2 RNE quantize, K3 dequantize, K4 casts, K5 statistics.
+//
+// All of these are HBM-bound streaming kernels: 16-byte
+// vector loads/stores, several loads in flight per thread, grids sized as a
+// multiple of the SM count, warp-shuffle reductions.  Semantics follow the
+// oracle (oracle/cpu_ref.c) bit for bit: s = absmax/127 (IEEE), q =
+// sat(rint(x/s)), dequant = float(q)*s.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace qsb {
+
+namespace {
+
+constexpr int kThreads = 512;
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Unpack a 16-byte vector of DT into floats (4 for F32, 8 for F16/BF16).
+template <int DT>
+struct Vec;
+template <>
+struct Vec<QSYNC_F32> {
+    static constexpr int N = 4;
+    __device__ static void unpack(uint4 r, float* f) {
+        f[0] = __uint_as_float(r.x);
+        f[1] = __uint_as_float(r.y);
+        f[2] = __uint_as_float(r.z);
+        f[3] = __uint_as_float(r.w);
+    }
+};
+template <>
+struct Vec<QSYNC_F16> {
+    static constexpr int N = 8;
+    __device__ static void unpack(uint4 r, float* f) {
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+            float2 v = __half22float2(h);
+            f[2 * i] = v.x;
+            f[2 * i + 1] = v.y;
+        }
+    }
+};
+template <>
+struct Vec<QSYNC_BF16> {
+    static constexpr int N = 8;
+    __device__ static void unpack(uint4 r, float* f) {
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+            float2 v = __bfloat1622float2(h);
+            f[2 * i] = v.x;
+            f[2 * i + 1] = v.y;
+        }
+    }
+};
+
+__host__ __device__ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm = 4) {
+    int64_t want = (work_items + per_block - 1) / per_block;
+    int64_t cap = static_cast<int64_t>(sm_count()) * max_blocks_per_sm;
+    return static_cast<int>(std::max<int64_t>(1, std::min(want, cap)));
+}
+
+// ---------------------------------------------------------------------------
+// K1: per-tensor absmax.  Grid-stride, 4 x 16B loads in flight per thread,
+// warp shuffle + smem block reduce, one atomicMax per block on the float bits
+// (valid ordering for non-negative floats; max is order-independent, so the
+// result is deterministic).
+// ---------------------------------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_absmax(const typename Elem<DT>::T* __restrict__ x,
+                                                     int64_t n, unsigned* __restrict__ out,
+                                                     int vec_ok) {
+    using V = Vec<DT>;
+    constexpr int U = 4;
+    float m = 0.0f;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t done = 0;
+    if (vec_ok) {
+        const int64_t nv = n / V::N;
+        const uint4* xv = reinterpret_cast<const uint4*>(x);
+        int64_t i = tid;
+        for (; i + (U - 1) * stride < nv; i += U * stride) {
+            uint4 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) r[u] = ld_stream(xv + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float f[V::N];
+                V::unpack(r[u], f);
+#pragma unroll
+                for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(f[j]));
+            }
+        }
+        for (; i < nv; i += stride) {
+            float f[V::N];
+            V::unpack(ld_stream(xv + i), f);
+#pragma unroll
+            for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(f[j]));
+        }
+        done = nv * V::N;
+    }
+    for (int64_t i = done + tid; i < n; i += stride) m = fmaxf(m, fabsf(Elem<DT>::f(x[i])));
+
+    __shared__ float red[32];
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0 && m > 0.0f) atomicMax(out, __float_as_uint(m));
+    }
+}
+
+// absmax of each row, one warp per row.
+template <int DT>
+__global__ void __launch_bounds__(256) k_absmax_rows(const typename Elem<DT>::T* __restrict__ x,
+                                                     int64_t rows, int64_t cols,
+                                                     float* __restrict__ out) {
+    const int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const typename Elem<DT>::T* xr = x + row * cols;
+    float m = 0.0f;
+    for (int64_t c = lane; c < cols; c += 32) m = fmaxf(m, fabsf(Elem<DT>::f(xr[c])));
+    m = warp_max(m);
+    if (lane == 0) out[row] = m;
+}
+
+// ---------------------------------------------------------------------------
+// K2: RNE quantize with the scale derived on the fly from absmax (absmax_in
+// holds float bits written by k_absmax).  16 elements per thread-iteration:
+// 4 (F32) or 2 (F16/BF16) 16B loads, one 16B store.  Block 0 publishes s.
+// ---------------------------------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::T* __restrict__ x,
+                                                       int64_t n, const float* __restrict__ absmax_in,
+                                                       const float* __restrict__ scale_in,
+                                                       int8_t* __restrict__ q,
+                                                       float* __restrict__ scale_out, int vec_ok) {
+    using V = Vec<DT>;
+    constexpr int LOADS = 16 / V::N;
+    const float s = scale_in ? *scale_in : scale_from_absmax(*absmax_in);
+    if (scale_out && blockIdx.x == 0 && threadIdx.x == 0) *scale_out = s;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t done = 0;
+    if (vec_ok) {
+        const int64_t n16 = n / 16;
+        const uint4* xv = reinterpret_cast<const uint4*>(x);
+        uint4* qv = reinterpret_cast<uint4*>(q);
+        for (int64_t i = tid; i < n16; i += stride) {
+            uint4 r[LOADS];
+#pragma unroll
+            for (int u = 0; u < LOADS; ++u) r[u] = ld_stream(xv + i * LOADS + u);
+            uint32_t packed[4];
+#pragma unroll
+            for (int u = 0; u < LOADS; ++u) {
+                float f[V::N];
+                V::unpack(r[u], f);
+#pragma unroll
+                for (int j = 0; j < V::N; j += 4) {
+                    uint32_t b0 = static_cast<uint8_t>(quant_rne(f[j], s));
+                    uint32_t b1 = static_cast<uint8_t>(quant_rne(f[j + 1], s));
+                    uint32_t b2 = static_cast<uint8_t>(quant_rne(f[j + 2], s));
+                    uint32_t b3 = static_cast<uint8_t>(quant_rne(f[j + 3], s));
+                    packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+                }
+            }
+            qv[i] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        }
+        done = n16 * 16;
+    }
+    for (int64_t i = done + tid; i < n; i += stride)
+        q[i] = static_cast<int8_t>(quant_rne(Elem<DT>::f(x[i]), s));
+}
+
+// ---------------------------------------------------------------------------
+// 2-D tile kernels (64 rows x 32 cols, block 32 x 8): quantize / cast with a
+// transposed FP16 copy, optional column sums.  Loads and the row-major store
+// are coalesced along cols; the transposed store is coalesced along rows via
+// a padded smem tile.
+// mode 0: quantize with absmax-derived scale -> q (int8) + q_t (fp16 ints)
+// mode 1: cast -> out (fp16) + out_t (fp16) + colsum (fp32, atomics)
+// ---------------------------------------------------------------------------
+constexpr int TR = 64, TC = 32;
+
+template <int DT, int MODE>
+__global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __restrict__ x,
+                                              int64_t rows, int64_t cols,
+                                              const float* __restrict__ absmax_in,
+                                              int8_t* __restrict__ q, uint16_t* __restrict__ out,
+                                              uint16_t* __restrict__ out_t,
+                                              float* __restrict__ colsum,
+                                              float* __restrict__ scale_out) {
+    __shared__ __half tile[TC][TR + 2];
+    __shared__ float csum[8][TC];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t r0 = blockIdx.y * (int64_t)TR, c0 = blockIdx.x * (int64_t)TC;
+    const int64_t c = c0 + tx;
+    float s = 1.0f;
+    if (MODE == 0) {
+        s = scale_from_absmax(*absmax_in);
+        if (scale_out && blockIdx.x == 0 && blockIdx.y == 0 && tx == 0 && ty == 0) *scale_out = s;
+    }
+    float cs = 0.0f;
+#pragma unroll
+    for (int j = 0; j < TR / 8; ++j) {
+        const int rl = ty + 8 * j;
+        const int64_t r = r0 + rl;
+        __half h = __float2half_rn(0.0f);
+        if (r < rows && c < cols) {
+            const float v = Elem<DT>::f(x[r * cols + c]);
+            if (MODE == 0) {
+                const int qi = quant_rne(v, s);
+                if (q) q[r * cols + c] = static_cast<int8_t>(qi);
+                h = __int2half_rn(qi);
+            } else {
+                h = __float2half_rn(v);
+                if (out) out[r * cols + c] = __half_as_ushort(h);
+                cs += v;
+            }
+        }
+        tile[tx][rl] = h;
+    }
+    if (MODE == 1 && colsum) csum[ty][tx] = cs;
+    __syncthreads();
+    if (out_t) {
+        // Each warp writes columns ty, ty+8, ty+16, ty+24 of the tile as rows of out_t.
+        for (int cc = ty; cc < TC; cc += 8) {
+            const int64_t oc = c0 + cc;
+            if (oc >= cols) continue;
+#pragma unroll
+            for (int k = 0; k < TR / 32; ++k) {
+                const int rl = tx + 32 * k;
+                const int64_t r = r0 + rl;
+                if (r < rows) out_t[oc * rows + r] = __half_as_ushort(tile[cc][rl]);
+            }
+        }
+    }
+    if (MODE == 1 && colsum && ty == 0 && c < cols) {
+        float t = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t += csum[j][tx];
+        atomicAdd(colsum + c, t);
+    }
+}
+
+// Per-channel quantize: one warp per row, absmax pass then quantize pass (the
+// second read of the row hits L1/L2).
+__global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w, int64_t rows,
+                                                    int64_t cols, int8_t* __restrict__ q,
+                                                    float* __restrict__ scales) {
+    const int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float* wr = w + row * cols;
+    int8_t* qr = q + row * cols;
+    const bool vec = (cols % 4 == 0) && aligned16(wr);
+    float m = 0.0f;
+    if (vec) {
+        const float4* v = reinterpret_cast<const float4*>(wr);
+        for (int64_t c = lane; c < cols / 4; c += 32) {
+            float4 f = v[c];
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(f.x), fabsf(f.y)), fmaxf(fabsf(f.z), fabsf(f.w))));
+        }
+    } else {
+        for (int64_t c = lane; c < cols; c += 32) m = fmaxf(m, fabsf(wr[c]));
+    }
+    m = warp_max(m);
+    const float s = scale_from_absmax(m);
+    if (lane == 0) scales[row] = s;
+    if (vec && (reinterpret_cast<uintptr_t>(qr) & 3u) == 0) {
+        const float4* v = reinterpret_cast<const float4*>(wr);
+        uint32_t* qo = reinterpret_cast<uint32_t*>(qr);
+        for (int64_t c = lane; c < cols / 4; c += 32) {
+            float4 f = v[c];
+            qo[c] = static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.x, s))) |
+                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.y, s))) << 8) |
+                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.z, s))) << 16) |
+                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.w, s))) << 24);
+        }
+    } else {
+        for (int64_t c = lane; c < cols; c += 32) qr[c] = static_cast<int8_t>(quant_rne(wr[c], s));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: dequantize, 16 int8 in -> 16 floats out per thread-iteration.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_dequant(const int8_t* __restrict__ q, int64_t n,
+                                                      const float* __restrict__ scale,
+                                                      float* __restrict__ out, int vec_ok) {
+    const float s = *scale;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t done = 0;
+    if (vec_ok) {
+        const int64_t n16 = n / 16;
+        const uint4* qv = reinterpret_cast<const uint4*>(q);
+        float4* ov = reinterpret_cast<float4*>(out);
+        for (int64_t i = tid; i < n16; i += stride) {
+            uint4 r = ld_stream(qv + i);
+            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float4 f;
+                f.x = static_cast<float>(static_cast<int8_t>(w[j] & 0xff)) * s;
+                f.y = static_cast<float>(static_cast<int8_t>((w[j] >> 8) & 0xff)) * s;
+                f.z = static_cast<float>(static_cast<int8_t>((w[j] >> 16) & 0xff)) * s;
+                f.w = static_cast<float>(static_cast<int8_t>(w[j] >> 24)) * s;
+                __stcs(ov + i * 4 + j, f);
+            }
+        }
+        done = n16 * 16;
+    }
+    for (int64_t i = done + tid; i < n; i += stride) out[i] = static_cast<float>(q[i]) * s;
+}
+
+__global__ void __launch_bounds__(256) k_dequant_rows(const int8_t* __restrict__ q, int64_t rows,
+                                                      int64_t cols, const float* __restrict__ scales,
+                                                      float* __restrict__ out) {
+    const int64_t row = blockIdx.y;
+    const float s = scales[row];
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols;
+         c += (int64_t)gridDim.x * blockDim.x)
+        out[row * cols + c] = static_cast<float>(q[row * cols + c]) * s;
+}
+
+// ---------------------------------------------------------------------------
+// K4: elementwise casts (RNE).
+// ---------------------------------------------------------------------------
+template <int SD, int DD>
+struct Store;
+template <int SD>
+struct Store<SD, QSYNC_F32> {
+    using T = float;
+    __device__ static T cvt(float v) { return v; }
+};
+template <int SD>
+struct Store<SD, QSYNC_F16> {
+    using T = __half;
+    __device__ static T cvt(float v) { return __float2half_rn(v); }
+};
+template <int SD>
+struct Store<SD, QSYNC_BF16> {
+    using T = __nv_bfloat16;
+    __device__ static T cvt(float v) { return __float2bfloat16_rn(v); }
+};
+
+template <int SD, int DD>
+__global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* __restrict__ x,
+                                                   typename Store<SD, DD>::T* __restrict__ out,
+                                                   int64_t n) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 8;
+    int64_t i = tid * U;
+    for (; i + U <= n; i += stride * U) {
+        float f[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) f[u] = Elem<SD>::f(x[i + u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) out[i + u] = Store<SD, DD>::cvt(f[u]);
+    }
+    for (; i < n; ++i) out[i] = Store<SD, DD>::cvt(Elem<SD>::f(x[i]));
+}
+
+// ---------------------------------------------------------------------------
+// K5: statistics.  Pass 1: per-block (sum x^2 in FP64, absmax) partials.
+// Pass 2: one block reduces the partials in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int kStatsBlocks = 1024;
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_stats_partial(const typename Elem<DT>::T* __restrict__ x,
+                                                            int64_t n, double* __restrict__ part,
+                                                            int vec_ok) {
+    using V = Vec<DT>;
+    double ss = 0.0;
+    float m = 0.0f;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t done = 0;
+    if (vec_ok) {
+        const int64_t nv = n / V::N;
+        const uint4* xv = reinterpret_cast<const uint4*>(x);
+        for (int64_t i = tid; i < nv; i += stride) {
+            float f[V::N];
+            V::unpack(ld_stream(xv + i), f);
+#pragma unroll
+            for (int j = 0; j < V::N; ++j) {
+                m = fmaxf(m, fabsf(f[j]));
+                ss = fma(static_cast<double>(f[j]), static_cast<double>(f[j]), ss);
+            }
+        }
+        done = nv * V::N;
+    }
+    for (int64_t i = done + tid; i < n; i += stride) {
+        const float v = Elem<DT>::f(x[i]);
+        m = fmaxf(m, fabsf(v));
+        ss = fma(static_cast<double>(v), static_cast<double>(v), ss);
+    }
+    __shared__ double rs[32];
+    __shared__ float rm[32];
+    ss = warp_sum(ss);
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) {
+        rs[threadIdx.x >> 5] = ss;
+        rm[threadIdx.x >> 5] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const bool live = threadIdx.x < (blockDim.x >> 5);
+        ss = warp_sum(live ? rs[threadIdx.x] : 0.0);
+        m = warp_max(live ? rm[threadIdx.x] : 0.0f);
+        if (threadIdx.x == 0) {
+            part[2 * blockIdx.x] = ss;
+            part[2 * blockIdx.x + 1] = static_cast<double>(m);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_stats_final(const double* __restrict__ part, int nparts,
+                                                      int64_t n, double* __restrict__ out) {
+    __shared__ double rs[32];
+    __shared__ double rm[32];
+    double ss = 0.0, m = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+        ss += part[2 * i];
+        m = fmax(m, part[2 * i + 1]);
+    }
+    ss = warp_sum(ss);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) {
+        rs[threadIdx.x >> 5] = ss;
+        rm[threadIdx.x >> 5] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0, mm = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            t += rs[w];
+            mm = fmax(mm, rm[w]);
+        }
+        const float a = static_cast<float>(mm);
+        out[0] = t;
+        out[1] = mm;
+        out[2] = static_cast<double>(scale_from_absmax(a));
+        out[3] = a > 0.0f ? floor(log2(mm)) : 0.0;
+        out[4] = static_cast<double>(n);
+    }
+}
+
+template <template <int> class F, typename... Args>
+int dispatch_dtype(int dtype, Args&&... args) {
+    switch (dtype) {
+        case QSYNC_F32: return F<QSYNC_F32>::run(args...);
+        case QSYNC_F16: return F<QSYNC_F16>::run(args...);
+        case QSYNC_BF16: return F<QSYNC_BF16>::run(args...);
+        default: return set_error(QSYNC_ERR_DOMAIN, "unsupported dtype " + std::to_string(dtype));
+    }
+}
+
+template <int DT>
+struct AbsmaxRun {
+    static int run(const void* x, int64_t n, float* absmax, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        QSB_TRY(cuda_status(cudaMemsetAsync(absmax, 0, sizeof(float), st), "memset"));
+        if (n == 0) return QSYNC_OK;
+        const int vec = aligned16(x);
+        const int grid = grid_for(n / Vec<DT>::N + 1, kThreads * 4);
+        k_absmax<DT><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n,
+                                                reinterpret_cast<unsigned*>(absmax), vec);
+        return check_launch("k_absmax");
+    }
+};
+
+template <int DT>
+struct AbsmaxRowsRun {
+    static int run(const void* x, int64_t rows, int64_t cols, float* out, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        if (rows == 0) return QSYNC_OK;
+        k_absmax_rows<DT><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
+            static_cast<const T*>(x), rows, cols, out);
+        return check_launch("k_absmax_rows");
+    }
+};
+
+template <int DT>
+struct QuantRun {
+    // scale[0] <- s, scale[1] <- absmax (scratch + output).
+    static int run(const void* x, int64_t rows, int64_t cols, int8_t* q, float* scale,
+                   uint16_t* q_t, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        const int64_t n = rows * cols;
+        QSB_TRY(AbsmaxRun<DT>::run(x, n, scale + 1, st));
+        if (q_t && n > 0) {
+            dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
+            k_tile<DT, 0><<<grid, dim3(32, 8), 0, st>>>(static_cast<const T*>(x), rows, cols,
+                                                        scale + 1, q, nullptr, q_t, nullptr, scale);
+            return check_launch("k_tile<quant>");
+        }
+        const int vec = aligned16(x) && aligned16(q);
+        const int grid = grid_for(n / 16 + 1, kThreads, 4);
+        k_quantize<DT><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, scale + 1, nullptr,
+                                                  q, scale, vec);
+        return check_launch("k_quantize");
+    }
+};
+
+template <int DT>
+struct QuantScaleRun {
+    static int run(const void* x, int64_t n, const float* scale, int8_t* q, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        if (n == 0) return QSYNC_OK;
+        const int vec = aligned16(x) && aligned16(q);
+        const int grid = grid_for(n / 16 + 1, kThreads, 4);
+        k_quantize<DT><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, nullptr, scale, q,
+                                                  nullptr, vec);
+        return check_launch("k_quantize");
+    }
+};
+
+template <int DT>
+struct CastTRun {
+    static int run(const void* x, int64_t rows, int64_t cols, uint16_t* out, uint16_t* out_t,
+                   float* colsum, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        if (colsum) QSB_TRY(cuda_status(cudaMemsetAsync(colsum, 0, sizeof(float) * cols, st), "memset"));
+        if (rows == 0 || cols == 0) return QSYNC_OK;
+        dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
+        k_tile<DT, 1><<<grid, dim3(32, 8), 0, st>>>(static_cast<const T*>(x), rows, cols, nullptr,
+                                                    nullptr, out, out_t, colsum, nullptr);
+        return check_launch("k_tile<cast>");
+    }
+};
+
+template <int DT>
+struct StatsRun {
+    static int run(const void* x, int64_t n, double* out, void* ws, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        const int vec = aligned16(x);
+        int grid = grid_for(n / Vec<DT>::N + 1, kThreads * 2, 4);
+        grid = std::min(grid, kStatsBlocks);
+        double* part = static_cast<double*>(ws);
+        k_stats_partial<DT><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, part, vec);
+        QSB_TRY(check_launch("k_stats_partial"));
+        k_stats_final<<<1, 1024, 0, st>>>(part, grid, n, out);
+        return check_launch("k_stats_final");
+    }
+};
+
+}  // namespace
+
+}  // namespace qsb
+
+using namespace qsb;
+
+extern "C" {
+
+int qsync_absmax(const void* x, int dtype, int64_t n, float* absmax, qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    return dispatch_dtype<AbsmaxRun>(dtype, x, n, absmax, to_stream(stream));
+}
+
+int qsync_absmax_rows(const void* x, int dtype, int64_t rows, int64_t cols, float* out,
+                      qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
+    return dispatch_dtype<AbsmaxRowsRun>(dtype, x, rows, cols, out, to_stream(stream));
+}
+
+int qsync_quantize_per_tensor(const void* x, int dtype, int64_t rows, int64_t cols, int8_t* q,
+                              float* scale, uint16_t* q_t_f16, qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
+    QSB_REQUIRE(scale != nullptr, QSYNC_ERR_VALIDATION, "scale buffer (float[2]) is required");
+    return dispatch_dtype<QuantRun>(dtype, x, rows, cols, q, scale, q_t_f16, to_stream(stream));
+}
+
+int qsync_quantize_with_scale(const void* x, int dtype, int64_t n, const float* scale, int8_t* q,
+                              qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    return dispatch_dtype<QuantScaleRun>(dtype, x, n, scale, q, to_stream(stream));
+}
+
+int qsync_quantize_per_channel(const float* w, int64_t rows, int64_t cols, int8_t* q,
+                               float* scales, uint16_t* w_t_f16, qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
+    cudaStream_t st = to_stream(stream);
+    if (rows == 0) return QSYNC_OK;
+    k_quant_rows<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(w, rows, cols, q, scales);
+    QSB_TRY(check_launch("k_quant_rows"));
+    if (w_t_f16) return CastTRun<QSYNC_F32>::run(w, rows, cols, nullptr, w_t_f16, nullptr, st);
+    return QSYNC_OK;
+}
+
+int qsync_dequantize_per_tensor(const int8_t* q, int64_t n, const float* scale, float* out,
+                                qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    if (n == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int vec = aligned16(q) && aligned16(out);
+    k_dequant<<<grid_for(n / 16 + 1, kThreads, 4), kThreads, 0, st>>>(q, n, scale, out, vec);
+    return check_launch("k_dequant");
+}
+
+int qsync_dequantize_per_channel(const int8_t* q, int64_t rows, int64_t cols, const float* scales,
+                                 float* out, qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
+    QSB_REQUIRE(rows < 65536, QSYNC_ERR_DOMAIN, "per-channel dequantize supports < 65536 rows");
+    if (rows == 0 || cols == 0) return QSYNC_OK;
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>((cols + 255) / 256, 64)), static_cast<unsigned>(rows));
+    k_dequant_rows<<<grid, 256, 0, to_stream(stream)>>>(q, rows, cols, scales, out);
+    return check_launch("k_dequant_rows");
+}
+
+int qsync_cast(const void* x, int src, void* out, int dst, int64_t n, qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    if (n == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int grid = grid_for(n / 8 + 1, kThreads, 4);
+#define QSB_CAST(S, D)                                                                     \
+    if (src == S && dst == D) {                                                            \
+        k_cast<S, D><<<grid, kThreads, 0, st>>>(static_cast<const typename Elem<S>::T*>(x), \
+                                                static_cast<typename Store<S, D>::T*>(out), n); \
+        return check_launch("k_cast");                                                     \
+    }
+    QSB_CAST(QSYNC_F32, QSYNC_F16)
+    QSB_CAST(QSYNC_F32, QSYNC_BF16)
+    QSB_CAST(QSYNC_F16, QSYNC_F32)
+    QSB_CAST(QSYNC_BF16, QSYNC_F32)
+    QSB_CAST(QSYNC_F16, QSYNC_BF16)
+    QSB_CAST(QSYNC_BF16, QSYNC_F16)
+#undef QSB_CAST
+    return set_error(QSYNC_ERR_DOMAIN, "unsupported cast " + std::to_string(src) + "->" + std::to_string(dst));
+}
+
+int qsync_cast_transpose(const void* x, int dtype, int64_t rows, int64_t cols, uint16_t* out,
+                         uint16_t* out_t, float* colsum, qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
+    QSB_REQUIRE(rows / TR < 65535, QSYNC_ERR_DOMAIN, "too many rows for cast_transpose");
+    return dispatch_dtype<CastTRun>(dtype, x, rows, cols, out, out_t, colsum, to_stream(stream));
+}
+
+size_t qsync_stats_workspace_bytes(void) { return sizeof(double) * 2 * kStatsBlocks; }
+
+int qsync_tensor_stats(const void* x, int dtype, int64_t n, double* out, void* workspace,
+                       qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    QSB_REQUIRE(workspace != nullptr, QSYNC_ERR_VALIDATION, "stats workspace is required");
+    return dispatch_dtype<StatsRun>(dtype, x, n, out, workspace, to_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,215 @@
+"""Tensor-level front end of the C ABI (torch tensors are plumbing: device memory
+and the current CUDA stream).  Every function launches this package's sm_100a
+kernels through ``libqsync_b200.so``; nothing here computes on the CPU.
+
+Numerics: symmetric INT8 grid, s = absmax/127 (IEEE FP32),
+q = sat(rint(x/s)) in [-127, 127]; INT8 GEMMs accumulate in int32 and emit FP32
+(graph.hpp:38-40); the FP16 backward emits dgrad in FP16 and wgrad in FP32
+(cost_mapper.cpp:13-15, :48-50).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import BF16, F16, F32, QsyncError, call
+
+_DT = {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _req(t: torch.Tensor, name: str, dtypes=None) -> None:
+    if not t.is_cuda:
+        raise QsyncError(2, f"validation: {name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise QsyncError(2, f"validation: {name} must be contiguous")
+    if dtypes is not None and t.dtype not in dtypes:
+        raise QsyncError(4, f"domain: {name} has unsupported dtype {t.dtype}")
+
+
+# --------------------------------------------------------------------------- K1
+def absmax(x: torch.Tensor) -> torch.Tensor:
+    _req(x, "x", _DT)
+    out = torch.empty(1, device=x.device, dtype=torch.float32)
+    call("qsync_absmax", _ptr(x), _DT[x.dtype], x.numel(), _ptr(out), _stream())
+    return out
+
+
+def absmax_rows(x: torch.Tensor) -> torch.Tensor:
+    _req(x, "x", _DT)
+    rows = x.shape[0]
+    out = torch.empty(rows, device=x.device, dtype=torch.float32)
+    call("qsync_absmax_rows", _ptr(x), _DT[x.dtype], rows, x.numel() // max(rows, 1), _ptr(out),
+         _stream())
+    return out
+
+
+# --------------------------------------------------------------------------- K2
+def quantize_per_tensor(x: torch.Tensor, transposed_f16: bool = False, out=None):
+    """Per-tensor RNE INT8 quantization of a 2-D (or flattened) tensor.
+
+    Returns (q int8 same shape, scale float32[2] = {s, absmax}, q_t f16 [cols, rows] or None).
+    """
+    _req(x, "x", _DT)
+    rows = x.shape[0] if x.dim() >= 2 else 1
+    cols = x.numel() // max(rows, 1)
+    q = out if out is not None else torch.empty(x.shape, device=x.device, dtype=torch.int8)
+    scale = torch.empty(2, device=x.device, dtype=torch.float32)
+    qt = torch.empty((cols, rows), device=x.device, dtype=torch.float16) if transposed_f16 else None
+    call("qsync_quantize_per_tensor", _ptr(x), _DT[x.dtype], rows, cols, _ptr(q), _ptr(scale),
+         _ptr(qt), _stream())
+    return q, scale, qt
+
+
+def quantize_with_scale(x: torch.Tensor, scale: torch.Tensor) -> torch.Tensor:
+    _req(x, "x", _DT)
+    q = torch.empty(x.shape, device=x.device, dtype=torch.int8)
+    call("qsync_quantize_with_scale", _ptr(x), _DT[x.dtype], x.numel(), _ptr(scale), _ptr(q),
+         _stream())
+    return q
+
+
+def quantize_per_channel(w: torch.Tensor, transposed_f16: bool = False):
+    """Per-output-channel (row) INT8 quantization of W [N, K]; optional FP16 W^T."""
+    _req(w, "w", (torch.float32,))
+    rows, cols = w.shape
+    q = torch.empty_like(w, dtype=torch.int8)
+    scales = torch.empty(rows, device=w.device, dtype=torch.float32)
+    wt = torch.empty((cols, rows), device=w.device, dtype=torch.float16) if transposed_f16 else None
+    call("qsync_quantize_per_channel", _ptr(w), rows, cols, _ptr(q), _ptr(scales), _ptr(wt),
+         _stream())
+    return q, scales, wt
+
+
+# --------------------------------------------------------------------------- K9
+def stochastic_round(x: torch.Tensor, q: float, zp: float, seed: int):
+    """Device qsync::stochastic_round (indicator.cpp:176-193): returns (rounded int64, deq f64)."""
+    _req(x, "x", (torch.float64,))
+    r = torch.empty(x.shape, device=x.device, dtype=torch.int64)
+    d = torch.empty(x.shape, device=x.device, dtype=torch.float64)
+    call("qsync_stochastic_round_f64", _ptr(x), x.numel(), float(q), float(zp), int(seed), _ptr(r),
+         _ptr(d), _stream())
+    return r, d
+
+
+def stochastic_round_float(x: torch.Tensor, e: int, k: int, seed: int) -> torch.Tensor:
+    _req(x, "x", (torch.float64,))
+    d = torch.empty(x.shape, device=x.device, dtype=torch.float64)
+    call("qsync_stochastic_round_float_f64", _ptr(x), x.numel(), int(e), int(k), int(seed),
+         _ptr(d), _stream())
+    return d
+
+
+def quantize_sr(x: torch.Tensor, scale: torch.Tensor, seed: int) -> torch.Tensor:
+    _req(x, "x", (torch.float32,))
+    q = torch.empty(x.shape, device=x.device, dtype=torch.int8)
+    call("qsync_quantize_sr", _ptr(x), x.numel(), _ptr(scale), int(seed), _ptr(q), _stream())
+    return q
+
+
+def mt64_draws(seed: int, n: int, offset: int = 0, device="cuda") -> torch.Tensor:
+    out = torch.empty(n, device=device, dtype=torch.int64)  # uint64 bits
+    call("qsync_mt64_draws", int(seed), int(offset), int(n), _ptr(out), _stream())
+    return out
+
+
+# --------------------------------------------------------------------------- K3
+def dequantize_per_tensor(q: torch.Tensor, scale: torch.Tensor) -> torch.Tensor:
+    _req(q, "q", (torch.int8,))
+    out = torch.empty(q.shape, device=q.device, dtype=torch.float32)
+    call("qsync_dequantize_per_tensor", _ptr(q), q.numel(), _ptr(scale), _ptr(out), _stream())
+    return out
+
+
+def dequantize_per_channel(q: torch.Tensor, scales: torch.Tensor) -> torch.Tensor:
+    _req(q, "q", (torch.int8,))
+    out = torch.empty(q.shape, device=q.device, dtype=torch.float32)
+    call("qsync_dequantize_per_channel", _ptr(q), q.shape[0], q.shape[1], _ptr(scales), _ptr(out),
+         _stream())
+    return out
+
+
+# --------------------------------------------------------------------------- K4
+def cast(x: torch.Tensor, dtype: torch.dtype, out=None) -> torch.Tensor:
+    _req(x, "x", _DT)
+    o = out if out is not None else torch.empty(x.shape, device=x.device, dtype=dtype)
+    call("qsync_cast", _ptr(x), _DT[x.dtype], _ptr(o), _DT[dtype], x.numel(), _stream())
+    return o
+
+
+def cast_transpose(x: torch.Tensor, want_out: bool = True, want_t: bool = True,
+                   want_colsum: bool = False):
+    """[rows, cols] -> (FP16 copy, FP16 transpose [cols, rows], FP32 column sums)."""
+    _req(x, "x", (torch.float32, torch.float16))
+    rows = x.shape[0]
+    cols = x.numel() // max(rows, 1)
+    o = torch.empty((rows, cols), device=x.device, dtype=torch.float16) if want_out else None
+    t = torch.empty((cols, rows), device=x.device, dtype=torch.float16) if want_t else None
+    s = torch.empty(cols, device=x.device, dtype=torch.float32) if want_colsum else None
+    call("qsync_cast_transpose", _ptr(x), _DT[x.dtype], rows, cols, _ptr(o), _ptr(t), _ptr(s),
+         _stream())
+    return o, t, s
+
+
+# --------------------------------------------------------------------------- K5
+_ws = {}
+
+
+def _stats_ws(device) -> torch.Tensor:
+    key = (device.type, device.index)
+    if key not in _ws:
+        n = int(_lib.lib().qsync_stats_workspace_bytes())
+        _ws[key] = torch.empty(n, device=device, dtype=torch.uint8)
+    return _ws[key]
+
+
+def tensor_stats(x: torch.Tensor, out=None) -> torch.Tensor:
+    """float64[5] = {||x||^2, absmax, q, e, numel} (OpStats fields, profile.hpp:95-108)."""
+    _req(x, "x", _DT)
+    o = out if out is not None else torch.empty(5, device=x.device, dtype=torch.float64)
+    call("qsync_tensor_stats", _ptr(x), _DT[x.dtype], x.numel(), _ptr(o), _ptr(_stats_ws(x.device)),
+         _stream())
+    return o
+
+
+# --------------------------------------------------------------------------- K6/K7
+def gemm_s8(a: torch.Tensor, b: torch.Tensor, scale_a=None, scale_b=None, bias=None,
+            out_i32: bool = False, out_f32: bool = True, b_per_channel: bool = True,
+            out=None):
+    """C = A B^T on tcgen05 kind::i8.  Returns (c_i32 or None, c_f32 or None)."""
+    _req(a, "a", (torch.int8,))
+    _req(b, "b", (torch.int8,))
+    M, K = a.shape
+    N = b.shape[0]
+    ci = torch.empty((M, N), device=a.device, dtype=torch.int32) if out_i32 else None
+    cf = None
+    if out_f32:
+        cf = out if out is not None else torch.empty((M, N), device=a.device, dtype=torch.float32)
+    call("qsync_gemm_s8", _ptr(a), _ptr(b), M, N, K, _ptr(ci), _ptr(cf), _ptr(scale_a),
+         _ptr(scale_b), int(b_per_channel), _ptr(bias), _stream())
+    return ci, cf
+
+
+def gemm_f16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32, alpha: float = 1.0,
+             alpha_dev=None, bias=None, out=None, accumulate: bool = False) -> torch.Tensor:
+    """C = alpha * A B^T on tcgen05 kind::f16 (FP32 accumulators)."""
+    _req(a, "a", (torch.float16, torch.bfloat16))
+    _req(b, "b", (a.dtype,))
+    M, K = a.shape
+    N = b.shape[0]
+    c = out if out is not None else torch.empty((M, N), device=a.device, dtype=out_dtype)
+    call("qsync_gemm_f16", _ptr(a), _ptr(b), _DT[a.dtype], M, N, K, _ptr(c), _DT[c.dtype],
+         float(alpha), _ptr(alpha_dev), _ptr(bias), int(accumulate), _stream())
+    return c
+
+
+def force_tile_n(bn: int) -> None:
+    """Test hook: pin the GEMM tile N (0 = heuristic)."""
+    call("qsync_gemm_force_tile_n", int(bn))
