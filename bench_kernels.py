@@ -1,0 +1,171 @@
+"""Kernel microbenchmarks (config 5 sweep + GEMM roofline), CUDA-event timed.
+
+    python bench_kernels.py [--sweep] [--gemm] [--json out.json]
+
+Every kernel is launched through the C ABI on torch's current stream and timed
+with CUDA events on that stream after warm-up.  Bandwidth kernels use inputs
+>= 64 MB (larger than nothing in L2 between iterations: a 256 MB scratch write
+flushes L2 between timed iterations for the smaller sizes).  Roofline
+denominators come from MEASURED_PEAKS.json; the INT8 dense peak is measured here
+with cuBLASLt (torch._int_mm) at 8192^3, best of 10.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+from paper_2407_02327_b200 import ops  # noqa: E402
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+
+
+_flush = None
+
+
+def flush_l2():
+    global _flush
+    if _flush is None:
+        _flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    _flush.zero_()
+
+
+def time_ms(fn, iters=20, warmup=3, flush=False) -> float:
+    """Mean device time of fn() over iters (flushing L2 before each if asked)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(iters):
+        if flush:
+            flush_l2()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    times.sort()
+    return sum(times[: max(1, len(times) * 3 // 4)]) / max(1, len(times) * 3 // 4)
+
+
+def int8_peak_cublas(n=8192) -> float:
+    a = torch.randint(-127, 128, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-127, 128, (n, n), dtype=torch.int8, device="cuda").t()
+    best = 1e9
+    for _ in range(3):
+        torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch._int_mm(a, b)
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e))
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def gemm_bench(results: dict) -> None:
+    pk = peaks()
+    i8_peak = int8_peak_cublas()
+    results["int8_peak_cublaslt_tops"] = i8_peak
+    rows = []
+    shapes = [(8192, 8192, 8192), (4096, 2304, 768), (4096, 768, 768), (4096, 3072, 768),
+              (4096, 768, 3072), (64, 1024, 1024)]
+    for (M, N, K) in shapes:
+        a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
+        b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
+        sa = torch.tensor([0.01], device="cuda")
+        sb = torch.rand(N, device="cuda") * 0.01
+        out = torch.empty((M, N), device="cuda")
+        for bn in (0, 128, 256):
+            ops.force_tile_n(bn)
+            t = time_ms(lambda: ops.gemm_s8(a, b, sa, sb, out=out))
+            rows.append({"kind": "i8", "M": M, "N": N, "K": K, "bn": bn, "ms": t,
+                         "tops": 2.0 * M * N * K / (t * 1e-3) / 1e12})
+        ops.force_tile_n(0)
+        ah = torch.randn((M, K), device="cuda").half()
+        bh = torch.randn((N, K), device="cuda").half()
+        outf = torch.empty((M, N), device="cuda")
+        t = time_ms(lambda: ops.gemm_f16(ah, bh, out=outf))
+        rows.append({"kind": "f16", "M": M, "N": N, "K": K, "bn": 0, "ms": t,
+                     "tops": 2.0 * M * N * K / (t * 1e-3) / 1e12})
+        t = time_ms(lambda: torch.matmul(ah, bh.t()))
+        rows.append({"kind": "cublas_f16", "M": M, "N": N, "K": K, "ms": t,
+                     "tops": 2.0 * M * N * K / (t * 1e-3) / 1e12})
+        if M % 8 == 0 and K % 8 == 0 and N % 8 == 0 and M > 16:
+            t = time_ms(lambda: torch._int_mm(a, b.t()))
+            rows.append({"kind": "cublaslt_i8", "M": M, "N": N, "K": K, "ms": t,
+                         "tops": 2.0 * M * N * K / (t * 1e-3) / 1e12})
+    results["gemm"] = rows
+    for r in rows:
+        frac = r["tops"] / (i8_peak if "i8" in r["kind"] else pk["bf16_tflops"])
+        print(f"{r['kind']:12s} {r['M']:5d}x{r['N']:5d}x{r['K']:5d} bn={r.get('bn', '-')!s:4s}"
+              f" {r['ms']*1e3:9.1f} us {r['tops']:8.1f} TOPS  frac={frac:.3f}")
+    print(f"int8 peak (cuBLASLt 8192^3 best of 10): {i8_peak:.1f} TOPS")
+
+
+def sweep_bench(results: dict) -> None:
+    pk = peaks()
+    bw = pk["hbm_gbs"]
+    rows = []
+    for nbytes in [1 << 16, 1 << 20, 1 << 24, 1 << 26, 1 << 28, 1 << 30]:
+        n = nbytes // 4
+        x = torch.randn(n, device="cuda")
+        rowsn = n // 1024
+        x2 = x.view(rowsn, 1024) if rowsn else x.view(1, n)
+        q = torch.empty(n, dtype=torch.int8, device="cuda")
+        sc = torch.tensor([0.01], device="cuda")
+        out = torch.empty(n, device="cuda")
+        h = torch.empty(n, dtype=torch.float16, device="cuda")
+        flush = nbytes < (256 << 20)
+        cases = {
+            "absmax": (lambda: ops.absmax(x), 4),
+            "quantize_per_tensor": (lambda: ops.quantize_per_tensor(x2, out=q.view(x2.shape)), 5),
+            "quantize_with_scale": (lambda: ops.quantize_with_scale(x, sc), 5),
+            "quantize_per_channel": (lambda: ops.quantize_per_channel(x2), 5),
+            "dequantize": (lambda: ops.dequantize_per_tensor(q, sc), 5),
+            "cast_f32_f16": (lambda: ops.cast(x, torch.float16, out=h), 6),
+            "tensor_stats": (lambda: ops.tensor_stats(x), 4),
+        }
+        for name, (fn, bpe) in cases.items():
+            t = time_ms(fn, iters=10 if nbytes >= (1 << 28) else 20, flush=flush)
+            gbs = n * bpe / (t * 1e-3) / 1e9
+            rows.append({"kernel": name, "bytes_in": nbytes, "n": n, "ms": t, "alg_bytes_per_elem": bpe,
+                         "gbs": gbs, "frac_hbm": gbs / bw})
+            print(f"{name:22s} {nbytes/2**20:8.2f} MiB {t*1e3:10.1f} us {gbs:8.1f} GB/s  frac={gbs/bw:.3f}")
+        del x, x2, q, out, h
+        torch.cuda.empty_cache()
+    results["sweep"] = rows
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--gemm", action="store_true")
+    ap.add_argument("--json", default=None)
+    args = ap.parse_args()
+    res: dict = {"peaks": peaks()}
+    if args.gemm or not args.sweep:
+        gemm_bench(res)
+    if args.sweep or not args.gemm:
+        sweep_bench(res)
+    if args.json:
+        with open(args.json, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -68,7 +68,7 @@ def build(verbose: bool = False) -> str:
         log.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
         if r.returncode != 0:
             raise RuntimeError(f"link failed\n{r.stdout}\n{r.stderr}")
-    with open(os.path.join(ROOT, "build", "ptxas.log"), "a") as f:
+    with open(os.path.join(ROOT, "build", "ptxas.log"), "w") as f:
         f.write("\n".join(log))
     if verbose:
         print("\n".join(log))

@@ -19,6 +19,7 @@
 // layer-wise activation x channel-wise weight scales (PAPER.md:426-427,
 // PAPER.md:588-592).
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -46,14 +47,19 @@ struct EpiParams {
     const float* alpha_dev;
     int accumulate;
     uint32_t idesc;
+    int tma_store;  // epilogue writes through tm_c (TMA store / reduce-add)
 };
+
+constexpr int kStageChunkBytes = 32 * 128;  // one warp's 32 rows x 128 B staging chunk
 
 template <int BN>
 struct Cfg {
     static constexpr int kStageBytes = (BM + BN) * BK_BYTES;
     static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
     static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kEpiStageBytes = 4 * 2 * kStageChunkBytes;  // 4 warps x double buffer
+    static constexpr int kSmemBytes =
+        kStages * kStageBytes + kEpiStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ float bits_f(uint32_t v) { return __uint_as_float(v); }
@@ -61,7 +67,7 @@ __device__ __forceinline__ float bits_f(uint32_t v) { return __uint_as_float(v);
 template <bool kI8, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-              const EpiParams p) {
+              const __grid_constant__ CUtensorMap tm_c, const EpiParams p) {
     using C = Cfg<BN>;
     constexpr int kStages = C::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -70,7 +76,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
     uint8_t* smem_a = smem;                              // kStages x [BM rows x 128B]
     uint8_t* smem_b = smem + kStages * BM * BK_BYTES;    // kStages x [BN rows x 128B]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+    uint8_t* smem_stage = smem + kStages * C::kStageBytes;  // 1024-aligned epilogue staging
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_stage + C::kEpiStageBytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + kStages;
     uint64_t* tfull = bars + 2 * kStages;
@@ -90,6 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tm_a);
         ptx::tma_prefetch(&tm_b);
+        if (p.tma_store) ptx::tma_prefetch(&tm_c);
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
@@ -169,103 +177,150 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ===================== epilogue (warps 2..5) =====================
+        // TMEM -> registers -> (scale, bias) -> 128B-swizzled smem staging ->
+        // TMA 2-D store (or reduce-add) of a 32-row x 128-byte chunk per warp,
+        // double-buffered per warp.  Direct global stores remain as the path for
+        // shapes TMA cannot address (row pitch not a multiple of 16 bytes).
         const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        uint8_t* my_stage = smem_stage + (warp - kEpiWarp0) * 2 * kStageChunkBytes;
+        int sbuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         float alpha = p.alpha;
         if (p.alpha_dev) alpha *= *p.alpha_dev;
         const float sa = (kI8 && p.scale_a) ? *p.scale_a : 1.0f;
-        const bool vec4 = (N % 4) == 0;
-        const bool vec8 = (N % 8) == 0;
+        const bool out16 = p.c && p.c_dtype != QSYNC_F32;
+        const bool raw = p.c_i32 != nullptr && p.c == nullptr;
+        const int chunk_cols = out16 ? 64 : 32;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
             const int64_t m0 = static_cast<int64_t>(t % num_m) * BM;
             const int64_t n0 = static_cast<int64_t>(t / num_m) * BN;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
-            const int64_t row = m0 + quad * 32 + lane;
+            const int64_t row0 = m0 + quad * 32;
+            const int64_t row = row0 + lane;
             const bool row_ok = row < M;
+            const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                                   static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t r[32];
-                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                                       static_cast<uint32_t>(acc * BN + c0);
-                ptx::tmem_ld32(taddr, r);
-                ptx::tmem_ld_wait();
+            for (int c0 = 0; c0 < BN; c0 += chunk_cols) {
+                uint32_t w[32];  // the 128 bytes of this thread's row in the chunk
+                uint32_t rawv[32];  // raw accumulators when both outputs are requested
+                float v[32];
                 const int64_t col0 = n0 + c0;
-                if (!row_ok || col0 >= N) continue;
-                const bool full_chunk = col0 + 32 <= N;
+                const int nsub = out16 ? 2 : 1;
+#pragma unroll
+                for (int sub = 0; sub < 2; ++sub) {
+                    if (sub >= nsub) break;
+                    uint32_t r[32];
+                    ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0 + 32 * sub), r);
+                    ptx::tmem_ld_wait();
+                    const int64_t cb = col0 + 32 * sub;
+                    if (raw) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) w[j] = r[j];
+                        continue;
+                    }
+                    if (p.c_i32) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) rawv[j] = r[j];
+                    }
+                    // Per-column factors: lane j loads column cb+j once, then broadcast.
+                    const int64_t mycol = cb + lane;
+                    const bool cok = mycol < N;
+                    float colscale = alpha;
+                    if (kI8) {
+                        float sb = 1.0f;
+                        if (p.scale_b) sb = p.b_per_channel ? (cok ? p.scale_b[mycol] : 0.0f) : *p.scale_b;
+                        colscale = __fmul_rn(sa, sb);
+                    }
+                    const float colbias = (p.bias && cok) ? p.bias[mycol] : 0.0f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float sj = __shfl_sync(0xffffffffu, colscale, j);
+                        const float bj = __shfl_sync(0xffffffffu, colbias, j);
+                        float x = kI8 ? __fmul_rn(__int2float_rn(static_cast<int>(r[j])), sj)
+                                      : __fmul_rn(bits_f(r[j]), sj);
+                        if (p.bias) x = __fadd_rn(x, bj);
+                        v[j] = x;
+                    }
+                    if (out16) {
+                        const bool bf = p.c_dtype == QSYNC_BF16;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const uint32_t lo = bf ? __bfloat16_as_ushort(__float2bfloat16_rn(v[2 * j]))
+                                                   : __half_as_ushort(__float2half_rn(v[2 * j]));
+                            const uint32_t hi = bf ? __bfloat16_as_ushort(__float2bfloat16_rn(v[2 * j + 1]))
+                                                   : __half_as_ushort(__float2half_rn(v[2 * j + 1]));
+                            w[16 * sub + j] = lo | (hi << 16);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
+                    }
+                }
+                if (row0 >= M || col0 >= N) continue;  // warp-uniform: chunk fully outside
+                if (p.tma_store) {
+                    // Free the staging buffer used two chunks ago, then write this
+                    // row's 8 x 16B pieces at their 128B-swizzled positions.
+                    if (lane == 0) ptx::bulk_wait_read<1>();
+                    __syncwarp();
+                    uint8_t* buf = my_stage + sbuf * kStageChunkBytes;
+                    const uint32_t rbase = ptx::smem_u32(buf) + lane * 128;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        ptx::st_shared_v4(rbase + ((c ^ (lane & 7)) << 4), w[4 * c], w[4 * c + 1],
+                                          w[4 * c + 2], w[4 * c + 3]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (p.accumulate)
+                            ptx::tma_reduce_add_2d(&tm_c, buf, static_cast<int32_t>(col0),
+                                                   static_cast<int32_t>(row0));
+                        else
+                            ptx::tma_store_2d(&tm_c, buf, static_cast<int32_t>(col0),
+                                              static_cast<int32_t>(row0));
+                        ptx::bulk_commit();
+                    }
+                    sbuf ^= 1;
+                    continue;
+                }
+                // ---- direct-store path (fully unrolled: keeps w[] in registers) ----
+                if (!row_ok) continue;
                 if (p.c_i32) {
                     int32_t* dst = p.c_i32 + row * N + col0;
-                    if (full_chunk && vec4) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<int4*>(dst + j) =
-                                make_int4(static_cast<int>(r[j]), static_cast<int>(r[j + 1]),
-                                          static_cast<int>(r[j + 2]), static_cast<int>(r[j + 3]));
-                    } else {
-                        for (int j = 0; j < 32 && col0 + j < N; ++j) dst[j] = static_cast<int>(r[j]);
-                    }
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < N) dst[j] = static_cast<int32_t>(raw ? w[j] : rawv[j]);
                 }
-                if (!p.c) continue;
-                float v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int64_t col = col0 + j;
-                    const int64_t cc = col < N ? col : N - 1;
-                    float x;
-                    if (kI8) {
-                        const float sb = p.scale_b ? (p.b_per_channel ? p.scale_b[cc] : *p.scale_b) : 1.0f;
-                        x = __fmul_rn(__int2float_rn(static_cast<int>(r[j])), __fmul_rn(sa, sb));
-                    } else {
-                        x = __fmul_rn(bits_f(r[j]), alpha);
-                    }
-                    if (p.bias) x = __fadd_rn(x, p.bias[cc]);
-                    v[j] = x;
-                }
-                if (p.c_dtype == QSYNC_F32) {
+                if (raw) continue;
+                if (!out16) {
                     float* dst = static_cast<float*>(p.c) + row * N + col0;
-                    if (full_chunk && vec4) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
-                            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                            if (p.accumulate) {
-                                const float4 old = *reinterpret_cast<const float4*>(dst + j);
-                                o.x += old.x;
-                                o.y += old.y;
-                                o.z += old.z;
-                                o.w += old.w;
-                            }
-                            *reinterpret_cast<float4*>(dst + j) = o;
+                    for (int j = 0; j < 32; ++j) {
+                        if (col0 + j < N) {
+                            const float x = __uint_as_float(w[j]);
+                            dst[j] = p.accumulate ? dst[j] + x : x;
                         }
-                    } else {
-                        for (int j = 0; j < 32 && col0 + j < N; ++j)
-                            dst[j] = p.accumulate ? dst[j] + v[j] : v[j];
                     }
                 } else {
-                    // 16-bit outputs (FP16 op outputs, FP16 dgrad).
                     uint16_t* dst = static_cast<uint16_t*>(p.c) + row * N + col0;
                     const bool bf = p.c_dtype == QSYNC_BF16;
-                    auto cvt = [bf](float f) -> uint16_t {
-                        return bf ? __bfloat16_as_ushort(__float2bfloat16_rn(f))
-                                  : __half_as_ushort(__float2half_rn(f));
-                    };
-                    auto back = [bf](uint16_t h) -> float {
-                        return bf ? __bfloat162float(__ushort_as_bfloat16(h))
-                                  : __half2float(__ushort_as_half(h));
-                    };
-                    if (full_chunk && vec8 && !p.accumulate) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            uint4 o;
-                            o.x = cvt(v[j]) | (static_cast<uint32_t>(cvt(v[j + 1])) << 16);
-                            o.y = cvt(v[j + 2]) | (static_cast<uint32_t>(cvt(v[j + 3])) << 16);
-                            o.z = cvt(v[j + 4]) | (static_cast<uint32_t>(cvt(v[j + 5])) << 16);
-                            o.w = cvt(v[j + 6]) | (static_cast<uint32_t>(cvt(v[j + 7])) << 16);
-                            *reinterpret_cast<uint4*>(dst + j) = o;
+                    for (int j = 0; j < 64; ++j) {
+                        if (col0 + j < N) {
+                            const uint16_t h = static_cast<uint16_t>((w[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+                            if (!p.accumulate) {
+                                dst[j] = h;
+                            } else {
+                                const float old = bf ? __bfloat162float(__ushort_as_bfloat16(dst[j]))
+                                                     : __half2float(__ushort_as_half(dst[j]));
+                                const float nv = (bf ? __bfloat162float(__ushort_as_bfloat16(h))
+                                                     : __half2float(__ushort_as_half(h))) + old;
+                                dst[j] = bf ? __bfloat16_as_ushort(__float2bfloat16_rn(nv))
+                                            : __half_as_ushort(__float2half_rn(nv));
+                            }
                         }
-                    } else {
-                        for (int j = 0; j < 32 && col0 + j < N; ++j)
-                            dst[j] = cvt(p.accumulate ? back(dst[j]) + v[j] : v[j]);
                     }
                 }
             }
@@ -276,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
+        if (lane == 0) ptx::bulk_wait<0>();
     }
 
     ptx::tc_fence_before();
@@ -311,6 +367,7 @@ EncodeFn encode_fn() {
 
 int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes,
              int64_t inner, int64_t outer, uint32_t box_inner, uint32_t box_outer) {
+    // (inner extent may be padded by the caller's pitch; here pitch == inner)
     EncodeFn fn = encode_fn();
     QSB_REQUIRE(fn != nullptr, QSYNC_ERR_INTERNAL, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
@@ -343,9 +400,25 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     using C = Cfg<BN>;
     const uint32_t eb = kI8 ? 1 : 2;
     const uint32_t box_k = BK_BYTES / eb;
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mc;
     QSB_TRY(make_map(&ma, a, dt, eb, p.K, p.M, box_k, BM));
     QSB_TRY(make_map(&mb, b, dt, eb, p.K, p.N, box_k, BN));
+    std::memset(&mc, 0, sizeof(mc));
+    // TMA-store epilogue when exactly one output is requested and its rows are
+    // 16-byte pitched and aligned; 16-bit accumulate keeps the direct path.
+    const bool raw = p.c_i32 && !p.c;
+    const bool one_out = (p.c_i32 != nullptr) != (p.c != nullptr);
+    const void* cptr = raw ? static_cast<const void*>(p.c_i32) : p.c;
+    const uint32_t ceb = (raw || p.c_dtype == QSYNC_F32) ? 4 : 2;
+    p.tma_store = one_out && (p.N * ceb) % 16 == 0 && (reinterpret_cast<uintptr_t>(cptr) & 15) == 0 &&
+                  !(p.accumulate && ceb == 2);
+    if (p.tma_store) {
+        const CUtensorMapDataType cdt = raw ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                      : p.c_dtype == QSYNC_F32  ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                      : p.c_dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+        QSB_TRY(make_map(&mc, cptr, cdt, ceb, p.N, p.M, 128 / ceb, 32));
+    }
     static bool configured = false;
     if (!configured) {
         QSB_TRY(cuda_status(cudaFuncSetAttribute(k_gemm_tc<kI8, BN>,
@@ -356,7 +429,7 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     }
     const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
     const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count()));
-    k_gemm_tc<kI8, BN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, p);
+    k_gemm_tc<kI8, BN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, p);
     return check_launch("k_gemm_tc");
 }
 

