@@ -57,6 +57,8 @@ const char* qsync_last_error(void);
 /* Kind tag of a status, as error_kind_name (errors.cpp:5-23). */
 const char* qsync_status_name(int status);
 int qsync_abi_version(void);
+/* Kernels this library has launched in the process (diagnostics / bench). */
+unsigned long long qsync_launch_count(void);
 /* Number of SMs of the current device (grid sizing), or -1. */
 int qsync_device_sm_count(void);
 

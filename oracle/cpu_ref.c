@@ -247,12 +247,13 @@ void ref_cast_f32_f16(const float* x, int64_t n, uint16_t* out) {
 /* Exact int8 x int8 -> int32 (INT32 accumulation). */
 void ref_gemm_s8_tn(const int8_t* a, const int8_t* b, int64_t M, int64_t N, int64_t K,
                     int32_t* c) {
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) collapse(2)
     for (int64_t m = 0; m < M; ++m) {
-        const int8_t* ar = a + m * K;
         for (int64_t n = 0; n < N; ++n) {
+            const int8_t* ar = a + m * K;
             const int8_t* br = b + n * K;
             int32_t acc = 0;
+#pragma omp simd reduction(+ : acc)
             for (int64_t k = 0; k < K; ++k) acc += (int32_t)ar[k] * (int32_t)br[k];
             c[m * N + n] = acc;
         }
@@ -325,6 +326,54 @@ void ref_tensor_stats_f32(const float* x, int64_t n, double* out) {
 }
 
 /* ------------------------------------------------------------------------- */
+/* Helpers for the Linear oracles: operands are rounded once (to binary16 or   */
+/* to their int8 grid values), transposed where the reduction would otherwise  */
+/* stride, and every dot product accumulates in FP64 (omp simd reduction: the  */
+/* summation order is not pinned -- the device accumulates in FP32 -- these     */
+/* outputs are compared within tolerance).                                     */
+/* ------------------------------------------------------------------------- */
+#include <stdlib.h>
+
+static float* round16(const float* x, int64_t n) {
+    float* o = (float*)malloc(sizeof(float) * (size_t)n);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) o[i] = ref_f16_to_f32(ref_f32_to_f16(x[i]));
+    return o;
+}
+
+static float* transpose(const float* x, int64_t rows, int64_t cols) {
+    float* o = (float*)malloc(sizeof(float) * (size_t)(rows * cols));
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < cols; ++c)
+        for (int64_t r = 0; r < rows; ++r) o[c * rows + r] = x[r * cols + c];
+    return o;
+}
+
+static inline double dot(const float* a, const float* b, int64_t n) {
+    double acc = 0.0;
+#pragma omp simd reduction(+ : acc)
+    for (int64_t i = 0; i < n; ++i) acc += (double)a[i] * (double)b[i];
+    return acc;
+}
+
+/* c[m, n] = sum_k a[m, k] b[n, k] in FP64, times alpha, rounded to FP32. */
+static void gemm_tn_f(const float* a, const float* b, int64_t M, int64_t N, int64_t K, double alpha,
+                      float* c) {
+#pragma omp parallel for schedule(static) collapse(2)
+    for (int64_t m = 0; m < M; ++m)
+        for (int64_t n = 0; n < N; ++n) c[m * N + n] = (float)(dot(a + m * K, b + n * K, K) * alpha);
+}
+
+static void colsum(const float* dy, int64_t M, int64_t N, float* db) {
+#pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n) {
+        double s = 0.0;
+        for (int64_t m = 0; m < M; ++m) s += (double)dy[m * N + n];
+        db[n] = (float)s;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
 /* One quantized Linear, forward + backward, exactly the composition the       */
 /* device runs:                                             */
 /*   fwd  INT8 : xq = Q(x) per-tensor, wq = Q(w) per-channel,                  */
@@ -344,30 +393,48 @@ void ref_qlinear_int8_fwd_bwd(const float* x, const float* w, const float* bias,
     ref_gemm_s8_tn(xq, wq, M, N, K, acc);
     ref_dequant_epilogue(acc, M, N, *s_x, s_w, bias, y);
     if (!dy) return;
-    const float sx = *s_x;
+    float* g16 = round16(dy, M * N);
+    float* w16 = round16(w, N * K);
+    float* w16t = transpose(w16, N, K);   /* [K, N] */
+    float* g16t = transpose(g16, M, N);   /* [N, M] */
+    float* xqf = (float*)malloc(sizeof(float) * (size_t)(M * K));
+    for (int64_t i = 0; i < M * K; ++i) xqf[i] = (float)xq[i];
+    float* xqt = transpose(xqf, M, K);    /* [K, M] */
+    gemm_tn_f(g16, w16t, M, K, N, 1.0, dx);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < M * K; ++i) dx[i] = ref_f16_to_f32(ref_f32_to_f16(dx[i]));
+    gemm_tn_f(g16t, xqt, N, K, M, (double)*s_x, dw);
+    if (db) colsum(dy, M, N, db);
+    free(g16); free(w16); free(w16t); free(g16t); free(xqf); free(xqt);
+}
+
+/* FP16 Linear, forward + backward (the FP16 kernel of a plan): operands rounded
+ * to binary16, wide accumulation, y emitted as FP16 (held as float); backward as
+ * the INT8 op's but with the FP16 activation in wgrad and alpha = 1. */
+void ref_qlinear_f16_fwd_bwd(const float* x, const float* w, const float* bias, const float* dy,
+                             int64_t M, int64_t N, int64_t K, float* y, float* dx, float* dw,
+                             float* db) {
+    float* x16 = round16(x, M * K);
+    float* w16 = round16(w, N * K);
+    gemm_tn_f(x16, w16, M, N, K, 1.0, y);
 #pragma omp parallel for schedule(static)
     for (int64_t m = 0; m < M; ++m)
-        for (int64_t k = 0; k < K; ++k) {
-            double a = 0.0;
-            for (int64_t n = 0; n < N; ++n)
-                a += (double)ref_f16_to_f32(ref_f32_to_f16(dy[m * N + n])) *
-                     (double)ref_f16_to_f32(ref_f32_to_f16(w[n * K + k]));
-            dx[m * K + k] = ref_f16_to_f32(ref_f32_to_f16((float)a));
+        for (int64_t n = 0; n < N; ++n) {
+            float v = y[m * N + n];
+            if (bias) v = v + bias[n];
+            y[m * N + n] = ref_f16_to_f32(ref_f32_to_f16(v));
         }
-#pragma omp parallel for schedule(static)
-    for (int64_t n = 0; n < N; ++n) {
-        for (int64_t k = 0; k < K; ++k) {
-            double a = 0.0;
-            for (int64_t m = 0; m < M; ++m)
-                a += (double)ref_f16_to_f32(ref_f32_to_f16(dy[m * N + n])) * (double)xq[m * K + k];
-            dw[n * K + k] = (float)(a * (double)sx);
-        }
-        if (db) {
-            double s = 0.0;
-            for (int64_t m = 0; m < M; ++m) s += (double)dy[m * N + n];
-            db[n] = (float)s;
-        }
+    if (dy) {
+        float* g16 = round16(dy, M * N);
+        float* w16t = transpose(w16, N, K);
+        float* g16t = transpose(g16, M, N);
+        float* x16t = transpose(x16, M, K);
+        gemm_tn_f(g16, w16t, M, K, N, 1.0, dx);
+        gemm_tn_f(g16t, x16t, N, K, M, 1.0, dw);
+        if (db) colsum(dy, M, N, db);
+        free(g16); free(w16t); free(g16t); free(x16t);
     }
+    free(x16); free(w16);
 }
 
 int ref_num_threads(void) {

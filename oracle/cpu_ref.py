@@ -67,6 +67,7 @@ class CpuRef:
         L.ref_gemm_f32_tn.argtypes = [_p, _p, _i64, _i64, _i64, _p]
         L.ref_tensor_stats_f32.argtypes = [_p, _i64, _p]
         L.ref_qlinear_int8_fwd_bwd.argtypes = [_p] * 4 + [_i64] * 3 + [_p] * 9
+        L.ref_qlinear_f16_fwd_bwd.argtypes = [_p] * 4 + [_i64] * 3 + [_p] * 4
         L.ref_num_threads.restype = C.c_int
 
     # -- RNG / SR ----------------------------------------------------------
@@ -203,6 +204,22 @@ class CpuRef:
                                         _ptr(wq), _ptr(sx), _ptr(sw), _ptr(acc), _ptr(y),
                                         _ptr(dx), _ptr(dw), _ptr(db))
         return dict(xq=xq, wq=wq, s_x=sx[0], s_w=sw, acc=acc, y=y, dx=dx, dw=dw, db=db)
+
+    def qlinear_f16(self, x, w, bias, dy):
+        """Forward + backward of one FP16 Linear (cpu_ref.c ref_qlinear_f16_fwd_bwd)."""
+        x = np.ascontiguousarray(x, np.float32)
+        w = np.ascontiguousarray(w, np.float32)
+        M, K = x.shape
+        N = w.shape[0]
+        b = np.ascontiguousarray(bias, np.float32) if bias is not None else None
+        g = np.ascontiguousarray(dy, np.float32) if dy is not None else None
+        y = np.empty((M, N), np.float32)
+        dx = np.empty((M, K), np.float32)
+        dw = np.empty((N, K), np.float32)
+        db = np.empty(N, np.float32)
+        self.L.ref_qlinear_f16_fwd_bwd(_ptr(x), _ptr(w), _ptr(b), _ptr(g), M, N, K, _ptr(y),
+                                       _ptr(dx), _ptr(dw), _ptr(db))
+        return dict(y=y, dx=dx, dw=dw, db=db)
 
     def num_threads(self) -> int:
         return int(self.L.ref_num_threads())

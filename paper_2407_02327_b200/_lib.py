@@ -42,6 +42,7 @@ SIGNATURES = {
     "qsync_status_name": [_int],
     "qsync_abi_version": [],
     "qsync_device_sm_count": [],
+    "qsync_launch_count": [],
     "qsync_absmax": [_p, _int, _i64, _p, _p],
     "qsync_absmax_rows": [_p, _int, _i64, _i64, _p, _p],
     "qsync_quantize_per_tensor": [_p, _int, _i64, _i64, _p, _p, _p, _p],
@@ -64,7 +65,7 @@ SIGNATURES = {
     "qsync_mt_jump_selftest": [],
 }
 _RESTYPES = {"qsync_last_error": C.c_char_p, "qsync_status_name": C.c_char_p,
-             "qsync_stats_workspace_bytes": C.c_size_t}
+             "qsync_stats_workspace_bytes": C.c_size_t, "qsync_launch_count": C.c_ulonglong}
 
 _lib = None
 

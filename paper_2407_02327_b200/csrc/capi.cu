@@ -6,6 +6,7 @@
 // re-raise without reformatting.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -44,7 +45,10 @@ int set_error(int status, const std::string& msg) {
     return status;
 }
 
+static std::atomic<unsigned long long> g_launches{0};
+
 int check_launch(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) return QSYNC_OK;
     return set_error(QSYNC_ERR_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
@@ -71,6 +75,8 @@ const char* qsync_last_error(void) { return qsb::g_last_error.c_str(); }
 const char* qsync_status_name(int status) { return qsb::kind_name(status); }
 
 int qsync_abi_version(void) { return 1; }
+
+unsigned long long qsync_launch_count(void) { return qsb::g_launches.load(); }
 
 int qsync_device_sm_count(void) {
     int dev = 0;

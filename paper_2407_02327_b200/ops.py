@@ -180,6 +180,21 @@ def tensor_stats(x: torch.Tensor, out=None) -> torch.Tensor:
 
 
 # --------------------------------------------------------------------------- K6/K7
+# Optional per-launch timing (bench.py): a list that receives
+# (kind, flops, start_event, end_event) for every GEMM launched while it is set.
+GEMM_TIMER: list | None = None
+
+
+def _timed(kind: str, flops: float):
+    if GEMM_TIMER is None:
+        return None
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    GEMM_TIMER.append((kind, flops, s, e))
+    return e
+
+
 def gemm_s8(a: torch.Tensor, b: torch.Tensor, scale_a=None, scale_b=None, bias=None,
             out_i32: bool = False, out_f32: bool = True, b_per_channel: bool = True,
             out=None):
@@ -192,8 +207,11 @@ def gemm_s8(a: torch.Tensor, b: torch.Tensor, scale_a=None, scale_b=None, bias=N
     cf = None
     if out_f32:
         cf = out if out is not None else torch.empty((M, N), device=a.device, dtype=torch.float32)
+    ev = _timed("gemm_s8", 2.0 * M * N * K)
     call("qsync_gemm_s8", _ptr(a), _ptr(b), M, N, K, _ptr(ci), _ptr(cf), _ptr(scale_a),
          _ptr(scale_b), int(b_per_channel), _ptr(bias), _stream())
+    if ev is not None:
+        ev.record()
     return ci, cf
 
 
@@ -205,9 +223,17 @@ def gemm_f16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32, alpha: f
     M, K = a.shape
     N = b.shape[0]
     c = out if out is not None else torch.empty((M, N), device=a.device, dtype=out_dtype)
+    ev = _timed("gemm_f16", 2.0 * M * N * K)
     call("qsync_gemm_f16", _ptr(a), _ptr(b), _DT[a.dtype], M, N, K, _ptr(c), _DT[c.dtype],
          float(alpha), _ptr(alpha_dev), _ptr(bias), int(accumulate), _stream())
+    if ev is not None:
+        ev.record()
     return c
+
+
+def launch_count() -> int:
+    """Kernels launched by libqsync_b200 so far in this process."""
+    return int(_lib.lib().qsync_launch_count())
 
 
 def force_tile_n(bn: int) -> None:

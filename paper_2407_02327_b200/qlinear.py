@@ -83,6 +83,23 @@ class _QLinearFp16(torch.autograd.Function):
         return dx, dw, db
 
 
+class _Cast(torch.autograd.Function):
+    """Autograd-aware device cast (K4) for the glue between planned operators."""
+
+    @staticmethod
+    def forward(ctx, x, dtype):
+        ctx.src = x.dtype
+        return ops.cast(x.contiguous(), dtype)
+
+    @staticmethod
+    def backward(ctx, g):
+        return ops.cast(g.contiguous(), ctx.src), None
+
+
+def cast(x: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
+    return x if x.dtype == dtype else _Cast.apply(x, dtype)
+
+
 def qlinear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, precision: str) -> torch.Tensor:
     """Y = X W^T + b for X [..., K] at the given plan precision."""
     shape = x.shape

@@ -173,7 +173,7 @@ def test_demo_bundle_omega(golden):
 
 def _declared_symbols():
     src = open(os.path.join(ROOT, "include", "qsync_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|size_t)\s+(qsync_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|size_t|unsigned long long)\s+(qsync_\w+)\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
