@@ -227,6 +227,10 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     n0 = ops.launch_count()
     ops.GEMM_TIMER = []
+    # Hold the stream with a ~0.25 s spin so the whole eager step is enqueued
+    # before the GPU reaches it: each GEMM's event pair then brackets only the
+    # kernel, not host launch gaps.
+    torch.cuda._sleep(500_000_000)
     step_eager()
     torch.cuda.synchronize()
     launches_per_step = ops.launch_count() - n0

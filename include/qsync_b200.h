@@ -79,10 +79,13 @@ int qsync_absmax_rows(const void* x, int dtype, int64_t rows, int64_t cols, floa
  * ------------------------------------------------------------------------- */
 /* Per-tensor: absmax + scale + quantize of a [rows, cols] matrix.  `scale` is a
  * device float[2]: scale[0] receives s, scale[1] the absmax.  If q_t_f16 != NULL the same quantized values are
- * also written transposed as FP16 integers, [cols, rows] (the saved activation
- * operand of the FP16 wgrad GEMM, cost_mapper.cpp:13-15). */
+ * also written transposed as FP16 integers, [cols, rows] with row pitch ld_t
+ * (>= rows, 0 = rows; pad columns untouched) -- the saved activation operand of
+ * the FP16 wgrad GEMM (cost_mapper.cpp:13-15), whose K (= rows) must be padded
+ * to a multiple of 8 for TMA. */
 int qsync_quantize_per_tensor(const void* x, int dtype, int64_t rows, int64_t cols, int8_t* q,
-                              float* scale, uint16_t* q_t_f16, qsync_stream_t stream);
+                              float* scale, uint16_t* q_t_f16, int64_t ld_t,
+                              qsync_stream_t stream);
 /* Quantize with a scale already on the device (e.g. delayed / shared scale). */
 int qsync_quantize_with_scale(const void* x, int dtype, int64_t n, const float* scale, int8_t* q,
                               qsync_stream_t stream);
@@ -127,11 +130,14 @@ int qsync_dequantize_per_channel(const int8_t* q, int64_t rows, int64_t cols, co
 int qsync_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64_t n,
                qsync_stream_t stream);
 /* [rows, cols] FP32/FP16 -> FP16 copy (optional), FP16 transposed [cols, rows]
- * (optional) and FP32 column sums (optional; the bias gradient of a Linear).
+ * (optional, row pitch ld_t >= rows, 0 = rows) and FP32 column sums
+ * (optional; the bias gradient of a Linear),
+ * added into `colsum` when colsum_accumulate != 0, else overwriting it.
  * This is the backward entry of an INT8/FP16 op: the incoming gradient is cast
  * to the FP16 backward format (cost_mapper.cpp:13-15) for dgrad and wgrad. */
 int qsync_cast_transpose(const void* x, int dtype, int64_t rows, int64_t cols, uint16_t* out,
-                         uint16_t* out_t, float* colsum, qsync_stream_t stream);
+                         uint16_t* out_t, int64_t ld_t, float* colsum, int colsum_accumulate,
+                         qsync_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * K5  fused tensor statistics for OpStats (profile.hpp:95-108).
@@ -170,6 +176,20 @@ int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_
 int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,
                    void* c, int c_dtype, float alpha, const float* alpha_dev, const float* bias,
                    int accumulate, qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Glue between planned operators: fused residual add + LayerNorm.
+ * fwd: s = a + b (b FP32 or FP16 [rows, cols], may be NULL), y = LN(s) with
+ *      gamma/beta; saves s (optional), mean[rows], rstd[rows].
+ * bwd: dx from dy; dgamma/dbeta ADDED into the given FP32 buffers.
+ * 128 <= cols <= 1024, cols % 128 == 0.
+ * ------------------------------------------------------------------------- */
+int qsync_layernorm_fwd(const float* a, const void* b, int b_dtype, const float* gamma,
+                        const float* beta, int64_t rows, int64_t cols, float eps, float* s_out,
+                        float* y, float* mean, float* rstd, qsync_stream_t stream);
+int qsync_layernorm_bwd(const float* dy, const float* s, const float* mean, const float* rstd,
+                        const float* gamma, int64_t rows, int64_t cols, float* dx, float* dgamma,
+                        float* dbeta, qsync_stream_t stream);
 
 #ifdef __cplusplus
 }

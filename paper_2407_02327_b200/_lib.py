@@ -45,7 +45,7 @@ SIGNATURES = {
     "qsync_launch_count": [],
     "qsync_absmax": [_p, _int, _i64, _p, _p],
     "qsync_absmax_rows": [_p, _int, _i64, _i64, _p, _p],
-    "qsync_quantize_per_tensor": [_p, _int, _i64, _i64, _p, _p, _p, _p],
+    "qsync_quantize_per_tensor": [_p, _int, _i64, _i64, _p, _p, _p, _i64, _p],
     "qsync_quantize_with_scale": [_p, _int, _i64, _p, _p, _p],
     "qsync_quantize_per_channel": [_p, _i64, _i64, _p, _p, _p, _p],
     "qsync_stochastic_round_f64": [_p, _i64, _f64, _f64, _u64, _p, _p, _p],
@@ -55,13 +55,16 @@ SIGNATURES = {
     "qsync_dequantize_per_tensor": [_p, _i64, _p, _p, _p],
     "qsync_dequantize_per_channel": [_p, _i64, _i64, _p, _p, _p],
     "qsync_cast": [_p, _int, _p, _int, _i64, _p],
-    "qsync_cast_transpose": [_p, _int, _i64, _i64, _p, _p, _p, _p],
+    "qsync_cast_transpose": [_p, _int, _i64, _i64, _p, _p, _i64, _p, _int, _p],
     "qsync_stats_workspace_bytes": [],
     "qsync_tensor_stats": [_p, _int, _i64, _p, _p, _p],
     "qsync_gemm_s8": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _int, _p, _p],
     "qsync_gemm_f16": [_p, _p, _int, _i64, _i64, _i64, _p, _int, _f32, _p, _p, _int, _p],
+    "qsync_layernorm_fwd": [_p, _p, _int, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p],
+    "qsync_layernorm_bwd": [_p, _p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p],
     # non-header helpers
     "qsync_gemm_force_tile_n": [_int],
+    "qsync_gemm_force_splitk": [_int],
     "qsync_mt_jump_selftest": [],
 }
 _RESTYPES = {"qsync_last_error": C.c_char_p, "qsync_status_name": C.c_char_p,

@@ -48,6 +48,8 @@ struct EpiParams {
     int accumulate;
     uint32_t idesc;
     int tma_store;  // epilogue writes through tm_c (TMA store / reduce-add)
+    int ksplit;     // split-K factor (>1 only with accumulate: partials reduce-add)
+    int kb_per;     // k-blocks per split
 };
 
 constexpr int kStageChunkBytes = 32 * 128;  // one warp's 32 rows x 128 B staging chunk
@@ -91,6 +93,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_m = static_cast<int>((M + BM - 1) / BM);
     const int num_n = static_cast<int>((N + BN - 1) / BN);
     const int num_tiles = num_m * num_n;
+    // Work units = (tile, K split); split-K partials are reduce-added by TMA.
+    const int ksplit = p.ksplit > 1 ? p.ksplit : 1;
+    const int num_units = num_tiles * ksplit;
     const int bk_elems = kI8 ? BK_BYTES : BK_BYTES / 2;
     const int num_kb = static_cast<int>((K + bk_elems - 1) / bk_elems);
 
@@ -119,10 +124,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+                const int t = u / ksplit;
                 const int m0 = (t % num_m) * BM;
                 const int n0 = (t / num_m) * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                const int kb0 = (u % ksplit) * p.kb_per;
+                const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
+                for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     ptx::tma_load_2d(smem_a + stage * BM * BK_BYTES, &tm_a, &full[stage],
@@ -143,11 +151,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+                const int kb0 = (u % ksplit) * p.kb_per;
+                const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t a_addr = ptx::smem_u32(smem_a + stage * BM * BK_BYTES);
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int k = 0; k < BK_BYTES / 32; ++k) {  // UMMA_K = 32 bytes
                         const uint64_t da = ptx::sw128_kmajor_desc(a_addr + k * 32);
                         const uint64_t db = ptx::sw128_kmajor_desc(b_addr + k * 32);
-                        const uint32_t accum = (kb | k) != 0 ? 1u : 0u;
+                        const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
                         if (kI8)
                             ptx::mma_i8(d_tmem, da, db, p.idesc, accum);
                         else
@@ -192,9 +202,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool out16 = p.c && p.c_dtype != QSYNC_F32;
         const bool raw = p.c_i32 != nullptr && p.c == nullptr;
         const int chunk_cols = out16 ? 64 : 32;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        constexpr int kNC = BN / 32;  // 32-column groups per tile
+        for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+            const int t = u / ksplit;
+            const bool add_bias = (u % ksplit) == 0;  // bias once per tile under split-K
             const int64_t m0 = static_cast<int64_t>(t % num_m) * BM;
             const int64_t n0 = static_cast<int64_t>(t / num_m) * BN;
+            // Per-column epilogue factors of this tile, loaded BEFORE waiting for
+            // the accumulator so their latency hides behind the tile's MMAs:
+            // lane j holds columns n0 + 32*i + j.
+            float col_sb[kNC], col_bias[kNC];
+#pragma unroll
+            for (int i = 0; i < kNC; ++i) {
+                const int64_t col = n0 + 32 * i + lane;
+                const bool ok = col < N;
+                float sb = 1.0f;
+                if (kI8 && p.scale_b) sb = p.b_per_channel ? (ok ? p.scale_b[col] : 0.0f) : *p.scale_b;
+                col_sb[i] = sb;
+                col_bias[i] = (p.bias && ok && add_bias) ? p.bias[col] : 0.0f;
+            }
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             const int64_t row0 = m0 + quad * 32;
@@ -215,7 +241,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[32];
                     ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0 + 32 * sub), r);
                     ptx::tmem_ld_wait();
-                    const int64_t cb = col0 + 32 * sub;
                     if (raw) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) w[j] = r[j];
@@ -225,20 +250,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j) rawv[j] = r[j];
                     }
-                    // Per-column factors: lane j loads column cb+j once, then broadcast.
-                    const int64_t mycol = cb + lane;
-                    const bool cok = mycol < N;
-                    float colscale = alpha;
-                    if (kI8) {
-                        float sb = 1.0f;
-                        if (p.scale_b) sb = p.b_per_channel ? (cok ? p.scale_b[mycol] : 0.0f) : *p.scale_b;
-                        colscale = __fmul_rn(sa, sb);
+                    // Select this 32-column group's factors (register selects, no
+                    // local memory), then broadcast column j's from lane j.
+                    const int g = (c0 >> 5) + sub;
+                    float sb = col_sb[0], bs = col_bias[0];
+#pragma unroll
+                    for (int i = 1; i < kNC; ++i) {
+                        if (g == i) {
+                            sb = col_sb[i];
+                            bs = col_bias[i];
+                        }
                     }
-                    const float colbias = (p.bias && cok) ? p.bias[mycol] : 0.0f;
+                    const float colscale = kI8 ? __fmul_rn(sa, sb) : alpha;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float sj = __shfl_sync(0xffffffffu, colscale, j);
-                        const float bj = __shfl_sync(0xffffffffu, colbias, j);
+                        const float bj = __shfl_sync(0xffffffffu, bs, j);
                         float x = kI8 ? __fmul_rn(__int2float_rn(static_cast<int>(r[j])), sj)
                                       : __fmul_rn(bits_f(r[j]), sj);
                         if (p.bias) x = __fadd_rn(x, bj);
@@ -395,6 +422,9 @@ uint32_t make_idesc(bool i8, bool bf16, int n) {
     return d;
 }
 
+int g_force_splitk = 0;  // test/bench hook (qsync_gemm_force_splitk): 0 = heuristic
+int g_splitk_wide = 0;   // accumulate GEMMs prefer BN=256 (bench hook)
+
 template <bool kI8, int BN>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
     using C = Cfg<BN>;
@@ -428,7 +458,30 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
         configured = true;
     }
     const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-    const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count()));
+    // Split-K when the tile grid leaves SMs idle and the result is reduce-added
+    // anyway (accumulating FP32 output, e.g. wgrad into the flat main_grad).
+    const int64_t bk_elems = BK_BYTES / eb;
+    const int64_t num_kb = (p.K + bk_elems - 1) / bk_elems;
+    p.ksplit = 1;
+    p.kb_per = static_cast<int>(num_kb);
+    const int sms = sm_count();
+    if (g_force_splitk > 0) {
+        if (p.accumulate && p.tma_store && p.c_dtype == QSYNC_F32 && !kI8 && g_force_splitk > 1) {
+            const int64_t per = (num_kb + g_force_splitk - 1) / g_force_splitk;
+            p.kb_per = static_cast<int>(per);
+            p.ksplit = static_cast<int>((num_kb + per - 1) / per);
+        }
+    } else if (p.accumulate && p.tma_store && p.c_dtype == QSYNC_F32 && !kI8 && tiles < sms) {
+        int64_t want = std::max<int64_t>(1, (2 * sms) / tiles);         // ~2 units per SM
+        want = std::min<int64_t>(want, std::max<int64_t>(1, num_kb / 8));  // >= 8 k-blocks each
+        if (want > 1) {
+            const int64_t per = (num_kb + want - 1) / want;
+            p.kb_per = static_cast<int>(per);
+            p.ksplit = static_cast<int>((num_kb + per - 1) / per);
+        }
+    }
+    const int64_t units = tiles * p.ksplit;
+    const int grid = static_cast<int>(std::min<int64_t>(units, sms));
     k_gemm_tc<kI8, BN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, p);
     return check_launch("k_gemm_tc");
 }
@@ -457,7 +510,10 @@ int pick_bn(int64_t M, int64_t N) {
 template <bool kI8>
 int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st,
              int force_bn) {
-    const int bn = force_bn ? force_bn : pick_bn(p.M, p.N);
+    // Accumulating FP32 outputs (wgrad into main_grad) use split-K to fill the
+    // chip, so they take the widest tile (fewest L2 bytes per FLOP).
+    const bool splitk_ok = !kI8 && p.accumulate && p.c_dtype == QSYNC_F32 && g_splitk_wide;
+    const int bn = force_bn ? force_bn : (splitk_ok ? 256 : pick_bn(p.M, p.N));
     p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, bn);
     switch (bn) {
         case 256: return launch<kI8, 256>(a, b, dt, p, st);
@@ -488,6 +544,12 @@ int validate(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int6
 using namespace qsb;
 
 extern "C" {
+
+int qsync_gemm_force_splitk(int ks) {
+    QSB_REQUIRE(ks >= 0 && ks <= 64, QSYNC_ERR_DOMAIN, "split-K override must be in [0, 64]");
+    g_force_splitk = ks;
+    return QSYNC_OK;
+}
 
 int qsync_gemm_force_tile_n(int bn) {
     QSB_REQUIRE(bn == 0 || bn == 64 || bn == 128 || bn == 256, QSYNC_ERR_DOMAIN, "tile N must be 0/64/128/256");

@@ -1,0 +1,239 @@
+// norm.cu -- fused residual-add + LayerNorm forward / backward (the glue between
+// the planned Linears of an encoder layer: LN(x + sublayer(x))).
+//
+// One warp per row, the row held in registers (cols <= 1024, cols % 128 == 0
+// for the vector path; BERT-base hidden 768), grid-stride over rows.
+//   fwd: s = a + b  (b FP32 or FP16 -- the planned op's output format,
+//        graph.hpp:38-40), y = (s - mean) * rstd * gamma + beta; saves s, mean, rstd.
+//   bwd: xh = (s - mean) * rstd, g = dy * gamma,
+//        dx = rstd * (g - mean(g) - xh * mean(g * xh)),
+//        dgamma += sum_rows dy * xh, dbeta += sum_rows dy  (accumulated into the
+//        caller's FP32 buffers -- the parameters' main_grad slices).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace qsb {
+namespace {
+
+template <int NV>
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int NV, int BDT>
+__global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
+                                                const typename Elem<BDT>::T* __restrict__ b,
+                                                const float* __restrict__ gamma,
+                                                const float* __restrict__ beta, int64_t rows,
+                                                int cols, float eps, float* __restrict__ s_out,
+                                                float* __restrict__ y, float* __restrict__ mean_out,
+                                                float* __restrict__ rstd_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    float4 g[NV], be[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        g[i] = reinterpret_cast<const float4*>(gamma)[lane + 32 * i];
+        be[i] = reinterpret_cast<const float4*>(beta)[lane + 32 * i];
+    }
+    const float inv_n = 1.0f / static_cast<float>(cols);
+    for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+         row += warps) {
+        float4 v[NV];
+        float sum = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int64_t off = row * cols + 4 * (lane + 32 * i);
+            float4 x = *reinterpret_cast<const float4*>(a + off);
+            if (b) {
+                if (BDT == QSYNC_F32) {
+                    const float4 r = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(b) + off);
+                    x.x += r.x; x.y += r.y; x.z += r.z; x.w += r.w;
+                } else {
+                    const uint2 r = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(b) + off);
+                    const float2 r0 = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+                    const float2 r1 = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+                    x.x += r0.x; x.y += r0.y; x.z += r1.x; x.w += r1.y;
+                }
+            }
+            v[i] = x;
+            sum += (x.x + x.y) + (x.z + x.w);
+            if (s_out) *reinterpret_cast<float4*>(s_out + off) = x;
+        }
+        const float mean = warp_sum_f<NV>(sum) * inv_n;
+        float sq = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const float dx = v[i].x - mean, dy = v[i].y - mean, dz = v[i].z - mean, dw = v[i].w - mean;
+            sq += (dx * dx + dy * dy) + (dz * dz + dw * dw);
+        }
+        const float rstd = rsqrtf(warp_sum_f<NV>(sq) * inv_n + eps);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int64_t off = row * cols + 4 * (lane + 32 * i);
+            float4 o;
+            o.x = (v[i].x - mean) * rstd * g[i].x + be[i].x;
+            o.y = (v[i].y - mean) * rstd * g[i].y + be[i].y;
+            o.z = (v[i].z - mean) * rstd * g[i].z + be[i].z;
+            o.w = (v[i].w - mean) * rstd * g[i].w + be[i].w;
+            *reinterpret_cast<float4*>(y + off) = o;
+        }
+        if (lane == 0) {
+            mean_out[row] = mean;
+            rstd_out[row] = rstd;
+        }
+    }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
+                                                const float* __restrict__ s,
+                                                const float* __restrict__ mean_in,
+                                                const float* __restrict__ rstd_in,
+                                                const float* __restrict__ gamma, int64_t rows,
+                                                int cols, float* __restrict__ dx,
+                                                float* __restrict__ dgamma,
+                                                float* __restrict__ dbeta) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    float4 g[NV], acc_g[NV], acc_b[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        g[i] = reinterpret_cast<const float4*>(gamma)[lane + 32 * i];
+        acc_g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        acc_b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float inv_n = 1.0f / static_cast<float>(cols);
+    for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; row < rows; row += warps) {
+        const float mean = mean_in[row], rstd = rstd_in[row];
+        float4 xh[NV], gy[NV];
+        float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int64_t off = row * cols + 4 * (lane + 32 * i);
+            const float4 d = *reinterpret_cast<const float4*>(dy + off);
+            const float4 x = *reinterpret_cast<const float4*>(s + off);
+            xh[i] = make_float4((x.x - mean) * rstd, (x.y - mean) * rstd, (x.z - mean) * rstd,
+                                (x.w - mean) * rstd);
+            gy[i] = make_float4(d.x * g[i].x, d.y * g[i].y, d.z * g[i].z, d.w * g[i].w);
+            s1 += (gy[i].x + gy[i].y) + (gy[i].z + gy[i].w);
+            s2 += (gy[i].x * xh[i].x + gy[i].y * xh[i].y) + (gy[i].z * xh[i].z + gy[i].w * xh[i].w);
+            acc_g[i].x += d.x * xh[i].x; acc_g[i].y += d.y * xh[i].y;
+            acc_g[i].z += d.z * xh[i].z; acc_g[i].w += d.w * xh[i].w;
+            acc_b[i].x += d.x; acc_b[i].y += d.y; acc_b[i].z += d.z; acc_b[i].w += d.w;
+        }
+        const float m1 = warp_sum_f<NV>(s1) * inv_n;
+        const float m2 = warp_sum_f<NV>(s2) * inv_n;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int64_t off = row * cols + 4 * (lane + 32 * i);
+            float4 o;
+            o.x = rstd * (gy[i].x - m1 - xh[i].x * m2);
+            o.y = rstd * (gy[i].y - m1 - xh[i].y * m2);
+            o.z = rstd * (gy[i].z - m1 - xh[i].z * m2);
+            o.w = rstd * (gy[i].w - m1 - xh[i].w * m2);
+            *reinterpret_cast<float4*>(dx + off) = o;
+        }
+    }
+    // Block-reduce the per-warp column partials (gamma, then beta through the
+    // same smem buffer), then one atomic per column per block.
+    __shared__ float red[8][1024 + 4];
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+        float* outp = pass == 0 ? dgamma : dbeta;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const float4 v = pass == 0 ? acc_g[i] : acc_b[i];
+            const int c = 4 * (lane + 32 * i);
+            red[warp][c] = v.x; red[warp][c + 1] = v.y; red[warp][c + 2] = v.z; red[warp][c + 3] = v.w;
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+            float t = 0.f;
+            for (int w = 0; w < nw; ++w) t += red[w][c];
+            if (outp) atomicAdd(outp + c, t);
+        }
+        __syncthreads();
+    }
+}
+
+template <int NV>
+int ln_fwd_nv(const float* a, const void* b, int b_dtype, const float* gamma, const float* beta,
+              int64_t rows, int cols, float eps, float* s_out, float* y, float* mean, float* rstd,
+              cudaStream_t st) {
+    const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 8LL));
+    if (b_dtype == QSYNC_F16)
+        k_ln_fwd<NV, QSYNC_F16><<<grid, 256, 0, st>>>(a, static_cast<const __half*>(b), gamma, beta,
+                                                      rows, cols, eps, s_out, y, mean, rstd);
+    else
+        k_ln_fwd<NV, QSYNC_F32><<<grid, 256, 0, st>>>(a, static_cast<const float*>(b), gamma, beta,
+                                                      rows, cols, eps, s_out, y, mean, rstd);
+    return check_launch("k_ln_fwd");
+}
+
+template <int NV>
+int ln_bwd_nv(const float* dy, const float* s, const float* mean, const float* rstd,
+              const float* gamma, int64_t rows, int cols, float* dx, float* dgamma, float* dbeta,
+              cudaStream_t st) {
+    const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 2LL));
+    k_ln_bwd<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta);
+    return check_launch("k_ln_bwd");
+}
+
+}  // namespace
+}  // namespace qsb
+
+using namespace qsb;
+
+extern "C" {
+
+int qsync_layernorm_fwd(const float* a, const void* b, int b_dtype, const float* gamma,
+                        const float* beta, int64_t rows, int64_t cols, float eps, float* s_out,
+                        float* y, float* mean, float* rstd, qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0, QSYNC_ERR_DOMAIN, "negative row count");
+    QSB_REQUIRE(cols % 128 == 0 && cols >= 128 && cols <= 1024, QSYNC_ERR_DOMAIN,
+                "layernorm supports 128 <= cols <= 1024, cols % 128 == 0");
+    QSB_REQUIRE(b_dtype == QSYNC_F32 || b_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN,
+                "residual operand must be F32 or F16");
+    if (rows == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int c = static_cast<int>(cols);
+    switch (c / 128) {
+        case 1: return ln_fwd_nv<1>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+        case 2: return ln_fwd_nv<2>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+        case 3: return ln_fwd_nv<3>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+        case 4: return ln_fwd_nv<4>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+        case 5: return ln_fwd_nv<5>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+        case 6: return ln_fwd_nv<6>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+        case 7: return ln_fwd_nv<7>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+        default: return ln_fwd_nv<8>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+    }
+}
+
+int qsync_layernorm_bwd(const float* dy, const float* s, const float* mean, const float* rstd,
+                        const float* gamma, int64_t rows, int64_t cols, float* dx, float* dgamma,
+                        float* dbeta, qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0, QSYNC_ERR_DOMAIN, "negative row count");
+    QSB_REQUIRE(cols % 128 == 0 && cols >= 128 && cols <= 1024, QSYNC_ERR_DOMAIN,
+                "layernorm supports 128 <= cols <= 1024, cols % 128 == 0");
+    if (rows == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int c = static_cast<int>(cols);
+    switch (c / 128) {
+        case 1: return ln_bwd_nv<1>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+        case 2: return ln_bwd_nv<2>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+        case 3: return ln_bwd_nv<3>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+        case 4: return ln_bwd_nv<4>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+        case 5: return ln_bwd_nv<5>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+        case 6: return ln_bwd_nv<6>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+        case 7: return ln_bwd_nv<7>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+        default: return ln_bwd_nv<8>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+    }
+}
+
+}  // extern "C"

@@ -190,73 +190,150 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
 }
 
 // ---------------------------------------------------------------------------
-// 2-D tile kernels (64 rows x 32 cols, block 32 x 8): quantize / cast with a
-// transposed FP16 copy, optional column sums.  Loads and the row-major store
-// are coalesced along cols; the transposed store is coalesced along rows via
-// a padded smem tile.
+// 2-D tile kernels: quantize / cast a [rows, cols] matrix and also emit its
+// FP16 transpose (the K-major operand the wgrad / dgrad GEMMs need), plus
+// optional column sums (bias gradient).  Tile 64 x 64, 256 threads; each
+// thread loads 4 consecutive elements of a row (16 B for F32, 8 B for 16-bit),
+// writes the row-major output as one 4/8-byte vector, and stages the values
+// in a padded smem tile from which the transpose is written as 16-byte rows.
 // mode 0: quantize with absmax-derived scale -> q (int8) + q_t (fp16 ints)
 // mode 1: cast -> out (fp16) + out_t (fp16) + colsum (fp32, atomics)
+// Shapes with cols % 4 != 0 or misaligned bases take the scalar edge path
+// inside the same kernel.
 // ---------------------------------------------------------------------------
-constexpr int TR = 64, TC = 32;
+constexpr int TR = 64, TC = 64;
+
+template <int DT>
+__device__ __forceinline__ void load4(const typename Elem<DT>::T* p, float* f) {
+    if (DT == QSYNC_F32) {
+        const float4 v = *reinterpret_cast<const float4*>(p);
+        f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+    } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        const uint32_t w[2] = {v.x, v.y};
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            float2 t;
+            if (DT == QSYNC_F16) t = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+            else t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+            f[2 * i] = t.x;
+            f[2 * i + 1] = t.y;
+        }
+    }
+}
 
 template <int DT, int MODE>
 __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __restrict__ x,
                                               int64_t rows, int64_t cols,
                                               const float* __restrict__ absmax_in,
                                               int8_t* __restrict__ q, uint16_t* __restrict__ out,
-                                              uint16_t* __restrict__ out_t,
+                                              uint16_t* __restrict__ out_t, int64_t ld_t,
                                               float* __restrict__ colsum,
-                                              float* __restrict__ scale_out) {
-    __shared__ __half tile[TC][TR + 2];
-    __shared__ float csum[8][TC];
-    const int tx = threadIdx.x, ty = threadIdx.y;
+                                              float* __restrict__ scale_out, int vec_ok) {
+    __shared__ __align__(16) __half tile[TC][TR + 8];  // [col][row], 16B-aligned rows
+    __shared__ float csum[16][TC + 1];
+    const int tid = threadIdx.x;
+    const int cg = tid & 15;   // 4-column group within the tile
+    const int rl0 = tid >> 4;  // 0..15
     const int64_t r0 = blockIdx.y * (int64_t)TR, c0 = blockIdx.x * (int64_t)TC;
-    const int64_t c = c0 + tx;
     float s = 1.0f;
     if (MODE == 0) {
         s = scale_from_absmax(*absmax_in);
-        if (scale_out && blockIdx.x == 0 && blockIdx.y == 0 && tx == 0 && ty == 0) *scale_out = s;
+        if (scale_out && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *scale_out = s;
     }
-    float cs = 0.0f;
+    const int64_t c = c0 + cg * 4;
+    const bool full_cols = vec_ok && (c + 4 <= cols);
+    float cs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int j = 0; j < TR / 8; ++j) {
-        const int rl = ty + 8 * j;
+    for (int pass = 0; pass < TR / 16; ++pass) {
+        const int rl = rl0 + 16 * pass;
         const int64_t r = r0 + rl;
-        __half h = __float2half_rn(0.0f);
-        if (r < rows && c < cols) {
-            const float v = Elem<DT>::f(x[r * cols + c]);
-            if (MODE == 0) {
-                const int qi = quant_rne(v, s);
-                if (q) q[r * cols + c] = static_cast<int8_t>(qi);
-                h = __int2half_rn(qi);
+        float f[4] = {0.f, 0.f, 0.f, 0.f};
+        if (r < rows) {
+            if (full_cols) {
+                load4<DT>(x + r * cols + c, f);
             } else {
-                h = __float2half_rn(v);
-                if (out) out[r * cols + c] = __half_as_ushort(h);
-                cs += v;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (c + i < cols) f[i] = Elem<DT>::f(x[r * cols + c + i]);
             }
         }
-        tile[tx][rl] = h;
+        __half h[4];
+        if (MODE == 0) {
+            int qi[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                qi[i] = quant_rne(f[i], s);
+                h[i] = __int2half_rn(qi[i]);
+            }
+            if (q && r < rows) {
+                if (full_cols) {
+                    const uint32_t pk = static_cast<uint32_t>(static_cast<uint8_t>(qi[0])) |
+                                        (static_cast<uint32_t>(static_cast<uint8_t>(qi[1])) << 8) |
+                                        (static_cast<uint32_t>(static_cast<uint8_t>(qi[2])) << 16) |
+                                        (static_cast<uint32_t>(static_cast<uint8_t>(qi[3])) << 24);
+                    *reinterpret_cast<uint32_t*>(q + r * cols + c) = pk;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (c + i < cols) q[r * cols + c + i] = static_cast<int8_t>(qi[i]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                h[i] = __float2half_rn(f[i]);
+                cs[i] += f[i];
+            }
+            if (out && r < rows) {
+                if (full_cols) {
+                    uint2 pk;
+                    pk.x = __half_as_ushort(h[0]) | (static_cast<uint32_t>(__half_as_ushort(h[1])) << 16);
+                    pk.y = __half_as_ushort(h[2]) | (static_cast<uint32_t>(__half_as_ushort(h[3])) << 16);
+                    *reinterpret_cast<uint2*>(out + r * cols + c) = pk;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (c + i < cols) out[r * cols + c + i] = __half_as_ushort(h[i]);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tile[cg * 4 + i][rl] = h[i];
     }
-    if (MODE == 1 && colsum) csum[ty][tx] = cs;
+    if (MODE == 1 && colsum) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) csum[rl0][cg * 4 + i] = cs[i];
+    }
     __syncthreads();
     if (out_t) {
-        // Each warp writes columns ty, ty+8, ty+16, ty+24 of the tile as rows of out_t.
-        for (int cc = ty; cc < TC; cc += 8) {
-            const int64_t oc = c0 + cc;
-            if (oc >= cols) continue;
+        // 64 columns x 64 rows: each thread writes 2 x (8 rows as one 16B store).
+        const bool vec_t = vec_ok && (ld_t % 8 == 0);
 #pragma unroll
-            for (int k = 0; k < TR / 32; ++k) {
-                const int rl = tx + 32 * k;
-                const int64_t r = r0 + rl;
-                if (r < rows) out_t[oc * rows + r] = __half_as_ushort(tile[cc][rl]);
+        for (int k = 0; k < 2; ++k) {
+            const int idx = tid + 256 * k;  // 0..511
+            const int cc = idx >> 3;        // column within tile
+            const int rg = (idx & 7) * 8;   // row group
+            const int64_t oc = c0 + cc;
+            const int64_t orow = r0 + rg;
+            if (oc >= cols || orow >= rows) continue;
+            if (vec_t && orow + 8 <= rows) {
+                *reinterpret_cast<uint4*>(out_t + oc * ld_t + orow) =
+                    *reinterpret_cast<const uint4*>(&tile[cc][rg]);
+            } else {
+                for (int i = 0; i < 8 && orow + i < rows; ++i)
+                    out_t[oc * ld_t + orow + i] = __half_as_ushort(tile[cc][rg + i]);
             }
         }
     }
-    if (MODE == 1 && colsum && ty == 0 && c < cols) {
-        float t = 0.0f;
+    if (MODE == 1 && colsum && tid < TC) {
+        const int64_t cc = c0 + tid;
+        if (cc < cols) {
+            float t = 0.0f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) t += csum[j][tx];
-        atomicAdd(colsum + c, t);
+            for (int j = 0; j < 16; ++j) t += csum[j][tid];
+            atomicAdd(colsum + cc, t);
+        }
     }
 }
 
@@ -554,14 +631,15 @@ template <int DT>
 struct QuantRun {
     // scale[0] <- s, scale[1] <- absmax (scratch + output).
     static int run(const void* x, int64_t rows, int64_t cols, int8_t* q, float* scale,
-                   uint16_t* q_t, cudaStream_t st) {
+                   uint16_t* q_t, int64_t ld_t, cudaStream_t st) {
         using T = typename Elem<DT>::T;
         const int64_t n = rows * cols;
         QSB_TRY(AbsmaxRun<DT>::run(x, n, scale + 1, st));
         if (q_t && n > 0) {
             dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
-            k_tile<DT, 0><<<grid, dim3(32, 8), 0, st>>>(static_cast<const T*>(x), rows, cols,
-                                                        scale + 1, q, nullptr, q_t, nullptr, scale);
+            const int vt = (cols % 4 == 0) && aligned16(x) && aligned16(q) && aligned16(q_t);
+            k_tile<DT, 0><<<grid, 256, 0, st>>>(static_cast<const T*>(x), rows, cols, scale + 1, q,
+                                                nullptr, q_t, ld_t, nullptr, scale, vt);
             return check_launch("k_tile<quant>");
         }
         const int vec = aligned16(x) && aligned16(q);
@@ -588,13 +666,15 @@ struct QuantScaleRun {
 template <int DT>
 struct CastTRun {
     static int run(const void* x, int64_t rows, int64_t cols, uint16_t* out, uint16_t* out_t,
-                   float* colsum, cudaStream_t st) {
+                   int64_t ld_t, float* colsum, int colsum_accumulate, cudaStream_t st) {
         using T = typename Elem<DT>::T;
-        if (colsum) QSB_TRY(cuda_status(cudaMemsetAsync(colsum, 0, sizeof(float) * cols, st), "memset"));
+        if (colsum && !colsum_accumulate)
+            QSB_TRY(cuda_status(cudaMemsetAsync(colsum, 0, sizeof(float) * cols, st), "memset"));
         if (rows == 0 || cols == 0) return QSYNC_OK;
         dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
-        k_tile<DT, 1><<<grid, dim3(32, 8), 0, st>>>(static_cast<const T*>(x), rows, cols, nullptr,
-                                                    nullptr, out, out_t, colsum, nullptr);
+        const int vt = (cols % 4 == 0) && aligned16(x) && aligned16(out) && aligned16(out_t);
+        k_tile<DT, 1><<<grid, 256, 0, st>>>(static_cast<const T*>(x), rows, cols, nullptr, nullptr,
+                                            out, out_t, ld_t, colsum, nullptr, vt);
         return check_launch("k_tile<cast>");
     }
 };
@@ -634,10 +714,13 @@ int qsync_absmax_rows(const void* x, int dtype, int64_t rows, int64_t cols, floa
 }
 
 int qsync_quantize_per_tensor(const void* x, int dtype, int64_t rows, int64_t cols, int8_t* q,
-                              float* scale, uint16_t* q_t_f16, qsync_stream_t stream) {
+                              float* scale, uint16_t* q_t_f16, int64_t ld_t,
+                              qsync_stream_t stream) {
     QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
     QSB_REQUIRE(scale != nullptr, QSYNC_ERR_VALIDATION, "scale buffer (float[2]) is required");
-    return dispatch_dtype<QuantRun>(dtype, x, rows, cols, q, scale, q_t_f16, to_stream(stream));
+    if (ld_t <= 0) ld_t = rows;
+    QSB_REQUIRE(ld_t >= rows, QSYNC_ERR_DOMAIN, "transposed pitch must be >= rows");
+    return dispatch_dtype<QuantRun>(dtype, x, rows, cols, q, scale, q_t_f16, ld_t, to_stream(stream));
 }
 
 int qsync_quantize_with_scale(const void* x, int dtype, int64_t n, const float* scale, int8_t* q,
@@ -653,7 +736,7 @@ int qsync_quantize_per_channel(const float* w, int64_t rows, int64_t cols, int8_
     if (rows == 0) return QSYNC_OK;
     k_quant_rows<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(w, rows, cols, q, scales);
     QSB_TRY(check_launch("k_quant_rows"));
-    if (w_t_f16) return CastTRun<QSYNC_F32>::run(w, rows, cols, nullptr, w_t_f16, nullptr, st);
+    if (w_t_f16) return CastTRun<QSYNC_F32>::run(w, rows, cols, nullptr, w_t_f16, rows, nullptr, 0, st);
     return QSYNC_OK;
 }
 
@@ -700,10 +783,14 @@ int qsync_cast(const void* x, int src, void* out, int dst, int64_t n, qsync_stre
 }
 
 int qsync_cast_transpose(const void* x, int dtype, int64_t rows, int64_t cols, uint16_t* out,
-                         uint16_t* out_t, float* colsum, qsync_stream_t stream) {
+                         uint16_t* out_t, int64_t ld_t, float* colsum, int colsum_accumulate,
+                         qsync_stream_t stream) {
     QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
     QSB_REQUIRE(rows / TR < 65535, QSYNC_ERR_DOMAIN, "too many rows for cast_transpose");
-    return dispatch_dtype<CastTRun>(dtype, x, rows, cols, out, out_t, colsum, to_stream(stream));
+    if (ld_t <= 0) ld_t = rows;
+    QSB_REQUIRE(ld_t >= rows, QSYNC_ERR_DOMAIN, "transposed pitch must be >= rows");
+    return dispatch_dtype<CastTRun>(dtype, x, rows, cols, out, out_t, ld_t, colsum,
+                                    colsum_accumulate, to_stream(stream));
 }
 
 size_t qsync_stats_workspace_bytes(void) { return sizeof(double) * 2 * kStatsBlocks; }

@@ -52,19 +52,33 @@ def absmax_rows(x: torch.Tensor) -> torch.Tensor:
 
 
 # --------------------------------------------------------------------------- K2
+def pad8(n: int) -> int:
+    """Row pitch of a transposed FP16 operand: the GEMM K it becomes must be a
+    multiple of 8 (16-byte TMA pitch); pad columns are zero."""
+    return (n + 7) // 8 * 8
+
+
+def _transposed(cols: int, rows: int, device) -> torch.Tensor:
+    ld = pad8(rows)
+    if ld == rows:
+        return torch.empty((cols, ld), device=device, dtype=torch.float16)
+    return torch.zeros((cols, ld), device=device, dtype=torch.float16)
+
+
 def quantize_per_tensor(x: torch.Tensor, transposed_f16: bool = False, out=None):
     """Per-tensor RNE INT8 quantization of a 2-D (or flattened) tensor.
 
-    Returns (q int8 same shape, scale float32[2] = {s, absmax}, q_t f16 [cols, rows] or None).
+    Returns (q int8 same shape, scale float32[2] = {s, absmax}, q_t f16 [cols, pad8(rows)] or
+    None).
     """
     _req(x, "x", _DT)
     rows = x.shape[0] if x.dim() >= 2 else 1
     cols = x.numel() // max(rows, 1)
     q = out if out is not None else torch.empty(x.shape, device=x.device, dtype=torch.int8)
     scale = torch.empty(2, device=x.device, dtype=torch.float32)
-    qt = torch.empty((cols, rows), device=x.device, dtype=torch.float16) if transposed_f16 else None
+    qt = _transposed(cols, rows, x.device) if transposed_f16 else None
     call("qsync_quantize_per_tensor", _ptr(x), _DT[x.dtype], rows, cols, _ptr(q), _ptr(scale),
-         _ptr(qt), _stream())
+         _ptr(qt), qt.shape[1] if qt is not None else 0, _stream())
     return q, scale, qt
 
 
@@ -145,16 +159,23 @@ def cast(x: torch.Tensor, dtype: torch.dtype, out=None) -> torch.Tensor:
 
 
 def cast_transpose(x: torch.Tensor, want_out: bool = True, want_t: bool = True,
-                   want_colsum: bool = False):
-    """[rows, cols] -> (FP16 copy, FP16 transpose [cols, rows], FP32 column sums)."""
+                   want_colsum: bool = False, colsum_into: torch.Tensor | None = None):
+    """[rows, cols] -> (FP16 copy, FP16 transpose [cols, pad8(rows)], FP32 column sums).
+
+    With ``colsum_into`` the column sums are ADDED into that FP32 buffer (the
+    bias gradient accumulated straight into its main_grad slot)."""
     _req(x, "x", (torch.float32, torch.float16))
     rows = x.shape[0]
     cols = x.numel() // max(rows, 1)
     o = torch.empty((rows, cols), device=x.device, dtype=torch.float16) if want_out else None
-    t = torch.empty((cols, rows), device=x.device, dtype=torch.float16) if want_t else None
-    s = torch.empty(cols, device=x.device, dtype=torch.float32) if want_colsum else None
-    call("qsync_cast_transpose", _ptr(x), _DT[x.dtype], rows, cols, _ptr(o), _ptr(t), _ptr(s),
-         _stream())
+    t = _transposed(cols, rows, x.device) if want_t else None
+    if colsum_into is not None:
+        s, acc = colsum_into, 1
+    else:
+        s = torch.empty(cols, device=x.device, dtype=torch.float32) if want_colsum else None
+        acc = 0
+    call("qsync_cast_transpose", _ptr(x), _DT[x.dtype], rows, cols, _ptr(o), _ptr(t),
+         t.shape[1] if t is not None else 0, _ptr(s), acc, _stream())
     return o, t, s
 
 
@@ -231,9 +252,43 @@ def gemm_f16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32, alpha: f
     return c
 
 
+# --------------------------------------------------------------------------- glue
+def layernorm_fwd(a: torch.Tensor, b: torch.Tensor | None, gamma, beta, eps: float):
+    """s = a + b, y = LN(s).  Returns (y, s, mean, rstd)."""
+    _req(a, "a", (torch.float32,))
+    cols = a.shape[-1]
+    rows = a.numel() // cols
+    y = torch.empty_like(a)
+    s = torch.empty_like(a) if b is not None else None
+    mean = torch.empty(rows, device=a.device, dtype=torch.float32)
+    rstd = torch.empty(rows, device=a.device, dtype=torch.float32)
+    bd = _DT[b.dtype] if b is not None else F32
+    if b is not None:
+        _req(b, "b", (torch.float32, torch.float16))
+    call("qsync_layernorm_fwd", _ptr(a), _ptr(b), bd, _ptr(gamma), _ptr(beta), rows, cols,
+         float(eps), _ptr(s), _ptr(y), _ptr(mean), _ptr(rstd), _stream())
+    return y, (s if s is not None else a), mean, rstd
+
+
+def layernorm_bwd(dy: torch.Tensor, s, mean, rstd, gamma, dgamma, dbeta) -> torch.Tensor:
+    """dx of LN; dgamma / dbeta are ADDED into the given FP32 buffers."""
+    _req(dy, "dy", (torch.float32,))
+    cols = dy.shape[-1]
+    rows = dy.numel() // cols
+    dx = torch.empty_like(dy)
+    call("qsync_layernorm_bwd", _ptr(dy), _ptr(s), _ptr(mean), _ptr(rstd), _ptr(gamma), rows, cols,
+         _ptr(dx), _ptr(dgamma), _ptr(dbeta), _stream())
+    return dx
+
+
 def launch_count() -> int:
     """Kernels launched by libqsync_b200 so far in this process."""
     return int(_lib.lib().qsync_launch_count())
+
+
+def force_splitk(ks: int) -> None:
+    """Bench hook: pin the split-K factor of accumulating GEMMs (0 = heuristic)."""
+    call("qsync_gemm_force_splitk", int(ks))
 
 
 def force_tile_n(bn: int) -> None:

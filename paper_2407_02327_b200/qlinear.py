@@ -35,27 +35,49 @@ def backward_precision(precision: str) -> str:
     return FP16 if precision == INT8 else precision
 
 
+def _main_grad(p):
+    return getattr(p, "main_grad", None) if p is not None else None
+
+
+def _fp16_backward(ctx, dy, x16_t, w16_t, alpha_dev):
+    """Shared FP16 backward (cost_mapper.cpp:13-15).  When the parameters carry a
+    ``main_grad`` (a slice of the flat FP32 gradient bucket), wgrad is ADDED into
+    it by the GEMM epilogue's TMA reduce-add and the bias gradient by the
+    cast-transpose column sums, and autograd receives None for them -- no
+    separate accumulate / zero kernels per parameter."""
+    w, b = ctx.w_ref, ctx.b_ref
+    dy = dy.contiguous()
+    mw, mb = _main_grad(w), _main_grad(b)
+    dy16, dy16_t, db = ops.cast_transpose(dy, True, True, b is not None and mb is None,
+                                          colsum_into=mb)
+    dx = ops.gemm_f16(dy16, w16_t, out_dtype=ctx.x_dtype)  # dgrad [M, K]
+    if mw is not None:
+        ops.gemm_f16(dy16_t, x16_t, alpha_dev=alpha_dev, out=mw, accumulate=True)
+        dw = None
+    else:
+        dw = ops.gemm_f16(dy16_t, x16_t, out_dtype=torch.float32, alpha_dev=alpha_dev)  # wgrad
+    if mb is not None:
+        db = None
+    return dx, dw, db
+
+
 class _QLinearInt8(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, b):
-        M = x.shape[0]
         xq, xs, xq_t = ops.quantize_per_tensor(x, transposed_f16=True)
         wq, ws, w_t16 = ops.quantize_per_channel(w, transposed_f16=True)
         _, y = ops.gemm_s8(xq, wq, xs, ws, b)
         ctx.save_for_backward(xq_t, xs, w_t16)
         ctx.x_dtype = x.dtype
-        ctx.has_bias = b is not None
-        ctx.M = M
+        ctx.w_ref, ctx.b_ref = w, b
         return y
 
     @staticmethod
     def backward(ctx, dy):
         xq_t, xs, w_t16 = ctx.saved_tensors
-        dy = dy.contiguous()
-        dy16, dy16_t, db = ops.cast_transpose(dy, True, True, ctx.has_bias)
-        dx = ops.gemm_f16(dy16, w_t16, out_dtype=ctx.x_dtype)              # dgrad [M, K]
-        dw = ops.gemm_f16(dy16_t, xq_t, out_dtype=torch.float32, alpha_dev=xs)  # wgrad [N, K]
-        return dx, dw, db
+        # wgrad = s_x * dY16^T X^ : the saved INT8 activation (as exact FP16
+        # integers) with the activation scale applied in the epilogue.
+        return _fp16_backward(ctx, dy, xq_t, w_t16, xs)
 
 
 class _QLinearFp16(torch.autograd.Function):
@@ -70,17 +92,13 @@ class _QLinearFp16(torch.autograd.Function):
         y = ops.gemm_f16(x16, w16, out_dtype=torch.float16, bias=b)
         ctx.save_for_backward(x16_t, w16_t)
         ctx.x_dtype = x.dtype
-        ctx.has_bias = b is not None
+        ctx.w_ref, ctx.b_ref = w, b
         return y
 
     @staticmethod
     def backward(ctx, dy):
         x16_t, w16_t = ctx.saved_tensors
-        dy = dy.contiguous()
-        dy16, dy16_t, db = ops.cast_transpose(dy, True, True, ctx.has_bias)
-        dx = ops.gemm_f16(dy16, w16_t, out_dtype=ctx.x_dtype)
-        dw = ops.gemm_f16(dy16_t, x16_t, out_dtype=torch.float32)
-        return dx, dw, db
+        return _fp16_backward(ctx, dy, x16_t, w16_t, None)
 
 
 class _Cast(torch.autograd.Function):

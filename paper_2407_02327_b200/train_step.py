@@ -24,7 +24,9 @@ from dataclasses import dataclass
 
 import torch
 import torch.nn.functional as F
+from flash_attn import flash_attn_qkvpacked_func
 
+from .glue import AddLayerNorm
 from .qlinear import FP16, FP32, INT8, QLinear, cast
 
 
@@ -92,20 +94,21 @@ class EncoderLayer(torch.nn.Module):
         self.o = QLinear(h, h, f"layer{i}.o")
         self.ff1 = QLinear(h, cfg.ffn, f"layer{i}.ff1")
         self.ff2 = QLinear(cfg.ffn, h, f"layer{i}.ff2")
-        self.ln1 = torch.nn.LayerNorm(h, eps=1e-12)
-        self.ln2 = torch.nn.LayerNorm(h, eps=1e-12)
+        self.ln1 = AddLayerNorm(h, eps=1e-12)
+        self.ln2 = AddLayerNorm(h, eps=1e-12)
 
     def forward(self, x):  # x [B, S, H] fp32 residual stream
         B, S, H = x.shape
         nh = self.cfg.heads
         qkv = self.qkv(x)  # [B, S, 3H] fp32 (INT8) / fp16 (FP16)
         qkv = cast(qkv, torch.float16)
-        q, k, v = qkv.view(B, S, 3, nh, H // nh).permute(2, 0, 3, 1, 4).unbind(0)
-        a = F.scaled_dot_product_attention(q, k, v)  # [B, nh, S, d] fp16
-        a = a.transpose(1, 2).reshape(B, S, H)
-        x = self.ln1(x + cast(self.o(a), torch.float32))
+        # Attention core stays floating point; packed QKV in,
+        # packed dQKV out -- no permute/stack copies around it.
+        a = flash_attn_qkvpacked_func(qkv.view(B, S, 3, nh, H // nh))  # [B, S, nh, d]
+        a = a.reshape(B, S, H)
+        x = self.ln1(x, self.o(a))        # fused residual add (FP32 or FP16 operand)
         f = F.gelu(self.ff1(x))
-        x = self.ln2(x + cast(self.ff2(f), torch.float32))
+        x = self.ln2(x, self.ff2(f))
         return x
 
 
@@ -118,7 +121,7 @@ class BertEncoderStack(torch.nn.Module):
         self.word = torch.nn.Embedding(cfg.vocab, cfg.hidden)
         self.pos = torch.nn.Embedding(cfg.max_pos, cfg.hidden)
         self.typ = torch.nn.Embedding(cfg.type_vocab, cfg.hidden)
-        self.ln = torch.nn.LayerNorm(cfg.hidden, eps=1e-12)
+        self.ln = AddLayerNorm(cfg.hidden, eps=1e-12)
         self.layers = torch.nn.ModuleList([EncoderLayer(cfg, i) for i in range(cfg.layers)])
         self.pooler = QLinear(cfg.hidden, cfg.hidden, "pooler")
         self.cls = torch.nn.Linear(cfg.hidden, cfg.num_labels)
@@ -153,53 +156,53 @@ def linear_flops_per_step(cfg: BertConfig, tokens: int) -> float:
 
 
 # --------------------------------------------------------------------------- DP
-class BucketReducer:
-    """Bucketed FP32 gradient all-reduce in backward (reverse-topological) order.
+class FlatGrads:
+    """All FP32 gradients in ONE flat buffer laid out in backward order (last
+    layer first), so that (a) each parameter's ``grad`` and ``main_grad`` are
+    views of it -- QLinear wgrad/bias-grad kernels accumulate straight into their
+    slice and the optimizer reads it in place; (b) zeroing is one memset; (c) DP
+    buckets are contiguous slices, all-reduced without packing copies."""
 
-    Buckets are fixed at construction from the parameter order, identical on all
-    ranks; ``reduce()`` issues one all-reduce per bucket, in order, on the
-    current stream, then divides by the world size.  Works on any device / any
-    torch.distributed backend (NCCL on B200, gloo in the CPU tests).
-    """
-
-    def __init__(self, params: list[torch.nn.Parameter], bucket_bytes: int = 25 << 20):
+    def __init__(self, params: list[torch.nn.Parameter], bucket_bytes: int = 32 << 20):
         self.params = [p for p in params if p.requires_grad]
-        self.buckets: list[list[torch.nn.Parameter]] = []
-        cur: list[torch.nn.Parameter] = []
-        size = 0
-        for p in reversed(self.params):  # backward order: last layer's grads first
-            cur.append(p)
-            size += p.numel() * 4
-            if size >= bucket_bytes:
-                self.buckets.append(cur)
-                cur, size = [], 0
-        if cur:
-            self.buckets.append(cur)
-        self.flat = None
+        order = list(reversed(self.params))
+        # Every slot starts on a 64-byte boundary: the GEMM epilogue's TMA
+        # reduce-add (and vector paths) need 16-byte aligned rows.
+        align = 16
+        slots, total = [], 0
+        for p in order:
+            slots.append(total)
+            total += (p.numel() + align - 1) // align * align
+        dev = order[0].device
+        self.flat = torch.zeros(total, device=dev, dtype=torch.float32)
+        self.buckets: list[tuple[int, int]] = []  # (start, end) element ranges
+        off = 0
+        b_start = 0
+        for p, start in zip(order, slots):
+            n = p.numel()
+            view = self.flat[start:start + n].view_as(p)
+            p.main_grad = view
+            p.grad = view
+            off = start + (n + align - 1) // align * align
+            if (off - b_start) * 4 >= bucket_bytes:
+                self.buckets.append((b_start, off))
+                b_start = off
+        if off > b_start:
+            self.buckets.append((b_start, off))
 
-    def _flat(self, device):
-        if self.flat is None:
-            self.flat = [torch.zeros(sum(p.numel() for p in b), device=device) for b in self.buckets]
-        return self.flat
+    def zero(self) -> None:
+        self.flat.zero_()
 
-    def reduce(self, world: int) -> None:
+    def allreduce(self, world: int) -> None:
+        """Bucket n after bucket n-1, all ranks in the same order (Eq. 6 slots,
+        replayer.cpp:48-62), then average."""
         import torch.distributed as dist
         if world <= 1:
             return
-        flats = self._flat(self.params[0].device)
-        for b, flat in zip(self.buckets, flats):
-            off = 0
-            for p in b:
-                n = p.numel()
-                flat[off:off + n].copy_(p.grad.reshape(-1))
-                off += n
-            dist.all_reduce(flat)
-            flat.div_(world)
-            off = 0
-            for p in b:
-                n = p.numel()
-                p.grad.copy_(flat[off:off + n].view_as(p.grad))
-                off += n
+        for (a, b) in self.buckets:
+            chunk = self.flat[a:b]
+            dist.all_reduce(chunk)
+        self.flat.div_(world)
 
 
 class TrainStep:
@@ -215,21 +218,18 @@ class TrainStep:
         self.tokens = torch.zeros((batch, cfg.seq), dtype=torch.long, device=dev)
         self.labels = torch.zeros((batch,), dtype=torch.long, device=dev)
         self.params = [p for p in model.parameters() if p.requires_grad]
-        for p in self.params:
-            p.grad = torch.zeros_like(p)
+        self.grads = FlatGrads(self.params)
         self.opt = torch.optim.AdamW(self.params, lr=lr, fused=True, capturable=graph)
-        self.reducer = BucketReducer(self.params)
         self.use_graph = graph
         self.graph = None
         self.loss = None
 
     def _body(self):
+        self.grads.zero()
         loss = self.model(self.tokens, self.labels)
         loss.backward()
-        self.reducer.reduce(self.world)
+        self.grads.allreduce(self.world)
         self.opt.step()
-        for p in self.params:
-            p.grad.zero_()
         return loss.detach()
 
     def capture(self, warmup: int = 3) -> None:

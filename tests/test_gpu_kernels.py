@@ -52,7 +52,11 @@ def test_quantize_per_tensor_bit_exact(shape, dist, cpuref):
     assert np.float32(_np(scale)[0]) == s_ref
     assert _np(scale)[1] == cpuref.absmax(x)
     assert np.array_equal(_np(q), q_ref)
-    assert np.array_equal(_np(qt).astype(np.int32), q_ref.T.astype(np.int32))
+    qt = _np(qt)
+    rows = shape[0]
+    assert qt.shape == (shape[1], (rows + 7) // 8 * 8)  # K-pitch padded to 8 for TMA
+    assert np.array_equal(qt[:, :rows].astype(np.int32), q_ref.T.astype(np.int32))
+    assert not qt[:, rows:].any()
     q2, scale2, _ = ops.quantize_per_tensor(_t(x))
     assert np.array_equal(_np(q2), q_ref) and _np(scale2)[0] == s_ref
 
@@ -130,7 +134,9 @@ def test_cast_transpose(shape, cpuref):
     o, t, s = ops.cast_transpose(_t(x), True, True, True)
     h = cpuref.cast_f32_f16(x)
     assert np.array_equal(_np(o).view(np.uint16), h.view(np.uint16))
-    assert np.array_equal(_np(t).view(np.uint16), h.T.view(np.uint16))
+    t = _np(t)
+    assert np.array_equal(t[:, :shape[0]].view(np.uint16), h.T.view(np.uint16))
+    assert not t[:, shape[0]:].astype(np.float32).any()
     np.testing.assert_allclose(_np(s), x.astype(np.float64).sum(0), rtol=1e-5, atol=1e-3)
 
 

@@ -1,0 +1,55 @@
+"""Run one hot kernel a few times for ncu (`ncu -k regex:... python tools/prof_targets.py <name>`).
+
+Targets use the bench's shapes: BERT-base FF1 forward (4096x3072x768 INT8 with the
+fused dequant epilogue), the INT8 GEMM at 8192^3, the FP16 dgrad shape, and the
+1 GiB quantize / cast / stats sweep points.
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2407_02327_b200 import ops  # noqa: E402
+
+
+def main(name: str, reps: int = 3) -> None:
+    dev = "cuda"
+    if name.startswith("gemm_s8"):
+        M, N, K = (8192, 8192, 8192) if name.endswith("8192") else (4096, 3072, 768)
+        a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device=dev)
+        b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device=dev)
+        sa = torch.tensor([0.01], device=dev)
+        sb = torch.rand(N, device=dev) * 0.01
+        bias = torch.randn(N, device=dev)
+        out = torch.empty((M, N), device=dev)
+        fn = lambda: ops.gemm_s8(a, b, sa, sb, bias, out=out)  # noqa: E731
+    elif name.startswith("gemm_f16"):
+        M, N, K = (8192, 8192, 8192) if name.endswith("8192") else (4096, 768, 3072)
+        a = torch.randn((M, K), device=dev).half()
+        b = torch.randn((N, K), device=dev).half()
+        out = torch.empty((M, N), device=dev)
+        fn = lambda: ops.gemm_f16(a, b, out=out)  # noqa: E731
+    else:
+        n = (1 << 30) // 4
+        x = torch.randn(n, device=dev)
+        x2 = x.view(-1, 1024)
+        q = torch.empty(n, dtype=torch.int8, device=dev)
+        sc = torch.tensor([0.01], device=dev)
+        h = torch.empty(n, dtype=torch.float16, device=dev)
+        fn = {
+            "quantize_per_tensor": lambda: ops.quantize_per_tensor(x2, out=q.view(x2.shape)),
+            "quantize_with_scale": lambda: ops.quantize_with_scale(x, sc),
+            "quantize_per_channel": lambda: ops.quantize_per_channel(x2),
+            "dequantize": lambda: ops.dequantize_per_tensor(q, sc),
+            "cast": lambda: ops.cast(x, torch.float16, out=h),
+            "stats": lambda: ops.tensor_stats(x),
+            "absmax": lambda: ops.absmax(x),
+        }[name]
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 3)
