@@ -1,0 +1,91 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the DP host logic: the flat
+FP32 gradient buffer, bucket order (reverse topological, identical on every
+rank whatever its precision plan), 64-byte slot alignment and the averaging
+all-reduce (Eq. 6 slot semantics, replayer.cpp:48-62)."""
+import json
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2407_02327_b200.qlinear import FP16, FP32, INT8
+from paper_2407_02327_b200.train_step import (BertConfig, FlatGrads, adjustable_ops, load_plan,
+                                              mixed_plan)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _params(seed_shape_only=True):
+    torch.manual_seed(0)
+    shapes = [(2,), (2, 768), (768,), (3072, 768), (768, 3072), (768,), (2304, 768), (2304,)]
+    return [torch.nn.Parameter(torch.randn(*s)) for s in shapes]
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    params = _params()
+    g = FlatGrads(params, bucket_bytes=4 << 20)
+    # every rank fills its grads differently (as different precision plans would)
+    for i, p in enumerate(params):
+        p.main_grad.copy_(torch.full_like(p, float(rank + 1) * (i + 1)))
+    g.allreduce(world)
+    res = {
+        "buckets": g.buckets,
+        "offsets": [int(p.main_grad.data_ptr() - g.flat.data_ptr()) for p in params],
+        "vals": [float(p.grad.flatten()[0]) for p in params],
+        "same_storage": all(p.grad.data_ptr() == p.main_grad.data_ptr() for p in params),
+    }
+    with open(os.path.join(out_dir, f"r{rank}.json"), "w") as f:
+        json.dump(res, f)
+    dist.destroy_process_group()
+
+
+def test_flat_grads_allreduce_world2(tmp_path):
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r0 = json.load(open(tmp_path / "r0.json"))
+    r1 = json.load(open(tmp_path / "r1.json"))
+    assert r0["buckets"] == r1["buckets"]            # identical bucket layout on all ranks
+    assert r0["offsets"] == r1["offsets"]
+    assert all(o % 64 == 0 for o in r0["offsets"])   # 64-byte aligned slots (TMA reduce-add)
+    # reverse topological order: the last parameter sits first in the flat buffer
+    assert r0["offsets"][-1] == 0 and r0["offsets"] == sorted(r0["offsets"], reverse=True)
+    # average of (rank+1)*(i+1) over ranks 1, 2 -> 1.5 * (i+1)
+    for i, v in enumerate(r0["vals"]):
+        assert v == pytest.approx(1.5 * (i + 1))
+    assert r0["vals"] == r1["vals"]
+    assert r0["same_storage"]
+    # buckets tile the buffer contiguously
+    b = r0["buckets"]
+    assert b[0][0] == 0 and all(b[i][1] == b[i + 1][0] for i in range(len(b) - 1))
+
+
+def test_plan_file_formats(tmp_path):
+    cfg = BertConfig(layers=2)
+    bare = {"per_device": {"infer": {"layer0.qkv": "INT8", "layer1.ff2": "FP16"}}}
+    p = tmp_path / "plan.json"
+    p.write_text(json.dumps(bare))
+    plan = load_plan(str(p), "infer")
+    assert plan == {"layer0.qkv": INT8, "layer1.ff2": FP16}
+    report = {"devices": {"infer": {"layer0.o": "FP32"}}, "omega_before": 1.0}
+    p.write_text(json.dumps(report))
+    assert load_plan(str(p), "infer") == {"layer0.o": FP32}
+    with pytest.raises(KeyError, match="reference"):
+        load_plan(str(p), "nope")
+    p.write_text(json.dumps({"per_device": {"d": {"x": "INT4"}}}))
+    with pytest.raises(ValueError, match="unknown precision"):
+        load_plan(str(p), "d")
+    mp_ = mixed_plan(cfg)
+    assert set(mp_) == set(adjustable_ops(cfg))
+    assert mp_["layer0.qkv"] == INT8 and mp_["layer1.qkv"] == FP16 and mp_["pooler"] == FP32
