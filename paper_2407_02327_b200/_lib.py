@@ -65,6 +65,7 @@ SIGNATURES = {
     # non-header helpers
     "qsync_gemm_force_tile_n": [_int],
     "qsync_gemm_force_splitk": [_int],
+    "qsync_gemm_force_cta": [_int],
     "qsync_mt_jump_selftest": [],
 }
 _RESTYPES = {"qsync_last_error": C.c_char_p, "qsync_status_name": C.c_char_p,

@@ -54,10 +54,14 @@ struct EpiParams {
 
 constexpr int kStageChunkBytes = 32 * 128;  // one warp's 32 rows x 128 B staging chunk
 
-template <int BN>
+// kCta = 1: one CTA computes a 128 x BN tile.  kCta = 2: a CTA pair (cluster of
+// 2, cta_group::2) computes a 256 x BN tile; each CTA holds its 128 A rows and
+// half (BN/2 rows) of B, and the leader issues 2-SM MMAs reading both halves.
+template <int BN, int kCta = 1>
 struct Cfg {
-    static constexpr int kStageBytes = (BM + BN) * BK_BYTES;
-    static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+    static constexpr int kBRows = BN / kCta;  // B rows held by one CTA
+    static constexpr int kStageBytes = (BM + kBRows) * BK_BYTES;
+    static constexpr int kStages = kStageBytes >= 48 * 1024 ? 4 : (kStageBytes >= 32 * 1024 ? 6 : 8);
     static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
     static constexpr int kEpiStageBytes = 4 * 2 * kStageChunkBytes;  // 4 warps x double buffer
     static constexpr int kSmemBytes =
@@ -66,18 +70,19 @@ struct Cfg {
 
 __device__ __forceinline__ float bits_f(uint32_t v) { return __uint_as_float(v); }
 
-template <bool kI8, int BN>
+template <bool kI8, int BN, int kCta>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
               const __grid_constant__ CUtensorMap tm_c, const EpiParams p) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, kCta>;
+    constexpr int kBRows = C::kBRows;
     constexpr int kStages = C::kStages;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B swizzle atoms.
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
     uint8_t* smem_a = smem;                              // kStages x [BM rows x 128B]
-    uint8_t* smem_b = smem + kStages * BM * BK_BYTES;    // kStages x [BN rows x 128B]
+    uint8_t* smem_b = smem + kStages * BM * BK_BYTES;    // kStages x [kBRows rows x 128B]
     uint8_t* smem_stage = smem + kStages * C::kStageBytes;  // 1024-aligned epilogue staging
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_stage + C::kEpiStageBytes);
     uint64_t* full = bars;
@@ -90,7 +95,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = threadIdx.x & 31;
 
     const int64_t M = p.M, N = p.N, K = p.K;
-    const int num_m = static_cast<int>((M + BM - 1) / BM);
+    constexpr int kTileM = BM * kCta;  // rows of one (pair) tile
+    const int num_m = static_cast<int>((M + kTileM - 1) / kTileM);
+    // CTA pairs share one work sequence; rank 0 of a pair leads the MMAs.
+    const uint32_t rank = kCta == 2 ? ptx::cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int unit0 = blockIdx.x / kCta;
+    const int unit_stride = gridDim.x / kCta;
     const int num_n = static_cast<int>((N + BN - 1) / BN);
     const int num_tiles = num_m * num_n;
     // Work units = (tile, K split); split-K partials are reduce-added by TMA.
@@ -109,34 +120,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 4 * 32);
+            ptx::mbar_init(&tempty[a], kCta * 4 * 32);  // epilogue threads of both CTAs
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    if (warp == 1) {
+        if (kCta == 2)
+            ptx::tmem_alloc_pair<C::kTmemCols>(tmem_slot);
+        else
+            ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if (kCta == 2)
+        ptx::cluster_sync();  // peer barriers initialised before any remote arrive
+    else
+        __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Leader-CTA addresses of the barriers the pair shares.
+    const uint32_t full_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
+    const uint32_t tempty_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
 
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+            for (int u = unit0; u < num_units; u += unit_stride) {
                 const int t = u / ksplit;
-                const int m0 = (t % num_m) * BM;
-                const int n0 = (t / num_m) * BN;
+                const int m0 = (t % num_m) * kTileM + static_cast<int>(rank) * BM;
+                const int n0 = (t / num_m) * BN + static_cast<int>(rank) * kBRows;
                 const int kb0 = (u % ksplit) * p.kb_per;
                 const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                    ptx::tma_load_2d(smem_a + stage * BM * BK_BYTES, &tm_a, &full[stage],
-                                     kb * bk_elems, m0);
-                    ptx::tma_load_2d(smem_b + stage * BN * BK_BYTES, &tm_b, &full[stage],
-                                     kb * bk_elems, n0);
+                    if (kCta == 2) {
+                        // Both CTAs' bytes complete on the leader's full barrier.
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], kCta * C::kStageBytes);
+                        const uint32_t fb = full_leader0 + stage * 8;
+                        ptx::tma_load_2d_pair(smem_a + stage * BM * BK_BYTES, &tm_a, fb,
+                                              kb * bk_elems, m0);
+                        ptx::tma_load_2d_pair(smem_b + stage * kBRows * BK_BYTES, &tm_b, fb,
+                                              kb * bk_elems, n0);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        ptx::tma_load_2d(smem_a + stage * BM * BK_BYTES, &tm_a, &full[stage],
+                                         kb * bk_elems, m0);
+                        ptx::tma_load_2d(smem_b + stage * kBRows * BK_BYTES, &tm_b, &full[stage],
+                                         kb * bk_elems, n0);
+                    }
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -145,13 +177,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        if (lane == 0) {
+        // ===================== MMA issuer (leader CTA of a pair) =====================
+        if (lane == 0 && leader) {
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+            for (int u = unit0; u < num_units; u += unit_stride) {
                 const int kb0 = (u % ksplit) * p.kb_per;
                 const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -161,24 +193,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t a_addr = ptx::smem_u32(smem_a + stage * BM * BK_BYTES);
-                    const uint32_t b_addr = ptx::smem_u32(smem_b + stage * BN * BK_BYTES);
+                    const uint32_t b_addr = ptx::smem_u32(smem_b + stage * kBRows * BK_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK_BYTES / 32; ++k) {  // UMMA_K = 32 bytes
                         const uint64_t da = ptx::sw128_kmajor_desc(a_addr + k * 32);
                         const uint64_t db = ptx::sw128_kmajor_desc(b_addr + k * 32);
                         const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
-                        if (kI8)
-                            ptx::mma_i8(d_tmem, da, db, p.idesc, accum);
-                        else
-                            ptx::mma_f16(d_tmem, da, db, p.idesc, accum);
+                        if (kCta == 2) {
+                            if (kI8)
+                                ptx::mma_i8_pair(d_tmem, da, db, p.idesc, accum);
+                            else
+                                ptx::mma_f16_pair(d_tmem, da, db, p.idesc, accum);
+                        } else {
+                            if (kI8)
+                                ptx::mma_i8(d_tmem, da, db, p.idesc, accum);
+                            else
+                                ptx::mma_f16(d_tmem, da, db, p.idesc, accum);
+                        }
                     }
-                    ptx::tc_commit(&empty[stage]);
+                    if (kCta == 2)
+                        ptx::tc_commit_pair(&empty[stage]);  // frees the stage in both CTAs
+                    else
+                        ptx::tc_commit(&empty[stage]);
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                ptx::tc_commit(&tfull[acc]);
+                if (kCta == 2)
+                    ptx::tc_commit_pair(&tfull[acc]);  // both CTAs' epilogues
+                else
+                    ptx::tc_commit(&tfull[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -203,10 +248,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool raw = p.c_i32 != nullptr && p.c == nullptr;
         const int chunk_cols = out16 ? 64 : 32;
         constexpr int kNC = BN / 32;  // 32-column groups per tile
-        for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        for (int u = unit0; u < num_units; u += unit_stride) {
             const int t = u / ksplit;
             const bool add_bias = (u % ksplit) == 0;  // bias once per tile under split-K
-            const int64_t m0 = static_cast<int64_t>(t % num_m) * BM;
+            const int64_t m0 = static_cast<int64_t>(t % num_m) * kTileM + static_cast<int64_t>(rank) * BM;
             const int64_t n0 = static_cast<int64_t>(t / num_m) * BN;
             // Per-column epilogue factors of this tile, loaded BEFORE waiting for
             // the accumulator so their latency hides behind the tile's MMAs:
@@ -352,7 +397,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[acc]);
+            if (kCta == 2)
+                ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);  // leader's barrier
+            else
+                ptx::mbar_arrive(&tempty[acc]);
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -362,10 +410,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if (kCta == 2)
+        ptx::cluster_sync();  // both CTAs done with TMEM and remote barriers
+    else
+        __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+        if (kCta == 2)
+            ptx::tmem_dealloc_pair<C::kTmemCols>(tmem_base);
+        else
+            ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
     }
 }
 
@@ -411,28 +465,29 @@ int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t
 
 // Instruction descriptor (tcgen05 "idesc"): c_format [4,6), a_format [7,10),
 // b_format [10,13), a/b major [15],[16] (0 = K-major), N>>3 [17,23), M>>4 [24,29).
-uint32_t make_idesc(bool i8, bool bf16, int n) {
+uint32_t make_idesc(bool i8, bool bf16, int n, int m) {
     uint32_t d = 0;
     d |= (i8 ? 2u : 1u) << 4;                         // S32 / F32 accumulator
     const uint32_t fmt = i8 ? 1u : (bf16 ? 1u : 0u);  // signed int8 / BF16 / F16
     d |= fmt << 7;
     d |= fmt << 10;
     d |= static_cast<uint32_t>(n >> 3) << 17;
-    d |= static_cast<uint32_t>(BM >> 4) << 24;
+    d |= static_cast<uint32_t>(m >> 4) << 24;         // 128 (1 CTA) or 256 (CTA pair)
     return d;
 }
 
 int g_force_splitk = 0;  // test/bench hook (qsync_gemm_force_splitk): 0 = heuristic
 int g_splitk_wide = 0;   // accumulate GEMMs prefer BN=256 (bench hook)
+int g_force_cta = 0;     // test/bench hook (qsync_gemm_force_cta): 0 = cost model, 1, 2
 
-template <bool kI8, int BN>
+template <bool kI8, int BN, int kCta>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, kCta>;
     const uint32_t eb = kI8 ? 1 : 2;
     const uint32_t box_k = BK_BYTES / eb;
     CUtensorMap ma, mb, mc;
     QSB_TRY(make_map(&ma, a, dt, eb, p.K, p.M, box_k, BM));
-    QSB_TRY(make_map(&mb, b, dt, eb, p.K, p.N, box_k, BN));
+    QSB_TRY(make_map(&mb, b, dt, eb, p.K, p.N, box_k, C::kBRows));
     std::memset(&mc, 0, sizeof(mc));
     // TMA-store epilogue when exactly one output is requested and its rows are
     // 16-byte pitched and aligned; 16-bit accumulate keeps the direct path.
@@ -451,13 +506,13 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     }
     static bool configured = false;
     if (!configured) {
-        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_gemm_tc<kI8, BN>,
+        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_gemm_tc<kI8, BN, kCta>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  C::kSmemBytes),
                             "cudaFuncSetAttribute"));
         configured = true;
     }
-    const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+    const int64_t tiles = ((p.M + BM * kCta - 1) / (BM * kCta)) * ((p.N + BN - 1) / BN);
     // Split-K when the tile grid leaves SMs idle and the result is reduce-added
     // anyway (accumulating FP32 output, e.g. wgrad into the flat main_grad).
     const int64_t bk_elems = BK_BYTES / eb;
@@ -465,14 +520,16 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     p.ksplit = 1;
     p.kb_per = static_cast<int>(num_kb);
     const int sms = sm_count();
+    const int slots = sms / kCta;  // concurrent (pair) tiles
+    const bool can_split = p.accumulate && p.tma_store && p.c_dtype == QSYNC_F32 && !kI8;
     if (g_force_splitk > 0) {
-        if (p.accumulate && p.tma_store && p.c_dtype == QSYNC_F32 && !kI8 && g_force_splitk > 1) {
+        if (can_split && g_force_splitk > 1) {
             const int64_t per = (num_kb + g_force_splitk - 1) / g_force_splitk;
             p.kb_per = static_cast<int>(per);
             p.ksplit = static_cast<int>((num_kb + per - 1) / per);
         }
-    } else if (p.accumulate && p.tma_store && p.c_dtype == QSYNC_F32 && !kI8 && tiles < sms) {
-        int64_t want = std::max<int64_t>(1, (2 * sms) / tiles);         // ~2 units per SM
+    } else if (can_split && tiles < slots) {
+        int64_t want = std::max<int64_t>(1, (2 * slots) / tiles);         // ~2 units per slot
         want = std::min<int64_t>(want, std::max<int64_t>(1, num_kb / 8));  // >= 8 k-blocks each
         if (want > 1) {
             const int64_t per = (num_kb + want - 1) / want;
@@ -481,27 +538,50 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
         }
     }
     const int64_t units = tiles * p.ksplit;
-    const int grid = static_cast<int>(std::min<int64_t>(units, sms));
-    k_gemm_tc<kI8, BN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, p);
-    return check_launch("k_gemm_tc");
+    const int grid = static_cast<int>(std::min<int64_t>(units, slots)) * kCta;
+    if (kCta == 1) {
+        k_gemm_tc<kI8, BN, 1><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, p);
+        return check_launch("k_gemm_tc");
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    QSB_TRY(cuda_status(cudaLaunchKernelEx(&cfg, k_gemm_tc<kI8, BN, kCta>, ma, mb, mc, p),
+                        "cudaLaunchKernelEx(cluster 2)"));
+    return check_launch("k_gemm_tc<pair>");
 }
 
-// Pick BN from {256, 128, 64} minimising (waves x per-tile cost), where the
-// per-k-block cost is max(MMA cycles, smem operand bytes / 128 B per cycle).
-int pick_bn(int64_t M, int64_t N) {
+// Tile-shape cost model: per k-block a tile costs max(MMA cycles, operand bytes
+// this SM pulls from L2 / ~64 B per cycle); total = waves x k-blocks x that.
+// CTA pairs halve the B bytes per SM (each CTA holds half of B).
+struct Shape {
+    int bn, cta;
+};
+Shape pick_shape(int64_t M, int64_t N, bool allow_pair) {
     const int sms = sm_count();
-    const int cands[3] = {256, 128, 64};
-    int best = 256;
+    const Shape cands[5] = {{256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
+    Shape best{256, 1};
     double best_cost = 1e300;
-    for (int bn : cands) {
-        const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-        const int64_t waves = (tiles + sms - 1) / sms;
-        const double mma = 4.0 * BM * bn / 256.0;
-        const double smem = (BM + bn) * 128.0 / 128.0;
-        const double cost = static_cast<double>(waves) * std::max(mma, smem);
+    for (const Shape& c : cands) {
+        if (c.cta == 2 && (!allow_pair || M <= BM)) continue;
+        const int64_t tiles = ((M + BM * c.cta - 1) / (BM * c.cta)) * ((N + c.bn - 1) / c.bn);
+        const int64_t slots = sms / c.cta;
+        const int64_t waves = (tiles + slots - 1) / slots;
+        const double mma = 4.0 * BM * c.bn / 256.0;
+        const double l2 = (BM + c.bn / c.cta) * 128.0 / 64.0;
+        const double cost = static_cast<double>(waves) * std::max(mma, l2);
         if (cost < best_cost - 1e-9) {
             best_cost = cost;
-            best = bn;
+            best = c;
         }
     }
     return best;
@@ -510,16 +590,25 @@ int pick_bn(int64_t M, int64_t N) {
 template <bool kI8>
 int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st,
              int force_bn) {
-    // Accumulating FP32 outputs (wgrad into main_grad) use split-K to fill the
-    // chip, so they take the widest tile (fewest L2 bytes per FLOP).
     const bool splitk_ok = !kI8 && p.accumulate && p.c_dtype == QSYNC_F32 && g_splitk_wide;
-    const int bn = force_bn ? force_bn : (splitk_ok ? 256 : pick_bn(p.M, p.N));
-    p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, bn);
-    switch (bn) {
-        case 256: return launch<kI8, 256>(a, b, dt, p, st);
-        case 128: return launch<kI8, 128>(a, b, dt, p, st);
-        case 64: return launch<kI8, 64>(a, b, dt, p, st);
-        default: return set_error(QSYNC_ERR_DOMAIN, "unsupported tile N " + std::to_string(bn));
+    Shape sh = pick_shape(p.M, p.N, g_force_cta != 1);
+    if (splitk_ok) sh.bn = 256;
+    if (force_bn) sh.bn = force_bn;
+    if (g_force_cta) sh.cta = g_force_cta;
+    if (sh.cta == 2 && sh.bn == 64) sh.cta = 1;  // pair tiles need BN/2 >= 64 rows of B
+    p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta);
+    if (sh.cta == 2) {
+        switch (sh.bn) {
+            case 256: return launch<kI8, 256, 2>(a, b, dt, p, st);
+            case 128: return launch<kI8, 128, 2>(a, b, dt, p, st);
+            default: break;
+        }
+    }
+    switch (sh.bn) {
+        case 256: return launch<kI8, 256, 1>(a, b, dt, p, st);
+        case 128: return launch<kI8, 128, 1>(a, b, dt, p, st);
+        case 64: return launch<kI8, 64, 1>(a, b, dt, p, st);
+        default: return set_error(QSYNC_ERR_DOMAIN, "unsupported tile N " + std::to_string(sh.bn));
     }
 }
 
@@ -548,6 +637,12 @@ extern "C" {
 int qsync_gemm_force_splitk(int ks) {
     QSB_REQUIRE(ks >= 0 && ks <= 64, QSYNC_ERR_DOMAIN, "split-K override must be in [0, 64]");
     g_force_splitk = ks;
+    return QSYNC_OK;
+}
+
+int qsync_gemm_force_cta(int cta) {
+    QSB_REQUIRE(cta >= 0 && cta <= 2, QSYNC_ERR_DOMAIN, "CTA override must be 0, 1 or 2");
+    g_force_cta = cta;
     return QSYNC_OK;
 }
 

@@ -382,35 +382,43 @@ __global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w,
 __global__ void __launch_bounds__(kThreads) k_dequant(const int8_t* __restrict__ q, int64_t n,
                                                       const float* __restrict__ scale,
                                                       float* __restrict__ out, int vec_ok) {
+    // Thread i owns output float4 i (4 int8 in, 16 B out): every store
+    // instruction writes 512 contiguous bytes per warp, so no partial sectors
+    // are written (partial-sector writes made L2 fetch lines from DRAM).
     const float s = *scale;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t done = 0;
     if (vec_ok) {
-        const int64_t n16 = n / 16;
-        const uint4* qv = reinterpret_cast<const uint4*>(q);
+        const int64_t n4 = n / 4;
+        const uint32_t* qv = reinterpret_cast<const uint32_t*>(q);
         float4* ov = reinterpret_cast<float4*>(out);
-        auto emit = [&](uint4 r, int64_t i) {
-            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float4 f;
-                f.x = static_cast<float>(static_cast<int8_t>(w[j] & 0xff)) * s;
-                f.y = static_cast<float>(static_cast<int8_t>((w[j] >> 8) & 0xff)) * s;
-                f.z = static_cast<float>(static_cast<int8_t>((w[j] >> 16) & 0xff)) * s;
-                f.w = static_cast<float>(static_cast<int8_t>(w[j] >> 24)) * s;
-                __stcs(ov + i * 4 + j, f);
-            }
-        };
+        constexpr int U = 4;
         int64_t i = tid;
-        for (; i + stride < n16; i += 2 * stride) {
-            const uint4 r0 = ld_stream(qv + i);
-            const uint4 r1 = ld_stream(qv + i + stride);
-            emit(r0, i);
-            emit(r1, i + stride);
+        for (; i + (U - 1) * stride < n4; i += U * stride) {
+            uint32_t w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) w[u] = __ldcs(qv + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float4 f;
+                f.x = static_cast<float>(static_cast<int8_t>(w[u] & 0xff)) * s;
+                f.y = static_cast<float>(static_cast<int8_t>((w[u] >> 8) & 0xff)) * s;
+                f.z = static_cast<float>(static_cast<int8_t>((w[u] >> 16) & 0xff)) * s;
+                f.w = static_cast<float>(static_cast<int8_t>(w[u] >> 24)) * s;
+                __stcs(ov + i + u * stride, f);
+            }
         }
-        for (; i < n16; i += stride) emit(ld_stream(qv + i), i);
-        done = n16 * 16;
+        for (; i < n4; i += stride) {
+            const uint32_t w = __ldcs(qv + i);
+            float4 f;
+            f.x = static_cast<float>(static_cast<int8_t>(w & 0xff)) * s;
+            f.y = static_cast<float>(static_cast<int8_t>((w >> 8) & 0xff)) * s;
+            f.z = static_cast<float>(static_cast<int8_t>((w >> 16) & 0xff)) * s;
+            f.w = static_cast<float>(static_cast<int8_t>(w >> 24)) * s;
+            __stcs(ov + i, f);
+        }
+        done = n4 * 4;
     }
     for (int64_t i = done + tid; i < n; i += stride) out[i] = static_cast<float>(q[i]) * s;
 }

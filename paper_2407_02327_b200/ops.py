@@ -291,6 +291,11 @@ def force_splitk(ks: int) -> None:
     call("qsync_gemm_force_splitk", int(ks))
 
 
+def force_cta(cta: int) -> None:
+    """Test hook: 1 = single-CTA tiles, 2 = CTA-pair (cta_group::2) tiles, 0 = cost model."""
+    call("qsync_gemm_force_cta", int(cta))
+
+
 def force_tile_n(bn: int) -> None:
     """Test hook: pin the GEMM tile N (0 = heuristic)."""
     call("qsync_gemm_force_tile_n", int(bn))

@@ -220,18 +220,22 @@ GEMM_SHAPES = [(128, 256, 128), (64, 1024, 1024), (200, 300, 64), (1, 16, 16), (
                (257, 129, 3072), (512, 2304, 768)]
 
 
-@pytest.mark.parametrize("bn", [0, 64, 128, 256])
+@pytest.mark.parametrize("cta_bn", [(1, 0), (1, 64), (1, 128), (1, 256), (2, 128), (2, 256), (0, 0)])
 @pytest.mark.parametrize("mnk", GEMM_SHAPES)
-def test_gemm_s8_int32_bit_exact(mnk, bn, cpuref):
+def test_gemm_s8_int32_bit_exact(mnk, cta_bn, cpuref):
+    """int32 accumulators bit-exact for single-CTA tiles and CTA-pair (cta_group::2) tiles."""
+    cta, bn = cta_bn
     M, N, K = mnk
     rng = np.random.default_rng(M * 7 + N + K)
     a = rng.integers(-127, 128, size=(M, K), dtype=np.int8)
     b = rng.integers(-127, 128, size=(N, K), dtype=np.int8)
     ops.force_tile_n(bn)
+    ops.force_cta(cta)
     try:
         ci, _ = ops.gemm_s8(_t(a), _t(b), out_i32=True, out_f32=False)
     finally:
         ops.force_tile_n(0)
+        ops.force_cta(0)
     assert np.array_equal(_np(ci), cpuref.gemm_s8_tn(a, b))
 
 
@@ -259,11 +263,20 @@ def test_gemm_s8_rejects_bad_k():
     assert e.value.kind == "domain"
 
 
+@pytest.mark.parametrize("cta", [1, 2])
 @pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("mnk", [(128, 128, 64), (64, 1024, 1024), (333, 200, 72),
                                  (4096, 768, 3072), (768, 3072, 4096)])
-def test_gemm_f16_within_tolerance(mnk, dt, cpuref):
+def test_gemm_f16_within_tolerance(mnk, dt, cta, cpuref):
     M, N, K = mnk
+    ops.force_cta(cta)
+    try:
+        _check_f16(M, N, K, dt)
+    finally:
+        ops.force_cta(0)
+
+
+def _check_f16(M, N, K, dt):
     rng = np.random.default_rng(M + N + K)
     a = torch.from_numpy(rng.normal(size=(M, K)).astype(np.float32)).to(dt)
     b = torch.from_numpy(rng.normal(size=(N, K)).astype(np.float32)).to(dt)
