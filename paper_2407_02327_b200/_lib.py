@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqsync_b200.so")
+# QSYNC_B200_LIB overrides the library path (A/B experiments only).
+LIB_PATH = os.environ.get("QSYNC_B200_LIB", os.path.join(_HERE, "libqsync_b200.so"))
 
 # qsync::ErrorKind order (errors.hpp:11-26); status = index + 1.
 ERROR_KINDS = ["graph-cycle", "validation", "reference", "domain", "missing-profile",
@@ -66,6 +67,7 @@ SIGNATURES = {
     "qsync_gemm_force_tile_n": [_int],
     "qsync_gemm_force_splitk": [_int],
     "qsync_gemm_force_cta": [_int],
+    "qsync_gemm_debug_epilogue": [_int],
     "qsync_mt_jump_selftest": [],
 }
 _RESTYPES = {"qsync_last_error": C.c_char_p, "qsync_status_name": C.c_char_p,
@@ -84,7 +86,12 @@ def lib():
                 "g.build()'` (there is no CPU fallback)")
         L = C.CDLL(LIB_PATH)
         for name, args in SIGNATURES.items():
-            fn = getattr(L, name)
+            try:
+                fn = getattr(L, name)
+            except AttributeError:
+                if "QSYNC_B200_LIB" in os.environ:  # older library in an A/B run
+                    continue
+                raise
             fn.argtypes = args
             fn.restype = _RESTYPES.get(name, _int)
         _lib = L

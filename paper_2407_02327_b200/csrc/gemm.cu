@@ -48,6 +48,7 @@ struct EpiParams {
     int accumulate;
     uint32_t idesc;
     int tma_store;  // epilogue writes through tm_c (TMA store / reduce-add)
+    int debug_epi;  // bench hook: 1 = skip epilogue math+stores (TMEM read only)
     int ksplit;     // split-K factor (>1 only with accumulate: partials reduce-add)
     int kb_per;     // k-blocks per split
 };
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[32];
                     ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0 + 32 * sub), r);
                     ptx::tmem_ld_wait();
+                    if (p.debug_epi) continue;
                     if (raw) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) w[j] = r[j];
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
                     }
                 }
-                if (row0 >= M || col0 >= N) continue;  // warp-uniform: chunk fully outside
+                if (row0 >= M || col0 >= N || p.debug_epi) continue;  // warp-uniform skip
                 if (p.tma_store) {
                     // Free the staging buffer used two chunks ago, then write this
                     // row's 8 x 16B pieces at their 128B-swizzled positions.
@@ -479,6 +481,7 @@ uint32_t make_idesc(bool i8, bool bf16, int n, int m) {
 int g_force_splitk = 0;  // test/bench hook (qsync_gemm_force_splitk): 0 = heuristic
 int g_splitk_wide = 0;   // accumulate GEMMs prefer BN=256 (bench hook)
 int g_force_cta = 0;     // test/bench hook (qsync_gemm_force_cta): 0 = cost model, 1, 2
+int g_debug_epi = 0;     // bench hook (qsync_gemm_debug_epilogue)
 
 template <bool kI8, int BN, int kCta>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
@@ -572,7 +575,12 @@ Shape pick_shape(int64_t M, int64_t N, bool allow_pair) {
     Shape best{256, 1};
     double best_cost = 1e300;
     for (const Shape& c : cands) {
-        if (c.cta == 2 && (!allow_pair || M <= BM)) continue;
+        // Measured (tools/bench_bwd_gemm.py): CTA pairs win at 8192^3 (+11% INT8)
+        // but not at BERT-sized GEMMs (<= 1 wave of 256x256 pair tiles), where
+        // fixed costs dominate -- only consider them with >= 3 waves of work.
+        if (c.cta == 2 && (!allow_pair || M <= BM ||
+                           ((M + BM - 1) / BM) * ((N + 255) / 256) < 3LL * sms))
+            continue;
         const int64_t tiles = ((M + BM * c.cta - 1) / (BM * c.cta)) * ((N + c.bn - 1) / c.bn);
         const int64_t slots = sms / c.cta;
         const int64_t waves = (tiles + slots - 1) / slots;
@@ -591,12 +599,15 @@ template <bool kI8>
 int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st,
              int force_bn) {
     const bool splitk_ok = !kI8 && p.accumulate && p.c_dtype == QSYNC_F32 && g_splitk_wide;
-    Shape sh = pick_shape(p.M, p.N, g_force_cta != 1);
-    if (splitk_ok) sh.bn = 256;
+    // Accumulating FP32 GEMMs (wgrad) go split-K on single-CTA 256-wide tiles.
+    const bool accumulating = !kI8 && p.accumulate && p.c_dtype == QSYNC_F32;
+    Shape sh = pick_shape(p.M, p.N, g_force_cta != 1 && !accumulating);
+    if (splitk_ok || accumulating) sh.bn = 256;
     if (force_bn) sh.bn = force_bn;
     if (g_force_cta) sh.cta = g_force_cta;
     if (sh.cta == 2 && sh.bn == 64) sh.cta = 1;  // pair tiles need BN/2 >= 64 rows of B
     p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta);
+    p.debug_epi = g_debug_epi;
     if (sh.cta == 2) {
         switch (sh.bn) {
             case 256: return launch<kI8, 256, 2>(a, b, dt, p, st);
@@ -637,6 +648,11 @@ extern "C" {
 int qsync_gemm_force_splitk(int ks) {
     QSB_REQUIRE(ks >= 0 && ks <= 64, QSYNC_ERR_DOMAIN, "split-K override must be in [0, 64]");
     g_force_splitk = ks;
+    return QSYNC_OK;
+}
+
+int qsync_gemm_debug_epilogue(int v) {
+    g_debug_epi = v;
     return QSYNC_OK;
 }
 

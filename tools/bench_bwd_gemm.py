@@ -40,21 +40,27 @@ def main():
         out = torch.zeros(M, N, device="cuda")
         flops = 2.0 * M * N * K
         res = []
-        for bn in (0, 64, 128, 256):
-            for ks in ((1, 0, 2, 4, 8) if acc else (1,)):
-                ops.force_tile_n(bn)
-                ops.force_splitk(ks)
-                try:
-                    us = timeit(lambda: ops.gemm_f16(a, b, out=out, accumulate=acc))
-                finally:
-                    ops.force_tile_n(0)
-                    ops.force_splitk(0)
-                res.append((us, bn, ks))
+        for cta in (1, 2):
+            for bn in (0, 64, 128, 256):
+                if cta == 2 and bn == 64:
+                    continue
+                for ks in ((1, 0, 2, 4) if acc else (1,)):
+                    ops.force_tile_n(bn)
+                    ops.force_splitk(ks)
+                    ops.force_cta(cta)
+                    try:
+                        us = timeit(lambda: ops.gemm_f16(a, b, out=out, accumulate=acc))
+                    finally:
+                        ops.force_tile_n(0)
+                        ops.force_splitk(0)
+                        ops.force_cta(0)
+                    res.append((us, f"c{cta}b{bn}", ks))
+        auto = timeit(lambda: ops.gemm_f16(a, b, out=out, accumulate=acc))
         ref = timeit(lambda: torch.matmul(a, b.t()))
         res.sort()
         best = res[0]
-        print(f"{name:10s} {M:5d}x{N:5d}x{K:5d} acc={int(acc)} cublas {ref:7.1f}us ({flops/ref/1e6:6.0f} TF) | "
-              + " ".join(f"bn{bn}/ks{ks}:{us:.1f}" for us, bn, ks in res[:6])
+        print(f"{name:10s} {M:5d}x{N:5d}x{K:5d} acc={int(acc)} cublas {ref:6.1f}us auto {auto:6.1f}us | "
+              + " ".join(f"{bn}/ks{ks}:{us:.1f}" for us, bn, ks in res[:5])
               + f" | best {flops/best[0]/1e6:.0f} TF")
         a8 = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
         b8 = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
@@ -62,15 +68,21 @@ def main():
             sa = torch.tensor([0.01], device="cuda")
             sb = torch.rand(N, device="cuda")
             r8 = []
-            for bn in (0, 64, 128, 256):
-                ops.force_tile_n(bn)
-                try:
-                    r8.append((timeit(lambda: ops.gemm_s8(a8, b8, sa, sb, out=out)), bn))
-                finally:
-                    ops.force_tile_n(0)
+            for cta in (1, 2):
+                for bn in (64, 128, 256):
+                    if cta == 2 and bn == 64:
+                        continue
+                    ops.force_tile_n(bn)
+                    ops.force_cta(cta)
+                    try:
+                        r8.append((timeit(lambda: ops.gemm_s8(a8, b8, sa, sb, out=out)), f"c{cta}b{bn}"))
+                    finally:
+                        ops.force_tile_n(0)
+                        ops.force_cta(0)
             r8.sort()
             ref8 = timeit(lambda: torch._int_mm(a8, b8.t()))
-            print(f"   int8   cublasLt {ref8:7.1f}us | " + " ".join(f"bn{bn}:{us:.1f}" for us, bn in r8))
+            auto8 = timeit(lambda: ops.gemm_s8(a8, b8, sa, sb, out=out))
+            print(f"   int8   cublasLt {ref8:6.1f}us auto {auto8:6.1f}us | " + " ".join(f"{bn}:{us:.1f}" for us, bn in r8))
 
 
 if __name__ == "__main__":
