@@ -78,13 +78,15 @@ int qsync_absmax_rows(const void* x, int dtype, int64_t rows, int64_t cols, floa
  * q = sat(rint(x / s)), s derived from absmax as above, FP32 IEEE division.
  * ------------------------------------------------------------------------- */
 /* Per-tensor: absmax + scale + quantize of a [rows, cols] matrix.  `scale` is a
- * device float[2]: scale[0] receives s, scale[1] the absmax.  If q_t_f16 != NULL the same quantized values are
- * also written transposed as FP16 integers, [cols, rows] with row pitch ld_t
+ * device float[2]: scale[0] receives s, scale[1] the absmax.  If q_t != NULL the
+ * same quantized values are also written transposed, as q_t_dtype QSYNC_I8 (the
+ * 1-byte activation an INT8 op keeps for backward) or QSYNC_F16 integers,
+ * [cols, rows] with row pitch ld_t
  * (>= rows, 0 = rows; pad columns untouched) -- the saved activation operand of
  * the FP16 wgrad GEMM (cost_mapper.cpp:13-15), whose K (= rows) must be padded
  * to a multiple of 8 for TMA. */
 int qsync_quantize_per_tensor(const void* x, int dtype, int64_t rows, int64_t cols, int8_t* q,
-                              float* scale, uint16_t* q_t_f16, int64_t ld_t,
+                              float* scale, void* q_t, int q_t_dtype, int64_t ld_t,
                               qsync_stream_t stream);
 /* Quantize with a scale already on the device (e.g. delayed / shared scale). */
 int qsync_quantize_with_scale(const void* x, int dtype, int64_t n, const float* scale, int8_t* q,
@@ -125,7 +127,8 @@ int qsync_dequantize_per_channel(const int8_t* q, int64_t rows, int64_t cols, co
                                  float* out, qsync_stream_t stream);
 
 /* ---------------------------------------------------------------------------
- * K4  float casts (CastScheme::FloatToFloat, profile.hpp:19).  RNE.
+ * K4  float casts (CastScheme::FloatToFloat, profile.hpp:19).  RNE.  Also
+ * I8 -> F16/F32 (exact): the FP16 backward's view of a saved INT8 activation.
  * ------------------------------------------------------------------------- */
 int qsync_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64_t n,
                qsync_stream_t stream);

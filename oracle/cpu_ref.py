@@ -248,6 +248,11 @@ class RefLib:
         L.qref_reduce_stats.argtypes = [_p, _p, C.c_int, C.c_int, _p, _p]
         L.qref_score_bundle.argtypes = [C.c_char_p, C.c_int, _i64, C.c_int, C.c_char_p, _i64]
         L.qref_score_bundle.restype = _i64
+        L.qref_plan_bundle.argtypes = [C.c_char_p, C.c_int, _i64, C.c_int, C.c_char_p, _i64,
+                                       C.c_int, C.c_char_p, _i64]
+        L.qref_plan_bundle.restype = _i64
+        L.qref_replay_bundle.argtypes = [C.c_char_p, C.c_char_p]
+        L.qref_replay_bundle.restype = _i64
 
     def _err(self, rc):
         if rc:
@@ -297,6 +302,25 @@ class RefLib:
         om = np.zeros(1, np.uint32)
         self._err(self.L.qref_reduce_stats(_ptr(v), _ptr(m), len(m), window, _ptr(out), _ptr(om)))
         return out, int(om[0])
+
+    def plan_bundle(self, path, loss_kind=0, loss_n=1, window=50, cap_device="", cap_bytes=0,
+                    b_max=8) -> dict:
+        """The reference planner (cli.cpp:116-136) on a bundle: the solve_report JSON."""
+        import json as _json
+        buf = C.create_string_buffer(8 << 20)
+        n = self.L.qref_plan_bundle(path.encode(), loss_kind, loss_n, window, cap_device.encode(),
+                                    cap_bytes, b_max, buf, 8 << 20)
+        if n < 0:
+            raise RuntimeError(self.L.qref_last_error().decode())
+        return _json.loads(buf.raw[:n].decode())
+
+    def replay_bundle(self, path, plan: dict) -> int:
+        """The reference replayer's makespan (ns) for a plan (cli.cpp:90-114)."""
+        import json as _json
+        n = self.L.qref_replay_bundle(path.encode(), _json.dumps(plan).encode())
+        if n < 0:
+            raise RuntimeError(self.L.qref_last_error().decode())
+        return int(n)
 
     def score_bundle(self, path, loss_kind, loss_n, window=50):
         buf = C.create_string_buffer(1 << 20)

@@ -16,7 +16,10 @@
 #include <string>
 #include <vector>
 
+#include "qsync/allocator.hpp"
+#include "qsync/graph.hpp"
 #include "qsync/indicator.hpp"
+#include "qsync/replayer.hpp"
 #include "qsync/profile.hpp"
 #include "qsync/rng.hpp"
 
@@ -158,6 +161,47 @@ int64_t qref_score_bundle(const char* path, int loss_kind, int64_t loss_n, int w
         if (static_cast<int64_t>(out.size()) > cap) return -100;
         std::memcpy(buf, out.data(), out.size());
         return static_cast<int64_t>(out.size());
+    } catch (const Error& e) {
+        g_err = e.what();
+        return -code_of(e);
+    }
+}
+
+// The reference's `plan` subcommand (cli.cpp:116-136) on a bundle file: writes
+// the solve_report JSON (allocator.cpp:404-437) into buf.  cap_device/cap_bytes
+// give one inference device's memory cap.  Returns bytes written or -code.
+int64_t qref_plan_bundle(const char* path, int loss_kind, int64_t loss_n, int window,
+                         const char* cap_device, int64_t cap_bytes, int b_max, char* buf,
+                         int64_t cap) {
+    try {
+        const ProfileBundle bundle = load_profile(path);
+        const TensorStats stats =
+            bundle.tensor_stats.empty() ? TensorStats{} : bundle.reduced_stats(window);
+        AllocProblem problem;
+        problem.bundle = &bundle;
+        problem.loss = LossSpec{static_cast<LossKind>(loss_kind), loss_n};
+        problem.scores = score_all(bundle.graph, stats, problem.loss);
+        if (cap_device && cap_device[0]) problem.mem_caps[cap_device] = cap_bytes;
+        problem.b_max = b_max;
+        const SolveResult result = solve(problem);
+        const std::string out = solve_report(result).dump();
+        if (static_cast<int64_t>(out.size()) > cap) return -100;
+        std::memcpy(buf, out.data(), out.size());
+        return static_cast<int64_t>(out.size());
+    } catch (const Error& e) {
+        g_err = e.what();
+        return -code_of(e);
+    }
+}
+
+// The reference's `replay` (cli.cpp:90-114): simulate one iteration of the
+// bundle under a plan JSON ({"per_device": ...}); returns makespan ns or -code.
+int64_t qref_replay_bundle(const char* path, const char* plan_json) {
+    try {
+        const ProfileBundle bundle = load_profile(path);
+        const PrecisionPlan plan = plan_from_json(nlohmann::json::parse(plan_json));
+        const Timeline t = simulate(build_global_dfg(bundle, plan).global);
+        return t.makespan_ns;
     } catch (const Error& e) {
         g_err = e.what();
         return -code_of(e);

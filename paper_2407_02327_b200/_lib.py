@@ -46,7 +46,7 @@ SIGNATURES = {
     "qsync_launch_count": [],
     "qsync_absmax": [_p, _int, _i64, _p, _p],
     "qsync_absmax_rows": [_p, _int, _i64, _i64, _p, _p],
-    "qsync_quantize_per_tensor": [_p, _int, _i64, _i64, _p, _p, _p, _i64, _p],
+    "qsync_quantize_per_tensor": [_p, _int, _i64, _i64, _p, _p, _p, _int, _i64, _p],
     "qsync_quantize_with_scale": [_p, _int, _i64, _p, _p, _p],
     "qsync_quantize_per_channel": [_p, _i64, _i64, _p, _p, _p, _p],
     "qsync_stochastic_round_f64": [_p, _i64, _f64, _f64, _u64, _p, _p, _p],

@@ -57,6 +57,12 @@ struct Elem<QSYNC_BF16> {
     __device__ static float f(T v) { return __bfloat162float(v); }
 };
 
+template <>
+struct Elem<QSYNC_I8> {
+    using T = int8_t;
+    __device__ static float f(T v) { return static_cast<float>(v); }
+};
+
 // Scale rule shared by every quantizer: s = absmax / 127 (IEEE), 1 if all-zero.
 __device__ __forceinline__ float scale_from_absmax(float a) {
     return a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;

@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __rest
                                               int8_t* __restrict__ q, uint16_t* __restrict__ out,
                                               uint16_t* __restrict__ out_t, int64_t ld_t,
                                               float* __restrict__ colsum,
-                                              float* __restrict__ scale_out, int vec_ok) {
+                                              float* __restrict__ scale_out, int vec_ok,
+                                              int8_t* __restrict__ out_t8 = nullptr) {
     __shared__ __align__(16) __half tile[TC][TR + 8];  // [col][row], 16B-aligned rows
     __shared__ float csum[16][TC + 1];
     const int tid = threadIdx.x;
@@ -323,6 +324,32 @@ __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __rest
             } else {
                 for (int i = 0; i < 8 && orow + i < rows; ++i)
                     out_t[oc * ld_t + orow + i] = __half_as_ushort(tile[cc][rg + i]);
+            }
+        }
+    }
+    if (MODE == 0 && out_t8) {
+        // INT8 transpose (the saved activation of an INT8 op, 1 byte/element):
+        // 8 rows as one 8-byte store.
+        const bool vec_t = vec_ok && (ld_t % 8 == 0);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int idx = tid + 256 * k;
+            const int cc = idx >> 3;
+            const int rg = (idx & 7) * 8;
+            const int64_t oc = c0 + cc;
+            const int64_t orow = r0 + rg;
+            if (oc >= cols || orow >= rows) continue;
+            if (vec_t && orow + 8 <= rows) {
+                uint32_t lo = 0, hi = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    lo |= static_cast<uint32_t>(static_cast<uint8_t>(__half2int_rn(tile[cc][rg + i]))) << (8 * i);
+                    hi |= static_cast<uint32_t>(static_cast<uint8_t>(__half2int_rn(tile[cc][rg + 4 + i]))) << (8 * i);
+                }
+                *reinterpret_cast<uint2*>(out_t8 + oc * ld_t + orow) = make_uint2(lo, hi);
+            } else {
+                for (int i = 0; i < 8 && orow + i < rows; ++i)
+                    out_t8[oc * ld_t + orow + i] = static_cast<int8_t>(__half2int_rn(tile[cc][rg + i]));
             }
         }
     }
@@ -459,7 +486,14 @@ struct Store<SD, QSYNC_BF16> {
 template <int SD>
 __device__ __forceinline__ void load8(const typename Elem<SD>::T* x, int64_t i, float* f) {
     const uint4* v = reinterpret_cast<const uint4*>(x + i);
-    if (SD == QSYNC_F32) {
+    if constexpr (SD == QSYNC_I8) {
+        const uint2 w = *reinterpret_cast<const uint2*>(x + i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            f[k] = static_cast<float>(static_cast<int8_t>((w.x >> (8 * k)) & 0xff));
+            f[4 + k] = static_cast<float>(static_cast<int8_t>((w.y >> (8 * k)) & 0xff));
+        }
+    } else if constexpr (SD == QSYNC_F32) {
         Vec<QSYNC_F32>::unpack(ld_stream(v), f);
         Vec<QSYNC_F32>::unpack(ld_stream(v + 1), f + 4);
     } else {
@@ -639,15 +673,18 @@ template <int DT>
 struct QuantRun {
     // scale[0] <- s, scale[1] <- absmax (scratch + output).
     static int run(const void* x, int64_t rows, int64_t cols, int8_t* q, float* scale,
-                   uint16_t* q_t, int64_t ld_t, cudaStream_t st) {
+                   void* q_t, int q_t_dtype, int64_t ld_t, cudaStream_t st) {
         using T = typename Elem<DT>::T;
         const int64_t n = rows * cols;
         QSB_TRY(AbsmaxRun<DT>::run(x, n, scale + 1, st));
         if (q_t && n > 0) {
             dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
             const int vt = (cols % 4 == 0) && aligned16(x) && aligned16(q) && aligned16(q_t);
+            const bool t8 = q_t_dtype == QSYNC_I8;
             k_tile<DT, 0><<<grid, 256, 0, st>>>(static_cast<const T*>(x), rows, cols, scale + 1, q,
-                                                nullptr, q_t, ld_t, nullptr, scale, vt);
+                                                nullptr, t8 ? nullptr : static_cast<uint16_t*>(q_t),
+                                                ld_t, nullptr, scale, vt,
+                                                t8 ? static_cast<int8_t*>(q_t) : nullptr);
             return check_launch("k_tile<quant>");
         }
         const int vec = aligned16(x) && aligned16(q);
@@ -722,13 +759,16 @@ int qsync_absmax_rows(const void* x, int dtype, int64_t rows, int64_t cols, floa
 }
 
 int qsync_quantize_per_tensor(const void* x, int dtype, int64_t rows, int64_t cols, int8_t* q,
-                              float* scale, uint16_t* q_t_f16, int64_t ld_t,
+                              float* scale, void* q_t, int q_t_dtype, int64_t ld_t,
                               qsync_stream_t stream) {
     QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
     QSB_REQUIRE(scale != nullptr, QSYNC_ERR_VALIDATION, "scale buffer (float[2]) is required");
+    QSB_REQUIRE(!q_t || q_t_dtype == QSYNC_F16 || q_t_dtype == QSYNC_I8, QSYNC_ERR_DOMAIN,
+                "transposed copy must be F16 or I8");
     if (ld_t <= 0) ld_t = rows;
     QSB_REQUIRE(ld_t >= rows, QSYNC_ERR_DOMAIN, "transposed pitch must be >= rows");
-    return dispatch_dtype<QuantRun>(dtype, x, rows, cols, q, scale, q_t_f16, ld_t, to_stream(stream));
+    return dispatch_dtype<QuantRun>(dtype, x, rows, cols, q, scale, q_t, q_t_dtype, ld_t,
+                                    to_stream(stream));
 }
 
 int qsync_quantize_with_scale(const void* x, int dtype, int64_t n, const float* scale, int8_t* q,
@@ -786,6 +826,8 @@ int qsync_cast(const void* x, int src, void* out, int dst, int64_t n, qsync_stre
     QSB_CAST(QSYNC_BF16, QSYNC_F32)
     QSB_CAST(QSYNC_F16, QSYNC_BF16)
     QSB_CAST(QSYNC_BF16, QSYNC_F16)
+    QSB_CAST(QSYNC_I8, QSYNC_F16)
+    QSB_CAST(QSYNC_I8, QSYNC_F32)
 #undef QSB_CAST
     return set_error(QSYNC_ERR_DOMAIN, "unsupported cast " + std::to_string(src) + "->" + std::to_string(dst));
 }

@@ -15,6 +15,7 @@ from . import _lib
 from ._lib import BF16, F16, F32, QsyncError, call
 
 _DT = {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}
+_DT_CAST = {**_DT, torch.int8: _lib.I8}
 
 
 def _stream() -> int:
@@ -58,27 +59,33 @@ def pad8(n: int) -> int:
     return (n + 7) // 8 * 8
 
 
-def _transposed(cols: int, rows: int, device) -> torch.Tensor:
+def _transposed(cols: int, rows: int, device, dtype=torch.float16) -> torch.Tensor:
     ld = pad8(rows)
     if ld == rows:
-        return torch.empty((cols, ld), device=device, dtype=torch.float16)
-    return torch.zeros((cols, ld), device=device, dtype=torch.float16)
+        return torch.empty((cols, ld), device=device, dtype=dtype)
+    return torch.zeros((cols, ld), device=device, dtype=dtype)
 
 
-def quantize_per_tensor(x: torch.Tensor, transposed_f16: bool = False, out=None):
+def quantize_per_tensor(x: torch.Tensor, transposed_f16: bool = False, out=None,
+                        transposed_i8: bool = False):
     """Per-tensor RNE INT8 quantization of a 2-D (or flattened) tensor.
 
-    Returns (q int8 same shape, scale float32[2] = {s, absmax}, q_t f16 [cols, pad8(rows)] or
-    None).
+    Returns (q int8 same shape, scale float32[2] = {s, absmax}, q_t [cols, pad8(rows)] or None):
+    q_t is FP16 with ``transposed_f16``, INT8 with ``transposed_i8``.
     """
     _req(x, "x", _DT)
     rows = x.shape[0] if x.dim() >= 2 else 1
     cols = x.numel() // max(rows, 1)
     q = out if out is not None else torch.empty(x.shape, device=x.device, dtype=torch.int8)
     scale = torch.empty(2, device=x.device, dtype=torch.float32)
-    qt = _transposed(cols, rows, x.device) if transposed_f16 else None
+    qt = None
+    if transposed_i8:
+        qt = _transposed(cols, rows, x.device, torch.int8)
+    elif transposed_f16:
+        qt = _transposed(cols, rows, x.device)
     call("qsync_quantize_per_tensor", _ptr(x), _DT[x.dtype], rows, cols, _ptr(q), _ptr(scale),
-         _ptr(qt), qt.shape[1] if qt is not None else 0, _stream())
+         _ptr(qt), _lib.I8 if transposed_i8 else F16, qt.shape[1] if qt is not None else 0,
+         _stream())
     return q, scale, qt
 
 
@@ -152,9 +159,9 @@ def dequantize_per_channel(q: torch.Tensor, scales: torch.Tensor) -> torch.Tenso
 
 # --------------------------------------------------------------------------- K4
 def cast(x: torch.Tensor, dtype: torch.dtype, out=None) -> torch.Tensor:
-    _req(x, "x", _DT)
+    _req(x, "x", _DT_CAST)
     o = out if out is not None else torch.empty(x.shape, device=x.device, dtype=dtype)
-    call("qsync_cast", _ptr(x), _DT[x.dtype], _ptr(o), _DT[dtype], x.numel(), _stream())
+    call("qsync_cast", _ptr(x), _DT_CAST[x.dtype], _ptr(o), _DT[dtype], x.numel(), _stream())
     return o
 
 

@@ -1,0 +1,328 @@
+"""Profiler: measure the hot path on the B200 and emit a QSync ProfileBundle.
+
+The reference planner consumes measured costs (README "Profile bundle
+schema"); this module produces them from this package's kernels, in the exact
+schema `bundle_from_json` validates (profile.cpp:283-413):
+
+* ``graph``        -- the BERT-base operator DAG: adjustable Linears (INT8/FP16/FP32),
+                      dependent GELU, fixed embeddings / attention core / LayerNorm /
+                      loss; residual edges included (depth = longest path, graph.cpp:178-183).
+* ``op_costs``     -- per (op, precision): ``pure_cost_ns`` = measured fwd + bwd time of
+                      the op's kernels on the device (CUDA events), ``fwd_fraction``
+                      measured, ``memory_bytes`` = the bytes that precision keeps
+                      resident (weights, low-precision copies, saved operands, output).
+* ``cast_samples`` -- measured K2/K3/K4 latencies over tensor sizes for every key
+                      ``required_cast_keys`` asks for (quantize includes the absmax pass).
+* ``tensor_stats`` -- per training step, per adjustable op, the K5 device statistics of
+                      the input activation, weight and incoming gradient (OpStats fields).
+* ``devices``      -- the DP ranks (a training device + a memory-capped inference device).
+
+The reference's ``plan`` (cli.cpp:116-136) then turns the bundle into per-rank plans
+that ``train_step.load_plan`` applies.
+"""
+from __future__ import annotations
+
+import json
+import statistics
+
+import torch
+import torch.nn.functional as F
+
+from . import ops, qlinear
+from .qlinear import FP16, FP32, INT8, QLinear
+from .train_step import BertConfig, BertEncoderStack
+
+_PREC_BYTES = {INT8: 1, FP16: 2, FP32: 4}
+
+
+# ----------------------------------------------------------------------------- timing
+def _time_ns(fn, reps: int = 10) -> int:
+    """Median device time of fn() (CUDA events; a device spin keeps launches queued)."""
+    fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(reps):
+        torch.cuda._sleep(2_000_000)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e) * 1e6)
+    return max(1, int(statistics.median(times)))
+
+
+# ----------------------------------------------------------------------------- graph
+def bert_graph(cfg: BertConfig, batch: int) -> dict:
+    T, H, Fh = batch * cfg.seq, cfg.hidden, cfg.ffn
+    nodes, edges = [], []
+
+    def node(i, kind, out, sub, prec, w=0):
+        nodes.append({"id": i, "kind": kind, "output_numel": out, "subgraph_id": sub,
+                      "supported_precisions": prec, "has_weight": w > 0, "weight_numel": w})
+
+    all3 = [INT8, FP16, FP32]
+    node("embed", "fixed", T * H, "embed", [FP32])
+    prev = "embed"
+    for i in range(cfg.layers):
+        L = f"layer{i}"
+        node(f"{L}.qkv", "adjustable", T * 3 * H, L, all3, 3 * H * H)
+        node(f"{L}.attn", "fixed", T * H, L, [FP32])
+        node(f"{L}.o", "adjustable", T * H, L, all3, H * H)
+        node(f"{L}.ln1", "fixed", T * H, L, [FP32])
+        node(f"{L}.ff1", "adjustable", T * Fh, L, all3, Fh * H)
+        node(f"{L}.gelu", "dependent", T * Fh, L, [FP16, FP32])
+        node(f"{L}.ff2", "adjustable", T * H, L, all3, H * Fh)
+        node(f"{L}.ln2", "fixed", T * H, L, [FP32])
+        edges += [[prev, f"{L}.qkv"], [f"{L}.qkv", f"{L}.attn"], [f"{L}.attn", f"{L}.o"],
+                  [f"{L}.o", f"{L}.ln1"], [prev, f"{L}.ln1"],           # residual
+                  [f"{L}.ln1", f"{L}.ff1"], [f"{L}.ff1", f"{L}.gelu"], [f"{L}.gelu", f"{L}.ff2"],
+                  [f"{L}.ff2", f"{L}.ln2"], [f"{L}.ln1", f"{L}.ln2"]]  # residual
+        prev = f"{L}.ln2"
+    node("pooler", "adjustable", batch * H, "head", all3, H * H)
+    node("loss", "fixed", batch, "head", [FP32])
+    edges += [[prev, "pooler"], ["pooler", "loss"]]
+    return {"nodes": nodes, "edges": edges,
+            "assignment": {n["id"]: FP32 for n in nodes}}
+
+
+# ----------------------------------------------------------------------------- op costs
+def linear_memory_bytes(precision: str, M: int, N: int, K: int) -> int:
+    """Bytes an op keeps resident at a precision: FP32 master weight + its FP32
+    gradient + AdamW moments, the precision's operand copies, the operand saved
+    for backward, and the output (graph.hpp:38-40 output format)."""
+    # What the op itself keeps resident between forward and backward: the FP32
+    # master weight, its FP32 gradient and the two AdamW moments, plus the
+    # operands saved for backward.  (Its output is the consumer's saved input.)
+    W = N * K
+    base = 4 * W * 4
+    if precision == INT8:
+        return base + M * K * 1            # Xq^T (int8); W16^T is recomputed in backward
+    if precision == FP16:
+        return base + M * K * 2 + W * 2    # X16^T, W16^T
+    return base + M * K * 4                # X
+
+
+def measure_linear(M: int, N: int, K: int, precision: str, reps: int = 10) -> dict:
+    lin = QLinear(K, N, "probe", precision=precision).cuda()
+    x = torch.randn(M, K, device="cuda", requires_grad=True)
+    dy = torch.randn(M, N, device="cuda").to(qlinear.output_dtype(precision))
+
+    def fwd():
+        with torch.no_grad():
+            lin(x)
+
+    def fwd_bwd():
+        y = lin(x)
+        y.backward(dy)
+        lin.weight.grad = None
+        lin.bias.grad = None
+        x.grad = None
+
+    f = _time_ns(fwd, reps)
+    t = _time_ns(fwd_bwd, reps)
+    return {"pure_cost_ns": max(t, f + 1), "fwd_fraction": min(1.0, f / max(t, f + 1)),
+            "memory_bytes": linear_memory_bytes(precision, M, N, K)}
+
+
+def measure_glue(cfg: BertConfig, batch: int, reps: int = 10) -> dict:
+    """Costs of the fixed / dependent operators (their FP32 or FP16 kernels)."""
+    from flash_attn import flash_attn_qkvpacked_func
+
+    from .glue import AddLayerNorm
+    T, H, Fh = batch * cfg.seq, cfg.hidden, cfg.ffn
+    out = {}
+    qkv = torch.randn(batch, cfg.seq, 3, cfg.heads, H // cfg.heads, device="cuda",
+                      dtype=torch.float16, requires_grad=True)
+    g = torch.randn(batch, cfg.seq, cfg.heads, H // cfg.heads, device="cuda", dtype=torch.float16)
+
+    def attn():
+        flash_attn_qkvpacked_func(qkv).backward(g)
+    t = _time_ns(attn, reps)
+    out["attn"] = {FP32: {"pure_cost_ns": t, "fwd_fraction": 1.0 / 3.0,
+                          "memory_bytes": T * 3 * H * 2 + T * H * 2}}
+    ln = AddLayerNorm(H).cuda()
+    a = torch.randn(T, H, device="cuda", requires_grad=True)
+    b = torch.randn(T, H, device="cuda", requires_grad=True)
+    gy = torch.randn(T, H, device="cuda")
+
+    def lnfb():
+        ln(a, b).backward(gy)
+    t = _time_ns(lnfb, reps)
+    out["ln"] = {FP32: {"pure_cost_ns": t, "fwd_fraction": 1.0 / 3.0,
+                        "memory_bytes": T * H * 4 * 2 + 2 * H * 4 * 4}}
+    out["gelu"] = {}
+    for p, dt in ((FP32, torch.float32), (FP16, torch.float16)):
+        xg = torch.randn(T, Fh, device="cuda", dtype=dt, requires_grad=True)
+        gg = torch.randn(T, Fh, device="cuda", dtype=dt)
+
+        def gelu(xg=xg, gg=gg):
+            F.gelu(xg).backward(gg)
+        out["gelu"][p] = {"pure_cost_ns": _time_ns(gelu, reps), "fwd_fraction": 1.0 / 3.0,
+                          "memory_bytes": T * Fh * _PREC_BYTES[p] * 2}
+    emb = torch.nn.Embedding(cfg.vocab, H).cuda()
+    tok = torch.randint(0, cfg.vocab, (batch, cfg.seq), device="cuda")
+    ge = torch.randn(batch, cfg.seq, H, device="cuda")
+
+    def embed():
+        emb(tok).backward(ge)
+    out["embed"] = {FP32: {"pure_cost_ns": _time_ns(embed, reps), "fwd_fraction": 1.0 / 3.0,
+                           "memory_bytes": cfg.vocab * H * 4 * 4 + T * H * 4}}
+    cls = torch.nn.Linear(H, cfg.num_labels).cuda()
+    pooled = torch.randn(batch, H, device="cuda", requires_grad=True)
+    lab = torch.randint(0, cfg.num_labels, (batch,), device="cuda")
+
+    def loss():
+        F.cross_entropy(cls(pooled), lab).backward()
+    out["loss"] = {FP32: {"pure_cost_ns": _time_ns(loss, reps), "fwd_fraction": 1.0 / 3.0,
+                          "memory_bytes": H * cfg.num_labels * 16 + batch * H * 4}}
+    return out
+
+
+def measure_op_costs(cfg: BertConfig, batch: int, reps: int = 10) -> dict:
+    T, H, Fh = batch * cfg.seq, cfg.hidden, cfg.ffn
+    shapes = {"qkv": (T, 3 * H, H), "o": (T, H, H), "ff1": (T, Fh, H), "ff2": (T, H, Fh)}
+    per_shape = {k: {p: measure_linear(*s, p, reps) for p in (INT8, FP16, FP32)}
+                 for k, s in shapes.items()}
+    pooler = {p: measure_linear(batch, H, H, p, reps) for p in (INT8, FP16, FP32)}
+    glue = measure_glue(cfg, batch, reps)
+    costs = {"embed": glue["embed"], "pooler": pooler, "loss": glue["loss"]}
+    for i in range(cfg.layers):
+        L = f"layer{i}"
+        for k in shapes:
+            costs[f"{L}.{k}"] = per_shape[k]
+        costs[f"{L}.attn"] = glue["attn"]
+        costs[f"{L}.ln1"] = glue["ln"]
+        costs[f"{L}.ln2"] = glue["ln"]
+        costs[f"{L}.gelu"] = glue["gelu"]
+    return costs
+
+
+# ----------------------------------------------------------------------------- casts
+def measure_cast_samples(sizes=(1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24), reps: int = 10):
+    """Measured latencies for every key required_cast_keys asks for (profile.cpp:212-228)."""
+    samples = []
+    for n in sizes:
+        x32 = torch.randn(n, device="cuda")
+        x16 = x32.half()
+        q = torch.randint(-127, 128, (n,), dtype=torch.int8, device="cuda")
+        sc = torch.tensor([0.01], device="cuda")
+        cases = [
+            (FP32, FP16, "float_to_float", lambda: ops.cast(x32, torch.float16)),
+            (FP16, FP32, "float_to_float", lambda: ops.cast(x16, torch.float32)),
+            (FP32, INT8, "quantize_fixed", lambda: ops.quantize_per_tensor(x32.view(1, -1))),
+            (FP16, INT8, "quantize_fixed", lambda: ops.quantize_per_tensor(x16.view(1, -1))),
+            (INT8, FP32, "dequantize_fixed", lambda: ops.dequantize_per_tensor(q, sc)),
+        ]
+        for src, dst, scheme, fn in cases:
+            samples.append({"src": src, "dst": dst, "scheme": scheme, "numel": n,
+                            "measured_ns": _time_ns(fn, reps)})
+    return samples
+
+
+# ----------------------------------------------------------------------------- stats
+class StatsRecorder:
+    """Collects device statistics per op for one step; ``snapshot()`` turns them
+    into the OpStats JSON fields (profile.hpp:95-108)."""
+
+    def __init__(self):
+        self.cur: dict[str, dict[str, torch.Tensor]] = {}
+
+    def record(self, name: str, kind: str, st: torch.Tensor) -> None:
+        self.cur.setdefault(name, {})[kind] = st
+
+    def snapshot(self) -> dict:
+        snap = {}
+        for name, d in self.cur.items():
+            if not {"act", "w", "grad"} <= set(d):
+                continue
+            a, w, g = (d[k].tolist() for k in ("act", "w", "grad"))
+            # [||x||^2, absmax, q = absmax/127, e = floor(log2 absmax), numel]
+            snap[name] = {"norm_w_sq": w[0], "norm_act_sq": a[0], "norm_grad_act_sq": g[0],
+                          "d_act": a[4], "d_w": w[4], "d_grad": g[4],
+                          "q_act": a[2], "q_w": w[2], "e_act": a[3], "e_w": w[3], "e_grad": g[3]}
+        self.cur = {}
+        return snap
+
+
+def collect_tensor_stats(model: BertEncoderStack, batch: int, steps: int, seed: int = 0):
+    """Run `steps` eager training steps (SGD, the plan currently applied) and record
+    one statistics snapshot per step."""
+    cfg = model.cfg
+    g = torch.Generator().manual_seed(seed)
+    opt = torch.optim.SGD(model.parameters(), lr=1e-4)
+    rec = StatsRecorder()
+    snaps = []
+    qlinear.STATS_RECORDER = rec
+    try:
+        for _ in range(steps):
+            tok = torch.randint(0, cfg.vocab, (batch, cfg.seq), generator=g).cuda()
+            lab = torch.randint(0, cfg.num_labels, (batch,), generator=g).cuda()
+            opt.zero_grad(set_to_none=True)
+            model(tok, lab).backward()
+            opt.step()
+            snaps.append(rec.snapshot())
+    finally:
+        qlinear.STATS_RECORDER = None
+    return snaps
+
+
+# ----------------------------------------------------------------------------- bundle
+def build_bundle(graph: dict, op_costs: dict, cast_samples: list, tensor_stats: list,
+                 devices: list, comm: dict | None = None) -> dict:
+    b = {"schema_version": 1, "graph": graph, "op_costs": op_costs,
+         "cast_samples": cast_samples, "tensor_stats": tensor_stats, "devices": devices}
+    if comm:
+        b["comm"] = comm
+    return b
+
+
+def default_cap(graph: dict, costs: dict, frac: float = 0.75) -> int:
+    """A binding but feasible memory cap for the inference device: halfway between
+    the all-lowest-precision and the all-FP32 footprint (the paper's cluster B caps
+    inference GPUs at 30% of their memory; here the cap is set relative
+    to this model's own footprint so the allocator has a real trade-off)."""
+    full = sum(costs[n["id"]][FP32]["memory_bytes"] if FP32 in costs[n["id"]] else
+               max(v["memory_bytes"] for v in costs[n["id"]].values()) for n in graph["nodes"])
+    # lowest footprint: adjustable ops at their cheapest precision; dependent ops
+    # may be forced up by the cascade (INT8 producers emit FP32), so take their max
+    low = sum((min if n["kind"] == "adjustable" else max)(v["memory_bytes"]
+                                                          for v in costs[n["id"]].values())
+              for n in graph["nodes"])
+    return int(low + frac * (full - low))
+
+
+def profile_bert(cfg: BertConfig, batch: int, stat_steps: int = 3, infer_cap_bytes: int | None = None,
+                 reps: int = 10) -> dict:
+    """Measure everything on the current device and return the bundle dict."""
+    model = BertEncoderStack(cfg).cuda()
+    model.apply_plan({})  # statistics are profiled at FP32 (the reference's assignment)
+    stats = collect_tensor_stats(model, batch, stat_steps)
+    del model
+    costs = measure_op_costs(cfg, batch, reps)
+    casts = measure_cast_samples(reps=reps)
+    graph = bert_graph(cfg, batch)
+    cap = infer_cap_bytes or default_cap(graph, costs)
+    devices = [{"id": "trainer", "is_inference": False, "mem_capacity_bytes": 183_000_000_000},
+               {"id": "infer", "is_inference": True, "mem_capacity_bytes": max(cap, 1)}]
+    return build_bundle(graph, costs, casts, stats, devices)
+
+
+def main(argv=None):
+    import argparse
+    ap = argparse.ArgumentParser(description="profile the B200 hot path into a QSync bundle")
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--layers", type=int, default=12)
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--stat-steps", type=int, default=3)
+    args = ap.parse_args(argv)
+    cfg = BertConfig(layers=args.layers)
+    bundle = profile_bert(cfg, args.batch, args.stat_steps)
+    with open(args.out, "w") as f:
+        json.dump(bundle, f, indent=1)
+    print(f"wrote {args.out}")
+
+
+if __name__ == "__main__":
+    main()

@@ -24,6 +24,16 @@ from . import ops
 INT8, FP16, FP32 = "INT8", "FP16", "FP32"
 PRECISIONS = (INT8, FP16, FP32)
 
+# Profiling hook (profiler.StatsRecorder): when set, every QLinear records the
+# device statistics of its input activation, weight and incoming gradient
+# (qsync_tensor_stats -> OpStats fields, profile.hpp:95-108).
+STATS_RECORDER = None
+
+
+def _record(name, kind, t):
+    if STATS_RECORDER is not None and name is not None:
+        STATS_RECORDER.record(name, kind, ops.tensor_stats(t.contiguous()))
+
 
 def output_dtype(precision: str) -> torch.dtype:
     """graph.hpp:38-40: fixed-point kernels emit FP32, float kernels their own format."""
@@ -63,26 +73,39 @@ def _fp16_backward(ctx, dy, x16_t, w16_t, alpha_dev):
 
 class _QLinearInt8(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w, b):
-        xq, xs, xq_t = ops.quantize_per_tensor(x, transposed_f16=True)
-        wq, ws, w_t16 = ops.quantize_per_channel(w, transposed_f16=True)
+    def forward(ctx, x, w, b, name=None):
+        _record(name, "act", x)
+        _record(name, "w", w)
+        ctx.name = name
+        # The INT8 op keeps only its 1-byte quantized activation (transposed, the
+        # K-major wgrad operand) for backward; FP16 views of it and of W are made
+        # in backward -- the "bp_cost" casts of the paper's cost model (PAPER.md:
+        # Fig. cost composition), which buy the INT8 op its memory saving.
+        xq, xs, xq_t8 = ops.quantize_per_tensor(x, transposed_i8=True)
+        wq, ws, _ = ops.quantize_per_channel(w)
         _, y = ops.gemm_s8(xq, wq, xs, ws, b)
-        ctx.save_for_backward(xq_t, xs, w_t16)
+        ctx.save_for_backward(xq_t8, xs)
         ctx.x_dtype = x.dtype
         ctx.w_ref, ctx.b_ref = w, b
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        xq_t, xs, w_t16 = ctx.saved_tensors
+        xq_t8, xs = ctx.saved_tensors
+        _record(ctx.name, "grad", dy)
+        xq_t = ops.cast(xq_t8, torch.float16)                        # exact: int8 values
+        _, w_t16, _ = ops.cast_transpose(ctx.w_ref.detach(), False, True, False)
         # wgrad = s_x * dY16^T X^ : the saved INT8 activation (as exact FP16
         # integers) with the activation scale applied in the epilogue.
-        return _fp16_backward(ctx, dy, xq_t, w_t16, xs)
+        return _fp16_backward(ctx, dy, xq_t, w_t16, xs) + (None,)
 
 
 class _QLinearFp16(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w, b):
+    def forward(ctx, x, w, b, name=None):
+        _record(name, "act", x)
+        _record(name, "w", w)
+        ctx.name = name
         if x.dtype == torch.float16:
             x16 = x
             _, x16_t, _ = ops.cast_transpose(x, False, True, False)
@@ -98,7 +121,8 @@ class _QLinearFp16(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dy):
         x16_t, w16_t = ctx.saved_tensors
-        return _fp16_backward(ctx, dy, x16_t, w16_t, None)
+        _record(ctx.name, "grad", dy)
+        return _fp16_backward(ctx, dy, x16_t, w16_t, None) + (None,)
 
 
 class _Cast(torch.autograd.Function):
@@ -118,18 +142,23 @@ def cast(x: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
     return x if x.dtype == dtype else _Cast.apply(x, dtype)
 
 
-def qlinear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, precision: str) -> torch.Tensor:
+def qlinear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, precision: str,
+            name: str | None = None) -> torch.Tensor:
     """Y = X W^T + b for X [..., K] at the given plan precision."""
     shape = x.shape
     x2 = x.reshape(-1, shape[-1])
     if not x2.is_contiguous():
         x2 = x2.contiguous()
     if precision == INT8:
-        y = _QLinearInt8.apply(x2, w, b)
+        y = _QLinearInt8.apply(x2, w, b, name)
     elif precision == FP16:
-        y = _QLinearFp16.apply(x2, w, b)
+        y = _QLinearFp16.apply(x2, w, b, name)
     elif precision == FP32:
+        _record(name, "act", x2)
+        _record(name, "w", w)
         y = F.linear(x2.float(), w, b)
+        if STATS_RECORDER is not None and name is not None and y.requires_grad:
+            y.register_hook(lambda g, n=name: _record(n, "grad", g))
     else:
         raise ValueError(f"validation: unknown precision \"{precision}\"")
     return y.reshape(*shape[:-1], w.shape[0])
@@ -151,7 +180,7 @@ class QLinear(torch.nn.Module):
         torch.nn.init.uniform_(self.weight, -bound, bound)
 
     def forward(self, x):
-        return qlinear(x, self.weight, self.bias, self.precision)
+        return qlinear(x, self.weight, self.bias, self.precision, self.name)
 
     def extra_repr(self):
         return f"{self.name}: {self.in_features}->{self.out_features} {self.precision}"

@@ -59,6 +59,12 @@ def test_quantize_per_tensor_bit_exact(shape, dist, cpuref):
     assert not qt[:, rows:].any()
     q2, scale2, _ = ops.quantize_per_tensor(_t(x))
     assert np.array_equal(_np(q2), q_ref) and _np(scale2)[0] == s_ref
+    # the 1-byte transposed copy an INT8 op keeps for backward, and its exact FP16 view
+    q3, _, qt8 = ops.quantize_per_tensor(_t(x), transposed_i8=True)
+    assert np.array_equal(_np(q3), q_ref)
+    qt8n = _np(qt8)
+    assert qt8n.dtype == np.int8 and np.array_equal(qt8n[:, :rows], q_ref.T) and not qt8n[:, rows:].any()
+    assert np.array_equal(_np(ops.cast(qt8, torch.float16)).astype(np.int32), qt8n.astype(np.int32))
 
 
 def test_quantize_edge_cases(cpuref):
