@@ -181,6 +181,22 @@ int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_
                    int accumulate, qsync_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * K8  Conv2d as GEMM, NHWC.  The column matrix
+ * A[(n,p,q), (r,s,c)] = x[n, p*sh-ph+r*dh, q*sw-pw+s*dw, c] (0 outside) is the
+ * K-major operand of qsync_gemm_s8 / qsync_gemm_f16 (weights [Cout, R*S*C],
+ * i.e. KRSC); `ld` is its row pitch (>= R*S*C, zero padded; 16-byte multiple
+ * for TMA).  col2im is the deterministic gather adjoint (dgrad), FP32 out.
+ * ------------------------------------------------------------------------- */
+int qsync_conv_out_size(int64_t H, int64_t W, int R, int S, int sh, int sw, int ph, int pw, int dh,
+                        int dw, int64_t* P, int64_t* Q);
+int qsync_im2col(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int R, int S,
+                 int sh, int sw, int ph, int pw, int dh, int dw, void* out, int64_t ld,
+                 qsync_stream_t stream);
+int qsync_col2im(const void* dcol, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int R,
+                 int S, int sh, int sw, int ph, int pw, int dh, int dw, int64_t ld, float* dx,
+                 qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * Glue between planned operators: fused residual add + LayerNorm.
  * fwd: s = a + b (b FP32 or FP16 [rows, cols], may be NULL), y = LN(s) with
  *      gamma/beta; saves s (optional), mean[rows], rstd[rows].

@@ -437,6 +437,57 @@ void ref_qlinear_f16_fwd_bwd(const float* x, const float* w, const float* bias, 
     free(x16); free(w16);
 }
 
+/* ------------------------------------------------------------------------- */
+/* Conv2d as GEMM, NHWC: the column matrix and its adjoint.     */
+/* A[(n,p,q),(r,s,c)] = x[n, p*sh-ph+r*dh, q*sw-pw+s*dw, c], 0 outside; K      */
+/* padded with zeros to ld.  esz = element size (1 int8, 2 fp16, 4 fp32).       */
+/* ------------------------------------------------------------------------- */
+void ref_im2col(const void* x, int esz, int64_t N, int64_t H, int64_t W, int64_t C, int R, int S,
+                int sh, int sw, int ph, int pw, int dh, int dw, int64_t P, int64_t Q, int64_t ld,
+                void* out) {
+    const char* xb = (const char*)x;
+    char* ob = (char*)out;
+    const int64_t K = (int64_t)R * S * C;
+#pragma omp parallel for schedule(static)
+    for (int64_t row = 0; row < N * P * Q; ++row) {
+        const int64_t q = row % Q, p = (row / Q) % P, n = row / (Q * P);
+        memset(ob + row * ld * esz, 0, (size_t)(ld * esz));
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) {
+                const int64_t h = p * sh - ph + (int64_t)r * dh, w = q * sw - pw + (int64_t)s * dw;
+                if (h < 0 || h >= H || w < 0 || w >= W) continue;
+                memcpy(ob + (row * ld + ((int64_t)r * S + s) * C) * esz,
+                       xb + (((n * H + h) * W + w) * C) * esz, (size_t)(C * esz));
+            }
+        (void)K;
+    }
+}
+
+/* dx[n,h,w,c] = sum of dcol entries that gathered x[n,h,w,c] (FP64 accumulate). */
+void ref_col2im(const float* dcol, int64_t N, int64_t H, int64_t W, int64_t C, int R, int S, int sh,
+                int sw, int ph, int pw, int dh, int dw, int64_t P, int64_t Q, int64_t ld,
+                float* dx) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < N * H * W * C; ++i) {
+        const int64_t c = i % C, w = (i / C) % W, h = (i / (C * W)) % H, n = i / (C * W * H);
+        double acc = 0.0;
+        for (int r = 0; r < R; ++r) {
+            const int64_t hp = h + ph - (int64_t)r * dh;
+            if (hp < 0 || hp % sh) continue;
+            const int64_t p = hp / sh;
+            if (p >= P) continue;
+            for (int s = 0; s < S; ++s) {
+                const int64_t wq = w + pw - (int64_t)s * dw;
+                if (wq < 0 || wq % sw) continue;
+                const int64_t q = wq / sw;
+                if (q >= Q) continue;
+                acc += dcol[((n * P + p) * Q + q) * ld + ((int64_t)r * S + s) * C + c];
+            }
+        }
+        dx[i] = (float)acc;
+    }
+}
+
 int ref_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

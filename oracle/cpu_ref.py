@@ -68,6 +68,8 @@ class CpuRef:
         L.ref_tensor_stats_f32.argtypes = [_p, _i64, _p]
         L.ref_qlinear_int8_fwd_bwd.argtypes = [_p] * 4 + [_i64] * 3 + [_p] * 9
         L.ref_qlinear_f16_fwd_bwd.argtypes = [_p] * 4 + [_i64] * 3 + [_p] * 4
+        L.ref_im2col.argtypes = [_p, C.c_int] + [_i64] * 4 + [C.c_int] * 8 + [_i64] * 3 + [_p]
+        L.ref_col2im.argtypes = [_p] + [_i64] * 4 + [C.c_int] * 8 + [_i64] * 3 + [_p]
         L.ref_num_threads.restype = C.c_int
 
     # -- RNG / SR ----------------------------------------------------------
@@ -220,6 +222,32 @@ class CpuRef:
         self.L.ref_qlinear_f16_fwd_bwd(_ptr(x), _ptr(w), _ptr(b), _ptr(g), M, N, K, _ptr(y),
                                        _ptr(dx), _ptr(dw), _ptr(db))
         return dict(y=y, dx=dx, dw=dw, db=db)
+
+    @staticmethod
+    def conv_out(H, W, R, S, stride, pad, dil=(1, 1)):
+        P = (H + 2 * pad[0] - dil[0] * (R - 1) - 1) // stride[0] + 1
+        Q = (W + 2 * pad[1] - dil[1] * (S - 1) - 1) // stride[1] + 1
+        return P, Q
+
+    def im2col(self, x, R, S, stride, pad, dil=(1, 1), ld=None):
+        x = np.ascontiguousarray(x)
+        N, H, W, Cc = x.shape
+        P, Q = self.conv_out(H, W, R, S, stride, pad, dil)
+        K = R * S * Cc
+        ld = ld or K
+        out = np.empty((N * P * Q, ld), x.dtype)
+        self.L.ref_im2col(_ptr(x), x.itemsize, N, H, W, Cc, R, S, stride[0], stride[1], pad[0],
+                          pad[1], dil[0], dil[1], P, Q, ld, _ptr(out))
+        return out, (P, Q)
+
+    def col2im(self, dcol, xshape, R, S, stride, pad, dil=(1, 1)):
+        dcol = np.ascontiguousarray(dcol, np.float32)
+        N, H, W, Cc = xshape
+        P, Q = self.conv_out(H, W, R, S, stride, pad, dil)
+        dx = np.empty((N, H, W, Cc), np.float32)
+        self.L.ref_col2im(_ptr(dcol), N, H, W, Cc, R, S, stride[0], stride[1], pad[0], pad[1],
+                          dil[0], dil[1], P, Q, dcol.shape[1], _ptr(dx))
+        return dx
 
     def num_threads(self) -> int:
         return int(self.L.ref_num_threads())

@@ -63,6 +63,9 @@ SIGNATURES = {
     "qsync_gemm_f16": [_p, _p, _int, _i64, _i64, _i64, _p, _int, _f32, _p, _p, _int, _p],
     "qsync_layernorm_fwd": [_p, _p, _int, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p],
     "qsync_layernorm_bwd": [_p, _p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p],
+    "qsync_conv_out_size": [_i64, _i64, _int, _int, _int, _int, _int, _int, _int, _int, _p, _p],
+    "qsync_im2col": [_p, _int, _i64, _i64, _i64, _i64] + [_int] * 8 + [_p, _i64, _p],
+    "qsync_col2im": [_p, _int, _i64, _i64, _i64, _i64] + [_int] * 8 + [_i64, _p, _p],
     # non-header helpers
     "qsync_gemm_force_tile_n": [_int],
     "qsync_gemm_force_splitk": [_int],

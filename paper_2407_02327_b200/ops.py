@@ -259,6 +259,39 @@ def gemm_f16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32, alpha: f
     return c
 
 
+# --------------------------------------------------------------------------- K8 conv
+def conv_out_size(H, W, R, S, stride, pad, dil=(1, 1)):
+    import ctypes as C
+    P, Q = C.c_int64(0), C.c_int64(0)
+    call("qsync_conv_out_size", H, W, R, S, stride[0], stride[1], pad[0], pad[1], dil[0], dil[1],
+         C.byref(P), C.byref(Q))
+    return P.value, Q.value
+
+
+def im2col(x: torch.Tensor, R: int, S: int, stride, pad, dil=(1, 1), ld: int | None = None):
+    """NHWC x (int8 / fp16) -> column matrix [N*P*Q, ld] (K = R*S*C, zero padded)."""
+    _req(x, "x", (torch.int8, torch.float16, torch.bfloat16))
+    N, H, W, Cc = x.shape
+    P, Q = conv_out_size(H, W, R, S, stride, pad, dil)
+    K = R * S * Cc
+    align = 16 if x.dtype == torch.int8 else 8
+    ld = ld or (K + align - 1) // align * align
+    out = torch.empty((N * P * Q, ld), device=x.device, dtype=x.dtype)
+    call("qsync_im2col", _ptr(x), _DT_CAST[x.dtype], N, H, W, Cc, R, S, stride[0], stride[1],
+         pad[0], pad[1], dil[0], dil[1], _ptr(out), ld, _stream())
+    return out, (P, Q)
+
+
+def col2im(dcol: torch.Tensor, xshape, R: int, S: int, stride, pad, dil=(1, 1)) -> torch.Tensor:
+    """Adjoint of im2col: dx NHWC FP32 from the column gradient (FP32 or FP16)."""
+    _req(dcol, "dcol", (torch.float32, torch.float16))
+    N, H, W, Cc = xshape
+    dx = torch.empty((N, H, W, Cc), device=dcol.device, dtype=torch.float32)
+    call("qsync_col2im", _ptr(dcol), _DT[dcol.dtype], N, H, W, Cc, R, S, stride[0], stride[1],
+         pad[0], pad[1], dil[0], dil[1], dcol.shape[1], _ptr(dx), _stream())
+    return dx
+
+
 # --------------------------------------------------------------------------- glue
 def layernorm_fwd(a: torch.Tensor, b: torch.Tensor | None, gamma, beta, eps: float):
     """s = a + b, y = LN(s).  Returns (y, s, mean, rstd)."""

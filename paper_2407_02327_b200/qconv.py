@@ -1,0 +1,110 @@
+"""Quantized Conv2d (NHWC) -- the convolution kernel a QSync plan selects.
+
+Forward is a GEMM over the im2col column matrix A [N*P*Q, R*S*C] and the KRSC
+weight W [Cout, R*S*C] (below-16-bit convolutions are channels-last):
+  * INT8 -- x quantized once per tensor (1 B/elem NHWC), im2col of the int8
+            tensor, per-channel weight scales, tcgen05 kind::i8 GEMM with the fused
+            dequant + bias epilogue -> FP32 NHWC output (graph.hpp:38-40).
+  * FP16 -- FP16 im2col, tcgen05 kind::f16 GEMM -> FP16 NHWC output.
+  * FP32 -- cuDNN-free FP32 path via torch (training devices stay FP32).
+Backward of INT8/FP16 runs in FP16 (cost_mapper.cpp:13-15): dgrad = col2im(dY16 W16)
+(deterministic gather, FP32), wgrad = dY16^T A16 (times s_x for INT8) in FP32
+(cost_mapper.cpp:48-50).  The INT8 op keeps only its int8 input for backward and
+rebuilds the column matrix there (the paper's backward casting cost).
+"""
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+from . import ops
+from .qlinear import FP16, FP32, INT8
+
+
+def _pad_k(w2: torch.Tensor, kp: int) -> torch.Tensor:
+    if w2.shape[1] == kp:
+        return w2.contiguous()
+    out = torch.zeros((w2.shape[0], kp), device=w2.device, dtype=w2.dtype)
+    out[:, : w2.shape[1]] = w2
+    return out
+
+
+class _QConv(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, b, geom, precision):
+        R, S, stride, pad = geom
+        N, H, W, C = x.shape
+        cout = w.shape[0]
+        K = R * S * C
+        align = 16 if precision == INT8 else 8
+        kp = (K + align - 1) // align * align
+        w2 = _pad_k(w.reshape(cout, K), kp)
+        if precision == INT8:
+            xq, xs, _ = ops.quantize_per_tensor(x.reshape(1, -1))
+            xq = xq.view(N, H, W, C)
+            A, (P, Q) = ops.im2col(xq, R, S, stride, pad, ld=kp)
+            wq, ws, _ = ops.quantize_per_channel(w2)
+            _, y = ops.gemm_s8(A, wq, xs, ws, b)
+            ctx.save_for_backward(xq, xs)
+        else:
+            x16 = x if x.dtype == torch.float16 else ops.cast(x.contiguous(), torch.float16)
+            A, (P, Q) = ops.im2col(x16, R, S, stride, pad, ld=kp)
+            w16 = ops.cast(w2, torch.float16)
+            y = ops.gemm_f16(A, w16, out_dtype=torch.float16, bias=b)
+            ctx.save_for_backward(x16, torch.ones(1, device=x.device))
+        ctx.geom, ctx.precision, ctx.kp = geom, precision, kp
+        ctx.shapes = (N, H, W, C, cout, P, Q, K)
+        ctx.w_ref, ctx.has_bias, ctx.x_dtype = w, b is not None, x.dtype
+        return y.view(N, P, Q, cout)
+
+    @staticmethod
+    def backward(ctx, dy):
+        xs_saved, alpha = ctx.saved_tensors
+        R, S, stride, pad = ctx.geom
+        N, H, W, C, cout, P, Q, K = ctx.shapes
+        kp = ctx.kp
+        dy2 = dy.reshape(N * P * Q, cout).contiguous()
+        dy16, dy16_t, db = ops.cast_transpose(dy2, True, True, ctx.has_bias)
+        w2 = _pad_k(ctx.w_ref.detach().reshape(cout, K), kp)
+        _, w16_t, _ = ops.cast_transpose(w2, False, True, False)          # [kp, cout]
+        dcol = ops.gemm_f16(dy16, w16_t, out_dtype=torch.float32)         # dgrad columns
+        dx = ops.col2im(dcol, (N, H, W, C), R, S, stride, pad)
+        # wgrad: rebuild the FP16 column matrix from the saved (int8 / fp16) input.
+        A, _ = ops.im2col(xs_saved, R, S, stride, pad, ld=kp)
+        A16 = A if A.dtype == torch.float16 else ops.cast(A, torch.float16)
+        _, A16_t, _ = ops.cast_transpose(A16, False, True, False)         # [kp, pad8(NPQ)]
+        dw2 = ops.gemm_f16(dy16_t, A16_t, out_dtype=torch.float32,
+                           alpha_dev=alpha if ctx.precision == INT8 else None)
+        dw = dw2[:, :K].reshape(ctx.w_ref.shape)
+        if ctx.x_dtype != torch.float32:
+            dx = dx.to(ctx.x_dtype)
+        return dx, dw, db, None, None
+
+
+def qconv2d(x, w, b, stride=(1, 1), pad=(0, 0), precision=FP32):
+    """x NHWC [N,H,W,C], w KRSC [Cout,R,S,C] -> y NHWC [N,P,Q,Cout]."""
+    cout, R, S, C = w.shape
+    if precision == FP32:
+        y = F.conv2d(x.permute(0, 3, 1, 2).float(), w.permute(0, 3, 1, 2), b, stride, pad)
+        return y.permute(0, 2, 3, 1)
+    if precision not in (INT8, FP16):
+        raise ValueError(f"validation: unknown precision \"{precision}\"")
+    return _QConv.apply(x.contiguous(), w, b, (R, S, tuple(stride), tuple(pad)), precision)
+
+
+class QConv2d(torch.nn.Module):
+    """NHWC Conv2d whose kernel precision is set by the device's plan entry."""
+
+    def __init__(self, cin, cout, kernel, name, stride=1, pad=0, bias=True, precision=FP32):
+        super().__init__()
+        k = (kernel, kernel) if isinstance(kernel, int) else kernel
+        self.name = name
+        self.stride = (stride, stride) if isinstance(stride, int) else stride
+        self.pad = (pad, pad) if isinstance(pad, int) else pad
+        self.weight = torch.nn.Parameter(torch.empty(cout, k[0], k[1], cin))
+        self.bias = torch.nn.Parameter(torch.zeros(cout)) if bias else None
+        self.precision = precision
+        torch.nn.init.kaiming_uniform_(self.weight.view(cout, -1), a=5 ** 0.5)
+
+    def forward(self, x):
+        return qconv2d(x, self.weight, self.bias, self.stride, self.pad, self.precision)
