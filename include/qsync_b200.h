@@ -173,12 +173,16 @@ int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_
  * A [M,K], B [N,K] of ab_dtype (QSYNC_F16 / QSYNC_BF16), K % 8 == 0.
  * c = alpha * (alpha_dev ? *alpha_dev : 1) * acc (+ bias[n]) (+ c if accumulate)
  * written as c_dtype (QSYNC_F32 or QSYNC_F16 / QSYNC_BF16).
+ * layout: 0 = A [M,K] and B [N,K] (K-major); 2 = B stored [K,N] (MN-major);
+ * 3 = A stored [K,M] and B stored [K,N] (both MN-major).  With MN-major operands
+ * the backward needs no transposed copies: dgrad reads W [N_out,K_in] as
+ * MN-major B, wgrad reads dY [M,N_out] and X [M,K_in] as MN-major A and B.
  * Used for FP16 forward, dgrad (FP16 out) and wgrad (FP32 out, alpha_dev = the
  * activation scale of an INT8 op; cost_mapper.cpp:48-50).
  * ------------------------------------------------------------------------- */
 int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,
                    void* c, int c_dtype, float alpha, const float* alpha_dev, const float* bias,
-                   int accumulate, qsync_stream_t stream);
+                   int accumulate, int layout, qsync_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * K8  Conv2d as GEMM, NHWC.  The column matrix

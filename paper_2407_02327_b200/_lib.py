@@ -60,7 +60,7 @@ SIGNATURES = {
     "qsync_stats_workspace_bytes": [],
     "qsync_tensor_stats": [_p, _int, _i64, _p, _p, _p],
     "qsync_gemm_s8": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _int, _p, _p],
-    "qsync_gemm_f16": [_p, _p, _int, _i64, _i64, _i64, _p, _int, _f32, _p, _p, _int, _p],
+    "qsync_gemm_f16": [_p, _p, _int, _i64, _i64, _i64, _p, _int, _f32, _p, _p, _int, _int, _p],
     "qsync_layernorm_fwd": [_p, _p, _int, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p],
     "qsync_layernorm_bwd": [_p, _p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p],
     "qsync_conv_out_size": [_i64, _i64, _int, _int, _int, _int, _int, _int, _int, _int, _p, _p],

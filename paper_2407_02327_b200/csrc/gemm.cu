@@ -71,7 +71,9 @@ struct Cfg {
 
 __device__ __forceinline__ float bits_f(uint32_t v) { return __uint_as_float(v); }
 
-template <bool kI8, int BN, int kCta>
+// kLay bit 0: A is MN-major (stored [K, M]); bit 1: B is MN-major ([K, N]).
+// MN-major tiles are loaded as 64-element-wide (128 B) blocks of bk K-rows.
+template <bool kI8, int BN, int kCta, int kLay>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
               const __grid_constant__ CUtensorMap tm_c, const EpiParams p) {
@@ -159,16 +161,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                         // Both CTAs' bytes complete on the leader's full barrier.
                         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], kCta * C::kStageBytes);
                         const uint32_t fb = full_leader0 + stage * 8;
-                        ptx::tma_load_2d_pair(smem_a + stage * BM * BK_BYTES, &tm_a, fb,
-                                              kb * bk_elems, m0);
-                        ptx::tma_load_2d_pair(smem_b + stage * kBRows * BK_BYTES, &tm_b, fb,
-                                              kb * bk_elems, n0);
+                        uint8_t* sa = smem_a + stage * BM * BK_BYTES;
+                        uint8_t* sb = smem_b + stage * kBRows * BK_BYTES;
+                        if (kLay & 1) {
+                            for (int j = 0; j < BM / 64; ++j)
+                                ptx::tma_load_2d_pair(sa + j * bk_elems * 128, &tm_a, fb, m0 + 64 * j,
+                                                      kb * bk_elems);
+                        } else {
+                            ptx::tma_load_2d_pair(sa, &tm_a, fb, kb * bk_elems, m0);
+                        }
+                        if (kLay & 2) {
+                            for (int j = 0; j < kBRows / 64; ++j)
+                                ptx::tma_load_2d_pair(sb + j * bk_elems * 128, &tm_b, fb, n0 + 64 * j,
+                                                      kb * bk_elems);
+                        } else {
+                            ptx::tma_load_2d_pair(sb, &tm_b, fb, kb * bk_elems, n0);
+                        }
                     } else {
                         ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                        ptx::tma_load_2d(smem_a + stage * BM * BK_BYTES, &tm_a, &full[stage],
-                                         kb * bk_elems, m0);
-                        ptx::tma_load_2d(smem_b + stage * kBRows * BK_BYTES, &tm_b, &full[stage],
-                                         kb * bk_elems, n0);
+                        uint8_t* sa = smem_a + stage * BM * BK_BYTES;
+                        uint8_t* sb = smem_b + stage * kBRows * BK_BYTES;
+                        if (kLay & 1) {
+                            for (int j = 0; j < BM / 64; ++j)
+                                ptx::tma_load_2d(sa + j * bk_elems * 128, &tm_a, &full[stage],
+                                                 m0 + 64 * j, kb * bk_elems);
+                        } else {
+                            ptx::tma_load_2d(sa, &tm_a, &full[stage], kb * bk_elems, m0);
+                        }
+                        if (kLay & 2) {
+                            for (int j = 0; j < kBRows / 64; ++j)
+                                ptx::tma_load_2d(sb + j * bk_elems * 128, &tm_b, &full[stage],
+                                                 n0 + 64 * j, kb * bk_elems);
+                        } else {
+                            ptx::tma_load_2d(sb, &tm_b, &full[stage], kb * bk_elems, n0);
+                        }
                     }
                     if (++stage == kStages) {
                         stage = 0;
@@ -197,8 +223,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b_addr = ptx::smem_u32(smem_b + stage * kBRows * BK_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK_BYTES / 32; ++k) {  // UMMA_K = 32 bytes
-                        const uint64_t da = ptx::sw128_kmajor_desc(a_addr + k * 32);
-                        const uint64_t db = ptx::sw128_kmajor_desc(b_addr + k * 32);
+                        // K-major: advance 32 bytes along the swizzled row; MN-major:
+                        // advance 16 K-rows (UMMA_K for 16-bit operands) of 128 bytes.
+                        const uint64_t da = (kLay & 1)
+                                                ? ptx::sw128_mnmajor_desc(a_addr + k * 16 * 128, bk_elems * 128)
+                                                : ptx::sw128_kmajor_desc(a_addr + k * 32);
+                        const uint64_t db = (kLay & 2)
+                                                ? ptx::sw128_mnmajor_desc(b_addr + k * 16 * 128, bk_elems * 128)
+                                                : ptx::sw128_kmajor_desc(b_addr + k * 32);
                         const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
                         if (kCta == 2) {
                             if (kI8)
@@ -467,8 +499,10 @@ int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t
 
 // Instruction descriptor (tcgen05 "idesc"): c_format [4,6), a_format [7,10),
 // b_format [10,13), a/b major [15],[16] (0 = K-major), N>>3 [17,23), M>>4 [24,29).
-uint32_t make_idesc(bool i8, bool bf16, int n, int m) {
+uint32_t make_idesc(bool i8, bool bf16, int n, int m, int lay = 0) {
     uint32_t d = 0;
+    d |= static_cast<uint32_t>(lay & 1) << 15;         // A MN-major
+    d |= static_cast<uint32_t>((lay >> 1) & 1) << 16;  // B MN-major
     d |= (i8 ? 2u : 1u) << 4;                         // S32 / F32 accumulator
     const uint32_t fmt = i8 ? 1u : (bf16 ? 1u : 0u);  // signed int8 / BF16 / F16
     d |= fmt << 7;
@@ -483,14 +517,20 @@ int g_splitk_wide = 0;   // accumulate GEMMs prefer BN=256 (bench hook)
 int g_force_cta = 0;     // test/bench hook (qsync_gemm_force_cta): 0 = cost model, 1, 2
 int g_debug_epi = 0;     // bench hook (qsync_gemm_debug_epilogue)
 
-template <bool kI8, int BN, int kCta>
+template <bool kI8, int BN, int kCta, int kLay>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
     using C = Cfg<BN, kCta>;
     const uint32_t eb = kI8 ? 1 : 2;
     const uint32_t box_k = BK_BYTES / eb;
     CUtensorMap ma, mb, mc;
-    QSB_TRY(make_map(&ma, a, dt, eb, p.K, p.M, box_k, BM));
-    QSB_TRY(make_map(&mb, b, dt, eb, p.K, p.N, box_k, C::kBRows));
+    if (kLay & 1)  // A stored [K, M]: boxes of 64 M-elements x box_k K-rows
+        QSB_TRY(make_map(&ma, a, dt, eb, p.M, p.K, 64, box_k));
+    else
+        QSB_TRY(make_map(&ma, a, dt, eb, p.K, p.M, box_k, BM));
+    if (kLay & 2)
+        QSB_TRY(make_map(&mb, b, dt, eb, p.N, p.K, 64, box_k));
+    else
+        QSB_TRY(make_map(&mb, b, dt, eb, p.K, p.N, box_k, C::kBRows));
     std::memset(&mc, 0, sizeof(mc));
     // TMA-store epilogue when exactly one output is requested and its rows are
     // 16-byte pitched and aligned; 16-bit accumulate keeps the direct path.
@@ -509,7 +549,7 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     }
     static bool configured = false;
     if (!configured) {
-        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_gemm_tc<kI8, BN, kCta>,
+        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_gemm_tc<kI8, BN, kCta, kLay>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  C::kSmemBytes),
                             "cudaFuncSetAttribute"));
@@ -543,7 +583,7 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     const int64_t units = tiles * p.ksplit;
     const int grid = static_cast<int>(std::min<int64_t>(units, slots)) * kCta;
     if (kCta == 1) {
-        k_gemm_tc<kI8, BN, 1><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, p);
+        k_gemm_tc<kI8, BN, 1, kLay><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, p);
         return check_launch("k_gemm_tc");
     }
     cudaLaunchConfig_t cfg{};
@@ -558,7 +598,7 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    QSB_TRY(cuda_status(cudaLaunchKernelEx(&cfg, k_gemm_tc<kI8, BN, kCta>, ma, mb, mc, p),
+    QSB_TRY(cuda_status(cudaLaunchKernelEx(&cfg, k_gemm_tc<kI8, BN, kCta, kLay>, ma, mb, mc, p),
                         "cudaLaunchKernelEx(cluster 2)"));
     return check_launch("k_gemm_tc<pair>");
 }
@@ -595,9 +635,27 @@ Shape pick_shape(int64_t M, int64_t N, bool allow_pair) {
     return best;
 }
 
+template <bool kI8, int kLay>
+int dispatch_shape(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p,
+                   cudaStream_t st, Shape sh) {
+    if (sh.cta == 2) {
+        switch (sh.bn) {
+            case 256: return launch<kI8, 256, 2, kLay>(a, b, dt, p, st);
+            case 128: return launch<kI8, 128, 2, kLay>(a, b, dt, p, st);
+            default: break;
+        }
+    }
+    switch (sh.bn) {
+        case 256: return launch<kI8, 256, 1, kLay>(a, b, dt, p, st);
+        case 128: return launch<kI8, 128, 1, kLay>(a, b, dt, p, st);
+        case 64: return launch<kI8, 64, 1, kLay>(a, b, dt, p, st);
+        default: return set_error(QSYNC_ERR_DOMAIN, "unsupported tile N " + std::to_string(sh.bn));
+    }
+}
+
 template <bool kI8>
 int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st,
-             int force_bn) {
+             int force_bn, int layout = 0) {
     const bool splitk_ok = !kI8 && p.accumulate && p.c_dtype == QSYNC_F32 && g_splitk_wide;
     // Accumulating FP32 GEMMs (wgrad) go split-K on single-CTA 256-wide tiles.
     const bool accumulating = !kI8 && p.accumulate && p.c_dtype == QSYNC_F32;
@@ -606,20 +664,14 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     if (force_bn) sh.bn = force_bn;
     if (g_force_cta) sh.cta = g_force_cta;
     if (sh.cta == 2 && sh.bn == 64) sh.cta = 1;  // pair tiles need BN/2 >= 64 rows of B
-    p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta);
+    p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout);
     p.debug_epi = g_debug_epi;
-    if (sh.cta == 2) {
-        switch (sh.bn) {
-            case 256: return launch<kI8, 256, 2>(a, b, dt, p, st);
-            case 128: return launch<kI8, 128, 2>(a, b, dt, p, st);
-            default: break;
-        }
-    }
-    switch (sh.bn) {
-        case 256: return launch<kI8, 256, 1>(a, b, dt, p, st);
-        case 128: return launch<kI8, 128, 1>(a, b, dt, p, st);
-        case 64: return launch<kI8, 64, 1>(a, b, dt, p, st);
-        default: return set_error(QSYNC_ERR_DOMAIN, "unsupported tile N " + std::to_string(sh.bn));
+    if (kI8) return dispatch_shape<kI8, 0>(a, b, dt, p, st, sh);
+    switch (layout) {
+        case 0: return dispatch_shape<kI8, 0>(a, b, dt, p, st, sh);
+        case 2: return dispatch_shape<kI8, 2>(a, b, dt, p, st, sh);
+        case 3: return dispatch_shape<kI8, 3>(a, b, dt, p, st, sh);
+        default: return set_error(QSYNC_ERR_DOMAIN, "unsupported operand layout " + std::to_string(layout));
     }
 }
 
@@ -692,8 +744,13 @@ int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_
 
 int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,
                    void* c, int c_dtype, float alpha, const float* alpha_dev, const float* bias,
-                   int accumulate, qsync_stream_t stream) {
-    QSB_TRY(validate(a, b, m, n, k, 8));
+                   int accumulate, int layout, qsync_stream_t stream) {
+    QSB_REQUIRE(layout == 0 || layout == 2 || layout == 3, QSYNC_ERR_DOMAIN,
+                "operand layout must be 0 (K-major A/B), 2 (MN-major B) or 3 (MN-major A and B)");
+    // 16-byte TMA row pitch: the contiguous extent of each operand.
+    QSB_TRY(validate(a, b, m, n, k, (layout & 3) == 3 ? 1 : 8));
+    QSB_REQUIRE(!(layout & 1) || m % 8 == 0, QSYNC_ERR_DOMAIN, "MN-major A needs M % 8 == 0");
+    QSB_REQUIRE(!(layout & 2) || n % 8 == 0, QSYNC_ERR_DOMAIN, "MN-major B needs N % 8 == 0");
     QSB_REQUIRE(c != nullptr, QSYNC_ERR_VALIDATION, "GEMM needs an output");
     QSB_REQUIRE(ab_dtype == QSYNC_F16 || ab_dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
                 "FP16 GEMM operands must be F16 or BF16");
@@ -711,7 +768,7 @@ int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_
     p.accumulate = accumulate;
     const CUtensorMapDataType dt =
         ab_dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    return dispatch<false>(a, b, dt, p, to_stream(stream), g_force_bn);
+    return dispatch<false>(a, b, dt, p, to_stream(stream), g_force_bn, layout);
 }
 
 }  // extern "C"

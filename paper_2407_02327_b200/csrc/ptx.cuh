@@ -132,6 +132,16 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
            (static_cast<uint64_t>(2) << 61);
 }
 
+// Same, for an MN-major operand: K rows of 128 bytes (64 FP16 MN-elements) with
+// the 128B swizzle; MN blocks of 64 elements are `lbo_bytes` apart, groups of 8
+// K rows 1024 bytes apart (canonical ((T,8,m),(8,k)):((1,T,LBO),(8T,SBO))).
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint32_t lbo_bytes) {
+    return (static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4)) |
+           (static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16) |
+           (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+           (static_cast<uint64_t>(2) << 61);
+}
+
 }  // namespace ptx
 }  // namespace qsb
 

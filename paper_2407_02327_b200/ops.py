@@ -244,16 +244,22 @@ def gemm_s8(a: torch.Tensor, b: torch.Tensor, scale_a=None, scale_b=None, bias=N
 
 
 def gemm_f16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32, alpha: float = 1.0,
-             alpha_dev=None, bias=None, out=None, accumulate: bool = False) -> torch.Tensor:
-    """C = alpha * A B^T on tcgen05 kind::f16 (FP32 accumulators)."""
+             alpha_dev=None, bias=None, out=None, accumulate: bool = False,
+             a_mn: bool = False, b_mn: bool = False) -> torch.Tensor:
+    """C = alpha * A B^T on tcgen05 kind::f16 (FP32 accumulators).
+
+    A is [M, K] (or [K, M] with ``a_mn``); B is [N, K] (or [K, N] with ``b_mn``)."""
     _req(a, "a", (torch.float16, torch.bfloat16))
     _req(b, "b", (a.dtype,))
-    M, K = a.shape
-    N = b.shape[0]
+    if a_mn and not b_mn:
+        raise QsyncError(4, "domain: MN-major A requires MN-major B")
+    K, M = a.shape if a_mn else (a.shape[1], a.shape[0])
+    N = b.shape[1] if b_mn else b.shape[0]
     c = out if out is not None else torch.empty((M, N), device=a.device, dtype=out_dtype)
     ev = _timed("gemm_f16", 2.0 * M * N * K)
     call("qsync_gemm_f16", _ptr(a), _ptr(b), _DT[a.dtype], M, N, K, _ptr(c), _DT[c.dtype],
-         float(alpha), _ptr(alpha_dev), _ptr(bias), int(accumulate), _stream())
+         float(alpha), _ptr(alpha_dev), _ptr(bias), int(accumulate),
+         (1 if a_mn else 0) | (2 if b_mn else 0), _stream())
     if ev is not None:
         ev.record()
     return c

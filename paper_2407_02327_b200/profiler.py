@@ -98,9 +98,9 @@ def linear_memory_bytes(precision: str, M: int, N: int, K: int) -> int:
     W = N * K
     base = 4 * W * 4
     if precision == INT8:
-        return base + M * K * 1            # Xq^T (int8); W16^T is recomputed in backward
+        return base + M * K * 1            # Xq (int8); W16 is recomputed in backward
     if precision == FP16:
-        return base + M * K * 2 + W * 2    # X16^T, W16^T
+        return base + M * K * 2 + W * 2    # X16, W16
     return base + M * K * 4                # X
 
 

@@ -64,16 +64,16 @@ class _QConv(torch.autograd.Function):
         N, H, W, C, cout, P, Q, K = ctx.shapes
         kp = ctx.kp
         dy2 = dy.reshape(N * P * Q, cout).contiguous()
-        dy16, dy16_t, db = ops.cast_transpose(dy2, True, True, ctx.has_bias)
-        w2 = _pad_k(ctx.w_ref.detach().reshape(cout, K), kp)
-        _, w16_t, _ = ops.cast_transpose(w2, False, True, False)          # [kp, cout]
-        dcol = ops.gemm_f16(dy16, w16_t, out_dtype=torch.float32)         # dgrad columns
+        dy16, _, db = ops.cast_transpose(dy2, True, False, ctx.has_bias)
+        w16 = ops.cast(_pad_k(ctx.w_ref.detach().reshape(cout, K), kp), torch.float16)
+        # dgrad columns = dY16 W16 (W16 [Cout, kp] read as an MN-major B operand)
+        dcol = ops.gemm_f16(dy16, w16, out_dtype=torch.float32, b_mn=True)
         dx = ops.col2im(dcol, (N, H, W, C), R, S, stride, pad)
-        # wgrad: rebuild the FP16 column matrix from the saved (int8 / fp16) input.
+        # wgrad = dY16^T A16 (both read MN-major): rebuild the FP16 column matrix
+        # from the saved (int8 / fp16) input.
         A, _ = ops.im2col(xs_saved, R, S, stride, pad, ld=kp)
         A16 = A if A.dtype == torch.float16 else ops.cast(A, torch.float16)
-        _, A16_t, _ = ops.cast_transpose(A16, False, True, False)         # [kp, pad8(NPQ)]
-        dw2 = ops.gemm_f16(dy16_t, A16_t, out_dtype=torch.float32,
+        dw2 = ops.gemm_f16(dy16, A16, out_dtype=torch.float32, a_mn=True, b_mn=True,
                            alpha_dev=alpha if ctx.precision == INT8 else None)
         dw = dw2[:, :K].reshape(ctx.w_ref.shape)
         if ctx.x_dtype != torch.float32:

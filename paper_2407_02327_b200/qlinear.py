@@ -49,23 +49,26 @@ def _main_grad(p):
     return getattr(p, "main_grad", None) if p is not None else None
 
 
-def _fp16_backward(ctx, dy, x16_t, w16_t, alpha_dev):
-    """Shared FP16 backward (cost_mapper.cpp:13-15).  When the parameters carry a
-    ``main_grad`` (a slice of the flat FP32 gradient bucket), wgrad is ADDED into
-    it by the GEMM epilogue's TMA reduce-add and the bias gradient by the
-    cast-transpose column sums, and autograd receives None for them -- no
-    separate accumulate / zero kernels per parameter."""
+def _fp16_backward(ctx, dy, x16, w16, alpha_dev):
+    """Shared FP16 backward (cost_mapper.cpp:13-15) on row-major operands.
+
+    dgrad = dY16 W16 reads W16 [N_out, K_in] as an MN-major B operand and wgrad =
+    dY16^T X16 reads dY16 [M, N_out] and X16 [M, K_in] as MN-major A and B, so no
+    transposed copies are made.  When the parameters carry a ``main_grad`` (a
+    slice of the flat FP32 gradient bucket), wgrad is ADDED into it by the GEMM
+    epilogue's TMA reduce-add and the bias gradient by the cast kernel's column
+    sums; autograd then receives None for them."""
     w, b = ctx.w_ref, ctx.b_ref
     dy = dy.contiguous()
     mw, mb = _main_grad(w), _main_grad(b)
-    dy16, dy16_t, db = ops.cast_transpose(dy, True, True, b is not None and mb is None,
-                                          colsum_into=mb)
-    dx = ops.gemm_f16(dy16, w16_t, out_dtype=ctx.x_dtype)  # dgrad [M, K]
+    dy16, _, db = ops.cast_transpose(dy, True, False, b is not None and mb is None, colsum_into=mb)
+    dx = ops.gemm_f16(dy16, w16, out_dtype=ctx.x_dtype, b_mn=True)  # dgrad [M, K_in]
     if mw is not None:
-        ops.gemm_f16(dy16_t, x16_t, alpha_dev=alpha_dev, out=mw, accumulate=True)
+        ops.gemm_f16(dy16, x16, alpha_dev=alpha_dev, out=mw, accumulate=True, a_mn=True, b_mn=True)
         dw = None
     else:
-        dw = ops.gemm_f16(dy16_t, x16_t, out_dtype=torch.float32, alpha_dev=alpha_dev)  # wgrad
+        dw = ops.gemm_f16(dy16, x16, out_dtype=torch.float32, alpha_dev=alpha_dev, a_mn=True,
+                          b_mn=True)
     if mb is not None:
         db = None
     return dx, dw, db
@@ -77,27 +80,25 @@ class _QLinearInt8(torch.autograd.Function):
         _record(name, "act", x)
         _record(name, "w", w)
         ctx.name = name
-        # The INT8 op keeps only its 1-byte quantized activation (transposed, the
-        # K-major wgrad operand) for backward; FP16 views of it and of W are made
-        # in backward -- the "bp_cost" casts of the paper's cost model (PAPER.md:
-        # Fig. cost composition), which buy the INT8 op its memory saving.
-        xq, xs, xq_t8 = ops.quantize_per_tensor(x, transposed_i8=True)
+        # The INT8 op keeps only its 1-byte quantized activation for backward;
+        # the FP16 views of it and of W are made there -- the "bp_cost" casts
+        # of the paper's cost model, which buy the INT8 op its memory saving.
+        xq, xs, _ = ops.quantize_per_tensor(x)
         wq, ws, _ = ops.quantize_per_channel(w)
         _, y = ops.gemm_s8(xq, wq, xs, ws, b)
-        ctx.save_for_backward(xq_t8, xs)
+        ctx.save_for_backward(xq, xs)
         ctx.x_dtype = x.dtype
         ctx.w_ref, ctx.b_ref = w, b
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        xq_t8, xs = ctx.saved_tensors
+        xq, xs = ctx.saved_tensors
         _record(ctx.name, "grad", dy)
-        xq_t = ops.cast(xq_t8, torch.float16)                        # exact: int8 values
-        _, w_t16, _ = ops.cast_transpose(ctx.w_ref.detach(), False, True, False)
-        # wgrad = s_x * dY16^T X^ : the saved INT8 activation (as exact FP16
-        # integers) with the activation scale applied in the epilogue.
-        return _fp16_backward(ctx, dy, xq_t, w_t16, xs) + (None,)
+        x16 = ops.cast(xq, torch.float16)              # exact: the int8 grid values
+        w16 = ops.cast(ctx.w_ref.detach(), torch.float16)
+        # wgrad = s_x * dY16^T X^ (activation scale applied in the GEMM epilogue)
+        return _fp16_backward(ctx, dy, x16, w16, xs) + (None,)
 
 
 class _QLinearFp16(torch.autograd.Function):
@@ -106,23 +107,19 @@ class _QLinearFp16(torch.autograd.Function):
         _record(name, "act", x)
         _record(name, "w", w)
         ctx.name = name
-        if x.dtype == torch.float16:
-            x16 = x
-            _, x16_t, _ = ops.cast_transpose(x, False, True, False)
-        else:
-            x16, x16_t, _ = ops.cast_transpose(x, True, True, False)
-        w16, w16_t, _ = ops.cast_transpose(w, True, True, False)
+        x16 = x if x.dtype == torch.float16 else ops.cast(x, torch.float16)
+        w16 = ops.cast(w, torch.float16)
         y = ops.gemm_f16(x16, w16, out_dtype=torch.float16, bias=b)
-        ctx.save_for_backward(x16_t, w16_t)
+        ctx.save_for_backward(x16, w16)
         ctx.x_dtype = x.dtype
         ctx.w_ref, ctx.b_ref = w, b
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        x16_t, w16_t = ctx.saved_tensors
+        x16, w16 = ctx.saved_tensors
         _record(ctx.name, "grad", dy)
-        return _fp16_backward(ctx, dy, x16_t, w16_t, None) + (None,)
+        return _fp16_backward(ctx, dy, x16, w16, None) + (None,)
 
 
 class _Cast(torch.autograd.Function):

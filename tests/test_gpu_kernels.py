@@ -308,3 +308,34 @@ def test_gemm_f16_bias_alpha_dev_accumulate():
     ops.gemm_f16(a, b, alpha=2.0, alpha_dev=s, bias=bias, out=base, accumulate=True)
     ref = 0.5 * (a.double() @ b.double().T) + bias.double() + 1.0
     assert (base.double() - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("cta", [1, 2])
+@pytest.mark.parametrize("lay", ["b_mn", "ab_mn"])
+@pytest.mark.parametrize("mnk", [(128, 128, 64), (4096, 768, 2304), (2304, 768, 4096), (768, 3072, 300),
+                                 (200, 136, 77), (512, 512, 1000)])
+def test_gemm_f16_mn_major_operands(mnk, lay, cta):
+    """MN-major operands (no transposed copies): dgrad reads W [N_out, K_in] as B,
+    wgrad reads dY [M, N_out] and X [M, K_in] as A and B; K need not be padded."""
+    M, N, K = mnk
+    if lay == "b_mn" and K % 8:
+        pytest.skip("K-major A needs K % 8 == 0")
+    rng = np.random.default_rng(M + 3 * N + K)
+    a = torch.from_numpy(rng.normal(size=(M, K)).astype(np.float32)).half()
+    b = torch.from_numpy(rng.normal(size=(N, K)).astype(np.float32)).half()
+    ref = a.double() @ b.double().T
+    ops.force_cta(cta)
+    try:
+        if lay == "b_mn":
+            c = ops.gemm_f16(a.cuda(), b.t().contiguous().cuda(), b_mn=True)
+        else:
+            c = ops.gemm_f16(a.t().contiguous().cuda(), b.t().contiguous().cuda(), a_mn=True, b_mn=True)
+        base = torch.ones(M, N, device=DEV)
+        ops.gemm_f16(a.t().contiguous().cuda(), b.t().contiguous().cuda(), a_mn=True, b_mn=True,
+                     out=base, accumulate=True, alpha=0.5)
+    finally:
+        ops.force_cta(0)
+    err = (torch.from_numpy(_np(c)).double() - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item()
+    err2 = (torch.from_numpy(_np(base)).double() - (1.0 + 0.5 * ref)).abs().max().item()
+    assert err2 <= 1e-3 * (1.0 + 0.5 * ref).abs().max().item()
