@@ -140,6 +140,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch: everything above (barrier init, TMEM
+    // allocation, descriptor prefetch) may overlap the previous kernel's tail;
+    // no global memory is touched before the previous grid has completed.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // Leader-CTA addresses of the barriers the pair shares.
     const uint32_t full_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
     const uint32_t tempty_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
@@ -516,6 +520,7 @@ int g_force_splitk = 0;  // test/bench hook (qsync_gemm_force_splitk): 0 = heuri
 int g_splitk_wide = 0;   // accumulate GEMMs prefer BN=256 (bench hook)
 int g_force_cta = 0;     // test/bench hook (qsync_gemm_force_cta): 0 = cost model, 1, 2
 int g_debug_epi = 0;     // bench hook (qsync_gemm_debug_epilogue)
+int g_pdl = 1;           // programmatic dependent launch (qsync_gemm_set_pdl)
 
 template <bool kI8, int BN, int kCta, int kLay>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
@@ -582,25 +587,30 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     }
     const int64_t units = tiles * p.ksplit;
     const int grid = static_cast<int>(std::min<int64_t>(units, slots)) * kCta;
-    if (kCta == 1) {
-        k_gemm_tc<kI8, BN, 1, kLay><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, p);
-        return check_launch("k_gemm_tc");
-    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (g_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (kCta == 2) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 2;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     QSB_TRY(cuda_status(cudaLaunchKernelEx(&cfg, k_gemm_tc<kI8, BN, kCta, kLay>, ma, mb, mc, p),
-                        "cudaLaunchKernelEx(cluster 2)"));
-    return check_launch("k_gemm_tc<pair>");
+                        "cudaLaunchKernelEx(k_gemm_tc)"));
+    return check_launch("k_gemm_tc");
 }
 
 // Tile-shape cost model: per k-block a tile costs max(MMA cycles, operand bytes
@@ -700,6 +710,11 @@ extern "C" {
 int qsync_gemm_force_splitk(int ks) {
     QSB_REQUIRE(ks >= 0 && ks <= 64, QSYNC_ERR_DOMAIN, "split-K override must be in [0, 64]");
     g_force_splitk = ks;
+    return QSYNC_OK;
+}
+
+int qsync_gemm_set_pdl(int on) {
+    g_pdl = on ? 1 : 0;
     return QSYNC_OK;
 }
 
