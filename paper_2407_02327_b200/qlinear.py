@@ -45,6 +45,12 @@ def backward_precision(precision: str) -> str:
     return FP16 if precision == INT8 else precision
 
 
+# Optional side stream for weight gradients (TrainStep enables it): wgrad only
+# feeds the optimizer, so it runs concurrently with the rest of the backward
+# chain (dgrad of the next layers); TrainStep joins it before the all-reduce.
+WGRAD_STREAM: torch.cuda.Stream | None = None
+
+
 def _main_grad(p):
     return getattr(p, "main_grad", None) if p is not None else None
 
@@ -63,7 +69,17 @@ def _fp16_backward(ctx, dy, x16, w16, alpha_dev):
     mw, mb = _main_grad(w), _main_grad(b)
     dy16, _, db = ops.cast_transpose(dy, True, False, b is not None and mb is None, colsum_into=mb)
     dx = ops.gemm_f16(dy16, w16, out_dtype=ctx.x_dtype, b_mn=True)  # dgrad [M, K_in]
-    if mw is not None:
+    if mw is not None and WGRAD_STREAM is not None:
+        cur = torch.cuda.current_stream()
+        WGRAD_STREAM.wait_stream(cur)
+        with torch.cuda.stream(WGRAD_STREAM):
+            ops.gemm_f16(dy16, x16, alpha_dev=alpha_dev, out=mw, accumulate=True, a_mn=True,
+                         b_mn=True)
+        for t in (dy16, x16, alpha_dev):
+            if t is not None:
+                t.record_stream(WGRAD_STREAM)
+        dw = None
+    elif mw is not None:
         ops.gemm_f16(dy16, x16, alpha_dev=alpha_dev, out=mw, accumulate=True, a_mn=True, b_mn=True)
         dw = None
     else:

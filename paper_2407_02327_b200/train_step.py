@@ -26,6 +26,7 @@ import torch
 import torch.nn.functional as F
 from flash_attn import flash_attn_qkvpacked_func
 
+from . import qlinear as _ql
 from .glue import AddLayerNorm
 from .qlinear import FP16, FP32, INT8, QLinear, cast
 
@@ -210,7 +211,7 @@ class TrainStep:
     + AdamW on FP32 master weights.  Optionally captured into a CUDA graph."""
 
     def __init__(self, model: BertEncoderStack, batch: int, world: int = 1, lr: float = 1e-4,
-                 graph: bool = True):
+                 graph: bool = True, overlap_wgrad: bool = True):
         self.model = model
         self.world = world
         cfg = model.cfg
@@ -223,11 +224,20 @@ class TrainStep:
         self.use_graph = graph
         self.graph = None
         self.loss = None
+        self.wgrad_stream = torch.cuda.Stream() if overlap_wgrad else None
 
     def _body(self):
         self.grads.zero()
         loss = self.model(self.tokens, self.labels)
-        loss.backward()
+        _ql.WGRAD_STREAM = self.wgrad_stream
+        if self.wgrad_stream is not None:
+            self.wgrad_stream.wait_stream(torch.cuda.current_stream())  # after the zeroing
+        try:
+            loss.backward()
+        finally:
+            _ql.WGRAD_STREAM = None
+        if self.wgrad_stream is not None:
+            torch.cuda.current_stream().wait_stream(self.wgrad_stream)  # join before the all-reduce
         self.grads.allreduce(self.world)
         self.opt.step()
         return loss.detach()
