@@ -214,6 +214,81 @@ int qsync_layernorm_bwd(const float* dy, const float* s, const float* mean, cons
                         const float* gamma, int64_t rows, int64_t cols, float* dx, float* dgamma,
                         float* dbeta, qsync_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Fused encoder-layer glue (the operators between two planned Linears fold
+ * into the kernels that produce / consume the planned operand format).
+ * ------------------------------------------------------------------------- */
+enum qsync_act { QSYNC_ACT_NONE = 0, QSYNC_ACT_GELU = 1 };
+
+/* LayerNorm forward that also emits what the NEXT planned Linear consumes:
+ * y16 (optional) = FP16(y) for an FP16 op; y_absmax (optional, device float,
+ * overwritten) = absmax(y) for an INT8 op, so its per-tensor quantizer is one
+ * pass (qsync_quantize_act).  Same y / s / mean / rstd as qsync_layernorm_fwd. */
+int qsync_layernorm_fwd_ex(const float* a, const void* b, int b_dtype, const float* gamma,
+                           const float* beta, int64_t rows, int64_t cols, float eps, float* s_out,
+                           float* y, float* mean, float* rstd, uint16_t* y16, float* y_absmax,
+                           qsync_stream_t stream);
+/* LayerNorm backward that also emits the incoming gradient of the Linear that
+ * produced the residual branch: dx16 (optional) = FP16(dx), the FP16 backward
+ * format (cost_mapper.cpp:13-15), and dcolsum (optional) += sum_rows dx, that
+ * Linear's bias gradient. */
+int qsync_layernorm_bwd_ex(const float* dy, const float* s, const float* mean, const float* rstd,
+                           const float* gamma, int64_t rows, int64_t cols, float* dx, float* dgamma,
+                           float* dbeta, uint16_t* dx16, float* dcolsum, qsync_stream_t stream);
+
+/* absmax of act(x) over n values (device float, overwritten). */
+int qsync_absmax_act(const void* x, int dtype, int64_t n, int act, float* absmax,
+                     qsync_stream_t stream);
+/* Per-tensor RNE quantize of act(x) with s = absmax/127 from a device absmax
+ * computed upstream (LayerNorm epilogue / qsync_absmax_act); *scale_out = s. */
+int qsync_quantize_act(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,
+                       float* scale_out, qsync_stream_t stream);
+/* out = act(x) cast to dst_dtype (F32/F16 -> F32/F16). */
+int qsync_act_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64_t n, int act,
+                   qsync_stream_t stream);
+/* Backward through act and into a planned op's FP16 backward format:
+ * g = dy * act'(h) (act NONE: g = dy; h may be NULL), out (optional) = g as
+ * out_dtype, colsum (optional) += sum_rows g (the bias gradient).  dy, h
+ * [rows, cols] F32/F16. */
+int qsync_act_bwd_colsum(const void* dy, int dy_dtype, const void* h, int h_dtype, int64_t rows,
+                         int64_t cols, int act, void* out, int out_dtype, float* colsum,
+                         qsync_stream_t stream);
+
+/* INT8 GEMM with the dequant epilogue written as c_dtype (F32 = the
+ * graph.hpp:38-40 format; F16 when the consumer is an FP16 kernel, e.g. the
+ * attention core -- the same FP32 value rounded once, so it equals
+ * qsync_gemm_s8 followed by qsync_cast). */
+int qsync_gemm_s8_ex(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k, void* c,
+                     int c_dtype, const float* scale_a, const float* scale_b, int b_per_channel,
+                     const float* bias, qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Optimizer on FP32 master weights fused with the per-step weight preparation
+ * of the planned kernels: AdamW (decoupled weight decay, bias-corrected, step
+ * counter on the device) over a table of parameter segments, each optionally
+ * emitting w16 = FP16(W) and/or wq = per-row INT8 quantization of W with its
+ * scales (the operands the next step's INT8 / FP16 Linears read).  With
+ * lr_scale = 0 ... no: `update` = 0 only (re)computes the prepared copies.
+ * ------------------------------------------------------------------------- */
+typedef struct qsync_adamw_seg {
+    float* p;          /* FP32 master weights [rows, cols] */
+    const float* g;    /* FP32 gradient (same layout) */
+    float* m;          /* first moment */
+    float* v;          /* second moment */
+    uint16_t* w16;     /* optional FP16 copy */
+    int8_t* wq;        /* optional per-row INT8 copy */
+    float* wscale;     /* [rows] scales of wq */
+    int64_t rows;
+    int64_t cols;
+} qsync_adamw_seg;
+/* segs: DEVICE array of nseg segments; seg_row_start: DEVICE int64[nseg + 1]
+ * prefix sums of the segments' rows (total_rows = last entry); step: device
+ * int64 counter, incremented once per call with update != 0 (the bias
+ * corrections use the incremented value, as torch.optim.AdamW). */
+int qsync_adamw_step(const qsync_adamw_seg* segs, int nseg, const int64_t* seg_row_start,
+                     int64_t total_rows, int64_t* step, float lr, float beta1, float beta2,
+                     float eps, float weight_decay, int update, qsync_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@ ERROR_KINDS = ["graph-cycle", "validation", "reference", "domain", "missing-prof
                "topology", "enumeration-limit", "infeasible", "io", "internal"]
 
 F32, F16, BF16, I8, I32 = 0, 1, 2, 3, 4
+ACT_NONE, ACT_GELU = 0, 1
 
 
 class QsyncError(RuntimeError):
@@ -66,6 +67,14 @@ SIGNATURES = {
     "qsync_conv_out_size": [_i64, _i64, _int, _int, _int, _int, _int, _int, _int, _int, _p, _p],
     "qsync_im2col": [_p, _int, _i64, _i64, _i64, _i64] + [_int] * 8 + [_p, _i64, _p],
     "qsync_col2im": [_p, _int, _i64, _i64, _i64, _i64] + [_int] * 8 + [_i64, _p, _p],
+    "qsync_layernorm_fwd_ex": [_p, _p, _int, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p, _p],
+    "qsync_layernorm_bwd_ex": [_p, _p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p],
+    "qsync_absmax_act": [_p, _int, _i64, _int, _p, _p],
+    "qsync_quantize_act": [_p, _int, _i64, _int, _p, _p, _p, _p],
+    "qsync_act_cast": [_p, _int, _p, _int, _i64, _int, _p],
+    "qsync_act_bwd_colsum": [_p, _int, _p, _int, _i64, _i64, _int, _p, _int, _p, _p],
+    "qsync_gemm_s8_ex": [_p, _p, _i64, _i64, _i64, _p, _int, _p, _p, _int, _p, _p],
+    "qsync_adamw_step": [_p, _int, _p, _i64, _p, _f32, _f32, _f32, _f32, _f32, _int, _p],
     # non-header helpers
     "qsync_gemm_force_tile_n": [_int],
     "qsync_gemm_force_splitk": [_int],

@@ -74,6 +74,20 @@ __device__ __forceinline__ int quant_rne(float x, float s) {
     return static_cast<int>(r);
 }
 
+// GELU (erf form, BERT's activation) and its derivative, every operation
+// rounded explicitly so that all kernels that evaluate it agree bit for bit:
+//   gelu(x)  = 0.5 x (1 + erf(x / sqrt 2))
+//   gelu'(x) = 0.5 (1 + erf(x / sqrt 2)) + x exp(-x^2 / 2) / sqrt(2 pi)
+__device__ __forceinline__ float gelu_erf(float x) {
+    const float e = erff(__fmul_rn(x, 0.70710678118654752f));
+    return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, e));
+}
+__device__ __forceinline__ float gelu_erf_grad(float x) {
+    const float cdf = __fmul_rn(0.5f, __fadd_rn(1.0f, erff(__fmul_rn(x, 0.70710678118654752f))));
+    const float pdf = __fmul_rn(expf(__fmul_rn(-0.5f, __fmul_rn(x, x))), 0.39894228040143268f);
+    return __fadd_rn(cdf, __fmul_rn(x, pdf));
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -735,6 +735,28 @@ int qsync_gemm_force_tile_n(int bn) {
     return QSYNC_OK;
 }
 
+int qsync_gemm_s8_ex(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k, void* c,
+                     int c_dtype, const float* scale_a, const float* scale_b, int b_per_channel,
+                     const float* bias, qsync_stream_t stream) {
+    QSB_TRY(validate(a, b, m, n, k, 16));
+    QSB_REQUIRE(c != nullptr, QSYNC_ERR_VALIDATION, "GEMM needs an output");
+    QSB_REQUIRE(c_dtype == QSYNC_F32 || c_dtype == QSYNC_F16 || c_dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
+                "INT8 GEMM epilogue output must be F32, F16 or BF16");
+    QSB_REQUIRE(scale_a && scale_b, QSYNC_ERR_VALIDATION, "the dequant epilogue needs scale_a and scale_b");
+    EpiParams p{};
+    p.M = m;
+    p.N = n;
+    p.K = k;
+    p.c = c;
+    p.c_dtype = c_dtype;
+    p.scale_a = scale_a;
+    p.scale_b = scale_b;
+    p.b_per_channel = b_per_channel;
+    p.bias = bias;
+    p.alpha = 1.0f;
+    return dispatch<true>(a, b, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, to_stream(stream), g_force_bn);
+}
+
 int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k,
                   int32_t* c_i32, float* c_f32, const float* scale_a, const float* scale_b,
                   int b_per_channel, const float* bias, qsync_stream_t stream) {

@@ -30,8 +30,11 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
                                                 const float* __restrict__ beta, int64_t rows,
                                                 int cols, float eps, float* __restrict__ s_out,
                                                 float* __restrict__ y, float* __restrict__ mean_out,
-                                                float* __restrict__ rstd_out) {
+                                                float* __restrict__ rstd_out,
+                                                __half* __restrict__ y16,
+                                                unsigned* __restrict__ y_absmax) {
     const int lane = threadIdx.x & 31;
+    float amax = 0.0f;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     float4 g[NV], be[NV];
 #pragma unroll
@@ -80,11 +83,26 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
             o.z = (v[i].z - mean) * rstd * g[i].z + be[i].z;
             o.w = (v[i].w - mean) * rstd * g[i].w + be[i].w;
             *reinterpret_cast<float4*>(y + off) = o;
+            if (y16) {
+                uint2 h;
+                h.x = __half_as_ushort(__float2half_rn(o.x)) |
+                      (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(o.y))) << 16);
+                h.y = __half_as_ushort(__float2half_rn(o.z)) |
+                      (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(o.w))) << 16);
+                *reinterpret_cast<uint2*>(y16 + off) = h;
+            }
+            amax = fmaxf(amax, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
         }
         if (lane == 0) {
             mean_out[row] = mean;
             rstd_out[row] = rstd;
         }
+    }
+    if (y_absmax) {
+        // absmax of y for the next INT8 op's per-tensor scale: warp max, then
+        // one atomicMax per warp on the float bits (order-independent).
+        amax = warp_max(amax);
+        if (lane == 0 && amax > 0.0f) atomicMax(y_absmax, __float_as_uint(amax));
     }
 }
 
@@ -96,16 +114,19 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
                                                 const float* __restrict__ gamma, int64_t rows,
                                                 int cols, float* __restrict__ dx,
                                                 float* __restrict__ dgamma,
-                                                float* __restrict__ dbeta) {
+                                                float* __restrict__ dbeta,
+                                                __half* __restrict__ dx16,
+                                                float* __restrict__ dcol) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    float4 g[NV], acc_g[NV], acc_b[NV];
+    float4 g[NV], acc_g[NV], acc_b[NV], acc_c[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         g[i] = reinterpret_cast<const float4*>(gamma)[lane + 32 * i];
         acc_g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         acc_b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        acc_c[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const float inv_n = 1.0f / static_cast<float>(cols);
     for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; row < rows; row += warps) {
@@ -137,6 +158,15 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
             o.z = rstd * (gy[i].z - m1 - xh[i].z * m2);
             o.w = rstd * (gy[i].w - m1 - xh[i].w * m2);
             *reinterpret_cast<float4*>(dx + off) = o;
+            if (dx16) {
+                uint2 h;
+                h.x = __half_as_ushort(__float2half_rn(o.x)) |
+                      (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(o.y))) << 16);
+                h.y = __half_as_ushort(__float2half_rn(o.z)) |
+                      (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(o.w))) << 16);
+                *reinterpret_cast<uint2*>(dx16 + off) = h;
+            }
+            acc_c[i].x += o.x; acc_c[i].y += o.y; acc_c[i].z += o.z; acc_c[i].w += o.w;
         }
     }
     // Block-reduce the per-warp column partials (gamma, then beta through the
@@ -144,11 +174,12 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
     __shared__ float red[8][1024 + 4];
     const int nw = blockDim.x >> 5;
 #pragma unroll
-    for (int pass = 0; pass < 2; ++pass) {
-        float* outp = pass == 0 ? dgamma : dbeta;
+    for (int pass = 0; pass < 3; ++pass) {
+        float* outp = pass == 0 ? dgamma : (pass == 1 ? dbeta : dcol);
+        if (pass == 2 && !dcol) break;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
-            const float4 v = pass == 0 ? acc_g[i] : acc_b[i];
+            const float4 v = pass == 0 ? acc_g[i] : (pass == 1 ? acc_b[i] : acc_c[i]);
             const int c = 4 * (lane + 32 * i);
             red[warp][c] = v.x; red[warp][c + 1] = v.y; red[warp][c + 2] = v.z; red[warp][c + 3] = v.w;
         }
@@ -165,23 +196,29 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
 template <int NV>
 int ln_fwd_nv(const float* a, const void* b, int b_dtype, const float* gamma, const float* beta,
               int64_t rows, int cols, float eps, float* s_out, float* y, float* mean, float* rstd,
-              cudaStream_t st) {
+              uint16_t* y16, float* y_absmax, cudaStream_t st) {
+    if (y_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(y_absmax, 0, sizeof(float), st), "memset"));
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 8LL));
     if (b_dtype == QSYNC_F16)
         k_ln_fwd<NV, QSYNC_F16><<<grid, 256, 0, st>>>(a, static_cast<const __half*>(b), gamma, beta,
-                                                      rows, cols, eps, s_out, y, mean, rstd);
+                                                      rows, cols, eps, s_out, y, mean, rstd,
+                                                      reinterpret_cast<__half*>(y16),
+                                                      reinterpret_cast<unsigned*>(y_absmax));
     else
         k_ln_fwd<NV, QSYNC_F32><<<grid, 256, 0, st>>>(a, static_cast<const float*>(b), gamma, beta,
-                                                      rows, cols, eps, s_out, y, mean, rstd);
+                                                      rows, cols, eps, s_out, y, mean, rstd,
+                                                      reinterpret_cast<__half*>(y16),
+                                                      reinterpret_cast<unsigned*>(y_absmax));
     return check_launch("k_ln_fwd");
 }
 
 template <int NV>
 int ln_bwd_nv(const float* dy, const float* s, const float* mean, const float* rstd,
               const float* gamma, int64_t rows, int cols, float* dx, float* dgamma, float* dbeta,
-              cudaStream_t st) {
+              uint16_t* dx16, float* dcol, cudaStream_t st) {
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 2LL));
-    k_ln_bwd<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta);
+    k_ln_bwd<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
+                                        reinterpret_cast<__half*>(dx16), dcol);
     return check_launch("k_ln_bwd");
 }
 
@@ -192,9 +229,10 @@ using namespace qsb;
 
 extern "C" {
 
-int qsync_layernorm_fwd(const float* a, const void* b, int b_dtype, const float* gamma,
-                        const float* beta, int64_t rows, int64_t cols, float eps, float* s_out,
-                        float* y, float* mean, float* rstd, qsync_stream_t stream) {
+int qsync_layernorm_fwd_ex(const float* a, const void* b, int b_dtype, const float* gamma,
+                           const float* beta, int64_t rows, int64_t cols, float eps, float* s_out,
+                           float* y, float* mean, float* rstd, uint16_t* y16, float* y_absmax,
+                           qsync_stream_t stream) {
     QSB_REQUIRE(rows >= 0, QSYNC_ERR_DOMAIN, "negative row count");
     QSB_REQUIRE(cols % 128 == 0 && cols >= 128 && cols <= 1024, QSYNC_ERR_DOMAIN,
                 "layernorm supports 128 <= cols <= 1024, cols % 128 == 0");
@@ -204,20 +242,20 @@ int qsync_layernorm_fwd(const float* a, const void* b, int b_dtype, const float*
     cudaStream_t st = to_stream(stream);
     const int c = static_cast<int>(cols);
     switch (c / 128) {
-        case 1: return ln_fwd_nv<1>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
-        case 2: return ln_fwd_nv<2>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
-        case 3: return ln_fwd_nv<3>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
-        case 4: return ln_fwd_nv<4>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
-        case 5: return ln_fwd_nv<5>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
-        case 6: return ln_fwd_nv<6>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
-        case 7: return ln_fwd_nv<7>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
-        default: return ln_fwd_nv<8>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, st);
+        case 1: return ln_fwd_nv<1>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        case 2: return ln_fwd_nv<2>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        case 3: return ln_fwd_nv<3>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        case 4: return ln_fwd_nv<4>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        case 5: return ln_fwd_nv<5>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        case 6: return ln_fwd_nv<6>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        case 7: return ln_fwd_nv<7>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        default: return ln_fwd_nv<8>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
     }
 }
 
-int qsync_layernorm_bwd(const float* dy, const float* s, const float* mean, const float* rstd,
-                        const float* gamma, int64_t rows, int64_t cols, float* dx, float* dgamma,
-                        float* dbeta, qsync_stream_t stream) {
+int qsync_layernorm_bwd_ex(const float* dy, const float* s, const float* mean, const float* rstd,
+                           const float* gamma, int64_t rows, int64_t cols, float* dx, float* dgamma,
+                           float* dbeta, uint16_t* dx16, float* dcolsum, qsync_stream_t stream) {
     QSB_REQUIRE(rows >= 0, QSYNC_ERR_DOMAIN, "negative row count");
     QSB_REQUIRE(cols % 128 == 0 && cols >= 128 && cols <= 1024, QSYNC_ERR_DOMAIN,
                 "layernorm supports 128 <= cols <= 1024, cols % 128 == 0");
@@ -225,15 +263,29 @@ int qsync_layernorm_bwd(const float* dy, const float* s, const float* mean, cons
     cudaStream_t st = to_stream(stream);
     const int c = static_cast<int>(cols);
     switch (c / 128) {
-        case 1: return ln_bwd_nv<1>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
-        case 2: return ln_bwd_nv<2>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
-        case 3: return ln_bwd_nv<3>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
-        case 4: return ln_bwd_nv<4>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
-        case 5: return ln_bwd_nv<5>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
-        case 6: return ln_bwd_nv<6>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
-        case 7: return ln_bwd_nv<7>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
-        default: return ln_bwd_nv<8>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, st);
+        case 1: return ln_bwd_nv<1>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, dx16, dcolsum, st);
+        case 2: return ln_bwd_nv<2>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, dx16, dcolsum, st);
+        case 3: return ln_bwd_nv<3>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, dx16, dcolsum, st);
+        case 4: return ln_bwd_nv<4>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, dx16, dcolsum, st);
+        case 5: return ln_bwd_nv<5>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, dx16, dcolsum, st);
+        case 6: return ln_bwd_nv<6>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, dx16, dcolsum, st);
+        case 7: return ln_bwd_nv<7>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, dx16, dcolsum, st);
+        default: return ln_bwd_nv<8>(dy, s, mean, rstd, gamma, rows, c, dx, dgamma, dbeta, dx16, dcolsum, st);
     }
+}
+
+int qsync_layernorm_fwd(const float* a, const void* b, int b_dtype, const float* gamma,
+                        const float* beta, int64_t rows, int64_t cols, float eps, float* s_out,
+                        float* y, float* mean, float* rstd, qsync_stream_t stream) {
+    return qsync_layernorm_fwd_ex(a, b, b_dtype, gamma, beta, rows, cols, eps, s_out, y, mean, rstd,
+                                  nullptr, nullptr, stream);
+}
+
+int qsync_layernorm_bwd(const float* dy, const float* s, const float* mean, const float* rstd,
+                        const float* gamma, int64_t rows, int64_t cols, float* dx, float* dgamma,
+                        float* dbeta, qsync_stream_t stream) {
+    return qsync_layernorm_bwd_ex(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta, nullptr,
+                                  nullptr, stream);
 }
 
 }  // extern "C"

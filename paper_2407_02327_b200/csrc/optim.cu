@@ -1,0 +1,185 @@
+// optim.cu -- AdamW on the FP32 master weights fused with the per-step weight
+// preparation of the planned kernels.
+//
+// Every planned Linear reads its weight in the plan's format each step: an
+// INT8 op per-channel INT8 W^ + scales and FP16 W for its
+// FP16 dgrad (cost_mapper.cpp:13-15), an FP16 op FP16 W.  Those copies are a
+// pure function of the master weights, which change only in the optimizer, so
+// the optimizer kernel that has just produced row r of W also emits row r's
+// copies: the weights are read once per step instead of once by the optimizer
+// and again by each quantize / cast kernel.
+//
+// One warp per weight row (row = output channel; 1-D parameters are one row).
+// Pass 1 updates p, m, v (16-byte vectors) and tracks the row absmax of the
+// new p; pass 2 re-reads the row (L2-resident, just written) and writes the
+// FP16 copy and the RNE INT8 copy with s = absmax/127 -- the same scale rule
+// and rounding as k_quant_rows, so the prepared copy is bit-identical to
+// qsync_quantize_per_channel of the updated weights.
+//
+// AdamW exactly as torch.optim.AdamW (decoupled decay):
+//   p *= 1 - lr*wd;  m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2
+//   p -= (lr / (1 - b1^t)) * m / (sqrt(v) / sqrt(1 - b2^t) + eps)
+// with t read from a device counter (graph-capturable), incremented by a
+// one-thread kernel after the update.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace qsb {
+namespace {
+
+constexpr int kWarps = 8;
+
+__device__ __forceinline__ int find_seg(const int64_t* __restrict__ start, int nseg, int64_t row) {
+    int lo = 0, hi = nseg - 1;  // largest s with start[s] <= row
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (start[mid] <= row) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+struct AdamCoef {
+    float lr, b1, b2, eps, decay;  // decay = 1 - lr*wd
+    float step_size, inv_bc2_sqrt;
+};
+
+__device__ __forceinline__ float adam1(float p, float g, float& m, float& v, const AdamCoef& c) {
+    p = p * c.decay;
+    m = c.b1 * m + (1.0f - c.b1) * g;
+    v = c.b2 * v + (1.0f - c.b2) * g * g;
+    const float denom = sqrtf(v) * c.inv_bc2_sqrt + c.eps;
+    return p - c.step_size * (m / denom);
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __restrict__ segs, int nseg,
+                                                       const int64_t* __restrict__ seg_start,
+                                                       int64_t total_rows, const int64_t* __restrict__ step,
+                                                       float lr, float b1, float b2, float eps, float wd,
+                                                       int update) {
+    const int lane = threadIdx.x & 31;
+    AdamCoef c{};
+    if (update) {
+        const float t = static_cast<float>(*step + 1);
+        const float bc1 = 1.0f - powf(b1, t);
+        const float bc2 = 1.0f - powf(b2, t);
+        c.lr = lr;
+        c.b1 = b1;
+        c.b2 = b2;
+        c.eps = eps;
+        c.decay = 1.0f - lr * wd;
+        c.step_size = lr / bc1;
+        c.inv_bc2_sqrt = 1.0f / sqrtf(bc2);
+    }
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+    for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5); row < total_rows;
+         row += nwarps) {
+        const int s = find_seg(seg_start, nseg, row);
+        const qsync_adamw_seg sg = segs[s];
+        const int64_t r = row - seg_start[s];
+        const int64_t cols = sg.cols;
+        float* p = sg.p + r * cols;
+        const bool vec = (cols % 4 == 0) && ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(sg.g) |
+                                              reinterpret_cast<uintptr_t>(sg.m) | reinterpret_cast<uintptr_t>(sg.v)) &
+                                             15u) == 0;
+        float amax = 0.0f;
+        if (update) {
+            const float* g = sg.g + r * cols;
+            float* m = sg.m + r * cols;
+            float* v = sg.v + r * cols;
+            if (vec) {
+                for (int64_t k = lane; k < cols / 4; k += 32) {
+                    float4 pv = reinterpret_cast<float4*>(p)[k];
+                    const float4 gv = reinterpret_cast<const float4*>(g)[k];
+                    float4 mv = reinterpret_cast<float4*>(m)[k];
+                    float4 vv = reinterpret_cast<float4*>(v)[k];
+                    pv.x = adam1(pv.x, gv.x, mv.x, vv.x, c);
+                    pv.y = adam1(pv.y, gv.y, mv.y, vv.y, c);
+                    pv.z = adam1(pv.z, gv.z, mv.z, vv.z, c);
+                    pv.w = adam1(pv.w, gv.w, mv.w, vv.w, c);
+                    reinterpret_cast<float4*>(p)[k] = pv;
+                    reinterpret_cast<float4*>(m)[k] = mv;
+                    reinterpret_cast<float4*>(v)[k] = vv;
+                    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(pv.x), fabsf(pv.y)), fmaxf(fabsf(pv.z), fabsf(pv.w))));
+                }
+            } else {
+                for (int64_t k = lane; k < cols; k += 32) {
+                    float mm = m[k], vv = v[k];
+                    const float pn = adam1(p[k], g[k], mm, vv, c);
+                    p[k] = pn;
+                    m[k] = mm;
+                    v[k] = vv;
+                    amax = fmaxf(amax, fabsf(pn));
+                }
+            }
+        } else if (sg.wq) {
+            for (int64_t k = lane; k < cols; k += 32) amax = fmaxf(amax, fabsf(p[k]));
+        }
+        if (!sg.w16 && !sg.wq) continue;
+        __syncwarp();  // this warp's p stores are visible to its own re-reads
+        amax = warp_max(amax);
+        const float sc = scale_from_absmax(amax);
+        if (sg.wq && lane == 0) sg.wscale[r] = sc;
+        uint16_t* w16 = sg.w16 ? sg.w16 + r * cols : nullptr;
+        int8_t* wq = sg.wq ? sg.wq + r * cols : nullptr;
+        const bool vec2 = vec && (!w16 || (reinterpret_cast<uintptr_t>(w16) & 7u) == 0) &&
+                          (!wq || (reinterpret_cast<uintptr_t>(wq) & 3u) == 0);
+        if (vec2) {
+            for (int64_t k = lane; k < cols / 4; k += 32) {
+                const float4 pv = reinterpret_cast<const float4*>(p)[k];
+                if (w16) {
+                    uint2 h;
+                    h.x = __half_as_ushort(__float2half_rn(pv.x)) |
+                          (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(pv.y))) << 16);
+                    h.y = __half_as_ushort(__float2half_rn(pv.z)) |
+                          (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(pv.w))) << 16);
+                    reinterpret_cast<uint2*>(w16)[k] = h;
+                }
+                if (wq) {
+                    reinterpret_cast<uint32_t*>(wq)[k] =
+                        static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.x, sc))) |
+                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.y, sc))) << 8) |
+                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.z, sc))) << 16) |
+                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.w, sc))) << 24);
+                }
+            }
+        } else {
+            for (int64_t k = lane; k < cols; k += 32) {
+                const float pv = p[k];
+                if (w16) w16[k] = __half_as_ushort(__float2half_rn(pv));
+                if (wq) wq[k] = static_cast<int8_t>(quant_rne(pv, sc));
+            }
+        }
+    }
+}
+
+__global__ void k_step_inc(int64_t* step) { *step += 1; }
+
+}  // namespace
+}  // namespace qsb
+
+using namespace qsb;
+
+extern "C" {
+
+int qsync_adamw_step(const qsync_adamw_seg* segs, int nseg, const int64_t* seg_row_start,
+                     int64_t total_rows, int64_t* step, float lr, float beta1, float beta2, float eps,
+                     float weight_decay, int update, qsync_stream_t stream) {
+    QSB_REQUIRE(segs && seg_row_start && nseg > 0, QSYNC_ERR_VALIDATION, "segment table is required");
+    QSB_REQUIRE(total_rows >= 0, QSYNC_ERR_DOMAIN, "negative row count");
+    QSB_REQUIRE(!update || step != nullptr, QSYNC_ERR_VALIDATION, "step counter is required");
+    QSB_REQUIRE(!update || (beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f),
+                QSYNC_ERR_DOMAIN, "AdamW needs 0 <= beta < 1 and eps > 0");
+    if (total_rows == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int grid = static_cast<int>(std::min<int64_t>((total_rows + kWarps - 1) / kWarps, sm_count() * 16LL));
+    k_adamw<<<grid, kWarps * 32, 0, st>>>(segs, nseg, seg_row_start, total_rows, step, lr, beta1, beta2, eps,
+                                          weight_decay, update);
+    QSB_TRY(check_launch("k_adamw"));
+    if (!update) return QSYNC_OK;
+    k_step_inc<<<1, 1, 0, st>>>(step);
+    return check_launch("k_step_inc");
+}
+
+}  // extern "C"

@@ -8,6 +8,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "vec.cuh"
 
 namespace qsb {
 
@@ -15,62 +16,13 @@ namespace {
 
 constexpr int kThreads = 512;
 
-__device__ __forceinline__ uint4 ld_stream(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-
-// Unpack a 16-byte vector of DT into floats (4 for F32, 8 for F16/BF16).
-template <int DT>
-struct Vec;
-template <>
-struct Vec<QSYNC_F32> {
-    static constexpr int N = 4;
-    __device__ static void unpack(uint4 r, float* f) {
-        f[0] = __uint_as_float(r.x);
-        f[1] = __uint_as_float(r.y);
-        f[2] = __uint_as_float(r.z);
-        f[3] = __uint_as_float(r.w);
-    }
-};
-template <>
-struct Vec<QSYNC_F16> {
-    static constexpr int N = 8;
-    __device__ static void unpack(uint4 r, float* f) {
-        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
-            float2 v = __half22float2(h);
-            f[2 * i] = v.x;
-            f[2 * i + 1] = v.y;
-        }
-    }
-};
-template <>
-struct Vec<QSYNC_BF16> {
-    static constexpr int N = 8;
-    __device__ static void unpack(uint4 r, float* f) {
-        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-            float2 v = __bfloat1622float2(h);
-            f[2 * i] = v.x;
-            f[2 * i + 1] = v.y;
-        }
-    }
-};
-
-__host__ __device__ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm = 4) {
-    int64_t want = (work_items + per_block - 1) / per_block;
-    int64_t cap = static_cast<int64_t>(sm_count()) * max_blocks_per_sm;
-    return static_cast<int>(std::max<int64_t>(1, std::min(want, cap)));
+// Fused prologue activation of the streaming kernels: ACT 0 = identity,
+// ACT 1 = GELU (the FF1 -> FF2 activation of an encoder layer, so the
+// quantizer / cast of the FF2 input reads the pre-activation directly).
+template <int ACT>
+__device__ __forceinline__ float act_f(float v) {
+    if constexpr (ACT == 1) return gelu_erf(v);
+    return v;
 }
 
 // ---------------------------------------------------------------------------
@@ -79,7 +31,7 @@ int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm = 4) {
 // (valid ordering for non-negative floats; max is order-independent, so the
 // result is deterministic).
 // ---------------------------------------------------------------------------
-template <int DT>
+template <int DT, int ACT = 0>
 __global__ void __launch_bounds__(kThreads) k_absmax(const typename Elem<DT>::T* __restrict__ x,
                                                      int64_t n, unsigned* __restrict__ out,
                                                      int vec_ok) {
@@ -102,18 +54,18 @@ __global__ void __launch_bounds__(kThreads) k_absmax(const typename Elem<DT>::T*
                 float f[V::N];
                 V::unpack(r[u], f);
 #pragma unroll
-                for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(f[j]));
+                for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(act_f<ACT>(f[j])));
             }
         }
         for (; i < nv; i += stride) {
             float f[V::N];
             V::unpack(ld_stream(xv + i), f);
 #pragma unroll
-            for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(f[j]));
+            for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(act_f<ACT>(f[j])));
         }
         done = nv * V::N;
     }
-    for (int64_t i = done + tid; i < n; i += stride) m = fmaxf(m, fabsf(Elem<DT>::f(x[i])));
+    for (int64_t i = done + tid; i < n; i += stride) m = fmaxf(m, fabsf(act_f<ACT>(Elem<DT>::f(x[i]))));
 
     __shared__ float red[32];
     m = warp_max(m);
@@ -146,7 +98,7 @@ __global__ void __launch_bounds__(256) k_absmax_rows(const typename Elem<DT>::T*
 // holds float bits written by k_absmax).  16 elements per thread-iteration:
 // 4 (F32) or 2 (F16/BF16) 16B loads, one 16B store.  Block 0 publishes s.
 // ---------------------------------------------------------------------------
-template <int DT>
+template <int DT, int ACT = 0>
 __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::T* __restrict__ x,
                                                        int64_t n, const float* __restrict__ absmax_in,
                                                        const float* __restrict__ scale_in,
@@ -174,10 +126,10 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                 V::unpack(r[u], f);
 #pragma unroll
                 for (int j = 0; j < V::N; j += 4) {
-                    uint32_t b0 = static_cast<uint8_t>(quant_rne(f[j], s));
-                    uint32_t b1 = static_cast<uint8_t>(quant_rne(f[j + 1], s));
-                    uint32_t b2 = static_cast<uint8_t>(quant_rne(f[j + 2], s));
-                    uint32_t b3 = static_cast<uint8_t>(quant_rne(f[j + 3], s));
+                    uint32_t b0 = static_cast<uint8_t>(quant_rne(act_f<ACT>(f[j]), s));
+                    uint32_t b1 = static_cast<uint8_t>(quant_rne(act_f<ACT>(f[j + 1]), s));
+                    uint32_t b2 = static_cast<uint8_t>(quant_rne(act_f<ACT>(f[j + 2]), s));
+                    uint32_t b3 = static_cast<uint8_t>(quant_rne(act_f<ACT>(f[j + 3]), s));
                     packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
                 }
             }
@@ -186,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
         done = n16 * 16;
     }
     for (int64_t i = done + tid; i < n; i += stride)
-        q[i] = static_cast<int8_t>(quant_rne(Elem<DT>::f(x[i]), s));
+        q[i] = static_cast<int8_t>(quant_rne(act_f<ACT>(Elem<DT>::f(x[i])), s));
 }
 
 // ---------------------------------------------------------------------------
@@ -520,7 +472,7 @@ __device__ __forceinline__ void store8(void* out, int64_t i, const float* f) {
     }
 }
 
-template <int SD, int DD>
+template <int SD, int DD, int ACT = 0>
 __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* __restrict__ x,
                                                    typename Store<SD, DD>::T* __restrict__ out,
                                                    int64_t n, int vec_ok) {
@@ -534,17 +486,24 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
             float f0[8], f1[8];
             load8<SD>(x, i * 8, f0);
             load8<SD>(x, (i + stride) * 8, f1);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                f0[j] = act_f<ACT>(f0[j]);
+                f1[j] = act_f<ACT>(f1[j]);
+            }
             store8<DD>(out, i * 8, f0);
             store8<DD>(out, (i + stride) * 8, f1);
         }
         for (; i < n8; i += stride) {
             float f0[8];
             load8<SD>(x, i * 8, f0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f0[j] = act_f<ACT>(f0[j]);
             store8<DD>(out, i * 8, f0);
         }
         done = n8 * 8;
     }
-    for (int64_t i = done + tid; i < n; i += stride) out[i] = Store<SD, DD>::cvt(Elem<SD>::f(x[i]));
+    for (int64_t i = done + tid; i < n; i += stride) out[i] = Store<SD, DD>::cvt(act_f<ACT>(Elem<SD>::f(x[i])));
 }
 
 // ---------------------------------------------------------------------------
@@ -739,6 +698,42 @@ struct StatsRun {
     }
 };
 
+template <int DT>
+struct AbsmaxActRun {
+    static int run(const void* x, int64_t n, int act, float* absmax, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        QSB_TRY(cuda_status(cudaMemsetAsync(absmax, 0, sizeof(float), st), "memset"));
+        if (n == 0) return QSYNC_OK;
+        const int vec = aligned16(x);
+        const int grid = grid_for(n / Vec<DT>::N + 1, kThreads * 4);
+        if (act == 1)
+            k_absmax<DT, 1><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n,
+                                                       reinterpret_cast<unsigned*>(absmax), vec);
+        else
+            k_absmax<DT, 0><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n,
+                                                       reinterpret_cast<unsigned*>(absmax), vec);
+        return check_launch("k_absmax");
+    }
+};
+
+template <int DT>
+struct QuantActRun {
+    static int run(const void* x, int64_t n, int act, const float* absmax, int8_t* q,
+                   float* scale_out, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        if (n == 0) return QSYNC_OK;
+        const int vec = aligned16(x) && aligned16(q);
+        const int grid = grid_for(n / 16 + 1, kThreads, 4);
+        if (act == 1)
+            k_quantize<DT, 1><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, absmax, nullptr,
+                                                         q, scale_out, vec);
+        else
+            k_quantize<DT, 0><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, absmax, nullptr,
+                                                         q, scale_out, vec);
+        return check_launch("k_quantize");
+    }
+};
+
 }  // namespace
 
 }  // namespace qsb
@@ -850,6 +845,45 @@ int qsync_tensor_stats(const void* x, int dtype, int64_t n, double* out, void* w
     QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
     QSB_REQUIRE(workspace != nullptr, QSYNC_ERR_VALIDATION, "stats workspace is required");
     return dispatch_dtype<StatsRun>(dtype, x, n, out, workspace, to_stream(stream));
+}
+
+int qsync_absmax_act(const void* x, int dtype, int64_t n, int act, float* absmax,
+                     qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU, QSYNC_ERR_DOMAIN, "unknown activation");
+    return dispatch_dtype<AbsmaxActRun>(dtype, x, n, act, absmax, to_stream(stream));
+}
+
+int qsync_quantize_act(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,
+                       float* scale_out, qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    QSB_REQUIRE(absmax != nullptr, QSYNC_ERR_VALIDATION, "absmax is required");
+    QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU, QSYNC_ERR_DOMAIN, "unknown activation");
+    return dispatch_dtype<QuantActRun>(dtype, x, n, act, absmax, q, scale_out, to_stream(stream));
+}
+
+int qsync_act_cast(const void* x, int src, void* out, int dst, int64_t n, int act,
+                   qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    if (act == QSYNC_ACT_NONE) return qsync_cast(x, src, out, dst, n, stream);
+    QSB_REQUIRE(act == QSYNC_ACT_GELU, QSYNC_ERR_DOMAIN, "unknown activation");
+    if (n == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int grid = grid_for(n / 8 + 1, kThreads * 2, 4);
+    const int vec = aligned16(x) && aligned16(out);
+#define QSB_ACAST(S, D)                                                                       \
+    if (src == S && dst == D) {                                                               \
+        k_cast<S, D, 1><<<grid, kThreads, 0, st>>>(static_cast<const typename Elem<S>::T*>(x), \
+                                                   static_cast<typename Store<S, D>::T*>(out), n, vec); \
+        return check_launch("k_cast<gelu>");                                                  \
+    }
+    QSB_ACAST(QSYNC_F32, QSYNC_F32)
+    QSB_ACAST(QSYNC_F32, QSYNC_F16)
+    QSB_ACAST(QSYNC_F16, QSYNC_F16)
+    QSB_ACAST(QSYNC_F16, QSYNC_F32)
+#undef QSB_ACAST
+    return set_error(QSYNC_ERR_DOMAIN, "unsupported activation cast " + std::to_string(src) + "->" +
+                                           std::to_string(dst));
 }
 
 }  // extern "C"

@@ -1,0 +1,353 @@
+"""Layer-fused execution of the planned encoder layer, and the fused optimizer.
+
+The per-operator path (``qlinear.py``) runs each planned Linear as its own
+autograd op with the glue (cast, GELU, residual add, LayerNorm) as separate
+kernels between them.  Here one autograd Function owns a whole encoder layer,
+so the glue folds into the kernels that already touch each tensor:
+
+forward, per planned op P (INT8 / FP16 / FP32; precision.hpp:12):
+  * the LayerNorm that produces an op's input also emits that op's operand
+    format: FP16(y) for an FP16 op, absmax(y) for an INT8 op (its per-tensor
+    quantizer is then one pass) -- ``layernorm_fwd_ex``;
+  * an INT8 QKV projection writes its dequantized output as FP16 straight from
+    the GEMM epilogue (the attention core is FP16);
+  * GELU is applied inside the FF2 operand kernel: absmax(gelu(h)) then
+    quantize(gelu(h)) for INT8, cast(gelu(h)) for FP16 -- the FP32 GELU output
+    is never materialised;
+  * weights are read in the plan's format from copies the optimizer emitted
+    when it last updated them (``FusedAdamW``): per-channel INT8 W^ + scales
+    and FP16 W.
+backward (cost_mapper.cpp:13-15: FP16 for INT8/FP16 ops, wgrad FP32 :48-50):
+  * LayerNorm backward also emits FP16(dx) (the next op's dY) and dx's column
+    sums (that op's bias gradient);
+  * GELU backward is fused with FF1's FP16 dY cast and bias column sums;
+  * the dgrad of the op that reads the residual stream is reduce-added by the
+    GEMM epilogue (TMA reduce-add) into the LayerNorm-backward output, which is
+    the residual gradient: no separate add;
+  * wgrad (and bias) accumulate into the flat FP32 gradient buffer
+    (``main_grad``); wgrad GEMMs run on the side stream.
+
+Numerics are those of the per-operator path (same kernels, same scale rules):
+the INT8 quantized operands and int32 GEMM accumulators are bit-identical;
+FP16 paths differ only where a value is now rounded once instead of twice.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+from flash_attn.flash_attn_interface import (_wrapped_flash_attn_backward,
+                                             _wrapped_flash_attn_forward)
+
+from . import ops
+from . import qlinear as _ql
+from ._lib import call
+from .qlinear import FP16, FP32, INT8
+
+_p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+
+
+# =============================================================================== optimizer
+class _Seg(C.Structure):
+    """Mirror of qsync_adamw_seg (include/qsync_b200.h)."""
+    _fields_ = [("p", C.c_void_p), ("g", C.c_void_p), ("m", C.c_void_p), ("v", C.c_void_p),
+                ("w16", C.c_void_p), ("wq", C.c_void_p), ("wscale", C.c_void_p),
+                ("rows", C.c_int64), ("cols", C.c_int64)]
+
+
+class FusedAdamW:
+    """AdamW on FP32 master weights (torch.optim.AdamW semantics, decoupled
+    decay) in ONE kernel over all parameters, which also re-emits the planned
+    Linears' weight copies (FP16 W; per-channel INT8 W^ + scales) from the
+    updated weights -- ``qsync_adamw_step``.  Gradients are read from each
+    parameter's ``main_grad`` (the flat FP32 buffer)."""
+
+    def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
+                 weight_decay: float = 1e-2):
+        self.params = [p for p in params if p.requires_grad]
+        self.lr, self.betas, self.eps, self.wd = lr, betas, eps, weight_decay
+        dev = self.params[0].device
+        self.m = [torch.zeros_like(p) for p in self.params]
+        self.v = [torch.zeros_like(p) for p in self.params]
+        self.step_t = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._prep: dict[int, object] = {}  # id(weight) -> QLinear
+        self._build()
+
+    def attach(self, qlinears) -> None:
+        """(Re)allocate the weight copies each planned Linear's precision needs
+        and compute them from the current weights."""
+        self._prep = {}
+        for m in qlinears:
+            w = m.weight
+            m.w16 = m.wq = m.ws = None
+            if m.precision in (INT8, FP16):
+                m.w16 = torch.empty(w.shape, device=w.device, dtype=torch.float16)
+            if m.precision == INT8:
+                m.wq = torch.empty(w.shape, device=w.device, dtype=torch.int8)
+                m.ws = torch.empty(w.shape[0], device=w.device, dtype=torch.float32)
+            if m.w16 is not None:
+                self._prep[id(w)] = m
+        self._build()
+        self.prepare()
+
+    def _build(self) -> None:
+        segs = (_Seg * len(self.params))()
+        starts = [0]
+        for i, p in enumerate(self.params):
+            g = getattr(p, "main_grad", None)
+            if g is None:
+                g = p.grad if p.grad is not None else torch.zeros_like(p)
+                p.grad = g
+            rows = p.shape[0] if p.dim() == 2 else 1
+            cols = p.numel() // rows
+            mod = self._prep.get(id(p))
+            s = segs[i]
+            s.p, s.g, s.m, s.v = p.data_ptr(), g.data_ptr(), self.m[i].data_ptr(), self.v[i].data_ptr()
+            s.w16 = _p(getattr(mod, "w16", None)) if mod is not None else None
+            s.wq = _p(getattr(mod, "wq", None)) if mod is not None else None
+            s.wscale = _p(getattr(mod, "ws", None)) if mod is not None else None
+            s.rows, s.cols = rows, cols
+            starts.append(starts[-1] + rows)
+        raw = np.frombuffer(bytes(segs), dtype=np.uint8).copy()
+        dev = self.params[0].device
+        self._segs = torch.from_numpy(raw).to(dev)
+        self._starts = torch.tensor(starts, dtype=torch.int64, device=dev)
+        self._nseg = len(self.params)
+        self._rows = starts[-1]
+
+    def _launch(self, update: int) -> None:
+        call("qsync_adamw_step", self._segs.data_ptr(), self._nseg, self._starts.data_ptr(),
+             self._rows, self.step_t.data_ptr(), float(self.lr), float(self.betas[0]),
+             float(self.betas[1]), float(self.eps), float(self.wd), int(update),
+             torch.cuda.current_stream().cuda_stream)
+
+    def step(self) -> None:
+        self._launch(1)
+
+    def prepare(self) -> None:
+        """Recompute the weight copies from the current weights (no update)."""
+        if self._prep:
+            self._launch(0)
+
+
+# =============================================================================== layer
+def _operand(x, aux, prec):
+    """The planned op's input operand (and what its backward keeps)."""
+    if prec == INT8:
+        if aux is not None and aux.dtype == torch.float32 and aux.numel() == 1:
+            xq, s = ops.quantize_act(x, aux)
+        else:
+            xq, sc, _ = ops.quantize_per_tensor(x)
+            s = sc[:1]
+        return ("i8", xq, s)
+    if prec == FP16:
+        if x.dtype == torch.float16:
+            return ("f16", x, None)
+        if aux is not None and aux.dtype == torch.float16:
+            return ("f16", aux, None)
+        return ("f16", ops.cast(x, torch.float16), None)
+    return ("f32", x.float() if x.dtype != torch.float32 else x, None)
+
+
+def _weights(m):
+    """(wq, ws, w16) of a planned Linear: the optimizer-emitted copies when
+    present, else made now (standalone use)."""
+    if m.precision == INT8:
+        if getattr(m, "wq", None) is not None:
+            return m.wq, m.ws, m.w16
+        wq, ws, _ = ops.quantize_per_channel(m.weight.detach())
+        return wq, ws, ops.cast(m.weight.detach(), torch.float16)
+    if m.precision == FP16:
+        if getattr(m, "w16", None) is not None:
+            return None, None, m.w16
+        return None, None, ops.cast(m.weight.detach(), torch.float16)
+    return None, None, None
+
+
+def _linear_fwd(m, opnd, out_dtype=None):
+    kind, x, s = opnd
+    w, b = m.weight, m.bias
+    bias = b.detach() if b is not None else None
+    wq, ws, w16 = _weights(m)
+    if kind == "i8":
+        y = ops.gemm_s8_ex(x, wq, s, ws, bias, out_dtype=out_dtype or torch.float32)
+    elif kind == "f16":
+        y = ops.gemm_f16(x, w16, out_dtype=torch.float16, bias=bias)
+    else:
+        y = F.linear(x, w.detach(), bias)
+    return y, w16
+
+
+def _wgrad(m, dy16_or_32, opnd, side):
+    """wgrad of one planned op into weight.main_grad (FP32, accumulate)."""
+    kind, x, s = opnd
+    mw = m.weight.main_grad
+    if kind == "f32":
+        mw.addmm_(dy16_or_32.float().t(), x)  # training-device FP32 path (cuBLAS), main stream
+        return
+    x16 = ops.cast(x, torch.float16) if kind == "i8" else x  # exact: INT8 grid values
+
+    def run():
+        ops.gemm_f16(dy16_or_32, x16, alpha_dev=s, out=mw, accumulate=True, a_mn=True, b_mn=True)
+
+    if side is not None:
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            run()
+        for t in (dy16_or_32, x16, s):
+            if t is not None:
+                t.record_stream(side)
+    else:
+        run()
+
+
+def _dgrad(m, dy, w16, out_dtype, acc_into=None):
+    """dgrad of one planned op: FP16 GEMM (INT8/FP16 ops) or FP32 (FP32 op);
+    with ``acc_into`` the result is ADDED into that FP32 buffer."""
+    if m.precision == FP32:
+        d = dy.float() @ m.weight.detach()
+        if acc_into is not None:
+            acc_into.add_(d)
+            return acc_into
+        return d.to(out_dtype)
+    if acc_into is not None:
+        return ops.gemm_f16(dy, w16, out=acc_into, accumulate=True, b_mn=True)
+    return ops.gemm_f16(dy, w16, out_dtype=out_dtype, b_mn=True)
+
+
+def _bias_main_grad(m):
+    return m.bias.main_grad if m.bias is not None else None
+
+
+def _need_aux(prec):
+    return (prec == FP16, prec == INT8)
+
+
+class _FusedLayerFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x0, aux0, layer, next_prec):
+        L = layer
+        B, S, H = x0.shape
+        nh = L.cfg.heads
+        M = B * S
+        x0f = x0.reshape(M, H)
+        pq, po, p1, p2 = L.qkv.precision, L.o.precision, L.ff1.precision, L.ff2.precision
+        # --- QKV projection -> FP16 packed QKV for the attention core
+        op_qkv = _operand(x0f, aux0, pq)
+        qkv, w16_qkv = _linear_fwd(L.qkv, op_qkv, out_dtype=torch.float16)
+        if qkv.dtype != torch.float16:
+            qkv = ops.cast(qkv, torch.float16)
+        qkv5 = qkv.view(B, S, 3, nh, H // nh)
+        q, k, v = qkv5[:, :, 0], qkv5[:, :, 1], qkv5[:, :, 2]
+        scale = (H // nh) ** -0.5
+        a, lse, _, rng = _wrapped_flash_attn_forward(q, k, v, 0.0, scale, causal=False,
+                                                     window_size_left=-1, window_size_right=-1,
+                                                     softcap=0.0, alibi_slopes=None,
+                                                     return_softmax=False)
+        a2 = a.reshape(M, H)
+        # --- output projection + residual LayerNorm (emits FF1's operand)
+        op_o = _operand(a2, None, po)
+        yo, w16_o = _linear_fwd(L.o, op_o)
+        f16, am = _need_aux(p1)
+        x1, s1, mean1, rstd1, x1_16, x1_am = ops.layernorm_fwd_ex(
+            x0f, yo, L.ln1.weight.detach(), L.ln1.bias.detach(), L.ln1.eps, f16, am)
+        # --- FF1 -> GELU folded into FF2's operand kernel
+        op_1 = _operand(x1, x1_16 if f16 else x1_am, p1)
+        h, w16_1 = _linear_fwd(L.ff1, op_1)
+        if p2 == INT8:
+            gam = ops.absmax_act(h, ops.ACT_GELU)
+            gq, gs = ops.quantize_act(h, gam, ops.ACT_GELU)
+            op_2 = ("i8", gq, gs)
+        elif p2 == FP16:
+            op_2 = ("f16", ops.act_cast(h, torch.float16, ops.ACT_GELU), None)
+        else:
+            op_2 = ("f32", ops.act_cast(h, torch.float32, ops.ACT_GELU), None)
+        f, w16_2 = _linear_fwd(L.ff2, op_2)
+        f16n, amn = _need_aux(next_prec)
+        x2, s2, mean2, rstd2, x2_16, x2_am = ops.layernorm_fwd_ex(
+            x1, f, L.ln2.weight.detach(), L.ln2.bias.detach(), L.ln2.eps, f16n, amn)
+        aux2 = x2_16 if f16n else (x2_am if amn else None)
+
+        ctx.layer = L
+        ctx.ops_ = (op_qkv, op_o, op_1, op_2)
+        ctx.w16 = (w16_qkv, w16_o, w16_1, w16_2)
+        ctx.attn = (q, k, v, a, lse, rng, scale)
+        ctx.ln = (s1, mean1, rstd1, s2, mean2, rstd2)
+        ctx.h = h
+        ctx.shape = (B, S, H)
+        out = x2.view(B, S, H)
+        if aux2 is None:
+            aux2 = torch.empty(0, device=x0.device)
+        ctx.mark_non_differentiable(aux2)
+        return out, aux2
+
+    @staticmethod
+    def backward(ctx, dx2, _daux):
+        L = ctx.layer
+        B, S, H = ctx.shape
+        M = B * S
+        op_qkv, op_o, op_1, op_2 = ctx.ops_
+        w16_qkv, w16_o, w16_1, w16_2 = ctx.w16
+        q, k, v, a, lse, rng, scale = ctx.attn
+        s1, mean1, rstd1, s2, mean2, rstd2 = ctx.ln
+        h = ctx.h
+        side = _ql.WGRAD_STREAM
+        dx2 = dx2.reshape(M, H).contiguous()
+        if dx2.dtype != torch.float32:
+            dx2 = dx2.float()
+        # --- LN2 backward -> FF2's dY (FP16) + ff2 bias grad
+        p2 = L.ff2.precision
+        ds2, ds2_16 = ops.layernorm_bwd_ex(dx2, s2, mean2, rstd2, L.ln2.weight.detach(),
+                                           L.ln2.weight.main_grad, L.ln2.bias.main_grad,
+                                           want_f16=p2 != FP32, colsum_into=_bias_main_grad(L.ff2))
+        dy2 = ds2_16 if p2 != FP32 else ds2
+        dg = _dgrad(L.ff2, dy2, w16_2, h.dtype)
+        _wgrad(L.ff2, dy2, op_2, side if p2 != FP32 else None)
+        # --- GELU backward fused with FF1's dY cast + ff1 bias grad
+        p1 = L.ff1.precision
+        dh = ops.act_bwd_colsum(dg, h, ops.ACT_GELU,
+                                out_dtype=torch.float16 if p1 != FP32 else torch.float32,
+                                colsum_into=_bias_main_grad(L.ff1))
+        # FF1 dgrad reduce-added into ds2: ds2 becomes d(x1) = residual + FF1 paths
+        _dgrad(L.ff1, dh, w16_1, torch.float32, acc_into=ds2)
+        _wgrad(L.ff1, dh, op_1, side if p1 != FP32 else None)
+        # --- LN1 backward -> O's dY + o bias grad
+        po = L.o.precision
+        ds1, ds1_16 = ops.layernorm_bwd_ex(ds2, s1, mean1, rstd1, L.ln1.weight.detach(),
+                                           L.ln1.weight.main_grad, L.ln1.bias.main_grad,
+                                           want_f16=po != FP32, colsum_into=_bias_main_grad(L.o))
+        dyo = ds1_16 if po != FP32 else ds1
+        da = _dgrad(L.o, dyo, w16_o, torch.float16)
+        _wgrad(L.o, dyo, op_o, side if po != FP32 else None)
+        # --- attention core backward (FP16) -> packed dQKV
+        nh = L.cfg.heads
+        dqkv = torch.empty((B, S, 3, nh, H // nh), device=da.device, dtype=torch.float16)
+        _wrapped_flash_attn_backward(da.view(B, S, nh, H // nh), q, k, v, a, lse,
+                                     dqkv[:, :, 0], dqkv[:, :, 1], dqkv[:, :, 2], 0.0, scale,
+                                     False, -1, -1, 0.0, None, False, rng_state=rng)
+        dqkv2 = dqkv.view(M, 3 * H)
+        # --- QKV backward: bias grad (column sums), dgrad reduce-added into ds1
+        pq = L.qkv.precision
+        mb = _bias_main_grad(L.qkv)
+        if pq == FP32:
+            dq32 = dqkv2.float()
+            if mb is not None:
+                mb.add_(dq32.sum(0))
+            _dgrad(L.qkv, dq32, None, torch.float32, acc_into=ds1)
+            _wgrad(L.qkv, dq32, op_qkv, None)
+        else:
+            if mb is not None:
+                ops.act_bwd_colsum(dqkv2, None, ops.ACT_NONE, out_dtype=None, colsum_into=mb)
+            _dgrad(L.qkv, dqkv2, w16_qkv, torch.float32, acc_into=ds1)
+            _wgrad(L.qkv, dqkv2, op_qkv, side)
+        return ds1.view(B, S, H), None, None, None
+
+
+def fused_layer(layer, x, aux, next_prec):
+    """Run one EncoderLayer through the layer-fused Function.  Returns (x, aux)
+    where aux is the next planned op's operand hint (FP16 copy or absmax)."""
+    out, aux2 = _FusedLayerFn.apply(x, aux, layer, next_prec)
+    return out, (aux2 if aux2.numel() else None)

@@ -327,6 +327,102 @@ def layernorm_bwd(dy: torch.Tensor, s, mean, rstd, gamma, dgamma, dbeta) -> torc
     return dx
 
 
+# --------------------------------------------------------------------------- fused layer glue
+ACT_NONE, ACT_GELU = _lib.ACT_NONE, _lib.ACT_GELU
+
+
+def layernorm_fwd_ex(a, b, gamma, beta, eps: float, want_f16: bool = False,
+                     want_absmax: bool = False, s_out: bool = True):
+    """LN forward that also emits the next planned op's operand: FP16(y) and/or
+    absmax(y) (device float[1]).  Returns (y, s, mean, rstd, y16, absmax)."""
+    _req(a, "a", (torch.float32,))
+    cols = a.shape[-1]
+    rows = a.numel() // cols
+    y = torch.empty_like(a)
+    s = torch.empty_like(a) if (b is not None and s_out) else None
+    mean = torch.empty(rows, device=a.device, dtype=torch.float32)
+    rstd = torch.empty(rows, device=a.device, dtype=torch.float32)
+    y16 = torch.empty(a.shape, device=a.device, dtype=torch.float16) if want_f16 else None
+    am = torch.empty(1, device=a.device, dtype=torch.float32) if want_absmax else None
+    bd = F32
+    if b is not None:
+        _req(b, "b", (torch.float32, torch.float16))
+        bd = _DT[b.dtype]
+    call("qsync_layernorm_fwd_ex", _ptr(a), _ptr(b), bd, _ptr(gamma), _ptr(beta), rows, cols,
+         float(eps), _ptr(s), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(y16), _ptr(am), _stream())
+    return y, (s if s is not None else a), mean, rstd, y16, am
+
+
+def layernorm_bwd_ex(dy, s, mean, rstd, gamma, dgamma, dbeta, want_f16: bool = False,
+                     colsum_into=None, out=None):
+    """LN backward; also FP16(dx) and dx's column sums ADDED into ``colsum_into``.
+    Returns (dx, dx16)."""
+    _req(dy, "dy", (torch.float32,))
+    cols = dy.shape[-1]
+    rows = dy.numel() // cols
+    dx = out if out is not None else torch.empty_like(dy)
+    dx16 = torch.empty(dy.shape, device=dy.device, dtype=torch.float16) if want_f16 else None
+    call("qsync_layernorm_bwd_ex", _ptr(dy), _ptr(s), _ptr(mean), _ptr(rstd), _ptr(gamma), rows,
+         cols, _ptr(dx), _ptr(dgamma), _ptr(dbeta), _ptr(dx16), _ptr(colsum_into), _stream())
+    return dx, dx16
+
+
+def absmax_act(x: torch.Tensor, act: int = ACT_NONE, out=None) -> torch.Tensor:
+    _req(x, "x", _DT)
+    o = out if out is not None else torch.empty(1, device=x.device, dtype=torch.float32)
+    call("qsync_absmax_act", _ptr(x), _DT[x.dtype], x.numel(), int(act), _ptr(o), _stream())
+    return o
+
+
+def quantize_act(x: torch.Tensor, absmax: torch.Tensor, act: int = ACT_NONE):
+    """q = sat(rint(act(x) / s)), s = absmax/127 from a device absmax.  Returns (q, s[1])."""
+    _req(x, "x", _DT)
+    q = torch.empty(x.shape, device=x.device, dtype=torch.int8)
+    s = torch.empty(1, device=x.device, dtype=torch.float32)
+    call("qsync_quantize_act", _ptr(x), _DT[x.dtype], x.numel(), int(act), _ptr(absmax), _ptr(q),
+         _ptr(s), _stream())
+    return q, s
+
+
+def act_cast(x: torch.Tensor, dtype: torch.dtype, act: int = ACT_NONE, out=None) -> torch.Tensor:
+    _req(x, "x", (torch.float32, torch.float16))
+    o = out if out is not None else torch.empty(x.shape, device=x.device, dtype=dtype)
+    call("qsync_act_cast", _ptr(x), _DT[x.dtype], _ptr(o), _DT[dtype], x.numel(), int(act),
+         _stream())
+    return o
+
+
+def act_bwd_colsum(dy: torch.Tensor, h: torch.Tensor | None, act: int = ACT_NONE,
+                   out_dtype: torch.dtype | None = torch.float16, colsum_into=None):
+    """g = dy * act'(h) as out_dtype (None: no output), column sums ADDED into ``colsum_into``."""
+    _req(dy, "dy", (torch.float32, torch.float16))
+    if h is not None:
+        _req(h, "h", (torch.float32, torch.float16))
+    cols = dy.shape[-1]
+    rows = dy.numel() // cols
+    o = torch.empty(dy.shape, device=dy.device, dtype=out_dtype) if out_dtype is not None else None
+    call("qsync_act_bwd_colsum", _ptr(dy), _DT[dy.dtype], _ptr(h), _DT[h.dtype] if h is not None else F32,
+         rows, cols, int(act), _ptr(o), _DT[out_dtype] if out_dtype is not None else F32,
+         _ptr(colsum_into), _stream())
+    return o
+
+
+def gemm_s8_ex(a: torch.Tensor, b: torch.Tensor, scale_a, scale_b, bias=None,
+               out_dtype=torch.float32, b_per_channel: bool = True, out=None) -> torch.Tensor:
+    """INT8 GEMM + dequant epilogue written as out_dtype (F32 / F16)."""
+    _req(a, "a", (torch.int8,))
+    _req(b, "b", (torch.int8,))
+    M, K = a.shape
+    N = b.shape[0]
+    c = out if out is not None else torch.empty((M, N), device=a.device, dtype=out_dtype)
+    ev = _timed("gemm_s8", 2.0 * M * N * K)
+    call("qsync_gemm_s8_ex", _ptr(a), _ptr(b), M, N, K, _ptr(c), _DT[c.dtype], _ptr(scale_a),
+         _ptr(scale_b), int(b_per_channel), _ptr(bias), _stream())
+    if ev is not None:
+        ev.record()
+    return c
+
+
 def launch_count() -> int:
     """Kernels launched by libqsync_b200 so far in this process."""
     return int(_lib.lib().qsync_launch_count())

@@ -125,6 +125,9 @@ class BertEncoderStack(torch.nn.Module):
         self.ln = AddLayerNorm(cfg.hidden, eps=1e-12)
         self.layers = torch.nn.ModuleList([EncoderLayer(cfg, i) for i in range(cfg.layers)])
         self.pooler = QLinear(cfg.hidden, cfg.hidden, "pooler")
+        # Layer-fused execution (fused.py); the per-operator path stays for
+        # profiling (per-op statistics) and as the parity reference.
+        self.fused = False
         self.cls = torch.nn.Linear(cfg.hidden, cfg.num_labels)
         for emb in (self.word, self.pos, self.typ):
             torch.nn.init.normal_(emb.weight, std=0.02)
@@ -142,8 +145,16 @@ class BertEncoderStack(torch.nn.Module):
         pos = torch.arange(S, device=tokens.device)
         x = self.word(tokens) + self.pos(pos)[None] + self.typ.weight[0][None, None]
         x = self.ln(x)
-        for layer in self.layers:
-            x = layer(x)
+        if self.fused:
+            from .fused import fused_layer
+            aux = None
+            n = len(self.layers)
+            for i, layer in enumerate(self.layers):
+                nxt = self.layers[i + 1].qkv.precision if i + 1 < n else None
+                x, aux = fused_layer(layer, x, aux, nxt)
+        else:
+            for layer in self.layers:
+                x = layer(x)
         pooled = torch.tanh(cast(self.pooler(x[:, 0].contiguous()), torch.float32))
         logits = self.cls(pooled)
         return F.cross_entropy(logits, labels)
@@ -211,7 +222,7 @@ class TrainStep:
     + AdamW on FP32 master weights.  Optionally captured into a CUDA graph."""
 
     def __init__(self, model: BertEncoderStack, batch: int, world: int = 1, lr: float = 1e-4,
-                 graph: bool = True, overlap_wgrad: bool = True):
+                 graph: bool = True, overlap_wgrad: bool = True, fused: bool = True):
         self.model = model
         self.world = world
         cfg = model.cfg
@@ -220,11 +231,25 @@ class TrainStep:
         self.labels = torch.zeros((batch,), dtype=torch.long, device=dev)
         self.params = [p for p in model.parameters() if p.requires_grad]
         self.grads = FlatGrads(self.params)
-        self.opt = torch.optim.AdamW(self.params, lr=lr, fused=True, capturable=graph)
+        self.fused = fused
+        model.fused = fused
+        if fused:
+            # One kernel: AdamW + the planned Linears' weight copies for the next step.
+            from .fused import FusedAdamW
+            self.opt = FusedAdamW(self.params, lr=lr)
+            self.opt.attach(model.qlinears().values())
+        else:
+            self.opt = torch.optim.AdamW(self.params, lr=lr, fused=True, capturable=graph)
         self.use_graph = graph
         self.graph = None
         self.loss = None
         self.wgrad_stream = torch.cuda.Stream() if overlap_wgrad else None
+
+    def apply_plan(self, plan: dict[str, str]) -> None:
+        """Switch this rank's plan (re-capture afterwards when graphed)."""
+        self.model.apply_plan(plan)
+        if self.fused:
+            self.opt.attach(self.model.qlinears().values())
 
     def _body(self):
         self.grads.zero()

@@ -86,8 +86,9 @@ def _batch(cfg, B, seed):
             torch.randint(0, 2, (B,), generator=g))
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("plan_kind", ["mixed", "int8", "fp16"])
-def test_train_step_graph_matches_eager_and_learns(plan_kind):
+def test_train_step_graph_matches_eager_and_learns(plan_kind, fused):
     cfg = _tiny_cfg()
     plans = {"mixed": mixed_plan(cfg), "int8": uniform_plan(cfg, INT8), "fp16": uniform_plan(cfg, FP16)}
     losses = {}
@@ -95,7 +96,7 @@ def test_train_step_graph_matches_eager_and_learns(plan_kind):
         torch.manual_seed(0)
         m = BertEncoderStack(cfg).to(DEV)
         m.apply_plan(plans[plan_kind])
-        st = TrainStep(m, batch=8, lr=3e-4, graph=use_graph)
+        st = TrainStep(m, batch=8, lr=3e-4, graph=use_graph, fused=fused)
         tok, lab = _batch(cfg, 8, 1)
         st.tokens.copy_(tok)
         st.labels.copy_(lab)
