@@ -50,9 +50,7 @@ __device__ __forceinline__ void store8v(void* base, int64_t i, const float* f) {
         uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t lo = __half_as_ushort(__float2half_rn(f[2 * k]));
-            const uint32_t hi = __half_as_ushort(__float2half_rn(f[2 * k + 1]));
-            w[k] = lo | (hi << 16);
+            w[k] = pack_half2(f[2 * k], f[2 * k + 1]);
         }
         *reinterpret_cast<uint4*>(static_cast<uint16_t*>(base) + i) = make_uint4(w[0], w[1], w[2], w[3]);
     }

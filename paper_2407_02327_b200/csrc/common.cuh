@@ -74,6 +74,16 @@ __device__ __forceinline__ int quant_rne(float x, float s) {
     return static_cast<int>(r);
 }
 
+// Two floats -> packed 16-bit pair (one F2FP.PACK_AB instruction), low half first.
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+    const __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t pack_bf162(float lo, float hi) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 // GELU (erf form, BERT's activation) and its derivative, every operation
 // rounded explicitly so that all kernels that evaluate it agree bit for bit:
 //   gelu(x)  = 0.5 x (1 + erf(x / sqrt 2))

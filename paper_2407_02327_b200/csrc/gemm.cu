@@ -317,12 +317,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float v[32];
                 const int64_t col0 = n0 + c0;
                 const int nsub = out16 ? 2 : 1;
+                // Both 32-column TMEM loads of a 16-bit chunk are in flight
+                // before the single wait.
+                uint32_t rr[2][32];
+                ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0), rr[0]);
+                if (out16) ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0 + 32), rr[1]);
+                ptx::tmem_ld_wait();
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     if (sub >= nsub) break;
-                    uint32_t r[32];
-                    ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0 + 32 * sub), r);
-                    ptx::tmem_ld_wait();
+                    uint32_t (&r)[32] = rr[sub];
                     if (p.debug_epi) continue;
                     if (raw) {
 #pragma unroll
@@ -345,25 +349,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     const float colscale = kI8 ? __fmul_rn(sa, sb) : alpha;
+                    // Column j's factors live in lane j: broadcast by shuffle only
+                    // where they vary per column (INT8 per-channel scale, bias); the
+                    // FP16 GEMMs' alpha is uniform.
+                    if (p.bias) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float sj = __shfl_sync(0xffffffffu, colscale, j);
-                        const float bj = __shfl_sync(0xffffffffu, bs, j);
-                        float x = kI8 ? __fmul_rn(__int2float_rn(static_cast<int>(r[j])), sj)
-                                      : __fmul_rn(bits_f(r[j]), sj);
-                        if (p.bias) x = __fadd_rn(x, bj);
-                        v[j] = x;
+                        for (int j = 0; j < 32; ++j) {
+                            const float sj = kI8 ? __shfl_sync(0xffffffffu, colscale, j) : alpha;
+                            const float bj = __shfl_sync(0xffffffffu, bs, j);
+                            const float x = kI8 ? __fmul_rn(__int2float_rn(static_cast<int>(r[j])), sj)
+                                                : __fmul_rn(bits_f(r[j]), sj);
+                            v[j] = __fadd_rn(x, bj);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float sj = kI8 ? __shfl_sync(0xffffffffu, colscale, j) : alpha;
+                            v[j] = kI8 ? __fmul_rn(__int2float_rn(static_cast<int>(r[j])), sj)
+                                       : __fmul_rn(bits_f(r[j]), sj);
+                        }
                     }
                     if (out16) {
                         const bool bf = p.c_dtype == QSYNC_BF16;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const uint32_t lo = bf ? __bfloat16_as_ushort(__float2bfloat16_rn(v[2 * j]))
-                                                   : __half_as_ushort(__float2half_rn(v[2 * j]));
-                            const uint32_t hi = bf ? __bfloat16_as_ushort(__float2bfloat16_rn(v[2 * j + 1]))
-                                                   : __half_as_ushort(__float2half_rn(v[2 * j + 1]));
-                            w[16 * sub + j] = lo | (hi << 16);
-                        }
+                        for (int j = 0; j < 16; ++j)
+                            w[16 * sub + j] = bf ? pack_bf162(v[2 * j], v[2 * j + 1]) : pack_half2(v[2 * j], v[2 * j + 1]);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);

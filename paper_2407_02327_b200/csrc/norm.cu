@@ -85,10 +85,8 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
             *reinterpret_cast<float4*>(y + off) = o;
             if (y16) {
                 uint2 h;
-                h.x = __half_as_ushort(__float2half_rn(o.x)) |
-                      (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(o.y))) << 16);
-                h.y = __half_as_ushort(__float2half_rn(o.z)) |
-                      (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(o.w))) << 16);
+                h.x = pack_half2(o.x, o.y);
+                h.y = pack_half2(o.z, o.w);
                 *reinterpret_cast<uint2*>(y16 + off) = h;
             }
             amax = fmaxf(amax, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
@@ -99,10 +97,17 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
         }
     }
     if (y_absmax) {
-        // absmax of y for the next INT8 op's per-tensor scale: warp max, then
-        // one atomicMax per warp on the float bits (order-independent).
+        // absmax of y for the next INT8 op's per-tensor scale: warp max, block
+        // max through shared memory, one atomicMax per block on the float bits
+        // (order-independent, so deterministic).
+        __shared__ float wmax[8];
         amax = warp_max(amax);
-        if (lane == 0 && amax > 0.0f) atomicMax(y_absmax, __float_as_uint(amax));
+        if (lane == 0) wmax[threadIdx.x >> 5] = amax;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            amax = warp_max(threadIdx.x < (blockDim.x >> 5) ? wmax[threadIdx.x] : 0.0f);
+            if (threadIdx.x == 0 && amax > 0.0f) atomicMax(y_absmax, __float_as_uint(amax));
+        }
     }
 }
 
@@ -160,10 +165,8 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
             *reinterpret_cast<float4*>(dx + off) = o;
             if (dx16) {
                 uint2 h;
-                h.x = __half_as_ushort(__float2half_rn(o.x)) |
-                      (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(o.y))) << 16);
-                h.y = __half_as_ushort(__float2half_rn(o.z)) |
-                      (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(o.w))) << 16);
+                h.x = pack_half2(o.x, o.y);
+                h.y = pack_half2(o.z, o.w);
                 *reinterpret_cast<uint2*>(dx16 + off) = h;
             }
             acc_c[i].x += o.x; acc_c[i].y += o.y; acc_c[i].z += o.z; acc_c[i].w += o.w;

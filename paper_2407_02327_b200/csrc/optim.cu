@@ -130,10 +130,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
                 const float4 pv = reinterpret_cast<const float4*>(p)[k];
                 if (w16) {
                     uint2 h;
-                    h.x = __half_as_ushort(__float2half_rn(pv.x)) |
-                          (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(pv.y))) << 16);
-                    h.y = __half_as_ushort(__float2half_rn(pv.z)) |
-                          (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(pv.w))) << 16);
+                    h.x = pack_half2(pv.x, pv.y);
+                    h.y = pack_half2(pv.z, pv.w);
                     reinterpret_cast<uint2*>(w16)[k] = h;
                 }
                 if (wq) {

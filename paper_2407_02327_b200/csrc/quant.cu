@@ -19,9 +19,17 @@ constexpr int kThreads = 512;
 // Fused prologue activation of the streaming kernels: ACT 0 = identity,
 // ACT 1 = GELU (the FF1 -> FF2 activation of an encoder layer, so the
 // quantizer / cast of the FF2 input reads the pre-activation directly).
-template <int ACT>
+// For a 16-bit input the activation is a dependent op of an FP16 producer and
+// runs in its precision (the cascade rule, graph.cpp:254-269): its output is
+// rounded to that format before it is quantized, exactly as if materialised.
+template <int ACT, int DT = QSYNC_F32>
 __device__ __forceinline__ float act_f(float v) {
-    if constexpr (ACT == 1) return gelu_erf(v);
+    if constexpr (ACT == 1) {
+        const float g = gelu_erf(v);
+        if constexpr (DT == QSYNC_F16) return __half2float(__float2half_rn(g));
+        if constexpr (DT == QSYNC_BF16) return __bfloat162float(__float2bfloat16_rn(g));
+        return g;
+    }
     return v;
 }
 
@@ -54,18 +62,18 @@ __global__ void __launch_bounds__(kThreads) k_absmax(const typename Elem<DT>::T*
                 float f[V::N];
                 V::unpack(r[u], f);
 #pragma unroll
-                for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(act_f<ACT>(f[j])));
+                for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(act_f<ACT, DT>(f[j])));
             }
         }
         for (; i < nv; i += stride) {
             float f[V::N];
             V::unpack(ld_stream(xv + i), f);
 #pragma unroll
-            for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(act_f<ACT>(f[j])));
+            for (int j = 0; j < V::N; ++j) m = fmaxf(m, fabsf(act_f<ACT, DT>(f[j])));
         }
         done = nv * V::N;
     }
-    for (int64_t i = done + tid; i < n; i += stride) m = fmaxf(m, fabsf(act_f<ACT>(Elem<DT>::f(x[i]))));
+    for (int64_t i = done + tid; i < n; i += stride) m = fmaxf(m, fabsf(act_f<ACT, DT>(Elem<DT>::f(x[i]))));
 
     __shared__ float red[32];
     m = warp_max(m);
@@ -126,10 +134,10 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                 V::unpack(r[u], f);
 #pragma unroll
                 for (int j = 0; j < V::N; j += 4) {
-                    uint32_t b0 = static_cast<uint8_t>(quant_rne(act_f<ACT>(f[j]), s));
-                    uint32_t b1 = static_cast<uint8_t>(quant_rne(act_f<ACT>(f[j + 1]), s));
-                    uint32_t b2 = static_cast<uint8_t>(quant_rne(act_f<ACT>(f[j + 2]), s));
-                    uint32_t b3 = static_cast<uint8_t>(quant_rne(act_f<ACT>(f[j + 3]), s));
+                    uint32_t b0 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j]), s));
+                    uint32_t b1 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j + 1]), s));
+                    uint32_t b2 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j + 2]), s));
+                    uint32_t b3 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j + 3]), s));
                     packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
                 }
             }
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
         done = n16 * 16;
     }
     for (int64_t i = done + tid; i < n; i += stride)
-        q[i] = static_cast<int8_t>(quant_rne(act_f<ACT>(Elem<DT>::f(x[i])), s));
+        q[i] = static_cast<int8_t>(quant_rne(act_f<ACT, DT>(Elem<DT>::f(x[i])), s));
 }
 
 // ---------------------------------------------------------------------------
@@ -462,11 +470,7 @@ __device__ __forceinline__ void store8(void* out, int64_t i, const float* f) {
         uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t lo = DD == QSYNC_F16 ? __half_as_ushort(__float2half_rn(f[2 * k]))
-                                                : __bfloat16_as_ushort(__float2bfloat16_rn(f[2 * k]));
-            const uint32_t hi = DD == QSYNC_F16 ? __half_as_ushort(__float2half_rn(f[2 * k + 1]))
-                                                : __bfloat16_as_ushort(__float2bfloat16_rn(f[2 * k + 1]));
-            w[k] = lo | (hi << 16);
+            w[k] = DD == QSYNC_F16 ? pack_half2(f[2 * k], f[2 * k + 1]) : pack_bf162(f[2 * k], f[2 * k + 1]);
         }
         __stcs(reinterpret_cast<uint4*>(static_cast<uint16_t*>(out) + i), make_uint4(w[0], w[1], w[2], w[3]));
     }
@@ -488,8 +492,8 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
             load8<SD>(x, (i + stride) * 8, f1);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                f0[j] = act_f<ACT>(f0[j]);
-                f1[j] = act_f<ACT>(f1[j]);
+                f0[j] = act_f<ACT, SD>(f0[j]);
+                f1[j] = act_f<ACT, SD>(f1[j]);
             }
             store8<DD>(out, i * 8, f0);
             store8<DD>(out, (i + stride) * 8, f1);
@@ -498,12 +502,12 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
             float f0[8];
             load8<SD>(x, i * 8, f0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) f0[j] = act_f<ACT>(f0[j]);
+            for (int j = 0; j < 8; ++j) f0[j] = act_f<ACT, SD>(f0[j]);
             store8<DD>(out, i * 8, f0);
         }
         done = n8 * 8;
     }
-    for (int64_t i = done + tid; i < n; i += stride) out[i] = Store<SD, DD>::cvt(act_f<ACT>(Elem<SD>::f(x[i])));
+    for (int64_t i = done + tid; i < n; i += stride) out[i] = Store<SD, DD>::cvt(act_f<ACT, SD>(Elem<SD>::f(x[i])));
 }
 
 // ---------------------------------------------------------------------------

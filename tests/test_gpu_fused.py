@@ -62,7 +62,9 @@ def test_gelu_quantize_matches_unfused(dtype, n):
     torch.manual_seed(2)
     h = (torch.randn(n, device=DEV) * 2).to(dtype)
     g = ops.act_cast(h, torch.float32, ops.ACT_GELU)
-    torch.testing.assert_close(g, F.gelu(h.float()), rtol=2e-6, atol=2e-7)
+    # an FP16 producer's GELU runs (and rounds) in FP16, as torch's F.gelu(h16)
+    tol = 2e-6 if dtype == torch.float32 else 1e-3
+    torch.testing.assert_close(g, F.gelu(h).float(), rtol=tol, atol=tol / 10)
     am = ops.absmax_act(h, ops.ACT_GELU)
     assert am.item() == g.abs().max().item()
     q, s = ops.quantize_act(h, am, ops.ACT_GELU)

@@ -25,10 +25,11 @@ def main(name: str, reps: int = 3) -> None:
         out = torch.empty((M, N), device=dev)
         fn = lambda: ops.gemm_s8(a, b, sa, sb, bias, out=out)  # noqa: E731
     elif name.startswith("gemm_f16"):
-        M, N, K = (8192, 8192, 8192) if name.endswith("8192") else (4096, 768, 3072)
+        M, N, K = {"gemm_f16_8192": (8192, 8192, 8192), "gemm_f16_ff1": (4096, 3072, 768)}.get(
+            name, (4096, 768, 3072))
         a = torch.randn((M, K), device=dev).half()
         b = torch.randn((N, K), device=dev).half()
-        out = torch.empty((M, N), device=dev)
+        out = torch.empty((M, N), device=dev, dtype=torch.float16 if name.endswith("ff1") else torch.float32)
         fn = lambda: ops.gemm_f16(a, b, out=out)  # noqa: E731
     else:
         n = (1 << 30) // 4
