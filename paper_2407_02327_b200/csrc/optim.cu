@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kWarps = 8;
 
-__device__ __forceinline__ int find_seg(const int64_t* __restrict__ start, int nseg, int64_t row) {
+__device__ __forceinline__ int find_seg(const int64_t* start, int nseg, int64_t row) {
     int lo = 0, hi = nseg - 1;  // largest s with start[s] <= row
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -54,7 +54,7 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, con
 }
 
 __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __restrict__ segs, int nseg,
-                                                       const int64_t* __restrict__ seg_start,
+                                                       const int64_t* seg_start,
                                                        int64_t total_rows, const int64_t* __restrict__ step,
                                                        float lr, float b1, float b2, float eps, float wd,
                                                        int update) {
@@ -72,6 +72,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
         c.step_size = lr / bc1;
         c.inv_bc2_sqrt = 1.0f / sqrtf(bc2);
     }
+    // Segment row offsets staged in shared memory: the per-row binary search
+    // would otherwise be a chain of dependent global loads.
+    extern __shared__ int64_t s_start[];
+    for (int i = threadIdx.x; i <= nseg; i += blockDim.x) s_start[i] = seg_start[i];
+    __syncthreads();
+    seg_start = s_start;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
     for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5); row < total_rows;
          row += nwarps) {
@@ -89,19 +95,47 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
             float* m = sg.m + r * cols;
             float* v = sg.v + r * cols;
             if (vec) {
-                for (int64_t k = lane; k < cols / 4; k += 32) {
-                    float4 pv = reinterpret_cast<float4*>(p)[k];
-                    const float4 gv = reinterpret_cast<const float4*>(g)[k];
-                    float4 mv = reinterpret_cast<float4*>(m)[k];
-                    float4 vv = reinterpret_cast<float4*>(v)[k];
-                    pv.x = adam1(pv.x, gv.x, mv.x, vv.x, c);
-                    pv.y = adam1(pv.y, gv.y, mv.y, vv.y, c);
-                    pv.z = adam1(pv.z, gv.z, mv.z, vv.z, c);
-                    pv.w = adam1(pv.w, gv.w, mv.w, vv.w, c);
-                    reinterpret_cast<float4*>(p)[k] = pv;
-                    reinterpret_cast<float4*>(m)[k] = mv;
-                    reinterpret_cast<float4*>(v)[k] = vv;
-                    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(pv.x), fabsf(pv.y)), fmaxf(fabsf(pv.z), fabsf(pv.w))));
+                // Two float4 of each operand per lane in flight (8 x 16 B loads);
+                // g / m / v are streamed (evict-first), p stays L2-resident for
+                // the prepared-copy pass below.
+                const int64_t n4 = cols / 4;
+                const bool w16_now = sg.w16 && !sg.wq && ((reinterpret_cast<uintptr_t>(sg.w16 + r * cols) & 7u) == 0);
+                float4* p4 = reinterpret_cast<float4*>(p);
+                const float4* g4 = reinterpret_cast<const float4*>(g);
+                float4* m4 = reinterpret_cast<float4*>(m);
+                float4* v4 = reinterpret_cast<float4*>(v);
+                for (int64_t k = lane; k < n4; k += 64) {
+                    const bool two = k + 32 < n4;
+                    float4 pv[2], gv[2], mv[2], vv[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        if (u == 1 && !two) break;
+                        const int64_t kk = k + 32 * u;
+                        pv[u] = p4[kk];
+                        gv[u] = __ldcs(g4 + kk);
+                        mv[u] = __ldcs(m4 + kk);
+                        vv[u] = __ldcs(v4 + kk);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        if (u == 1 && !two) break;
+                        const int64_t kk = k + 32 * u;
+                        pv[u].x = adam1(pv[u].x, gv[u].x, mv[u].x, vv[u].x, c);
+                        pv[u].y = adam1(pv[u].y, gv[u].y, mv[u].y, vv[u].y, c);
+                        pv[u].z = adam1(pv[u].z, gv[u].z, mv[u].z, vv[u].z, c);
+                        pv[u].w = adam1(pv[u].w, gv[u].w, mv[u].w, vv[u].w, c);
+                        p4[kk] = pv[u];
+                        __stcs(m4 + kk, mv[u]);
+                        __stcs(v4 + kk, vv[u]);
+                        amax = fmaxf(amax, fmaxf(fmaxf(fabsf(pv[u].x), fabsf(pv[u].y)),
+                                                 fmaxf(fabsf(pv[u].z), fabsf(pv[u].w))));
+                        if (w16_now) {  // an FP16-only copy needs no row scale: write it now
+                            uint2 h;
+                            h.x = pack_half2(pv[u].x, pv[u].y);
+                            h.y = pack_half2(pv[u].z, pv[u].w);
+                            reinterpret_cast<uint2*>(sg.w16 + r * cols)[kk] = h;
+                        }
+                    }
                 }
             } else {
                 for (int64_t k = lane; k < cols; k += 32) {
@@ -117,6 +151,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
             for (int64_t k = lane; k < cols; k += 32) amax = fmaxf(amax, fabsf(p[k]));
         }
         if (!sg.w16 && !sg.wq) continue;
+        if (update && vec && !sg.wq && (reinterpret_cast<uintptr_t>(sg.w16 + r * cols) & 7u) == 0) continue;
         __syncwarp();  // this warp's p stores are visible to its own re-reads
         amax = warp_max(amax);
         const float sc = scale_from_absmax(amax);
@@ -172,7 +207,9 @@ int qsync_adamw_step(const qsync_adamw_seg* segs, int nseg, const int64_t* seg_r
     if (total_rows == 0) return QSYNC_OK;
     cudaStream_t st = to_stream(stream);
     const int grid = static_cast<int>(std::min<int64_t>((total_rows + kWarps - 1) / kWarps, sm_count() * 16LL));
-    k_adamw<<<grid, kWarps * 32, 0, st>>>(segs, nseg, seg_row_start, total_rows, step, lr, beta1, beta2, eps,
+    const size_t smem = sizeof(int64_t) * (static_cast<size_t>(nseg) + 1);
+    QSB_REQUIRE(smem <= 48 * 1024, QSYNC_ERR_DOMAIN, "too many parameter segments");
+    k_adamw<<<grid, kWarps * 32, smem, st>>>(segs, nseg, seg_row_start, total_rows, step, lr, beta1, beta2, eps,
                                           weight_decay, update);
     QSB_TRY(check_launch("k_adamw"));
     if (!update) return QSYNC_OK;

@@ -343,6 +343,8 @@ class _FusedLayerFn(torch.autograd.Function):
                 ops.act_bwd_colsum(dqkv2, None, ops.ACT_NONE, out_dtype=None, colsum_into=mb)
             _dgrad(L.qkv, dqkv2, w16_qkv, torch.float32, acc_into=ds1)
             _wgrad(L.qkv, dqkv2, op_qkv, side)
+        if _ql.GRAD_READY is not None:
+            _ql.GRAD_READY(list(L.parameters()))
         return ds1.view(B, S, H), None, None, None
 
 

@@ -49,6 +49,9 @@ def backward_precision(precision: str) -> str:
 # feeds the optimizer, so it runs concurrently with the rest of the backward
 # chain (dgrad of the next layers); TrainStep joins it before the all-reduce.
 WGRAD_STREAM: torch.cuda.Stream | None = None
+# Data-parallel readiness hook (TrainStep, world > 1): called with a list of
+# parameters whose gradients are final, so their all-reduce bucket can start.
+GRAD_READY = None
 
 
 def _main_grad(p):

@@ -202,19 +202,91 @@ class FlatGrads:
         if off > b_start:
             self.buckets.append((b_start, off))
 
+        # Bucket membership for the overlapped all-reduce: params never straddle.
+        self.bucket_of: dict[int, int] = {}
+        self._members = [0] * len(self.buckets)
+        for p, start in zip(order, slots):
+            b = next(i for i, (a, e) in enumerate(self.buckets) if a <= start < e)
+            self.bucket_of[id(p)] = b
+            self._members[b] += 1
+        self._pending: list[int] = []
+        self._next = 0
+        self._world = 1
+        self._side = None
+        self.comm_stream = None
+        self.issue_log: list[tuple[int, int]] = []  # (bucket, pending params at issue) -- tests
+
     def zero(self) -> None:
         self.flat.zero_()
 
-    def allreduce(self, world: int) -> None:
-        """Bucket n after bucket n-1, all ranks in the same order (Eq. 6 slots,
-        replayer.cpp:48-62), then average."""
+    # ---- overlapped, in-order bucket all-reduce (Eq. 6 slots, replayer.cpp:48-62)
+    def begin(self, world: int, side_stream=None) -> None:
+        """Start a backward pass: bucket n is all-reduced as soon as all of its
+        parameters are final AND bucket n-1 has been issued -- one comm stream,
+        in order, identical on every rank whatever its precision plan."""
+        self._world = world
+        self._pending = list(self._members)
+        self._next = 0
+        self._side = side_stream
+        self.issue_log = []
+        if self.flat.is_cuda and world > 1 and self.comm_stream is None:
+            self.comm_stream = torch.cuda.Stream()
+
+    def params_ready(self, params) -> None:
+        """The gradients of ``params`` are final (their producing kernels are
+        enqueued on the current stream and, for wgrad, the side stream)."""
+        if self._world <= 1:
+            return
+        for p in params:
+            b = self.bucket_of.get(id(p))
+            if b is not None and self._pending[b] > 0:
+                self._pending[b] -= 1
+        self._issue(force=False)
+
+    def finish(self) -> None:
+        """End of backward: issue every remaining bucket, then make the current
+        stream (the optimizer) wait for the last one (replayer.cpp:64-73)."""
+        if self._world <= 1:
+            return
+        self._issue(force=True)
+        if self.comm_stream is not None:
+            torch.cuda.current_stream().wait_stream(self.comm_stream)
+
+    def _issue(self, force: bool) -> None:
         import torch.distributed as dist
+        ready = []
+        while self._next < len(self.buckets) and (force or self._pending[self._next] == 0):
+            ready.append(self._next)
+            self.issue_log.append((self._next, self._pending[self._next]))
+            self._next += 1
+        if not ready:
+            return
+        world = self._world
+        nccl = dist.get_backend() == "nccl"
+        if self.comm_stream is not None:
+            self.comm_stream.wait_stream(torch.cuda.current_stream())
+            if self._side is not None:
+                self.comm_stream.wait_stream(self._side)
+            ctx = torch.cuda.stream(self.comm_stream)
+        else:
+            import contextlib
+            ctx = contextlib.nullcontext()
+        with ctx:
+            for i in ready:
+                a, b = self.buckets[i]
+                chunk = self.flat[a:b]
+                if nccl:
+                    dist.all_reduce(chunk, op=dist.ReduceOp.AVG)
+                else:
+                    dist.all_reduce(chunk)
+                    chunk.div_(world)
+
+    def allreduce(self, world: int) -> None:
+        """Non-overlapped form: every bucket in order after the backward."""
         if world <= 1:
             return
-        for (a, b) in self.buckets:
-            chunk = self.flat[a:b]
-            dist.all_reduce(chunk)
-        self.flat.div_(world)
+        self.begin(world)
+        self.finish()
 
 
 class TrainStep:
@@ -244,6 +316,10 @@ class TrainStep:
         self.graph = None
         self.loss = None
         self.wgrad_stream = torch.cuda.Stream() if overlap_wgrad else None
+        if world > 1 and fused:
+            for m in (model.pooler, model.cls):
+                for prm in m.parameters():
+                    prm.register_post_accumulate_grad_hook(lambda t: self.grads.params_ready([t]))
 
     def apply_plan(self, plan: dict[str, str]) -> None:
         """Switch this rank's plan (re-capture afterwards when graphed)."""
@@ -257,13 +333,19 @@ class TrainStep:
         _ql.WGRAD_STREAM = self.wgrad_stream
         if self.wgrad_stream is not None:
             self.wgrad_stream.wait_stream(torch.cuda.current_stream())  # after the zeroing
+        # Buckets are all-reduced while the backward continues: a fused layer
+        # reports its parameters final when its backward is enqueued, autograd
+        # parameters (pooler, classifier) through their post-accumulate hooks.
+        self.grads.begin(self.world, self.wgrad_stream)
+        _ql.GRAD_READY = self.grads.params_ready if (self.world > 1 and self.fused) else None
         try:
             loss.backward()
         finally:
             _ql.WGRAD_STREAM = None
+            _ql.GRAD_READY = None
         if self.wgrad_stream is not None:
-            torch.cuda.current_stream().wait_stream(self.wgrad_stream)  # join before the all-reduce
-        self.grads.allreduce(self.world)
+            torch.cuda.current_stream().wait_stream(self.wgrad_stream)  # join before the last buckets
+        self.grads.finish()
         self.opt.step()
         return loss.detach()
 

@@ -89,3 +89,61 @@ def test_plan_file_formats(tmp_path):
     mp_ = mixed_plan(cfg)
     assert set(mp_) == set(adjustable_ops(cfg))
     assert mp_["layer0.qkv"] == INT8 and mp_["layer1.qkv"] == FP16 and mp_["pooler"] == FP32
+
+
+def _worker_overlap(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    params = _params()
+    g = FlatGrads(params, bucket_bytes=4 << 20)
+    g.begin(world)
+    issued_after = []
+    # backward order = reverse of the forward parameter order; grads become final
+    # one parameter at a time, as the layers' backward passes report them
+    for i, p in enumerate(reversed(params)):
+        p.main_grad.copy_(torch.full_like(p, float(rank + 1) * (i + 1)))
+        g.params_ready([p])
+        issued_after.append(g._next)
+    g.finish()
+    first = {"issued_after": issued_after, "log": g.issue_log,
+             "bucket_of": [g.bucket_of[id(p)] for p in reversed(params)],
+             "vals": [float(p.main_grad.flatten()[0]) for p in reversed(params)]}
+    # second pass: only the first two parameters report; finish() forces the rest
+    g.zero()
+    g.begin(world)
+    for i, p in enumerate(reversed(params)):
+        p.main_grad.fill_(float(rank + 1))
+    g.params_ready(list(reversed(params))[:2])
+    partial = g._next
+    g.finish()
+    second = {"partial": partial, "log": g.issue_log,
+              "vals": [float(p.main_grad.flatten()[0]) for p in params]}
+    with open(os.path.join(out_dir, f"o{rank}.json"), "w") as f:
+        json.dump({"first": first, "second": second, "nb": len(g.buckets)}, f)
+    dist.destroy_process_group()
+
+
+def test_overlapped_bucket_allreduce_world2(tmp_path):
+    """Bucket n is reduced as soon as its last parameter is final and bucket
+    n-1 was issued (in order, identical on both ranks); the averaged result
+    equals the non-overlapped all-reduce; finish() forces the rest."""
+    port = _free_port()
+    mp.spawn(_worker_overlap, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r0 = json.load(open(tmp_path / "o0.json"))
+    r1 = json.load(open(tmp_path / "o1.json"))
+    f0 = r0["first"]
+    assert f0["log"] == r1["first"]["log"]
+    nb = r0["nb"]
+    assert [b for b, _ in f0["log"]] == list(range(nb))       # every bucket once, in order
+    assert all(pending == 0 for _, pending in f0["log"])      # never before its grads were final
+    # issued exactly when the bucket's last parameter reported
+    bo = f0["bucket_of"]
+    for i, n_issued in enumerate(f0["issued_after"]):
+        done = i == len(bo) - 1 or bo[i + 1] != bo[i]
+        assert n_issued == (bo[i] + 1 if done else bo[i])
+    for i, v in enumerate(f0["vals"]):
+        assert v == pytest.approx(1.5 * (i + 1))
+    s0 = r0["second"]
+    assert s0["partial"] <= 1 and [b for b, _ in s0["log"]] == list(range(nb))
+    assert all(v == pytest.approx(1.5) for v in s0["vals"])
