@@ -262,6 +262,17 @@ int qsync_gemm_s8_ex(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int
                      int c_dtype, const float* scale_a, const float* scale_b, int b_per_channel,
                      const float* bias, qsync_stream_t stream);
 
+/* Attention core softmax(Q K^T scale) V of an encoder layer (stays
+ * floating point), in the planned projections' formats: qkv packed
+ * [B, S, 3, H, D] FP16 (the QKV projection's output), out [B, S, H, D] FP16,
+ * lse [B, H, S] FP32 (row log-sum-exp, kept for the backward), out_absmax
+ * (optional, device float, overwritten) = absmax(out) for an INT8 O projection.
+ * Backward: dqkv packed like qkv from dout [B, S, H, D].  S = 128, D = 64. */
+int qsync_attention_fwd(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t D, float scale, void* out,
+                        float* lse, float* out_absmax, qsync_stream_t stream);
+int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, int64_t B,
+                        int64_t S, int64_t H, int64_t D, float scale, void* dqkv, qsync_stream_t stream);
+
 /* ---------------------------------------------------------------------------
  * Optimizer on FP32 master weights fused with the per-step weight preparation
  * of the planned kernels: AdamW (decoupled weight decay, bias-corrected, step

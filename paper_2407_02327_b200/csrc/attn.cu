@@ -1,0 +1,423 @@
+// attn.cu -- the encoder layer's attention core softmax(Q K^T * scale) V, forward
+// and backward, FP16 in / FP16 out with FP32 softmax statistics.  QSync leaves
+// this operator in floating point; it sits between the planned
+// QKV and O projections, so its I/O is in their formats:
+//   in : packed QKV [B, S, 3, H, D] FP16 (what the QKV projection emits)
+//   out: O [B, S, H, D] FP16 (+ optional absmax(O) for an INT8 O projection)
+//        and the row log-sum-exp [B, H, S] FP32 for the backward;
+//   bwd: dQKV packed [B, S, 3, H, D] FP16 (the QKV projection's FP16 dY).
+//
+// Sequence length 128, head dim 64 (BERT-base): one CTA owns one (batch, head),
+// the whole sequence fits on chip, so there is no online softmax and no
+// atomics.  8 warps; the tensor-core work is mma.sync m16n8k16 (FP16 x FP16 ->
+// FP32) on ldmatrix fragments of 128B-row tiles whose 16-byte chunks are
+// XOR-swizzled by row (conflict-free ldmatrix).  Forward: warp w owns query
+// rows 16w..16w+15.  Backward: phase 1 warp w owns key rows 16w.. and computes
+// S^T, P^T, dP^T, dS^T for all queries, accumulating dV = P^T dO and
+// dK = dS^T Q; dS^T goes to shared memory; phase 2 warp w owns query rows and
+// computes dQ = dS K.  HBM traffic per (b, h): fwd 3 x 16 KB in, 16 KB out;
+// bwd 5 x 16 KB in (Q, K, V, O, dO), 48 KB out.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace qsb {
+namespace {
+
+constexpr int kS = 128;
+constexpr int kD = 64;
+constexpr int kThreadsA = 256;
+constexpr int kTile = kS * kD * 2;  // bytes of one [128 x 64] FP16 tile
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// [rows x 64] FP16 tile, 128-byte rows of 8 chunks; chunk c of row r lives at c ^ (r & 7).
+__device__ __forceinline__ uint32_t t64(uint32_t base, int r, int c) {
+    return base + r * 128 + ((c ^ (r & 7)) << 4);
+}
+// [rows x 128] FP16 tile (256-byte rows, 16 chunks), same swizzle.
+__device__ __forceinline__ uint32_t t128(uint32_t base, int r, int c) {
+    return base + r * 256 + ((c ^ (r & 7)) << 4);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Copy a [128 x 64] FP16 tile (global row stride `rs` elements) into a swizzled smem tile.
+__device__ __forceinline__ void load_tile(uint32_t sbase, const __half* g, int64_t rs) {
+    for (int i = threadIdx.x; i < kS * 8; i += kThreadsA) {
+        const int r = i >> 3, c = i & 7;
+        cp_async16(t64(sbase, r, c), g + r * rs + c * 8);
+    }
+}
+
+// A-operand fragments (16 x 16 at rows r0, k-step ks) of a row-major tile.
+__device__ __forceinline__ void frag_a(uint32_t base, int r0, int ks, int lane, uint32_t (&a)[4]) {
+    ldsm4(t64(base, r0 + (lane & 15), 2 * ks + (lane >> 4)), a);
+}
+// B-operand fragments for n-tiles n0 and n0+8 at k-step ks from a tile stored
+// [n][k] (rows = n): {b0(n0), b1(n0), b0(n0+8), b1(n0+8)}.
+__device__ __forceinline__ void frag_b_nk(uint32_t base, int n0, int ks, int lane, uint32_t (&b)[4]) {
+    ldsm4(t64(base, n0 + (lane & 7) + ((lane >> 4) << 3), 2 * ks + ((lane >> 3) & 1)), b);
+}
+// B-operand fragments for n-tiles n0, n0+8 at k rows k0.. from a tile stored
+// [k][n] (rows = k): transposing ldmatrix.
+__device__ __forceinline__ void frag_b_kn(uint32_t base, int k0, int n0, int lane, uint32_t (&b)[4]) {
+    ldsm4t(t64(base, k0 + (lane & 7) + (((lane >> 3) & 1) << 3), (n0 >> 3) + (lane >> 4)), b);
+}
+
+__device__ __forceinline__ uint32_t pk(float a, float b) { return pack_half2(a, b); }
+
+// ---------------------------------------------------------------------------- forward
+__global__ void __launch_bounds__(kThreadsA) k_attn_fwd(const __half* __restrict__ qkv, int H, float scale,
+                                                        __half* __restrict__ out, float* __restrict__ lse,
+                                                        unsigned* __restrict__ out_absmax) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int bh = blockIdx.x;
+    const int b = bh / H, h = bh % H;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t sQ = smem_addr(sm), sK = sQ + kTile, sV = sK + kTile;
+    const int64_t rs = 3LL * H * kD;                         // packed row stride
+    const __half* base = qkv + static_cast<int64_t>(b) * kS * rs + static_cast<int64_t>(h) * kD;
+    load_tile(sQ, base, rs);
+    load_tile(sK, base + H * kD, rs);
+    load_tile(sV, base + 2 * H * kD, rs);
+    cp_async_wait_all();
+    __syncthreads();
+
+    const int m0 = warp * 16;
+    uint32_t qa[4][4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) frag_a(sQ, m0, ks, lane, qa[ks]);
+    float s[16][4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+        for (int np = 0; np < 8; ++np) {
+            uint32_t bf[4];
+            frag_b_nk(sK, 16 * np, ks, lane, bf);
+            mma16816(s[2 * np], qa[ks], bf[0], bf[1]);
+            mma16816(s[2 * np + 1], qa[ks], bf[2], bf[3]);
+        }
+    }
+    // Row softmax (rows g and g+8 of this warp's 16), scores scaled by `scale`.
+    const float sl2 = scale * kLog2e;
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        mx0 = fmaxf(mx0, fmaxf(s[j][0], s[j][1]));
+        mx1 = fmaxf(mx1, fmaxf(s[j][2], s[j][3]));
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    float sum0 = 0.f, sum1 = 0.f;
+    uint32_t pa[8][4];  // P as A fragments (FP16), keys 16kk.. per k-step
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const float p0 = exp2f(s[j][0] * sl2 - mx0 * sl2), p1 = exp2f(s[j][1] * sl2 - mx0 * sl2);
+        const float p2 = exp2f(s[j][2] * sl2 - mx1 * sl2), p3 = exp2f(s[j][3] * sl2 - mx1 * sl2);
+        sum0 += p0 + p1;
+        sum1 += p2 + p3;
+        pa[j >> 1][(j & 1) * 2] = pk(p0, p1);
+        pa[j >> 1][(j & 1) * 2 + 1] = pk(p2, p3);
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        sum0 += __shfl_xor_sync(0xffffffffu, sum0, o);
+        sum1 += __shfl_xor_sync(0xffffffffu, sum1, o);
+    }
+    float oacc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        // pa[kk] = {row g keys 2t.., row g+8 keys 2t.., row g keys 8+2t.., row g+8 keys 8+2t..}
+        const uint32_t a[4] = {pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3]};
+#pragma unroll
+        for (int np = 0; np < 4; ++np) {
+            uint32_t bf[4];
+            frag_b_kn(sV, 16 * kk, 16 * np, lane, bf);
+            mma16816(oacc[2 * np], a, bf[0], bf[1]);
+            mma16816(oacc[2 * np + 1], a, bf[2], bf[3]);
+        }
+    }
+    const float inv0 = 1.f / sum0, inv1 = 1.f / sum1;
+    const int64_t orow = static_cast<int64_t>(H) * kD;
+    __half* o0 = out + (static_cast<int64_t>(b) * kS + m0 + g) * orow + static_cast<int64_t>(h) * kD;
+    __half* o1 = o0 + 8 * orow;
+    float amax = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t w0 = pk(oacc[j][0] * inv0, oacc[j][1] * inv0);
+        const uint32_t w1 = pk(oacc[j][2] * inv1, oacc[j][3] * inv1);
+        *reinterpret_cast<uint32_t*>(o0 + 8 * j + 2 * t) = w0;
+        *reinterpret_cast<uint32_t*>(o1 + 8 * j + 2 * t) = w1;
+        if (out_absmax) {
+            const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&w0));
+            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&w1));
+            amax = fmaxf(amax, fmaxf(fmaxf(fabsf(f0.x), fabsf(f0.y)), fmaxf(fabsf(f1.x), fabsf(f1.y))));
+        }
+    }
+    if (t == 0) {
+        float* l = lse + static_cast<int64_t>(bh) * kS + m0;
+        l[g] = mx0 * scale + logf(sum0);
+        l[g + 8] = mx1 * scale + logf(sum1);
+    }
+    if (out_absmax) {
+        __shared__ float wm[8];
+        amax = warp_max(amax);
+        if (lane == 0) wm[warp] = amax;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            amax = warp_max(threadIdx.x < 8 ? wm[threadIdx.x] : 0.f);
+            if (threadIdx.x == 0 && amax > 0.f) atomicMax(out_absmax, __float_as_uint(amax));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- backward
+__global__ void __launch_bounds__(kThreadsA) k_attn_bwd(const __half* __restrict__ qkv,
+                                                        const __half* __restrict__ out,
+                                                        const __half* __restrict__ dout,
+                                                        const float* __restrict__ lse, int H, float scale,
+                                                        __half* __restrict__ dqkv) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int bh = blockIdx.x;
+    const int b = bh / H, h = bh % H;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t sQ = smem_addr(sm), sK = sQ + kTile, sV = sK + kTile, sdO = sV + kTile;
+    const uint32_t sdST = sdO + kTile;                              // [128 keys x 128 queries] FP16
+    float* lse_s = reinterpret_cast<float*>(sm + 4 * kTile + 2 * kTile);
+    float* d_s = lse_s + kS;
+    const int64_t rs = 3LL * H * kD;
+    const int64_t orow = static_cast<int64_t>(H) * kD;
+    const __half* base = qkv + static_cast<int64_t>(b) * kS * rs + static_cast<int64_t>(h) * kD;
+    const __half* obase = out + static_cast<int64_t>(b) * kS * orow + static_cast<int64_t>(h) * kD;
+    const __half* dobase = dout + static_cast<int64_t>(b) * kS * orow + static_cast<int64_t>(h) * kD;
+    load_tile(sQ, base, rs);
+    load_tile(sK, base + H * kD, rs);
+    load_tile(sV, base + 2 * H * kD, rs);
+    load_tile(sdO, dobase, orow);
+    // D[q] = sum_d dO[q, d] O[q, d]  (two threads per query row)
+    {
+        const int q = threadIdx.x >> 1, hf = threadIdx.x & 1;
+        const uint4* op = reinterpret_cast<const uint4*>(obase + q * orow + hf * 32);
+        const uint4* dp = reinterpret_cast<const uint4*>(dobase + q * orow + hf * 32);
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint4 ov = op[i], dv = dp[i];
+            const __half2* oh = reinterpret_cast<const __half2*>(&ov);
+            const __half2* dh = reinterpret_cast<const __half2*>(&dv);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 a = __half22float2(oh[e]), c = __half22float2(dh[e]);
+                acc += a.x * c.x + a.y * c.y;
+            }
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (hf == 0) d_s[q] = acc;
+        if (threadIdx.x < kS) lse_s[threadIdx.x] = lse[static_cast<int64_t>(bh) * kS + threadIdx.x] * kLog2e;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    const float sl2 = scale * kLog2e;
+    // ---- phase 1: warp w owns key rows k0 = 16w
+    {
+        const int k0 = warp * 16;
+        uint32_t ka[4][4], va[4][4];
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            frag_a(sK, k0, ks, lane, ka[ks]);
+            frag_a(sV, k0, ks, lane, va[ks]);
+        }
+        float dv[8][4], dk[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
+            dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = 0.f;
+        }
+#pragma unroll 1
+        for (int qc = 0; qc < 4; ++qc) {  // 32 queries per chunk (4 n-tiles)
+            float st[4][4], dpt[4][4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                st[j][0] = st[j][1] = st[j][2] = st[j][3] = 0.f;
+                dpt[j][0] = dpt[j][1] = dpt[j][2] = dpt[j][3] = 0.f;
+            }
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+                for (int np = 0; np < 2; ++np) {
+                    uint32_t bq[4], bo[4];
+                    frag_b_nk(sQ, 32 * qc + 16 * np, ks, lane, bq);
+                    frag_b_nk(sdO, 32 * qc + 16 * np, ks, lane, bo);
+                    mma16816(st[2 * np], ka[ks], bq[0], bq[1]);
+                    mma16816(st[2 * np + 1], ka[ks], bq[2], bq[3]);
+                    mma16816(dpt[2 * np], va[ks], bo[0], bo[1]);
+                    mma16816(dpt[2 * np + 1], va[ks], bo[2], bo[3]);
+                }
+            }
+            // P^T = exp(S^T scale - lse[q]), dS^T = P^T (dP^T - D[q]); columns are queries.
+            uint32_t pa[2][4], dsa[2][4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int q = 32 * qc + 8 * j + 2 * t;
+                const float l0 = lse_s[q], l1 = lse_s[q + 1];
+                const float d0 = d_s[q], d1 = d_s[q + 1];
+                const float p0 = exp2f(st[j][0] * sl2 - l0), p1 = exp2f(st[j][1] * sl2 - l1);
+                const float p2 = exp2f(st[j][2] * sl2 - l0), p3 = exp2f(st[j][3] * sl2 - l1);
+                const float s0 = p0 * (dpt[j][0] - d0), s1 = p1 * (dpt[j][1] - d1);
+                const float s2 = p2 * (dpt[j][2] - d0), s3 = p3 * (dpt[j][3] - d1);
+                pa[j >> 1][(j & 1) * 2] = pk(p0, p1);
+                pa[j >> 1][(j & 1) * 2 + 1] = pk(p2, p3);
+                const uint32_t w01 = pk(s0, s1), w23 = pk(s2, s3);
+                dsa[j >> 1][(j & 1) * 2] = w01;
+                dsa[j >> 1][(j & 1) * 2 + 1] = w23;
+                // dS^T rows k0+g, k0+g+8, columns q, q+1 -> shared [key][query]
+                const int c = q >> 3, e = (q & 7) * 2;
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(t128(sdST, k0 + g, c) + e), "r"(w01));
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(t128(sdST, k0 + g + 8, c) + e), "r"(w23));
+            }
+            // dV += P^T dO, dK += dS^T Q over this chunk's 32 queries (2 k-steps).
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                const uint32_t ap[4] = {pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3]};
+                const uint32_t as[4] = {dsa[kk][0], dsa[kk][1], dsa[kk][2], dsa[kk][3]};
+                const int qr = 32 * qc + 16 * kk;
+#pragma unroll
+                for (int np = 0; np < 4; ++np) {
+                    uint32_t bo[4], bq[4];
+                    frag_b_kn(sdO, qr, 16 * np, lane, bo);
+                    frag_b_kn(sQ, qr, 16 * np, lane, bq);
+                    mma16816(dv[2 * np], ap, bo[0], bo[1]);
+                    mma16816(dv[2 * np + 1], ap, bo[2], bo[3]);
+                    mma16816(dk[2 * np], as, bq[0], bq[1]);
+                    mma16816(dk[2 * np + 1], as, bq[2], bq[3]);
+                }
+            }
+        }
+        __half* dk0 = dqkv + (static_cast<int64_t>(b) * kS + k0 + g) * rs + H * kD + static_cast<int64_t>(h) * kD;
+        __half* dv0 = dk0 + H * kD;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            *reinterpret_cast<uint32_t*>(dk0 + 8 * j + 2 * t) = pk(dk[j][0] * scale, dk[j][1] * scale);
+            *reinterpret_cast<uint32_t*>(dk0 + 8 * rs + 8 * j + 2 * t) = pk(dk[j][2] * scale, dk[j][3] * scale);
+            *reinterpret_cast<uint32_t*>(dv0 + 8 * j + 2 * t) = pk(dv[j][0], dv[j][1]);
+            *reinterpret_cast<uint32_t*>(dv0 + 8 * rs + 8 * j + 2 * t) = pk(dv[j][2], dv[j][3]);
+        }
+    }
+    __syncthreads();
+    // ---- phase 2: warp w owns query rows m0 = 16w: dQ = dS K scale
+    {
+        const int m0 = warp * 16;
+        float dq[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            // A = dS[m0.., keys 16kk..] read transposed from dS^T [key][query]
+            uint32_t a[4];
+            ldsm4t(t128(sdST, 16 * kk + (lane & 7) + ((lane >> 4) << 3), (m0 >> 3) + ((lane >> 3) & 1)), a);
+#pragma unroll
+            for (int np = 0; np < 4; ++np) {
+                uint32_t bk[4];
+                frag_b_kn(sK, 16 * kk, 16 * np, lane, bk);
+                mma16816(dq[2 * np], a, bk[0], bk[1]);
+                mma16816(dq[2 * np + 1], a, bk[2], bk[3]);
+            }
+        }
+        __half* dq0 = dqkv + (static_cast<int64_t>(b) * kS + m0 + g) * rs + static_cast<int64_t>(h) * kD;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            *reinterpret_cast<uint32_t*>(dq0 + 8 * j + 2 * t) = pk(dq[j][0] * scale, dq[j][1] * scale);
+            *reinterpret_cast<uint32_t*>(dq0 + 8 * rs + 8 * j + 2 * t) = pk(dq[j][2] * scale, dq[j][3] * scale);
+        }
+    }
+}
+
+constexpr int kFwdSmem = 3 * kTile;
+constexpr int kBwdSmem = 4 * kTile + 2 * kTile + 2 * kS * 4;
+
+int check_shape(int64_t B, int64_t S, int64_t H, int64_t D) {
+    QSB_REQUIRE(S == kS && D == kD, QSYNC_ERR_DOMAIN,
+                "attention core supports seq 128, head dim 64 (got seq " + std::to_string(S) + ", dim " +
+                    std::to_string(D) + ")");
+    QSB_REQUIRE(B > 0 && H > 0 && B * H < (int64_t(1) << 31), QSYNC_ERR_DOMAIN, "bad batch / head count");
+    return QSYNC_OK;
+}
+
+}  // namespace
+}  // namespace qsb
+
+using namespace qsb;
+
+extern "C" {
+
+int qsync_attention_fwd(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t D, float scale, void* out,
+                        float* lse, float* out_absmax, qsync_stream_t stream) {
+    QSB_REQUIRE(qkv && out && lse, QSYNC_ERR_VALIDATION, "attention needs qkv, out and lse buffers");
+    QSB_TRY(check_shape(B, S, H, D));
+    cudaStream_t st = to_stream(stream);
+    static bool configured = false;
+    if (!configured) {
+        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem),
+                            "cudaFuncSetAttribute"));
+        configured = true;
+    }
+    if (out_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(out_absmax, 0, sizeof(float), st), "memset"));
+    k_attn_fwd<<<static_cast<unsigned>(B * H), kThreadsA, kFwdSmem, st>>>(
+        static_cast<const __half*>(qkv), static_cast<int>(H), scale, static_cast<__half*>(out), lse,
+        reinterpret_cast<unsigned*>(out_absmax));
+    return check_launch("k_attn_fwd");
+}
+
+int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, int64_t B,
+                        int64_t S, int64_t H, int64_t D, float scale, void* dqkv, qsync_stream_t stream) {
+    QSB_REQUIRE(qkv && out && dout && lse && dqkv, QSYNC_ERR_VALIDATION, "attention backward needs all buffers");
+    QSB_TRY(check_shape(B, S, H, D));
+    cudaStream_t st = to_stream(stream);
+    static bool configured = false;
+    if (!configured) {
+        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem),
+                            "cudaFuncSetAttribute"));
+        configured = true;
+    }
+    k_attn_bwd<<<static_cast<unsigned>(B * H), kThreadsA, kBwdSmem, st>>>(
+        static_cast<const __half*>(qkv), static_cast<const __half*>(out), static_cast<const __half*>(dout), lse,
+        static_cast<int>(H), scale, static_cast<__half*>(dqkv));
+    return check_launch("k_attn_bwd");
+}
+
+}  // extern "C"

@@ -10,7 +10,9 @@ forward, per planned op P (INT8 / FP16 / FP32; precision.hpp:12):
     format: FP16(y) for an FP16 op, absmax(y) for an INT8 op (its per-tensor
     quantizer is then one pass) -- ``layernorm_fwd_ex``;
   * an INT8 QKV projection writes its dequantized output as FP16 straight from
-    the GEMM epilogue (the attention core is FP16; PAPER.md:399);
+    the GEMM epilogue; the attention core (FP16) is this
+    package's kernel (csrc/attn.cu), reading the packed QKV as the projection
+    wrote it and emitting absmax(out) for an INT8 O projection;
   * GELU is applied inside the FF2 operand kernel: absmax(gelu(h)) then
     quantize(gelu(h)) for INT8, cast(gelu(h)) for FP16 -- the FP32 GELU output
     is never materialised;
@@ -38,8 +40,6 @@ import ctypes as C
 import numpy as np
 import torch
 import torch.nn.functional as F
-from flash_attn.flash_attn_interface import (_wrapped_flash_attn_backward,
-                                             _wrapped_flash_attn_forward)
 
 from . import ops
 from . import qlinear as _ql
@@ -241,15 +241,13 @@ class _FusedLayerFn(torch.autograd.Function):
         if qkv.dtype != torch.float16:
             qkv = ops.cast(qkv, torch.float16)
         qkv5 = qkv.view(B, S, 3, nh, H // nh)
-        q, k, v = qkv5[:, :, 0], qkv5[:, :, 1], qkv5[:, :, 2]
         scale = (H // nh) ** -0.5
-        a, lse, _, rng = _wrapped_flash_attn_forward(q, k, v, 0.0, scale, causal=False,
-                                                     window_size_left=-1, window_size_right=-1,
-                                                     softcap=0.0, alibi_slopes=None,
-                                                     return_softmax=False)
+        # Attention core (FP16, csrc/attn.cu); it also emits absmax(out) when the
+        # O projection is INT8, so that op's quantizer is one pass.
+        a, lse, a_am = ops.attention_fwd(qkv5, scale, want_absmax=po == INT8)
         a2 = a.reshape(M, H)
         # --- output projection + residual LayerNorm (emits FF1's operand)
-        op_o = _operand(a2, None, po)
+        op_o = _operand(a2, a_am, po)
         yo, w16_o = _linear_fwd(L.o, op_o)
         f16, am = _need_aux(p1)
         x1, s1, mean1, rstd1, x1_16, x1_am = ops.layernorm_fwd_ex(
@@ -274,7 +272,7 @@ class _FusedLayerFn(torch.autograd.Function):
         ctx.layer = L
         ctx.ops_ = (op_qkv, op_o, op_1, op_2)
         ctx.w16 = (w16_qkv, w16_o, w16_1, w16_2)
-        ctx.attn = (q, k, v, a, lse, rng, scale)
+        ctx.attn = (qkv5, a, lse, scale)
         ctx.ln = (s1, mean1, rstd1, s2, mean2, rstd2)
         ctx.h = h
         ctx.shape = (B, S, H)
@@ -291,7 +289,7 @@ class _FusedLayerFn(torch.autograd.Function):
         M = B * S
         op_qkv, op_o, op_1, op_2 = ctx.ops_
         w16_qkv, w16_o, w16_1, w16_2 = ctx.w16
-        q, k, v, a, lse, rng, scale = ctx.attn
+        qkv5, a, lse, scale = ctx.attn
         s1, mean1, rstd1, s2, mean2, rstd2 = ctx.ln
         h = ctx.h
         side = _ql.WGRAD_STREAM
@@ -323,11 +321,7 @@ class _FusedLayerFn(torch.autograd.Function):
         da = _dgrad(L.o, dyo, w16_o, torch.float16)
         _wgrad(L.o, dyo, op_o, side if po != FP32 else None)
         # --- attention core backward (FP16) -> packed dQKV
-        nh = L.cfg.heads
-        dqkv = torch.empty((B, S, 3, nh, H // nh), device=da.device, dtype=torch.float16)
-        _wrapped_flash_attn_backward(da.view(B, S, nh, H // nh), q, k, v, a, lse,
-                                     dqkv[:, :, 0], dqkv[:, :, 1], dqkv[:, :, 2], 0.0, scale,
-                                     False, -1, -1, 0.0, None, False, rng_state=rng)
+        dqkv = ops.attention_bwd(qkv5, a, da.view(a.shape), lse, scale)
         dqkv2 = dqkv.view(M, 3 * H)
         # --- QKV backward: bias grad (column sums), dgrad reduce-added into ds1
         pq = L.qkv.precision

@@ -1,5 +1,6 @@
 """Glue between planned operators, on this package's kernels: fused
-residual-add + LayerNorm (the post-LN of every encoder sublayer)."""
+residual-add + LayerNorm (the post-LN of every encoder sublayer) and the
+attention core (softmax(Q K^T scale) V on the packed QKV, csrc/attn.cu)."""
 from __future__ import annotations
 
 import torch
@@ -44,3 +45,24 @@ class AddLayerNorm(torch.nn.Module):
 
     def forward(self, a, b=None):
         return _AddLayerNorm.apply(a, b, self.weight, self.bias, self.eps)
+
+
+class _Attention(torch.autograd.Function):
+    """Attention core on packed QKV [B, S, 3, H, D] FP16 -> [B, S, H, D] FP16
+    (the attention core stays floating point)."""
+
+    @staticmethod
+    def forward(ctx, qkv):
+        qkv = qkv.contiguous()
+        out, lse, _ = ops.attention_fwd(qkv)
+        ctx.save_for_backward(qkv, out, lse)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        qkv, out, lse = ctx.saved_tensors
+        return ops.attention_bwd(qkv, out, dout.contiguous(), lse)
+
+
+def attention(qkv: torch.Tensor) -> torch.Tensor:
+    return _Attention.apply(qkv)

@@ -423,6 +423,32 @@ def gemm_s8_ex(a: torch.Tensor, b: torch.Tensor, scale_a, scale_b, bias=None,
     return c
 
 
+def attention_fwd(qkv: torch.Tensor, scale: float | None = None, want_absmax: bool = False):
+    """Attention core on packed QKV [B, S, 3, H, D] FP16 -> (out [B, S, H, D] FP16,
+    lse [B, H, S] FP32, absmax(out) device float[1] or None)."""
+    _req(qkv, "qkv", (torch.float16,))
+    B, S, _, H, D = qkv.shape
+    scale = D ** -0.5 if scale is None else scale
+    out = torch.empty((B, S, H, D), device=qkv.device, dtype=torch.float16)
+    lse = torch.empty((B, H, S), device=qkv.device, dtype=torch.float32)
+    am = torch.empty(1, device=qkv.device, dtype=torch.float32) if want_absmax else None
+    call("qsync_attention_fwd", _ptr(qkv), B, S, H, D, float(scale), _ptr(out), _ptr(lse), _ptr(am), _stream())
+    return out, lse, am
+
+
+def attention_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor,
+                  scale: float | None = None) -> torch.Tensor:
+    """dQKV (packed like qkv) of the attention core."""
+    _req(qkv, "qkv", (torch.float16,))
+    _req(dout, "dout", (torch.float16,))
+    B, S, _, H, D = qkv.shape
+    scale = D ** -0.5 if scale is None else scale
+    dqkv = torch.empty_like(qkv)
+    call("qsync_attention_bwd", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), B, S, H, D, float(scale),
+         _ptr(dqkv), _stream())
+    return dqkv
+
+
 def launch_count() -> int:
     """Kernels launched by libqsync_b200 so far in this process."""
     return int(_lib.lib().qsync_launch_count())

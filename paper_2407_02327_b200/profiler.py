@@ -145,9 +145,7 @@ def measure_linear(M: int, N: int, K: int, precision: str, reps: int = 10) -> di
 
 def measure_glue(cfg: BertConfig, batch: int, reps: int = 10) -> dict:
     """Costs of the fixed / dependent operators (their FP32 or FP16 kernels)."""
-    from flash_attn import flash_attn_qkvpacked_func
-
-    from .glue import AddLayerNorm
+    from .glue import AddLayerNorm, attention
     T, H, Fh = batch * cfg.seq, cfg.hidden, cfg.ffn
     out = {}
     qkv = torch.randn(batch, cfg.seq, 3, cfg.heads, H // cfg.heads, device="cuda",
@@ -155,7 +153,7 @@ def measure_glue(cfg: BertConfig, batch: int, reps: int = 10) -> dict:
     g = torch.randn(batch, cfg.seq, cfg.heads, H // cfg.heads, device="cuda", dtype=torch.float16)
 
     def attn():
-        flash_attn_qkvpacked_func(qkv).backward(g)
+        attention(qkv).backward(g)
     t = _time_ns(attn, reps)
     out["attn"] = {FP32: {"pure_cost_ns": t, "fwd_fraction": 1.0 / 3.0,
                           "memory_bytes": T * 3 * H * 2 + T * H * 2}}

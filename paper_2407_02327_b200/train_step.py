@@ -24,10 +24,9 @@ from dataclasses import dataclass
 
 import torch
 import torch.nn.functional as F
-from flash_attn import flash_attn_qkvpacked_func
 
 from . import qlinear as _ql
-from .glue import AddLayerNorm
+from .glue import AddLayerNorm, attention
 from .qlinear import FP16, FP32, INT8, QLinear, cast
 
 
@@ -105,7 +104,7 @@ class EncoderLayer(torch.nn.Module):
         qkv = cast(qkv, torch.float16)
         # Attention core stays floating point; packed QKV in,
         # packed dQKV out -- no permute/stack copies around it.
-        a = flash_attn_qkvpacked_func(qkv.view(B, S, 3, nh, H // nh))  # [B, S, nh, d]
+        a = attention(qkv.view(B, S, 3, nh, H // nh))  # [B, S, nh, d]
         a = a.reshape(B, S, H)
         x = self.ln1(x, self.o(a))        # fused residual add (FP32 or FP16 operand)
         f = F.gelu(self.ff1(x))
