@@ -48,6 +48,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -103,10 +106,13 @@ __global__ void __launch_bounds__(kThreadsA) k_attn_fwd(const __half* __restrict
     const uint32_t sQ = smem_addr(sm), sK = sQ + kTile, sV = sK + kTile;
     const int64_t rs = 3LL * H * kD;                         // packed row stride
     const __half* base = qkv + static_cast<int64_t>(b) * kS * rs + static_cast<int64_t>(h) * kD;
+    // Q and K first; V streams in while Q K^T and the softmax run.
     load_tile(sQ, base, rs);
     load_tile(sK, base + H * kD, rs);
+    cp_async_commit();
     load_tile(sV, base + 2 * H * kD, rs);
-    cp_async_wait_all();
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
 
     const int m0 = warp * 16;
@@ -155,6 +161,8 @@ __global__ void __launch_bounds__(kThreadsA) k_attn_fwd(const __half* __restrict
         sum0 += __shfl_xor_sync(0xffffffffu, sum0, o);
         sum1 += __shfl_xor_sync(0xffffffffu, sum1, o);
     }
+    cp_async_wait<0>();
+    __syncthreads();
     float oacc[8][4];
 #pragma unroll
     for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
@@ -205,7 +213,7 @@ __global__ void __launch_bounds__(kThreadsA) k_attn_fwd(const __half* __restrict
 }
 
 // ---------------------------------------------------------------------------- backward
-__global__ void __launch_bounds__(kThreadsA) k_attn_bwd(const __half* __restrict__ qkv,
+__global__ void __launch_bounds__(kThreadsA, 2) k_attn_bwd(const __half* __restrict__ qkv,
                                                         const __half* __restrict__ out,
                                                         const __half* __restrict__ dout,
                                                         const float* __restrict__ lse, int H, float scale,
@@ -256,12 +264,6 @@ __global__ void __launch_bounds__(kThreadsA) k_attn_bwd(const __half* __restrict
     // ---- phase 1: warp w owns key rows k0 = 16w
     {
         const int k0 = warp * 16;
-        uint32_t ka[4][4], va[4][4];
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-            frag_a(sK, k0, ks, lane, ka[ks]);
-            frag_a(sV, k0, ks, lane, va[ks]);
-        }
         float dv[8][4], dk[8][4];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -278,15 +280,18 @@ __global__ void __launch_bounds__(kThreadsA) k_attn_bwd(const __half* __restrict
             }
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
+                uint32_t ka[4], va[4];  // re-read per k-step: keeps the kernel at 2 CTAs / SM
+                frag_a(sK, k0, ks, lane, ka);
+                frag_a(sV, k0, ks, lane, va);
 #pragma unroll
                 for (int np = 0; np < 2; ++np) {
                     uint32_t bq[4], bo[4];
                     frag_b_nk(sQ, 32 * qc + 16 * np, ks, lane, bq);
                     frag_b_nk(sdO, 32 * qc + 16 * np, ks, lane, bo);
-                    mma16816(st[2 * np], ka[ks], bq[0], bq[1]);
-                    mma16816(st[2 * np + 1], ka[ks], bq[2], bq[3]);
-                    mma16816(dpt[2 * np], va[ks], bo[0], bo[1]);
-                    mma16816(dpt[2 * np + 1], va[ks], bo[2], bo[3]);
+                    mma16816(st[2 * np], ka, bq[0], bq[1]);
+                    mma16816(st[2 * np + 1], ka, bq[2], bq[3]);
+                    mma16816(dpt[2 * np], va, bo[0], bo[1]);
+                    mma16816(dpt[2 * np + 1], va, bo[2], bo[3]);
                 }
             }
             // P^T = exp(S^T scale - lse[q]), dS^T = P^T (dP^T - D[q]); columns are queries.

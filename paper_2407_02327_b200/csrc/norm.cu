@@ -196,6 +196,106 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
     }
 }
 
+// Same LN backward with each row split over a warp PAIR (NV even): every lane
+// owns NV/2 float4 columns, which halves the per-lane column accumulators and
+// brings the kernel to 2 blocks / SM.  The two halves' row sums are exchanged
+// through shared memory under a 64-thread named barrier.
+template <int NV>
+__global__ void __launch_bounds__(256, 2) k_ln_bwd2(const float* __restrict__ dy,
+                                                    const float* __restrict__ s,
+                                                    const float* __restrict__ mean_in,
+                                                    const float* __restrict__ rstd_in,
+                                                    const float* __restrict__ gamma, int64_t rows,
+                                                    int cols, float* __restrict__ dx,
+                                                    float* __restrict__ dgamma,
+                                                    float* __restrict__ dbeta,
+                                                    __half* __restrict__ dx16,
+                                                    float* __restrict__ dcol) {
+    constexpr int NH = NV / 2;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int pair = warp >> 1, half = warp & 1;
+    const int cbase = half * NH * 128;  // first column of this warp's half
+    const int64_t pairs = (int64_t)gridDim.x * 4;
+    float4 g[NH], acc_g[NH], acc_b[NH], acc_c[NH];
+#pragma unroll
+    for (int i = 0; i < NH; ++i) {
+        g[i] = reinterpret_cast<const float4*>(gamma + cbase)[lane + 32 * i];
+        acc_g[i] = acc_b[i] = acc_c[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float inv_n = 1.0f / static_cast<float>(cols);
+    int parity = 0;
+    for (int64_t row = blockIdx.x * (int64_t)4 + pair; row < rows; row += pairs) {
+        const float mean = mean_in[row], rstd = rstd_in[row];
+        float4 xh[NH], gy[NH];
+        float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+            const int64_t off = row * cols + cbase + 4 * (lane + 32 * i);
+            const float4 d = *reinterpret_cast<const float4*>(dy + off);
+            const float4 x = *reinterpret_cast<const float4*>(s + off);
+            xh[i] = make_float4((x.x - mean) * rstd, (x.y - mean) * rstd, (x.z - mean) * rstd,
+                                (x.w - mean) * rstd);
+            gy[i] = make_float4(d.x * g[i].x, d.y * g[i].y, d.z * g[i].z, d.w * g[i].w);
+            s1 += (gy[i].x + gy[i].y) + (gy[i].z + gy[i].w);
+            s2 += (gy[i].x * xh[i].x + gy[i].y * xh[i].y) + (gy[i].z * xh[i].z + gy[i].w * xh[i].w);
+            acc_g[i].x += d.x * xh[i].x; acc_g[i].y += d.y * xh[i].y;
+            acc_g[i].z += d.z * xh[i].z; acc_g[i].w += d.w * xh[i].w;
+            acc_b[i].x += d.x; acc_b[i].y += d.y; acc_b[i].z += d.z; acc_b[i].w += d.w;
+        }
+        s1 = warp_sum_f<NV>(s1);
+        s2 = warp_sum_f<NV>(s2);
+        // exchange with the partner warp (double-buffered by row parity)
+        __shared__ float xb[2][4][2][2];
+        if (lane == 0) {
+            xb[parity][pair][half][0] = s1;
+            xb[parity][pair][half][1] = s2;
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+        s1 += xb[parity][pair][half ^ 1][0];
+        s2 += xb[parity][pair][half ^ 1][1];
+        parity ^= 1;
+        const float m1 = s1 * inv_n;
+        const float m2 = s2 * inv_n;
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+            const int64_t off = row * cols + cbase + 4 * (lane + 32 * i);
+            float4 o;
+            o.x = rstd * (gy[i].x - m1 - xh[i].x * m2);
+            o.y = rstd * (gy[i].y - m1 - xh[i].y * m2);
+            o.z = rstd * (gy[i].z - m1 - xh[i].z * m2);
+            o.w = rstd * (gy[i].w - m1 - xh[i].w * m2);
+            *reinterpret_cast<float4*>(dx + off) = o;
+            if (dx16) {
+                uint2 h;
+                h.x = pack_half2(o.x, o.y);
+                h.y = pack_half2(o.z, o.w);
+                *reinterpret_cast<uint2*>(dx16 + off) = h;
+            }
+            acc_c[i].x += o.x; acc_c[i].y += o.y; acc_c[i].z += o.z; acc_c[i].w += o.w;
+        }
+    }
+    // Column partials: 4 pairs per block, reduced through shared memory.
+    __shared__ float red[4][1024 + 4];
+#pragma unroll
+    for (int pass = 0; pass < 3; ++pass) {
+        float* outp = pass == 0 ? dgamma : (pass == 1 ? dbeta : dcol);
+        if (pass == 2 && !dcol) break;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+            const float4 v = pass == 0 ? acc_g[i] : (pass == 1 ? acc_b[i] : acc_c[i]);
+            const int c = cbase + 4 * (lane + 32 * i);
+            red[pair][c] = v.x; red[pair][c + 1] = v.y; red[pair][c + 2] = v.z; red[pair][c + 3] = v.w;
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+            const float t = (red[0][c] + red[1][c]) + (red[2][c] + red[3][c]);
+            if (outp) atomicAdd(outp + c, t);
+        }
+    }
+}
+
 template <int NV>
 int ln_fwd_nv(const float* a, const void* b, int b_dtype, const float* gamma, const float* beta,
               int64_t rows, int cols, float eps, float* s_out, float* y, float* mean, float* rstd,
@@ -219,6 +319,12 @@ template <int NV>
 int ln_bwd_nv(const float* dy, const float* s, const float* mean, const float* rstd,
               const float* gamma, int64_t rows, int cols, float* dx, float* dgamma, float* dbeta,
               uint16_t* dx16, float* dcol, cudaStream_t st) {
+    if constexpr (NV % 2 == 0) {
+        const int grid = static_cast<int>(std::min<int64_t>((rows + 3) / 4, sm_count() * 4LL));
+        k_ln_bwd2<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
+                                             reinterpret_cast<__half*>(dx16), dcol);
+        return check_launch("k_ln_bwd");
+    }
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 2LL));
     k_ln_bwd<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
                                         reinterpret_cast<__half*>(dx16), dcol);

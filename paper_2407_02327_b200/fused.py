@@ -280,6 +280,7 @@ class _FusedLayerFn(torch.autograd.Function):
         if aux2 is None:
             aux2 = torch.empty(0, device=x0.device)
         ctx.mark_non_differentiable(aux2)
+        ctx.set_materialize_grads(False)  # no zero-filled gradient for the aux output
         return out, aux2
 
     @staticmethod
