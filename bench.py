@@ -48,6 +48,27 @@ def _peaks() -> dict:
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def _ncu_traffic(prefix: str, shapes) -> float | None:
+    """Mean per-launch DRAM traffic (read + write bytes) of a kernel at the step's
+    shapes, from the committed `ncu --set full` capture (profiles/*_ncu_metrics.json,
+    written by tools/summarize_round.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_metrics.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        m = json.load(f)
+    sc = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    vals = []
+    for s in shapes:
+        d = m.get(f"{prefix}_{s}")
+        if not d or "dram__bytes_read.sum" not in d:
+            return None
+        vals.append(d["dram__bytes_read.sum"] * sc.get(d.get("dram__bytes_read.sum.unit"), 1.0)
+                    + d["dram__bytes_write.sum"] * sc.get(d.get("dram__bytes_write.sum.unit"), 1.0))
+    return sum(vals) / len(vals)
+
+
 def _config(world: int, plan_desc: str) -> dict:
     return {"workload": "BERT-base encoder stack train step (configs[1]; DP configs[3])",
             "model": "bert-base (12x768, ffn 3072, 12 heads), fused QKV",
@@ -302,7 +323,8 @@ def run_ours(args) -> None:
             "roofline": {
                 "bound": "tensor", "kernel": "k_gemm_tc<kI8=true> (tcgen05 kind::i8, fused dequant)",
                 "achieved": ach, "peak": i8, "unit": "TFLOP/s", "frac": ach / i8 if i8 else None,
-                "traffic": None,
+                "traffic": _ncu_traffic("gemm_s8", ("qkv", "o", "ff1", "ff2")),
+                "traffic_unit": "bytes per launch (DRAM read+write, ncu --set full, mean of the 4 step shapes)",
                 "peak_source": "INT8 dense measured in this run: cuBLASLt torch._int_mm 8192^3 best of 10",
                 "achieved_how": (f"sum of 2MNK over the {k8['launches']} INT8 GEMM launches of one eager "
                                  f"step / their CUDA-event durations on the launch stream"),

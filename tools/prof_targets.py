@@ -15,8 +15,10 @@ from paper_2407_02327_b200 import ops  # noqa: E402
 
 def main(name: str, reps: int = 3) -> None:
     dev = "cuda"
+    T, H, F = 4096, 768, 3072
+    bert = {"qkv": (T, 3 * H, H), "o": (T, H, H), "ff1": (T, F, H), "ff2": (T, H, F), "8192": (8192, 8192, 8192)}
     if name.startswith("gemm_s8"):
-        M, N, K = (8192, 8192, 8192) if name.endswith("8192") else (4096, 3072, 768)
+        M, N, K = bert[name.split("_")[-1]]
         a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device=dev)
         b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device=dev)
         sa = torch.tensor([0.01], device=dev)
@@ -31,6 +33,34 @@ def main(name: str, reps: int = 3) -> None:
         b = torch.randn((N, K), device=dev).half()
         out = torch.empty((M, N), device=dev, dtype=torch.float16 if name.endswith("ff1") else torch.float32)
         fn = lambda: ops.gemm_f16(a, b, out=out)  # noqa: E731
+    elif name in ("attn_fwd", "attn_bwd"):
+        qkv = torch.randn(32, 128, 3, 12, 64, device=dev).half()
+        dout = torch.randn(32, 128, 12, 64, device=dev).half()
+        out, lse, _ = ops.attention_fwd(qkv)
+        fn = (lambda: ops.attention_fwd(qkv)) if name == "attn_fwd" else (  # noqa: E731
+            lambda: ops.attention_bwd(qkv, out, dout, lse))
+    elif name == "ln_bwd":
+        a = torch.randn(T, H, device=dev)
+        g, be = torch.rand(H, device=dev) + 0.5, torch.randn(H, device=dev)
+        y, s_, m, r = ops.layernorm_fwd(a, a, g, be, 1e-12)
+        dg, db, col = (torch.zeros(H, device=dev) for _ in range(3))
+        fn = lambda: ops.layernorm_bwd_ex(a, s_, m, r, g, dg, db, True, col)  # noqa: E731
+    elif name == "act_bwd":
+        dg = torch.randn(T, F, device=dev)
+        h = torch.randn(T, F, device=dev)
+        col = torch.zeros(F, device=dev)
+        fn = lambda: ops.act_bwd_colsum(dg, h, ops.ACT_GELU, torch.float16, col)  # noqa: E731
+    elif name == "adamw":
+        from paper_2407_02327_b200.fused import FusedAdamW
+        from paper_2407_02327_b200.train_step import BertConfig, BertEncoderStack, FlatGrads, mixed_plan
+        cfg = BertConfig()
+        mdl = BertEncoderStack(cfg).to(dev)
+        mdl.apply_plan(mixed_plan(cfg))
+        params = list(mdl.parameters())
+        FlatGrads(params)
+        opt = FusedAdamW(params)
+        opt.attach(mdl.qlinears().values())
+        fn = opt.step
     else:
         n = (1 << 30) // 4
         x = torch.randn(n, device=dev)

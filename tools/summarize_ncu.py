@@ -31,7 +31,7 @@ def launches(path, out):
     fills = [i for i, (k, v) in enumerate(rows) if "FillFunctor" in k and v > 20e3]
     seg = rows
     for a, b in zip(fills[-2::-1], fills[:0:-1]):
-        if any("multi_tensor_apply" in k for k, _ in rows[a:b]):
+        if any("multi_tensor_apply" in k or "k_adamw" in k for k, _ in rows[a:b]):
             seg = rows[a:b]
             break
     tot = collections.defaultdict(float)
