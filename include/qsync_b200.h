@@ -236,6 +236,21 @@ int qsync_layernorm_bwd_ex(const float* dy, const float* s, const float* mean, c
                            const float* gamma, int64_t rows, int64_t cols, float* dx, float* dgamma,
                            float* dbeta, uint16_t* dx16, float* dcolsum, qsync_stream_t stream);
 
+/* Embedding + LayerNorm of the encoder input: row r's input is
+ * word[tokens[r]] + pos[r % seq] + typ[0] (gathered, never materialised), then
+ * LayerNorm as qsync_layernorm_fwd_ex (s_out, mean, rstd saved; optional y16 /
+ * y_absmax for the first planned op).  The backward scatter-adds the row
+ * gradients into dword[tokens[r]] and dpos[r % seq] (vector reductions), adds
+ * their column sums into dtyp, and dgamma / dbeta as qsync_layernorm_bwd. */
+int qsync_embed_layernorm_fwd(const int64_t* tokens, int64_t rows, int64_t seq, const float* word,
+                              const float* pos, const float* typ, const float* gamma, const float* beta,
+                              int64_t cols, float eps, float* s_out, float* y, float* mean, float* rstd,
+                              uint16_t* y16, float* y_absmax, qsync_stream_t stream);
+int qsync_embed_layernorm_bwd(const float* dy, const float* s, const float* mean, const float* rstd,
+                              const float* gamma, const int64_t* tokens, int64_t rows, int64_t seq, int64_t cols,
+                              float* dgamma, float* dbeta, float* dword, float* dpos, float* dtyp,
+                              qsync_stream_t stream);
+
 /* absmax of act(x) over n values (device float, overwritten). */
 int qsync_absmax_act(const void* x, int dtype, int64_t n, int act, float* absmax,
                      qsync_stream_t stream);

@@ -23,6 +23,12 @@ __device__ __forceinline__ float warp_sum_f(float v) {
     return v;
 }
 
+__device__ __forceinline__ void red_add_v4(float* p, float4 v) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+
 template <int NV, int BDT>
 __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
                                                 const typename Elem<BDT>::T* __restrict__ b,
@@ -32,7 +38,11 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
                                                 float* __restrict__ y, float* __restrict__ mean_out,
                                                 float* __restrict__ rstd_out,
                                                 __half* __restrict__ y16,
-                                                unsigned* __restrict__ y_absmax) {
+                                                unsigned* __restrict__ y_absmax,
+                                                const int64_t* __restrict__ tok = nullptr,
+                                                const float* __restrict__ pos = nullptr,
+                                                const float* __restrict__ typ = nullptr,
+                                                int seq = 1) {
     const int lane = threadIdx.x & 31;
     float amax = 0.0f;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -48,10 +58,20 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
         float4 v[NV];
         float sum = 0.0f;
 #pragma unroll
+        // Embedding mode: a is the word table, the row's input is
+        // word[tok[row]] + pos[row % seq] + typ[0] (gathered, never materialised).
+        const int64_t arow = tok ? tok[row] : row;
+        const int64_t prow = tok ? row % seq : 0;
         for (int i = 0; i < NV; ++i) {
             const int64_t off = row * cols + 4 * (lane + 32 * i);
-            float4 x = *reinterpret_cast<const float4*>(a + off);
-            if (b) {
+            float4 x = *reinterpret_cast<const float4*>(a + arow * cols + 4 * (lane + 32 * i));
+            if (tok) {
+                const float4 p4 = *reinterpret_cast<const float4*>(pos + prow * cols + 4 * (lane + 32 * i));
+                const float4 t4 = reinterpret_cast<const float4*>(typ)[lane + 32 * i];
+                // (word + pos) + typ: the association of the unfused path, bit for bit
+                x.x = (x.x + p4.x) + t4.x; x.y = (x.y + p4.y) + t4.y;
+                x.z = (x.z + p4.z) + t4.z; x.w = (x.w + p4.w) + t4.w;
+            } else if (b) {
                 if (BDT == QSYNC_F32) {
                     const float4 r = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(b) + off);
                     x.x += r.x; x.y += r.y; x.z += r.z; x.w += r.w;
@@ -210,7 +230,11 @@ __global__ void __launch_bounds__(256, 2) k_ln_bwd2(const float* __restrict__ dy
                                                     float* __restrict__ dgamma,
                                                     float* __restrict__ dbeta,
                                                     __half* __restrict__ dx16,
-                                                    float* __restrict__ dcol) {
+                                                    float* __restrict__ dcol,
+                                                    const int64_t* __restrict__ tok = nullptr,
+                                                    float* __restrict__ dword = nullptr,
+                                                    float* __restrict__ dpos = nullptr,
+                                                    int seq = 1) {
     constexpr int NH = NV / 2;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -265,7 +289,15 @@ __global__ void __launch_bounds__(256, 2) k_ln_bwd2(const float* __restrict__ dy
             o.y = rstd * (gy[i].y - m1 - xh[i].y * m2);
             o.z = rstd * (gy[i].z - m1 - xh[i].z * m2);
             o.w = rstd * (gy[i].w - m1 - xh[i].w * m2);
-            *reinterpret_cast<float4*>(dx + off) = o;
+            if (tok) {
+                // Embedding mode: scatter-add into the word row and the position row
+                // (vector reductions in L2), never materialising dx.
+                const int c = cbase + 4 * (lane + 32 * i);
+                red_add_v4(dword + tok[row] * cols + c, o);
+                red_add_v4(dpos + (row % seq) * cols + c, o);
+            } else {
+                *reinterpret_cast<float4*>(dx + off) = o;
+            }
             if (dx16) {
                 uint2 h;
                 h.x = pack_half2(o.x, o.y);
@@ -329,6 +361,28 @@ int ln_bwd_nv(const float* dy, const float* s, const float* mean, const float* r
     k_ln_bwd<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
                                         reinterpret_cast<__half*>(dx16), dcol);
     return check_launch("k_ln_bwd");
+}
+
+template <int NV>
+int embed_ln_fwd_nv(const int64_t* tok, int64_t rows, int seq, const float* word, const float* pos,
+                    const float* typ, const float* gamma, const float* beta, int cols, float eps, float* s_out,
+                    float* y, float* mean, float* rstd, uint16_t* y16, float* y_absmax, cudaStream_t st) {
+    if (y_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(y_absmax, 0, sizeof(float), st), "memset"));
+    const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 8LL));
+    k_ln_fwd<NV, QSYNC_F32><<<grid, 256, 0, st>>>(word, nullptr, gamma, beta, rows, cols, eps, s_out, y, mean,
+                                                  rstd, reinterpret_cast<__half*>(y16),
+                                                  reinterpret_cast<unsigned*>(y_absmax), tok, pos, typ, seq);
+    return check_launch("k_ln_fwd<embed>");
+}
+
+template <int NV>
+int embed_ln_bwd_nv(const float* dy, const float* s, const float* mean, const float* rstd, const float* gamma,
+                    const int64_t* tok, int64_t rows, int seq, int cols, float* dgamma, float* dbeta,
+                    float* dword, float* dpos, float* dtyp, cudaStream_t st) {
+    const int grid = static_cast<int>(std::min<int64_t>((rows + 3) / 4, sm_count() * 4LL));
+    k_ln_bwd2<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, nullptr, dgamma, dbeta, nullptr,
+                                         dtyp, tok, dword, dpos, seq);
+    return check_launch("k_ln_bwd<embed>");
 }
 
 }  // namespace
@@ -395,6 +449,46 @@ int qsync_layernorm_bwd(const float* dy, const float* s, const float* mean, cons
                         float* dbeta, qsync_stream_t stream) {
     return qsync_layernorm_bwd_ex(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta, nullptr,
                                   nullptr, stream);
+}
+
+int qsync_embed_layernorm_fwd(const int64_t* tokens, int64_t rows, int64_t seq, const float* word,
+                              const float* pos, const float* typ, const float* gamma, const float* beta,
+                              int64_t cols, float eps, float* s_out, float* y, float* mean, float* rstd,
+                              uint16_t* y16, float* y_absmax, qsync_stream_t stream) {
+    QSB_REQUIRE(tokens && word && pos && typ && s_out && y && mean && rstd, QSYNC_ERR_VALIDATION,
+                "embedding LayerNorm needs tokens, tables and outputs");
+    QSB_REQUIRE(rows >= 0 && seq > 0, QSYNC_ERR_DOMAIN, "bad row / sequence count");
+    QSB_REQUIRE(cols == 768 || cols == 1024 || cols == 512 || cols == 256, QSYNC_ERR_DOMAIN,
+                "embedding LayerNorm supports hidden 256, 512, 768, 1024");
+    if (rows == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int c = static_cast<int>(cols), sq = static_cast<int>(seq);
+    switch (c / 128) {
+        case 2: return embed_ln_fwd_nv<2>(tokens, rows, sq, word, pos, typ, gamma, beta, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        case 4: return embed_ln_fwd_nv<4>(tokens, rows, sq, word, pos, typ, gamma, beta, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        case 6: return embed_ln_fwd_nv<6>(tokens, rows, sq, word, pos, typ, gamma, beta, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+        default: return embed_ln_fwd_nv<8>(tokens, rows, sq, word, pos, typ, gamma, beta, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
+    }
+}
+
+int qsync_embed_layernorm_bwd(const float* dy, const float* s, const float* mean, const float* rstd,
+                              const float* gamma, const int64_t* tokens, int64_t rows, int64_t seq, int64_t cols,
+                              float* dgamma, float* dbeta, float* dword, float* dpos, float* dtyp,
+                              qsync_stream_t stream) {
+    QSB_REQUIRE(dy && s && mean && rstd && gamma && tokens && dword && dpos && dtyp, QSYNC_ERR_VALIDATION,
+                "embedding LayerNorm backward needs all buffers");
+    QSB_REQUIRE(rows >= 0 && seq > 0, QSYNC_ERR_DOMAIN, "bad row / sequence count");
+    QSB_REQUIRE(cols == 768 || cols == 1024 || cols == 512 || cols == 256, QSYNC_ERR_DOMAIN,
+                "embedding LayerNorm supports hidden 256, 512, 768, 1024");
+    if (rows == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int c = static_cast<int>(cols), sq = static_cast<int>(seq);
+    switch (c / 128) {
+        case 2: return embed_ln_bwd_nv<2>(dy, s, mean, rstd, gamma, tokens, rows, sq, c, dgamma, dbeta, dword, dpos, dtyp, st);
+        case 4: return embed_ln_bwd_nv<4>(dy, s, mean, rstd, gamma, tokens, rows, sq, c, dgamma, dbeta, dword, dpos, dtyp, st);
+        case 6: return embed_ln_bwd_nv<6>(dy, s, mean, rstd, gamma, tokens, rows, sq, c, dgamma, dbeta, dword, dpos, dtyp, st);
+        default: return embed_ln_bwd_nv<8>(dy, s, mean, rstd, gamma, tokens, rows, sq, c, dgamma, dbeta, dword, dpos, dtyp, st);
+    }
 }
 
 }  // extern "C"

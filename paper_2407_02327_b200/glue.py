@@ -66,3 +66,45 @@ class _Attention(torch.autograd.Function):
 
 def attention(qkv: torch.Tensor) -> torch.Tensor:
     return _Attention.apply(qkv)
+
+
+class _EmbedLN(torch.autograd.Function):
+    """Embedding sum + LayerNorm of the encoder input in one kernel each way
+    (word[tok] + pos[s] + typ[0] gathered, never materialised; the backward
+    scatter-adds straight into the tables' gradients).  Returns (y, aux) where
+    aux is the first planned op's operand hint (FP16 copy / absmax) or empty."""
+
+    @staticmethod
+    def forward(ctx, tokens, word, pos, typ, gamma, beta, eps, want_f16, want_absmax):
+        B, S = tokens.shape
+        y, s, mean, rstd, y16, am = ops.embed_layernorm_fwd(tokens, word, pos, typ, gamma, beta, eps,
+                                                            want_f16, want_absmax)
+        ctx.save_for_backward(tokens, s, mean, rstd)
+        ctx.params = (word, pos, typ, gamma, beta)
+        aux = y16 if want_f16 else (am if want_absmax else torch.empty(0, device=y.device))
+        ctx.mark_non_differentiable(aux)
+        ctx.set_materialize_grads(False)
+        return y.view(B, S, -1), aux
+
+    @staticmethod
+    def backward(ctx, dy, _daux):
+        tokens, s, mean, rstd = ctx.saved_tensors
+        word, pos, typ, gamma, beta = ctx.params
+        grads = []
+        for p in (word, pos, typ, gamma, beta):
+            mg = getattr(p, "main_grad", None)
+            grads.append(mg if mg is not None else torch.zeros_like(p))
+        dy = dy.reshape(-1, dy.shape[-1]).contiguous()
+        ops.embed_layernorm_bwd(dy, s, mean, rstd, gamma.detach(), tokens, grads[3], grads[4], grads[0],
+                                grads[1], grads[2])
+        out = [None, None, None, None, None, None, None, None, None]
+        for i, p in enumerate((word, pos, typ, gamma, beta)):
+            if getattr(p, "main_grad", None) is None:
+                out[1 + i] = grads[i]
+        return tuple(out)
+
+
+def embed_layernorm(tokens, word, pos, typ, ln, want_f16=False, want_absmax=False):
+    y, aux = _EmbedLN.apply(tokens, word.weight, pos.weight, typ.weight, ln.weight, ln.bias, ln.eps,
+                            want_f16, want_absmax)
+    return y, (aux if aux.numel() else None)

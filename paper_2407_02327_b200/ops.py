@@ -423,6 +423,34 @@ def gemm_s8_ex(a: torch.Tensor, b: torch.Tensor, scale_a, scale_b, bias=None,
     return c
 
 
+def embed_layernorm_fwd(tokens, word, pos, typ, gamma, beta, eps: float, want_f16: bool = False,
+                        want_absmax: bool = False):
+    """y = LN(word[tok] + pos[s] + typ[0]) for tokens [B, S] (int64).
+    Returns (y [B*S, H], s, mean, rstd, y16, absmax)."""
+    _req(tokens, "tokens", (torch.int64,))
+    B, S = tokens.shape
+    H = word.shape[1]
+    rows = B * S
+    dev = word.device
+    y = torch.empty((rows, H), device=dev, dtype=torch.float32)
+    s = torch.empty_like(y)
+    mean = torch.empty(rows, device=dev, dtype=torch.float32)
+    rstd = torch.empty(rows, device=dev, dtype=torch.float32)
+    y16 = torch.empty((rows, H), device=dev, dtype=torch.float16) if want_f16 else None
+    am = torch.empty(1, device=dev, dtype=torch.float32) if want_absmax else None
+    call("qsync_embed_layernorm_fwd", _ptr(tokens), rows, S, _ptr(word), _ptr(pos), _ptr(typ), _ptr(gamma),
+         _ptr(beta), H, float(eps), _ptr(s), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(y16), _ptr(am), _stream())
+    return y, s, mean, rstd, y16, am
+
+
+def embed_layernorm_bwd(dy, s, mean, rstd, gamma, tokens, dgamma, dbeta, dword, dpos, dtyp) -> None:
+    """Backward of embed_layernorm_fwd; every gradient is ADDED into its buffer."""
+    _req(dy, "dy", (torch.float32,))
+    B, S = tokens.shape
+    call("qsync_embed_layernorm_bwd", _ptr(dy), _ptr(s), _ptr(mean), _ptr(rstd), _ptr(gamma), _ptr(tokens),
+         B * S, S, dy.shape[-1], _ptr(dgamma), _ptr(dbeta), _ptr(dword), _ptr(dpos), _ptr(dtyp), _stream())
+
+
 def attention_fwd(qkv: torch.Tensor, scale: float | None = None, want_absmax: bool = False):
     """Attention core on packed QKV [B, S, 3, H, D] FP16 -> (out [B, S, H, D] FP16,
     lse [B, H, S] FP32, absmax(out) device float[1] or None)."""

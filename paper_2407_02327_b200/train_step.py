@@ -141,17 +141,20 @@ class BertEncoderStack(torch.nn.Module):
 
     def forward(self, tokens, labels):
         B, S = tokens.shape
-        pos = torch.arange(S, device=tokens.device)
-        x = self.word(tokens) + self.pos(pos)[None] + self.typ.weight[0][None, None]
-        x = self.ln(x)
         if self.fused:
             from .fused import fused_layer
-            aux = None
+            from .glue import embed_layernorm
+            p0 = self.layers[0].qkv.precision if len(self.layers) else None
+            x, aux = embed_layernorm(tokens, self.word, self.pos, self.typ, self.ln,
+                                     want_f16=p0 == FP16, want_absmax=p0 == INT8)
             n = len(self.layers)
             for i, layer in enumerate(self.layers):
                 nxt = self.layers[i + 1].qkv.precision if i + 1 < n else None
                 x, aux = fused_layer(layer, x, aux, nxt)
         else:
+            pos = torch.arange(S, device=tokens.device)
+            x = self.word(tokens) + self.pos(pos)[None] + self.typ.weight[0][None, None]
+            x = self.ln(x)
             for layer in self.layers:
                 x = layer(x)
         pooled = torch.tanh(cast(self.pooler(x[:, 0].contiguous()), torch.float32))

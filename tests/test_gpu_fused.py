@@ -208,3 +208,36 @@ def test_fused_trainstep_graph_learns():
     ls = [float(st().item()) for _ in range(12)]
     assert ls[-1] < ls[0]
     assert int(st.opt.step_t.item()) == 3 + 12  # warm-up + replays (capture only records)
+
+
+def test_embed_layernorm_vs_torch():
+    """Gathered embedding sum + LN (fwd) and the scatter-add backward vs torch
+    fp32 autograd of Embedding + LayerNorm."""
+    from paper_2407_02327_b200.glue import embed_layernorm
+    from paper_2407_02327_b200.glue import AddLayerNorm
+    torch.manual_seed(11)
+    V, P, H, B, S = 1000, 128, 768, 8, 128
+    word, pos, typ = (torch.nn.Embedding(n, H).to(DEV) for n in (V, P, 2))
+    ln = AddLayerNorm(H, eps=1e-12).to(DEV)
+    with torch.no_grad():
+        ln.weight.uniform_(0.5, 1.5)
+        ln.bias.uniform_(-0.5, 0.5)
+    tok = torch.randint(0, V, (B, S), device=DEV)
+    tok[0, :10] = 7  # repeated ids: the scatter must accumulate
+    y, am = embed_layernorm(tok, word, pos, typ, ln, want_absmax=True)
+    ref_ln = torch.nn.LayerNorm(H, eps=1e-12).to(DEV)
+    ref_ln.load_state_dict(ln.state_dict())
+    params = [word.weight, pos.weight, typ.weight, ref_ln.weight, ref_ln.bias]
+    x = word.weight[tok] + pos.weight[torch.arange(S, device=DEV)][None] + typ.weight[0][None, None]
+    y_ref = ref_ln(x)
+    torch.testing.assert_close(y, y_ref, rtol=1e-4, atol=1e-4)
+    assert am.item() == y.abs().max().item()
+    g = torch.randn_like(y_ref)
+    y.backward(g)
+    got = [word.weight.grad, pos.weight.grad, typ.weight.grad, ln.weight.grad, ln.bias.grad]
+    for p in params:
+        p.grad = None
+    y_ref.backward(g)
+    for name, a, b in zip(("word", "pos", "typ", "gamma", "beta"), got, [p.grad for p in params]):
+        err = ((a - b).abs().max() / b.abs().max()).item()
+        assert err < 1e-4, f"{name}: {err}"
