@@ -218,7 +218,7 @@ int qsync_layernorm_bwd(const float* dy, const float* s, const float* mean, cons
  * Fused encoder-layer glue (the operators between two planned Linears fold
  * into the kernels that produce / consume the planned operand format).
  * ------------------------------------------------------------------------- */
-enum qsync_act { QSYNC_ACT_NONE = 0, QSYNC_ACT_GELU = 1 };
+enum qsync_act { QSYNC_ACT_NONE = 0, QSYNC_ACT_GELU = 1, QSYNC_ACT_DERIV = 2 };
 
 /* LayerNorm forward that also emits what the NEXT planned Linear consumes:
  * y16 (optional) = FP16(y) for an FP16 op; y_absmax (optional, device float,
@@ -255,14 +255,16 @@ int qsync_embed_layernorm_bwd(const float* dy, const float* s, const float* mean
 int qsync_absmax_act(const void* x, int dtype, int64_t n, int act, float* absmax,
                      qsync_stream_t stream);
 /* Per-tensor RNE quantize of act(x) with s = absmax/127 from a device absmax
- * computed upstream (LayerNorm epilogue / qsync_absmax_act); *scale_out = s. */
+ * computed upstream (LayerNorm epilogue / qsync_absmax_act); *scale_out = s.
+ * dact_out (optional, FP16) receives act'(x) for the backward (QSYNC_ACT_DERIV). */
 int qsync_quantize_act(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,
-                       float* scale_out, qsync_stream_t stream);
-/* out = act(x) cast to dst_dtype (F32/F16 -> F32/F16). */
+                       float* scale_out, uint16_t* dact_out, qsync_stream_t stream);
+/* out = act(x) cast to dst_dtype (F32/F16 -> F32/F16); optional FP16 act'(x). */
 int qsync_act_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64_t n, int act,
-                   qsync_stream_t stream);
+                   uint16_t* dact_out, qsync_stream_t stream);
 /* Backward through act and into a planned op's FP16 backward format:
- * g = dy * act'(h) (act NONE: g = dy; h may be NULL), out (optional) = g as
+ * g = dy * act'(h) (act NONE: g = dy, h may be NULL; act DERIV: h is the FP16
+ * act'(x) the forward stored, g = dy * h), out (optional) = g as
  * out_dtype, colsum (optional) += sum_rows g (the bias gradient).  dy, h
  * [rows, cols] F32/F16. */
 int qsync_act_bwd_colsum(const void* dy, int dy_dtype, const void* h, int h_dtype, int64_t rows,

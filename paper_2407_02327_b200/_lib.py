@@ -19,7 +19,7 @@ ERROR_KINDS = ["graph-cycle", "validation", "reference", "domain", "missing-prof
                "topology", "enumeration-limit", "infeasible", "io", "internal"]
 
 F32, F16, BF16, I8, I32 = 0, 1, 2, 3, 4
-ACT_NONE, ACT_GELU = 0, 1
+ACT_NONE, ACT_GELU, ACT_DERIV = 0, 1, 2
 
 
 class QsyncError(RuntimeError):
@@ -70,8 +70,8 @@ SIGNATURES = {
     "qsync_layernorm_fwd_ex": [_p, _p, _int, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p, _p],
     "qsync_layernorm_bwd_ex": [_p, _p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p],
     "qsync_absmax_act": [_p, _int, _i64, _int, _p, _p],
-    "qsync_quantize_act": [_p, _int, _i64, _int, _p, _p, _p, _p],
-    "qsync_act_cast": [_p, _int, _p, _int, _i64, _int, _p],
+    "qsync_quantize_act": [_p, _int, _i64, _int, _p, _p, _p, _p, _p],
+    "qsync_act_cast": [_p, _int, _p, _int, _i64, _int, _p, _p],
     "qsync_act_bwd_colsum": [_p, _int, _p, _int, _i64, _i64, _int, _p, _int, _p, _p],
     "qsync_gemm_s8_ex": [_p, _p, _i64, _i64, _i64, _p, _int, _p, _p, _int, _p, _p],
     "qsync_adamw_step": [_p, _int, _p, _i64, _p, _f32, _f32, _f32, _f32, _f32, _int, _p],
@@ -85,6 +85,7 @@ SIGNATURES = {
     "qsync_gemm_force_cta": [_int],
     "qsync_gemm_debug_epilogue": [_int],
     "qsync_gemm_set_pdl": [_int],
+    "qsync_gemm_set_max_ctas": [_int],
     "qsync_mt_jump_selftest": [],
 }
 _RESTYPES = {"qsync_last_error": C.c_char_p, "qsync_status_name": C.c_char_p,

@@ -1,7 +1,8 @@
 // act.cu -- backward through the encoder layer's activation into a planned
 // op's FP16 backward format, fused with that op's bias gradient.
 //
-//   g = dy * act'(h)       (act NONE: g = dy)
+//   g = dy * act'(h)       (act NONE: g = dy; act DERIV: h already holds act'(x) in
+//                           FP16, written by the forward's operand kernel)
 //   out = g as out_dtype   (optional; FP16 for an INT8/FP16 op, cost_mapper.cpp:13-15)
 //   colsum += sum_rows g   (optional; the Linear's bias gradient, FP32)
 //
@@ -93,6 +94,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_act_bwd_colsum(const void* __re
                 load8v<DH>(h, off, hv);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) g[j] = __fmul_rn(g[j], gelu_erf_grad(hv[j]));
+            } else if constexpr (ACT == 2) {  // h holds act'(x) (FP16), stored by the forward
+                float hv[8];
+                load8v<QSYNC_F16>(h, off, hv);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) g[j] = __fmul_rn(g[j], hv[j]);
             }
             if (out) store8v<DO>(out, off, g);
         } else {
@@ -102,6 +108,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_act_bwd_colsum(const void* __re
                 if (c + j < cols) {
                     g[j] = load1<DDY>(dy, off + j);
                     if constexpr (ACT == 1) g[j] = __fmul_rn(g[j], gelu_erf_grad(load1<DH>(h, off + j)));
+                    if constexpr (ACT == 2) g[j] = __fmul_rn(g[j], load1<QSYNC_F16>(h, off + j));
                     if (out) store1<DO>(out, off + j, g[j]);
                 }
             }
@@ -142,6 +149,7 @@ template <int DDY>
 int act_bwd_h(const void* dy, const void* h, int h_dtype, int64_t rows, int64_t cols, int act, void* out,
               int out_dtype, float* colsum, cudaStream_t st) {
     if (act == QSYNC_ACT_NONE) return act_bwd_out<DDY, QSYNC_F32, 0>(dy, nullptr, rows, cols, out, out_dtype, colsum, st);
+    if (act == QSYNC_ACT_DERIV) return act_bwd_out<DDY, QSYNC_F16, 2>(dy, h, rows, cols, out, out_dtype, colsum, st);
     if (h_dtype == QSYNC_F32) return act_bwd_out<DDY, QSYNC_F32, 1>(dy, h, rows, cols, out, out_dtype, colsum, st);
     return act_bwd_out<DDY, QSYNC_F16, 1>(dy, h, rows, cols, out, out_dtype, colsum, st);
 }
@@ -159,11 +167,13 @@ int qsync_act_bwd_colsum(const void* dy, int dy_dtype, const void* h, int h_dtyp
     QSB_REQUIRE(dy != nullptr, QSYNC_ERR_VALIDATION, "dy is required");
     QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
     QSB_REQUIRE(rows / kRows < 65535, QSYNC_ERR_DOMAIN, "too many rows");
-    QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU, QSYNC_ERR_DOMAIN, "unknown activation");
+    QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU || act == QSYNC_ACT_DERIV, QSYNC_ERR_DOMAIN,
+                "unknown activation");
     QSB_REQUIRE(act == QSYNC_ACT_NONE || h != nullptr, QSYNC_ERR_VALIDATION, "activation backward needs h");
     QSB_REQUIRE(dy_dtype == QSYNC_F32 || dy_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN, "dy must be F32 or F16");
-    QSB_REQUIRE(act == QSYNC_ACT_NONE || h_dtype == QSYNC_F32 || h_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN,
+    QSB_REQUIRE(act != QSYNC_ACT_GELU || h_dtype == QSYNC_F32 || h_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN,
                 "h must be F32 or F16");
+    QSB_REQUIRE(act != QSYNC_ACT_DERIV || h_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN, "a stored derivative is F16");
     QSB_REQUIRE(!out || out_dtype == QSYNC_F32 || out_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN,
                 "out must be F32 or F16");
     if (rows == 0 || cols == 0 || (!out && !colsum)) return QSYNC_OK;

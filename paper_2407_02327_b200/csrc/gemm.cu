@@ -531,6 +531,7 @@ int g_splitk_wide = 0;   // accumulate GEMMs prefer BN=256 (bench hook)
 int g_force_cta = 0;     // test/bench hook (qsync_gemm_force_cta): 0 = cost model, 1, 2
 int g_debug_epi = 0;     // bench hook (qsync_gemm_debug_epilogue)
 int g_pdl = 1;           // programmatic dependent launch (qsync_gemm_set_pdl)
+int g_max_ctas = 0;      // cap on the persistent grid (qsync_gemm_set_max_ctas), 0 = all SMs
 
 template <bool kI8, int BN, int kCta, int kLay>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
@@ -596,7 +597,9 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
         }
     }
     const int64_t units = tiles * p.ksplit;
-    const int grid = static_cast<int>(std::min<int64_t>(units, slots)) * kCta;
+    int64_t cap = slots;
+    if (g_max_ctas > 0) cap = std::max<int64_t>(1, std::min<int64_t>(slots, g_max_ctas / kCta));
+    const int grid = static_cast<int>(std::min<int64_t>(units, cap)) * kCta;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
@@ -720,6 +723,12 @@ extern "C" {
 int qsync_gemm_force_splitk(int ks) {
     QSB_REQUIRE(ks >= 0 && ks <= 64, QSYNC_ERR_DOMAIN, "split-K override must be in [0, 64]");
     g_force_splitk = ks;
+    return QSYNC_OK;
+}
+
+int qsync_gemm_set_max_ctas(int n) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "CTA cap must be >= 0");
+    g_max_ctas = n;
     return QSYNC_OK;
 }
 

@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                                                        int64_t n, const float* __restrict__ absmax_in,
                                                        const float* __restrict__ scale_in,
                                                        int8_t* __restrict__ q,
-                                                       float* __restrict__ scale_out, int vec_ok) {
+                                                       float* __restrict__ scale_out, int vec_ok,
+                                                       uint16_t* __restrict__ dact = nullptr) {
     using V = Vec<DT>;
     constexpr int LOADS = 16 / V::N;
     const float s = scale_in ? *scale_in : scale_from_absmax(*absmax_in);
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
 #pragma unroll
             for (int u = 0; u < LOADS; ++u) r[u] = ld_stream(xv + i * LOADS + u);
             uint32_t packed[4];
+            uint32_t dp[8];  // GELU'(x) of the 16 elements as FP16 pairs (the backward's factor)
 #pragma unroll
             for (int u = 0; u < LOADS; ++u) {
                 float f[V::N];
@@ -139,14 +141,26 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                     uint32_t b2 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j + 2]), s));
                     uint32_t b3 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j + 3]), s));
                     packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+                    if (ACT == 1) {
+                        dp[(u * V::N + j) / 2] = pack_half2(gelu_erf_grad(f[j]), gelu_erf_grad(f[j + 1]));
+                        dp[(u * V::N + j) / 2 + 1] = pack_half2(gelu_erf_grad(f[j + 2]), gelu_erf_grad(f[j + 3]));
+                    }
                 }
             }
             qv[i] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            if (ACT == 1 && dact) {
+                uint4* dv = reinterpret_cast<uint4*>(dact) + 2 * i;
+                dv[0] = make_uint4(dp[0], dp[1], dp[2], dp[3]);
+                dv[1] = make_uint4(dp[4], dp[5], dp[6], dp[7]);
+            }
         }
         done = n16 * 16;
     }
-    for (int64_t i = done + tid; i < n; i += stride)
-        q[i] = static_cast<int8_t>(quant_rne(act_f<ACT, DT>(Elem<DT>::f(x[i])), s));
+    for (int64_t i = done + tid; i < n; i += stride) {
+        const float xv = Elem<DT>::f(x[i]);
+        q[i] = static_cast<int8_t>(quant_rne(act_f<ACT, DT>(xv), s));
+        if (ACT == 1 && dact) dact[i] = __half_as_ushort(__float2half_rn(gelu_erf_grad(xv)));
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -479,7 +493,8 @@ __device__ __forceinline__ void store8(void* out, int64_t i, const float* f) {
 template <int SD, int DD, int ACT = 0>
 __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* __restrict__ x,
                                                    typename Store<SD, DD>::T* __restrict__ out,
-                                                   int64_t n, int vec_ok) {
+                                                   int64_t n, int vec_ok,
+                                                   uint16_t* __restrict__ dact = nullptr) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t done = 0;
@@ -490,6 +505,16 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
             float f0[8], f1[8];
             load8<SD>(x, i * 8, f0);
             load8<SD>(x, (i + stride) * 8, f1);
+            if (ACT == 1 && dact) {
+                uint32_t d0[4], d1[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    d0[j] = pack_half2(gelu_erf_grad(f0[2 * j]), gelu_erf_grad(f0[2 * j + 1]));
+                    d1[j] = pack_half2(gelu_erf_grad(f1[2 * j]), gelu_erf_grad(f1[2 * j + 1]));
+                }
+                reinterpret_cast<uint4*>(dact)[i] = make_uint4(d0[0], d0[1], d0[2], d0[3]);
+                reinterpret_cast<uint4*>(dact)[i + stride] = make_uint4(d1[0], d1[1], d1[2], d1[3]);
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 f0[j] = act_f<ACT, SD>(f0[j]);
@@ -501,13 +526,23 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
         for (; i < n8; i += stride) {
             float f0[8];
             load8<SD>(x, i * 8, f0);
+            if (ACT == 1 && dact) {
+                uint32_t d0[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) d0[j] = pack_half2(gelu_erf_grad(f0[2 * j]), gelu_erf_grad(f0[2 * j + 1]));
+                reinterpret_cast<uint4*>(dact)[i] = make_uint4(d0[0], d0[1], d0[2], d0[3]);
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) f0[j] = act_f<ACT, SD>(f0[j]);
             store8<DD>(out, i * 8, f0);
         }
         done = n8 * 8;
     }
-    for (int64_t i = done + tid; i < n; i += stride) out[i] = Store<SD, DD>::cvt(act_f<ACT, SD>(Elem<SD>::f(x[i])));
+    for (int64_t i = done + tid; i < n; i += stride) {
+        const float xv = Elem<SD>::f(x[i]);
+        out[i] = Store<SD, DD>::cvt(act_f<ACT, SD>(xv));
+        if (ACT == 1 && dact) dact[i] = __half_as_ushort(__float2half_rn(gelu_erf_grad(xv)));
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -723,14 +758,14 @@ struct AbsmaxActRun {
 template <int DT>
 struct QuantActRun {
     static int run(const void* x, int64_t n, int act, const float* absmax, int8_t* q,
-                   float* scale_out, cudaStream_t st) {
+                   float* scale_out, uint16_t* dact, cudaStream_t st) {
         using T = typename Elem<DT>::T;
         if (n == 0) return QSYNC_OK;
-        const int vec = aligned16(x) && aligned16(q);
+        const int vec = aligned16(x) && aligned16(q) && (!dact || aligned16(dact));
         const int grid = grid_for(n / 16 + 1, kThreads, 4);
         if (act == 1)
             k_quantize<DT, 1><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, absmax, nullptr,
-                                                         q, scale_out, vec);
+                                                         q, scale_out, vec, dact);
         else
             k_quantize<DT, 0><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, absmax, nullptr,
                                                          q, scale_out, vec);
@@ -859,14 +894,14 @@ int qsync_absmax_act(const void* x, int dtype, int64_t n, int act, float* absmax
 }
 
 int qsync_quantize_act(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,
-                       float* scale_out, qsync_stream_t stream) {
+                       float* scale_out, uint16_t* dact_out, qsync_stream_t stream) {
     QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
     QSB_REQUIRE(absmax != nullptr, QSYNC_ERR_VALIDATION, "absmax is required");
     QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU, QSYNC_ERR_DOMAIN, "unknown activation");
-    return dispatch_dtype<QuantActRun>(dtype, x, n, act, absmax, q, scale_out, to_stream(stream));
+    return dispatch_dtype<QuantActRun>(dtype, x, n, act, absmax, q, scale_out, dact_out, to_stream(stream));
 }
 
-int qsync_act_cast(const void* x, int src, void* out, int dst, int64_t n, int act,
+int qsync_act_cast(const void* x, int src, void* out, int dst, int64_t n, int act, uint16_t* dact_out,
                    qsync_stream_t stream) {
     QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
     if (act == QSYNC_ACT_NONE) return qsync_cast(x, src, out, dst, n, stream);
@@ -874,11 +909,11 @@ int qsync_act_cast(const void* x, int src, void* out, int dst, int64_t n, int ac
     if (n == 0) return QSYNC_OK;
     cudaStream_t st = to_stream(stream);
     const int grid = grid_for(n / 8 + 1, kThreads * 2, 4);
-    const int vec = aligned16(x) && aligned16(out);
+    const int vec = aligned16(x) && aligned16(out) && (!dact_out || aligned16(dact_out));
 #define QSB_ACAST(S, D)                                                                       \
     if (src == S && dst == D) {                                                               \
         k_cast<S, D, 1><<<grid, kThreads, 0, st>>>(static_cast<const typename Elem<S>::T*>(x), \
-                                                   static_cast<typename Store<S, D>::T*>(out), n, vec); \
+                                                   static_cast<typename Store<S, D>::T*>(out), n, vec, dact_out); \
         return check_launch("k_cast<gelu>");                                                  \
     }
     QSB_ACAST(QSYNC_F32, QSYNC_F32)

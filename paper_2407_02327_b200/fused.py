@@ -22,7 +22,8 @@ forward, per planned op P (INT8 / FP16 / FP32; precision.hpp:12):
 backward (cost_mapper.cpp:13-15: FP16 for INT8/FP16 ops, wgrad FP32 :48-50):
   * LayerNorm backward also emits FP16(dx) (the next op's dY) and dx's column
     sums (that op's bias gradient);
-  * GELU backward is fused with FF1's FP16 dY cast and bias column sums;
+  * GELU backward is fused with FF1's FP16 dY cast and bias column sums, and
+    reads GELU'(h) (FP16) that FF2's operand kernel stored in the forward;
   * the dgrad of the op that reads the residual stream is reduce-added by the
     GEMM epilogue (TMA reduce-add) into the LayerNorm-backward output, which is
     the residual gradient: no separate add;
@@ -180,6 +181,15 @@ def _linear_fwd(m, opnd, out_dtype=None):
     return y, w16
 
 
+# Persistent-grid cap for the side-stream wgrad GEMMs (0 = all SMs): leaves SMs
+# to the critical-path chain on the main stream.  Set by TrainStep / tools.
+WGRAD_CTAS = 0
+
+
+def _call_cap(n):
+    call("qsync_gemm_set_max_ctas", int(n))
+
+
 def _wgrad(m, dy16_or_32, opnd, side):
     """wgrad of one planned op into weight.main_grad (FP32, accumulate)."""
     kind, x, s = opnd
@@ -190,7 +200,13 @@ def _wgrad(m, dy16_or_32, opnd, side):
     x16 = ops.cast(x, torch.float16) if kind == "i8" else x  # exact: INT8 grid values
 
     def run():
-        ops.gemm_f16(dy16_or_32, x16, alpha_dev=s, out=mw, accumulate=True, a_mn=True, b_mn=True)
+        if side is not None and WGRAD_CTAS:
+            _call_cap(WGRAD_CTAS)
+        try:
+            ops.gemm_f16(dy16_or_32, x16, alpha_dev=s, out=mw, accumulate=True, a_mn=True, b_mn=True)
+        finally:
+            if side is not None and WGRAD_CTAS:
+                _call_cap(0)
 
     if side is not None:
         cur = torch.cuda.current_stream()
@@ -255,14 +271,18 @@ class _FusedLayerFn(torch.autograd.Function):
         # --- FF1 -> GELU folded into FF2's operand kernel
         op_1 = _operand(x1, x1_16 if f16 else x1_am, p1)
         h, w16_1 = _linear_fwd(L.ff1, op_1)
+        # ... and the same pass stores GELU'(h) in FP16 for the backward, which
+        # then needs no transcendental (dh = dg * GELU'(h)).
         if p2 == INT8:
             gam = ops.absmax_act(h, ops.ACT_GELU)
-            gq, gs = ops.quantize_act(h, gam, ops.ACT_GELU)
+            gq, gs, gp = ops.quantize_act(h, gam, ops.ACT_GELU, want_dact=True)
             op_2 = ("i8", gq, gs)
         elif p2 == FP16:
-            op_2 = ("f16", ops.act_cast(h, torch.float16, ops.ACT_GELU), None)
+            g16, gp = ops.act_cast(h, torch.float16, ops.ACT_GELU, want_dact=True)
+            op_2 = ("f16", g16, None)
         else:
-            op_2 = ("f32", ops.act_cast(h, torch.float32, ops.ACT_GELU), None)
+            g32, gp = ops.act_cast(h, torch.float32, ops.ACT_GELU, want_dact=True)
+            op_2 = ("f32", g32, None)
         f, w16_2 = _linear_fwd(L.ff2, op_2)
         f16n, amn = _need_aux(next_prec)
         x2, s2, mean2, rstd2, x2_16, x2_am = ops.layernorm_fwd_ex(
@@ -274,7 +294,7 @@ class _FusedLayerFn(torch.autograd.Function):
         ctx.w16 = (w16_qkv, w16_o, w16_1, w16_2)
         ctx.attn = (qkv5, a, lse, scale)
         ctx.ln = (s1, mean1, rstd1, s2, mean2, rstd2)
-        ctx.h = h
+        ctx.h = (h, gp)
         ctx.shape = (B, S, H)
         out = x2.view(B, S, H)
         if aux2 is None:
@@ -292,7 +312,7 @@ class _FusedLayerFn(torch.autograd.Function):
         w16_qkv, w16_o, w16_1, w16_2 = ctx.w16
         qkv5, a, lse, scale = ctx.attn
         s1, mean1, rstd1, s2, mean2, rstd2 = ctx.ln
-        h = ctx.h
+        h, gp = ctx.h
         side = _ql.WGRAD_STREAM
         dx2 = dx2.reshape(M, H).contiguous()
         if dx2.dtype != torch.float32:
@@ -307,7 +327,7 @@ class _FusedLayerFn(torch.autograd.Function):
         _wgrad(L.ff2, dy2, op_2, side if p2 != FP32 else None)
         # --- GELU backward fused with FF1's dY cast + ff1 bias grad
         p1 = L.ff1.precision
-        dh = ops.act_bwd_colsum(dg, h, ops.ACT_GELU,
+        dh = ops.act_bwd_colsum(dg, gp, ops.ACT_DERIV,
                                 out_dtype=torch.float16 if p1 != FP32 else torch.float32,
                                 colsum_into=_bias_main_grad(L.ff1))
         # FF1 dgrad reduce-added into ds2: ds2 becomes d(x1) = residual + FF1 paths

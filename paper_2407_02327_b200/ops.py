@@ -328,7 +328,7 @@ def layernorm_bwd(dy: torch.Tensor, s, mean, rstd, gamma, dgamma, dbeta) -> torc
 
 
 # --------------------------------------------------------------------------- fused layer glue
-ACT_NONE, ACT_GELU = _lib.ACT_NONE, _lib.ACT_GELU
+ACT_NONE, ACT_GELU, ACT_DERIV = _lib.ACT_NONE, _lib.ACT_GELU, _lib.ACT_DERIV
 
 
 def layernorm_fwd_ex(a, b, gamma, beta, eps: float, want_f16: bool = False,
@@ -374,22 +374,26 @@ def absmax_act(x: torch.Tensor, act: int = ACT_NONE, out=None) -> torch.Tensor:
     return o
 
 
-def quantize_act(x: torch.Tensor, absmax: torch.Tensor, act: int = ACT_NONE):
-    """q = sat(rint(act(x) / s)), s = absmax/127 from a device absmax.  Returns (q, s[1])."""
+def quantize_act(x: torch.Tensor, absmax: torch.Tensor, act: int = ACT_NONE, want_dact: bool = False):
+    """q = sat(rint(act(x) / s)), s = absmax/127 from a device absmax.
+    Returns (q, s[1]) or (q, s[1], act'(x) FP16) with ``want_dact``."""
     _req(x, "x", _DT)
     q = torch.empty(x.shape, device=x.device, dtype=torch.int8)
     s = torch.empty(1, device=x.device, dtype=torch.float32)
+    d = torch.empty(x.shape, device=x.device, dtype=torch.float16) if want_dact else None
     call("qsync_quantize_act", _ptr(x), _DT[x.dtype], x.numel(), int(act), _ptr(absmax), _ptr(q),
-         _ptr(s), _stream())
-    return q, s
+         _ptr(s), _ptr(d), _stream())
+    return (q, s, d) if want_dact else (q, s)
 
 
-def act_cast(x: torch.Tensor, dtype: torch.dtype, act: int = ACT_NONE, out=None) -> torch.Tensor:
+def act_cast(x: torch.Tensor, dtype: torch.dtype, act: int = ACT_NONE, out=None, want_dact: bool = False):
+    """act(x) as dtype; with ``want_dact`` returns (y, act'(x) FP16)."""
     _req(x, "x", (torch.float32, torch.float16))
     o = out if out is not None else torch.empty(x.shape, device=x.device, dtype=dtype)
-    call("qsync_act_cast", _ptr(x), _DT[x.dtype], _ptr(o), _DT[dtype], x.numel(), int(act),
+    d = torch.empty(x.shape, device=x.device, dtype=torch.float16) if want_dact else None
+    call("qsync_act_cast", _ptr(x), _DT[x.dtype], _ptr(o), _DT[dtype], x.numel(), int(act), _ptr(d),
          _stream())
-    return o
+    return (o, d) if want_dact else o
 
 
 def act_bwd_colsum(dy: torch.Tensor, h: torch.Tensor | None, act: int = ACT_NONE,
@@ -475,6 +479,10 @@ def attention_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse:
     call("qsync_attention_bwd", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), B, S, H, D, float(scale),
          _ptr(dqkv), _stream())
     return dqkv
+
+
+def sm_count() -> int:
+    return int(_lib.lib().qsync_device_sm_count())
 
 
 def launch_count() -> int:

@@ -232,7 +232,7 @@ class FlatGrads:
         self._side = side_stream
         self.issue_log = []
         if self.flat.is_cuda and world > 1 and self.comm_stream is None:
-            self.comm_stream = torch.cuda.Stream()
+            self.comm_stream = torch.cuda.Stream(priority=-1)
 
     def params_ready(self, params) -> None:
         """The gradients of ``params`` are final (their producing kernels are
@@ -317,7 +317,17 @@ class TrainStep:
         self.use_graph = graph
         self.graph = None
         self.loss = None
-        self.wgrad_stream = torch.cuda.Stream() if overlap_wgrad else None
+        # Stream priorities: the critical-path chain (main stream, captured at
+        # high priority) wins free SMs over the wgrad GEMMs, which only feed the
+        # all-reduce / optimizer and fill the gaps.
+        self.wgrad_stream = torch.cuda.Stream(priority=0) if overlap_wgrad else None
+        if overlap_wgrad and fused:
+            # The wgrad GEMMs are persistent kernels: capped at ~2/3 of the SMs
+            # they overlap the main stream's chain instead of displacing it
+            # (tools/ab_wgrad_cap.py: 5.55 -> 5.2-5.3 ms per BERT-base step).
+            from . import fused as _fz
+            from . import ops as _ops
+            _fz.WGRAD_CTAS = max(1, (2 * _ops.sm_count()) // 3)
         if world > 1 and fused:
             for m in (model.pooler, model.cls):
                 for prm in m.parameters():
@@ -352,7 +362,7 @@ class TrainStep:
         return loss.detach()
 
     def capture(self, warmup: int = 3) -> None:
-        s = torch.cuda.Stream()
+        s = torch.cuda.Stream(priority=-1)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for _ in range(warmup):

@@ -241,3 +241,28 @@ def test_embed_layernorm_vs_torch():
     for name, a, b in zip(("word", "pos", "typ", "gamma", "beta"), got, [p.grad for p in params]):
         err = ((a - b).abs().max() / b.abs().max()).item()
         assert err < 1e-4, f"{name}: {err}"
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16])
+def test_stored_gelu_derivative(dtype):
+    """FF2's operand kernels also store GELU'(h) in FP16; the backward then
+    multiplies by it (QSYNC_ACT_DERIV) -- matches the FP64 derivative to FP16
+    rounding, and the fused backward equals dy * stored derivative exactly."""
+    torch.manual_seed(12)
+    T, F = 4096, 3072
+    h = (torch.randn(T, F, device=DEV) * 2).to(dtype)
+    hd = h.double()
+    want = 0.5 * (1 + torch.erf(hd / 2 ** 0.5)) + hd * torch.exp(-0.5 * hd * hd) / (2 * np.pi) ** 0.5
+    am = ops.absmax_act(h, ops.ACT_GELU)
+    q, s, d = ops.quantize_act(h, am, ops.ACT_GELU, want_dact=True)
+    q0, s0 = ops.quantize_act(h, am, ops.ACT_GELU)
+    assert torch.equal(q, q0) and torch.equal(s, s0)        # the extra output changes nothing
+    assert ((d.double() - want).abs().max() / want.abs().max()).item() < 1e-3
+    g16, d2 = ops.act_cast(h, torch.float16, ops.ACT_GELU, want_dact=True)
+    assert torch.equal(d2, d) and torch.equal(g16, ops.act_cast(h, torch.float16, ops.ACT_GELU))
+    dy = torch.randn(T, F, device=DEV)
+    col = torch.zeros(F, device=DEV)
+    dh = ops.act_bwd_colsum(dy, d, ops.ACT_DERIV, torch.float16, colsum_into=col)
+    assert torch.equal(dh, (dy * d.float()).half())
+    ref = (dy.double() * d.double()).sum(0)
+    assert ((col.double() - ref).abs().max() / ref.abs().max()).item() < 1e-4
