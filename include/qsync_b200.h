@@ -316,6 +316,14 @@ typedef struct qsync_adamw_seg {
 int qsync_adamw_step(const qsync_adamw_seg* segs, int nseg, const int64_t* seg_row_start,
                      int64_t total_rows, int64_t* step, float lr, float beta1, float beta2,
                      float eps, float weight_decay, int update, qsync_stream_t stream);
+/* The same update over the global rows [row_begin, row_end) only (a gradient
+ * bucket whose parameters are final -- the optimizer then overlaps the rest of
+ * the backward), reading the step counter without advancing it; call
+ * qsync_adamw_advance once after every range of the step has been enqueued. */
+int qsync_adamw_step_range(const qsync_adamw_seg* segs, int nseg, const int64_t* seg_row_start,
+                           int64_t row_begin, int64_t row_end, const int64_t* step, float lr, float beta1,
+                           float beta2, float eps, float weight_decay, int update, qsync_stream_t stream);
+int qsync_adamw_advance(int64_t* step, qsync_stream_t stream);
 
 #ifdef __cplusplus
 }

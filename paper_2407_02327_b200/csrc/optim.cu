@@ -54,7 +54,7 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, con
 }
 
 __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __restrict__ segs, int nseg,
-                                                       const int64_t* seg_start,
+                                                       const int64_t* seg_start, int64_t row_begin,
                                                        int64_t total_rows, const int64_t* __restrict__ step,
                                                        float lr, float b1, float b2, float eps, float wd,
                                                        int update) {
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
     __syncthreads();
     seg_start = s_start;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
-    for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5); row < total_rows;
+    for (int64_t row = row_begin + static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5); row < total_rows;
          row += nwarps) {
         const int s = find_seg(seg_start, nseg, row);
         const qsync_adamw_seg sg = segs[s];
@@ -196,25 +196,39 @@ using namespace qsb;
 
 extern "C" {
 
-int qsync_adamw_step(const qsync_adamw_seg* segs, int nseg, const int64_t* seg_row_start,
-                     int64_t total_rows, int64_t* step, float lr, float beta1, float beta2, float eps,
-                     float weight_decay, int update, qsync_stream_t stream) {
+int qsync_adamw_step_range(const qsync_adamw_seg* segs, int nseg, const int64_t* seg_row_start,
+                           int64_t row_begin, int64_t row_end, const int64_t* step, float lr, float beta1,
+                           float beta2, float eps, float weight_decay, int update, qsync_stream_t stream) {
     QSB_REQUIRE(segs && seg_row_start && nseg > 0, QSYNC_ERR_VALIDATION, "segment table is required");
-    QSB_REQUIRE(total_rows >= 0, QSYNC_ERR_DOMAIN, "negative row count");
+    QSB_REQUIRE(row_begin >= 0 && row_end >= row_begin, QSYNC_ERR_DOMAIN, "bad row range");
     QSB_REQUIRE(!update || step != nullptr, QSYNC_ERR_VALIDATION, "step counter is required");
     QSB_REQUIRE(!update || (beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f),
                 QSYNC_ERR_DOMAIN, "AdamW needs 0 <= beta < 1 and eps > 0");
-    if (total_rows == 0) return QSYNC_OK;
+    if (row_end == row_begin) return QSYNC_OK;
     cudaStream_t st = to_stream(stream);
-    const int grid = static_cast<int>(std::min<int64_t>((total_rows + kWarps - 1) / kWarps, sm_count() * 16LL));
+    const int grid =
+        static_cast<int>(std::min<int64_t>((row_end - row_begin + kWarps - 1) / kWarps, sm_count() * 16LL));
     const size_t smem = sizeof(int64_t) * (static_cast<size_t>(nseg) + 1);
     QSB_REQUIRE(smem <= 48 * 1024, QSYNC_ERR_DOMAIN, "too many parameter segments");
-    k_adamw<<<grid, kWarps * 32, smem, st>>>(segs, nseg, seg_row_start, total_rows, step, lr, beta1, beta2, eps,
-                                          weight_decay, update);
-    QSB_TRY(check_launch("k_adamw"));
-    if (!update) return QSYNC_OK;
-    k_step_inc<<<1, 1, 0, st>>>(step);
+    k_adamw<<<grid, kWarps * 32, smem, st>>>(segs, nseg, seg_row_start, row_begin, row_end, step, lr, beta1,
+                                             beta2, eps, weight_decay, update);
+    return check_launch("k_adamw");
+}
+
+int qsync_adamw_advance(int64_t* step, qsync_stream_t stream) {
+    QSB_REQUIRE(step != nullptr, QSYNC_ERR_VALIDATION, "step counter is required");
+    k_step_inc<<<1, 1, 0, to_stream(stream)>>>(step);
     return check_launch("k_step_inc");
+}
+
+int qsync_adamw_step(const qsync_adamw_seg* segs, int nseg, const int64_t* seg_row_start,
+                     int64_t total_rows, int64_t* step, float lr, float beta1, float beta2, float eps,
+                     float weight_decay, int update, qsync_stream_t stream) {
+    QSB_REQUIRE(total_rows >= 0, QSYNC_ERR_DOMAIN, "negative row count");
+    QSB_TRY(qsync_adamw_step_range(segs, nseg, seg_row_start, 0, total_rows, step, lr, beta1, beta2, eps,
+                                   weight_decay, update, stream));
+    if (!update || total_rows == 0) return QSYNC_OK;
+    return qsync_adamw_advance(step, stream);
 }
 
 }  // extern "C"

@@ -111,6 +111,8 @@ class FusedAdamW:
             s.wscale = _p(getattr(mod, "ws", None)) if mod is not None else None
             s.rows, s.cols = rows, cols
             starts.append(starts[-1] + rows)
+        self._index = {id(p): i for i, p in enumerate(self.params)}
+        self._row_start = starts
         raw = np.frombuffer(bytes(segs), dtype=np.uint8).copy()
         dev = self.params[0].device
         self._segs = torch.from_numpy(raw).to(dev)
@@ -126,6 +128,25 @@ class FusedAdamW:
 
     def step(self) -> None:
         self._launch(1)
+
+    def rows_of(self, params) -> tuple[int, int]:
+        """Global row range [begin, end) covering ``params`` (contiguous in the
+        optimizer's parameter order, as a gradient bucket is)."""
+        idx = [self._index[id(p)] for p in params if id(p) in self._index]
+        if not idx:
+            return 0, 0
+        return self._row_start[min(idx)], self._row_start[max(idx) + 1]
+
+    def step_range(self, r0: int, r1: int) -> None:
+        """Update rows [r0, r1) now (bucket-wise optimizer); no step advance."""
+        if r1 > r0:
+            call("qsync_adamw_step_range", self._segs.data_ptr(), self._nseg, self._starts.data_ptr(), int(r0),
+                 int(r1), self.step_t.data_ptr(), float(self.lr), float(self.betas[0]), float(self.betas[1]),
+                 float(self.eps), float(self.wd), 1, torch.cuda.current_stream().cuda_stream)
+
+    def advance(self) -> None:
+        """Advance the device step counter once every range of the step is enqueued."""
+        call("qsync_adamw_advance", self.step_t.data_ptr(), torch.cuda.current_stream().cuda_stream)
 
     def prepare(self) -> None:
         """Recompute the weight copies from the current weights (no update)."""
