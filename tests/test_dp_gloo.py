@@ -97,7 +97,8 @@ def _worker_overlap(rank, world, port, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     params = _params()
     g = FlatGrads(params, bucket_bytes=4 << 20)
-    g.begin(world)
+    finals = []
+    g.begin(world, on_final=lambda b: finals.append((b, float(g.flat[g.buckets[b][0]]))))
     issued_after = []
     # backward order = reverse of the forward parameter order; grads become final
     # one parameter at a time, as the layers' backward passes report them
@@ -106,7 +107,8 @@ def _worker_overlap(rank, world, port, out_dir):
         g.params_ready([p])
         issued_after.append(g._next)
     g.finish()
-    first = {"issued_after": issued_after, "log": g.issue_log,
+    first = {"issued_after": issued_after, "log": g.issue_log, "finals": finals,
+             "expect_first": [float(g.flat[a]) for a, _ in g.buckets],
              "bucket_of": [g.bucket_of[id(p)] for p in reversed(params)],
              "vals": [float(p.main_grad.flatten()[0]) for p in reversed(params)]}
     # second pass: only the first two parameters report; finish() forces the rest
@@ -144,6 +146,10 @@ def test_overlapped_bucket_allreduce_world2(tmp_path):
         assert n_issued == (bo[i] + 1 if done else bo[i])
     for i, v in enumerate(f0["vals"]):
         assert v == pytest.approx(1.5 * (i + 1))
+    # the per-bucket hook (the bucket-wise optimizer) runs once per bucket, in
+    # order, and sees the already-averaged gradients
+    assert [b for b, _ in f0["finals"]] == list(range(nb))
+    assert [v for _, v in f0["finals"]] == pytest.approx(f0["expect_first"])
     s0 = r0["second"]
     assert s0["partial"] <= 1 and [b for b, _ in s0["log"]] == list(range(nb))
     assert all(v == pytest.approx(1.5) for v in s0["vals"])
