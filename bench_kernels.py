@@ -117,6 +117,116 @@ def gemm_bench(results: dict) -> None:
     print(f"int8 peak (cuBLASLt 8192^3 best of 10): {i8_peak:.1f} TOPS")
 
 
+def graph_time_us(fn, n=10, reps=5):
+    """Per-call device time of fn() captured n times into one CUDA graph."""
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        fn()
+    torch.cuda.current_stream().wait_stream(st)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(n):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e3 / n)
+    return best
+
+
+def spin_time_ms(fn, reps=5, spin_cycles=100_000_000):
+    """Median device time of fn() with its launches queued behind a device spin."""
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        torch.cuda._sleep(spin_cycles)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def resnet50_convs(batch: int = 64):
+    """The 53 Conv2d layers of ResNet-50 at 224x224 (NHWC): (name, N, H, W, C, Cout, R, stride, pad)."""
+    convs = [("conv1", batch, 224, 224, 3, 64, 7, 2, 3)]
+    h, cin = 56, 64
+    for stage, (width, blocks, stride) in enumerate([(64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2)]):
+        for b in range(blocks):
+            s = stride if b == 0 else 1
+            hin = h
+            ho = h // s
+            convs.append((f"res{stage + 2}.{b}.a", batch, hin, hin, cin, width, 1, 1, 0))
+            convs.append((f"res{stage + 2}.{b}.b", batch, hin, hin, width, width, 3, s, 1))
+            convs.append((f"res{stage + 2}.{b}.c", batch, ho, ho, width, 4 * width, 1, 1, 0))
+            if b == 0:
+                convs.append((f"res{stage + 2}.{b}.ds", batch, hin, hin, cin, 4 * width, 1, s, 0))
+            cin, h = 4 * width, ho
+    return convs
+
+
+def conv_bench(results: dict, batch: int = 64) -> None:
+    """BASELINE configs[2]: the ResNet-50 convolutions as GEMMs (INT8 / FP16 plans),
+    forward and forward+backward per distinct layer shape, summed over the 53 layers."""
+    from paper_2407_02327_b200.qconv import qconv2d
+    from paper_2407_02327_b200.qlinear import FP16, INT8
+    convs = resnet50_convs(batch)
+    distinct = {}
+    for c in convs:
+        distinct.setdefault(c[1:], []).append(c[0])
+    rows = []
+    totals = {INT8: [0.0, 0.0], FP16: [0.0, 0.0]}
+    flops_fwd = 0.0
+    for key, names in distinct.items():
+        N, H, W, C, Cout, R, st, pd = key
+        P = (H + 2 * pd - R) // st + 1
+        fl = 2.0 * N * P * P * Cout * R * R * C
+        flops_fwd += fl * len(names)
+        x = torch.randn(N, H, W, C, device="cuda")
+        w = (torch.randn(Cout, R, R, C, device="cuda") / (R * R * C) ** 0.5).requires_grad_(True)
+        b = torch.zeros(Cout, device="cuda", requires_grad=True)
+        for prec in (INT8, FP16):
+            xin = x if prec == INT8 else x.half()
+            xg = xin.detach().clone().requires_grad_(True)
+            # Device time with the launches queued behind a device spin, so the
+            # host's launch overhead is excluded (as in the CUDA-graphed step).
+            tf = spin_time_ms(lambda: qconv2d(xin, w, b, (st, st), (pd, pd), prec))
+            y = qconv2d(xg, w, b, (st, st), (pd, pd), prec)
+            gy = torch.randn_like(y)
+
+            def fb():
+                yy = qconv2d(xg, w, b, (st, st), (pd, pd), prec)
+                yy.backward(gy)
+            tfb = spin_time_ms(fb)
+            totals[prec][0] += tf * len(names)
+            totals[prec][1] += tfb * len(names)
+            rows.append({"layers": names, "N": N, "H": H, "C": C, "Cout": Cout, "R": R, "stride": st,
+                         "precision": prec, "fwd_ms": tf, "fwd_bwd_ms": tfb,
+                         "fwd_tops": fl / (tf * 1e-3) / 1e12, "fwd_bwd_tops": 3 * fl / (tfb * 1e-3) / 1e12})
+            print(f"{names[0]:10s} x{len(names)} {prec} C={C:4d}->{Cout:4d} R={R} s={st} H={H:3d}: "
+                  f"fwd {tf*1e3:8.1f} us ({fl/(tf*1e-3)/1e12:6.1f} TOPS)  fwd+bwd {tfb*1e3:8.1f} us", flush=True)
+        del x, w, b
+        torch.cuda.empty_cache()
+    results["resnet50_convs"] = {
+        "batch": batch, "layers": len(convs), "fwd_gflop": flops_fwd / 1e9, "rows": rows,
+        "stack": {p: {"fwd_ms": v[0], "fwd_bwd_ms": v[1], "fwd_tflops": flops_fwd / (v[0] * 1e-3) / 1e12,
+                      "fwd_bwd_tflops": 3 * flops_fwd / (v[1] * 1e-3) / 1e12} for p, v in totals.items()}}
+    for p, v in totals.items():
+        print(f"ResNet-50 conv stack (53 layers, batch {batch}) {p}: fwd {v[0]:.2f} ms, fwd+bwd {v[1]:.2f} ms "
+              f"({3 * flops_fwd / (v[1] * 1e-3) / 1e12:.0f} TFLOP/s)")
+
+
 def sweep_bench(results: dict) -> None:
     pk = peaks()
     bw = pk["hbm_gbs"]
@@ -155,12 +265,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--gemm", action="store_true")
+    ap.add_argument("--conv", action="store_true")
     ap.add_argument("--json", default=None)
     args = ap.parse_args()
     res: dict = {"peaks": peaks()}
-    if args.gemm or not args.sweep:
+    everything = not (args.gemm or args.sweep or args.conv)
+    if args.gemm or everything:
         gemm_bench(res)
-    if args.sweep or not args.gemm:
+    if args.conv or everything:
+        conv_bench(res)
+    if args.sweep or everything:
         sweep_bench(res)
     if args.json:
         with open(args.json, "w") as f:

@@ -22,47 +22,53 @@ struct ConvGeom {
     int64_t ld;  // row pitch of the column matrix (>= R*S*C)
 };
 
-// One thread per 16-byte (or element, on the scalar path) chunk of a column row.
-// Rows are (n,p,q); within a row the (r,s) taps are C-contiguous runs.
+// One warp per column row (n,p,q): the row's coordinates are decoded once, the
+// lanes stride over its 16-byte chunks (tap = chunk / (C/V), 32-bit math).
+// Scalar fallback (C not a multiple of the vector width) keeps one element per lane.
 template <typename T>
 __global__ void __launch_bounds__(256) k_im2col(const T* __restrict__ x, ConvGeom g,
                                                 T* __restrict__ out, int vec) {
     constexpr int V = 16 / sizeof(T);  // elements per 16-byte chunk
-    const int64_t K = static_cast<int64_t>(g.R) * g.S * g.C;
-    const int64_t chunks_per_row = vec ? g.ld / V : g.ld;
-    const int64_t total = g.N * g.P * g.Q * chunks_per_row;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = idx / chunks_per_row;
-        const int64_t ch = idx - row * chunks_per_row;
-        const int64_t q = row % g.Q;
-        const int64_t p = (row / g.Q) % g.P;
-        const int64_t n = row / (g.Q * g.P);
+    const int lane = threadIdx.x & 31;
+    const int K = g.R * g.S * static_cast<int>(g.C);
+    const int C = static_cast<int>(g.C);
+    const int rows = static_cast<int>(g.N * g.P * g.Q);
+    const int P = static_cast<int>(g.P), Q = static_cast<int>(g.Q);
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows; row += warps) {
+        const int q = row % Q;
+        const int p = (row / Q) % P;
+        const int n = row / (Q * P);
+        const int h0 = p * g.sh - g.ph, w0 = q * g.sw - g.pw;
+        const T* xn = x + static_cast<int64_t>(n) * g.H * g.W * C;
+        T* orow = out + static_cast<int64_t>(row) * g.ld;
         if (vec) {
-            const int64_t k0 = ch * V;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (k0 < K) {
-                const int64_t tap = k0 / g.C;
-                const int64_t c = k0 - tap * g.C;
-                const int r = static_cast<int>(tap / g.S), s = static_cast<int>(tap % g.S);
-                const int64_t h = p * g.sh - g.ph + r * g.dh;
-                const int64_t w = q * g.sw - g.pw + s * g.dw;
-                if (h >= 0 && h < g.H && w >= 0 && w < g.W)
-                    v = *reinterpret_cast<const uint4*>(x + ((n * g.H + h) * g.W + w) * g.C + c);
+            const int CV = C / V;
+            const int nch = static_cast<int>(g.ld / V);
+            for (int j = lane; j < nch; j += 32) {
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (j * V < K) {
+                    const int tap = j / CV;
+                    const int c = (j - tap * CV) * V;
+                    const int r = tap / g.S, ss = tap - r * g.S;
+                    const int h = h0 + r * g.dh, w = w0 + ss * g.dw;
+                    if (h >= 0 && h < g.H && w >= 0 && w < g.W)
+                        v = *reinterpret_cast<const uint4*>(xn + (static_cast<int64_t>(h) * g.W + w) * C + c);
+                }
+                *reinterpret_cast<uint4*>(orow + j * V) = v;
             }
-            *reinterpret_cast<uint4*>(out + row * g.ld + k0) = v;
         } else {
-            const int64_t k = ch;
-            T v = T(0);
-            if (k < K) {
-                const int64_t tap = k / g.C;
-                const int64_t c = k - tap * g.C;
-                const int r = static_cast<int>(tap / g.S), s = static_cast<int>(tap % g.S);
-                const int64_t h = p * g.sh - g.ph + r * g.dh;
-                const int64_t w = q * g.sw - g.pw + s * g.dw;
-                if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = x[((n * g.H + h) * g.W + w) * g.C + c];
+            for (int k = lane; k < g.ld; k += 32) {
+                T v = T(0);
+                if (k < K) {
+                    const int tap = k / C;
+                    const int c = k - tap * C;
+                    const int r = tap / g.S, ss = tap - r * g.S;
+                    const int h = h0 + r * g.dh, w = w0 + ss * g.dw;
+                    if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = xn[(static_cast<int64_t>(h) * g.W + w) * C + c];
+                }
+                orow[k] = v;
             }
-            out[row * g.ld + k] = v;
         }
     }
 }
@@ -72,30 +78,95 @@ __device__ __forceinline__ float ldf(const void* p, int64_t i) {
     return Elem<DT>::f(static_cast<const typename Elem<DT>::T*>(p)[i]);
 }
 
-// dx[n,h,w,c] (FP32) = sum of the column entries that gathered x[n,h,w,c].
+// dx[n,h,w,c] (FP32) = sum of the column entries that gathered x[n,h,w,c]: one
+// warp per input pixel (the (r,s) tap validity is warp-uniform), lanes over
+// channel groups of 4 (16-byte FP32 column loads, one float4 store).
 template <int DT>
 __global__ void __launch_bounds__(256) k_col2im(const void* __restrict__ dcol, ConvGeom g,
-                                                float* __restrict__ dx) {
-    const int64_t total = g.N * g.H * g.W * g.C;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = idx % g.C;
-        const int64_t w = (idx / g.C) % g.W;
-        const int64_t h = (idx / (g.C * g.W)) % g.H;
-        const int64_t n = idx / (g.C * g.W * g.H);
-        float acc = 0.0f;
-        for (int r = 0; r < g.R; ++r) {
-            const int64_t hp = h + g.ph - r * g.dh;
-            if (hp < 0 || hp % g.sh) continue;
-            const int64_t p = hp / g.sh;
+                                                float* __restrict__ dx, int vec) {
+    const int lane = threadIdx.x & 31;
+    const int C = static_cast<int>(g.C);
+    const int pixels = static_cast<int>(g.N * g.H * g.W);
+    const int H = static_cast<int>(g.H), W = static_cast<int>(g.W);
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int pix = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); pix < pixels; pix += warps) {
+        const int w = pix % W;
+        const int h = (pix / W) % H;
+        const int n = pix / (W * H);
+        float* out = dx + static_cast<int64_t>(pix) * C;
+        const int groups = vec ? C / 4 : C;
+        for (int cg = lane; cg < groups; cg += 32) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            // With dilation 1 only every sh-th (sw-th) tap can land on this
+            // pixel: start at the first such tap and step by the stride.
+            const int r0 = g.dh == 1 ? (h + g.ph) % g.sh : 0, rstep = g.dh == 1 ? g.sh : 1;
+            const int s0 = g.dw == 1 ? (w + g.pw) % g.sw : 0, sstep = g.dw == 1 ? g.sw : 1;
+            for (int r = r0; r < g.R; r += rstep) {
+                const int hp = h + g.ph - r * g.dh;
+                if (hp < 0) break;
+                if (hp % g.sh) continue;
+                const int p = hp / g.sh;
+                if (p >= g.P) continue;
+                for (int s = s0; s < g.S; s += sstep) {
+                    const int wq = w + g.pw - s * g.dw;
+                    if (wq < 0) break;
+                    if (wq % g.sw) continue;
+                    const int q = wq / g.sw;
+                    if (q >= g.Q) continue;
+                    const int64_t row = (static_cast<int64_t>(n) * g.P + p) * g.Q + q;
+                    const int64_t base = row * g.ld + static_cast<int64_t>(r * g.S + s) * C;
+                    if (vec) {
+                        if (DT == QSYNC_F32) {
+                            const float4 v = *reinterpret_cast<const float4*>(static_cast<const float*>(dcol) + base + 4 * cg);
+                            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                        } else {
+                            const uint2 u = *reinterpret_cast<const uint2*>(static_cast<const __half*>(dcol) + base + 4 * cg);
+                            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+                            const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+                            acc.x += a.x; acc.y += a.y; acc.z += b.x; acc.w += b.y;
+                        }
+                    } else {
+                        acc.x += ldf<DT>(dcol, base + cg);
+                    }
+                }
+            }
+            if (vec)
+                *reinterpret_cast<float4*>(out + 4 * cg) = acc;
+            else
+                out[cg] = acc.x;
+        }
+    }
+}
+
+// Scalar col2im for channel counts that are not a vector multiple (ResNet
+// conv1, C = 3): one thread per element, 32-bit index math, so narrow pixels
+// do not leave most of a warp idle.
+template <int DT>
+__global__ void __launch_bounds__(256) k_col2im_s(const void* __restrict__ dcol, ConvGeom g, float* __restrict__ dx) {
+    const int C = static_cast<int>(g.C);
+    const int H = static_cast<int>(g.H), W = static_cast<int>(g.W);
+    const int total = static_cast<int>(g.N * g.H * g.W * g.C);  // < 2^31 (checked by the caller)
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int pix = idx / C;
+        const int c = idx - pix * C;
+        const int w = pix % W, h = (pix / W) % H, n = pix / (W * H);
+        float acc = 0.f;
+        const int r0 = g.dh == 1 ? (h + g.ph) % g.sh : 0, rstep = g.dh == 1 ? g.sh : 1;
+        const int s0 = g.dw == 1 ? (w + g.pw) % g.sw : 0, sstep = g.dw == 1 ? g.sw : 1;
+        for (int r = r0; r < g.R; r += rstep) {
+            const int hp = h + g.ph - r * g.dh;
+            if (hp < 0) break;
+            if (hp % g.sh) continue;
+            const int p = hp / g.sh;
             if (p >= g.P) continue;
-            for (int s = 0; s < g.S; ++s) {
-                const int64_t wq = w + g.pw - s * g.dw;
-                if (wq < 0 || wq % g.sw) continue;
-                const int64_t q = wq / g.sw;
+            for (int s = s0; s < g.S; s += sstep) {
+                const int wq = w + g.pw - s * g.dw;
+                if (wq < 0) break;
+                if (wq % g.sw) continue;
+                const int q = wq / g.sw;
                 if (q >= g.Q) continue;
-                const int64_t row = (n * g.P + p) * g.Q + q;
-                acc += ldf<DT>(dcol, row * g.ld + (static_cast<int64_t>(r) * g.S + s) * g.C + c);
+                const int64_t row = (static_cast<int64_t>(n) * g.P + p) * g.Q + q;
+                acc += ldf<DT>(dcol, row * g.ld + static_cast<int64_t>(r * g.S + s) * C + c);
             }
         }
         dx[idx] = acc;
@@ -119,9 +190,9 @@ int make_geom(ConvGeom& g, int64_t N, int64_t H, int64_t W, int64_t C, int R, in
     return QSYNC_OK;
 }
 
-int grid_of(int64_t work) {
-    const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap)));
+int grid_of(int64_t warps_of_work) {  // blocks of 8 warps
+    const int64_t cap = static_cast<int64_t>(sm_count()) * 16;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((warps_of_work + 7) / 8, cap)));
 }
 
 }  // namespace
@@ -146,16 +217,17 @@ int qsync_im2col(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int6
     ConvGeom g;
     QSB_TRY(make_geom(g, N, H, W, C, R, S, sh, sw, ph, pw, dh, dw, ld));
     if (N == 0) return QSYNC_OK;
+    QSB_REQUIRE(g.N * g.P * g.Q < (int64_t(1) << 31), QSYNC_ERR_DOMAIN, "conv too large");
     cudaStream_t st = to_stream(stream);
     const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     if (dtype == QSYNC_I8) {
         const int vec = (C % 16 == 0) && (g.ld % 16 == 0) && al(x) && al(out);
-        const int64_t work = g.N * g.P * g.Q * (vec ? g.ld / 16 : g.ld);
+        const int64_t work = g.N * g.P * g.Q;
         k_im2col<int8_t><<<grid_of(work), 256, 0, st>>>(static_cast<const int8_t*>(x), g,
                                                          static_cast<int8_t*>(out), vec);
     } else if (dtype == QSYNC_F16 || dtype == QSYNC_BF16) {
         const int vec = (C % 8 == 0) && (g.ld % 8 == 0) && al(x) && al(out);
-        const int64_t work = g.N * g.P * g.Q * (vec ? g.ld / 8 : g.ld);
+        const int64_t work = g.N * g.P * g.Q;
         k_im2col<uint16_t><<<grid_of(work), 256, 0, st>>>(static_cast<const uint16_t*>(x), g,
                                                            static_cast<uint16_t*>(out), vec);
     } else {
@@ -171,10 +243,21 @@ int qsync_col2im(const void* dcol, int dtype, int64_t N, int64_t H, int64_t W, i
     QSB_TRY(make_geom(g, N, H, W, C, R, S, sh, sw, ph, pw, dh, dw, ld));
     if (N == 0) return QSYNC_OK;
     cudaStream_t st = to_stream(stream);
-    const int grid = grid_of(N * H * W * C);
+    QSB_REQUIRE(N * H * W * C < (int64_t(1) << 31) && g.N * g.P * g.Q < (int64_t(1) << 31), QSYNC_ERR_DOMAIN,
+                "conv too large");
+    const int grid = grid_of(N * H * W);
+    const int vec = (C % 4 == 0) && (g.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(dcol) & 15u) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(dx) & 15u) == 0);
+    const int grid_s = grid_of(N * H * W * C / 32 + 1);
     switch (dtype) {
-        case QSYNC_F32: k_col2im<QSYNC_F32><<<grid, 256, 0, st>>>(dcol, g, dx); break;
-        case QSYNC_F16: k_col2im<QSYNC_F16><<<grid, 256, 0, st>>>(dcol, g, dx); break;
+        case QSYNC_F32:
+            if (vec) k_col2im<QSYNC_F32><<<grid, 256, 0, st>>>(dcol, g, dx, vec);
+            else k_col2im_s<QSYNC_F32><<<grid_s, 256, 0, st>>>(dcol, g, dx);
+            break;
+        case QSYNC_F16:
+            if (vec) k_col2im<QSYNC_F16><<<grid, 256, 0, st>>>(dcol, g, dx, vec);
+            else k_col2im_s<QSYNC_F16><<<grid_s, 256, 0, st>>>(dcol, g, dx);
+            break;
         default: return set_error(QSYNC_ERR_DOMAIN, "col2im supports F32 and F16 columns");
     }
     return check_launch("k_col2im");

@@ -73,8 +73,12 @@ class _QConv(torch.autograd.Function):
         # from the saved (int8 / fp16) input.
         A, _ = ops.im2col(xs_saved, R, S, stride, pad, ld=kp)
         A16 = A if A.dtype == torch.float16 else ops.cast(A, torch.float16)
-        dw2 = ops.gemm_f16(dy16, A16, out_dtype=torch.float32, a_mn=True, b_mn=True,
-                           alpha_dev=alpha if ctx.precision == INT8 else None)
+        # K of this GEMM is the pixel count (up to N*P*Q = 802,816 for conv1) while
+        # M x N is tiny: accumulate into a zeroed FP32 buffer so the kernel
+        # splits K across the SMs (partials reduce-added by TMA).
+        dw2 = torch.zeros((cout, kp), device=dy.device, dtype=torch.float32)
+        ops.gemm_f16(dy16, A16, out=dw2, accumulate=True, a_mn=True, b_mn=True,
+                     alpha_dev=alpha if ctx.precision == INT8 else None)
         dw = dw2[:, :K].reshape(ctx.w_ref.shape)
         if ctx.x_dtype != torch.float32:
             dx = dx.to(ctx.x_dtype)
