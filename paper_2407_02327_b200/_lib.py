@@ -81,6 +81,8 @@ SIGNATURES = {
     "qsync_attention_bwd": [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _f32, _p, _p],
     "qsync_embed_layernorm_fwd": [_p, _i64, _i64, _p, _p, _p, _p, _p, _i64, _f32, _p, _p, _p, _p, _p, _p, _p],
     "qsync_embed_layernorm_bwd": [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p],
+    "qsync_conv_fwd_implicit": [_p, _int, _i64, _i64, _i64, _i64, _int, _int, _int, _int, _int, _int, _p,
+                                _i64, _p, _int, _p, _p, _int, _p, _p],
     # non-header helpers
     "qsync_gemm_force_tile_n": [_int],
     "qsync_gemm_force_splitk": [_int],

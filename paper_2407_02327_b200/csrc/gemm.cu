@@ -51,6 +51,10 @@ struct EpiParams {
     int debug_epi;  // bench hook: 1 = skip epilogue math+stores (TMEM read only)
     int ksplit;     // split-K factor (>1 only with accumulate: partials reduce-add)
     int kb_per;     // k-blocks per split
+    // Implicit-GEMM convolution (kLay bit 2): A[(n,p,q), (r,s,c)] is gathered from
+    // the NHWC input on the fly -- never materialised.
+    const uint8_t* cx;  // NHWC input (elements of the GEMM operand type)
+    int cN, cH, cW, cC, cP, cQ, cS, csh, csw, cph, cpw;
 };
 
 constexpr int kStageChunkBytes = 32 * 128;  // one warp's 32 rows x 128 B staging chunk
@@ -114,11 +118,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_kb = static_cast<int>((K + bk_elems - 1) / bk_elems);
 
     if (warp == 0 && lane == 0) {
-        ptx::tma_prefetch(&tm_a);
+        if (!(kLay & 4)) ptx::tma_prefetch(&tm_a);
         ptx::tma_prefetch(&tm_b);
         if (p.tma_store) ptx::tma_prefetch(&tm_c);
         for (int s = 0; s < kStages; ++s) {
-            ptx::mbar_init(&full[s], 1);
+            // implicit conv: + one cp.async completion arrival per producer lane
+            ptx::mbar_init(&full[s], (kLay & 4) ? 33 : 1);
             ptx::mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -148,7 +153,75 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t full_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
     const uint32_t tempty_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
 
-    if (warp == 0) {
+    if (warp == 0 && (kLay & 4)) {
+        // ============ implicit-GEMM conv producer (all 32 lanes) ============
+        // A tile row m = output pixel (n,p,q); its 128-byte K-slice kb is one
+        // (r,s) tap's contiguous channel run x[n, p*sh-ph+r, q*sw-pw+s, c0:c0+bk]
+        // (C*elem % 128 == 0), copied by eight 16-byte cp.async into the
+        // 128B-swizzled K-major layout the UMMA descriptor reads; padding taps
+        // and rows past M are zero-filled (src-size 0).  Lane l owns rows l,
+        // l+32, l+64, l+96; lane 0 also TMA-loads the weight tile (B).
+        int stage = 0;
+        uint32_t phase = 0;
+        const int eb = kI8 ? 1 : 2;
+        const int rowbytes = p.cC * eb;
+        for (int u = unit0; u < num_units; u += unit_stride) {
+            const int t = u / ksplit;
+            const int m0 = (t % num_m) * kTileM;
+            const int n0 = (t / num_m) * BN;
+            int hb[4], wb[4];
+            const uint8_t* pix[4];
+            bool rok[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int m = m0 + lane + 32 * i;
+                rok[i] = m < M;
+                const int mm = rok[i] ? m : 0;
+                const int q = mm % p.cQ, pp = (mm / p.cQ) % p.cP, n = mm / (p.cQ * p.cP);
+                hb[i] = pp * p.csh - p.cph;
+                wb[i] = q * p.csw - p.cpw;
+                pix[i] = p.cx + static_cast<int64_t>(n) * p.cH * p.cW * rowbytes;
+            }
+            const int kb0 = (u % ksplit) * p.kb_per;
+            const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem_a + stage * BM * BK_BYTES;
+                uint8_t* sb = smem_b + stage * kBRows * BK_BYTES;
+                if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(&full[stage], kBRows * BK_BYTES);
+                    if (kLay & 2) {
+                        for (int j = 0; j < kBRows / 64; ++j)
+                            ptx::tma_load_2d(sb + j * bk_elems * 128, &tm_b, &full[stage], n0 + 64 * j,
+                                             kb * bk_elems);
+                    } else {
+                        ptx::tma_load_2d(sb, &tm_b, &full[stage], kb * bk_elems, n0);
+                    }
+                }
+                const int kbyte = kb * BK_BYTES;            // byte offset along K = (tap, c)
+                const int tap = kbyte / rowbytes;
+                const int cbyte = kbyte - tap * rowbytes;
+                const int r = tap / p.cS, sx = tap - r * p.cS;
+                const uint32_t sbase = ptx::smem_u32(sa);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int row = lane + 32 * i;
+                    const int h = hb[i] + r, w = wb[i] + sx;
+                    const bool ok = rok[i] && h >= 0 && h < p.cH && w >= 0 && w < p.cW;
+                    const uint8_t* src = ok ? pix[i] + (static_cast<int64_t>(h) * p.cW + w) * rowbytes + cbyte : p.cx;
+                    const uint32_t nbytes = ok ? 16u : 0u;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        ptx::cp_async16_zfill(sbase + row * 128 + ((j ^ (row & 7)) << 4), src + 16 * j, nbytes);
+                }
+                ptx::cp_async_mbar_arrive_noinc(&full[stage]);
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
             int stage = 0;
@@ -222,6 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
+                    // cp.async (generic proxy) wrote A: order it before the
+                    // tensor core's async-proxy reads.
+                    if (kLay & 4) ptx::fence_proxy_async_smem();
                     ptx::tc_fence_after();
                     const uint32_t a_addr = ptx::smem_u32(smem_a + stage * BM * BK_BYTES);
                     const uint32_t b_addr = ptx::smem_u32(smem_b + stage * kBRows * BK_BYTES);
@@ -539,7 +615,9 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     const uint32_t eb = kI8 ? 1 : 2;
     const uint32_t box_k = BK_BYTES / eb;
     CUtensorMap ma, mb, mc;
-    if (kLay & 1)  // A stored [K, M]: boxes of 64 M-elements x box_k K-rows
+    if (kLay & 4)  // implicit conv: A is gathered by the producer lanes
+        std::memset(&ma, 0, sizeof(ma));
+    else if (kLay & 1)  // A stored [K, M]: boxes of 64 M-elements x box_k K-rows
         QSB_TRY(make_map(&ma, a, dt, eb, p.M, p.K, 64, box_k));
     else
         QSB_TRY(make_map(&ma, a, dt, eb, p.K, p.M, box_k, BM));
@@ -689,6 +767,15 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     if (sh.cta == 2 && sh.bn == 64) sh.cta = 1;  // pair tiles need BN/2 >= 64 rows of B
     p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout);
     p.debug_epi = g_debug_epi;
+    if (layout == 4) {  // implicit conv: single-CTA tiles
+        sh.cta = 1;
+        p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM, 0);
+        switch (sh.bn) {
+            case 256: return launch<kI8, 256, 1, 4>(a, b, dt, p, st);
+            case 128: return launch<kI8, 128, 1, 4>(a, b, dt, p, st);
+            default: return launch<kI8, 64, 1, 4>(a, b, dt, p, st);
+        }
+    }
     if (kI8) return dispatch_shape<kI8, 0>(a, b, dt, p, st, sh);
     switch (layout) {
         case 0: return dispatch_shape<kI8, 0>(a, b, dt, p, st, sh);
@@ -796,6 +883,51 @@ int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_
     p.bias = bias;
     p.alpha = 1.0f;
     return dispatch<true>(a, b, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, to_stream(stream), g_force_bn);
+}
+
+int qsync_conv_fwd_implicit(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int R,
+                            int S, int sh, int sw, int ph, int pw, const void* w, int64_t cout, void* y,
+                            int y_dtype, const float* scale_a, const float* scale_b, int b_per_channel,
+                            const float* bias, qsync_stream_t stream) {
+    QSB_REQUIRE(x && w && y, QSYNC_ERR_VALIDATION, "implicit conv needs x, w and y");
+    QSB_REQUIRE(dtype == QSYNC_I8 || dtype == QSYNC_F16 || dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
+                "implicit conv input must be I8, F16 or BF16");
+    const int eb = dtype == QSYNC_I8 ? 1 : 2;
+    QSB_REQUIRE(N > 0 && H > 0 && W > 0 && C > 0 && R > 0 && S > 0 && sh > 0 && sw > 0 && ph >= 0 && pw >= 0,
+                QSYNC_ERR_DOMAIN, "bad conv geometry");
+    QSB_REQUIRE((C * eb) % BK_BYTES == 0, QSYNC_ERR_DOMAIN,
+                "implicit conv needs C * element size to be a multiple of 128 bytes (use im2col)");
+    const int64_t P = (H + 2 * ph - R) / sh + 1, Q = (W + 2 * pw - S) / sw + 1;
+    QSB_REQUIRE(P > 0 && Q > 0, QSYNC_ERR_DOMAIN, "conv output would be empty");
+    const int64_t M = N * P * Q, K = static_cast<int64_t>(R) * S * C;
+    QSB_REQUIRE(M < (int64_t(1) << 31) && N * H * W * C * eb < (int64_t(1) << 40), QSYNC_ERR_DOMAIN,
+                "conv too large");
+    QSB_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0,
+                QSYNC_ERR_DOMAIN, "implicit conv operands must be 16-byte aligned");
+    QSB_REQUIRE(y_dtype == QSYNC_F32 || y_dtype == QSYNC_F16 || y_dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
+                "conv output must be F32, F16 or BF16");
+    EpiParams p{};
+    p.M = M;
+    p.N = cout;
+    p.K = K;
+    p.c = y;
+    p.c_dtype = y_dtype;
+    p.bias = bias;
+    p.alpha = 1.0f;
+    p.cx = static_cast<const uint8_t*>(x);
+    p.cN = static_cast<int>(N); p.cH = static_cast<int>(H); p.cW = static_cast<int>(W);
+    p.cC = static_cast<int>(C); p.cP = static_cast<int>(P); p.cQ = static_cast<int>(Q);
+    p.cS = S; p.csh = sh; p.csw = sw; p.cph = ph; p.cpw = pw;
+    if (dtype == QSYNC_I8) {
+        QSB_REQUIRE(scale_a && scale_b, QSYNC_ERR_VALIDATION, "the dequant epilogue needs scale_a and scale_b");
+        p.scale_a = scale_a;
+        p.scale_b = scale_b;
+        p.b_per_channel = b_per_channel;
+        return dispatch<true>(x, w, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, to_stream(stream), g_force_bn, 4);
+    }
+    const CUtensorMapDataType dt =
+        dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    return dispatch<false>(x, w, dt, p, to_stream(stream), g_force_bn, 4);
 }
 
 int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,

@@ -288,6 +288,32 @@ def im2col(x: torch.Tensor, R: int, S: int, stride, pad, dil=(1, 1), ld: int | N
     return out, (P, Q)
 
 
+def implicit_conv_ok(C: int, dtype: torch.dtype) -> bool:
+    """Whether the implicit-GEMM forward applies: each (r,s) tap's channel run
+    must be a whole number of 128-byte K-slices."""
+    return (C * (1 if dtype == torch.int8 else 2)) % 128 == 0
+
+
+def conv_fwd_implicit(x: torch.Tensor, w2: torch.Tensor, R: int, S: int, stride, pad, scale_a=None,
+                      scale_b=None, bias=None, out_dtype=torch.float32, b_per_channel: bool = True):
+    """Implicit-GEMM Conv2d forward: x NHWC (int8 / fp16), w2 [Cout, R*S*C] (KRSC
+    flattened) -> y [N*P*Q, Cout].  The column matrix is gathered tile by tile by
+    the GEMM's producer warp, never materialised."""
+    _req(x, "x", (torch.int8, torch.float16, torch.bfloat16))
+    _req(w2, "w2", (x.dtype,))
+    N, H, W, C = x.shape
+    P, Q = conv_out_size(H, W, R, S, stride, pad)
+    cout = w2.shape[0]
+    y = torch.empty((N * P * Q, cout), device=x.device, dtype=out_dtype)
+    ev = _timed("gemm_s8" if x.dtype == torch.int8 else "gemm_f16", 2.0 * N * P * Q * cout * R * S * C)
+    call("qsync_conv_fwd_implicit", _ptr(x), _DT_CAST[x.dtype], N, H, W, C, R, S, stride[0], stride[1],
+         pad[0], pad[1], _ptr(w2), cout, _ptr(y), _DT[out_dtype], _ptr(scale_a), _ptr(scale_b),
+         int(b_per_channel), _ptr(bias), _stream())
+    if ev is not None:
+        ev.record()
+    return y, (P, Q)
+
+
 def col2im(dcol: torch.Tensor, xshape, R: int, S: int, stride, pad, dil=(1, 1)) -> torch.Tensor:
     """Adjoint of im2col: dx NHWC FP32 from the column gradient (FP32 or FP16)."""
     _req(dcol, "dcol", (torch.float32, torch.float16))

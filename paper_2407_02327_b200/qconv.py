@@ -1,7 +1,11 @@
 """Quantized Conv2d (NHWC) -- the convolution kernel a QSync plan selects.
 
-Forward is a GEMM over the im2col column matrix A [N*P*Q, R*S*C] and the KRSC
-weight W [Cout, R*S*C] (below-16-bit convolutions are channels-last):
+Forward is a GEMM over the column matrix A [N*P*Q, R*S*C] and the KRSC weight
+W [Cout, R*S*C] (below-16-bit convolutions are channels-last).  When
+each (r,s) tap's channel run is a whole number of 128-byte K-slices (C % 128 INT8,
+C % 64 FP16: every ResNet-50 conv but conv1) A is never materialised: the GEMM's
+producer warp gathers it tile by tile from the NHWC input (implicit GEMM,
+`qsync_conv_fwd_implicit`); otherwise im2col builds it.
   * INT8 -- x quantized once per tensor (1 B/elem NHWC), im2col of the int8
             tensor, per-channel weight scales, tcgen05 kind::i8 GEMM with the fused
             dequant + bias epilogue -> FP32 NHWC output (graph.hpp:38-40).
@@ -42,15 +46,23 @@ class _QConv(torch.autograd.Function):
         if precision == INT8:
             xq, xs, _ = ops.quantize_per_tensor(x.reshape(1, -1))
             xq = xq.view(N, H, W, C)
-            A, (P, Q) = ops.im2col(xq, R, S, stride, pad, ld=kp)
             wq, ws, _ = ops.quantize_per_channel(w2)
-            _, y = ops.gemm_s8(A, wq, xs, ws, b)
+            if ops.implicit_conv_ok(C, torch.int8):
+                # implicit GEMM: the producer warp gathers the column tiles from xq
+                y, (P, Q) = ops.conv_fwd_implicit(xq, wq, R, S, stride, pad, xs, ws, b)
+            else:
+                A, (P, Q) = ops.im2col(xq, R, S, stride, pad, ld=kp)
+                _, y = ops.gemm_s8(A, wq, xs, ws, b)
             ctx.save_for_backward(xq, xs)
         else:
             x16 = x if x.dtype == torch.float16 else ops.cast(x.contiguous(), torch.float16)
-            A, (P, Q) = ops.im2col(x16, R, S, stride, pad, ld=kp)
             w16 = ops.cast(w2, torch.float16)
-            y = ops.gemm_f16(A, w16, out_dtype=torch.float16, bias=b)
+            if ops.implicit_conv_ok(C, torch.float16):
+                y, (P, Q) = ops.conv_fwd_implicit(x16, w16, R, S, stride, pad, bias=b,
+                                                  out_dtype=torch.float16)
+            else:
+                A, (P, Q) = ops.im2col(x16, R, S, stride, pad, ld=kp)
+                y = ops.gemm_f16(A, w16, out_dtype=torch.float16, bias=b)
             ctx.save_for_backward(x16, torch.ones(1, device=x.device))
         ctx.geom, ctx.precision, ctx.kp = geom, precision, kp
         ctx.shapes = (N, H, W, C, cout, P, Q, K)

@@ -9,6 +9,8 @@ from paper_2407_02327_b200 import ops
 from paper_2407_02327_b200.qconv import qconv2d
 from paper_2407_02327_b200.qlinear import FP16, INT8
 
+DEV = "cuda"
+
 pytestmark = pytest.mark.gpu
 
 # (N, H, W, C, Cout, R, stride, pad): stem 7x7/2, res2 3x3, res3 1x1/2 downsample, res5 3x3
@@ -103,3 +105,44 @@ def test_fp16_conv_vs_torch_fp32(case):
     assert _rel(dx, xt.grad.permute(0, 2, 3, 1).cpu().numpy()) < 1e-2
     assert _rel(dw, wt.grad.permute(0, 2, 3, 1).cpu().numpy()) < 1e-2
     assert _rel(db, bt.grad.cpu().numpy()) < 1e-3
+
+
+@pytest.mark.parametrize("geom", [(2, 14, 14, 128, 256, 3, 1, 1), (2, 15, 15, 128, 128, 3, 2, 1),
+                                  (3, 7, 7, 256, 512, 1, 1, 0), (1, 28, 28, 128, 64, 1, 2, 0),
+                                  (2, 9, 11, 128, 200, 3, 1, 1)])
+def test_implicit_conv_int8_bit_exact_vs_im2col(geom):
+    """Implicit-GEMM forward (A gathered by the producer warp) == im2col + GEMM:
+    same int8 operands, same K order -> identical int32 accumulators and epilogue."""
+    N, H, W, C, Co, R, st, pd = geom
+    torch.manual_seed(sum(geom))
+    x = torch.randint(-127, 128, (N, H, W, C), dtype=torch.int8, device=DEV)
+    w2 = torch.randint(-127, 128, (Co, R * R * C), dtype=torch.int8, device=DEV)
+    sa = torch.tensor([0.0123], device=DEV)
+    sb = torch.rand(Co, device=DEV) * 0.01
+    bias = torch.randn(Co, device=DEV)
+    assert ops.implicit_conv_ok(C, torch.int8)
+    y, (P, Q) = ops.conv_fwd_implicit(x, w2, R, R, (st, st), (pd, pd), sa, sb, bias)
+    A, (P2, Q2) = ops.im2col(x, R, R, (st, st), (pd, pd))
+    _, y_ref = ops.gemm_s8(A, w2, sa, sb, bias)
+    assert (P, Q) == (P2, Q2)
+    assert torch.equal(y, y_ref)
+
+
+@pytest.mark.parametrize("geom", [(2, 14, 14, 64, 256, 3, 1, 1), (2, 28, 28, 128, 128, 3, 2, 1),
+                                  (4, 7, 7, 64, 96, 1, 1, 0)])
+def test_implicit_conv_fp16_matches_im2col(geom):
+    N, H, W, C, Co, R, st, pd = geom
+    torch.manual_seed(sum(geom))
+    x = torch.randn(N, H, W, C, device=DEV).half()
+    w2 = (torch.randn(Co, R * R * C, device=DEV) / (R * R * C) ** 0.5).half()
+    y, _ = ops.conv_fwd_implicit(x, w2, R, R, (st, st), (pd, pd), out_dtype=torch.float16)
+    A, _ = ops.im2col(x, R, R, (st, st), (pd, pd))
+    y_ref = ops.gemm_f16(A, w2, out_dtype=torch.float16)
+    assert torch.equal(y, y_ref)  # same operands, same K order, same accumulation
+
+
+def test_implicit_conv_rejects_narrow_channels():
+    x = torch.zeros(1, 8, 8, 3, dtype=torch.int8, device=DEV)
+    w2 = torch.zeros(16, 27, dtype=torch.int8, device=DEV)
+    with pytest.raises(Exception, match="128 bytes"):
+        ops.conv_fwd_implicit(x, w2, 3, 3, (1, 1), (1, 1), torch.ones(1, device=DEV), torch.ones(16, device=DEV))
