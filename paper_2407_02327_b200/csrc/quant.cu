@@ -16,6 +16,13 @@ namespace {
 
 constexpr int kThreads = 512;
 
+template <int DT>
+__device__ __forceinline__ float round_to(float g) {
+    if constexpr (DT == QSYNC_F16) return __half2float(__float2half_rn(g));
+    if constexpr (DT == QSYNC_BF16) return __bfloat162float(__float2bfloat16_rn(g));
+    return g;
+}
+
 // Fused prologue activation of the streaming kernels: ACT 0 = identity,
 // ACT 1 = GELU (the FF1 -> FF2 activation of an encoder layer, so the
 // quantizer / cast of the FF2 input reads the pre-activation directly).
@@ -136,15 +143,25 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                 V::unpack(r[u], f);
 #pragma unroll
                 for (int j = 0; j < V::N; j += 4) {
-                    uint32_t b0 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j]), s));
-                    uint32_t b1 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j + 1]), s));
-                    uint32_t b2 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j + 2]), s));
-                    uint32_t b3 = static_cast<uint8_t>(quant_rne(act_f<ACT, DT>(f[j + 3]), s));
-                    packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
-                    if (ACT == 1) {
-                        dp[(u * V::N + j) / 2] = pack_half2(gelu_erf_grad(f[j]), gelu_erf_grad(f[j + 1]));
-                        dp[(u * V::N + j) / 2 + 1] = pack_half2(gelu_erf_grad(f[j + 2]), gelu_erf_grad(f[j + 3]));
+                    float a[4];
+                    if (ACT == 1 && dact) {  // GELU and GELU' share the erf
+                        float d[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            gelu_and_grad(f[j + e], a[e], d[e]);
+                            a[e] = round_to<DT>(a[e]);
+                        }
+                        dp[(u * V::N + j) / 2] = pack_half2(d[0], d[1]);
+                        dp[(u * V::N + j) / 2 + 1] = pack_half2(d[2], d[3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) a[e] = act_f<ACT, DT>(f[j + e]);
                     }
+                    uint32_t b0 = static_cast<uint8_t>(quant_rne(a[0], s));
+                    uint32_t b1 = static_cast<uint8_t>(quant_rne(a[1], s));
+                    uint32_t b2 = static_cast<uint8_t>(quant_rne(a[2], s));
+                    uint32_t b3 = static_cast<uint8_t>(quant_rne(a[3], s));
+                    packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
                 }
             }
             qv[i] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
@@ -505,20 +522,27 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
             float f0[8], f1[8];
             load8<SD>(x, i * 8, f0);
             load8<SD>(x, (i + stride) * 8, f1);
-            if (ACT == 1 && dact) {
-                uint32_t d0[4], d1[4];
+            if (ACT == 1 && dact) {  // GELU and GELU' share the erf
+                float d0[8], d1[8];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    d0[j] = pack_half2(gelu_erf_grad(f0[2 * j]), gelu_erf_grad(f0[2 * j + 1]));
-                    d1[j] = pack_half2(gelu_erf_grad(f1[2 * j]), gelu_erf_grad(f1[2 * j + 1]));
+                for (int j = 0; j < 8; ++j) {
+                    gelu_and_grad(f0[j], f0[j], d0[j]);
+                    gelu_and_grad(f1[j], f1[j], d1[j]);
+                    f0[j] = round_to<SD>(f0[j]);
+                    f1[j] = round_to<SD>(f1[j]);
                 }
-                reinterpret_cast<uint4*>(dact)[i] = make_uint4(d0[0], d0[1], d0[2], d0[3]);
-                reinterpret_cast<uint4*>(dact)[i + stride] = make_uint4(d1[0], d1[1], d1[2], d1[3]);
-            }
+                reinterpret_cast<uint4*>(dact)[i] =
+                    make_uint4(pack_half2(d0[0], d0[1]), pack_half2(d0[2], d0[3]), pack_half2(d0[4], d0[5]),
+                               pack_half2(d0[6], d0[7]));
+                reinterpret_cast<uint4*>(dact)[i + stride] =
+                    make_uint4(pack_half2(d1[0], d1[1]), pack_half2(d1[2], d1[3]), pack_half2(d1[4], d1[5]),
+                               pack_half2(d1[6], d1[7]));
+            } else {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                f0[j] = act_f<ACT, SD>(f0[j]);
-                f1[j] = act_f<ACT, SD>(f1[j]);
+                for (int j = 0; j < 8; ++j) {
+                    f0[j] = act_f<ACT, SD>(f0[j]);
+                    f1[j] = act_f<ACT, SD>(f1[j]);
+                }
             }
             store8<DD>(out, i * 8, f0);
             store8<DD>(out, (i + stride) * 8, f1);
@@ -527,13 +551,19 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
             float f0[8];
             load8<SD>(x, i * 8, f0);
             if (ACT == 1 && dact) {
-                uint32_t d0[4];
+                float d0[8];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) d0[j] = pack_half2(gelu_erf_grad(f0[2 * j]), gelu_erf_grad(f0[2 * j + 1]));
-                reinterpret_cast<uint4*>(dact)[i] = make_uint4(d0[0], d0[1], d0[2], d0[3]);
+                for (int j = 0; j < 8; ++j) {
+                    gelu_and_grad(f0[j], f0[j], d0[j]);
+                    f0[j] = round_to<SD>(f0[j]);
+                }
+                reinterpret_cast<uint4*>(dact)[i] =
+                    make_uint4(pack_half2(d0[0], d0[1]), pack_half2(d0[2], d0[3]), pack_half2(d0[4], d0[5]),
+                               pack_half2(d0[6], d0[7]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f0[j] = act_f<ACT, SD>(f0[j]);
             }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) f0[j] = act_f<ACT, SD>(f0[j]);
             store8<DD>(out, i * 8, f0);
         }
         done = n8 * 8;
