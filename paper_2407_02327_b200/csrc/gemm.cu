@@ -530,7 +530,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
-        if (lane == 0) ptx::bulk_wait<0>();
+        // The staging smem must outlive the TMA reads only; the global writes complete
+        // with the grid (the next kernel sees them after its griddepcontrol.wait).
+        if (lane == 0) ptx::bulk_wait_read<0>();
     }
 
     ptx::tc_fence_before();
