@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_act_bwd_colsum(const void* __re
                                                                 void* __restrict__ out,
                                                                 float* __restrict__ colsum,
                                                                 int vec_ok) {
+    QSB_PDL_ENTER();
     __shared__ float red[kWarps][kCols];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -134,7 +135,7 @@ int launch_act_bwd(const void* dy, const void* h, int64_t rows, int64_t cols, vo
                    float* colsum, cudaStream_t st) {
     const int vec = (cols % 8 == 0) && aligned16(dy) && (!h || aligned16(h)) && (!out || aligned16(out));
     dim3 grid(static_cast<unsigned>((cols + kCols - 1) / kCols), static_cast<unsigned>((rows + kRows - 1) / kRows));
-    k_act_bwd_colsum<DDY, DH, DO, ACT><<<grid, kWarps * 32, 0, st>>>(dy, h, rows, cols, out, colsum, vec);
+    pdl_launch(k_act_bwd_colsum<DDY, DH, DO, ACT>, dim3(grid), dim3(kWarps * 32), 0, st, dy, h, rows, cols, out, colsum, vec);
     return check_launch("k_act_bwd_colsum");
 }
 

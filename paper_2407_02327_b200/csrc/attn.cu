@@ -98,6 +98,7 @@ __device__ __forceinline__ uint32_t pk(float a, float b) { return pack_half2(a, 
 __global__ void __launch_bounds__(kThreadsA) k_attn_fwd(const __half* __restrict__ qkv, int H, float scale,
                                                         __half* __restrict__ out, float* __restrict__ lse,
                                                         unsigned* __restrict__ out_absmax) {
+    QSB_PDL_ENTER();
     extern __shared__ __align__(128) uint8_t sm[];
     const int bh = blockIdx.x;
     const int b = bh / H, h = bh % H;
@@ -218,6 +219,7 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_attn_bwd(const __half* __restr
                                                         const __half* __restrict__ dout,
                                                         const float* __restrict__ lse, int H, float scale,
                                                         __half* __restrict__ dqkv) {
+    QSB_PDL_ENTER();
     extern __shared__ __align__(128) uint8_t sm[];
     const int bh = blockIdx.x;
     const int b = bh / H, h = bh % H;
@@ -402,7 +404,7 @@ int qsync_attention_fwd(const void* qkv, int64_t B, int64_t S, int64_t H, int64_
         configured = true;
     }
     if (out_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(out_absmax, 0, sizeof(float), st), "memset"));
-    k_attn_fwd<<<static_cast<unsigned>(B * H), kThreadsA, kFwdSmem, st>>>(
+    pdl_launch(k_attn_fwd, dim3(static_cast<unsigned>(B * H)), dim3(kThreadsA), kFwdSmem, st, 
         static_cast<const __half*>(qkv), static_cast<int>(H), scale, static_cast<__half*>(out), lse,
         reinterpret_cast<unsigned*>(out_absmax));
     return check_launch("k_attn_fwd");
@@ -419,7 +421,7 @@ int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, cons
                             "cudaFuncSetAttribute"));
         configured = true;
     }
-    k_attn_bwd<<<static_cast<unsigned>(B * H), kThreadsA, kBwdSmem, st>>>(
+    pdl_launch(k_attn_bwd, dim3(static_cast<unsigned>(B * H)), dim3(kThreadsA), kBwdSmem, st, 
         static_cast<const __half*>(qkv), static_cast<const __half*>(out), static_cast<const __half*>(dout), lse,
         static_cast<int>(H), scale, static_cast<__half*>(dqkv));
     return check_launch("k_attn_bwd");

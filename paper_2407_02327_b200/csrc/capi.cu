@@ -46,6 +46,7 @@ int set_error(int status, const std::string& msg) {
 }
 
 static std::atomic<unsigned long long> g_launches{0};
+int g_pdl_enabled = 1;
 
 int check_launch(const char* what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);

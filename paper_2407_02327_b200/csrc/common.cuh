@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "qsync_b200.h"
 
@@ -37,6 +38,55 @@ inline int cuda_status(cudaError_t e, const char* what) {
 inline cudaStream_t to_stream(qsync_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Every kernel of this library starts with QSB_PDL_ENTER(): it waits for the
+// preceding grid in the stream to complete (griddepcontrol.wait -- a no-op when
+// not launched with PDL) and immediately allows the next grid to be scheduled,
+// so inside a CUDA graph a kernel's launch and prologue overlap the previous
+// kernel's tail.  launch_pdl() launches with the programmatic-serialization
+// attribute (qsync_gemm_set_pdl turns it off for A/B runs).
+extern int g_pdl_enabled;
+#define QSB_PDL_ENTER()                                              \
+    do {                                                             \
+        asm volatile("griddepcontrol.wait;" ::: "memory");           \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    } while (0)
+
+// Launch with PDL; the caller's check_launch() reports errors (as for <<<>>>).
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl_enabled ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+               Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl_enabled ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e != cudaSuccess) return cuda_status(e, what);
+    return check_launch(what);
+}
 
 // ---- typed loads ----------------------------------------------------------
 template <int DT>

@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // allocation, descriptor prefetch) may overlap the previous kernel's tail;
     // no global memory is touched before the previous grid has completed.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // Leader-CTA addresses of the barriers the pair shares.
     const uint32_t full_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
     const uint32_t tempty_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
@@ -823,6 +824,7 @@ int qsync_gemm_set_max_ctas(int n) {
 
 int qsync_gemm_set_pdl(int on) {
     g_pdl = on ? 1 : 0;
+    g_pdl_enabled = g_pdl;
     return QSYNC_OK;
 }
 

@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
                                                 const float* __restrict__ pos = nullptr,
                                                 const float* __restrict__ typ = nullptr,
                                                 int seq = 1) {
+    QSB_PDL_ENTER();
     const int lane = threadIdx.x & 31;
     float amax = 0.0f;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
                                                 float* __restrict__ dbeta,
                                                 __half* __restrict__ dx16,
                                                 float* __restrict__ dcol) {
+    QSB_PDL_ENTER();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(256, 2) k_ln_bwd2(const float* __restrict__ dy
                                                     float* __restrict__ dword = nullptr,
                                                     float* __restrict__ dpos = nullptr,
                                                     int seq = 1) {
+    QSB_PDL_ENTER();
     constexpr int NH = NV / 2;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -335,15 +338,17 @@ int ln_fwd_nv(const float* a, const void* b, int b_dtype, const float* gamma, co
     if (y_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(y_absmax, 0, sizeof(float), st), "memset"));
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 8LL));
     if (b_dtype == QSYNC_F16)
-        k_ln_fwd<NV, QSYNC_F16><<<grid, 256, 0, st>>>(a, static_cast<const __half*>(b), gamma, beta,
+        pdl_launch(k_ln_fwd<NV, QSYNC_F16>, dim3(grid), dim3(256), 0, st, a, static_cast<const __half*>(b), gamma, beta,
                                                       rows, cols, eps, s_out, y, mean, rstd,
                                                       reinterpret_cast<__half*>(y16),
-                                                      reinterpret_cast<unsigned*>(y_absmax));
+                                                      reinterpret_cast<unsigned*>(y_absmax), nullptr, nullptr,
+                                                      nullptr, 1);
     else
-        k_ln_fwd<NV, QSYNC_F32><<<grid, 256, 0, st>>>(a, static_cast<const float*>(b), gamma, beta,
+        pdl_launch(k_ln_fwd<NV, QSYNC_F32>, dim3(grid), dim3(256), 0, st, a, static_cast<const float*>(b), gamma, beta,
                                                       rows, cols, eps, s_out, y, mean, rstd,
                                                       reinterpret_cast<__half*>(y16),
-                                                      reinterpret_cast<unsigned*>(y_absmax));
+                                                      reinterpret_cast<unsigned*>(y_absmax), nullptr, nullptr,
+                                                      nullptr, 1);
     return check_launch("k_ln_fwd");
 }
 
@@ -353,12 +358,12 @@ int ln_bwd_nv(const float* dy, const float* s, const float* mean, const float* r
               uint16_t* dx16, float* dcol, cudaStream_t st) {
     if constexpr (NV % 2 == 0) {
         const int grid = static_cast<int>(std::min<int64_t>((rows + 3) / 4, sm_count() * 4LL));
-        k_ln_bwd2<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
-                                             reinterpret_cast<__half*>(dx16), dcol);
+        pdl_launch(k_ln_bwd2<NV>, dim3(grid), dim3(256), 0, st, dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
+                                             reinterpret_cast<__half*>(dx16), dcol, nullptr, nullptr, nullptr, 1);
         return check_launch("k_ln_bwd");
     }
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 2LL));
-    k_ln_bwd<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
+    pdl_launch(k_ln_bwd<NV>, dim3(grid), dim3(256), 0, st, dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
                                         reinterpret_cast<__half*>(dx16), dcol);
     return check_launch("k_ln_bwd");
 }
@@ -369,7 +374,7 @@ int embed_ln_fwd_nv(const int64_t* tok, int64_t rows, int seq, const float* word
                     float* y, float* mean, float* rstd, uint16_t* y16, float* y_absmax, cudaStream_t st) {
     if (y_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(y_absmax, 0, sizeof(float), st), "memset"));
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 8LL));
-    k_ln_fwd<NV, QSYNC_F32><<<grid, 256, 0, st>>>(word, nullptr, gamma, beta, rows, cols, eps, s_out, y, mean,
+    pdl_launch(k_ln_fwd<NV, QSYNC_F32>, dim3(grid), dim3(256), 0, st, word, static_cast<const float*>(nullptr), gamma, beta, rows, cols, eps, s_out, y, mean,
                                                   rstd, reinterpret_cast<__half*>(y16),
                                                   reinterpret_cast<unsigned*>(y_absmax), tok, pos, typ, seq);
     return check_launch("k_ln_fwd<embed>");
@@ -380,8 +385,8 @@ int embed_ln_bwd_nv(const float* dy, const float* s, const float* mean, const fl
                     const int64_t* tok, int64_t rows, int seq, int cols, float* dgamma, float* dbeta,
                     float* dword, float* dpos, float* dtyp, cudaStream_t st) {
     const int grid = static_cast<int>(std::min<int64_t>((rows + 3) / 4, sm_count() * 4LL));
-    k_ln_bwd2<NV><<<grid, 256, 0, st>>>(dy, s, mean, rstd, gamma, rows, cols, nullptr, dgamma, dbeta, nullptr,
-                                         dtyp, tok, dword, dpos, seq);
+    pdl_launch(k_ln_bwd2<NV>, dim3(grid), dim3(256), 0, st, dy, s, mean, rstd, gamma, rows, cols, static_cast<float*>(nullptr), dgamma, dbeta,
+                                         static_cast<__half*>(nullptr), dtyp, tok, dword, dpos, seq);
     return check_launch("k_ln_bwd<embed>");
 }
 

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
                                                        int64_t total_rows, const int64_t* __restrict__ step,
                                                        float lr, float b1, float b2, float eps, float wd,
                                                        int update) {
+    QSB_PDL_ENTER();
     const int lane = threadIdx.x & 31;
     AdamCoef c{};
     if (update) {
@@ -187,7 +188,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
     }
 }
 
-__global__ void k_step_inc(int64_t* step) { *step += 1; }
+__global__ void k_step_inc(int64_t* step) {
+    QSB_PDL_ENTER(); *step += 1; }
 
 }  // namespace
 }  // namespace qsb
@@ -210,14 +212,14 @@ int qsync_adamw_step_range(const qsync_adamw_seg* segs, int nseg, const int64_t*
         static_cast<int>(std::min<int64_t>((row_end - row_begin + kWarps - 1) / kWarps, sm_count() * 16LL));
     const size_t smem = sizeof(int64_t) * (static_cast<size_t>(nseg) + 1);
     QSB_REQUIRE(smem <= 48 * 1024, QSYNC_ERR_DOMAIN, "too many parameter segments");
-    k_adamw<<<grid, kWarps * 32, smem, st>>>(segs, nseg, seg_row_start, row_begin, row_end, step, lr, beta1,
+    pdl_launch(k_adamw, dim3(grid), dim3(kWarps * 32), smem, st, segs, nseg, seg_row_start, row_begin, row_end, step, lr, beta1,
                                              beta2, eps, weight_decay, update);
     return check_launch("k_adamw");
 }
 
 int qsync_adamw_advance(int64_t* step, qsync_stream_t stream) {
     QSB_REQUIRE(step != nullptr, QSYNC_ERR_VALIDATION, "step counter is required");
-    k_step_inc<<<1, 1, 0, to_stream(stream)>>>(step);
+    pdl_launch(k_step_inc, dim3(1), dim3(1), 0, to_stream(stream), step);
     return check_launch("k_step_inc");
 }
 

@@ -50,6 +50,7 @@ template <int DT, int ACT = 0>
 __global__ void __launch_bounds__(kThreads) k_absmax(const typename Elem<DT>::T* __restrict__ x,
                                                      int64_t n, unsigned* __restrict__ out,
                                                      int vec_ok) {
+    QSB_PDL_ENTER();
     using V = Vec<DT>;
     constexpr int U = 4;
     float m = 0.0f;
@@ -98,6 +99,7 @@ template <int DT>
 __global__ void __launch_bounds__(256) k_absmax_rows(const typename Elem<DT>::T* __restrict__ x,
                                                      int64_t rows, int64_t cols,
                                                      float* __restrict__ out) {
+    QSB_PDL_ENTER();
     const int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                                                        int8_t* __restrict__ q,
                                                        float* __restrict__ scale_out, int vec_ok,
                                                        uint16_t* __restrict__ dact = nullptr) {
+    QSB_PDL_ENTER();
     using V = Vec<DT>;
     constexpr int LOADS = 16 / V::N;
     const float s = scale_in ? *scale_in : scale_from_absmax(*absmax_in);
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __rest
                                               float* __restrict__ colsum,
                                               float* __restrict__ scale_out, int vec_ok,
                                               int8_t* __restrict__ out_t8 = nullptr) {
+    QSB_PDL_ENTER();
     __shared__ __align__(16) __half tile[TC][TR + 8];  // [col][row], 16B-aligned rows
     __shared__ float csum[16][TC + 1];
     const int tid = threadIdx.x;
@@ -360,6 +364,7 @@ __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __rest
 __global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w, int64_t rows,
                                                     int64_t cols, int8_t* __restrict__ q,
                                                     float* __restrict__ scales) {
+    QSB_PDL_ENTER();
     const int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
@@ -400,6 +405,7 @@ __global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w,
 __global__ void __launch_bounds__(kThreads) k_dequant(const int8_t* __restrict__ q, int64_t n,
                                                       const float* __restrict__ scale,
                                                       float* __restrict__ out, int vec_ok) {
+    QSB_PDL_ENTER();
     // Thread i owns output float4 i (4 int8 in, 16 B out): every store
     // instruction writes 512 contiguous bytes per warp, so no partial sectors
     // are written (partial-sector writes made L2 fetch lines from DRAM).
@@ -444,6 +450,7 @@ __global__ void __launch_bounds__(kThreads) k_dequant(const int8_t* __restrict__
 __global__ void __launch_bounds__(256) k_dequant_rows(const int8_t* __restrict__ q, int64_t rows,
                                                       int64_t cols, const float* __restrict__ scales,
                                                       float* __restrict__ out) {
+    QSB_PDL_ENTER();
     const int64_t row = blockIdx.y;
     const float s = scales[row];
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols;
@@ -512,6 +519,7 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
                                                    typename Store<SD, DD>::T* __restrict__ out,
                                                    int64_t n, int vec_ok,
                                                    uint16_t* __restrict__ dact = nullptr) {
+    QSB_PDL_ENTER();
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t done = 0;
@@ -585,6 +593,7 @@ template <int DT>
 __global__ void __launch_bounds__(kThreads) k_stats_partial(const typename Elem<DT>::T* __restrict__ x,
                                                             int64_t n, double* __restrict__ part,
                                                             int vec_ok) {
+    QSB_PDL_ENTER();
     using V = Vec<DT>;
     double ss = 0.0;
     float m = 0.0f;
@@ -632,6 +641,7 @@ __global__ void __launch_bounds__(kThreads) k_stats_partial(const typename Elem<
 
 __global__ void __launch_bounds__(1024) k_stats_final(const double* __restrict__ part, int nparts,
                                                       int64_t n, double* __restrict__ out) {
+    QSB_PDL_ENTER();
     __shared__ double rs[32];
     __shared__ double rm[32];
     double ss = 0.0, m = 0.0;
@@ -680,7 +690,7 @@ struct AbsmaxRun {
         if (n == 0) return QSYNC_OK;
         const int vec = aligned16(x);
         const int grid = grid_for(n / Vec<DT>::N + 1, kThreads * 4);
-        k_absmax<DT><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n,
+        pdl_launch(k_absmax<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n,
                                                 reinterpret_cast<unsigned*>(absmax), vec);
         return check_launch("k_absmax");
     }
@@ -691,7 +701,7 @@ struct AbsmaxRowsRun {
     static int run(const void* x, int64_t rows, int64_t cols, float* out, cudaStream_t st) {
         using T = typename Elem<DT>::T;
         if (rows == 0) return QSYNC_OK;
-        k_absmax_rows<DT><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
+        pdl_launch(k_absmax_rows<DT>, dim3(static_cast<unsigned>((rows + 7) / 8)), dim3(256), 0, st, 
             static_cast<const T*>(x), rows, cols, out);
         return check_launch("k_absmax_rows");
     }
@@ -709,7 +719,7 @@ struct QuantRun {
             dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
             const int vt = (cols % 4 == 0) && aligned16(x) && aligned16(q) && aligned16(q_t);
             const bool t8 = q_t_dtype == QSYNC_I8;
-            k_tile<DT, 0><<<grid, 256, 0, st>>>(static_cast<const T*>(x), rows, cols, scale + 1, q,
+            pdl_launch(k_tile<DT, 0>, dim3(grid), dim3(256), 0, st, static_cast<const T*>(x), rows, cols, scale + 1, q,
                                                 nullptr, t8 ? nullptr : static_cast<uint16_t*>(q_t),
                                                 ld_t, nullptr, scale, vt,
                                                 t8 ? static_cast<int8_t*>(q_t) : nullptr);
@@ -717,8 +727,8 @@ struct QuantRun {
         }
         const int vec = aligned16(x) && aligned16(q);
         const int grid = grid_for(n / 16 + 1, kThreads, 4);
-        k_quantize<DT><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, scale + 1, nullptr,
-                                                  q, scale, vec);
+        pdl_launch(k_quantize<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, scale + 1, nullptr,
+                                                  q, scale, vec, static_cast<uint16_t*>(nullptr));
         return check_launch("k_quantize");
     }
 };
@@ -730,8 +740,8 @@ struct QuantScaleRun {
         if (n == 0) return QSYNC_OK;
         const int vec = aligned16(x) && aligned16(q);
         const int grid = grid_for(n / 16 + 1, kThreads, 4);
-        k_quantize<DT><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, nullptr, scale, q,
-                                                  nullptr, vec);
+        pdl_launch(k_quantize<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, nullptr, scale, q,
+                                                  nullptr, vec, static_cast<uint16_t*>(nullptr));
         return check_launch("k_quantize");
     }
 };
@@ -746,8 +756,8 @@ struct CastTRun {
         if (rows == 0 || cols == 0) return QSYNC_OK;
         dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
         const int vt = (cols % 4 == 0) && aligned16(x) && aligned16(out) && aligned16(out_t);
-        k_tile<DT, 1><<<grid, 256, 0, st>>>(static_cast<const T*>(x), rows, cols, nullptr, nullptr,
-                                            out, out_t, ld_t, colsum, nullptr, vt);
+        pdl_launch(k_tile<DT, 1>, dim3(grid), dim3(256), 0, st, static_cast<const T*>(x), rows, cols, nullptr, nullptr,
+                                            out, out_t, ld_t, colsum, nullptr, vt, static_cast<int8_t*>(nullptr));
         return check_launch("k_tile<cast>");
     }
 };
@@ -760,9 +770,9 @@ struct StatsRun {
         int grid = grid_for(n / Vec<DT>::N + 1, kThreads * 2, 4);
         grid = std::min(grid, kStatsBlocks);
         double* part = static_cast<double*>(ws);
-        k_stats_partial<DT><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, part, vec);
+        pdl_launch(k_stats_partial<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, part, vec);
         QSB_TRY(check_launch("k_stats_partial"));
-        k_stats_final<<<1, 1024, 0, st>>>(part, grid, n, out);
+        pdl_launch(k_stats_final, dim3(1), dim3(1024), 0, st, part, grid, n, out);
         return check_launch("k_stats_final");
     }
 };
@@ -776,10 +786,10 @@ struct AbsmaxActRun {
         const int vec = aligned16(x);
         const int grid = grid_for(n / Vec<DT>::N + 1, kThreads * 4);
         if (act == 1)
-            k_absmax<DT, 1><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n,
+            pdl_launch(k_absmax<DT, 1>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n,
                                                        reinterpret_cast<unsigned*>(absmax), vec);
         else
-            k_absmax<DT, 0><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n,
+            pdl_launch(k_absmax<DT, 0>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n,
                                                        reinterpret_cast<unsigned*>(absmax), vec);
         return check_launch("k_absmax");
     }
@@ -794,11 +804,11 @@ struct QuantActRun {
         const int vec = aligned16(x) && aligned16(q) && (!dact || aligned16(dact));
         const int grid = grid_for(n / 16 + 1, kThreads, 4);
         if (act == 1)
-            k_quantize<DT, 1><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, absmax, nullptr,
+            pdl_launch(k_quantize<DT, 1>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, absmax, nullptr,
                                                          q, scale_out, vec, dact);
         else
-            k_quantize<DT, 0><<<grid, kThreads, 0, st>>>(static_cast<const T*>(x), n, absmax, nullptr,
-                                                         q, scale_out, vec);
+            pdl_launch(k_quantize<DT, 0>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, absmax, nullptr,
+                                                         q, scale_out, vec, static_cast<uint16_t*>(nullptr));
         return check_launch("k_quantize");
     }
 };
@@ -846,7 +856,7 @@ int qsync_quantize_per_channel(const float* w, int64_t rows, int64_t cols, int8_
     QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
     cudaStream_t st = to_stream(stream);
     if (rows == 0) return QSYNC_OK;
-    k_quant_rows<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(w, rows, cols, q, scales);
+    pdl_launch(k_quant_rows, dim3(static_cast<unsigned>((rows + 7) / 8)), dim3(256), 0, st, w, rows, cols, q, scales);
     QSB_TRY(check_launch("k_quant_rows"));
     if (w_t_f16) return CastTRun<QSYNC_F32>::run(w, rows, cols, nullptr, w_t_f16, rows, nullptr, 0, st);
     return QSYNC_OK;
@@ -858,7 +868,7 @@ int qsync_dequantize_per_tensor(const int8_t* q, int64_t n, const float* scale, 
     if (n == 0) return QSYNC_OK;
     cudaStream_t st = to_stream(stream);
     const int vec = aligned16(q) && aligned16(out);
-    k_dequant<<<grid_for(n / 16 + 1, kThreads, 4), kThreads, 0, st>>>(q, n, scale, out, vec);
+    pdl_launch(k_dequant, dim3(grid_for(n / 16 + 1, kThreads, 4)), dim3(kThreads), 0, st, q, n, scale, out, vec);
     return check_launch("k_dequant");
 }
 
@@ -868,7 +878,7 @@ int qsync_dequantize_per_channel(const int8_t* q, int64_t rows, int64_t cols, co
     QSB_REQUIRE(rows < 65536, QSYNC_ERR_DOMAIN, "per-channel dequantize supports < 65536 rows");
     if (rows == 0 || cols == 0) return QSYNC_OK;
     dim3 grid(static_cast<unsigned>(std::min<int64_t>((cols + 255) / 256, 64)), static_cast<unsigned>(rows));
-    k_dequant_rows<<<grid, 256, 0, to_stream(stream)>>>(q, rows, cols, scales, out);
+    pdl_launch(k_dequant_rows, dim3(grid), dim3(256), 0, to_stream(stream), q, rows, cols, scales, out);
     return check_launch("k_dequant_rows");
 }
 
@@ -880,8 +890,8 @@ int qsync_cast(const void* x, int src, void* out, int dst, int64_t n, qsync_stre
     const int vec = aligned16(x) && aligned16(out);
 #define QSB_CAST(S, D)                                                                     \
     if (src == S && dst == D) {                                                            \
-        k_cast<S, D><<<grid, kThreads, 0, st>>>(static_cast<const typename Elem<S>::T*>(x), \
-                                                static_cast<typename Store<S, D>::T*>(out), n, vec); \
+        pdl_launch(k_cast<S, D>, dim3(grid), dim3(kThreads), 0, st, static_cast<const typename Elem<S>::T*>(x), \
+                                                static_cast<typename Store<S, D>::T*>(out), n, vec, static_cast<uint16_t*>(nullptr)); \
         return check_launch("k_cast");                                                     \
     }
     QSB_CAST(QSYNC_F32, QSYNC_F16)
@@ -942,7 +952,7 @@ int qsync_act_cast(const void* x, int src, void* out, int dst, int64_t n, int ac
     const int vec = aligned16(x) && aligned16(out) && (!dact_out || aligned16(dact_out));
 #define QSB_ACAST(S, D)                                                                       \
     if (src == S && dst == D) {                                                               \
-        k_cast<S, D, 1><<<grid, kThreads, 0, st>>>(static_cast<const typename Elem<S>::T*>(x), \
+        pdl_launch(k_cast<S, D, 1>, dim3(grid), dim3(kThreads), 0, st, static_cast<const typename Elem<S>::T*>(x), \
                                                    static_cast<typename Store<S, D>::T*>(out), n, vec, dact_out); \
         return check_launch("k_cast<gelu>");                                                  \
     }
