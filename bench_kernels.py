@@ -96,6 +96,22 @@ def gemm_bench(results: dict) -> None:
             rows.append({"kind": "i8", "M": M, "N": N, "K": K, "bn": bn, "ms": t,
                          "tops": 2.0 * M * N * K / (t * 1e-3) / 1e12})
         ops.force_tile_n(0)
+        # FP8 rung (E4M3, kind::f8f6f4) beside cuBLASLt FP8 (torch._scaled_mm)
+        if K % 16 == 0 and M >= 128:
+            a8, s8a = ops.quantize_fp8(torch.randn((M, K), device="cuda"))
+            b8, s8b = ops.quantize_fp8_rows(torch.randn((N, K), device="cuda"))
+            out8 = torch.empty((M, N), device="cuda")
+            t = time_ms(lambda: ops.gemm_f8(a8, b8, s8a, s8b, out=out8))
+            rows.append({"kind": "f8", "M": M, "N": N, "K": K, "bn": 0, "ms": t,
+                         "tops": 2.0 * M * N * K / (t * 1e-3) / 1e12})
+            try:
+                one = torch.ones((), device="cuda")
+                t = time_ms(lambda: torch._scaled_mm(a8, b8.t(), scale_a=one, scale_b=one,
+                                                     out_dtype=torch.float32))
+                rows.append({"kind": "cublaslt_f8", "M": M, "N": N, "K": K, "ms": t,
+                             "tops": 2.0 * M * N * K / (t * 1e-3) / 1e12})
+            except Exception as e:  # noqa: BLE001
+                print(f"cuBLASLt FP8 unavailable: {e}")
         ah = torch.randn((M, K), device="cuda").half()
         bh = torch.randn((N, K), device="cuda").half()
         outf = torch.empty((M, N), device="cuda")
@@ -111,7 +127,7 @@ def gemm_bench(results: dict) -> None:
                          "tops": 2.0 * M * N * K / (t * 1e-3) / 1e12})
     results["gemm"] = rows
     for r in rows:
-        frac = r["tops"] / (i8_peak if "i8" in r["kind"] else pk["bf16_tflops"])
+        frac = r["tops"] / (i8_peak if ("i8" in r["kind"] or "f8" in r["kind"]) else pk["bf16_tflops"])
         print(f"{r['kind']:12s} {r['M']:5d}x{r['N']:5d}x{r['K']:5d} bn={r.get('bn', '-')!s:4s}"
               f" {r['ms']*1e3:9.1f} us {r['tops']:8.1f} TOPS  frac={frac:.3f}")
     print(f"int8 peak (cuBLASLt 8192^3 best of 10): {i8_peak:.1f} TOPS")

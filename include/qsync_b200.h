@@ -50,7 +50,7 @@ enum qsync_status {
 };
 
 /* Element types for the typed entries. */
-enum qsync_dtype { QSYNC_F32 = 0, QSYNC_F16 = 1, QSYNC_BF16 = 2, QSYNC_I8 = 3, QSYNC_I32 = 4 };
+enum qsync_dtype { QSYNC_F32 = 0, QSYNC_F16 = 1, QSYNC_BF16 = 2, QSYNC_I8 = 3, QSYNC_I32 = 4, QSYNC_F8E4M3 = 5 };
 
 /* "<kind>: message" of the last failure on this host thread (errors.hpp:33). */
 const char* qsync_last_error(void);
@@ -128,7 +128,8 @@ int qsync_dequantize_per_channel(const int8_t* q, int64_t rows, int64_t cols, co
 
 /* ---------------------------------------------------------------------------
  * K4  float casts (CastScheme::FloatToFloat, profile.hpp:19).  RNE.  Also
- * I8 -> F16/F32 (exact): the FP16 backward's view of a saved INT8 activation.
+ * I8 / F8E4M3 -> F16/F32 (exact): the FP16 backward's view of a saved INT8 / FP8
+ * activation.
  * ------------------------------------------------------------------------- */
 int qsync_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64_t n,
                qsync_stream_t stream);
@@ -167,6 +168,21 @@ int qsync_tensor_stats(const void* x, int dtype, int64_t n, double* out, void* w
 int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k,
                   int32_t* c_i32, float* c_f32, const float* scale_a, const float* scale_b,
                   int b_per_channel, const float* bias, qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * FP8 rung of the precision ladder: E4M3 operands on the
+ * tcgen05 kind::f8f6f4 tensor cores, FP32 accumulators, the same dequant
+ * epilogue as K6 (c = acc * (scale_a[0] * scale_b[n]) + bias[n]).  Quantizers:
+ * s = absmax / 448, q = e4m3_rn_satfinite(x / s); per tensor (absmax from
+ * qsync_absmax) or per row (weights).  K % 16 == 0.
+ * ------------------------------------------------------------------------- */
+int qsync_gemm_f8(const uint8_t* a, const uint8_t* b, int64_t m, int64_t n, int64_t k, void* c, int c_dtype,
+                  const float* scale_a, const float* scale_b, int b_per_channel, const float* bias,
+                  qsync_stream_t stream);
+int qsync_quantize_fp8(const void* x, int dtype, int64_t n, const float* absmax, uint8_t* q, float* scale_out,
+                       qsync_stream_t stream);
+int qsync_quantize_fp8_rows(const float* w, int64_t rows, int64_t cols, uint8_t* q, float* scales,
+                            qsync_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * K7  FP16/BF16 GEMM on tcgen05 (kind::f16, FP32 accumulators in TMEM).

@@ -18,7 +18,7 @@ ERROR_KINDS = ["graph-cycle", "validation", "reference", "domain", "missing-prof
                "missing-model", "degenerate-fit", "stats-incomplete", "kind-mismatch",
                "topology", "enumeration-limit", "infeasible", "io", "internal"]
 
-F32, F16, BF16, I8, I32 = 0, 1, 2, 3, 4
+F32, F16, BF16, I8, I32, F8 = 0, 1, 2, 3, 4, 5
 ACT_NONE, ACT_GELU, ACT_DERIV = 0, 1, 2
 
 
@@ -83,6 +83,9 @@ SIGNATURES = {
     "qsync_embed_layernorm_bwd": [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p],
     "qsync_conv_fwd_implicit": [_p, _int, _i64, _i64, _i64, _i64, _int, _int, _int, _int, _int, _int, _p,
                                 _i64, _p, _int, _p, _p, _int, _p, _p],
+    "qsync_gemm_f8": [_p, _p, _i64, _i64, _i64, _p, _int, _p, _p, _int, _p, _p],
+    "qsync_quantize_fp8": [_p, _int, _i64, _p, _p, _p, _p],
+    "qsync_quantize_fp8_rows": [_p, _i64, _i64, _p, _p, _p],
     # non-header helpers
     "qsync_gemm_force_tile_n": [_int],
     "qsync_gemm_force_splitk": [_int],

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -111,6 +112,14 @@ template <>
 struct Elem<QSYNC_I8> {
     using T = int8_t;
     __device__ static float f(T v) { return static_cast<float>(v); }
+};
+template <>
+struct Elem<QSYNC_F8E4M3> {
+    using T = uint8_t;
+    __device__ static float f(T v) {
+        const __half_raw h = __nv_cvt_fp8_to_halfraw(static_cast<__nv_fp8_storage_t>(v), __NV_E4M3);
+        return __half2float(__half(h));
+    }
 };
 
 // Scale rule shared by every quantizer: s = absmax / 127 (IEEE), 1 if all-zero.

@@ -53,6 +53,7 @@ struct EpiParams {
     int kb_per;     // k-blocks per split
     // Implicit-GEMM convolution (kLay bit 2): A[(n,p,q), (r,s,c)] is gathered from
     // the NHWC input on the fly -- never materialised.
+    int fp8;            // byte operands are FP8 E4M3 (kind::f8f6f4, FP32 accumulators)
     const uint8_t* cx;  // NHWC input (elements of the GEMM operand type)
     int cN, cH, cW, cC, cP, cQ, cS, csh, csw, cph, cpw;
 };
@@ -314,12 +315,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                 : ptx::sw128_kmajor_desc(b_addr + k * 32);
                         const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
                         if (kCta == 2) {
-                            if (kI8)
+                            if (kI8 && p.fp8)
+                                ptx::mma_f8_pair(d_tmem, da, db, p.idesc, accum);
+                            else if (kI8)
                                 ptx::mma_i8_pair(d_tmem, da, db, p.idesc, accum);
                             else
                                 ptx::mma_f16_pair(d_tmem, da, db, p.idesc, accum);
                         } else {
-                            if (kI8)
+                            if (kI8 && p.fp8)
+                                ptx::mma_f8(d_tmem, da, db, p.idesc, accum);
+                            else if (kI8)
                                 ptx::mma_i8(d_tmem, da, db, p.idesc, accum);
                             else
                                 ptx::mma_f16(d_tmem, da, db, p.idesc, accum);
@@ -434,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j) {
                             const float sj = kI8 ? __shfl_sync(0xffffffffu, colscale, j) : alpha;
                             const float bj = __shfl_sync(0xffffffffu, bs, j);
-                            const float x = kI8 ? __fmul_rn(__int2float_rn(static_cast<int>(r[j])), sj)
+                            const float x = kI8 ? __fmul_rn(p.fp8 ? bits_f(r[j]) : __int2float_rn(static_cast<int>(r[j])), sj)
                                                 : __fmul_rn(bits_f(r[j]), sj);
                             v[j] = __fadd_rn(x, bj);
                         }
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const float sj = kI8 ? __shfl_sync(0xffffffffu, colscale, j) : alpha;
-                            v[j] = kI8 ? __fmul_rn(__int2float_rn(static_cast<int>(r[j])), sj)
+                            v[j] = kI8 ? __fmul_rn(p.fp8 ? bits_f(r[j]) : __int2float_rn(static_cast<int>(r[j])), sj)
                                        : __fmul_rn(bits_f(r[j]), sj);
                         }
                     }
@@ -592,12 +597,13 @@ int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t
 
 // Instruction descriptor (tcgen05 "idesc"): c_format [4,6), a_format [7,10),
 // b_format [10,13), a/b major [15],[16] (0 = K-major), N>>3 [17,23), M>>4 [24,29).
-uint32_t make_idesc(bool i8, bool bf16, int n, int m, int lay = 0) {
+uint32_t make_idesc(bool i8, bool bf16, int n, int m, int lay = 0, bool fp8 = false) {
     uint32_t d = 0;
     d |= static_cast<uint32_t>(lay & 1) << 15;         // A MN-major
     d |= static_cast<uint32_t>((lay >> 1) & 1) << 16;  // B MN-major
-    d |= (i8 ? 2u : 1u) << 4;                         // S32 / F32 accumulator
-    const uint32_t fmt = i8 ? 1u : (bf16 ? 1u : 0u);  // signed int8 / BF16 / F16
+    d |= (i8 && !fp8 ? 2u : 1u) << 4;                 // S32 / F32 accumulator
+    // kind::i8: signed = 1; kind::f16: F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0
+    const uint32_t fmt = fp8 ? 0u : (i8 ? 1u : (bf16 ? 1u : 0u));
     d |= fmt << 7;
     d |= fmt << 10;
     d |= static_cast<uint32_t>(n >> 3) << 17;
@@ -768,11 +774,11 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     if (force_bn) sh.bn = force_bn;
     if (g_force_cta) sh.cta = g_force_cta;
     if (sh.cta == 2 && sh.bn == 64) sh.cta = 1;  // pair tiles need BN/2 >= 64 rows of B
-    p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout);
+    p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout, p.fp8);
     p.debug_epi = g_debug_epi;
     if (layout == 4) {  // implicit conv: single-CTA tiles
         sh.cta = 1;
-        p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM, 0);
+        p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM, 0, p.fp8);
         switch (sh.bn) {
             case 256: return launch<kI8, 256, 1, 4>(a, b, dt, p, st);
             case 128: return launch<kI8, 128, 1, 4>(a, b, dt, p, st);
@@ -843,6 +849,29 @@ int qsync_gemm_force_tile_n(int bn) {
     QSB_REQUIRE(bn == 0 || bn == 64 || bn == 128 || bn == 256, QSYNC_ERR_DOMAIN, "tile N must be 0/64/128/256");
     g_force_bn = bn;
     return QSYNC_OK;
+}
+
+int qsync_gemm_f8(const uint8_t* a, const uint8_t* b, int64_t m, int64_t n, int64_t k, void* c, int c_dtype,
+                  const float* scale_a, const float* scale_b, int b_per_channel, const float* bias,
+                  qsync_stream_t stream) {
+    QSB_TRY(validate(a, b, m, n, k, 16));
+    QSB_REQUIRE(c != nullptr, QSYNC_ERR_VALIDATION, "GEMM needs an output");
+    QSB_REQUIRE(c_dtype == QSYNC_F32 || c_dtype == QSYNC_F16 || c_dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
+                "FP8 GEMM epilogue output must be F32, F16 or BF16");
+    QSB_REQUIRE(scale_a && scale_b, QSYNC_ERR_VALIDATION, "the dequant epilogue needs scale_a and scale_b");
+    EpiParams p{};
+    p.M = m;
+    p.N = n;
+    p.K = k;
+    p.c = c;
+    p.c_dtype = c_dtype;
+    p.scale_a = scale_a;
+    p.scale_b = scale_b;
+    p.b_per_channel = b_per_channel;
+    p.bias = bias;
+    p.alpha = 1.0f;
+    p.fp8 = 1;
+    return dispatch<true>(a, b, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, to_stream(stream), g_force_bn);
 }
 
 int qsync_gemm_s8_ex(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k, void* c,

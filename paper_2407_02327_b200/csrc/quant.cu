@@ -7,6 +7,8 @@
 // sat(rint(x/s)), dequant = float(q)*s.
 #include <algorithm>
 
+#include <cuda_fp8.h>
+
 #include "common.cuh"
 #include "vec.cuh"
 
@@ -400,6 +402,97 @@ __global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w,
 }
 
 // ---------------------------------------------------------------------------
+// FP8 (E4M3) quantizers for the FP8 rung of the precision ladder: s =
+// absmax / 448 (IEEE; 1 for an all-zero tensor), q = e4m3_rn_satfinite(x / s).
+// Per-tensor (activations, absmax computed upstream) and per-row (weights).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float scale_fp8(float a) { return a > 0.0f ? __fdiv_rn(a, 448.0f) : 1.0f; }
+__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d) {
+    const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+    const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(c, d), __NV_SATFINITE, __NV_E4M3);
+    return lo | (hi << 16);
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_quantize_fp8(const typename Elem<DT>::T* __restrict__ x, int64_t n,
+                                                           const float* __restrict__ absmax_in,
+                                                           uint8_t* __restrict__ q, float* __restrict__ scale_out,
+                                                           int vec_ok) {
+    QSB_PDL_ENTER();
+    using V = Vec<DT>;
+    constexpr int LOADS = 16 / V::N;
+    const float s = scale_fp8(*absmax_in);
+    if (scale_out && blockIdx.x == 0 && threadIdx.x == 0) *scale_out = s;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t done = 0;
+    if (vec_ok) {
+        const int64_t n16 = n / 16;
+        const uint4* xv = reinterpret_cast<const uint4*>(x);
+        uint4* qv = reinterpret_cast<uint4*>(q);
+        for (int64_t i = tid; i < n16; i += stride) {
+            uint4 r[LOADS];
+#pragma unroll
+            for (int u = 0; u < LOADS; ++u) r[u] = ld_stream(xv + i * LOADS + u);
+            uint32_t packed[4];
+#pragma unroll
+            for (int u = 0; u < LOADS; ++u) {
+                float f[V::N];
+                V::unpack(r[u], f);
+#pragma unroll
+                for (int j = 0; j < V::N; j += 4)
+                    packed[(u * V::N + j) / 4] = e4m3x4(__fdiv_rn(f[j], s), __fdiv_rn(f[j + 1], s),
+                                                        __fdiv_rn(f[j + 2], s), __fdiv_rn(f[j + 3], s));
+            }
+            qv[i] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        }
+        done = n16 * 16;
+    }
+    for (int64_t i = done + tid; i < n; i += stride)
+        q[i] = static_cast<uint8_t>(__nv_cvt_float_to_fp8(__fdiv_rn(Elem<DT>::f(x[i]), s), __NV_SATFINITE, __NV_E4M3));
+}
+
+__global__ void __launch_bounds__(256) k_quant_rows_fp8(const float* __restrict__ w, int64_t rows, int64_t cols,
+                                                        uint8_t* __restrict__ q, float* __restrict__ scales) {
+    QSB_PDL_ENTER();
+    const int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float* wr = w + row * cols;
+    uint8_t* qr = q + row * cols;
+    float m = 0.0f;
+    for (int64_t c = lane; c < cols; c += 32) m = fmaxf(m, fabsf(wr[c]));
+    m = warp_max(m);
+    const float s = scale_fp8(m);
+    if (lane == 0) scales[row] = s;
+    const bool vec = (cols % 4 == 0) && aligned16(wr) && ((reinterpret_cast<uintptr_t>(qr) & 3u) == 0);
+    if (vec) {
+        const float4* v = reinterpret_cast<const float4*>(wr);
+        uint32_t* qo = reinterpret_cast<uint32_t*>(qr);
+        for (int64_t c = lane; c < cols / 4; c += 32) {
+            const float4 f = v[c];
+            qo[c] = e4m3x4(__fdiv_rn(f.x, s), __fdiv_rn(f.y, s), __fdiv_rn(f.z, s), __fdiv_rn(f.w, s));
+        }
+    } else {
+        for (int64_t c = lane; c < cols; c += 32)
+            qr[c] = static_cast<uint8_t>(__nv_cvt_float_to_fp8(__fdiv_rn(wr[c], s), __NV_SATFINITE, __NV_E4M3));
+    }
+}
+
+template <int DT>
+struct QuantFp8Run {
+    static int run(const void* x, int64_t n, const float* absmax, uint8_t* q, float* scale_out, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        if (n == 0) return QSYNC_OK;
+        const int vec = aligned16(x) && aligned16(q);
+        const int grid = grid_for(n / 16 + 1, kThreads, 4);
+        pdl_launch(k_quantize_fp8<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, absmax, q,
+                   scale_out, vec);
+        return check_launch("k_quantize_fp8");
+    }
+};
+
+// ---------------------------------------------------------------------------
 // K3: dequantize, 16 int8 in -> 16 floats out per thread-iteration.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_dequant(const int8_t* __restrict__ q, int64_t n,
@@ -484,7 +577,18 @@ struct Store<SD, QSYNC_BF16> {
 template <int SD>
 __device__ __forceinline__ void load8(const typename Elem<SD>::T* x, int64_t i, float* f) {
     const uint4* v = reinterpret_cast<const uint4*>(x + i);
-    if constexpr (SD == QSYNC_I8) {
+    if constexpr (SD == QSYNC_F8E4M3) {
+        const uint2 w = *reinterpret_cast<const uint2*>(x + i);
+        const uint32_t ww[2] = {w.x, w.y};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2(
+                static_cast<__nv_fp8x2_storage_t>((ww[k >> 1] >> (16 * (k & 1))) & 0xffffu), __NV_E4M3);
+            const float2 t = __half22float2(__half2(h));
+            f[2 * k] = t.x;
+            f[2 * k + 1] = t.y;
+        }
+    } else if constexpr (SD == QSYNC_I8) {
         const uint2 w = *reinterpret_cast<const uint2*>(x + i);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -902,6 +1006,8 @@ int qsync_cast(const void* x, int src, void* out, int dst, int64_t n, qsync_stre
     QSB_CAST(QSYNC_BF16, QSYNC_F16)
     QSB_CAST(QSYNC_I8, QSYNC_F16)
     QSB_CAST(QSYNC_I8, QSYNC_F32)
+    QSB_CAST(QSYNC_F8E4M3, QSYNC_F16)
+    QSB_CAST(QSYNC_F8E4M3, QSYNC_F32)
 #undef QSB_CAST
     return set_error(QSYNC_ERR_DOMAIN, "unsupported cast " + std::to_string(src) + "->" + std::to_string(dst));
 }
@@ -963,6 +1069,22 @@ int qsync_act_cast(const void* x, int src, void* out, int dst, int64_t n, int ac
 #undef QSB_ACAST
     return set_error(QSYNC_ERR_DOMAIN, "unsupported activation cast " + std::to_string(src) + "->" +
                                            std::to_string(dst));
+}
+
+int qsync_quantize_fp8(const void* x, int dtype, int64_t n, const float* absmax, uint8_t* q, float* scale_out,
+                       qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    QSB_REQUIRE(absmax != nullptr, QSYNC_ERR_VALIDATION, "absmax is required");
+    return dispatch_dtype<QuantFp8Run>(dtype, x, n, absmax, q, scale_out, to_stream(stream));
+}
+
+int qsync_quantize_fp8_rows(const float* w, int64_t rows, int64_t cols, uint8_t* q, float* scales,
+                            qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
+    if (rows == 0) return QSYNC_OK;
+    pdl_launch(k_quant_rows_fp8, dim3(static_cast<unsigned>((rows + 7) / 8)), dim3(256), 0, to_stream(stream), w,
+               rows, cols, q, scales);
+    return check_launch("k_quant_rows_fp8");
 }
 
 }  // extern "C"

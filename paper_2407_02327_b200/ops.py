@@ -15,7 +15,7 @@ from . import _lib
 from ._lib import BF16, F16, F32, QsyncError, call
 
 _DT = {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}
-_DT_CAST = {**_DT, torch.int8: _lib.I8}
+_DT_CAST = {**_DT, torch.int8: _lib.I8, torch.float8_e4m3fn: _lib.F8}
 
 
 def _stream() -> int:
@@ -509,6 +509,42 @@ def attention_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse:
 
 def sm_count() -> int:
     return int(_lib.lib().qsync_device_sm_count())
+
+
+# --------------------------------------------------------------------------- FP8 rung
+def quantize_fp8(x: torch.Tensor):
+    """Per-tensor E4M3: s = absmax/448, q = e4m3(x / s).  Returns (q float8_e4m3fn, s[1])."""
+    _req(x, "x", _DT)
+    am = absmax(x)
+    q = torch.empty(x.shape, device=x.device, dtype=torch.float8_e4m3fn)
+    s = torch.empty(1, device=x.device, dtype=torch.float32)
+    call("qsync_quantize_fp8", _ptr(x), _DT[x.dtype], x.numel(), _ptr(am), _ptr(q), _ptr(s), _stream())
+    return q, s
+
+
+def quantize_fp8_rows(w: torch.Tensor):
+    """Per-row (output channel) E4M3 of W [N, K]: returns (q, scales[N])."""
+    _req(w, "w", (torch.float32,))
+    q = torch.empty(w.shape, device=w.device, dtype=torch.float8_e4m3fn)
+    s = torch.empty(w.shape[0], device=w.device, dtype=torch.float32)
+    call("qsync_quantize_fp8_rows", _ptr(w), w.shape[0], w.shape[1], _ptr(q), _ptr(s), _stream())
+    return q, s
+
+
+def gemm_f8(a: torch.Tensor, b: torch.Tensor, scale_a, scale_b, bias=None, out_dtype=torch.float32,
+            b_per_channel: bool = True, out=None) -> torch.Tensor:
+    """C = (A B^T) * scale_a * scale_b[n] + bias on tcgen05 kind::f8f6f4 (E4M3, FP32 accumulation)."""
+    _req(a, "a", (torch.float8_e4m3fn,))
+    _req(b, "b", (torch.float8_e4m3fn,))
+    M, K = a.shape
+    N = b.shape[0]
+    c = out if out is not None else torch.empty((M, N), device=a.device, dtype=out_dtype)
+    ev = _timed("gemm_f8", 2.0 * M * N * K)
+    call("qsync_gemm_f8", _ptr(a), _ptr(b), M, N, K, _ptr(c), _DT[c.dtype], _ptr(scale_a), _ptr(scale_b),
+         int(b_per_channel), _ptr(bias), _stream())
+    if ev is not None:
+        ev.record()
+    return c
 
 
 def launch_count() -> int:

@@ -22,6 +22,12 @@ import torch.nn.functional as F
 from . import ops
 
 INT8, FP16, FP32 = "INT8", "FP16", "FP32"
+# FP8 (E4M3) is the B200 extension of the ladder: a
+# fixed-point-like rung between INT8 and FP16 -- per-tensor activation and
+# per-channel weight scales, FP32 accumulation, FP32 output, FP16 backward.
+# The reference planner's Precision enum (precision.hpp:12) does not know it,
+# so plans from the reference never select it.
+FP8 = "FP8"
 PRECISIONS = (INT8, FP16, FP32)
 
 # Profiling hook (profiler.StatsRecorder): when set, every QLinear records the
@@ -41,8 +47,8 @@ def output_dtype(precision: str) -> torch.dtype:
 
 
 def backward_precision(precision: str) -> str:
-    """cost_mapper.cpp:13-15."""
-    return FP16 if precision == INT8 else precision
+    """cost_mapper.cpp:13-15 (FP8 backs off to FP16 like INT8)."""
+    return FP16 if precision in (INT8, FP8) else precision
 
 
 # Optional side stream for weight gradients (TrainStep enables it): wgrad only
@@ -120,6 +126,33 @@ class _QLinearInt8(torch.autograd.Function):
         return _fp16_backward(ctx, dy, x16, w16, xs) + (None,)
 
 
+class _QLinearFp8(torch.autograd.Function):
+    """FP8 rung: E4M3 operands (per-tensor activation, per-channel weight scales),
+    tcgen05 kind::f8f6f4 GEMM with the dequant epilogue -> FP32; FP16 backward
+    reading the saved 1-byte activation (exact in FP16) times s_x."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, name=None):
+        _record(name, "act", x)
+        _record(name, "w", w)
+        ctx.name = name
+        xq, xs = ops.quantize_fp8(x)
+        wq, ws = ops.quantize_fp8_rows(w)
+        y = ops.gemm_f8(xq, wq, xs, ws, b)
+        ctx.save_for_backward(xq, xs)
+        ctx.x_dtype = x.dtype
+        ctx.w_ref, ctx.b_ref = w, b
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        xq, xs = ctx.saved_tensors
+        _record(ctx.name, "grad", dy)
+        x16 = ops.cast(xq, torch.float16)  # exact: E4M3 values are FP16 values
+        w16 = ops.cast(ctx.w_ref.detach(), torch.float16)
+        return _fp16_backward(ctx, dy, x16, w16, xs) + (None,)
+
+
 class _QLinearFp16(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, b, name=None):
@@ -169,6 +202,8 @@ def qlinear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, precision:
         y = _QLinearInt8.apply(x2, w, b, name)
     elif precision == FP16:
         y = _QLinearFp16.apply(x2, w, b, name)
+    elif precision == FP8:
+        y = _QLinearFp8.apply(x2, w, b, name)
     elif precision == FP32:
         _record(name, "act", x2)
         _record(name, "w", w)
