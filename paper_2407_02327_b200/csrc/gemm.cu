@@ -67,7 +67,10 @@ template <int BN, int kCta = 1>
 struct Cfg {
     static constexpr int kBRows = BN / kCta;  // B rows held by one CTA
     static constexpr int kStageBytes = (BM + kBRows) * BK_BYTES;
-    static constexpr int kStages = kStageBytes >= 48 * 1024 ? 4 : (kStageBytes >= 32 * 1024 ? 6 : 8);
+#ifndef QSB_GEMM_STAGES_48K
+#define QSB_GEMM_STAGES_48K 4
+#endif
+    static constexpr int kStages = kStageBytes >= 48 * 1024 ? QSB_GEMM_STAGES_48K : (kStageBytes >= 32 * 1024 ? 6 : 8);
     static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
     static constexpr int kEpiStageBytes = 4 * 2 * kStageChunkBytes;  // 4 warps x double buffer
     static constexpr int kSmemBytes =

@@ -222,8 +222,11 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
 // owns NV/2 float4 columns, which halves the per-lane column accumulators and
 // brings the kernel to 2 blocks / SM.  The two halves' row sums are exchanged
 // through shared memory under a 64-thread named barrier.
+#ifndef QSB_LN_BWD_MINB
+#define QSB_LN_BWD_MINB 2
+#endif
 template <int NV>
-__global__ void __launch_bounds__(256, 2) k_ln_bwd2(const float* __restrict__ dy,
+__global__ void __launch_bounds__(256, QSB_LN_BWD_MINB) k_ln_bwd2(const float* __restrict__ dy,
                                                     const float* __restrict__ s,
                                                     const float* __restrict__ mean_in,
                                                     const float* __restrict__ rstd_in,
