@@ -151,12 +151,14 @@ __device__ __forceinline__ float gelu_erf(float x) {
     const float e = erff(__fmul_rn(x, 0.70710678118654752f));
     return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, e));
 }
-// Both at once, sharing the erf (the FF2 operand kernels store GELU'(x) for the
-// backward): g is bit-identical to gelu_erf(x), gp to gelu_erf_grad(x).
+// Both at once, sharing the erf (the FF2 operand kernels store GELU'(x) in FP16
+// for the backward): g is bit-identical to gelu_erf(x); gp uses the fast
+// exponential (it is rounded to FP16 anyway).
 __device__ __forceinline__ void gelu_and_grad(float x, float& g, float& gp) {
     const float e1 = __fadd_rn(1.0f, erff(__fmul_rn(x, 0.70710678118654752f)));
     g = __fmul_rn(__fmul_rn(0.5f, x), e1);
-    const float pdf = __fmul_rn(expf(__fmul_rn(-0.5f, __fmul_rn(x, x))), 0.39894228040143268f);
+    // gp is stored in FP16: the fast exponential's few-ulp error is far below that
+    const float pdf = __fmul_rn(__expf(__fmul_rn(-0.5f, __fmul_rn(x, x))), 0.39894228040143268f);
     gp = __fadd_rn(__fmul_rn(0.5f, e1), __fmul_rn(x, pdf));
 }
 __device__ __forceinline__ float gelu_erf_grad(float x) {
