@@ -93,6 +93,7 @@ SIGNATURES = {
     "qsync_gemm_debug_epilogue": [_int],
     "qsync_gemm_set_pdl": [_int],
     "qsync_gemm_set_max_ctas": [_int],
+    "qsync_attention_set_impl": [_int],
     "qsync_mt_jump_selftest": [],
 }
 _RESTYPES = {"qsync_last_error": C.c_char_p, "qsync_status_name": C.c_char_p,

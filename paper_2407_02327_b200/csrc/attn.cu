@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace qsb {
 namespace {
@@ -374,6 +375,152 @@ __global__ void __launch_bounds__(kThreadsA, 2) k_attn_bwd(const __half* __restr
     }
 }
 
+// ---------------------------------------------------------------------------- tcgen05 forward
+// One CTA (4 warps) per (batch, head), the two GEMMs on the 5th-generation tensor
+// cores: Q, K, V land by TMA (128B swizzle) from the packed QKV; S = Q K^T
+// (M = 128 queries, N = 128 keys, K = 64) accumulates in TMEM; thread t owns
+// query row t (TMEM lane t), so the row softmax needs no shuffles; P (FP16) is
+// written into shared memory in the K-major UMMA layout and O = P V (N = 64,
+// K = 128, V read MN-major) accumulates in the same TMEM columns once S has been
+// read out.  P overwrites Q and K (dead after S), so a CTA needs 48 KB of shared
+// memory and 128 TMEM columns: 4 CTAs (4 heads) per SM.
+constexpr int kTcThreads = 128;
+constexpr int kTcFwdSmem = 3 * kTile + 1024 + 64;
+
+__device__ __forceinline__ uint32_t idesc_f16_f32(int n, int m, bool b_mn) {
+    uint32_t d = 1u << 4;                                // F32 accumulator; A/B F16
+    d |= static_cast<uint32_t>(b_mn) << 16;              // B MN-major
+    d |= static_cast<uint32_t>(n >> 3) << 17;
+    d |= static_cast<uint32_t>(m >> 4) << 24;
+    return d;
+}
+
+__global__ void __launch_bounds__(kTcThreads) k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, int H,
+                                                            float scale, __half* __restrict__ out,
+                                                            float* __restrict__ lse,
+                                                            unsigned* __restrict__ out_absmax) {
+    QSB_PDL_ENTER();
+    extern __shared__ uint8_t sm_raw[];
+    const uint32_t raw = ptx::smem_u32(sm_raw);
+    uint8_t* sm = sm_raw + ((1024 - (raw & 1023)) & 1023);
+    uint8_t* sQ = sm;
+    uint8_t* sK = sm + kTile;
+    uint8_t* sV = sm + 2 * kTile;
+    uint8_t* sP = sm;  // over Q and K: 2 K-blocks (keys 0..63, 64..127) of [128 x 128B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 3 * kTile);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+    const int bh = blockIdx.x, b = bh / H, h = bh % H;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    if (t == 0) {
+        ptx::tma_prefetch(&tm_qkv);
+        for (int i = 0; i < 3; ++i) ptx::mbar_init(&bars[i], 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<128>(tslot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    if (t == 0) {
+        ptx::mbar_arrive_expect_tx(&bars[0], 3 * kTile);
+        const int row = b * kS;
+        ptx::tma_load_2d(sQ, &tm_qkv, &bars[0], h * kD, row);
+        ptx::tma_load_2d(sK, &tm_qkv, &bars[0], (H + h) * kD, row);
+        ptx::tma_load_2d(sV, &tm_qkv, &bars[0], (2 * H + h) * kD, row);
+        ptx::mbar_wait(&bars[0], 0);
+        ptx::tc_fence_after();
+        const uint32_t id_s = idesc_f16_f32(kS, kS, false);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k)
+            ptx::mma_f16(tmem, ptx::sw128_kmajor_desc(ptx::smem_u32(sQ) + k * 32),
+                         ptx::sw128_kmajor_desc(ptx::smem_u32(sK) + k * 32), id_s, k > 0 ? 1u : 0u);
+        ptx::tc_commit(&bars[1]);
+    }
+    ptx::mbar_wait(&bars[1], 0);
+    ptx::tc_fence_after();
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(trow + 32 * c, r);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
+    }
+    const float sl2 = scale * kLog2e;
+    float sum = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(trow + 32 * c, r);
+        ptx::tmem_ld_wait();
+        uint32_t pkd[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const float p0 = exp2f(__uint_as_float(r[2 * j]) * sl2 - mx * sl2);
+            const float p1 = exp2f(__uint_as_float(r[2 * j + 1]) * sl2 - mx * sl2);
+            sum += p0 + p1;
+            pkd[j] = pk(p0, p1);
+        }
+        const uint32_t blk = ptx::smem_u32(sP + (c >> 1) * kTile) + t * 128;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int chunk = (c & 1) * 4 + q;
+            ptx::st_shared_v4(blk + ((chunk ^ (t & 7)) << 4), pkd[4 * q], pkd[4 * q + 1], pkd[4 * q + 2],
+                              pkd[4 * q + 3]);
+        }
+    }
+    ptx::fence_proxy_async_smem();  // P (generic-proxy stores) before the tensor core reads it
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (t == 0) {
+        const uint32_t id_o = idesc_f16_f32(kD, kS, true);
+#pragma unroll
+        for (int k = 0; k < kS / 16; ++k) {
+            const uint64_t da = ptx::sw128_kmajor_desc(ptx::smem_u32(sP) + (k >> 2) * kTile + (k & 3) * 32);
+            const uint64_t db = ptx::sw128_mnmajor_desc(ptx::smem_u32(sV) + k * 16 * 128, kTile);
+            ptx::mma_f16(tmem, da, db, id_o, k > 0 ? 1u : 0u);
+        }
+        ptx::tc_commit(&bars[2]);
+    }
+    ptx::mbar_wait(&bars[2], 0);
+    ptx::tc_fence_after();
+    uint32_t o[2][32];
+    ptx::tmem_ld32(trow, o[0]);
+    ptx::tmem_ld32(trow + 32, o[1]);
+    ptx::tmem_ld_wait();
+    const float inv = 1.f / sum;
+    uint32_t w[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        w[j] = pk(__uint_as_float(o[j >> 4][(2 * j) & 31]) * inv, __uint_as_float(o[j >> 4][(2 * j + 1) & 31]) * inv);
+    __half* orow = out + (static_cast<int64_t>(b * kS + t) * H + h) * kD;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        reinterpret_cast<uint4*>(orow)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    lse[static_cast<int64_t>(bh) * kS + t] = mx * scale + logf(sum);
+    if (out_absmax) {
+        float amax = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+            amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+        }
+        amax = warp_max(amax);
+        if (lane == 0 && amax > 0.f) atomicMax(out_absmax, __float_as_uint(amax));
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<128>(tmem);
+    }
+}
+
+int g_attn_tc = 1;  // tcgen05 forward (qsync_attention_set_impl)
+
 constexpr int kFwdSmem = 3 * kTile;
 constexpr int kBwdSmem = 4 * kTile + 2 * kTile + 2 * kS * 4;
 
@@ -404,6 +551,20 @@ int qsync_attention_fwd(const void* qkv, int64_t B, int64_t S, int64_t H, int64_
         configured = true;
     }
     if (out_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(out_absmax, 0, sizeof(float), st), "memset"));
+    if (g_attn_tc) {
+        static bool tc_configured = false;
+        if (!tc_configured) {
+            QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     kTcFwdSmem),
+                                "cudaFuncSetAttribute"));
+            tc_configured = true;
+        }
+        CUtensorMap tm;
+        QSB_TRY(make_tma_2d(&tm, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 3 * H * kD, B * kS, kD, kS));
+        pdl_launch(k_attn_fwd_tc, dim3(static_cast<unsigned>(B * H)), dim3(kTcThreads), kTcFwdSmem, st, tm,
+                   static_cast<int>(H), scale, static_cast<__half*>(out), lse, reinterpret_cast<unsigned*>(out_absmax));
+        return check_launch("k_attn_fwd_tc");
+    }
     pdl_launch(k_attn_fwd, dim3(static_cast<unsigned>(B * H)), dim3(kThreadsA), kFwdSmem, st, 
         static_cast<const __half*>(qkv), static_cast<int>(H), scale, static_cast<__half*>(out), lse,
         reinterpret_cast<unsigned*>(out_absmax));
@@ -425,6 +586,11 @@ int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, cons
         static_cast<const __half*>(qkv), static_cast<const __half*>(out), static_cast<const __half*>(dout), lse,
         static_cast<int>(H), scale, static_cast<__half*>(dqkv));
     return check_launch("k_attn_bwd");
+}
+
+int qsync_attention_set_impl(int tc) {
+    g_attn_tc = tc ? 1 : 0;
+    return QSYNC_OK;
 }
 
 }  // extern "C"

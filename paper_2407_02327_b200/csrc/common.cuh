@@ -39,6 +39,9 @@ inline int cuda_status(cudaError_t e, const char* what) {
 inline cudaStream_t to_stream(qsync_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+// 2-D SWIZZLE_128B TMA map (row pitch = inner * elem_bytes), defined in gemm.cu.
+int make_tma_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes, int64_t inner,
+                int64_t outer, uint32_t box_inner, uint32_t box_outer);
 
 // ---- programmatic dependent launch (PDL) -----------------------------------
 // Every kernel of this library starts with QSB_PDL_ENTER(): it waits for the

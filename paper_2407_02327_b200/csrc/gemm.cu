@@ -813,6 +813,12 @@ int validate(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int6
 }
 
 }  // namespace
+
+// 2-D SWIZZLE_128B tensor map for kernels outside this file (attention core).
+int make_tma_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes, int64_t inner,
+                int64_t outer, uint32_t box_inner, uint32_t box_outer) {
+    return make_map(map, ptr, dt, elem_bytes, inner, outer, box_inner, box_outer);
+}
 }  // namespace qsb
 
 using namespace qsb;

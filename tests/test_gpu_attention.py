@@ -47,3 +47,21 @@ def test_attention_rejects_unsupported_shapes():
     qkv = torch.zeros(1, 64, 3, 2, 64, device=DEV, dtype=torch.float16)
     with pytest.raises(Exception, match="seq 128"):
         ops.attention_fwd(qkv)
+
+
+def test_attention_fwd_tcgen05_vs_mma_sync():
+    """The tcgen05 forward (TMEM accumulators, TMA operands) and the mma.sync
+    forward agree (same P rounding, different accumulation order)."""
+    from paper_2407_02327_b200._lib import call
+    torch.manual_seed(21)
+    qkv = torch.randn(8, 128, 3, 12, 64, device=DEV).half()
+    call("qsync_attention_set_impl", 1)
+    o1, l1, a1 = ops.attention_fwd(qkv, want_absmax=True)
+    call("qsync_attention_set_impl", 0)
+    try:
+        o0, l0, a0 = ops.attention_fwd(qkv, want_absmax=True)
+    finally:
+        call("qsync_attention_set_impl", 1)
+    assert _rel(o1, o0) < 2e-3
+    assert (l1 - l0).abs().max().item() < 1e-4
+    assert a1.item() == o1.float().abs().max().item()
