@@ -198,6 +198,9 @@ def conv_bench(results: dict, batch: int = 64) -> None:
     from paper_2407_02327_b200.qconv import qconv2d
     from paper_2407_02327_b200.qlinear import FP16, INT8
     convs = resnet50_convs(batch)
+    if os.environ.get("QSB_CONV_BWD_COL"):  # A/B: materialised im2col / col2im backward
+        ops.implicit_dgrad_ok = lambda *a: False
+        ops.implicit_wgrad_ok = lambda *a: False
     distinct = {}
     for c in convs:
         distinct.setdefault(c[1:], []).append(c[0])
@@ -214,16 +217,18 @@ def conv_bench(results: dict, batch: int = 64) -> None:
         b = torch.zeros(Cout, device="cuda", requires_grad=True)
         for prec in (INT8, FP16):
             xin = x if prec == INT8 else x.half()
-            xg = xin.detach().clone().requires_grad_(True)
+            # the stem's input is the image: no dgrad (as in training)
+            xg = xin.detach().clone().requires_grad_(C != 3)
+            wrt = [t for t in (xg, w, b) if t.requires_grad]
             # Device time with the launches queued behind a device spin, so the
             # host's launch overhead is excluded (as in the CUDA-graphed step).
             tf = spin_time_ms(lambda: qconv2d(xin, w, b, (st, st), (pd, pd), prec))
             y = qconv2d(xg, w, b, (st, st), (pd, pd), prec)
             gy = torch.randn_like(y)
 
-            def fb():
+            def fb():  # gradients returned, not accumulated into .grad
                 yy = qconv2d(xg, w, b, (st, st), (pd, pd), prec)
-                yy.backward(gy)
+                torch.autograd.grad(yy, wrt, gy)
             tfb = spin_time_ms(fb)
             totals[prec][0] += tf * len(names)
             totals[prec][1] += tfb * len(names)

@@ -216,6 +216,32 @@ int qsync_col2im(const void* dcol, int dtype, int64_t N, int64_t H, int64_t W, i
                  int S, int sh, int sw, int ph, int pw, int dh, int dw, int64_t ld, float* dx,
                  qsync_stream_t stream);
 
+/* Implicit-GEMM Conv2d (replaces the im2col + GEMM pair of the reference's
+ * quantized conv, graph.hpp:38-40 / cost_mapper.cpp:13-15): the GEMM's producer
+ * warp gathers the column tiles straight from the NHWC tensor, nothing is
+ * materialised.  Dilation 1.
+ *   fwd:   y[(n,p,q), k] = sum x[n, p*sh-ph+r, q*sw-pw+s, c] w[k,(r,s,c)]
+ *          x I8 (dequant epilogue with scale_a / scale_b, as qsync_gemm_s8) or
+ *          F16/BF16; needs C * elem % 128 == 0.  y [N*P*Q, cout] y_dtype.
+ *   dgrad: dx[(n,h,w), c] = sum dy[n, (h+ph-r)/sh, (w+pw-s)/sw, k] w[k,r,s,c]
+ *          (terms off the stride grid vanish); dy F16/BF16 [N,P,Q,cout] with
+ *          cout % 64 == 0, w [cout, R, S, C] (unpadded, C % 8 == 0), dx
+ *          [N*H*W, C] dx_dtype.
+ *   wgrad: dw[k, (r,s,c)] (+)= alpha * alpha_dev * sum dy[(n,p,q), k] *
+ *          x[n, p*sh-ph+r, q*sw-pw+s, c]; x F16/BF16 with C % 64 == 0, dy
+ *          [N*P*Q, cout] (cout % 8 == 0), dw FP32 [cout, R*S*C]; accumulate != 0
+ *          adds into dw (the K = pixels reduction is then split across SMs). */
+int qsync_conv_fwd_implicit(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int R,
+                            int S, int sh, int sw, int ph, int pw, const void* w, int64_t cout, void* y,
+                            int y_dtype, const float* scale_a, const float* scale_b, int b_per_channel,
+                            const float* bias, qsync_stream_t stream);
+int qsync_conv_dgrad_implicit(const void* dy, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int R,
+                              int S, int sh, int sw, int ph, int pw, const void* w, int64_t cout, void* dx,
+                              int dx_dtype, qsync_stream_t stream);
+int qsync_conv_wgrad_implicit(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int R,
+                              int S, int sh, int sw, int ph, int pw, const void* dy, int64_t cout, float* dw,
+                              float alpha, const float* alpha_dev, int accumulate, qsync_stream_t stream);
+
 /* ---------------------------------------------------------------------------
  * Glue between planned operators: fused residual add + LayerNorm.
  * fwd: s = a + b (b FP32 or FP16 [rows, cols], may be NULL), y = LN(s) with

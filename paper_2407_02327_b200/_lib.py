@@ -83,6 +83,10 @@ SIGNATURES = {
     "qsync_embed_layernorm_bwd": [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p],
     "qsync_conv_fwd_implicit": [_p, _int, _i64, _i64, _i64, _i64, _int, _int, _int, _int, _int, _int, _p,
                                 _i64, _p, _int, _p, _p, _int, _p, _p],
+    "qsync_conv_dgrad_implicit": [_p, _int, _i64, _i64, _i64, _i64, _int, _int, _int, _int, _int, _int, _p,
+                                  _i64, _p, _int, _p],
+    "qsync_conv_wgrad_implicit": [_p, _int, _i64, _i64, _i64, _i64, _int, _int, _int, _int, _int, _int, _p,
+                                  _i64, _p, _f32, _p, _int, _p],
     "qsync_gemm_f8": [_p, _p, _i64, _i64, _i64, _p, _int, _p, _p, _int, _p, _p],
     "qsync_quantize_fp8": [_p, _int, _i64, _p, _p, _p, _p],
     "qsync_quantize_fp8_rows": [_p, _i64, _i64, _p, _p, _p],
@@ -92,6 +96,7 @@ SIGNATURES = {
     "qsync_gemm_force_cta": [_int],
     "qsync_gemm_debug_epilogue": [_int],
     "qsync_gemm_set_pdl": [_int],
+    "qsync_conv_set_impl": [_int],
     "qsync_gemm_set_max_ctas": [_int],
     "qsync_attention_set_impl": [_int],
     "qsync_mt_jump_selftest": [],

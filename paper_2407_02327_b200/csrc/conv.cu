@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) k_im2col(const T* __restrict__ x, ConvGeo
         const int h0 = p * g.sh - g.ph, w0 = q * g.sw - g.pw;
         const T* xn = x + static_cast<int64_t>(n) * g.H * g.W * C;
         T* orow = out + static_cast<int64_t>(row) * g.ld;
-        if (vec) {
+        if (vec == 1) {
             const int CV = C / V;
             const int nch = static_cast<int>(g.ld / V);
             for (int j = lane; j < nch; j += 32) {
@@ -56,6 +56,36 @@ __global__ void __launch_bounds__(256) k_im2col(const T* __restrict__ x, ConvGeo
                         v = *reinterpret_cast<const uint4*>(xn + (static_cast<int64_t>(h) * g.W + w) * C + c);
                 }
                 *reinterpret_cast<uint4*>(orow + j * V) = v;
+            }
+        } else if (vec == 2) {
+            // Narrow C (the stem's C = 3): each lane assembles a 16-byte chunk of
+            // the row, stepping (c, s, r) incrementally instead of dividing per element.
+            const int nch = static_cast<int>(g.ld / V);
+            for (int j = lane; j < nch; j += 32) {
+                const int k0 = j * V;
+                int tap = k0 / C;
+                int c = k0 - tap * C;
+                int r = tap / g.S, ss = tap - r * g.S;
+                union {
+                    uint4 u;
+                    T e[V];
+                } v;
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    T val = T(0);
+                    const int h = h0 + r * g.dh, w = w0 + ss * g.dw;
+                    if (k0 + e < K && h >= 0 && h < g.H && w >= 0 && w < g.W)
+                        val = xn[(static_cast<int64_t>(h) * g.W + w) * C + c];
+                    v.e[e] = val;
+                    if (++c == C) {
+                        c = 0;
+                        if (++ss == g.S) {
+                            ss = 0;
+                            ++r;
+                        }
+                    }
+                }
+                *reinterpret_cast<uint4*>(orow + j * V) = v.u;
             }
         } else {
             for (int k = lane; k < g.ld; k += 32) {
@@ -221,12 +251,16 @@ int qsync_im2col(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int6
     cudaStream_t st = to_stream(stream);
     const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     if (dtype == QSYNC_I8) {
-        const int vec = (C % 16 == 0) && (g.ld % 16 == 0) && al(x) && al(out);
+        const int vec = (C % 16 == 0) && (g.ld % 16 == 0) && al(x) && al(out) ? 1
+                        : (g.ld % 16 == 0 && al(out))                          ? 2
+                                                                               : 0;
         const int64_t work = g.N * g.P * g.Q;
         k_im2col<int8_t><<<grid_of(work), 256, 0, st>>>(static_cast<const int8_t*>(x), g,
                                                          static_cast<int8_t*>(out), vec);
     } else if (dtype == QSYNC_F16 || dtype == QSYNC_BF16) {
-        const int vec = (C % 8 == 0) && (g.ld % 8 == 0) && al(x) && al(out);
+        const int vec = (C % 8 == 0) && (g.ld % 8 == 0) && al(x) && al(out) ? 1
+                        : (g.ld % 8 == 0 && al(out))                         ? 2
+                                                                             : 0;
         const int64_t work = g.N * g.P * g.Q;
         k_im2col<uint16_t><<<grid_of(work), 256, 0, st>>>(static_cast<const uint16_t*>(x), g,
                                                            static_cast<uint16_t*>(out), vec);

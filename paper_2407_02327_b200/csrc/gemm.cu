@@ -54,8 +54,17 @@ struct EpiParams {
     // Implicit-GEMM convolution (kLay bit 2): A[(n,p,q), (r,s,c)] is gathered from
     // the NHWC input on the fly -- never materialised.
     int fp8;            // byte operands are FP8 E4M3 (kind::f8f6f4, FP32 accumulators)
+    // kLay bit 3: B (MN-major) is gathered instead -- the conv wgrad, whose
+    // B[(n,p,q), (r,s,c)] is the same column matrix read K-rows = pixels.
+    // The dgrad runs as a kLay-bit-2 gather over dY with ctap = -1 (h_in =
+    // h + ph - r) and cdv = the forward stride (taps with h_in % stride != 0
+    // are zero), its B = W [Cout][R*S][C] read by a 3-D TMA map (kLay bit 4).
     const uint8_t* cx;  // NHWC input (elements of the GEMM operand type)
-    int cN, cH, cW, cC, cP, cQ, cS, csh, csw, cph, cpw;
+    int cN, cH, cW, cC, cP, cQ, cR, cS, csh, csw, cph, cpw;
+    int ctap, cdvh, cdvw;
+    // kLay bits 5 / 6: the same operands loaded by TMA in im2col mode instead
+    // (A for fwd / stride-1 dgrad -- the dgrad as a conv of dY with pad k-1-p and
+    // flipped taps; B for wgrad); one elected thread, no gather lanes.
 };
 
 constexpr int kStageChunkBytes = 32 * 128;  // one warp's 32 rows x 128 B staging chunk
@@ -123,11 +132,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0 && lane == 0) {
         if (!(kLay & 4)) ptx::tma_prefetch(&tm_a);
-        ptx::tma_prefetch(&tm_b);
+        if (!(kLay & 8)) ptx::tma_prefetch(&tm_b);
         if (p.tma_store) ptx::tma_prefetch(&tm_c);
         for (int s = 0; s < kStages; ++s) {
             // implicit conv: + one cp.async completion arrival per producer lane
-            ptx::mbar_init(&full[s], (kLay & 4) ? 33 : 1);
+            ptx::mbar_init(&full[s], (kLay & 12) ? 33 : 1);
             ptx::mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -158,18 +167,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t full_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
     const uint32_t tempty_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
 
-    if (warp == 0 && (kLay & 4)) {
+    if (warp == 0 && (kLay & 12)) {
         // ============ implicit-GEMM conv producer (all 32 lanes) ============
-        // A tile row m = output pixel (n,p,q); its 128-byte K-slice kb is one
-        // (r,s) tap's contiguous channel run x[n, p*sh-ph+r, q*sw-pw+s, c0:c0+bk]
-        // (C*elem % 128 == 0), copied by eight 16-byte cp.async into the
-        // 128B-swizzled K-major layout the UMMA descriptor reads; padding taps
-        // and rows past M are zero-filled (src-size 0).  Lane l owns rows l,
-        // l+32, l+64, l+96; lane 0 also TMA-loads the weight tile (B).
+        // kLay & 4 (fwd / dgrad): A tile row m = output pixel (n,p,q); its
+        // 128-byte K-slice kb is one (r,s) tap's contiguous channel run
+        // x[n, p*sh-ph+r, q*sw-pw+s, c0:c0+bk] (C*elem % 128 == 0), copied by
+        // eight 16-byte cp.async into the 128B-swizzled K-major layout the UMMA
+        // descriptor reads; padding taps and rows past M are zero-filled
+        // (src-size 0).  Lane l owns rows l, l+32, l+64, l+96; lane 0 also
+        // TMA-loads the weight tile (B).
+        // kLay & 8 (wgrad): B is MN-major -- per 64-column block j (one tap's
+        // 64-channel run) the stage holds bk K-rows = pixels of 128 B, the same
+        // swizzle; lane l owns K-rows l, l+32; lane 0 TMA-loads dY (A, MN-major).
         int stage = 0;
         uint32_t phase = 0;
         const int eb = kI8 ? 1 : 2;
         const int rowbytes = p.cC * eb;
+        const int64_t img = static_cast<int64_t>(p.cH) * p.cW * rowbytes;
         for (int u = unit0; u < num_units; u += unit_stride) {
             const int t = u / ksplit;
             const int m0 = (t % num_m) * kTileM;
@@ -177,15 +191,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             int hb[4], wb[4];
             const uint8_t* pix[4];
             bool rok[4];
+            if (kLay & 4) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int m = m0 + lane + 32 * i;
-                rok[i] = m < M;
-                const int mm = rok[i] ? m : 0;
-                const int q = mm % p.cQ, pp = (mm / p.cQ) % p.cP, n = mm / (p.cQ * p.cP);
-                hb[i] = pp * p.csh - p.cph;
-                wb[i] = q * p.csw - p.cpw;
-                pix[i] = p.cx + static_cast<int64_t>(n) * p.cH * p.cW * rowbytes;
+                for (int i = 0; i < 4; ++i) {
+                    const int m = m0 + lane + 32 * i;
+                    rok[i] = m < M;
+                    const int mm = rok[i] ? m : 0;
+                    const int q = mm % p.cQ, pp = (mm / p.cQ) % p.cP, n = mm / (p.cQ * p.cP);
+                    hb[i] = pp * p.csh - p.cph;
+                    wb[i] = q * p.csw - p.cpw;
+                    pix[i] = p.cx + static_cast<int64_t>(n) * img;
+                }
             }
             const int kb0 = (u % ksplit) * p.kb_per;
             const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
@@ -194,30 +210,92 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* sa = smem_a + stage * BM * BK_BYTES;
                 uint8_t* sb = smem_b + stage * kBRows * BK_BYTES;
                 if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(&full[stage], kBRows * BK_BYTES);
-                    if (kLay & 2) {
-                        for (int j = 0; j < kBRows / 64; ++j)
-                            ptx::tma_load_2d(sb + j * bk_elems * 128, &tm_b, &full[stage], n0 + 64 * j,
-                                             kb * bk_elems);
+                    if (kLay & 4) {
+                        ptx::mbar_arrive_expect_tx(&full[stage], kBRows * BK_BYTES);
+                        if (kLay & 16) {  // W [Cout][R*S][C]: K index = (rs, k) with k < cC
+                            const int kk = kb * bk_elems;
+                            for (int j = 0; j < kBRows / 64; ++j)
+                                ptx::tma_load_3d(sb + j * bk_elems * 128, &tm_b, &full[stage], n0 + 64 * j,
+                                                 kk % p.cC, kk / p.cC);
+                        } else if (kLay & 2) {
+                            for (int j = 0; j < kBRows / 64; ++j)
+                                ptx::tma_load_2d(sb + j * bk_elems * 128, &tm_b, &full[stage], n0 + 64 * j,
+                                                 kb * bk_elems);
+                        } else {
+                            ptx::tma_load_2d(sb, &tm_b, &full[stage], kb * bk_elems, n0);
+                        }
                     } else {
-                        ptx::tma_load_2d(sb, &tm_b, &full[stage], kb * bk_elems, n0);
+                        ptx::mbar_arrive_expect_tx(&full[stage], BM * BK_BYTES);
+                        for (int j = 0; j < BM / 64; ++j)
+                            ptx::tma_load_2d(sa + j * bk_elems * 128, &tm_a, &full[stage], m0 + 64 * j,
+                                             kb * bk_elems);
                     }
                 }
-                const int kbyte = kb * BK_BYTES;            // byte offset along K = (tap, c)
-                const int tap = kbyte / rowbytes;
-                const int cbyte = kbyte - tap * rowbytes;
-                const int r = tap / p.cS, sx = tap - r * p.cS;
-                const uint32_t sbase = ptx::smem_u32(sa);
+                if (kLay & 4) {
+                    const int kbyte = kb * BK_BYTES;  // byte offset along K = (tap, c)
+                    const int tap = kbyte / rowbytes;
+                    const int cbyte = kbyte - tap * rowbytes;
+                    const int r = tap / p.cS, sx = tap - r * p.cS;
+                    const uint32_t sbase = ptx::smem_u32(sa);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int row = lane + 32 * i;
-                    const int h = hb[i] + r, w = wb[i] + sx;
-                    const bool ok = rok[i] && h >= 0 && h < p.cH && w >= 0 && w < p.cW;
-                    const uint8_t* src = ok ? pix[i] + (static_cast<int64_t>(h) * p.cW + w) * rowbytes + cbyte : p.cx;
-                    const uint32_t nbytes = ok ? 16u : 0u;
+                    for (int i = 0; i < 4; ++i) {
+                        const int row = lane + 32 * i;
+                        int h = hb[i] + p.ctap * r, w = wb[i] + p.ctap * sx;
+                        bool ok = rok[i];
+                        if (p.cdvh > 1) {  // dgrad of a strided conv: only taps on the stride grid
+                            ok = ok && h >= 0 && h % p.cdvh == 0;
+                            h /= p.cdvh;
+                        }
+                        if (p.cdvw > 1) {
+                            ok = ok && w >= 0 && w % p.cdvw == 0;
+                            w /= p.cdvw;
+                        }
+                        ok = ok && h >= 0 && h < p.cH && w >= 0 && w < p.cW;
+                        const uint8_t* src =
+                            ok ? pix[i] + (static_cast<int64_t>(h) * p.cW + w) * rowbytes + cbyte : p.cx;
+                        const uint32_t nbytes = ok ? 16u : 0u;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        ptx::cp_async16_zfill(sbase + row * 128 + ((j ^ (row & 7)) << 4), src + 16 * j, nbytes);
+                        for (int j = 0; j < 8; ++j)
+                            ptx::cp_async16_zfill(sbase + row * 128 + ((j ^ (row & 7)) << 4), src + 16 * j,
+                                                  nbytes);
+                    }
+                } else {
+                    constexpr int kRows = kI8 ? 4 : 2;  // K-rows (pixels) per lane per stage
+                    int kh[kRows], kw[kRows];
+                    const uint8_t* kpix[kRows];
+                    bool kok[kRows];
+#pragma unroll
+                    for (int i = 0; i < kRows; ++i) {
+                        const int64_t m = static_cast<int64_t>(kb) * bk_elems + lane + 32 * i;
+                        kok[i] = m < K;
+                        const int mm = kok[i] ? static_cast<int>(m) : 0;
+                        const int q = mm % p.cQ, pp = (mm / p.cQ) % p.cP, n = mm / (p.cQ * p.cP);
+                        kh[i] = pp * p.csh - p.cph;
+                        kw[i] = q * p.csw - p.cpw;
+                        kpix[i] = p.cx + static_cast<int64_t>(n) * img;
+                    }
+#pragma unroll 1
+                    for (int j = 0; j < kBRows / 64; ++j) {
+                        const int col = n0 + 64 * j;  // first (r,s,c) column of this block
+                        const int kbyte = col * eb;
+                        const int tap = kbyte / rowbytes;
+                        const int cbyte = kbyte - tap * rowbytes;
+                        const int r = tap / p.cS, sx = tap - r * p.cS;
+                        const uint32_t sbase = ptx::smem_u32(sb + j * bk_elems * 128);
+#pragma unroll
+                        for (int i = 0; i < kRows; ++i) {
+                            const int row = lane + 32 * i;
+                            const int h = kh[i] + r, w = kw[i] + sx;
+                            const bool ok = kok[i] && col < N && h >= 0 && h < p.cH && w >= 0 && w < p.cW;
+                            const uint8_t* src =
+                                ok ? kpix[i] + (static_cast<int64_t>(h) * p.cW + w) * rowbytes + cbyte : p.cx;
+                            const uint32_t nbytes = ok ? 16u : 0u;
+#pragma unroll
+                            for (int c = 0; c < 8; ++c)
+                                ptx::cp_async16_zfill(sbase + row * 128 + ((c ^ (row & 7)) << 4), src + 16 * c,
+                                                      nbytes);
+                        }
+                    }
                 }
                 ptx::cp_async_mbar_arrive_noinc(&full[stage]);
                 if (++stage == kStages) {
@@ -258,6 +336,50 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                       kb * bk_elems);
                         } else {
                             ptx::tma_load_2d_pair(sb, &tm_b, fb, kb * bk_elems, n0);
+                        }
+                    } else if (kLay & 96) {
+                        // TMA im2col (implicit-GEMM conv): the hardware walks the
+                        // NHWC bounding box, padding taps come back as zeros.
+                        uint8_t* sa = smem_a + stage * BM * BK_BYTES;
+                        uint8_t* sb = smem_b + stage * kBRows * BK_BYTES;
+                        const int eb = kI8 ? 1 : 2;
+                        const int rowbytes = p.cC * eb;
+                        if (kLay & 32) {  // A = column tile of 128 output pixels from m0
+                            ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                            const int kbyte = kb * BK_BYTES;
+                            const int tap = kbyte / rowbytes;
+                            const int c0 = (kbyte - tap * rowbytes) / eb;
+                            const int r = tap / p.cS, sx = tap - r * p.cS;
+                            const int q = m0 % p.cQ, pp = (m0 / p.cQ) % p.cP, n = m0 / (p.cQ * p.cP);
+                            ptx::tma_load_im2col_4d(sa, &tm_a, &full[stage], c0, q * p.csw - p.cpw,
+                                                    pp * p.csh - p.cph, n, static_cast<uint16_t>(sx),
+                                                    static_cast<uint16_t>(r));
+                            if (kLay & 16) {  // dgrad: W [Cout][R*S][C], taps flipped
+                                const int kk = kb * bk_elems;
+                                const int rs = p.cS * (p.K / p.cC / p.cS) - 1 - kk / p.cC;
+                                for (int j = 0; j < kBRows / 64; ++j)
+                                    ptx::tma_load_3d(sb + j * bk_elems * 128, &tm_b, &full[stage], n0 + 64 * j,
+                                                     kk % p.cC, rs);
+                            } else {
+                                ptx::tma_load_2d(sb, &tm_b, &full[stage], kb * bk_elems, n0);
+                            }
+                        } else {  // wgrad: A = dY (MN-major), B = column blocks, K rows = pixels
+                            const int nblk = min(kBRows / 64, static_cast<int>((N - n0 + 63) / 64));
+                            ptx::mbar_arrive_expect_tx(&full[stage], BM * BK_BYTES + nblk * bk_elems * 128);
+                            for (int j = 0; j < BM / 64; ++j)
+                                ptx::tma_load_2d(sa + j * bk_elems * 128, &tm_a, &full[stage], m0 + 64 * j,
+                                                 kb * bk_elems);
+                            const int pix = kb * bk_elems;
+                            const int q = pix % p.cQ, pp = (pix / p.cQ) % p.cP, n = pix / (p.cQ * p.cP);
+                            for (int j = 0; j < nblk; ++j) {
+                                const int kbyte = (n0 + 64 * j) * eb;
+                                const int tap = kbyte / rowbytes;
+                                const int c0 = (kbyte - tap * rowbytes) / eb;
+                                const int r = tap / p.cS, sx = tap - r * p.cS;
+                                ptx::tma_load_im2col_4d(sb + j * bk_elems * 128, &tm_b, &full[stage], c0,
+                                                        q * p.csw - p.cpw, pp * p.csh - p.cph, n,
+                                                        static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+                            }
                         }
                     } else {
                         ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
@@ -302,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&full[stage], phase);
                     // cp.async (generic proxy) wrote A: order it before the
                     // tensor core's async-proxy reads.
-                    if (kLay & 4) ptx::fence_proxy_async_smem();
+                    if (kLay & 12) ptx::fence_proxy_async_smem();
                     ptx::tc_fence_after();
                     const uint32_t a_addr = ptx::smem_u32(smem_a + stage * BM * BK_BYTES);
                     const uint32_t b_addr = ptx::smem_u32(smem_b + stage * kBRows * BK_BYTES);
@@ -598,6 +720,72 @@ int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t
     return QSYNC_OK;
 }
 
+// 3-D map: dims (inner, d1, d2) with byte strides (s1, s2) for d1, d2 (any
+// order), box (box_inner, box_1, 1).
+int make_map_3d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes,
+                int64_t inner, int64_t d1, int64_t d2, int64_t s1, int64_t s2, uint32_t box_inner,
+                uint32_t box_1) {
+    EncodeFn fn = encode_fn();
+    QSB_REQUIRE(fn != nullptr, QSYNC_ERR_INTERNAL, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(d1),
+                          static_cast<cuuint64_t>(d2)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(s1), static_cast<cuuint64_t>(s2)};
+    cuuint32_t box[3] = {box_inner, box_1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    (void)elem_bytes;
+    CUresult r = fn(map, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    QSB_REQUIRE(r == CUDA_SUCCESS, QSYNC_ERR_INTERNAL,
+                "cuTensorMapEncodeTiled (3-D) failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return QSYNC_OK;
+}
+
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+    static EncodeIm2colFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeIm2colFn>(f);
+    });
+    return fn;
+}
+
+// im2col map over the NHWC tensor the conv gathers from (p.cx geometry): dims
+// {C, W, H, N}; the bounding box spans input coordinates [-pad, dim-1+pad-(k-1)]
+// walked with the conv strides, so consecutive box pixels are consecutive GEMM
+// rows (n, p, q); `pixels` rows of 128 bytes per load, 128B-swizzled.
+int make_im2col_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t eb, const EpiParams& p,
+                    uint32_t pixels) {
+    EncodeIm2colFn fn = encode_im2col_fn();
+    QSB_REQUIRE(fn != nullptr, QSYNC_ERR_INTERNAL, "cuTensorMapEncodeIm2col unavailable");
+    const int R = static_cast<int>(p.cR), S = p.cS;
+    QSB_REQUIRE(p.cpw <= 127 && p.cph <= 127 && p.cpw - (S - 1) >= -128 && p.cph - (R - 1) >= -128 &&
+                    p.csw <= 8 && p.csh <= 8 && R <= 65535 && S <= 65535,
+                QSYNC_ERR_DOMAIN, "conv geometry outside the TMA im2col range");
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(p.cC), static_cast<cuuint64_t>(p.cW),
+                          static_cast<cuuint64_t>(p.cH), static_cast<cuuint64_t>(p.cN)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(p.cC) * eb, static_cast<cuuint64_t>(p.cW) * p.cC * eb,
+                             static_cast<cuuint64_t>(p.cH) * p.cW * p.cC * eb};
+    int lower[2] = {-p.cpw, -p.cph};
+    int upper[2] = {p.cpw - (S - 1), p.cph - (R - 1)};
+    cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(p.csw), static_cast<cuuint32_t>(p.csh), 1};
+    CUresult r = fn(map, dt, 4, const_cast<void*>(ptr), dims, strides, lower, upper, BK_BYTES / eb, pixels, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    QSB_REQUIRE(r == CUDA_SUCCESS, QSYNC_ERR_INTERNAL,
+                "cuTensorMapEncodeIm2col failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return QSYNC_OK;
+}
+
 // Instruction descriptor (tcgen05 "idesc"): c_format [4,6), a_format [7,10),
 // b_format [10,13), a/b major [15],[16] (0 = K-major), N>>3 [17,23), M>>4 [24,29).
 uint32_t make_idesc(bool i8, bool bf16, int n, int m, int lay = 0, bool fp8 = false) {
@@ -620,6 +808,7 @@ int g_force_cta = 0;     // test/bench hook (qsync_gemm_force_cta): 0 = cost mod
 int g_debug_epi = 0;     // bench hook (qsync_gemm_debug_epilogue)
 int g_pdl = 1;           // programmatic dependent launch (qsync_gemm_set_pdl)
 int g_max_ctas = 0;      // cap on the persistent grid (qsync_gemm_set_max_ctas), 0 = all SMs
+int g_conv_tma = 1;      // implicit conv operand loads: 1 = TMA im2col, 0 = cp.async gather lanes
 
 template <bool kI8, int BN, int kCta, int kLay>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
@@ -629,11 +818,20 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     CUtensorMap ma, mb, mc;
     if (kLay & 4)  // implicit conv: A is gathered by the producer lanes
         std::memset(&ma, 0, sizeof(ma));
+    else if (kLay & 32)  // A = im2col view of the NHWC input, 128 pixels x 128 bytes
+        QSB_TRY(make_im2col_map(&ma, a, dt, eb, p, BM));
     else if (kLay & 1)  // A stored [K, M]: boxes of 64 M-elements x box_k K-rows
         QSB_TRY(make_map(&ma, a, dt, eb, p.M, p.K, 64, box_k));
     else
         QSB_TRY(make_map(&ma, a, dt, eb, p.K, p.M, box_k, BM));
-    if (kLay & 2)
+    if (kLay & 8)  // implicit wgrad: B is gathered by the producer lanes
+        std::memset(&mb, 0, sizeof(mb));
+    else if (kLay & 64)  // wgrad B = im2col view of the input, bk pixels x 128 bytes
+        QSB_TRY(make_im2col_map(&mb, b, dt, eb, p, box_k));
+    else if (kLay & 16)  // dgrad weights W [Cout][R*S][C] as the MN-major B [(rs, k), c]
+        QSB_TRY(make_map_3d(&mb, b, dt, eb, p.N, p.cC, p.K / p.cC,
+                            (p.K / p.cC) * p.N * eb, static_cast<int64_t>(p.N) * eb, 64, box_k));
+    else if (kLay & 2)
         QSB_TRY(make_map(&mb, b, dt, eb, p.N, p.K, 64, box_k));
     else
         QSB_TRY(make_map(&mb, b, dt, eb, p.K, p.N, box_k, C::kBRows));
@@ -779,14 +977,41 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     if (sh.cta == 2 && sh.bn == 64) sh.cta = 1;  // pair tiles need BN/2 >= 64 rows of B
     p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout, p.fp8);
     p.debug_epi = g_debug_epi;
-    if (layout == 4) {  // implicit conv: single-CTA tiles
+    if (layout & 108) {  // implicit conv (fwd 4/32, dgrad 22/50, wgrad 11/67): single-CTA tiles
         sh.cta = 1;
-        p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM, 0, p.fp8);
-        switch (sh.bn) {
-            case 256: return launch<kI8, 256, 1, 4>(a, b, dt, p, st);
-            case 128: return launch<kI8, 128, 1, 4>(a, b, dt, p, st);
-            default: return launch<kI8, 64, 1, 4>(a, b, dt, p, st);
+        p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM, layout & 3, p.fp8);
+        if (layout == 4) {
+            switch (sh.bn) {
+                case 256: return launch<kI8, 256, 1, 4>(a, b, dt, p, st);
+                case 128: return launch<kI8, 128, 1, 4>(a, b, dt, p, st);
+                default: return launch<kI8, 64, 1, 4>(a, b, dt, p, st);
+            }
         }
+        if (layout == 32) {
+            switch (sh.bn) {
+                case 256: return launch<kI8, 256, 1, 32>(a, b, dt, p, st);
+                case 128: return launch<kI8, 128, 1, 32>(a, b, dt, p, st);
+                default: return launch<kI8, 64, 1, 32>(a, b, dt, p, st);
+            }
+        }
+        if (kI8) return set_error(QSYNC_ERR_DOMAIN, "implicit conv backward is FP16/BF16 only");
+        if (layout == 22) {
+            switch (sh.bn) {
+                case 256: return launch<false, 256, 1, 22>(a, b, dt, p, st);
+                case 128: return launch<false, 128, 1, 22>(a, b, dt, p, st);
+                default: return launch<false, 64, 1, 22>(a, b, dt, p, st);
+            }
+        }
+        if (layout == 50) {
+            switch (sh.bn) {
+                case 256: return launch<false, 256, 1, 50>(a, b, dt, p, st);
+                case 128: return launch<false, 128, 1, 50>(a, b, dt, p, st);
+                default: return launch<false, 64, 1, 50>(a, b, dt, p, st);
+            }
+        }
+        if (layout == 11) return launch<false, 256, 1, 11>(a, b, dt, p, st);
+        if (layout == 67) return launch<false, 256, 1, 67>(a, b, dt, p, st);
+        return set_error(QSYNC_ERR_DOMAIN, "unsupported implicit conv layout " + std::to_string(layout));
     }
     if (kI8) return dispatch_shape<kI8, 0>(a, b, dt, p, st, sh);
     switch (layout) {
@@ -834,6 +1059,11 @@ int qsync_gemm_force_splitk(int ks) {
 int qsync_gemm_set_max_ctas(int n) {
     QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "CTA cap must be >= 0");
     g_max_ctas = n;
+    return QSYNC_OK;
+}
+
+int qsync_conv_set_impl(int tma) {
+    g_conv_tma = tma ? 1 : 0;
     return QSYNC_OK;
 }
 
@@ -959,17 +1189,103 @@ int qsync_conv_fwd_implicit(const void* x, int dtype, int64_t N, int64_t H, int6
     p.cx = static_cast<const uint8_t*>(x);
     p.cN = static_cast<int>(N); p.cH = static_cast<int>(H); p.cW = static_cast<int>(W);
     p.cC = static_cast<int>(C); p.cP = static_cast<int>(P); p.cQ = static_cast<int>(Q);
-    p.cS = S; p.csh = sh; p.csw = sw; p.cph = ph; p.cpw = pw;
+    p.cR = R; p.cS = S; p.csh = sh; p.csw = sw; p.cph = ph; p.cpw = pw;
+    p.ctap = 1; p.cdvh = 1; p.cdvw = 1;
+    const int lay = g_conv_tma ? 32 : 4;
     if (dtype == QSYNC_I8) {
         QSB_REQUIRE(scale_a && scale_b, QSYNC_ERR_VALIDATION, "the dequant epilogue needs scale_a and scale_b");
         p.scale_a = scale_a;
         p.scale_b = scale_b;
         p.b_per_channel = b_per_channel;
-        return dispatch<true>(x, w, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, to_stream(stream), g_force_bn, 4);
+        return dispatch<true>(x, w, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, to_stream(stream), g_force_bn, lay);
     }
     const CUtensorMapDataType dt =
         dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    return dispatch<false>(x, w, dt, p, to_stream(stream), g_force_bn, 4);
+    return dispatch<false>(x, w, dt, p, to_stream(stream), g_force_bn, lay);
+}
+
+int qsync_conv_dgrad_implicit(const void* dy, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int R,
+                              int S, int sh, int sw, int ph, int pw, const void* w, int64_t cout, void* dx,
+                              int dx_dtype, qsync_stream_t stream) {
+    QSB_REQUIRE(dy && w && dx, QSYNC_ERR_VALIDATION, "implicit conv dgrad needs dy, w and dx");
+    QSB_REQUIRE(dtype == QSYNC_F16 || dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
+                "implicit conv dgrad operands must be F16 or BF16");
+    QSB_REQUIRE(N > 0 && H > 0 && W > 0 && C > 0 && R > 0 && S > 0 && sh > 0 && sw > 0 && ph >= 0 && pw >= 0,
+                QSYNC_ERR_DOMAIN, "bad conv geometry");
+    QSB_REQUIRE((cout * 2) % BK_BYTES == 0, QSYNC_ERR_DOMAIN,
+                "implicit conv dgrad needs Cout % 64 == 0 (use col2im)");
+    QSB_REQUIRE(C % 8 == 0, QSYNC_ERR_DOMAIN, "implicit conv dgrad needs C % 8 == 0 (16-byte weight rows)");
+    const int64_t P = (H + 2 * ph - R) / sh + 1, Q = (W + 2 * pw - S) / sw + 1;
+    QSB_REQUIRE(P > 0 && Q > 0, QSYNC_ERR_DOMAIN, "conv output would be empty");
+    const int64_t M = N * H * W, K = static_cast<int64_t>(R) * S * cout;
+    QSB_REQUIRE(M < (int64_t(1) << 31) && N * P * Q * cout * 2 < (int64_t(1) << 40), QSYNC_ERR_DOMAIN,
+                "conv too large");
+    QSB_REQUIRE((reinterpret_cast<uintptr_t>(dy) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0,
+                QSYNC_ERR_DOMAIN, "implicit conv operands must be 16-byte aligned");
+    QSB_REQUIRE(dx_dtype == QSYNC_F32 || dx_dtype == QSYNC_F16 || dx_dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
+                "conv dgrad output must be F32, F16 or BF16");
+    // dX[(n,h,w), c] = sum_{r,s,k} dY[n, (h+ph-r)/sh, (w+pw-s)/sw, k] W[k,r,s,c]
+    // (terms whose numerators are off the stride grid or out of range vanish).
+    EpiParams p{};
+    p.M = M;
+    p.N = C;
+    p.K = K;
+    p.c = dx;
+    p.c_dtype = dx_dtype;
+    p.alpha = 1.0f;
+    p.cx = static_cast<const uint8_t*>(dy);
+    p.cN = static_cast<int>(N); p.cH = static_cast<int>(P); p.cW = static_cast<int>(Q);
+    p.cC = static_cast<int>(cout); p.cP = static_cast<int>(H); p.cQ = static_cast<int>(W);
+    p.cR = R; p.cS = S; p.csh = 1; p.csw = 1;
+    const CUtensorMapDataType dt =
+        dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    if (g_conv_tma && sh == 1 && sw == 1) {
+        // a stride-1 conv of dY with pad (k-1-p) and flipped taps: TMA im2col
+        p.cph = R - 1 - ph; p.cpw = S - 1 - pw;
+        p.ctap = 1; p.cdvh = 1; p.cdvw = 1;
+        return dispatch<false>(dy, w, dt, p, to_stream(stream), g_force_bn, 50);
+    }
+    p.cph = -ph; p.cpw = -pw;
+    p.ctap = -1; p.cdvh = sh; p.cdvw = sw;
+    return dispatch<false>(dy, w, dt, p, to_stream(stream), g_force_bn, 22);
+}
+
+int qsync_conv_wgrad_implicit(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int R,
+                              int S, int sh, int sw, int ph, int pw, const void* dy, int64_t cout, float* dw,
+                              float alpha, const float* alpha_dev, int accumulate, qsync_stream_t stream) {
+    QSB_REQUIRE(x && dy && dw, QSYNC_ERR_VALIDATION, "implicit conv wgrad needs x, dy and dw");
+    QSB_REQUIRE(dtype == QSYNC_F16 || dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
+                "implicit conv wgrad operands must be F16 or BF16");
+    QSB_REQUIRE(N > 0 && H > 0 && W > 0 && C > 0 && R > 0 && S > 0 && sh > 0 && sw > 0 && ph >= 0 && pw >= 0,
+                QSYNC_ERR_DOMAIN, "bad conv geometry");
+    QSB_REQUIRE((C * 2) % BK_BYTES == 0, QSYNC_ERR_DOMAIN,
+                "implicit conv wgrad needs C % 64 == 0 (use im2col)");
+    QSB_REQUIRE(cout % 8 == 0, QSYNC_ERR_DOMAIN, "implicit conv wgrad needs Cout % 8 == 0");
+    const int64_t P = (H + 2 * ph - R) / sh + 1, Q = (W + 2 * pw - S) / sw + 1;
+    QSB_REQUIRE(P > 0 && Q > 0, QSYNC_ERR_DOMAIN, "conv output would be empty");
+    const int64_t M = cout, K = N * P * Q, Ncol = static_cast<int64_t>(R) * S * C;
+    QSB_REQUIRE(K < (int64_t(1) << 31) && N * H * W * C * 2 < (int64_t(1) << 40), QSYNC_ERR_DOMAIN,
+                "conv too large");
+    QSB_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0,
+                QSYNC_ERR_DOMAIN, "implicit conv operands must be 16-byte aligned");
+    // dW[k, (r,s,c)] (+)= alpha * sum_{(n,p,q)} dY[(n,p,q), k] x[n, p*sh-ph+r, q*sw-pw+s, c]
+    EpiParams p{};
+    p.M = M;
+    p.N = Ncol;
+    p.K = K;
+    p.c = dw;
+    p.c_dtype = QSYNC_F32;
+    p.alpha = alpha;
+    p.alpha_dev = alpha_dev;
+    p.accumulate = accumulate;
+    p.cx = static_cast<const uint8_t*>(x);
+    p.cN = static_cast<int>(N); p.cH = static_cast<int>(H); p.cW = static_cast<int>(W);
+    p.cC = static_cast<int>(C); p.cP = static_cast<int>(P); p.cQ = static_cast<int>(Q);
+    p.cR = R; p.cS = S; p.csh = sh; p.csw = sw; p.cph = ph; p.cpw = pw;
+    p.ctap = 1; p.cdvh = 1; p.cdvw = 1;
+    const CUtensorMapDataType dt =
+        dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    return dispatch<false>(dy, x, dt, p, to_stream(stream), 256, g_conv_tma ? 67 : 11);
 }
 
 int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,

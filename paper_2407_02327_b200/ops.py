@@ -314,6 +314,64 @@ def conv_fwd_implicit(x: torch.Tensor, w2: torch.Tensor, R: int, S: int, stride,
     return y, (P, Q)
 
 
+def implicit_dgrad_ok(C: int, cout: int, stride=(1, 1)) -> bool:
+    """Whether qconv takes the implicit-GEMM dgrad: dY channel runs of 128 B,
+    16-byte weight rows, and stride 1 -- a strided conv's dgrad is a fractionally
+    strided gather (the cp.async lanes zero 3 of 4 taps at stride 2, measured
+    slower than dY W + col2im), so it keeps the column path."""
+    return cout % 64 == 0 and C % 8 == 0 and tuple(stride) == (1, 1)
+
+
+def conv_set_impl(tma: bool) -> None:
+    """Implicit-conv operand loads: TMA im2col mode (default) or the cp.async
+    gather lanes (A/B and the strided dgrad, which TMA im2col cannot express)."""
+    call("qsync_conv_set_impl", int(bool(tma)))
+
+
+def implicit_wgrad_ok(C: int) -> bool:
+    """Whether the implicit-GEMM wgrad applies (FP16 channel runs of 128 B)."""
+    return C % 64 == 0
+
+
+def conv_dgrad_implicit(dy: torch.Tensor, w: torch.Tensor, xshape, stride, pad,
+                        out_dtype=torch.float32) -> torch.Tensor:
+    """Implicit-GEMM Conv2d dgrad: dy NHWC [N,P,Q,Cout] FP16, w [Cout,R,S,C] FP16 ->
+    dx NHWC [N,H,W,C] out_dtype.  dY taps are gathered by the GEMM's producer warp
+    (no column-gradient matrix, no col2im)."""
+    _req(dy, "dy", (torch.float16, torch.bfloat16))
+    _req(w, "w", (dy.dtype,))
+    N, H, W, C = xshape
+    cout, R, S, _ = w.shape
+    dx = torch.empty((N, H, W, C), device=dy.device, dtype=out_dtype)
+    ev = _timed("gemm_f16", 2.0 * N * H * W * C * R * S * cout)
+    call("qsync_conv_dgrad_implicit", _ptr(dy), _DT_CAST[dy.dtype], N, H, W, C, R, S, stride[0], stride[1],
+         pad[0], pad[1], _ptr(w), cout, _ptr(dx), _DT[out_dtype], _stream())
+    if ev is not None:
+        ev.record()
+    return dx
+
+
+def conv_wgrad_implicit(x: torch.Tensor, dy: torch.Tensor, R: int, S: int, stride, pad, out=None,
+                        accumulate: bool = False, alpha: float = 1.0, alpha_dev=None) -> torch.Tensor:
+    """Implicit-GEMM Conv2d wgrad: x NHWC FP16 [N,H,W,C], dy [N*P*Q, Cout] FP16 ->
+    dw FP32 [Cout, R*S*C] (+)= alpha * dY^T A, the column matrix A gathered from x
+    by the GEMM's producer warp."""
+    _req(x, "x", (torch.float16, torch.bfloat16))
+    _req(dy, "dy", (x.dtype,))
+    N, H, W, C = x.shape
+    cout = dy.shape[-1]
+    P, Q = conv_out_size(H, W, R, S, stride, pad)
+    if out is None:
+        out = (torch.zeros if accumulate else torch.empty)((cout, R * S * C), device=x.device,
+                                                           dtype=torch.float32)
+    ev = _timed("gemm_f16", 2.0 * N * P * Q * cout * R * S * C)
+    call("qsync_conv_wgrad_implicit", _ptr(x), _DT_CAST[x.dtype], N, H, W, C, R, S, stride[0], stride[1],
+         pad[0], pad[1], _ptr(dy), cout, _ptr(out), float(alpha), _ptr(alpha_dev), int(accumulate), _stream())
+    if ev is not None:
+        ev.record()
+    return out
+
+
 def col2im(dcol: torch.Tensor, xshape, R: int, S: int, stride, pad, dil=(1, 1)) -> torch.Tensor:
     """Adjoint of im2col: dx NHWC FP32 from the column gradient (FP32 or FP16)."""
     _req(dcol, "dcol", (torch.float32, torch.float16))

@@ -11,10 +11,12 @@ producer warp gathers it tile by tile from the NHWC input (implicit GEMM,
             dequant + bias epilogue -> FP32 NHWC output (graph.hpp:38-40).
   * FP16 -- FP16 im2col, tcgen05 kind::f16 GEMM -> FP16 NHWC output.
   * FP32 -- cuDNN-free FP32 path via torch (training devices stay FP32).
-Backward of INT8/FP16 runs in FP16 (cost_mapper.cpp:13-15): dgrad = col2im(dY16 W16)
-(deterministic gather, FP32), wgrad = dY16^T A16 (times s_x for INT8) in FP32
-(cost_mapper.cpp:48-50).  The INT8 op keeps only its int8 input for backward and
-rebuilds the column matrix there (the paper's backward casting cost).
+Backward of INT8/FP16 runs in FP16 (cost_mapper.cpp:13-15): dgrad = the implicit
+GEMM over dY taps (`qsync_conv_dgrad_implicit`, Cout % 64 == 0) or col2im(dY16 W16),
+FP32 out; wgrad = dY16^T A16 (times s_x for INT8) in FP32 (cost_mapper.cpp:48-50),
+A16 gathered from the FP16 input by the GEMM (`qsync_conv_wgrad_implicit`, C % 64
+== 0) or rebuilt by im2col.  The INT8 op keeps only its int8 input for backward
+and widens it there (the paper's backward casting cost).
 """
 from __future__ import annotations
 
@@ -77,22 +79,40 @@ class _QConv(torch.autograd.Function):
         kp = ctx.kp
         dy2 = dy.reshape(N * P * Q, cout).contiguous()
         dy16, _, db = ops.cast_transpose(dy2, True, False, ctx.has_bias)
-        w16 = ops.cast(_pad_k(ctx.w_ref.detach().reshape(cout, K), kp), torch.float16)
-        # dgrad columns = dY16 W16 (W16 [Cout, kp] read as an MN-major B operand)
-        dcol = ops.gemm_f16(dy16, w16, out_dtype=torch.float32, b_mn=True)
-        dx = ops.col2im(dcol, (N, H, W, C), R, S, stride, pad)
-        # wgrad = dY16^T A16 (both read MN-major): rebuild the FP16 column matrix
-        # from the saved (int8 / fp16) input.
-        A, _ = ops.im2col(xs_saved, R, S, stride, pad, ld=kp)
-        A16 = A if A.dtype == torch.float16 else ops.cast(A, torch.float16)
-        # K of this GEMM is the pixel count (up to N*P*Q = 802,816 for conv1) while
-        # M x N is tiny: accumulate into a zeroed FP32 buffer so the kernel
+        w_fp = ctx.w_ref.detach()
+        dx = None
+        if ctx.needs_input_grad[0]:
+            if ops.implicit_dgrad_ok(C, cout, stride):
+                # implicit dgrad: dY taps gathered by the GEMM producer, weights
+                # read in place as [Cout][R*S][C] -- no column gradient, no col2im
+                w16 = ops.cast(w_fp.contiguous(), torch.float16)
+                dx = ops.conv_dgrad_implicit(dy16.view(N, P, Q, cout), w16, (N, H, W, C), stride, pad)
+            else:
+                # dgrad columns = dY16 W16 (W16 [Cout, kp] read as an MN-major B operand)
+                w16 = ops.cast(_pad_k(w_fp.reshape(cout, K), kp), torch.float16)
+                dcol = ops.gemm_f16(dy16, w16, out_dtype=torch.float32, b_mn=True)
+                dx = ops.col2im(dcol, (N, H, W, C), R, S, stride, pad)
+        alpha_dev = alpha if ctx.precision == INT8 else None
+        # K of the wgrad GEMM is the pixel count (up to N*P*Q = 802,816 for conv1)
+        # while M x N is tiny: accumulate into a zeroed FP32 buffer so the kernel
         # splits K across the SMs (partials reduce-added by TMA).
         dw2 = torch.zeros((cout, kp), device=dy.device, dtype=torch.float32)
-        ops.gemm_f16(dy16, A16, out=dw2, accumulate=True, a_mn=True, b_mn=True,
-                     alpha_dev=alpha if ctx.precision == INT8 else None)
+        if ops.implicit_wgrad_ok(C) and kp == K:
+            # implicit wgrad = dY16^T A16 with A16 gathered from the FP16 input
+            # (the INT8 op's saved int8 input widened once: N*H*W*C, not R*S x that)
+            x16 = xs_saved if xs_saved.dtype == torch.float16 else ops.cast(xs_saved, torch.float16)
+            ops.conv_wgrad_implicit(x16, dy16, R, S, stride, pad, out=dw2, accumulate=True,
+                                    alpha_dev=alpha_dev)
+        else:
+            # wgrad = dY16^T A16 (both read MN-major): rebuild the FP16 column matrix
+            # from the saved (int8 / fp16) input.
+            # from the saved input, widened to FP16 first (N*H*W*C elements, not
+            # the R*S times larger column matrix).
+            x16 = xs_saved if xs_saved.dtype == torch.float16 else ops.cast(xs_saved, torch.float16)
+            A16, _ = ops.im2col(x16, R, S, stride, pad, ld=kp)
+            ops.gemm_f16(dy16, A16, out=dw2, accumulate=True, a_mn=True, b_mn=True, alpha_dev=alpha_dev)
         dw = dw2[:, :K].reshape(ctx.w_ref.shape)
-        if ctx.x_dtype != torch.float32:
+        if dx is not None and ctx.x_dtype != torch.float32:
             dx = dx.to(ctx.x_dtype)
         return dx, dw, db, None, None
 

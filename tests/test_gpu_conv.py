@@ -13,6 +13,14 @@ DEV = "cuda"
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(params=[1, 0], ids=["tma_im2col", "gather"])
+def conv_impl(request):
+    """Both implicit-conv operand loaders: TMA im2col mode and cp.async lanes."""
+    ops.conv_set_impl(request.param)
+    yield request.param
+    ops.conv_set_impl(1)
+
 # (N, H, W, C, Cout, R, stride, pad): stem 7x7/2, res2 3x3, res3 1x1/2 downsample, res5 3x3
 CASES = [(1, 32, 32, 3, 64, 7, 2, 3), (2, 14, 14, 64, 64, 3, 1, 1), (2, 28, 28, 128, 256, 1, 2, 0),
          (2, 7, 7, 512, 512, 3, 1, 1), (3, 9, 11, 16, 48, 3, 2, 1)]
@@ -110,7 +118,7 @@ def test_fp16_conv_vs_torch_fp32(case):
 @pytest.mark.parametrize("geom", [(2, 14, 14, 128, 256, 3, 1, 1), (2, 15, 15, 128, 128, 3, 2, 1),
                                   (3, 7, 7, 256, 512, 1, 1, 0), (1, 28, 28, 128, 64, 1, 2, 0),
                                   (2, 9, 11, 128, 200, 3, 1, 1)])
-def test_implicit_conv_int8_bit_exact_vs_im2col(geom):
+def test_implicit_conv_int8_bit_exact_vs_im2col(geom, conv_impl):
     """Implicit-GEMM forward (A gathered by the producer warp) == im2col + GEMM:
     same int8 operands, same K order -> identical int32 accumulators and epilogue."""
     N, H, W, C, Co, R, st, pd = geom
@@ -130,7 +138,7 @@ def test_implicit_conv_int8_bit_exact_vs_im2col(geom):
 
 @pytest.mark.parametrize("geom", [(2, 14, 14, 64, 256, 3, 1, 1), (2, 28, 28, 128, 128, 3, 2, 1),
                                   (4, 7, 7, 64, 96, 1, 1, 0)])
-def test_implicit_conv_fp16_matches_im2col(geom):
+def test_implicit_conv_fp16_matches_im2col(geom, conv_impl):
     N, H, W, C, Co, R, st, pd = geom
     torch.manual_seed(sum(geom))
     x = torch.randn(N, H, W, C, device=DEV).half()
@@ -141,8 +149,132 @@ def test_implicit_conv_fp16_matches_im2col(geom):
     assert torch.equal(y, y_ref)  # same operands, same K order, same accumulation
 
 
+@pytest.mark.parametrize("geom", [(2, 10, 13, 128, 128, 1, 3, 1, 2, 0, 1), (1, 12, 9, 64, 64, 3, 1, 2, 1, 1, 0),
+                                  (2, 11, 11, 128, 256, 5, 5, 2, 2, 2, 2)])
+def test_implicit_conv_asymmetric_geometry(geom, conv_impl):
+    """R != S, different strides and pads per axis: the TMA im2col map's W/H
+    ordering and bounding box match im2col (oracle-pinned) bit for bit."""
+    N, H, W, C, Co, R, S, sh, sw, ph, pw = geom
+    torch.manual_seed(sum(geom))
+    x = torch.randn(N, H, W, C, device=DEV).half()
+    w2 = (torch.randn(Co, R * S * C, device=DEV) / (R * S * C) ** 0.5).half()
+    y, (P, Q) = ops.conv_fwd_implicit(x, w2, R, S, (sh, sw), (ph, pw), out_dtype=torch.float16)
+    A, (P2, Q2) = ops.im2col(x, R, S, (sh, sw), (ph, pw))
+    assert (P, Q) == (P2, Q2)
+    assert torch.equal(y, ops.gemm_f16(A, w2, out_dtype=torch.float16))
+    dy = torch.randn(N, P, Q, Co, device=DEV).half()
+    wt = w2.view(Co, R, S, C)
+    xt = x.double().permute(0, 3, 1, 2).requires_grad_(True)
+    wd = wt.double().permute(0, 3, 1, 2).requires_grad_(True)
+    torch.nn.functional.conv2d(xt, wd, None, (sh, sw), (ph, pw)).backward(dy.double().permute(0, 3, 1, 2))
+    dx = ops.conv_dgrad_implicit(dy, wt, (N, H, W, C), (sh, sw), (ph, pw))
+    assert _nrel(dx, xt.grad.permute(0, 2, 3, 1)) < 1e-5
+    dw = ops.conv_wgrad_implicit(x, dy.view(-1, Co), R, S, (sh, sw), (ph, pw))
+    assert _nrel(dw.view(Co, R, S, C), wd.grad.permute(0, 2, 3, 1)) < 1e-5
+
+
 def test_implicit_conv_rejects_narrow_channels():
     x = torch.zeros(1, 8, 8, 3, dtype=torch.int8, device=DEV)
     w2 = torch.zeros(16, 27, dtype=torch.int8, device=DEV)
     with pytest.raises(Exception, match="128 bytes"):
         ops.conv_fwd_implicit(x, w2, 3, 3, (1, 1), (1, 1), torch.ones(1, device=DEV), torch.ones(16, device=DEV))
+
+
+DGRAD_GEOMS = [(2, 14, 14, 64, 64, 3, 1, 1), (2, 15, 15, 128, 128, 3, 2, 1), (2, 16, 16, 64, 128, 3, 2, 1),
+               (1, 28, 28, 256, 128, 1, 2, 0), (3, 7, 7, 200, 64, 1, 1, 0), (2, 9, 11, 24, 192, 3, 1, 1),
+               (1, 32, 32, 3, 64, 7, 2, 3)]
+
+
+def _f64_conv_grads(x16, w16, dy16, st, pd):
+    """Float64 autograd of conv2d on the FP16 values (the GEMMs accumulate
+    exact FP16 products in FP32: tolerance 1e-5 relative to the norm)."""
+    xt = x16.double().permute(0, 3, 1, 2).requires_grad_(True)
+    wt = w16.double().permute(0, 3, 1, 2).requires_grad_(True)
+    y = torch.nn.functional.conv2d(xt, wt, None, st, pd)
+    y.backward(dy16.double().permute(0, 3, 1, 2))
+    return xt.grad.permute(0, 2, 3, 1), wt.grad.permute(0, 2, 3, 1)
+
+
+def _nrel(a, b):
+    return float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("geom", DGRAD_GEOMS)
+def test_implicit_dgrad_vs_f64(geom, conv_impl):
+    """Implicit dgrad (dY taps gathered by the producer warp, W read in place
+    through a 3-D TMA map) == conv2d's input gradient; strided convs keep only
+    the taps on the stride grid."""
+    N, H, W, C, Co, R, st, pd = geom
+    if not ops.implicit_dgrad_ok(C, Co):  # (the op itself also takes strided geometries)
+        pytest.skip("geometry outside the implicit dgrad (C % 8)")
+    torch.manual_seed(sum(geom))
+    P, Q = ops.conv_out_size(H, W, R, R, (st, st), (pd, pd))
+    x16 = torch.randn(N, H, W, C, device=DEV).half()
+    w16 = (torch.randn(Co, R, R, C, device=DEV) / (R * R * C) ** 0.5).half()
+    dy16 = torch.randn(N, P, Q, Co, device=DEV).half()
+    dx = ops.conv_dgrad_implicit(dy16, w16, (N, H, W, C), (st, st), (pd, pd))
+    dx_ref, _ = _f64_conv_grads(x16, w16, dy16, (st, st), (pd, pd))
+    assert dx.shape == (N, H, W, C) and dx.dtype == torch.float32
+    assert _nrel(dx, dx_ref) < 1e-5
+    # and the col2im path on the same operands
+    dcol = ops.gemm_f16(dy16.view(-1, Co), w16.view(Co, -1).contiguous(), out_dtype=torch.float32, b_mn=True) \
+        if (R * R * C) % 8 == 0 else None
+    if dcol is not None:
+        dx2 = ops.col2im(dcol, (N, H, W, C), R, R, (st, st), (pd, pd))
+        assert _nrel(dx, dx2) < 1e-5  # different FP32 summation order of the taps
+
+
+WGRAD_GEOMS = [(2, 14, 14, 64, 64, 3, 1, 1), (2, 15, 15, 128, 256, 3, 2, 1), (3, 7, 7, 64, 200, 1, 1, 0),
+               (1, 28, 28, 128, 64, 1, 2, 0), (8, 56, 56, 64, 64, 3, 1, 1)]
+
+
+@pytest.mark.parametrize("geom", WGRAD_GEOMS)
+def test_implicit_wgrad_vs_f64(geom, conv_impl):
+    """Implicit wgrad (column matrix gathered as the MN-major B operand, K = pixels
+    split across SMs and reduce-added) == conv2d's weight gradient; accumulate
+    and the device alpha behave as in qsync_gemm_f16."""
+    N, H, W, C, Co, R, st, pd = geom
+    torch.manual_seed(sum(geom))
+    P, Q = ops.conv_out_size(H, W, R, R, (st, st), (pd, pd))
+    x16 = torch.randn(N, H, W, C, device=DEV).half()
+    w16 = torch.zeros(Co, R, R, C, device=DEV).half()
+    dy16 = torch.randn(N, P, Q, Co, device=DEV).half()
+    _, dw_ref = _f64_conv_grads(x16, w16, dy16, (st, st), (pd, pd))
+    dw = ops.conv_wgrad_implicit(x16, dy16.view(-1, Co), R, R, (st, st), (pd, pd))
+    assert dw.shape == (Co, R * R * C)
+    # K = N*P*Q FP16 products summed in FP32 (tensor-core partial sums, split-K
+    # partials reduce-added): 1e-5 of the norm up to ~4k pixels, 1e-4 beyond
+    tol = 1e-5 if N * P * Q <= 4096 else 1e-4
+    assert _nrel(dw.view(Co, R, R, C), dw_ref) < tol
+    base = torch.randn(Co, R * R * C, device=DEV)
+    out = base.clone()
+    alpha = torch.tensor([0.25], device=DEV)
+    ops.conv_wgrad_implicit(x16, dy16.view(-1, Co), R, R, (st, st), (pd, pd), out=out, accumulate=True,
+                            alpha_dev=alpha)
+    exp = base.double() + 0.25 * dw_ref.reshape(Co, -1)
+    assert _nrel(out, exp) < tol
+
+
+@pytest.mark.parametrize("precision", [INT8, FP16])
+def test_qconv_backward_implicit_matches_col_path(precision, monkeypatch):
+    """The autograd op with implicit dgrad/wgrad == the same op forced onto the
+    materialised im2col / col2im path."""
+    torch.manual_seed(5)
+    x = torch.randn(2, 14, 14, 128, device=DEV, requires_grad=True)
+    w = torch.randn(128, 3, 3, 128, device=DEV) * 0.03
+    w.requires_grad_(True)
+    g = torch.randn(2, 7, 7, 128, device=DEV)
+
+    def run():
+        x.grad = None
+        w.grad = None
+        y = qconv2d(x, w, None, (2, 2), (1, 1), precision)
+        y.backward(g.to(y.dtype))
+        return x.grad.clone(), w.grad.clone()
+
+    dx_i, dw_i = run()
+    monkeypatch.setattr(ops, "implicit_dgrad_ok", lambda *a: False)
+    monkeypatch.setattr(ops, "implicit_wgrad_ok", lambda *a: False)
+    dx_c, dw_c = run()
+    assert _nrel(dx_i, dx_c) < 1e-5
+    assert _nrel(dw_i, dw_c) < 1e-5
