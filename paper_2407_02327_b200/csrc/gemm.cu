@@ -79,9 +79,14 @@ struct Cfg {
 #ifndef QSB_GEMM_STAGES_48K
 #define QSB_GEMM_STAGES_48K 4
 #endif
-    static constexpr int kStages = kStageBytes >= 48 * 1024 ? QSB_GEMM_STAGES_48K : (kStageBytes >= 32 * 1024 ? 6 : 8);
-    static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
+    static constexpr int kStagesWant =
+        kStageBytes >= 48 * 1024 ? QSB_GEMM_STAGES_48K : (kStageBytes >= 32 * 1024 ? 6 : 8);
     static constexpr int kEpiStageBytes = 4 * 2 * kStageChunkBytes;  // 4 warps x double buffer
+    // ... as many as fit next to the epilogue staging in 227 KB (BN = 192: 4 x 40 KB)
+    static constexpr int kStagesFit = (227 * 1024 - kEpiStageBytes - 1024 - 256) / kStageBytes;
+    static constexpr int kStages = kStagesWant < kStagesFit ? kStagesWant : kStagesFit;
+    // two accumulator buffers; TMEM allocations are powers of two (BN = 192 -> 512)
+    static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
     static constexpr int kSmemBytes =
         kStages * kStageBytes + kEpiStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -922,7 +927,9 @@ struct Shape {
 };
 Shape pick_shape(int64_t M, int64_t N, bool allow_pair) {
     const int sms = sm_count();
-    const Shape cands[5] = {{256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
+    // 192-wide tiles: N = 768 is 4 of them, so M = 4096 fills 128 SMs in one
+    // wave where 256-wide tiles leave a third of the SMs idle (96 tiles).
+    const Shape cands[6] = {{256, 2}, {256, 1}, {192, 1}, {128, 2}, {128, 1}, {64, 1}};
     Shape best{256, 1};
     double best_cost = 1e300;
     for (const Shape& c : cands) {
@@ -958,6 +965,7 @@ int dispatch_shape(const void* a, const void* b, CUtensorMapDataType dt, EpiPara
     }
     switch (sh.bn) {
         case 256: return launch<kI8, 256, 1, kLay>(a, b, dt, p, st);
+        case 192: return launch<kI8, 192, 1, kLay>(a, b, dt, p, st);
         case 128: return launch<kI8, 128, 1, kLay>(a, b, dt, p, st);
         case 64: return launch<kI8, 64, 1, kLay>(a, b, dt, p, st);
         default: return set_error(QSYNC_ERR_DOMAIN, "unsupported tile N " + std::to_string(sh.bn));
@@ -974,11 +982,12 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     if (splitk_ok || accumulating) sh.bn = 256;
     if (force_bn) sh.bn = force_bn;
     if (g_force_cta) sh.cta = g_force_cta;
-    if (sh.cta == 2 && sh.bn == 64) sh.cta = 1;  // pair tiles need BN/2 >= 64 rows of B
+    if (sh.cta == 2 && (sh.bn == 64 || sh.bn == 192)) sh.cta = 1;  // pairs: BN/2 a multiple of 64
     p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout, p.fp8);
     p.debug_epi = g_debug_epi;
     if (layout & 108) {  // implicit conv (fwd 4/32, dgrad 22/50, wgrad 11/67): single-CTA tiles
         sh.cta = 1;
+        if (sh.bn == 192) sh.bn = 256;  // (no 192-wide conv instantiations)
         p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM, layout & 3, p.fp8);
         if (layout == 4) {
             switch (sh.bn) {
@@ -1085,7 +1094,8 @@ int qsync_gemm_force_cta(int cta) {
 }
 
 int qsync_gemm_force_tile_n(int bn) {
-    QSB_REQUIRE(bn == 0 || bn == 64 || bn == 128 || bn == 256, QSYNC_ERR_DOMAIN, "tile N must be 0/64/128/256");
+    QSB_REQUIRE(bn == 0 || bn == 64 || bn == 128 || bn == 192 || bn == 256, QSYNC_ERR_DOMAIN,
+                "tile N must be 0/64/128/192/256");
     g_force_bn = bn;
     return QSYNC_OK;
 }

@@ -344,7 +344,9 @@ class _FusedLayerFn(torch.autograd.Function):
                                            L.ln2.weight.main_grad, L.ln2.bias.main_grad,
                                            want_f16=p2 != FP32, colsum_into=_bias_main_grad(L.ff2))
         dy2 = ds2_16 if p2 != FP32 else ds2
-        dg = _dgrad(L.ff2, dy2, w16_2, h.dtype)
+        # FF2's FP16 backward kernel emits its input gradient in FP16 (as the
+        # reference's FP16 op does before the cast back), halving dG's traffic
+        dg = _dgrad(L.ff2, dy2, w16_2, torch.float16 if p2 != FP32 else h.dtype)
         _wgrad(L.ff2, dy2, op_2, side if p2 != FP32 else None)
         # --- GELU backward fused with FF1's dY cast + ff1 bias grad
         p1 = L.ff1.precision

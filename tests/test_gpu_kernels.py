@@ -226,7 +226,7 @@ GEMM_SHAPES = [(128, 256, 128), (64, 1024, 1024), (200, 300, 64), (1, 16, 16), (
                (257, 129, 3072), (512, 2304, 768)]
 
 
-@pytest.mark.parametrize("cta_bn", [(1, 0), (1, 64), (1, 128), (1, 256), (2, 128), (2, 256), (0, 0)])
+@pytest.mark.parametrize("cta_bn", [(1, 0), (1, 64), (1, 128), (1, 192), (1, 256), (2, 128), (2, 256), (0, 0)])
 @pytest.mark.parametrize("mnk", GEMM_SHAPES)
 def test_gemm_s8_int32_bit_exact(mnk, cta_bn, cpuref):
     """int32 accumulators bit-exact for single-CTA tiles and CTA-pair (cta_group::2) tiles."""
@@ -269,17 +269,21 @@ def test_gemm_s8_rejects_bad_k():
     assert e.value.kind == "domain"
 
 
-@pytest.mark.parametrize("cta", [1, 2])
+@pytest.mark.parametrize("cta", [1, 2, "bn192"])
 @pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("mnk", [(128, 128, 64), (64, 1024, 1024), (333, 200, 72),
                                  (4096, 768, 3072), (768, 3072, 4096)])
 def test_gemm_f16_within_tolerance(mnk, dt, cta, cpuref):
     M, N, K = mnk
-    ops.force_cta(cta)
+    if cta == "bn192":
+        ops.force_tile_n(192)
+    else:
+        ops.force_cta(cta)
     try:
         _check_f16(M, N, K, dt)
     finally:
         ops.force_cta(0)
+        ops.force_tile_n(0)
 
 
 def _check_f16(M, N, K, dt):
@@ -310,7 +314,7 @@ def test_gemm_f16_bias_alpha_dev_accumulate():
     assert (base.double() - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
 
 
-@pytest.mark.parametrize("cta", [1, 2])
+@pytest.mark.parametrize("cta", [1, 2, "bn192"])
 @pytest.mark.parametrize("lay", ["b_mn", "ab_mn"])
 @pytest.mark.parametrize("mnk", [(128, 128, 64), (4096, 768, 2304), (2304, 768, 4096), (768, 3072, 300),
                                  (200, 136, 77), (512, 512, 1000)])
@@ -324,7 +328,10 @@ def test_gemm_f16_mn_major_operands(mnk, lay, cta):
     a = torch.from_numpy(rng.normal(size=(M, K)).astype(np.float32)).half()
     b = torch.from_numpy(rng.normal(size=(N, K)).astype(np.float32)).half()
     ref = a.double() @ b.double().T
-    ops.force_cta(cta)
+    if cta == "bn192":
+        ops.force_tile_n(192)
+    else:
+        ops.force_cta(cta)
     try:
         if lay == "b_mn":
             c = ops.gemm_f16(a.cuda(), b.t().contiguous().cuda(), b_mn=True)
@@ -335,6 +342,7 @@ def test_gemm_f16_mn_major_operands(mnk, lay, cta):
                      out=base, accumulate=True, alpha=0.5)
     finally:
         ops.force_cta(0)
+        ops.force_tile_n(0)
     err = (torch.from_numpy(_np(c)).double() - ref).abs().max().item()
     assert err <= 1e-3 * ref.abs().max().item()
     err2 = (torch.from_numpy(_np(base)).double() - (1.0 + 0.5 * ref)).abs().max().item()
