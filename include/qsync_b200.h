@@ -301,6 +301,10 @@ int qsync_absmax_act(const void* x, int dtype, int64_t n, int act, float* absmax
  * dact_out (optional, FP16) receives act'(x) for the backward (QSYNC_ACT_DERIV). */
 int qsync_quantize_act(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,
                        float* scale_out, uint16_t* dact_out, qsync_stream_t stream);
+/* The same, also writing q16_out (optional) = FP16(q): the grid values exactly,
+ * the operand the op's FP16 wgrad reads in the backward (no separate cast). */
+int qsync_quantize_act_ex(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,
+                          float* scale_out, uint16_t* dact_out, uint16_t* q16_out, qsync_stream_t stream);
 /* out = act(x) cast to dst_dtype (F32/F16 -> F32/F16); optional FP16 act'(x). */
 int qsync_act_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64_t n, int act,
                    uint16_t* dact_out, qsync_stream_t stream);

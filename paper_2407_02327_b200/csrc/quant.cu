@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                                                        const float* __restrict__ scale_in,
                                                        int8_t* __restrict__ q,
                                                        float* __restrict__ scale_out, int vec_ok,
-                                                       uint16_t* __restrict__ dact = nullptr) {
+                                                       uint16_t* __restrict__ dact = nullptr,
+                                                       uint16_t* __restrict__ q16 = nullptr) {
     QSB_PDL_ENTER();
     using V = Vec<DT>;
     constexpr int LOADS = 16 / V::N;
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
             for (int u = 0; u < LOADS; ++u) r[u] = ld_stream(xv + i * LOADS + u);
             uint32_t packed[4];
             uint32_t dp[8];  // GELU'(x) of the 16 elements as FP16 pairs (the backward's factor)
+            uint32_t hq[8];  // the 16 grid values as FP16 pairs (exact; the wgrad's operand)
 #pragma unroll
             for (int u = 0; u < LOADS; ++u) {
                 float f[V::N];
@@ -170,14 +172,21 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
 #pragma unroll
                         for (int e = 0; e < 4; ++e) a[e] = act_f<ACT, DT>(f[j + e]);
                     }
-                    uint32_t b0 = static_cast<uint8_t>(quant_rne(a[0], s));
-                    uint32_t b1 = static_cast<uint8_t>(quant_rne(a[1], s));
-                    uint32_t b2 = static_cast<uint8_t>(quant_rne(a[2], s));
-                    uint32_t b3 = static_cast<uint8_t>(quant_rne(a[3], s));
+                    const int i0 = quant_rne(a[0], s), i1 = quant_rne(a[1], s);
+                    const int i2 = quant_rne(a[2], s), i3 = quant_rne(a[3], s);
+                    const uint32_t b0 = static_cast<uint8_t>(i0), b1 = static_cast<uint8_t>(i1);
+                    const uint32_t b2 = static_cast<uint8_t>(i2), b3 = static_cast<uint8_t>(i3);
                     packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+                    hq[(u * V::N + j) / 2] = pack_half2(static_cast<float>(i0), static_cast<float>(i1));
+                    hq[(u * V::N + j) / 2 + 1] = pack_half2(static_cast<float>(i2), static_cast<float>(i3));
                 }
             }
             qv[i] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            if (q16) {
+                uint4* hv = reinterpret_cast<uint4*>(q16) + 2 * i;
+                hv[0] = make_uint4(hq[0], hq[1], hq[2], hq[3]);
+                hv[1] = make_uint4(hq[4], hq[5], hq[6], hq[7]);
+            }
             if (ACT == 1 && dact) {
                 uint4* dv = reinterpret_cast<uint4*>(dact) + 2 * i;
                 dv[0] = make_uint4(dp[0], dp[1], dp[2], dp[3]);
@@ -188,7 +197,9 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
     }
     for (int64_t i = done + tid; i < n; i += stride) {
         const float xv = Elem<DT>::f(x[i]);
-        q[i] = static_cast<int8_t>(quant_rne(act_f<ACT, DT>(xv), s));
+        const int qi = quant_rne(act_f<ACT, DT>(xv), s);
+        q[i] = static_cast<int8_t>(qi);
+        if (q16) q16[i] = __half_as_ushort(__int2half_rn(qi));
         if (ACT == 1 && dact) dact[i] = __half_as_ushort(__float2half_rn(gelu_erf_grad(xv)));
     }
 }
@@ -840,7 +851,7 @@ struct QuantRun {
         const int vec = aligned16(x) && aligned16(q);
         const int grid = grid_for(n / 16 + 1, kThreads, 4);
         pdl_launch(k_quantize<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, scale + 1, nullptr,
-                                                  q, scale, vec, static_cast<uint16_t*>(nullptr));
+                                                  q, scale, vec, static_cast<uint16_t*>(nullptr), static_cast<uint16_t*>(nullptr));
         return check_launch("k_quantize");
     }
 };
@@ -853,7 +864,7 @@ struct QuantScaleRun {
         const int vec = aligned16(x) && aligned16(q);
         const int grid = grid_for(n / 16 + 1, kThreads, 4);
         pdl_launch(k_quantize<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, nullptr, scale, q,
-                                                  nullptr, vec, static_cast<uint16_t*>(nullptr));
+                                                  nullptr, vec, static_cast<uint16_t*>(nullptr), static_cast<uint16_t*>(nullptr));
         return check_launch("k_quantize");
     }
 };
@@ -910,17 +921,17 @@ struct AbsmaxActRun {
 template <int DT>
 struct QuantActRun {
     static int run(const void* x, int64_t n, int act, const float* absmax, int8_t* q,
-                   float* scale_out, uint16_t* dact, cudaStream_t st) {
+                   float* scale_out, uint16_t* dact, uint16_t* q16, cudaStream_t st) {
         using T = typename Elem<DT>::T;
         if (n == 0) return QSYNC_OK;
-        const int vec = aligned16(x) && aligned16(q) && (!dact || aligned16(dact));
+        const int vec = aligned16(x) && aligned16(q) && (!dact || aligned16(dact)) && (!q16 || aligned16(q16));
         const int grid = grid_for(n / 16 + 1, kThreads, 4);
         if (act == 1)
             pdl_launch(k_quantize<DT, 1>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, absmax, nullptr,
-                                                         q, scale_out, vec, dact);
+                                                         q, scale_out, vec, dact, q16);
         else
             pdl_launch(k_quantize<DT, 0>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, absmax, nullptr,
-                                                         q, scale_out, vec, static_cast<uint16_t*>(nullptr));
+                                                         q, scale_out, vec, static_cast<uint16_t*>(nullptr), q16);
         return check_launch("k_quantize");
     }
 };
@@ -1052,7 +1063,17 @@ int qsync_quantize_act(const void* x, int dtype, int64_t n, int act, const float
     QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
     QSB_REQUIRE(absmax != nullptr, QSYNC_ERR_VALIDATION, "absmax is required");
     QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU, QSYNC_ERR_DOMAIN, "unknown activation");
-    return dispatch_dtype<QuantActRun>(dtype, x, n, act, absmax, q, scale_out, dact_out, to_stream(stream));
+    return dispatch_dtype<QuantActRun>(dtype, x, n, act, absmax, q, scale_out, dact_out,
+                                       static_cast<uint16_t*>(nullptr), to_stream(stream));
+}
+
+int qsync_quantize_act_ex(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,
+                          float* scale_out, uint16_t* dact_out, uint16_t* q16_out, qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    QSB_REQUIRE(absmax != nullptr, QSYNC_ERR_VALIDATION, "absmax is required");
+    QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU, QSYNC_ERR_DOMAIN, "unknown activation");
+    return dispatch_dtype<QuantActRun>(dtype, x, n, act, absmax, q, scale_out, dact_out, q16_out,
+                                       to_stream(stream));
 }
 
 int qsync_act_cast(const void* x, int src, void* out, int dst, int64_t n, int act, uint16_t* dact_out,

@@ -159,11 +159,11 @@ def _operand(x, aux, prec):
     """The planned op's input operand (and what its backward keeps)."""
     if prec == INT8:
         if aux is not None and aux.dtype == torch.float32 and aux.numel() == 1:
-            xq, s = ops.quantize_act(x, aux)
-        else:
-            xq, sc, _ = ops.quantize_per_tensor(x)
-            s = sc[:1]
-        return ("i8", xq, s)
+            # the quantizer also writes FP16(q) for the wgrad (no cast kernel there)
+            xq, s, x16 = ops.quantize_act(x, aux, want_q16=True)
+            return ("i8", xq, s, x16)
+        xq, sc, _ = ops.quantize_per_tensor(x)
+        return ("i8", xq, sc[:1])
     if prec == FP16:
         if x.dtype == torch.float16:
             return ("f16", x, None)
@@ -189,7 +189,7 @@ def _weights(m):
 
 
 def _linear_fwd(m, opnd, out_dtype=None):
-    kind, x, s = opnd
+    kind, x, s = opnd[:3]
     w, b = m.weight, m.bias
     bias = b.detach() if b is not None else None
     wq, ws, w16 = _weights(m)
@@ -213,12 +213,15 @@ def _call_cap(n):
 
 def _wgrad(m, dy16_or_32, opnd, side):
     """wgrad of one planned op into weight.main_grad (FP32, accumulate)."""
-    kind, x, s = opnd
+    kind, x, s = opnd[:3]
     mw = m.weight.main_grad
     if kind == "f32":
         mw.addmm_(dy16_or_32.float().t(), x)  # training-device FP32 path (cuBLAS), main stream
         return
-    x16 = ops.cast(x, torch.float16) if kind == "i8" else x  # exact: INT8 grid values
+    if kind == "i8":  # FP16 copy of the INT8 grid values (exact), from the quantizer when it wrote one
+        x16 = opnd[3] if len(opnd) > 3 else ops.cast(x, torch.float16)
+    else:
+        x16 = x
 
     def run():
         if side is not None and WGRAD_CTAS:
@@ -296,8 +299,8 @@ class _FusedLayerFn(torch.autograd.Function):
         # then needs no transcendental (dh = dg * GELU'(h)).
         if p2 == INT8:
             gam = ops.absmax_act(h, ops.ACT_GELU)
-            gq, gs, gp = ops.quantize_act(h, gam, ops.ACT_GELU, want_dact=True)
-            op_2 = ("i8", gq, gs)
+            gq, gs, gp, g16 = ops.quantize_act(h, gam, ops.ACT_GELU, want_dact=True, want_q16=True)
+            op_2 = ("i8", gq, gs, g16)
         elif p2 == FP16:
             g16, gp = ops.act_cast(h, torch.float16, ops.ACT_GELU, want_dact=True)
             op_2 = ("f16", g16, None)
@@ -315,7 +318,7 @@ class _FusedLayerFn(torch.autograd.Function):
         ctx.w16 = (w16_qkv, w16_o, w16_1, w16_2)
         ctx.attn = (qkv5, a, lse, scale)
         ctx.ln = (s1, mean1, rstd1, s2, mean2, rstd2)
-        ctx.h = (h, gp)
+        ctx.h = (h.dtype, gp)  # GELU'(h) is all the backward needs of h
         ctx.shape = (B, S, H)
         out = x2.view(B, S, H)
         if aux2 is None:
@@ -333,7 +336,7 @@ class _FusedLayerFn(torch.autograd.Function):
         w16_qkv, w16_o, w16_1, w16_2 = ctx.w16
         qkv5, a, lse, scale = ctx.attn
         s1, mean1, rstd1, s2, mean2, rstd2 = ctx.ln
-        h, gp = ctx.h
+        h_dtype, gp = ctx.h
         side = _ql.WGRAD_STREAM
         dx2 = dx2.reshape(M, H).contiguous()
         if dx2.dtype != torch.float32:
@@ -346,7 +349,7 @@ class _FusedLayerFn(torch.autograd.Function):
         dy2 = ds2_16 if p2 != FP32 else ds2
         # FF2's FP16 backward kernel emits its input gradient in FP16 (as the
         # reference's FP16 op does before the cast back), halving dG's traffic
-        dg = _dgrad(L.ff2, dy2, w16_2, torch.float16 if p2 != FP32 else h.dtype)
+        dg = _dgrad(L.ff2, dy2, w16_2, torch.float16 if p2 != FP32 else h_dtype)
         _wgrad(L.ff2, dy2, op_2, side if p2 != FP32 else None)
         # --- GELU backward fused with FF1's dY cast + ff1 bias grad
         p1 = L.ff1.precision

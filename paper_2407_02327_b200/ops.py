@@ -458,16 +458,19 @@ def absmax_act(x: torch.Tensor, act: int = ACT_NONE, out=None) -> torch.Tensor:
     return o
 
 
-def quantize_act(x: torch.Tensor, absmax: torch.Tensor, act: int = ACT_NONE, want_dact: bool = False):
+def quantize_act(x: torch.Tensor, absmax: torch.Tensor, act: int = ACT_NONE, want_dact: bool = False,
+                 want_q16: bool = False):
     """q = sat(rint(act(x) / s)), s = absmax/127 from a device absmax.
-    Returns (q, s[1]) or (q, s[1], act'(x) FP16) with ``want_dact``."""
+    Returns (q, s[1]) [+ act'(x) FP16 with ``want_dact``] [+ FP16(q) with ``want_q16``]."""
     _req(x, "x", _DT)
     q = torch.empty(x.shape, device=x.device, dtype=torch.int8)
     s = torch.empty(1, device=x.device, dtype=torch.float32)
     d = torch.empty(x.shape, device=x.device, dtype=torch.float16) if want_dact else None
-    call("qsync_quantize_act", _ptr(x), _DT[x.dtype], x.numel(), int(act), _ptr(absmax), _ptr(q),
-         _ptr(s), _ptr(d), _stream())
-    return (q, s, d) if want_dact else (q, s)
+    h = torch.empty(x.shape, device=x.device, dtype=torch.float16) if want_q16 else None
+    call("qsync_quantize_act_ex", _ptr(x), _DT[x.dtype], x.numel(), int(act), _ptr(absmax), _ptr(q),
+         _ptr(s), _ptr(d), _ptr(h), _stream())
+    out = (q, s) + ((d,) if want_dact else ()) + ((h,) if want_q16 else ())
+    return out
 
 
 def act_cast(x: torch.Tensor, dtype: torch.dtype, act: int = ACT_NONE, out=None, want_dact: bool = False):

@@ -307,3 +307,17 @@ def test_bucketwise_optimizer_matches_single_launch():
         losses[overlap] = [float(st().item()) for _ in range(3)]
         assert int(st.opt.step_t.item()) == 3
     np.testing.assert_allclose(losses[True], losses[False], rtol=2e-3, atol=2e-3)
+
+
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("n", [4096 * 768, 1001])
+def test_quantize_act_q16_is_exact_copy(act, n):
+    """The quantizer's FP16 copy of the grid values (the wgrad operand) equals
+    FP16(q) exactly, and writing it changes nothing else."""
+    torch.manual_seed(n + act)
+    h = torch.randn(n, device="cuda") * 3
+    am = ops.absmax_act(h, act)
+    q0, s0 = ops.quantize_act(h, am, act)
+    q, s, q16 = ops.quantize_act(h, am, act, want_q16=True)
+    assert torch.equal(q, q0) and torch.equal(s, s0)
+    assert q16.dtype == torch.float16 and torch.equal(q16, q.to(torch.float16))
