@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_act_bwd_colsum(const void* __re
 #pragma unroll
     for (int j = 0; j < 8; ++j) cs[j] = 0.0f;
     const bool full = vec_ok && c + 8 <= cols;
-#pragma unroll 2
+#pragma unroll 4
     for (int rr = 0; rr < kRowsPerWarp; ++rr) {
         const int64_t r = r0 + rr;
         if (r >= rows) break;
