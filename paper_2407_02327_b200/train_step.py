@@ -333,12 +333,12 @@ class TrainStep:
         # all-reduce / optimizer and fill the gaps.
         self.wgrad_stream = torch.cuda.Stream(priority=0) if overlap_wgrad else None
         if overlap_wgrad and fused:
-            # The wgrad GEMMs are persistent kernels: capped at ~2/3 of the SMs
-            # they overlap the main stream's chain instead of displacing it
-            # (tools/ab_wgrad_cap.py: 5.55 -> 5.2-5.3 ms per BERT-base step).
+            # Side-stream wgrad GEMM grid cap (persistent kernels).  A 2/3-of-SMs
+            # cap once paid (5.55 -> 5.25 ms); with 192-wide tiles and the FP16
+            # wgrad operands written by the quantizer the uncapped grid is best
+            # (tools/ab_wgrad_cap.py: 5.09 ms uncapped vs 5.20 at 98 CTAs).
             from . import fused as _fz
-            from . import ops as _ops
-            _fz.WGRAD_CTAS = max(1, (2 * _ops.sm_count()) // 3)
+            _fz.WGRAD_CTAS = 0
         # Bucket-wise optimizer (DP): each bucket's AdamW runs on the comm stream
         # right after its all-reduce, overlapping the remaining buckets' reductions
         # and the rest of the backward.  On one GPU it only contends with the

@@ -10,12 +10,12 @@ from paper_2407_02327_b200.train_step import BertConfig, BertEncoderStack, Train
 
 
 def step_ms(cap, steps=30):
-    fused.WGRAD_CTAS = cap
     cfg = BertConfig()
     torch.manual_seed(0)
     m = BertEncoderStack(cfg).cuda()
     m.apply_plan(mixed_plan(cfg))
     st = TrainStep(m, batch=32, graph=True)
+    fused.WGRAD_CTAS = cap  # after TrainStep, which sets its default (2/3 of the SMs)
     st.tokens.random_(0, cfg.vocab)
     st.capture(warmup=3)
     torch.cuda.synchronize()
@@ -28,5 +28,5 @@ def step_ms(cap, steps=30):
     return s.elapsed_time(e) / steps
 
 
-for cap in [int(c) for c in (sys.argv[1:] or ["0", "32", "64", "96", "0", "48", "74"])]:
+for cap in [int(c) for c in (sys.argv[1:] or ["0", "64", "80", "98", "112", "128", "98"])]:
     print(f"wgrad cap={cap:4d} step_ms={step_ms(cap):.3f}", flush=True)
