@@ -690,7 +690,179 @@ __global__ void __launch_bounds__(2 * kTcThreads) k_attn_bwd_tc(const __grid_con
     }
 }
 
-int g_attn_tc = 1;  // tcgen05 forward (qsync_attention_set_impl)
+// Two CTAs per SM: P^T never touches shared memory.  The elementwise phase
+// writes P^T (FP16 pairs) into the consumed S^T columns of tensor memory and dV
+// = P^T dO reads it from there (tcgen05.mma with A in TMEM); dS^T goes to smem
+// over the dead V tile and one more (it is also dQ's MN-major A).  Five 16 KB
+// tiles instead of seven: 2 x ~83 KB smem and 2 x 256 TMEM columns per SM, so
+// one CTA's MMAs / loads overlap the other's elementwise phase and epilogue.
+//   TMEM: phase 1  S^T cols 0..127, dP^T 128..255
+//         phase 2  P^T 0..63 (packed), dV 64..127, dK 128..191, dQ 192..255
+constexpr int kTcBwd2Smem = 5 * kTile + 1024 + 2 * kS * 4 + 64;
+
+__global__ void __launch_bounds__(2 * kTcThreads, 2) k_attn_bwd_tc2(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                const __grid_constant__ CUtensorMap tm_do,
+                                                                const __half* __restrict__ out,
+                                                                const __half* __restrict__ dout,
+                                                                const float* __restrict__ lse, int H, float scale,
+                                                                __half* __restrict__ dqkv) {
+    QSB_PDL_ENTER();
+    extern __shared__ uint8_t sm_raw[];
+    const uint32_t raw = ptx::smem_u32(sm_raw);
+    uint8_t* sm = sm_raw + ((1024 - (raw & 1023)) & 1023);
+    uint8_t* sQ = sm;
+    uint8_t* sK = sm + kTile;
+    uint8_t* sdO = sm + 2 * kTile;
+    uint8_t* sV = sm + 3 * kTile;   // dead after dP^T: dS^T is written over it
+    uint8_t* sDS = sm + 3 * kTile;  // dS^T [128 keys x 128 queries] as 2 K-blocks of [128 x 128B]
+    float* sL = reinterpret_cast<float*>(sm + 5 * kTile);
+    float* sD = sL + kS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + kS);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+    const int bh = blockIdx.x, b = bh / H, h = bh % H;
+    const int t = threadIdx.x & 127, warp = (threadIdx.x >> 5) & 3, wg = threadIdx.x >> 7;
+    if (threadIdx.x == 0) {
+        ptx::tma_prefetch(&tm_qkv);
+        ptx::tma_prefetch(&tm_do);
+        for (int i = 0; i < 3; ++i) ptx::mbar_init(&bars[i], 1);
+        ptx::fence_mbar_init();
+    }
+    if (threadIdx.x < 32) ptx::tmem_alloc<256>(tslot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int64_t orow = static_cast<int64_t>(H) * kD;
+    if (threadIdx.x == 0) {
+        ptx::mbar_arrive_expect_tx(&bars[0], 4 * kTile);
+        const int row = b * kS;
+        ptx::tma_load_2d(sQ, &tm_qkv, &bars[0], h * kD, row);
+        ptx::tma_load_2d(sK, &tm_qkv, &bars[0], (H + h) * kD, row);
+        ptx::tma_load_2d(sV, &tm_qkv, &bars[0], (2 * H + h) * kD, row);
+        ptx::tma_load_2d(sdO, &tm_do, &bars[0], h * kD, row);
+    }
+    if (wg == 0) {   // D[q] = sum_d dO[q,d] O[q,d] (thread t = query t) and lse in log2 units
+        const uint4* op = reinterpret_cast<const uint4*>(out + (static_cast<int64_t>(b) * kS + t) * orow + h * kD);
+        const uint4* dp = reinterpret_cast<const uint4*>(dout + (static_cast<int64_t>(b) * kS + t) * orow + h * kD);
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint4 ov = op[i], dv = dp[i];
+            const __half2* oh = reinterpret_cast<const __half2*>(&ov);
+            const __half2* dh = reinterpret_cast<const __half2*>(&dv);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 a = __half22float2(oh[e]), c = __half22float2(dh[e]);
+                acc += a.x * c.x + a.y * c.y;
+            }
+        }
+        sD[t] = acc;
+        sL[t] = lse[static_cast<int64_t>(bh) * kS + t] * kLog2e;
+    }
+    if (threadIdx.x == 0) {
+        ptx::mbar_wait(&bars[0], 0);
+        ptx::tc_fence_after();
+        const uint32_t id = idesc_f16_f32_ab(kS, kS, false, false);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+            ptx::mma_f16(tmem, ptx::sw128_kmajor_desc(ptx::smem_u32(sK) + k * 32),
+                         ptx::sw128_kmajor_desc(ptx::smem_u32(sQ) + k * 32), id, k > 0 ? 1u : 0u);
+            ptx::mma_f16(tmem + kS, ptx::sw128_kmajor_desc(ptx::smem_u32(sV) + k * 32),
+                         ptx::sw128_kmajor_desc(ptx::smem_u32(sdO) + k * 32), id, k > 0 ? 1u : 0u);
+        }
+        ptx::tc_commit(&bars[1]);
+    }
+    __syncthreads();  // sD / sL visible to every thread
+    ptx::mbar_wait(&bars[1], 0);
+    ptx::tc_fence_after();
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const float sl2 = scale * kLog2e;
+    uint32_t keep[2][16];  // this warp's P^T chunks, stored to TMEM once every S^T column is read
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {  // 32 queries per chunk; each warpgroup takes half
+        const int c = 2 * wg + cc;
+        uint32_t rs[32], rp[32];
+        ptx::tmem_ld32(trow + 32 * c, rs);
+        ptx::tmem_ld32(trow + kS + 32 * c, rp);
+        ptx::tmem_ld_wait();
+        uint32_t pd[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int q = 32 * c + 2 * j;
+            const float p0 = exp2f(__uint_as_float(rs[2 * j]) * sl2 - sL[q]);
+            const float p1 = exp2f(__uint_as_float(rs[2 * j + 1]) * sl2 - sL[q + 1]);
+            const float d0 = p0 * (__uint_as_float(rp[2 * j]) - sD[q]);
+            const float d1 = p1 * (__uint_as_float(rp[2 * j + 1]) - sD[q + 1]);
+            keep[cc][j] = pk(p0, p1);
+            pd[j] = pk(d0, d1);
+        }
+        const uint32_t off = (c >> 1) * kTile + t * 128;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            const uint32_t sw = ((((c & 1) * 4 + q4) ^ (t & 7)) << 4);
+            ptx::st_shared_v4(ptx::smem_u32(sDS) + off + sw, pd[4 * q4], pd[4 * q4 + 1], pd[4 * q4 + 2], pd[4 * q4 + 3]);
+        }
+    }
+    // every warp has read its S^T / dP^T columns: P^T may now overwrite S^T
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) ptx::tmem_st16(trow + 16 * (2 * wg + cc), keep[cc]);
+    ptx::tmem_st_wait();
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (threadIdx.x == 0) {
+        const uint32_t id_kv = idesc_f16_f32_ab(kD, kS, false, true);
+        const uint32_t id_q = idesc_f16_f32_ab(kD, kS, true, true);
+#pragma unroll
+        for (int k = 0; k < kS / 16; ++k) {
+            const uint32_t aoff = (k >> 2) * kTile + (k & 3) * 32;
+            const uint32_t brow = k * 16 * 128;
+            const uint32_t acc = k > 0 ? 1u : 0u;
+            // dV = P^T dO   (A = P^T from TMEM, 8 columns per 16 queries; B MN-major)
+            ptx::mma_f16_ts(tmem + 64, tmem + 8 * k, ptx::sw128_mnmajor_desc(ptx::smem_u32(sdO) + brow, kTile),
+                            id_kv, acc);
+            // dK = dS^T Q
+            ptx::mma_f16(tmem + 128, ptx::sw128_kmajor_desc(ptx::smem_u32(sDS) + aoff),
+                         ptx::sw128_mnmajor_desc(ptx::smem_u32(sQ) + brow, kTile), id_kv, acc);
+            // dQ = dS K   (A = dS MN-major from the dS^T tile: rows = keys; B = K MN-major)
+            ptx::mma_f16(tmem + 192, ptx::sw128_mnmajor_desc(ptx::smem_u32(sDS) + brow, kTile),
+                         ptx::sw128_mnmajor_desc(ptx::smem_u32(sK) + brow, kTile), id_q, acc);
+        }
+        ptx::tc_commit(&bars[2]);
+    }
+    ptx::mbar_wait(&bars[2], 0);
+    ptx::tc_fence_after();
+    const int64_t rs3 = 3LL * H * kD;
+#pragma unroll 1
+    for (int which = wg; which < 3; which += 2) {  // 0 dQ (row = query t), 1 dK, 2 dV (row = key t)
+        const uint32_t col = which == 0 ? 192 : (which == 1 ? 128 : 64);
+        const float f = which == 2 ? 1.f : scale;
+        uint32_t r[2][32];
+        ptx::tmem_ld32(trow + col, r[0]);
+        ptx::tmem_ld32(trow + col + 32, r[1]);
+        ptx::tmem_ld_wait();
+        uint32_t w[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            w[j] = pk(__uint_as_float(r[j >> 4][(2 * j) & 31]) * f, __uint_as_float(r[j >> 4][(2 * j + 1) & 31]) * f);
+        __half* dst = dqkv + (static_cast<int64_t>(b) * kS + t) * rs3 + (static_cast<int64_t>(which) * H + h) * kD;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<256>(tmem);
+    }
+}
+
+int g_attn_tc = 2;  // 0 mma.sync kernels, 1 tcgen05, 2 tcgen05 backward at 2 CTAs / SM (qsync_attention_set_impl)
 
 constexpr int kFwdSmem = 3 * kTile;
 constexpr int kBwdSmem = 4 * kTile + 2 * kTile + 2 * kS * 4;
@@ -747,6 +919,22 @@ int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, cons
     QSB_REQUIRE(qkv && out && dout && lse && dqkv, QSYNC_ERR_VALIDATION, "attention backward needs all buffers");
     QSB_TRY(check_shape(B, S, H, D));
     cudaStream_t st = to_stream(stream);
+    if (g_attn_tc == 2) {
+        static bool tc2_configured = false;
+        if (!tc2_configured) {
+            QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_bwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     kTcBwd2Smem),
+                                "cudaFuncSetAttribute"));
+            tc2_configured = true;
+        }
+        CUtensorMap tq, td;
+        QSB_TRY(make_tma_2d(&tq, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 3 * H * kD, B * kS, kD, kS));
+        QSB_TRY(make_tma_2d(&td, dout, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, H * kD, B * kS, kD, kS));
+        pdl_launch(k_attn_bwd_tc2, dim3(static_cast<unsigned>(B * H)), dim3(2 * kTcThreads), kTcBwd2Smem, st, tq,
+                   td, static_cast<const __half*>(out), static_cast<const __half*>(dout), lse, static_cast<int>(H),
+                   scale, static_cast<__half*>(dqkv));
+        return check_launch("k_attn_bwd_tc2");
+    }
     if (g_attn_tc) {
         static bool tc_configured = false;
         if (!tc_configured) {
@@ -776,7 +964,8 @@ int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, cons
 }
 
 int qsync_attention_set_impl(int tc) {
-    g_attn_tc = tc ? 1 : 0;
+    QSB_REQUIRE(tc >= 0 && tc <= 2, QSYNC_ERR_DOMAIN, "attention impl must be 0 (mma.sync), 1 or 2 (tcgen05)");
+    g_attn_tc = tc;
     return QSYNC_OK;
 }
 

@@ -25,8 +25,17 @@ def _rel(a, b):
     return ((a.float() - b.float()).abs().max() / b.float().abs().max()).item()
 
 
+@pytest.fixture(params=[2, 1, 0], ids=["tc_2cta", "tc", "mma_sync"])
+def attn_impl(request):
+    """tcgen05 at 2 CTAs/SM (P^T in TMEM, the default), tcgen05 at 1 CTA/SM, mma.sync."""
+    from paper_2407_02327_b200._lib import call
+    call("qsync_attention_set_impl", request.param)
+    yield request.param
+    call("qsync_attention_set_impl", 2)
+
+
 @pytest.mark.parametrize("B,H,amp", [(4, 12, 1.0), (2, 3, 4.0), (32, 12, 0.5)])
-def test_attention_fwd_bwd_vs_fp32(B, H, amp):
+def test_attention_fwd_bwd_vs_fp32(B, H, amp, attn_impl):
     torch.manual_seed(B * 100 + H)
     S, D = 128, 64
     qkv = (torch.randn(B, S, 3, H, D, device=DEV) * amp).half()
@@ -61,7 +70,25 @@ def test_attention_fwd_tcgen05_vs_mma_sync():
     try:
         o0, l0, a0 = ops.attention_fwd(qkv, want_absmax=True)
     finally:
-        call("qsync_attention_set_impl", 1)
+        call("qsync_attention_set_impl", 2)
     assert _rel(o1, o0) < 2e-3
     assert (l1 - l0).abs().max().item() < 1e-4
     assert a1.item() == o1.float().abs().max().item()
+
+
+def test_attention_bwd_tmem_p_matches_smem_p():
+    """The 2-CTA/SM backward (P^T kept in tensor memory, dV's A operand read from
+    TMEM) equals the 1-CTA/SM one (P^T staged in shared memory): same FP16 P,
+    same MMA shapes."""
+    from paper_2407_02327_b200._lib import call
+    torch.manual_seed(31)
+    qkv = torch.randn(16, 128, 3, 12, 64, device=DEV).half()
+    dout = torch.randn(16, 128, 12, 64, device=DEV).half()
+    out, lse, _ = ops.attention_fwd(qkv)
+    call("qsync_attention_set_impl", 1)
+    try:
+        d1 = ops.attention_bwd(qkv, out, dout, lse)
+    finally:
+        call("qsync_attention_set_impl", 2)
+    d2 = ops.attention_bwd(qkv, out, dout, lse)
+    assert _rel(d2, d1) < 1e-3

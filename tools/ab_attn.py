@@ -1,4 +1,6 @@
-"""A/B the graphed BERT-base step: tcgen05 vs mma.sync attention core."""
+"""A/B the graphed BERT-base step over the attention-core implementations
+(0 mma.sync, 1 tcgen05, 2 tcgen05 backward at 2 CTAs / SM):
+    python tools/ab_attn.py [impl ...]"""
 import os
 import sys
 
@@ -30,5 +32,5 @@ def step_ms(tc, steps=50):
     return s.elapsed_time(e) / steps
 
 
-for tc in (1, 0, 1, 0, 1, 0):
+for tc in [int(a) for a in (sys.argv[1:] or ["2", "1", "2", "1", "0"])]:
     print(f"attn_tc={tc} step_ms={step_ms(tc):.3f}", flush=True)
