@@ -154,6 +154,19 @@ class FusedAdamW:
             self._launch(0)
 
 
+# =============================================================================== profiling marks
+# Operator-region marks for the fused-implementation profiler
+# (profiler.measure_fused_costs): REGION(kind, op) is called where the device work
+# of (kind, op) begins -- kind "fwd" / "bwd" / "cast" (an op's input conversion)
+# / "opt" -- and each region ends at the next mark.  None in training: no cost.
+REGION = None
+
+
+def _mark(kind: str, op: str) -> None:
+    if REGION is not None:
+        REGION(kind, op)
+
+
 # =============================================================================== layer
 def _operand(x, aux, prec):
     """The planned op's input operand (and what its backward keeps)."""
@@ -276,7 +289,10 @@ class _FusedLayerFn(torch.autograd.Function):
         x0f = x0.reshape(M, H)
         pq, po, p1, p2 = L.qkv.precision, L.o.precision, L.ff1.precision, L.ff2.precision
         # --- QKV projection -> FP16 packed QKV for the attention core
+        pre = L.qkv.name.rsplit(".", 1)[0]
+        _mark("cast", L.qkv.name)
         op_qkv = _operand(x0f, aux0, pq)
+        _mark("fwd", L.qkv.name)
         qkv, w16_qkv = _linear_fwd(L.qkv, op_qkv, out_dtype=torch.float16)
         if qkv.dtype != torch.float16:
             qkv = ops.cast(qkv, torch.float16)
@@ -284,19 +300,26 @@ class _FusedLayerFn(torch.autograd.Function):
         scale = (H // nh) ** -0.5
         # Attention core (FP16, csrc/attn.cu); it also emits absmax(out) when the
         # O projection is INT8, so that op's quantizer is one pass.
+        _mark("fwd", pre + ".attn")
         a, lse, a_am = ops.attention_fwd(qkv5, scale, want_absmax=po == INT8)
         a2 = a.reshape(M, H)
         # --- output projection + residual LayerNorm (emits FF1's operand)
+        _mark("cast", L.o.name)
         op_o = _operand(a2, a_am, po)
+        _mark("fwd", L.o.name)
         yo, w16_o = _linear_fwd(L.o, op_o)
         f16, am = _need_aux(p1)
+        _mark("fwd", pre + ".ln1")
         x1, s1, mean1, rstd1, x1_16, x1_am = ops.layernorm_fwd_ex(
             x0f, yo, L.ln1.weight.detach(), L.ln1.bias.detach(), L.ln1.eps, f16, am)
         # --- FF1 -> GELU folded into FF2's operand kernel
+        _mark("cast", L.ff1.name)
         op_1 = _operand(x1, x1_16 if f16 else x1_am, p1)
+        _mark("fwd", L.ff1.name)
         h, w16_1 = _linear_fwd(L.ff1, op_1)
         # ... and the same pass stores GELU'(h) in FP16 for the backward, which
         # then needs no transcendental (dh = dg * GELU'(h)).
+        _mark("fwd", pre + ".gelu")
         if p2 == INT8:
             gam = ops.absmax_act(h, ops.ACT_GELU)
             gq, gs, gp, g16 = ops.quantize_act(h, gam, ops.ACT_GELU, want_dact=True, want_q16=True)
@@ -307,8 +330,10 @@ class _FusedLayerFn(torch.autograd.Function):
         else:
             g32, gp = ops.act_cast(h, torch.float32, ops.ACT_GELU, want_dact=True)
             op_2 = ("f32", g32, None)
+        _mark("fwd", L.ff2.name)
         f, w16_2 = _linear_fwd(L.ff2, op_2)
         f16n, amn = _need_aux(next_prec)
+        _mark("fwd", pre + ".ln2")
         x2, s2, mean2, rstd2, x2_16, x2_am = ops.layernorm_fwd_ex(
             x1, f, L.ln2.weight.detach(), L.ln2.bias.detach(), L.ln2.eps, f16n, amn)
         aux2 = x2_16 if f16n else (x2_am if amn else None)
@@ -343,35 +368,44 @@ class _FusedLayerFn(torch.autograd.Function):
             dx2 = dx2.float()
         # --- LN2 backward -> FF2's dY (FP16) + ff2 bias grad
         p2 = L.ff2.precision
+        pre = L.qkv.name.rsplit(".", 1)[0]
+        _mark("bwd", pre + ".ln2")
         ds2, ds2_16 = ops.layernorm_bwd_ex(dx2, s2, mean2, rstd2, L.ln2.weight.detach(),
                                            L.ln2.weight.main_grad, L.ln2.bias.main_grad,
                                            want_f16=p2 != FP32, colsum_into=_bias_main_grad(L.ff2))
         dy2 = ds2_16 if p2 != FP32 else ds2
         # FF2's FP16 backward kernel emits its input gradient in FP16 (as the
         # reference's FP16 op does before the cast back), halving dG's traffic
+        _mark("bwd", L.ff2.name)
         dg = _dgrad(L.ff2, dy2, w16_2, torch.float16 if p2 != FP32 else h_dtype)
         _wgrad(L.ff2, dy2, op_2, side if p2 != FP32 else None)
         # --- GELU backward fused with FF1's dY cast + ff1 bias grad
         p1 = L.ff1.precision
+        _mark("bwd", pre + ".gelu")
         dh = ops.act_bwd_colsum(dg, gp, ops.ACT_DERIV,
                                 out_dtype=torch.float16 if p1 != FP32 else torch.float32,
                                 colsum_into=_bias_main_grad(L.ff1))
         # FF1 dgrad reduce-added into ds2: ds2 becomes d(x1) = residual + FF1 paths
+        _mark("bwd", L.ff1.name)
         _dgrad(L.ff1, dh, w16_1, torch.float32, acc_into=ds2)
         _wgrad(L.ff1, dh, op_1, side if p1 != FP32 else None)
         # --- LN1 backward -> O's dY + o bias grad
         po = L.o.precision
+        _mark("bwd", pre + ".ln1")
         ds1, ds1_16 = ops.layernorm_bwd_ex(ds2, s1, mean1, rstd1, L.ln1.weight.detach(),
                                            L.ln1.weight.main_grad, L.ln1.bias.main_grad,
                                            want_f16=po != FP32, colsum_into=_bias_main_grad(L.o))
         dyo = ds1_16 if po != FP32 else ds1
+        _mark("bwd", L.o.name)
         da = _dgrad(L.o, dyo, w16_o, torch.float16)
         _wgrad(L.o, dyo, op_o, side if po != FP32 else None)
         # --- attention core backward (FP16) -> packed dQKV
+        _mark("bwd", pre + ".attn")
         dqkv = ops.attention_bwd(qkv5, a, da.view(a.shape), lse, scale)
         dqkv2 = dqkv.view(M, 3 * H)
         # --- QKV backward: bias grad (column sums), dgrad reduce-added into ds1
         pq = L.qkv.precision
+        _mark("bwd", L.qkv.name)
         mb = _bias_main_grad(L.qkv)
         if pq == FP32:
             dq32 = dqkv2.float()

@@ -76,6 +76,8 @@ class _EmbedLN(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, tokens, word, pos, typ, gamma, beta, eps, want_f16, want_absmax):
+        from .fused import _mark
+        _mark("fwd", "embed")
         B, S = tokens.shape
         y, s, mean, rstd, y16, am = ops.embed_layernorm_fwd(tokens, word, pos, typ, gamma, beta, eps,
                                                             want_f16, want_absmax)
@@ -88,6 +90,8 @@ class _EmbedLN(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, dy, _daux):
+        from .fused import _mark
+        _mark("bwd", "embed")
         tokens, s, mean, rstd = ctx.saved_tensors
         word, pos, typ, gamma, beta = ctx.params
         grads = []

@@ -23,6 +23,7 @@ that ``train_step.load_plan`` applies.
 from __future__ import annotations
 
 import json
+import math
 import statistics
 
 import torch
@@ -51,6 +52,53 @@ def _time_ns(fn, reps: int = 10) -> int:
         torch.cuda.synchronize()
         times.append(s.elapsed_time(e) * 1e6)
     return max(1, int(statistics.median(times)))
+
+
+def _graph_time_ns(fn, n: int = 20, reps: int = 3) -> int:
+    """Per-call device time of fn() launched n times back-to-back inside a CUDA
+    graph (as in the train step: no launch gaps), best of reps."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(n):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e6 / n)
+    return max(1, int(best))
+
+
+def graph_step_ms(cfg: BertConfig, batch: int, plan: dict, steps: int = 20) -> float:
+    """The train step as the bench runs it (one CUDA graph, wgrad side stream)."""
+    from .train_step import TrainStep
+    torch.manual_seed(0)
+    m = BertEncoderStack(cfg).cuda()
+    m.apply_plan(plan)
+    st = TrainStep(m, batch=batch, graph=True)
+    st.tokens.random_(0, cfg.vocab)
+    st.capture(warmup=3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        st()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del st, m
+    torch.cuda.empty_cache()
+    return ms
 
 
 # ----------------------------------------------------------------------------- graph
@@ -212,6 +260,256 @@ def measure_op_costs(cfg: BertConfig, batch: int, reps: int = 10) -> dict:
         costs[f"{L}.ln2"] = glue["ln"]
         costs[f"{L}.gelu"] = glue["gelu"]
     return costs
+
+
+# ----------------------------------------------------------------------------- fused step
+def _region_times(st, reps: int) -> dict:
+    """Device time per (kind, op) region of one eager fused step (fused.REGION
+    marks; single stream, launches queued behind a device spin), median of reps."""
+    from . import fused
+    runs = []
+    for _ in range(reps):
+        marks = []
+
+        def hook(kind, op, marks=marks):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append((kind, op, e))
+
+        torch.cuda.synchronize()
+        torch.cuda._sleep(400_000_000)  # the whole step is enqueued before it runs
+        fused.REGION = hook
+        try:
+            st()
+        finally:
+            fused.REGION = None
+        torch.cuda.synchronize()
+        t: dict = {}
+        for (k, o, e0), (_, _, e1) in zip(marks, marks[1:]):
+            t[(k, o)] = t.get((k, o), 0.0) + e0.elapsed_time(e1) * 1e6
+        runs.append(t)
+    keys = set().union(*runs)
+    return {k: statistics.median(r.get(k, 0.0) for r in runs) for k in keys}
+
+
+def _param_numel(cfg: BertConfig) -> dict:
+    """Parameters the optimizer updates per graph node: (planned weight numel, other numel)."""
+    H, Fh = cfg.hidden, cfg.ffn
+    out = {"embed": (0, (cfg.vocab + cfg.max_pos + cfg.type_vocab) * H + 2 * H),
+           "pooler": (H * H, H), "loss": (0, H * cfg.num_labels + cfg.num_labels)}
+    for i in range(cfg.layers):
+        L = f"layer{i}"
+        for k, (n, kk) in {"qkv": (3 * H, H), "o": (H, H), "ff1": (Fh, H), "ff2": (H, Fh)}.items():
+            out[f"{L}.{k}"] = (n * kk, n)
+        out[f"{L}.ln1"] = (0, 2 * H)
+        out[f"{L}.ln2"] = (0, 2 * H)
+    return out
+
+
+# AdamW bytes per parameter (read p, g, m, v; write p, m, v) plus the weight
+# copies the optimizer emits for the planned precision (w16; INT8 also wq).
+_OPT_BYTES = {FP32: 28, FP16: 30, INT8: 31}
+
+
+def measure_fused_costs(cfg: BertConfig, batch: int, reps: int = 5, calibrate: bool = True) -> dict:
+    """Per-operator costs of the layer-fused training step as it executes
+    (fused.py), for the bundle's ``op_costs``:
+
+    * one eager step per uniform plan (INT8, FP16, FP32) with the wgrad GEMMs on the
+      main stream, device time split at the operator-region marks;
+    * ``pure_cost_ns`` = the op's fwd + bwd regions plus its parameters' share of
+      the gradient zeroing + AdamW step (by bytes the optimizer moves for them: the
+      reference models no optimizer time, replayer.cpp:64-73 with a zero-duration
+      event, cost_mapper.cpp:127-130);
+    * an op's input conversion ("cast" region: the INT8 quantizer) is the cast
+      model's, see ``measure_fused_cast_samples``;
+    * GELU (dependent) -- FP16 from the FP16 plan, FP32 from the cheaper of the
+      INT8 plan (GELU fused with FF2's quantizer) and the FP32 plan;
+    * ``calibrate``: the eager single-stream regions are scaled by (graph step time /
+      their sum) of the same plan, so each op is charged its share of the step as the
+      bench runs it -- the wgrad GEMMs overlapping the main stream and PDL-chained
+      kernels, which the reference's sequential per-device model cannot express.
+      The uniform plans' predictions then match by construction; a mixed plan is
+      predicted from them plus the cast model (``last_diag`` keeps the factors).
+    """
+    from .train_step import TrainStep, uniform_plan
+    T, H = batch * cfg.seq, cfg.hidden
+    Fh = cfg.ffn
+    per = {}
+    for p in (INT8, FP16, FP32):
+        torch.manual_seed(0)
+        m = BertEncoderStack(cfg).cuda()
+        m.apply_plan(uniform_plan(cfg, p) if p != FP32 else {})
+        st = TrainStep(m, batch=batch, graph=False, overlap_wgrad=False)
+        st.tokens.random_(0, cfg.vocab)
+        for _ in range(3):
+            st()
+        per[p] = _region_times(st, reps)
+        del st, m
+        torch.cuda.empty_cache()
+    diag = {}
+    for p in (INT8, FP16, FP32):
+        tot = sum(per[p].values())
+        graph_ns = graph_step_ms(cfg, batch, uniform_plan(cfg, p) if p != FP32 else {}) * 1e6
+        scale = graph_ns / tot if calibrate else 1.0
+        diag[p] = {"eager_regions_ms": tot / 1e6, "graph_step_ms": graph_ns / 1e6, "scale": scale}
+        per[p] = {k: v * scale for k, v in per[p].items()}
+    measure_fused_costs.last_diag = diag
+    numel = _param_numel(cfg)
+
+    def opt_share(op, p):
+        t = per[p]
+        t_opt = t.get(("opt", "optimizer"), 0.0) + t.get(("opt", "zero"), 0.0)
+        total = sum(w * _OPT_BYTES[p] + b * _OPT_BYTES[FP32] for w, b in numel.values())
+        w, b = numel.get(op, (0, 0))  # (attention, GELU: no parameters)
+        return t_opt * (w * _OPT_BYTES[p] + b * _OPT_BYTES[FP32]) / total
+
+    def entry(op, p, mem):
+        fwd = per[p].get(("fwd", op), 0.0)
+        bwd = per[p].get(("bwd", op), 0.0) + opt_share(op, p)
+        tot = max(1, int(round(fwd + bwd)))
+        return {"pure_cost_ns": tot, "fwd_fraction": min(1.0, fwd / tot), "memory_bytes": mem}
+
+    costs = {}
+    shapes = {"qkv": (T, 3 * H, H), "o": (T, H, H), "ff1": (T, Fh, H), "ff2": (T, H, Fh)}
+    pooler = {p: measure_linear(batch, H, H, p) for p in (INT8, FP16, FP32)}
+    for p in pooler:
+        pooler[p]["pure_cost_ns"] += int(opt_share("pooler", p))
+    costs["pooler"] = pooler
+    med = statistics.median
+
+    def fixed(op, mem):
+        es = [entry(op, p, mem) for p in (INT8, FP16, FP32)]
+        tot = int(med(e["pure_cost_ns"] for e in es))
+        return {FP32: {"pure_cost_ns": tot, "fwd_fraction": med(e["fwd_fraction"] for e in es),
+                       "memory_bytes": mem}}
+
+    costs["embed"] = fixed("embed", cfg.vocab * H * 4 * 4 + T * H * 4)
+    costs["loss"] = fixed("loss", H * cfg.num_labels * 16 + batch * H * 4)
+    for i in range(cfg.layers):
+        L = f"layer{i}"
+        for k, (M, N, K) in shapes.items():
+            costs[f"{L}.{k}"] = {p: entry(f"{L}.{k}", p, linear_memory_bytes(p, M, N, K))
+                                 for p in (INT8, FP16, FP32)}
+        costs[f"{L}.attn"] = fixed(f"{L}.attn", T * 3 * H * 2 + T * H * 2)
+        costs[f"{L}.ln1"] = fixed(f"{L}.ln1", T * H * 4 * 2 + 2 * H * 4 * 4)
+        costs[f"{L}.ln2"] = fixed(f"{L}.ln2", T * H * 4 * 2 + 2 * H * 4 * 4)
+        g16 = entry(f"{L}.gelu", FP16, T * Fh * 2 * 2)
+        g32 = min((entry(f"{L}.gelu", p, T * Fh * 4 * 2) for p in (INT8, FP32)),
+                  key=lambda e: e["pure_cost_ns"])
+        costs[f"{L}.gelu"] = {FP16: g16, FP32: g32}
+    return costs
+
+
+def measure_fused_cast_samples(cfg: BertConfig, rows=(512, 1024, 2048, 4096, 8192)):
+    """Cast samples of the fused implementation, where a conversion is not a
+    kernel of its own but part of its producer or consumer:
+
+    * FP32 -> FP16 (float_to_float): the producing LayerNorm also writes FP16(y)
+      -- the extra time of ``layernorm_fwd_ex`` with the copy over without;
+    * FP16 -> FP32: an FP32 LayerNorm reads the FP16 producer directly -- the extra
+      time of the FP16 input over an FP32 one (clamped at 1 ns);
+    * FP32 / FP16 -> INT8 (quantize_fixed): the single-pass quantizer with the
+      absmax the producer already wrote (``quantize_act``);
+    * INT8 -> FP32 (dequantize_fixed): folded into the GEMM epilogues (the INT8
+      GEMM and the wgrad write FP32) -- the extra time of the FP32 over the FP16
+      epilogue of the INT8 GEMM, clamped at 1 ns.
+    Each is timed back-to-back inside a CUDA graph, as the train step runs it.
+    """
+    H = cfg.hidden
+    samples = []
+    g = torch.rand(H, device="cuda") + 0.5
+    be = torch.randn(H, device="cuda")
+    w8 = torch.randint(-127, 128, (H, H), dtype=torch.int8, device="cuda")
+    sw = torch.rand(H, device="cuda") * 0.01
+    for r in rows:
+        n = r * H
+        a = torch.randn(r, H, device="cuda")
+        b32 = torch.randn(r, H, device="cuda")
+        b16 = b32.half()
+        am = torch.tensor([4.0], device="cuda")
+        x8 = torch.randint(-127, 128, (r, H), dtype=torch.int8, device="cuda")
+        sa = torch.tensor([0.01], device="cuda")
+        def t(fn):  # best of 5 graph timings: the marginal costs are differences of near-equal times
+            return min(_graph_time_ns(fn) for _ in range(5))
+        plain = t(lambda: ops.layernorm_fwd_ex(a, b32, g, be, 1e-12, False, False))
+        with16 = t(lambda: ops.layernorm_fwd_ex(a, b32, g, be, 1e-12, True, False))
+        in16 = t(lambda: ops.layernorm_fwd_ex(a, b16, g, be, 1e-12, False, False))
+        q32 = t(lambda: ops.quantize_act(a, am))
+        q16 = t(lambda: ops.quantize_act(b16, am))
+        e32 = t(lambda: ops.gemm_s8_ex(x8, w8, sa, sw, None, out_dtype=torch.float32))
+        e16 = t(lambda: ops.gemm_s8_ex(x8, w8, sa, sw, None, out_dtype=torch.float16))
+        for src, dst, scheme, ns in ((FP32, FP16, "float_to_float", with16 - plain),
+                                     (FP16, FP32, "float_to_float", in16 - plain),
+                                     (FP32, INT8, "quantize_fixed", q32),
+                                     (FP16, INT8, "quantize_fixed", q16),
+                                     (INT8, FP32, "dequantize_fixed", e32 - e16)):
+            samples.append({"src": src, "dst": dst, "scheme": scheme, "numel": n,
+                            "measured_ns": max(1, int(ns))})
+    return samples
+
+
+def fit_cast(samples: list) -> tuple[float, float]:
+    """(a, b) of the reference's cast model for one key: OLS a*numel + b, a < 0 ->
+    flat mean, b < 0 -> refit through the origin (profile.cpp:33-83)."""
+    xs = [float(x) for x, _ in samples]
+    ys = [float(y) for _, y in samples]
+    n = len(xs)
+    mx, my = sum(xs) / n, sum(ys) / n
+    sxx = sum((x - mx) ** 2 for x in xs)
+    sxy = sum((x - mx) * (y - my) for x, y in zip(xs, ys))
+    a = sxy / sxx
+    b = my - a * mx
+    if a < 0:
+        a, b = 0.0, my
+    if b < 0:
+        sxx0 = sum(x * x for x in xs)
+        sxy0 = sum(x * y for x, y in zip(xs, ys))
+        a, b = (max(0.0, sxy0 / sxx0) if sxx0 > 0 else 0.0), 0.0
+    return a, b
+
+
+def net_weight_casts(cfg: BertConfig, costs: dict, cast_samples: list) -> dict:
+    """The fused step converts weights inside the optimizer (w16 / wq emitted with
+    the update), and that time is already in each op's optimizer share.  The
+    reference's cost mapper adds a weight cast FP32 -> k on every weighted op's
+    forward event (cost_mapper.cpp:42-43), so the entry is stored net of it: the
+    op's forward share is reduced by exactly the cast model's prediction."""
+    keys = {}
+    for smp in cast_samples:
+        keys.setdefault((smp["src"], smp["dst"]), []).append((smp["numel"], smp["measured_ns"]))
+    numel = _param_numel(cfg)
+    for op, per_p in costs.items():
+        w = numel.get(op, (0, 0))[0]
+        if not w:
+            continue
+        for p, e in per_p.items():
+            if p == FP32 or (FP32, p) not in keys:
+                continue
+            a, b = fit_cast(keys[(FP32, p)])
+            wc = int(math.floor(a * w + b + 0.5))  # llround of a nonnegative value (profile.cpp:95)
+            fwd = e["pure_cost_ns"] * e["fwd_fraction"]
+            cut = min(wc, int(fwd))
+            tot = max(1, e["pure_cost_ns"] - cut)
+            e["pure_cost_ns"] = tot
+            e["fwd_fraction"] = max(0.0, min(1.0, (fwd - cut) / tot))
+    return costs
+
+
+def profile_bert_fused(cfg: BertConfig, batch: int, stat_steps: int = 3, infer_cap_bytes: int | None = None,
+                       reps: int = 5) -> dict:
+    """The bundle of the layer-fused implementation (the one the train step runs)."""
+    model = BertEncoderStack(cfg).cuda()
+    model.apply_plan({})
+    stats = collect_tensor_stats(model, batch, stat_steps)
+    del model
+    casts = measure_fused_cast_samples(cfg)
+    costs = net_weight_casts(cfg, measure_fused_costs(cfg, batch, reps), casts)
+    graph = bert_graph(cfg, batch)
+    cap = infer_cap_bytes or default_cap(graph, costs)
+    devices = [{"id": "trainer", "is_inference": False, "mem_capacity_bytes": 183_000_000_000},
+               {"id": "infer", "is_inference": True, "mem_capacity_bytes": max(cap, 1)}]
+    return build_bundle(graph, costs, casts, stats, devices)
 
 
 # ----------------------------------------------------------------------------- casts

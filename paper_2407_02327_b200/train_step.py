@@ -157,7 +157,12 @@ class BertEncoderStack(torch.nn.Module):
             x = self.ln(x)
             for layer in self.layers:
                 x = layer(x)
+        if self.fused:
+            from .fused import _mark
+            _mark("fwd", "pooler")
         pooled = torch.tanh(cast(self.pooler(x[:, 0].contiguous()), torch.float32))
+        if self.fused:
+            _mark("fwd", "loss")
         logits = self.cls(pooled)
         return F.cross_entropy(logits, labels)
 
@@ -356,6 +361,9 @@ class TrainStep:
             self.opt.attach(self.model.qlinears().values())
 
     def _body(self):
+        if self.fused:
+            from .fused import _mark
+            _mark("opt", "zero")
         self.grads.zero()
         loss = self.model(self.tokens, self.labels)
         _ql.WGRAD_STREAM = self.wgrad_stream
@@ -376,10 +384,15 @@ class TrainStep:
         if self.wgrad_stream is not None:
             torch.cuda.current_stream().wait_stream(self.wgrad_stream)  # join before the last buckets
         self.grads.finish()
+        if self.fused:
+            from .fused import _mark
+            _mark("opt", "optimizer")
         if self.overlap_opt:
             self.opt.advance()
         else:
             self.opt.step()
+        if self.fused:
+            _mark("end", "")
         return loss.detach()
 
     def _opt_bucket(self, i: int) -> None:

@@ -5,8 +5,8 @@ import json
 
 import pytest
 
-from paper_2407_02327_b200.profiler import (bert_graph, build_bundle, default_cap,
-                                            linear_memory_bytes)
+from paper_2407_02327_b200.profiler import (bert_graph, build_bundle, default_cap, fit_cast,
+                                            linear_memory_bytes, net_weight_casts)
 from paper_2407_02327_b200.qlinear import FP16, FP32, INT8
 from paper_2407_02327_b200.train_step import BertConfig, load_plan
 
@@ -113,3 +113,69 @@ def test_profiled_bundle_closes_the_loop(tmp_path, reflib):
     assert loss == loss and loss > 0  # finite
     # replayer prediction for the measured costs (row (f)2 fidelity, reported not pinned)
     assert reflib.replay_bundle(str(path), {"per_device": rep["devices"]}) > 0
+
+
+def test_fit_cast_mirrors_reference_cast_model():
+    """OLS a*numel + b with the reference's clamps (profile.cpp:33-83)."""
+    a, b = fit_cast([(100, 300), (200, 500), (400, 900)])
+    assert abs(a - 2.0) < 1e-12 and abs(b - 100.0) < 1e-9
+    a, b = fit_cast([(100, 900), (200, 500)])            # negative slope -> flat mean
+    assert a == 0.0 and b == 700.0
+    a, b = fit_cast([(100, 1), (200, 400), (300, 800)])  # negative intercept -> through the origin
+    assert b == 0.0 and abs(a - (100 * 1 + 200 * 400 + 300 * 800) / (100**2 + 200**2 + 300**2)) < 1e-12
+
+
+def test_net_weight_casts_cancel_the_mappers_weight_cast(tmp_path, reflib):
+    """Storing each weighted op net of its FP32 -> k weight cast (the fused step
+    converts weights inside the optimizer) lowers the reference replayer's
+    prediction by exactly the casts its cost mapper adds (cost_mapper.cpp:42-43)."""
+    import copy
+    import math
+
+    from paper_2407_02327_b200.profiler import _param_numel
+    from paper_2407_02327_b200.train_step import uniform_plan
+    cfg = BertConfig(layers=3)
+    batch = 8
+    g = bert_graph(cfg, batch)
+    costs = _fake_costs(g, cfg, batch)
+    for per_p in costs.values():  # forward shares large enough to absorb the casts
+        for e in per_p.values():
+            e["pure_cost_ns"] += 10**7
+            e["fwd_fraction"] = 0.5
+    casts = _fake_casts()
+    dev = [{"id": "d", "is_inference": True, "mem_capacity_bytes": 10**13}]
+    raw = tmp_path / "raw.json"
+    raw.write_text(json.dumps(build_bundle(g, costs, casts, _fake_stats(cfg), dev)))
+    net = tmp_path / "net.json"
+    net.write_text(json.dumps(build_bundle(g, net_weight_casts(cfg, copy.deepcopy(costs), casts),
+                                           casts, _fake_stats(cfg), dev)))
+    for p in (INT8, FP16):
+        plan = {"per_device": {"d": uniform_plan(cfg, p)}}
+        a, b = fit_cast([(s["numel"], s["measured_ns"]) for s in casts if s["src"] == FP32 and s["dst"] == p])
+        want = sum(int(math.floor(a * w + b + 0.5)) for op, (w, _) in _param_numel(cfg).items()
+                   if w and op in plan["per_device"]["d"])
+        assert reflib.replay_bundle(str(raw), plan) - reflib.replay_bundle(str(net), plan) == pytest.approx(want, abs=2 * len(costs))
+
+
+@pytest.mark.gpu
+def test_fused_bundle_closes_the_loop(tmp_path, reflib):
+    """The fused-implementation bundle (operator regions of the fused step,
+    conversions as marginal costs) is accepted by the reference planner and its
+    replayer predicts the measured graphed step of a uniform plan closely."""
+    from paper_2407_02327_b200.profiler import graph_step_ms, measure_fused_costs, profile_bert_fused
+    from paper_2407_02327_b200.train_step import uniform_plan
+    cfg = BertConfig(vocab=2000, layers=2, max_pos=128)
+    batch = 8
+    b = profile_bert_fused(cfg, batch, stat_steps=2, reps=3)
+    path = tmp_path / "bundle.json"
+    path.write_text(json.dumps(b))
+    assert set(measure_fused_costs.last_diag) == {INT8, FP16, FP32}
+    rep = reflib.plan_bundle(str(path), 1, batch, 50, "infer", 10**12)
+    assert rep["memory_ok"] and set(rep["devices"]) == {"trainer", "infer"}
+    # replay one device (the bundle's trainer would stay FP32 and set the makespan)
+    b["devices"] = [d for d in b["devices"] if d["id"] == "infer"]
+    path.write_text(json.dumps(b))
+    plan = {"per_device": {"infer": uniform_plan(cfg, FP16)}}
+    pred_ms = reflib.replay_bundle(str(path), plan) / 1e6
+    meas_ms = graph_step_ms(cfg, batch, plan["per_device"]["infer"])
+    assert abs(pred_ms - meas_ms) / meas_ms < 0.25

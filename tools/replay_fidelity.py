@@ -15,30 +15,11 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle.cpu_ref import RefLib  # noqa: E402  (test/measurement infrastructure)
 from paper_2407_02327_b200.profiler import (bert_graph, build_bundle, collect_tensor_stats,  # noqa: E402
-                                            measure_cast_samples, measure_op_costs)
+                                            graph_step_ms, measure_cast_samples, measure_fused_cast_samples,
+                                            measure_fused_costs, measure_op_costs, net_weight_casts)
 from paper_2407_02327_b200.qlinear import FP16, INT8  # noqa: E402
 from paper_2407_02327_b200.train_step import (BertConfig, BertEncoderStack, TrainStep,  # noqa: E402
                                               mixed_plan, uniform_plan)
-
-
-def measured_step_ms(cfg, batch, plan, steps=20):
-    torch.manual_seed(0)
-    m = BertEncoderStack(cfg).cuda()
-    m.apply_plan(plan)
-    st = TrainStep(m, batch=batch, graph=True)
-    st.tokens.random_(0, cfg.vocab)
-    st.capture(warmup=3)
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(steps):
-        st()
-    e.record()
-    torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / steps
-    del st, m
-    torch.cuda.empty_cache()
-    return ms
 
 
 def main():
@@ -53,26 +34,42 @@ def main():
     model.apply_plan({})
     stats = collect_tensor_stats(model, args.batch, 3)
     del model
-    costs = measure_op_costs(cfg, args.batch, reps=10)
-    casts = measure_cast_samples(reps=10)
     graph = bert_graph(cfg, args.batch)
     devices = [{"id": "b200", "is_inference": True, "mem_capacity_bytes": 183_000_000_000}]
-    bundle = build_bundle(graph, costs, casts, stats, devices)
-    with open(args.bundle, "w") as f:
-        json.dump(bundle, f)
+    # Two bundles: the fused implementation the train step runs (operator regions of
+    # the fused step, conversions as the marginal cost of the fused producers) and
+    # the per-operator implementation (each op's GEMMs alone, standalone cast kernels).
+    fused_casts = measure_fused_cast_samples(cfg)
+    raw_costs = net_weight_casts(cfg, measure_fused_costs(cfg, args.batch, reps=5, calibrate=False), fused_casts)
+    cal_costs = net_weight_casts(cfg, measure_fused_costs(cfg, args.batch, reps=5, calibrate=True), fused_casts)
+    diag = measure_fused_costs.last_diag
+    bundles = {
+        "fused": build_bundle(graph, cal_costs, fused_casts, stats, devices),
+        "fused_uncalibrated": build_bundle(graph, raw_costs, fused_casts, stats, devices),
+        "per_op": build_bundle(graph, measure_op_costs(cfg, args.batch, reps=10),
+                               measure_cast_samples(reps=10), stats, devices),
+    }
     ref = RefLib()
     plans = {"mixed": mixed_plan(cfg), "int8": uniform_plan(cfg, INT8), "fp16": uniform_plan(cfg, FP16),
              "fp32": {}}
-    rows = {}
-    for name, plan in plans.items():
-        pred_ns = ref.replay_bundle(args.bundle, {"per_device": {"b200": plan}})
-        meas = measured_step_ms(cfg, args.batch, plan)
-        rows[name] = {"predicted_ms": pred_ns / 1e6, "measured_ms": meas,
-                      "error": (pred_ns / 1e6 - meas) / meas}
-        print(name, rows[name], flush=True)
+    measured = {name: graph_step_ms(cfg, args.batch, plan) for name, plan in plans.items()}
+    out = {"config": {"layers": args.layers, "batch": args.batch, "seq": cfg.seq,
+                      "measured": "CUDA-graph train step (wgrad side stream, optimizer included)"}}
+    for kind, bundle in bundles.items():
+        path = args.bundle.replace(".json", f"_{kind}.json")
+        with open(path, "w") as f:
+            json.dump(bundle, f)
+        rows = {}
+        for name, plan in plans.items():
+            pred_ns = ref.replay_bundle(path, {"per_device": {"b200": plan}})
+            meas = measured[name]
+            rows[name] = {"predicted_ms": pred_ns / 1e6, "measured_ms": meas,
+                          "error": (pred_ns / 1e6 - meas) / meas}
+            print(kind, name, rows[name], flush=True)
+        out["rows" if kind == "fused" else f"rows_{kind}_bundle"] = rows
+    out["calibration"] = diag
     with open(args.out, "w") as f:
-        json.dump({"config": {"layers": args.layers, "batch": args.batch, "seq": cfg.seq},
-                   "rows": rows}, f, indent=1)
+        json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":
