@@ -7,10 +7,11 @@
 //   colsum += sum_rows g   (optional; the Linear's bias gradient, FP32)
 //
 // Layout: row-major [rows, cols].  A block of 8 warps owns a 256-column strip
-// and 64 rows; each lane owns 8 consecutive columns (one 16-byte FP16 vector,
-// two FP32 vectors) and walks 8 rows, so every warp access is a contiguous
-// 512 B (FP16) / 1 KB (FP32) row segment.  Column partials are reduced through
-// shared memory, then one FP32 atomic per column per block.  HBM-bound:
+// and a chunk of rows sized so the grid is one resident wave; each lane owns 8
+// consecutive columns (one 16-byte FP16 vector, two FP32 vectors) and walks
+// chunk/8 rows, so every warp access is a contiguous 512 B (FP16) / 1 KB (FP32)
+// row segment.  Column partials are reduced through shared memory, then one
+// FP32 atomic per column per block.  HBM-bound:
 // algorithmic bytes per element = size(dy) + size(h) + size(out).
 #include <algorithm>
 
@@ -21,9 +22,7 @@ namespace qsb {
 namespace {
 
 constexpr int kCols = 256;      // columns per block (32 lanes x 8)
-constexpr int kRowsPerWarp = 8;
 constexpr int kWarps = 8;
-constexpr int kRows = kRowsPerWarp * kWarps;  // rows per block
 
 template <int DT>
 __device__ __forceinline__ void load8v(const void* base, int64_t i, float* f) {
@@ -66,54 +65,64 @@ __device__ __forceinline__ void store1(void* base, int64_t i, float v) {
 }
 
 template <int DDY, int DH, int DO, int ACT>
+__device__ __forceinline__ void act_row8(const void* __restrict__ dy, const void* __restrict__ h,
+                                         void* __restrict__ out, int64_t off, int64_t c, int64_t cols,
+                                         bool full, float (&g)[8]) {
+    if (full) {
+        load8v<DDY>(dy, off, g);
+        if constexpr (ACT == 1) {
+            float hv[8];
+            load8v<DH>(h, off, hv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) g[j] = __fmul_rn(g[j], gelu_erf_grad(hv[j]));
+        } else if constexpr (ACT == 2) {  // h holds act'(x) (FP16), stored by the forward
+            float hv[8];
+            load8v<QSYNC_F16>(h, off, hv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) g[j] = __fmul_rn(g[j], hv[j]);
+        }
+        if (out) store8v<DO>(out, off, g);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            g[j] = 0.0f;
+            if (c + j < cols) {
+                g[j] = load1<DDY>(dy, off + j);
+                if constexpr (ACT == 1) g[j] = __fmul_rn(g[j], gelu_erf_grad(load1<DH>(h, off + j)));
+                if constexpr (ACT == 2) g[j] = __fmul_rn(g[j], load1<QSYNC_F16>(h, off + j));
+                if (out) store1<DO>(out, off + j, g[j]);
+            }
+        }
+    }
+}
+
+// Grid = (256-column strips) x (row chunks), the chunk height chosen so the whole
+// grid is ONE resident wave (a fixed 64-row chunk left a 4% tail wave at
+// [4096, 3072]); each block reduces its column partials once.
+template <int DDY, int DH, int DO, int ACT>
 __global__ void __launch_bounds__(kWarps * 32) k_act_bwd_colsum(const void* __restrict__ dy,
                                                                 const void* __restrict__ h,
                                                                 int64_t rows, int64_t cols,
                                                                 void* __restrict__ out,
                                                                 float* __restrict__ colsum,
-                                                                int vec_ok) {
+                                                                int vec_ok, int chunk) {
     QSB_PDL_ENTER();
     __shared__ float red[kWarps][kCols];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t c = static_cast<int64_t>(blockIdx.x) * kCols + lane * 8;
-    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kRows + warp * kRowsPerWarp;
+    const int per_warp = chunk / kWarps;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * chunk + warp * per_warp;
     float cs[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) cs[j] = 0.0f;
     const bool full = vec_ok && c + 8 <= cols;
 #pragma unroll 4
-    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+    for (int rr = 0; rr < per_warp; ++rr) {
         const int64_t r = r0 + rr;
         if (r >= rows) break;
-        const int64_t off = r * cols + c;
         float g[8];
-        if (full) {
-            load8v<DDY>(dy, off, g);
-            if constexpr (ACT == 1) {
-                float hv[8];
-                load8v<DH>(h, off, hv);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) g[j] = __fmul_rn(g[j], gelu_erf_grad(hv[j]));
-            } else if constexpr (ACT == 2) {  // h holds act'(x) (FP16), stored by the forward
-                float hv[8];
-                load8v<QSYNC_F16>(h, off, hv);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) g[j] = __fmul_rn(g[j], hv[j]);
-            }
-            if (out) store8v<DO>(out, off, g);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                g[j] = 0.0f;
-                if (c + j < cols) {
-                    g[j] = load1<DDY>(dy, off + j);
-                    if constexpr (ACT == 1) g[j] = __fmul_rn(g[j], gelu_erf_grad(load1<DH>(h, off + j)));
-                    if constexpr (ACT == 2) g[j] = __fmul_rn(g[j], load1<QSYNC_F16>(h, off + j));
-                    if (out) store1<DO>(out, off + j, g[j]);
-                }
-            }
-        }
+        act_row8<DDY, DH, DO, ACT>(dy, h, out, r * cols + c, c, cols, full, g);
 #pragma unroll
         for (int j = 0; j < 8; ++j) cs[j] += g[j];
     }
@@ -134,8 +143,23 @@ template <int DDY, int DH, int DO, int ACT>
 int launch_act_bwd(const void* dy, const void* h, int64_t rows, int64_t cols, void* out,
                    float* colsum, cudaStream_t st) {
     const int vec = (cols % 8 == 0) && aligned16(dy) && (!h || aligned16(h)) && (!out || aligned16(out));
-    dim3 grid(static_cast<unsigned>((cols + kCols - 1) / kCols), static_cast<unsigned>((rows + kRows - 1) / kRows));
-    pdl_launch(k_act_bwd_colsum<DDY, DH, DO, ACT>, dim3(grid), dim3(kWarps * 32), 0, st, dy, h, rows, cols, out, colsum, vec);
+    static int per_sm = 0;
+    if (!per_sm) {
+        QSB_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                &per_sm, k_act_bwd_colsum<DDY, DH, DO, ACT>, kWarps * 32, 0),
+                            "cudaOccupancyMaxActiveBlocksPerMultiprocessor"));
+        per_sm = std::max(per_sm, 1);
+    }
+    const int64_t strips = (cols + kCols - 1) / kCols;
+    const int64_t slots = int64_t(sm_count()) * per_sm;
+    const int64_t chunks_want = std::max<int64_t>(1, slots / strips);
+    int64_t chunk = (rows + chunks_want - 1) / chunks_want;
+    chunk = std::max<int64_t>(kWarps, (chunk + kWarps - 1) / kWarps * kWarps);  // whole rows per warp
+    const int64_t chunks = (rows + chunk - 1) / chunk;
+    QSB_REQUIRE(chunks < 65535 && chunk < (int64_t(1) << 30), QSYNC_ERR_DOMAIN, "too many rows");
+    dim3 grid(static_cast<unsigned>(strips), static_cast<unsigned>(chunks));
+    pdl_launch(k_act_bwd_colsum<DDY, DH, DO, ACT>, grid, dim3(kWarps * 32), 0, st, dy, h, rows, cols, out,
+               colsum, vec, static_cast<int>(chunk));
     return check_launch("k_act_bwd_colsum");
 }
 
@@ -167,7 +191,6 @@ int qsync_act_bwd_colsum(const void* dy, int dy_dtype, const void* h, int h_dtyp
                          qsync_stream_t stream) {
     QSB_REQUIRE(dy != nullptr, QSYNC_ERR_VALIDATION, "dy is required");
     QSB_REQUIRE(rows >= 0 && cols >= 0, QSYNC_ERR_DOMAIN, "negative shape");
-    QSB_REQUIRE(rows / kRows < 65535, QSYNC_ERR_DOMAIN, "too many rows");
     QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU || act == QSYNC_ACT_DERIV, QSYNC_ERR_DOMAIN,
                 "unknown activation");
     QSB_REQUIRE(act == QSYNC_ACT_NONE || h != nullptr, QSYNC_ERR_VALIDATION, "activation backward needs h");

@@ -44,6 +44,8 @@ def cases():
     colF = torch.zeros(F, device=d)
     yield "act_bwd f32,f32->f16", lambda: ops.act_bwd_colsum(dg32, h32, ops.ACT_GELU, torch.float16, colF), T * F * 10
     yield "act_bwd f16,f16->f16", lambda: ops.act_bwd_colsum(dg16, h16, ops.ACT_GELU, torch.float16, colF), T * F * 6
+    # as in the step: FP16 dG x the stored FP16 GELU'(h) -> FP16 dH + bias sums
+    yield "act_bwd deriv f16 (step)", lambda: ops.act_bwd_colsum(dg16, h16, ops.ACT_DERIV, torch.float16, colF), T * F * 6
     q16 = torch.randn(T, 3 * H, device=d).half()
     col3 = torch.zeros(3 * H, device=d)
     yield "colsum f16 (qkv bias)", lambda: ops.act_bwd_colsum(q16, None, ops.ACT_NONE, None, col3), T * 3 * H * 2

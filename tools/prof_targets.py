@@ -45,11 +45,23 @@ def main(name: str, reps: int = 3) -> None:
         y, s_, m, r = ops.layernorm_fwd(a, a, g, be, 1e-12)
         dg, db, col = (torch.zeros(H, device=dev) for _ in range(3))
         fn = lambda: ops.layernorm_bwd_ex(a, s_, m, r, g, dg, db, True, col)  # noqa: E731
-    elif name == "act_bwd":
-        dg = torch.randn(T, F, device=dev)
-        h = torch.randn(T, F, device=dev)
+    elif name == "act_bwd":  # as in the step: FP16 dG (FF2's dgrad) x stored FP16 GELU'(h)
+        dg = torch.randn(T, F, device=dev).half()
+        gp = torch.rand(T, F, device=dev).half()
         col = torch.zeros(F, device=dev)
-        fn = lambda: ops.act_bwd_colsum(dg, h, ops.ACT_GELU, torch.float16, col)  # noqa: E731
+        fn = lambda: ops.act_bwd_colsum(dg, gp, ops.ACT_DERIV, torch.float16, col)  # noqa: E731
+    elif name in ("conv_fwd", "conv_wgrad", "conv_dgrad"):
+        # ResNet-50 res3 3x3 (batch 64, 28x28, 128 -> 128), FP16 implicit GEMM (TMA im2col)
+        N, Hc, C, Co = 64, 28, 128, 128
+        x = torch.randn(N, Hc, Hc, C, device=dev).half()
+        w = (torch.randn(Co, 3, 3, C, device=dev) * 0.03).half()
+        dy = torch.randn(N, Hc, Hc, Co, device=dev).half()
+        dw = torch.zeros(Co, 9 * C, device=dev)
+        fn = {"conv_fwd": lambda: ops.conv_fwd_implicit(x, w.view(Co, -1), 3, 3, (1, 1), (1, 1),
+                                                        out_dtype=torch.float16),
+              "conv_wgrad": lambda: ops.conv_wgrad_implicit(x, dy.view(-1, Co), 3, 3, (1, 1), (1, 1), out=dw,
+                                                            accumulate=True),
+              "conv_dgrad": lambda: ops.conv_dgrad_implicit(dy, w, (N, Hc, Hc, C), (1, 1), (1, 1))}[name]
     elif name == "adamw":
         from paper_2407_02327_b200.fused import FusedAdamW
         from paper_2407_02327_b200.train_step import BertConfig, BertEncoderStack, FlatGrads, mixed_plan

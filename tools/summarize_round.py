@@ -24,7 +24,9 @@ ALG = {  # algorithmic flops (GEMM) or bytes (streaming) per launch
     "gemm_f16_ff1": (2.0 * T * F * H, "flops"),
     "attn_fwd": (32 * 12 * (3 * 128 * 64 * 2 + 128 * 64 * 2 + 128 * 4), "bytes"),
     "attn_bwd": (32 * 12 * (5 * 128 * 64 * 2 + 128 * 4 + 3 * 128 * 64 * 2), "bytes"),
-    "ln_bwd": (T * H * (4 + 4 + 4 + 2), "bytes"), "act_bwd": (T * F * (4 + 4 + 2), "bytes"),
+    "ln_bwd": (T * H * (4 + 4 + 4 + 2), "bytes"), "act_bwd": (T * F * (2 + 2 + 2), "bytes"),
+    "conv_fwd": (2.0 * 64 * 28 * 28 * 128 * 9 * 128, "flops"), "conv_wgrad": (2.0 * 64 * 28 * 28 * 128 * 9 * 128, "flops"),
+    "conv_dgrad": (2.0 * 64 * 28 * 28 * 128 * 9 * 128, "flops"),
     "quantize_with_scale": ((1 << 28) * 5, "bytes"), "quantize_per_channel": ((1 << 28) * 5, "bytes"),
     "absmax": ((1 << 28) * 4, "bytes"), "stats": ((1 << 28) * 4, "bytes"), "cast": ((1 << 28) * 6, "bytes"),
     "dequantize": ((1 << 28) * 5, "bytes"),
