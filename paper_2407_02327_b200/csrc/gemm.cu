@@ -873,6 +873,7 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     // anyway (accumulating FP32 output, e.g. wgrad into the flat main_grad).
     const int64_t bk_elems = BK_BYTES / eb;
     const int64_t num_kb = (p.K + bk_elems - 1) / bk_elems;
+    const int preset = p.ksplit;  // chosen by dispatch (choose_acc), 0 = decide here
     p.ksplit = 1;
     p.kb_per = static_cast<int>(num_kb);
     const int sms = sm_count();
@@ -881,6 +882,12 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     if (g_force_splitk > 0) {
         if (can_split && g_force_splitk > 1) {
             const int64_t per = (num_kb + g_force_splitk - 1) / g_force_splitk;
+            p.kb_per = static_cast<int>(per);
+            p.ksplit = static_cast<int>((num_kb + per - 1) / per);
+        }
+    } else if (can_split && preset > 0) {
+        if (preset > 1) {
+            const int64_t per = (num_kb + preset - 1) / preset;
             p.kb_per = static_cast<int>(per);
             p.ksplit = static_cast<int>((num_kb + per - 1) / per);
         }
@@ -957,6 +964,39 @@ Shape pick_shape(int64_t M, int64_t N, bool allow_pair) {
     return best;
 }
 
+// Tile width and split-K of an accumulating FP32 GEMM (wgrad into main_grad),
+// chosen together: a unit (tile, K range) costs its k-blocks x max(MMA, L2
+// feed) cycles plus a fixed pipeline fill + reduce-add epilogue; the GEMM costs
+// waves x that.  E.g. wgrad QKV 2304x768x4096 -> 192-wide tiles split 2 ways =
+// 144 units, one wave; wgrad FF1/FF2 -> 256-wide split 2 ways (not 4: two
+// waves of half-length units).
+struct AccChoice {
+    int bn, ksplit;
+};
+AccChoice choose_acc(int64_t M, int64_t N, int64_t num_kb) {
+    int slots = sm_count();
+    if (g_max_ctas > 0) slots = std::min(slots, g_max_ctas);
+    AccChoice best{256, 1};
+    double best_cost = 1e300;
+    for (int bn : {256, 192, 128}) {
+        const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+        const double kb_cost = std::max(4.0 * BM * bn / 256.0, (BM + bn) * 128.0 / 64.0);
+        const double fixed = 1500.0 + 8.0 * bn;
+        for (int ks = 1; ks <= 16; ++ks) {
+            const int64_t per = (num_kb + ks - 1) / ks;
+            if (ks > 1 && per < 4) break;
+            const int64_t units = tiles * ((num_kb + per - 1) / per);
+            const int64_t waves = (units + slots - 1) / slots;
+            const double cost = static_cast<double>(waves) * (static_cast<double>(per) * kb_cost + fixed);
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = {bn, ks};
+            }
+        }
+    }
+    return best;
+}
+
 template <bool kI8, int kLay>
 int dispatch_shape(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p,
                    cudaStream_t st, Shape sh) {
@@ -983,7 +1023,15 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     // Accumulating FP32 GEMMs (wgrad) go split-K on single-CTA 256-wide tiles.
     const bool accumulating = !kI8 && p.accumulate && p.c_dtype == QSYNC_F32;
     Shape sh = pick_shape(p.M, p.N, g_force_cta != 1 && !accumulating);
-    if (splitk_ok || accumulating) sh.bn = 256;
+    if (splitk_ok) sh.bn = 256;
+    if (accumulating && !splitk_ok && !force_bn && g_force_splitk == 0 && !(layout & 108)) {
+        const AccChoice c = choose_acc(p.M, p.N, (p.K + 63) / 64);
+        sh.bn = c.bn;
+        sh.cta = 1;
+        p.ksplit = c.ksplit;
+    } else if (accumulating) {
+        sh.bn = 256;
+    }
     if (force_bn) sh.bn = force_bn;
     if (g_force_cta) sh.cta = g_force_cta;
     if (sh.cta == 2 && (sh.bn == 64 || sh.bn == 192)) sh.cta = 1;  // pairs: BN/2 a multiple of 64
