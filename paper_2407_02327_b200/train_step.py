@@ -312,7 +312,8 @@ class TrainStep:
     + AdamW on FP32 master weights.  Optionally captured into a CUDA graph."""
 
     def __init__(self, model: BertEncoderStack, batch: int, world: int = 1, lr: float = 1e-4,
-                 graph: bool = True, overlap_wgrad: bool = True, fused: bool = True):
+                 graph: bool = True, overlap_wgrad: bool = True, fused: bool = True,
+                 overlap_opt: bool | None = None):
         self.model = model
         self.world = world
         cfg = model.cfg
@@ -347,8 +348,8 @@ class TrainStep:
         # Bucket-wise optimizer (DP): each bucket's AdamW runs on the comm stream
         # right after its all-reduce, overlapping the remaining buckets' reductions
         # and the rest of the backward.  On one GPU it only contends with the
-        # backward for HBM (measured 5.41 vs 5.35 ms), so it is off there.
-        self.overlap_opt = fused and world > 1
+        # backward for HBM (tools/ab_overlap_opt.py: 5.01 vs 4.97 ms), so it is off there.
+        self.overlap_opt = fused and (world > 1 if overlap_opt is None else overlap_opt)
         if (world > 1 or self.overlap_opt) and fused:
             for m in (model.pooler, model.cls):
                 for prm in m.parameters():
