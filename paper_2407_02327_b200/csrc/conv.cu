@@ -220,6 +220,52 @@ int make_geom(ConvGeom& g, int64_t N, int64_t H, int64_t W, int64_t C, int R, in
     return QSYNC_OK;
 }
 
+// Narrow C (the stem's C = 3): one THREAD per 16-byte chunk of the column matrix
+// (a warp per row would leave 22 of 32 lanes idle on a 160-byte row); the chunk's
+// elements step (c, s, r) incrementally, no division per element.
+template <typename T>
+__global__ void __launch_bounds__(256) k_im2col_narrow(const T* __restrict__ x, ConvGeom g,
+                                                       T* __restrict__ out) {
+    constexpr int V = 16 / sizeof(T);
+    const int C = static_cast<int>(g.C);
+    const int K = g.R * g.S * C;
+    const int nch = static_cast<int>(g.ld / V);
+    const int P = static_cast<int>(g.P), Q = static_cast<int>(g.Q);
+    const int64_t items = g.N * g.P * g.Q * nch;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < items;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int row = static_cast<int>(i / nch);
+        const int j = static_cast<int>(i - static_cast<int64_t>(row) * nch);
+        const int q = row % Q, p = (row / Q) % P, n = row / (Q * P);
+        const int h0 = p * g.sh - g.ph, w0 = q * g.sw - g.pw;
+        const T* xn = x + static_cast<int64_t>(n) * g.H * g.W * C;
+        const int k0 = j * V;
+        int tap = k0 / C;
+        int c = k0 - tap * C;
+        int r = tap / g.S, ss = tap - r * g.S;
+        union {
+            uint4 u;
+            T e[V];
+        } v;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            T val = T(0);
+            const int h = h0 + r * g.dh, w = w0 + ss * g.dw;
+            if (k0 + e < K && h >= 0 && h < g.H && w >= 0 && w < g.W)
+                val = xn[(static_cast<int64_t>(h) * g.W + w) * C + c];
+            v.e[e] = val;
+            if (++c == C) {
+                c = 0;
+                if (++ss == g.S) {
+                    ss = 0;
+                    ++r;
+                }
+            }
+        }
+        *reinterpret_cast<uint4*>(out + static_cast<int64_t>(row) * g.ld + k0) = v.u;
+    }
+}
+
 int grid_of(int64_t warps_of_work) {  // blocks of 8 warps
     const int64_t cap = static_cast<int64_t>(sm_count()) * 16;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((warps_of_work + 7) / 8, cap)));
@@ -255,15 +301,23 @@ int qsync_im2col(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int6
                         : (g.ld % 16 == 0 && al(out))                          ? 2
                                                                                : 0;
         const int64_t work = g.N * g.P * g.Q;
-        k_im2col<int8_t><<<grid_of(work), 256, 0, st>>>(static_cast<const int8_t*>(x), g,
-                                                         static_cast<int8_t*>(out), vec);
+        if (vec == 2)
+            k_im2col_narrow<int8_t><<<grid_of(work * (g.ld / 16) / 32 + 1), 256, 0, st>>>(
+                static_cast<const int8_t*>(x), g, static_cast<int8_t*>(out));
+        else
+            k_im2col<int8_t><<<grid_of(work), 256, 0, st>>>(static_cast<const int8_t*>(x), g,
+                                                             static_cast<int8_t*>(out), vec);
     } else if (dtype == QSYNC_F16 || dtype == QSYNC_BF16) {
         const int vec = (C % 8 == 0) && (g.ld % 8 == 0) && al(x) && al(out) ? 1
                         : (g.ld % 8 == 0 && al(out))                         ? 2
                                                                              : 0;
         const int64_t work = g.N * g.P * g.Q;
-        k_im2col<uint16_t><<<grid_of(work), 256, 0, st>>>(static_cast<const uint16_t*>(x), g,
-                                                           static_cast<uint16_t*>(out), vec);
+        if (vec == 2)
+            k_im2col_narrow<uint16_t><<<grid_of(work * (g.ld / 8) / 32 + 1), 256, 0, st>>>(
+                static_cast<const uint16_t*>(x), g, static_cast<uint16_t*>(out));
+        else
+            k_im2col<uint16_t><<<grid_of(work), 256, 0, st>>>(static_cast<const uint16_t*>(x), g,
+                                                               static_cast<uint16_t*>(out), vec);
     } else {
         return set_error(QSYNC_ERR_DOMAIN, "im2col supports I8, F16 and BF16 inputs");
     }
