@@ -305,6 +305,13 @@ int qsync_quantize_act(const void* x, int dtype, int64_t n, int act, const float
  * the operand the op's FP16 wgrad reads in the backward (no separate cast). */
 int qsync_quantize_act_ex(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,
                           float* scale_out, uint16_t* dact_out, uint16_t* q16_out, qsync_stream_t stream);
+/* y = GELU(x) in x's format (F32 / F16: the value the GELU-prologue quantizer
+ * would quantize), dact_out (optional, F16) = GELU'(x) from the same erf, and
+ * *absmax (device float, overwritten) = max |y|.  FF2's INT8 operand is then
+ * qsync_quantize_act(y, ..., QSYNC_ACT_NONE): bit-identical q and s to the
+ * GELU-prologue form, with one GELU evaluation instead of two. */
+int qsync_gelu_absmax_store(const void* x, int dtype, int64_t n, float* absmax, void* y, uint16_t* dact_out,
+                            qsync_stream_t stream);
 /* out = act(x) cast to dst_dtype (F32/F16 -> F32/F16); optional FP16 act'(x). */
 int qsync_act_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64_t n, int act,
                    uint16_t* dact_out, qsync_stream_t stream);

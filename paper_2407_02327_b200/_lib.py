@@ -72,6 +72,7 @@ SIGNATURES = {
     "qsync_absmax_act": [_p, _int, _i64, _int, _p, _p],
     "qsync_quantize_act": [_p, _int, _i64, _int, _p, _p, _p, _p, _p],
     "qsync_quantize_act_ex": [_p, _int, _i64, _int, _p, _p, _p, _p, _p, _p],
+    "qsync_gelu_absmax_store": [_p, _int, _i64, _p, _p, _p, _p],
     "qsync_act_cast": [_p, _int, _p, _int, _i64, _int, _p, _p],
     "qsync_act_bwd_colsum": [_p, _int, _p, _int, _i64, _i64, _int, _p, _int, _p, _p],
     "qsync_gemm_s8_ex": [_p, _p, _i64, _i64, _i64, _p, _int, _p, _p, _int, _p, _p],

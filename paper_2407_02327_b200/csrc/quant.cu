@@ -104,6 +104,81 @@ __global__ void __launch_bounds__(kThreads) k_absmax(const typename Elem<DT>::T*
     }
 }
 
+// FF2's INT8 operand in two passes with ONE GELU evaluation: this pass computes
+// g = GELU(x) (rounded to x's format, the cascade rule) and GELU'(x) from one
+// erf, writes both, and reduces absmax(g); the quantizer then reads g with no
+// activation (a pure HBM pass) instead of recomputing the erf.  g is the value
+// k_quantize<DT, 1> would quantize, so q / s are bit-identical.
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_gelu_absmax_store(const typename Elem<DT>::T* __restrict__ x,
+                                                                int64_t n, unsigned* __restrict__ out,
+                                                                typename Elem<DT>::T* __restrict__ y,
+                                                                uint16_t* __restrict__ dact, int vec_ok) {
+    QSB_PDL_ENTER();
+    using V = Vec<DT>;
+    using T = typename Elem<DT>::T;
+    float m = 0.0f;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t done = 0;
+    if (vec_ok) {
+        const int64_t n8 = n / 8;  // 8 elements per step: 2 (F32) or 1 (F16) 16 B loads
+        for (int64_t i = tid; i < n8; i += stride) {
+            float f[8];
+            if constexpr (DT == QSYNC_F32) {
+                const uint4* xv = reinterpret_cast<const uint4*>(x) + 2 * i;
+                V::unpack(ld_stream(xv), f);
+                V::unpack(ld_stream(xv + 1), f + 4);
+            } else {
+                V::unpack(ld_stream(reinterpret_cast<const uint4*>(x) + i), f);
+            }
+            float g[8];
+            uint32_t dp[4];
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+                float d0, d1;
+                gelu_and_grad(f[j], g[j], d0);
+                gelu_and_grad(f[j + 1], g[j + 1], d1);
+                g[j] = round_to<DT>(g[j]);
+                g[j + 1] = round_to<DT>(g[j + 1]);
+                m = fmaxf(m, fmaxf(fabsf(g[j]), fabsf(g[j + 1])));
+                dp[j / 2] = pack_half2(d0, d1);
+            }
+            if constexpr (DT == QSYNC_F32) {
+                float4* yv = reinterpret_cast<float4*>(y) + 2 * i;
+                yv[0] = make_float4(g[0], g[1], g[2], g[3]);
+                yv[1] = make_float4(g[4], g[5], g[6], g[7]);
+            } else {
+                reinterpret_cast<uint4*>(y)[i] = make_uint4(pack_half2(g[0], g[1]), pack_half2(g[2], g[3]),
+                                                            pack_half2(g[4], g[5]), pack_half2(g[6], g[7]));
+            }
+            if (dact) reinterpret_cast<uint4*>(dact)[i] = make_uint4(dp[0], dp[1], dp[2], dp[3]);
+        }
+        done = n8 * 8;
+    }
+    for (int64_t i = done + tid; i < n; i += stride) {
+        float g, d;
+        gelu_and_grad(Elem<DT>::f(x[i]), g, d);
+        g = round_to<DT>(g);
+        m = fmaxf(m, fabsf(g));
+        if constexpr (DT == QSYNC_F32)
+            y[i] = g;
+        else
+            y[i] = __float2half_rn(g);
+        if (dact) dact[i] = __half_as_ushort(__float2half_rn(d));
+    }
+    __shared__ float red[32];
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0 && m > 0.0f) atomicMax(out, __float_as_uint(m));
+    }
+    (void)sizeof(T);
+}
+
 // absmax of each row, one warp per row.
 template <int DT>
 __global__ void __launch_bounds__(256) k_absmax_rows(const typename Elem<DT>::T* __restrict__ x,
@@ -919,6 +994,20 @@ struct AbsmaxActRun {
 };
 
 template <int DT>
+struct GeluAbsmaxStoreRun {
+    static int run(const void* x, int64_t n, float* absmax, void* y, uint16_t* dact, cudaStream_t st) {
+        using T = typename Elem<DT>::T;
+        QSB_TRY(cuda_status(cudaMemsetAsync(absmax, 0, sizeof(float), st), "memset"));
+        if (n == 0) return QSYNC_OK;
+        const int vec = aligned16(x) && aligned16(y) && (!dact || aligned16(dact));
+        const int grid = grid_for(n / 8 + 1, kThreads, 4);
+        pdl_launch(k_gelu_absmax_store<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n,
+                   reinterpret_cast<unsigned*>(absmax), static_cast<T*>(y), dact, vec);
+        return check_launch("k_gelu_absmax_store");
+    }
+};
+
+template <int DT>
 struct QuantActRun {
     static int run(const void* x, int64_t n, int act, const float* absmax, int8_t* q,
                    float* scale_out, uint16_t* dact, uint16_t* q16, cudaStream_t st) {
@@ -1065,6 +1154,16 @@ int qsync_quantize_act(const void* x, int dtype, int64_t n, int act, const float
     QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU, QSYNC_ERR_DOMAIN, "unknown activation");
     return dispatch_dtype<QuantActRun>(dtype, x, n, act, absmax, q, scale_out, dact_out,
                                        static_cast<uint16_t*>(nullptr), to_stream(stream));
+}
+
+int qsync_gelu_absmax_store(const void* x, int dtype, int64_t n, float* absmax, void* y, uint16_t* dact_out,
+                            qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    QSB_REQUIRE(absmax != nullptr && y != nullptr, QSYNC_ERR_VALIDATION, "absmax and y are required");
+    QSB_REQUIRE(dtype == QSYNC_F32 || dtype == QSYNC_F16, QSYNC_ERR_DOMAIN, "x must be F32 or F16");
+    if (dtype == QSYNC_F32)
+        return GeluAbsmaxStoreRun<QSYNC_F32>::run(x, n, absmax, y, dact_out, to_stream(stream));
+    return GeluAbsmaxStoreRun<QSYNC_F16>::run(x, n, absmax, y, dact_out, to_stream(stream));
 }
 
 int qsync_quantize_act_ex(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,

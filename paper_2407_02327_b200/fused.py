@@ -321,8 +321,11 @@ class _FusedLayerFn(torch.autograd.Function):
         # then needs no transcendental (dh = dg * GELU'(h)).
         _mark("fwd", pre + ".gelu")
         if p2 == INT8:
-            gam = ops.absmax_act(h, ops.ACT_GELU)
-            gq, gs, gp, g16 = ops.quantize_act(h, gam, ops.ACT_GELU, want_dact=True, want_q16=True)
+            # one GELU evaluation: g (and GELU') stored with the absmax pass, the
+            # quantizer then a pure streaming pass over g (bit-identical q, s)
+            gam, g_act, gp = ops.gelu_absmax_store(h)
+            gq, gs, g16 = ops.quantize_act(g_act, gam, want_q16=True)
+            del g_act
             op_2 = ("i8", gq, gs, g16)
         elif p2 == FP16:
             g16, gp = ops.act_cast(h, torch.float16, ops.ACT_GELU, want_dact=True)

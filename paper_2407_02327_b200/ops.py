@@ -473,6 +473,16 @@ def quantize_act(x: torch.Tensor, absmax: torch.Tensor, act: int = ACT_NONE, wan
     return out
 
 
+def gelu_absmax_store(x: torch.Tensor, want_dact: bool = True):
+    """(absmax[1], y = GELU(x) in x's dtype, GELU'(x) FP16 or None) from one erf per element."""
+    _req(x, "x", (torch.float32, torch.float16))
+    am = torch.empty(1, device=x.device, dtype=torch.float32)
+    y = torch.empty_like(x)
+    d = torch.empty(x.shape, device=x.device, dtype=torch.float16) if want_dact else None
+    call("qsync_gelu_absmax_store", _ptr(x), _DT[x.dtype], x.numel(), _ptr(am), _ptr(y), _ptr(d), _stream())
+    return am, y, d
+
+
 def act_cast(x: torch.Tensor, dtype: torch.dtype, act: int = ACT_NONE, out=None, want_dact: bool = False):
     """act(x) as dtype; with ``want_dact`` returns (y, act'(x) FP16)."""
     _req(x, "x", (torch.float32, torch.float16))

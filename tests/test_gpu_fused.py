@@ -321,3 +321,19 @@ def test_quantize_act_q16_is_exact_copy(act, n):
     q, s, q16 = ops.quantize_act(h, am, act, want_q16=True)
     assert torch.equal(q, q0) and torch.equal(s, s0)
     assert q16.dtype == torch.float16 and torch.equal(q16, q.to(torch.float16))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16])
+@pytest.mark.parametrize("n", [4096 * 3072, 1000003])
+def test_gelu_absmax_store_then_quantize_is_bit_identical(dtype, n):
+    """FF2's INT8 operand via gelu_absmax_store + a plain quantize equals the
+    GELU-prologue absmax + quantize (q, s, FP16 q copy and GELU' all bit-identical)."""
+    torch.manual_seed(n % 97)
+    h = (torch.randn(n, device=DEV) * 2).to(dtype)
+    am0 = ops.absmax_act(h, ops.ACT_GELU)
+    q0, s0, d0, h0 = ops.quantize_act(h, am0, ops.ACT_GELU, want_dact=True, want_q16=True)
+    am, g, d = ops.gelu_absmax_store(h)
+    q, s, h16 = ops.quantize_act(g, am, want_q16=True)
+    assert am.item() == am0.item()
+    assert torch.equal(g, ops.act_cast(h, dtype, ops.ACT_GELU))
+    assert torch.equal(q, q0) and torch.equal(s, s0) and torch.equal(h16, h0) and torch.equal(d, d0)

@@ -52,6 +52,14 @@ def cases():
     am = ops.absmax_act(h32, ops.ACT_GELU)
     yield "absmax gelu f32", lambda: ops.absmax_act(h32, ops.ACT_GELU, out=am), T * F * 4
     yield "quantize gelu f32", lambda: ops.quantize_act(h32, am, ops.ACT_GELU), T * F * 5
+    # FF2's INT8 operand as the step builds it: the old two-erf form vs one erf + stored GELU
+    yield "ff2 int8 operand: absmax+quantize gelu (2 erf)", lambda: ops.quantize_act(
+        h32, ops.absmax_act(h32, ops.ACT_GELU), ops.ACT_GELU, want_dact=True, want_q16=True), T * F * (4 + 4 + 1 + 2 + 2)
+
+    def one_erf():
+        am2, g, _ = ops.gelu_absmax_store(h32)
+        ops.quantize_act(g, am2, want_q16=True)
+    yield "ff2 int8 operand: gelu_absmax_store+quantize (1 erf)", one_erf, T * F * (4 + 4 + 1 + 2 + 2)
     yield "absmax gelu f16", lambda: ops.absmax_act(h16, ops.ACT_GELU, out=am), T * F * 2
     yield "gelu cast f16->f16", lambda: ops.act_cast(h16, torch.float16, ops.ACT_GELU), T * F * 4
     yield "absmax f32 (act)", lambda: ops.absmax(a), T * H * 4
