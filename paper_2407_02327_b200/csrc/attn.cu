@@ -893,7 +893,7 @@ int qsync_attention_fwd(const void* qkv, int64_t B, int64_t S, int64_t H, int64_
                             "cudaFuncSetAttribute"));
         configured = true;
     }
-    if (out_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(out_absmax, 0, sizeof(float), st), "memset"));
+    if (out_absmax) QSB_TRY(zero_async(out_absmax, sizeof(float), st));
     if (g_attn_tc) {
         static bool tc_configured = false;
         if (!tc_configured) {

@@ -55,6 +55,26 @@ int check_launch(const char* what) {
     return set_error(QSYNC_ERR_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Zero n 32-bit words as a kernel launched with PDL (an accumulator such as a
+// device absmax before the atomicMax kernel that produces it).  A memset node
+// would break the programmatic-dependent chain of the CUDA graph: the next
+// kernel could no longer overlap its launch and prologue with this one.
+__global__ void k_zero_words(uint32_t* __restrict__ p, int64_t n) {
+    QSB_PDL_ENTER();
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = 0u;
+}
+
+int zero_async(void* p, int64_t bytes, cudaStream_t st) {
+    if (!p || bytes <= 0) return QSYNC_OK;
+    QSB_REQUIRE(bytes % 4 == 0 && (reinterpret_cast<uintptr_t>(p) & 3) == 0, QSYNC_ERR_DOMAIN,
+                "zero_async needs 4-byte words");
+    const int64_t n = bytes / 4;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 1024));
+    return launch_pdl("k_zero_words", k_zero_words, dim3(grid), dim3(256), 0, st, static_cast<uint32_t*>(p), n);
+}
+
 int sm_count() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 148;

@@ -39,6 +39,8 @@ inline int cuda_status(cudaError_t e, const char* what) {
 inline cudaStream_t to_stream(qsync_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+// Zero `bytes` (a multiple of 4) as a PDL kernel (keeps the graph's kernel chain).
+int zero_async(void* p, int64_t bytes, cudaStream_t st);
 // 2-D SWIZZLE_128B TMA map (row pitch = inner * elem_bytes), defined in gemm.cu.
 int make_tma_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes, int64_t inner,
                 int64_t outer, uint32_t box_inner, uint32_t box_outer);

@@ -352,7 +352,7 @@ template <int NV>
 int ln_fwd_nv(const float* a, const void* b, int b_dtype, const float* gamma, const float* beta,
               int64_t rows, int cols, float eps, float* s_out, float* y, float* mean, float* rstd,
               uint16_t* y16, float* y_absmax, cudaStream_t st) {
-    if (y_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(y_absmax, 0, sizeof(float), st), "memset"));
+    if (y_absmax) QSB_TRY(zero_async(y_absmax, sizeof(float), st));
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 8LL));
     if (b_dtype == QSYNC_F16)
         pdl_launch(k_ln_fwd<NV, QSYNC_F16>, dim3(grid), dim3(256), 0, st, a, static_cast<const __half*>(b), gamma, beta,
@@ -392,7 +392,7 @@ template <int NV>
 int embed_ln_fwd_nv(const int64_t* tok, int64_t rows, int seq, const float* word, const float* pos,
                     const float* typ, const float* gamma, const float* beta, int cols, float eps, float* s_out,
                     float* y, float* mean, float* rstd, uint16_t* y16, float* y_absmax, cudaStream_t st) {
-    if (y_absmax) QSB_TRY(cuda_status(cudaMemsetAsync(y_absmax, 0, sizeof(float), st), "memset"));
+    if (y_absmax) QSB_TRY(zero_async(y_absmax, sizeof(float), st));
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 8LL));
     pdl_launch(k_ln_fwd<NV, QSYNC_F32>, dim3(grid), dim3(256), 0, st, word, static_cast<const float*>(nullptr), gamma, beta, rows, cols, eps, s_out, y, mean,
                                                   rstd, reinterpret_cast<__half*>(y16),

@@ -884,7 +884,7 @@ template <int DT>
 struct AbsmaxRun {
     static int run(const void* x, int64_t n, float* absmax, cudaStream_t st) {
         using T = typename Elem<DT>::T;
-        QSB_TRY(cuda_status(cudaMemsetAsync(absmax, 0, sizeof(float), st), "memset"));
+        QSB_TRY(zero_async(absmax, sizeof(float), st));
         if (n == 0) return QSYNC_OK;
         const int vec = aligned16(x);
         const int grid = grid_for(n / Vec<DT>::N + 1, kThreads * 4);
@@ -950,7 +950,7 @@ struct CastTRun {
                    int64_t ld_t, float* colsum, int colsum_accumulate, cudaStream_t st) {
         using T = typename Elem<DT>::T;
         if (colsum && !colsum_accumulate)
-            QSB_TRY(cuda_status(cudaMemsetAsync(colsum, 0, sizeof(float) * cols, st), "memset"));
+            QSB_TRY(zero_async(colsum, sizeof(float) * cols, st));
         if (rows == 0 || cols == 0) return QSYNC_OK;
         dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
         const int vt = (cols % 4 == 0) && aligned16(x) && aligned16(out) && aligned16(out_t);
@@ -979,7 +979,7 @@ template <int DT>
 struct AbsmaxActRun {
     static int run(const void* x, int64_t n, int act, float* absmax, cudaStream_t st) {
         using T = typename Elem<DT>::T;
-        QSB_TRY(cuda_status(cudaMemsetAsync(absmax, 0, sizeof(float), st), "memset"));
+        QSB_TRY(zero_async(absmax, sizeof(float), st));
         if (n == 0) return QSYNC_OK;
         const int vec = aligned16(x);
         const int grid = grid_for(n / Vec<DT>::N + 1, kThreads * 4);
@@ -997,7 +997,7 @@ template <int DT>
 struct GeluAbsmaxStoreRun {
     static int run(const void* x, int64_t n, float* absmax, void* y, uint16_t* dact, cudaStream_t st) {
         using T = typename Elem<DT>::T;
-        QSB_TRY(cuda_status(cudaMemsetAsync(absmax, 0, sizeof(float), st), "memset"));
+        QSB_TRY(zero_async(absmax, sizeof(float), st));
         if (n == 0) return QSYNC_OK;
         const int vec = aligned16(x) && aligned16(y) && (!dact || aligned16(dact));
         const int grid = grid_for(n / 8 + 1, kThreads, 4);
