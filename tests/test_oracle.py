@@ -186,6 +186,21 @@ def test_library_exports_every_declared_symbol():
         assert s in _lib.SIGNATURES, s
 
 
+def test_python_signatures_match_header_arity():
+    """Every C entry's ctypes argtypes (the Python mirror) has the header's arity,
+    so a caller can never pass a shifted argument list."""
+    from paper_2407_02327_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "qsync_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    protos = re.findall(r"^\s*(?:int|const char\*|size_t|unsigned long long)\s+(qsync_\w+)\(([^)]*)\);", src,
+                        re.M | re.S)
+    assert len(protos) >= 40
+    for name, params in protos:
+        params = params.strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        assert len(_lib.SIGNATURES[name]) == n, (name, n, len(_lib.SIGNATURES[name]))
+
+
 def test_library_error_names_mirror_error_kinds():
     from paper_2407_02327_b200 import _lib
     L = _lib.lib()
