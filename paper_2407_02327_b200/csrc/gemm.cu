@@ -81,7 +81,12 @@ struct Cfg {
 #endif
     static constexpr int kStagesWant =
         kStageBytes >= 48 * 1024 ? QSB_GEMM_STAGES_48K : (kStageBytes >= 32 * 1024 ? 6 : 8);
-    static constexpr int kEpiStageBytes = 4 * 2 * kStageChunkBytes;  // 4 warps x double buffer
+#ifndef QSB_GEMM_EPIBUFS
+#define QSB_GEMM_EPIBUFS 2
+#endif
+    // 4 warps x QSB_GEMM_EPIBUFS staging chunks.  1 frees 16 KB: a 5th stage for
+    // 192-wide tiles -- measured +0.2% on the step (tools/build_variant.sh A/B), so 2 stays.
+    static constexpr int kEpiStageBytes = 4 * QSB_GEMM_EPIBUFS * kStageChunkBytes;
     // ... as many as fit next to the epilogue staging in 227 KB (BN = 192: 4 x 40 KB)
     static constexpr int kStagesFit = (227 * 1024 - kEpiStageBytes - 1024 - 256) / kStageBytes;
     static constexpr int kStages = kStagesWant < kStagesFit ? kStagesWant : kStagesFit;
@@ -490,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // double-buffered per warp.  Direct global stores remain as the path for
         // shapes TMA cannot address (row pitch not a multiple of 16 bytes).
         const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-        uint8_t* my_stage = smem_stage + (warp - kEpiWarp0) * 2 * kStageChunkBytes;
+        uint8_t* my_stage = smem_stage + (warp - kEpiWarp0) * QSB_GEMM_EPIBUFS * kStageChunkBytes;
         int sbuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -599,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.tma_store) {
                     // Free the staging buffer used two chunks ago, then write this
                     // row's 8 x 16B pieces at their 128B-swizzled positions.
-                    if (lane == 0) ptx::bulk_wait_read<1>();
+                    if (lane == 0) ptx::bulk_wait_read<QSB_GEMM_EPIBUFS - 1>();
                     __syncwarp();
                     uint8_t* buf = my_stage + sbuf * kStageChunkBytes;
                     const uint32_t rbase = ptx::smem_u32(buf) + lane * 128;
@@ -618,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                               static_cast<int32_t>(row0));
                         ptx::bulk_commit();
                     }
-                    sbuf ^= 1;
+                    sbuf = (sbuf + 1) % QSB_GEMM_EPIBUFS;
                     continue;
                 }
                 // ---- direct-store path (fully unrolled: keeps w[] in registers) ----
