@@ -19,7 +19,6 @@ and the optimizer) are PyTorch plumbing; the hot path is the Linear kernels.
 from __future__ import annotations
 
 import json
-import math
 from dataclasses import dataclass
 
 import torch

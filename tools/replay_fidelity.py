@@ -10,16 +10,13 @@ import json
 import os
 import sys
 
-import torch
-
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle.cpu_ref import RefLib  # noqa: E402  (test/measurement infrastructure)
 from paper_2407_02327_b200.profiler import (bert_graph, build_bundle, collect_tensor_stats,  # noqa: E402
                                             graph_step_ms, measure_cast_samples, measure_fused_cast_samples,
                                             measure_fused_costs, measure_op_costs, net_weight_casts)
 from paper_2407_02327_b200.qlinear import FP16, INT8  # noqa: E402
-from paper_2407_02327_b200.train_step import (BertConfig, BertEncoderStack, TrainStep,  # noqa: E402
-                                              mixed_plan, uniform_plan)
+from paper_2407_02327_b200.train_step import BertConfig, BertEncoderStack, mixed_plan, uniform_plan  # noqa: E402
 
 
 def main():
