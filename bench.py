@@ -36,6 +36,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "QSync mixed-precision train samples/s at 1/2/4/8 B200; INT8 GEMM TOPS vs peak"
 BATCH, SEQ = 32, 128
+PLAN_DESC = {"mixed": "mixed INT8/FP16 per layer (rank r%2 mirrored), pooler FP32",
+             "int8": "all encoder Linears INT8", "fp16": "all encoder Linears FP16"}
 
 
 def _peaks() -> dict:
@@ -129,7 +131,7 @@ def run_reference(args) -> None:
             "steps_timed": steps,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int8/fp16 (f64 accumulation on CPU)",
-            "data": "synthetic", "config": _config(1, "mixed INT8/FP16 (even layers INT8)"),
+            "data": "synthetic", "config": _config(args.gpus, PLAN_DESC["mixed"]),
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -139,15 +141,55 @@ def run_reference(args) -> None:
 
 # --------------------------------------------------------------------------- GPU leg
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region.  NVML is read
+    from a thread every ~4 ms, so even a 0.1 s region (the driver's 20 steps)
+    yields ~25 samples; nvidia-smi -lms 100 is the fallback when NVML is absent."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, pci_bus_id: str | None = None, period_s: float = 0.004):
         self.index = index
+        self.pci = pci_bus_id
+        self.period = period_s
         self.proc = None
+        self.thread = None
+        self.samples: list[tuple[float, float, int]] = []  # (sm MHz, max MHz, reason bits)
+        self.out = ""
+
+    def _nvml_loop(self, nv, h):
+        import time as _t
+        while not self._stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx), int(rs)))
+            except Exception:  # noqa: BLE001 -- a failed read is a missing sample
+                pass
+            _t.sleep(self.period)
 
     def __enter__(self):
+        import threading
+        self._stop = False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            if self.pci:
+                try:
+                    h = nv.nvmlDeviceGetHandleByPciBusId(self.pci)
+                except Exception:  # noqa: BLE001
+                    h = None
+            if h is None:
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:  # noqa: BLE001 -- no NVML: nvidia-smi fallback
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -158,7 +200,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        self._stop = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -167,20 +211,30 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self) -> dict:
-        rows = [r.split(", ") for r in getattr(self, "out", "").strip().splitlines() if r.strip()]
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            try:
-                sm.append(float(r[1]))
-                mx = float(r[2])
-                for i, nm in enumerate(names):
-                    if r[5 + i].strip().lower() == "active":
+        if self.samples:
+            for s, m, bits in self.samples:
+                sm.append(s)
+                mx = m
+                for nm, bit in self.REASONS:
+                    if bits & bit:
                         reasons.add(nm)
-            except (ValueError, IndexError):
-                continue
+            src = f"NVML every {self.period * 1e3:.0f} ms"
+        else:
+            rows = [r.split(", ") for r in self.out.strip().splitlines() if r.strip()]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for r in rows:
+                try:
+                    sm.append(float(r[1]))
+                    mx = float(r[2])
+                    for i, nm in enumerate(names):
+                        if r[5 + i].strip().lower() == "active":
+                            reasons.add(nm)
+                except (ValueError, IndexError):
+                    continue
+            src = "nvidia-smi -lms 100"
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": src}
 
 
 def int8_peak(torch) -> float:
@@ -215,6 +269,9 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}: launch through "
+                         f"torch.distributed.run or let bench.py spawn the ranks")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.manual_seed(1234)  # identical initial weights on every rank
@@ -230,8 +287,7 @@ def run_ours(args) -> None:
     elif rank % 2 == 1:
         plan = {k: ({INT8: FP16, FP16: INT8}.get(v, v)) for k, v in plan.items()}
     model.apply_plan(plan)
-    plan_desc = {"mixed": "mixed INT8/FP16 per layer (rank r%2 mirrored), pooler FP32",
-                 "int8": "all encoder Linears INT8", "fp16": "all encoder Linears FP16"}[args.plan]
+    plan_desc = PLAN_DESC[args.plan]
 
     step = TrainStep(model, BATCH, world=world, graph=not args.no_graph)
     g = torch.Generator().manual_seed(100 + rank)
@@ -273,29 +329,35 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
 
     # ---- device-timed region: K captured steps, inputs resident in HBM ----
+    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
+    pr = torch.cuda.get_device_properties(local)
+    try:
+        pci = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+    except (AttributeError, TypeError, ValueError):
+        pci = None
     barrier()
-    with ClockSampler(local) as clk:
+    # Clocks are sampled over both timed regions (device-timed and e2e).
+    with ClockSampler(local, pci) as clk:
         t_s, t_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t_s.record()
         for _ in range(args.steps):
             loss = step()
         t_e.record()
         barrier()
-    ms = t_s.elapsed_time(t_e)
+        ms = t_s.elapsed_time(t_e)
 
-    # ---- e2e: H2D of each step's batch from pinned memory + D2H of the loss ----
-    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
-    barrier()
-    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_s.record()
-    for k in range(args.steps):
-        step.tokens.copy_(host_tokens[k % nb], non_blocking=True)
-        step.labels.copy_(host_labels[k % nb], non_blocking=True)
-        loss = step()
-        loss_host.copy_(loss, non_blocking=True)
-    e_e.record()
-    barrier()
-    ms_e2e = e_s.elapsed_time(e_e)
+        # ---- e2e: H2D of each step's batch from pinned memory + D2H of the loss ----
+        barrier()
+        e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_s.record()
+        for k in range(args.steps):
+            step.tokens.copy_(host_tokens[k % nb], non_blocking=True)
+            step.labels.copy_(host_labels[k % nb], non_blocking=True)
+            loss = step()
+            loss_host.copy_(loss, non_blocking=True)
+        e_e.record()
+        barrier()
+        ms_e2e = e_s.elapsed_time(e_e)
     h2d = host_tokens[0].numel() * 8 + host_labels[0].numel() * 8
     d2h = 4
 
@@ -351,6 +413,56 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """``python bench.py --gpus N`` with N > 1 and no torchrun environment:
+    re-launch this script as N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1, exactly as the driver does.  NCCL INIT
+    logging is on so every communicator reports its nranks (on stderr)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_selftest(args) -> None:
+    """Rank plumbing without a GPU (tests/test_bench_spawn.py): gloo rendezvous,
+    per-rank timing, MAX over ranks, one JSON line from rank 0."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    x = torch.full((1024,), float(rank + 1))
+    for _ in range(args.steps):
+        if world > 1:
+            dist.all_reduce(x)
+    ms = (time.perf_counter() - t0) * 1e3
+    t = torch.tensor([ms, float(rank)])
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "selftest": True, "n_gpus": world, "steps": args.steps,
+                          "ms_max_over_ranks": float(t[0]), "max_rank": int(t[1]),
+                          "allreduce_value": float(x[0])}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -360,10 +472,15 @@ def main():
     ap.add_argument("--plan", choices=["mixed", "int8", "fp16"], default="mixed")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--selftest", action="store_true", help="rank plumbing only (CPU, gloo)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    if args.impl == "reference":
+    if args.selftest:
+        run_selftest(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
