@@ -378,6 +378,36 @@ int qsync_adamw_step_range(const qsync_adamw_seg* segs, int nseg, const int64_t*
                            float beta2, float eps, float weight_decay, int update, qsync_stream_t stream);
 int qsync_adamw_advance(int64_t* step, qsync_stream_t stream);
 
+
+/* ---------------------------------------------------------------------------
+ * C1  data-parallel gradient exchange over NCCL (NVLink 5 / NVSwitch).
+ * The reference models it, it does not run it: per-rank bucket slots
+ * {earliest_ready_offset_ns, duration_ns, bucket_bytes} (profile.hpp:118-129),
+ * slot n starts at max(every rank ready, end of slot n-1) and the optimizer
+ * waits for the last slot (replayer.cpp:48-73).  These entries are that
+ * exchange: one communicator per rank (one process per GPU), FP32 buckets
+ * reduced in place on the caller's stream, in the order the caller issues them
+ * (identical on every rank whatever its precision plan).  NCCL is resolved at
+ * run time (the libnccl.so.2 already in the process, else the system one), so
+ * the library links no NCCL; failures map to QSYNC_ERR_INTERNAL with NCCL's
+ * message, bad arguments to VALIDATION / DOMAIN.  Capturable in a CUDA graph.
+ * ------------------------------------------------------------------------- */
+#define QSYNC_COMM_ID_BYTES 128
+typedef struct qsync_comm_s* qsync_comm_t;
+/* A fresh communicator id (rank 0 creates it, the caller broadcasts the bytes). */
+int qsync_comm_unique_id(uint8_t id[QSYNC_COMM_ID_BYTES]);
+/* Join communicator `id` as `rank` of `nranks` on the CURRENT CUDA device
+ * (collective: every rank must call it). */
+int qsync_comm_init(qsync_comm_t* comm, int nranks, int rank, const uint8_t id[QSYNC_COMM_ID_BYTES]);
+int qsync_comm_destroy(qsync_comm_t comm);
+/* nranks / rank / CUDA device of a communicator (any pointer may be NULL). */
+int qsync_comm_info(qsync_comm_t comm, int* nranks, int* rank, int* device);
+/* In-place all-reduce of `count` FP32 values at `buf` (one gradient bucket):
+ * average != 0 -> mean over ranks (ncclAvg), else sum. */
+int qsync_allreduce_bucket(qsync_comm_t comm, float* buf, int64_t count, int average, qsync_stream_t stream);
+/* NCCL version of the resolved library (e.g. 22809), or -1 if none loads. */
+int qsync_comm_nccl_version(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -130,6 +130,49 @@ inline TensorStats5 tensor_stats(const void* device_x, int dtype, int64_t n,
     return {h[0], h[1], h[2], h[3], h[4]};
 }
 
+/// One rank's NCCL communicator for the data-parallel gradient exchange (C1):
+/// the in-order bucket all-reduce whose slots the replayer models
+/// (profile.hpp:118-129, replayer.cpp:48-73).  Rank 0 creates the id with
+/// unique_id(); the caller broadcasts it (MPI, a file, a TCP store ...).
+class Communicator {
+  public:
+    using Id = std::vector<std::uint8_t>;
+    static Id unique_id() {
+        Id id(QSYNC_COMM_ID_BYTES);
+        check(qsync_comm_unique_id(id.data()));
+        return id;
+    }
+    /// Collective over the ranks; binds the CURRENT CUDA device.
+    Communicator(int nranks, int rank, const Id& id) {
+        if (id.size() != QSYNC_COMM_ID_BYTES)
+            throw Error(QSYNC_ERR_VALIDATION, "validation: communicator id must be 128 bytes");
+        check(qsync_comm_init(&c_, nranks, rank, id.data()));
+    }
+    ~Communicator() {
+        if (c_) qsync_comm_destroy(c_);
+    }
+    Communicator(const Communicator&) = delete;
+    Communicator& operator=(const Communicator&) = delete;
+    int nranks() const {
+        int n = 0;
+        check(qsync_comm_info(c_, &n, nullptr, nullptr));
+        return n;
+    }
+    int rank() const {
+        int r = 0;
+        check(qsync_comm_info(c_, nullptr, &r, nullptr));
+        return r;
+    }
+    /// In-place FP32 bucket all-reduce on `stream` (mean over ranks by default).
+    void allreduce_bucket(float* device_buf, std::int64_t count, cudaStream_t stream = nullptr,
+                          bool average = true) {
+        check(qsync_allreduce_bucket(c_, device_buf, count, average ? 1 : 0, stream));
+    }
+
+  private:
+    qsync_comm_t c_ = nullptr;
+};
+
 }  // namespace qsync_b200
 
 #endif  // QSYNC_B200_HPP

@@ -30,7 +30,7 @@ _p = C.c_void_p
 
 def build() -> None:
     """Compile the oracle libraries (the reference one only if its tree exists)."""
-    subprocess.run(["make", "-s", "-f", os.path.join(HERE, "Makefile")], check=True)
+    subprocess.run(["make", "-s", "-f", os.path.join(HERE, "Makefile"), "all", "acceptance"], check=True)
 
 
 def _ptr(a: np.ndarray):
@@ -281,6 +281,8 @@ class RefLib:
         L.qref_plan_bundle.restype = _i64
         L.qref_replay_bundle.argtypes = [C.c_char_p, C.c_char_p]
         L.qref_replay_bundle.restype = _i64
+        L.qref_replay_trace.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _i64]
+        L.qref_replay_trace.restype = _i64
 
     def _err(self, rc):
         if rc:
@@ -349,6 +351,15 @@ class RefLib:
         if n < 0:
             raise RuntimeError(self.L.qref_last_error().decode())
         return int(n)
+
+    def replay_trace(self, path, plan: dict) -> dict:
+        """The replayer's Chrome trace of one simulated iteration (replayer.cpp:126-148)."""
+        import json as _json
+        buf = C.create_string_buffer(16 << 20)
+        n = self.L.qref_replay_trace(path.encode(), _json.dumps(plan).encode(), buf, 16 << 20)
+        if n < 0:
+            raise RuntimeError(self.L.qref_last_error().decode())
+        return _json.loads(buf.raw[:n].decode())
 
     def score_bundle(self, path, loss_kind, loss_n, window=50):
         buf = C.create_string_buffer(1 << 20)

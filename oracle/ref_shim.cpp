@@ -208,4 +208,21 @@ int64_t qref_replay_bundle(const char* path, const char* plan_json) {
     }
 }
 
+// The replayer's Chrome trace (trace_to_json, replayer.cpp:126-148) of one
+// simulated iteration; writes the JSON into buf.  Returns bytes or -code.
+int64_t qref_replay_trace(const char* path, const char* plan_json, char* buf, int64_t cap) {
+    try {
+        const ProfileBundle bundle = load_profile(path);
+        const PrecisionPlan plan = plan_from_json(nlohmann::json::parse(plan_json));
+        const Timeline t = simulate(build_global_dfg(bundle, plan).global);
+        const std::string out = trace_to_json(t).dump();
+        if (static_cast<int64_t>(out.size()) > cap) return -100;
+        std::memcpy(buf, out.data(), out.size());
+        return static_cast<int64_t>(out.size());
+    } catch (const Error& e) {
+        g_err = e.what();
+        return -code_of(e);
+    }
+}
+
 }  // extern "C"

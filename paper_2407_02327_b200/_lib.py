@@ -92,6 +92,12 @@ SIGNATURES = {
     "qsync_gemm_f8": [_p, _p, _i64, _i64, _i64, _p, _int, _p, _p, _int, _p, _p],
     "qsync_quantize_fp8": [_p, _int, _i64, _p, _p, _p, _p],
     "qsync_quantize_fp8_rows": [_p, _i64, _i64, _p, _p, _p],
+    "qsync_comm_unique_id": [_p],
+    "qsync_comm_init": [_p, _int, _int, _p],
+    "qsync_comm_destroy": [_p],
+    "qsync_comm_info": [_p, _p, _p, _p],
+    "qsync_allreduce_bucket": [_p, _p, _i64, _int, _p],
+    "qsync_comm_nccl_version": [],
     # non-header helpers
     "qsync_gemm_force_tile_n": [_int],
     "qsync_gemm_force_splitk": [_int],

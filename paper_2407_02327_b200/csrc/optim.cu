@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
         amax = warp_max(amax);
         const float sc = scale_from_absmax(amax);
         if (sg.wq && lane == 0) sg.wscale[r] = sc;
+        const QScale qsc = make_qscale(sc);
         uint16_t* w16 = sg.w16 ? sg.w16 + r * cols : nullptr;
         int8_t* wq = sg.wq ? sg.wq + r * cols : nullptr;
         const bool vec2 = vec && (!w16 || (reinterpret_cast<uintptr_t>(w16) & 7u) == 0) &&
@@ -172,17 +173,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __
                 }
                 if (wq) {
                     reinterpret_cast<uint32_t*>(wq)[k] =
-                        static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.x, sc))) |
-                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.y, sc))) << 8) |
-                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.z, sc))) << 16) |
-                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.w, sc))) << 24);
+                        static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.x, qsc))) |
+                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.y, qsc))) << 8) |
+                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.z, qsc))) << 16) |
+                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.w, qsc))) << 24);
                 }
             }
         } else {
             for (int64_t k = lane; k < cols; k += 32) {
                 const float pv = p[k];
                 if (w16) w16[k] = __half_as_ushort(__float2half_rn(pv));
-                if (wq) wq[k] = static_cast<int8_t>(quant_rne(pv, sc));
+                if (wq) wq[k] = static_cast<int8_t>(quant_rne(pv, qsc));
             }
         }
     }

@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
     constexpr int LOADS = 16 / V::N;
     const float s = scale_in ? *scale_in : scale_from_absmax(*absmax_in);
     if (scale_out && blockIdx.x == 0 && threadIdx.x == 0) *scale_out = s;
+    const QScale qs = make_qscale(s);
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t done = 0;
@@ -247,8 +248,8 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
 #pragma unroll
                         for (int e = 0; e < 4; ++e) a[e] = act_f<ACT, DT>(f[j + e]);
                     }
-                    const int i0 = quant_rne(a[0], s), i1 = quant_rne(a[1], s);
-                    const int i2 = quant_rne(a[2], s), i3 = quant_rne(a[3], s);
+                    const int i0 = quant_rne(a[0], qs), i1 = quant_rne(a[1], qs);
+                    const int i2 = quant_rne(a[2], qs), i3 = quant_rne(a[3], qs);
                     const uint32_t b0 = static_cast<uint8_t>(i0), b1 = static_cast<uint8_t>(i1);
                     const uint32_t b2 = static_cast<uint8_t>(i2), b3 = static_cast<uint8_t>(i3);
                     packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
     }
     for (int64_t i = done + tid; i < n; i += stride) {
         const float xv = Elem<DT>::f(x[i]);
-        const int qi = quant_rne(act_f<ACT, DT>(xv), s);
+        const int qi = quant_rne(act_f<ACT, DT>(xv), qs);
         q[i] = static_cast<int8_t>(qi);
         if (q16) q16[i] = __half_as_ushort(__int2half_rn(qi));
         if (ACT == 1 && dact) dact[i] = __half_as_ushort(__float2half_rn(gelu_erf_grad(xv)));
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __rest
         s = scale_from_absmax(*absmax_in);
         if (scale_out && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *scale_out = s;
     }
+    const QScale qs = make_qscale(s);
     const int64_t c = c0 + cg * 4;
     const bool full_cols = vec_ok && (c + 4 <= cols);
     float cs[4] = {0.f, 0.f, 0.f, 0.f};
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __rest
             int qi[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                qi[i] = quant_rne(f[i], s);
+                qi[i] = quant_rne(f[i], qs);
                 h[i] = __int2half_rn(qi[i]);
             }
             if (q && r < rows) {
@@ -480,18 +482,19 @@ __global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w,
     m = warp_max(m);
     const float s = scale_from_absmax(m);
     if (lane == 0) scales[row] = s;
+    const QScale qs = make_qscale(s);
     if (vec && (reinterpret_cast<uintptr_t>(qr) & 3u) == 0) {
         const float4* v = reinterpret_cast<const float4*>(wr);
         uint32_t* qo = reinterpret_cast<uint32_t*>(qr);
         for (int64_t c = lane; c < cols / 4; c += 32) {
             float4 f = v[c];
-            qo[c] = static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.x, s))) |
-                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.y, s))) << 8) |
-                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.z, s))) << 16) |
-                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.w, s))) << 24);
+            qo[c] = static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.x, qs))) |
+                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.y, qs))) << 8) |
+                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.z, qs))) << 16) |
+                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.w, qs))) << 24);
         }
     } else {
-        for (int64_t c = lane; c < cols; c += 32) qr[c] = static_cast<int8_t>(quant_rne(wr[c], s));
+        for (int64_t c = lane; c < cols; c += 32) qr[c] = static_cast<int8_t>(quant_rne(wr[c], qs));
     }
 }
 

@@ -636,3 +636,59 @@ def force_cta(cta: int) -> None:
 def force_tile_n(bn: int) -> None:
     """Test hook: pin the GEMM tile N (0 = heuristic)."""
     call("qsync_gemm_force_tile_n", int(bn))
+
+
+# --------------------------------------------------------------------------- C1
+class Communicator:
+    """One NCCL communicator of this rank through the C ABI (``qsync_comm_*``):
+    the data-parallel gradient exchange of the training step.  ``group`` is any
+    initialised torch.distributed process group (gloo or nccl) used once, to
+    broadcast rank 0's communicator id -- host plumbing only; the buckets go
+    through ``allreduce_bucket`` (ncclAllReduce on the caller's stream)."""
+
+    def __init__(self, world: int, rank: int, group=None, comm_id: bytes | None = None):
+        import ctypes as C
+        self._C = C
+        if comm_id is None:
+            buf = (C.c_uint8 * 128)()
+            if rank == 0:
+                call("qsync_comm_unique_id", C.addressof(buf))
+            if world > 1:
+                import torch.distributed as dist
+                obj = [bytes(buf) if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                comm_id = obj[0]
+            else:
+                comm_id = bytes(buf)
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(comm_id)
+        h = C.c_void_p()
+        call("qsync_comm_init", C.byref(h), int(world), int(rank), C.addressof(idbuf))
+        self.handle = h
+        self.world, self.rank = int(world), int(rank)
+
+    def info(self) -> tuple[int, int, int]:
+        C = self._C
+        n, r, d = C.c_int(), C.c_int(), C.c_int()
+        call("qsync_comm_info", self.handle, C.byref(n), C.byref(r), C.byref(d))
+        return n.value, r.value, d.value
+
+    def allreduce_bucket(self, buf: torch.Tensor, average: bool = True) -> None:
+        """In-place FP32 all-reduce (mean over ranks by default) on the current stream."""
+        _req(buf, "bucket", (torch.float32,))
+        call("qsync_allreduce_bucket", self.handle, _ptr(buf), buf.numel(), int(average), _stream())
+
+    def close(self) -> None:
+        if self.handle is not None and self.handle.value:
+            call("qsync_comm_destroy", self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter teardown
+            pass
+
+
+def nccl_version() -> int:
+    """Version of the NCCL library the C ABI resolved (e.g. 22809), -1 if none."""
+    return int(_lib.lib().qsync_comm_nccl_version())

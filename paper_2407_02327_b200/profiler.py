@@ -355,6 +355,9 @@ def measure_fused_costs(cfg: BertConfig, batch: int, reps: int = 5, calibrate: b
         diag[p] = {"eager_regions_ms": tot / 1e6, "graph_step_ms": graph_ns / 1e6, "scale": scale}
         per[p] = {k: v * scale for k, v in per[p].items()}
     measure_fused_costs.last_diag = diag
+    for p in per:  # the pooler is costed from its kernels (measure_linear); its autograd
+        # backward region stays with the head's, as before the head had marks
+        per[p][("bwd", "loss")] = per[p].get(("bwd", "loss"), 0.0) + per[p].pop(("bwd", "pooler"), 0.0)
     numel = _param_numel(cfg)
 
     def opt_share(op, p):
@@ -497,8 +500,9 @@ def net_weight_casts(cfg: BertConfig, costs: dict, cast_samples: list) -> dict:
 
 
 def profile_bert_fused(cfg: BertConfig, batch: int, stat_steps: int = 3, infer_cap_bytes: int | None = None,
-                       reps: int = 5) -> dict:
-    """The bundle of the layer-fused implementation (the one the train step runs)."""
+                       reps: int = 5, with_comm: bool = True) -> dict:
+    """The bundle of the layer-fused implementation (the one the train step runs),
+    with the measured gradient-exchange slots (``comm``) of every device."""
     model = BertEncoderStack(cfg).cuda()
     model.apply_plan({})
     stats = collect_tensor_stats(model, batch, stat_steps)
@@ -510,6 +514,99 @@ def profile_bert_fused(cfg: BertConfig, batch: int, stat_steps: int = 3, infer_c
     devices = [{"id": "trainer", "is_inference": False, "mem_capacity_bytes": 183_000_000_000},
                {"id": "infer", "is_inference": True, "mem_capacity_bytes": max(cap, 1)}]
     return build_bundle(graph, costs, casts, stats, devices)
+
+
+# ----------------------------------------------------------------------------- comm
+def _timed_step(cfg: BertConfig, batch: int, plan: dict, comm=None, world: int = 1):
+    """An eager single-stream TrainStep (wgrad on the main stream) whose gradient
+    buckets go through ``comm`` (an ops.Communicator; a 1-rank one on a single
+    GPU) with CommSlot timing on."""
+    from .ops import Communicator
+    from .train_step import TrainStep
+    if comm is None:
+        comm = Communicator(1, 0)
+    torch.manual_seed(0)
+    m = BertEncoderStack(cfg).cuda()
+    m.apply_plan(plan)
+    st = TrainStep(m, batch=batch, world=world, graph=False, overlap_wgrad=False, comm=comm)
+    st.tokens.random_(0, cfg.vocab)
+    st.grads.timing = True
+    for _ in range(3):
+        st()
+    torch.cuda.synchronize()
+    return st, comm
+
+
+def measure_comm_slots(cfg: BertConfig, batch: int, plan: dict | None = None, comm=None,
+                       world: int = 1, reps: int = 5) -> list[dict]:
+    """CommSlots (profile.hpp:118-129) of the train step's bucketed gradient
+    exchange, measured through the C ABI's NCCL all-reduce: per bucket the
+    earliest ready offset from the step start, the all-reduce's device time and
+    the bucket's bytes; median over ``reps`` eager steps.  The replayer attaches
+    slots to backward events on the FP32 timeline (cost_mapper.cpp:55-90), so the
+    default plan is all-FP32 (the assignment the reference profiles at)."""
+    st, comm = _timed_step(cfg, batch, plan or {}, comm, world)
+    runs = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        torch.cuda._sleep(200_000_000)  # enqueue the whole step before it runs
+        st()
+        runs.append(st.grads.comm_slots())
+    med = statistics.median
+    out = []
+    for k in range(len(runs[0])):
+        out.append({"earliest_ready_offset_ns": int(med(r[k]["earliest_ready_offset_ns"] for r in runs)),
+                    "duration_ns": max(1, int(med(r[k]["duration_ns"] for r in runs))),
+                    "bucket_bytes": runs[0][k]["bucket_bytes"]})
+    measure_comm_slots.last_world = comm.world
+    return out
+
+
+def measured_op_trace(cfg: BertConfig, batch: int, plan: dict, device_id: str = "b200", comm=None,
+                      world: int = 1) -> dict:
+    """One measured eager step as a Chrome trace in the reference replayer's
+    format (replayer.cpp:126-148): event name = the replayer's event id
+    ("fwd:<op>", "bwd:<op>", "optimizer"; the input conversion of an op is part of
+    its "fwd:" event, as the cost mapper charges fwd_cast to it,
+    cost_mapper.cpp:34-43), pid = device, tid 0 = compute, tid 1 =
+    "allreduce:<n>" slots.  Regions come from the fused step's operator marks
+    (fused.REGION); "zero_grad" (the flat-gradient memset) has no replayer
+    counterpart."""
+    from . import fused
+    st, comm = _timed_step(cfg, batch, plan, comm, world)
+    marks = []
+
+    def hook(kind, op):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append((kind, op, e))
+
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)
+    fused.REGION = hook
+    try:
+        st()
+    finally:
+        fused.REGION = None
+    torch.cuda.synchronize()
+    t0 = st.grads.t0
+    names = {"fwd": "fwd:", "cast": "fwd:", "bwd": "bwd:"}
+    events = []
+    for (k, o, e0), (_, _, e1) in zip(marks, marks[1:]):
+        if k == "opt":
+            name = "optimizer" if o == "optimizer" else "zero_grad"
+        else:
+            name = names[k] + o
+        s_us, e_us = t0.elapsed_time(e0) * 1e3, t0.elapsed_time(e1) * 1e3
+        if events and events[-1]["name"] == name and events[-1]["tid"] == 0:
+            events[-1]["dur"] = e_us - events[-1]["ts"]  # cast + fwd of one op: one event
+            continue
+        events.append({"name": name, "ph": "X", "ts": s_us, "dur": e_us - s_us, "pid": device_id, "tid": 0})
+    for n, (i, r_main, r_side, e_s, e_e, nbytes) in enumerate(sorted(st.grads._slot_events, key=lambda t: t[0])):
+        s_us, e_us = t0.elapsed_time(e_s) * 1e3, t0.elapsed_time(e_e) * 1e3
+        events.append({"name": f"allreduce:{n + 1}", "ph": "X", "ts": s_us, "dur": e_us - s_us,
+                       "pid": device_id, "tid": 1, "args": {"bucket_bytes": nbytes}})
+    return {"traceEvents": events, "displayTimeUnit": "ms"}
 
 
 # ----------------------------------------------------------------------------- casts

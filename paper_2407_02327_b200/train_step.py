@@ -163,7 +163,13 @@ class BertEncoderStack(torch.nn.Module):
         if self.fused:
             _mark("fwd", "loss")
         logits = self.cls(pooled)
-        return F.cross_entropy(logits, labels)
+        loss = F.cross_entropy(logits, labels)
+        if self.fused and loss.requires_grad:
+            from . import fused as _fz
+            if _fz.REGION is not None:  # operator regions of the backward head (profiling only)
+                loss.register_hook(lambda g: (_fz._mark("bwd", "loss"), g)[1])
+                pooled.register_hook(lambda g: (_fz._mark("bwd", "pooler"), g)[1])
+        return loss
 
 
 def linear_flops_per_step(cfg: BertConfig, tokens: int) -> float:
@@ -225,6 +231,17 @@ class FlatGrads:
         self._side = None
         self.comm_stream = None
         self.issue_log: list[tuple[int, int]] = []  # (bucket, pending params at issue) -- tests
+        # The C1 exchange: an ops.Communicator (NCCL through the C ABI) when the
+        # flat buffer lives on a GPU; None -> torch.distributed (the gloo tests).
+        self.comm = None
+        # CommSlot measurement (profile.hpp:118-129): with ``timing`` on (eager
+        # steps only -- no events inside a CUDA-graph capture) every bucket gets
+        # ready / start / end events; ``t0`` is the step-start event the ready
+        # offsets are measured from (the replayer's clock starts at the first
+        # forward event, cost_mapper.cpp:60-70).
+        self.timing = False
+        self.t0 = None
+        self._slot_events: list[tuple] = []
 
     def zero(self) -> None:
         self.flat.zero_()
@@ -239,11 +256,12 @@ class FlatGrads:
         bucket, overlapping the rest of the backward."""
         self._world = world
         self._on_final = on_final
-        self._active = world > 1 or on_final is not None
+        self._active = world > 1 or on_final is not None or self.comm is not None
         self._pending = list(self._members)
         self._next = 0
         self._side = side_stream
         self.issue_log = []
+        self._slot_events = []
         if self.flat.is_cuda and self._active and self.comm_stream is None:
             self.comm_stream = torch.cuda.Stream(priority=-1)
 
@@ -277,7 +295,15 @@ class FlatGrads:
         if not ready:
             return
         world = self._world
-        nccl = world > 1 and dist.get_backend() == "nccl"
+        timing = self.timing and self.flat.is_cuda and not torch.cuda.is_current_stream_capturing()
+        if timing:
+            # Ready = the producing streams reached this point (main and wgrad side stream).
+            r_main = torch.cuda.Event(enable_timing=True)
+            r_main.record()
+            r_side = None
+            if self._side is not None:
+                r_side = torch.cuda.Event(enable_timing=True)
+                r_side.record(self._side)
         if self.comm_stream is not None:
             self.comm_stream.wait_stream(torch.cuda.current_stream())
             if self._side is not None:
@@ -290,13 +316,37 @@ class FlatGrads:
             for i in ready:
                 a, b = self.buckets[i]
                 chunk = self.flat[a:b]
-                if nccl:
-                    dist.all_reduce(chunk, op=dist.ReduceOp.AVG)
+                if timing:
+                    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e_s.record()
+                if self.comm is not None:
+                    self.comm.allreduce_bucket(chunk, average=True)  # C ABI -> ncclAllReduce(ncclAvg)
                 elif world > 1:
                     dist.all_reduce(chunk)
                     chunk.div_(world)
+                if timing:
+                    e_e.record()
+                    self._slot_events.append((i, r_main, r_side, e_s, e_e, (b - a) * 4))
                 if self._on_final is not None:
                     self._on_final(i)
+
+    def comm_slots(self) -> list[dict]:
+        """The last timed backward's buckets as CommSlot records
+        (profile.hpp:118-129; schema profile.cpp:385-403), in slot order:
+        earliest_ready_offset_ns = ready - step start, duration_ns = the
+        all-reduce's device time, bucket_bytes = the FP32 bucket size."""
+        if not self._slot_events:
+            return []
+        torch.cuda.synchronize()
+        out = []
+        for i, r_main, r_side, e_s, e_e, nbytes in sorted(self._slot_events, key=lambda t: t[0]):
+            ready_ms = self.t0.elapsed_time(r_main) if self.t0 is not None else 0.0
+            if r_side is not None and self.t0 is not None:
+                ready_ms = max(ready_ms, self.t0.elapsed_time(r_side))
+            out.append({"earliest_ready_offset_ns": max(0, int(round(ready_ms * 1e6))),
+                        "duration_ns": max(1, int(round(e_s.elapsed_time(e_e) * 1e6))),
+                        "bucket_bytes": int(nbytes)})
+        return out
 
     def allreduce(self, world: int) -> None:
         """Non-overlapped form: every bucket in order after the backward."""
@@ -312,7 +362,7 @@ class TrainStep:
 
     def __init__(self, model: BertEncoderStack, batch: int, world: int = 1, lr: float = 1e-4,
                  graph: bool = True, overlap_wgrad: bool = True, fused: bool = True,
-                 overlap_opt: bool | None = None):
+                 overlap_opt: bool | None = None, comm="auto"):
         self.model = model
         self.world = world
         cfg = model.cfg
@@ -321,6 +371,17 @@ class TrainStep:
         self.labels = torch.zeros((batch,), dtype=torch.long, device=dev)
         self.params = [p for p in model.parameters() if p.requires_grad]
         self.grads = FlatGrads(self.params)
+        # C1: the gradient buckets go through this library's NCCL entry points
+        # (qsync_allreduce_bucket); "auto" = one communicator per rank when DP runs
+        # on GPUs under an NCCL process group.  Pass an ops.Communicator (e.g. a 1-rank one) to time the
+        # exchange on a single GPU, or None for torch.distributed (CPU / gloo).
+        if comm == "auto":
+            comm = None
+            import torch.distributed as dist
+            if world > 1 and dev.type == "cuda" and dist.get_backend() == "nccl":
+                from .ops import Communicator
+                comm = Communicator(world, dist.get_rank())
+        self.grads.comm = comm
         self.fused = fused
         model.fused = fused
         if fused:
@@ -349,7 +410,8 @@ class TrainStep:
         # and the rest of the backward.  On one GPU it only contends with the
         # backward for HBM (tools/ab_overlap_opt.py: 5.01 vs 4.97 ms), so it is off there.
         self.overlap_opt = fused and (world > 1 if overlap_opt is None else overlap_opt)
-        if (world > 1 or self.overlap_opt) and fused:
+        self._hooked = (world > 1 or self.overlap_opt or comm is not None) and fused
+        if self._hooked:
             for m in (model.pooler, model.cls):
                 for prm in m.parameters():
                     prm.register_post_accumulate_grad_hook(lambda t: self.grads.params_ready([t]))
@@ -361,6 +423,9 @@ class TrainStep:
             self.opt.attach(self.model.qlinears().values())
 
     def _body(self):
+        if self.grads.timing and not torch.cuda.is_current_stream_capturing():
+            self.grads.t0 = torch.cuda.Event(enable_timing=True)
+            self.grads.t0.record()
         if self.fused:
             from .fused import _mark
             _mark("opt", "zero")
@@ -374,8 +439,7 @@ class TrainStep:
         # parameters (pooler, classifier) through their post-accumulate hooks.
         self.grads.begin(self.world, self.wgrad_stream,
                          on_final=self._opt_bucket if self.overlap_opt else None)
-        _ql.GRAD_READY = (self.grads.params_ready
-                          if self.fused and (self.world > 1 or self.overlap_opt) else None)
+        _ql.GRAD_READY = self.grads.params_ready if self._hooked else None
         try:
             loss.backward()
         finally:

@@ -148,6 +148,27 @@ int main() {
         const double limit = 3.0 * q / (2.0 * std::sqrt(static_cast<double>(d)));
         require(std::abs(out_mean - in_mean) <= limit, "criterion 3: unbiased within 3 sigma");
     }
+    // C1: the gradient exchange through the C++ mirror -- a 1-rank communicator
+    // (the box has one GPU), in-place bucket mean is the identity.
+    {
+        Communicator comm(1, 0, Communicator::unique_id());
+        const int n = 1 << 20;
+        std::vector<float> h(n), back(n);
+        for (int i = 0; i < n; ++i) h[i] = static_cast<float>(i % 977) * 0.5f - 100.0f;
+        DeviceBuffer<float> g(n);
+        g.upload(h.data());
+        comm.allreduce_bucket(g.get(), n);
+        cuda_check(cudaDeviceSynchronize(), "sync");
+        g.download(back.data());
+        require(comm.nranks() == 1 && comm.rank() == 0 && back == h, "1-rank bucket all-reduce is the identity");
+        bool threw = false;
+        try {
+            Communicator bad(2, 7, Communicator::unique_id());
+        } catch (const Error& e) {
+            threw = e.kind() == "domain";
+        }
+        require(threw, "rank outside [0, nranks) raises domain");
+    }
     std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASS", g_fail);
     return g_fail ? 1 : 0;
 }

@@ -1,0 +1,141 @@
+"""C1 through the C ABI (qsync_comm_* / qsync_allreduce_bucket, include/qsync_b200.h):
+a 1-rank NCCL communicator on the box's one GPU (NCCL forbids two ranks on one
+device; the 2-rank host logic is covered by the gloo tests), eager and inside a
+CUDA graph, its error statuses, and the training step routed through it --
+bit-identical to the step without the exchange (the mean over one rank is the
+identity) -- with its measured CommSlots accepted by the reference loader
+(profile.cpp:385-410) and replayer (replayer.cpp:48-73)."""
+import ctypes as C
+import json
+
+import pytest
+import torch
+
+from paper_2407_02327_b200 import _lib, ops
+from paper_2407_02327_b200._lib import QsyncError
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm():
+    torch.cuda.set_device(0)
+    c = ops.Communicator(1, 0)
+    yield c
+    c.close()
+
+
+def test_nccl_resolved():
+    v = ops.nccl_version()
+    assert v >= 21000, v
+
+
+def test_comm_info(comm):
+    assert comm.info() == (1, 0, 0)
+
+
+@pytest.mark.parametrize("average", [True, False])
+def test_allreduce_one_rank_is_identity(comm, average):
+    x = torch.randn(3_000_001, device="cuda")
+    ref = x.clone()
+    comm.allreduce_bucket(x, average=average)
+    torch.cuda.synchronize()
+    assert torch.equal(x, ref)
+
+
+def test_allreduce_empty_bucket(comm):
+    comm.allreduce_bucket(torch.empty(0, device="cuda"))
+
+
+def test_allreduce_in_cuda_graph(comm):
+    x = torch.randn(1 << 20, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        x.mul_(2.0)
+        comm.allreduce_bucket(x)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        x.mul_(2.0)
+        comm.allreduce_bucket(x)
+    ref = x.clone()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(x, ref * 2.0)
+
+
+def test_comm_errors():
+    L = _lib.lib()
+    idbuf = (C.c_uint8 * 128)()
+    h = C.c_void_p()
+    assert L.qsync_comm_init(C.byref(h), 2, 5, C.addressof(idbuf)) == 4  # domain: rank out of range
+    assert "domain: rank 5" in L.qsync_last_error().decode()
+    assert L.qsync_comm_init(C.byref(h), 0, 0, C.addressof(idbuf)) == 4
+    assert L.qsync_allreduce_bucket(None, None, 4, 1, None) == 2  # validation: null communicator
+    with pytest.raises(QsyncError) as e:
+        ops.Communicator(1, 0).allreduce_bucket(torch.zeros(4, dtype=torch.float16, device="cuda"))
+    assert e.value.kind == "domain"
+
+
+def _tiny_step(comm, timing=False):
+    from paper_2407_02327_b200.train_step import BertConfig, BertEncoderStack, TrainStep, mixed_plan
+    cfg = BertConfig(vocab=1000, hidden=256, layers=2, heads=4, ffn=1024, max_pos=128, seq=128)
+    torch.manual_seed(0)
+    m = BertEncoderStack(cfg).cuda()
+    m.apply_plan(mixed_plan(cfg))
+    st = TrainStep(m, batch=4, world=1, lr=1e-3, graph=False, fused=True, comm=comm)
+    st.grads.timing = timing
+    g = torch.Generator().manual_seed(3)
+    st.tokens.copy_(torch.randint(0, cfg.vocab, (4, cfg.seq), generator=g))
+    st.labels.copy_(torch.randint(0, 2, (4,), generator=g))
+    losses = [float(st().item()) for _ in range(2)]
+    torch.cuda.synchronize()
+    return st, m, losses
+
+
+def test_train_step_through_comm_matches(comm):
+    """Routing the buckets through the communicator changes nothing numerically
+    (the mean over one rank is the identity, checked bit-exactly above); the step
+    itself reduce-adds split-K partials and column sums with atomics, so two runs
+    agree to rounding, not bit for bit -- the bound is two runs of the same step."""
+    st0, m0, l0 = _tiny_step(None)
+    _, m0b, l0b = _tiny_step(None)
+    st1, m1, l1 = _tiny_step(comm)
+    run_to_run = max(float((a - b).abs().max()) for a, b in zip(m0.parameters(), m0b.parameters()))
+    for x, y in zip(l0, l1):
+        assert abs(x - y) <= 1e-4 * abs(x)
+    for a, b in zip(m0.parameters(), m1.parameters()):
+        assert float((a - b).abs().max()) <= max(10 * run_to_run, 1e-6)
+    assert [b for b, _ in st1.grads.issue_log] == list(range(len(st1.grads.buckets)))
+
+
+def _fp32_bundle(cfg, slots):
+    """Smallest bundle around the measured slots: the model's graph restricted to
+    FP32, unit op costs, one device carrying the slots."""
+    from paper_2407_02327_b200.profiler import bert_graph, build_bundle
+    g = bert_graph(cfg, 4)
+    for n in g["nodes"]:
+        n["supported_precisions"] = ["FP32"]
+    costs = {n["id"]: {"FP32": {"pure_cost_ns": 1000, "fwd_fraction": 1 / 3, "memory_bytes": 1}}
+             for n in g["nodes"]}
+    dev = [{"id": "b200", "is_inference": True, "mem_capacity_bytes": 1 << 40}]
+    return build_bundle(g, costs, [], [], dev, comm={"b200": slots})
+
+
+def test_comm_slots_feed_reference(comm, tmp_path):
+    from oracle.cpu_ref import RefLib
+    if not RefLib.available():
+        pytest.skip("reference library not built")
+    st, _, _ = _tiny_step(comm, timing=True)
+    slots = st.grads.comm_slots()
+    assert len(slots) == len(st.grads.buckets)
+    assert sum(s["bucket_bytes"] for s in slots) == st.grads.flat.numel() * 4
+    offs = [s["earliest_ready_offset_ns"] for s in slots]
+    assert offs == sorted(offs) and all(s["duration_ns"] > 0 for s in slots)
+    path = tmp_path / "b.json"
+    bundle = _fp32_bundle(st.model.cfg, slots)
+    path.write_text(json.dumps(bundle))
+    ns = RefLib().replay_bundle(str(path), {"per_device": {"b200": {}}})
+    assert ns > 0

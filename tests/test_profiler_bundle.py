@@ -79,6 +79,39 @@ def test_bundle_accepted_by_reference_planner(tmp_path, reflib):
     assert reflib.replay_bundle(str(path), {"per_device": rep["devices"]}) > 0
 
 
+def test_comm_slots_accepted_and_replayed(tmp_path, reflib):
+    """The CommSlot sink (profile.hpp:118-129): a bundle carrying per-device
+    bucket slots validates (profile.cpp:385-410) and the replayer's Eq. 6 slots
+    (replayer.cpp:48-73) lengthen the step when the exchange is exposed."""
+    cfg = BertConfig(layers=3)
+    batch = 8
+    g = bert_graph(cfg, batch)
+    costs = _fake_costs(g, cfg, batch)
+    devices = [{"id": "trainer", "is_inference": False, "mem_capacity_bytes": 10**12},
+               {"id": "infer", "is_inference": True, "mem_capacity_bytes": 10**12}]
+    plan = {"per_device": {"trainer": {}, "infer": {}}}
+    base = build_bundle(g, costs, _fake_casts(), _fake_stats(cfg), devices)
+    p0 = tmp_path / "b0.json"
+    p0.write_text(json.dumps(base))
+    t0 = reflib.replay_bundle(str(p0), plan)
+    slots = [{"earliest_ready_offset_ns": 1000 * (i + 1), "duration_ns": 10_000_000, "bucket_bytes": 32 << 20}
+             for i in range(3)]
+    withc = build_bundle(g, costs, _fake_casts(), _fake_stats(cfg), devices,
+                         comm={"trainer": slots, "infer": slots})
+    p1 = tmp_path / "b1.json"
+    p1.write_text(json.dumps(withc))
+    t1 = reflib.replay_bundle(str(p1), plan)
+    # three 10 ms slots run back to back (in order) and the optimizer waits for the last
+    assert t1 > t0 and t1 >= 3 * 10_000_000
+    bad = build_bundle(g, costs, _fake_casts(), _fake_stats(cfg), devices,
+                       comm={"trainer": slots, "infer": slots[:2]})
+    p2 = tmp_path / "b2.json"
+    p2.write_text(json.dumps(bad))
+    with pytest.raises(Exception) as e:
+        reflib.replay_bundle(str(p2), plan)
+    assert "topology" in str(e.value)
+
+
 @pytest.mark.gpu
 def test_profiled_bundle_closes_the_loop(tmp_path, reflib):
     """Measure on the B200 -> reference plan -> apply the plan -> train."""

@@ -83,6 +83,7 @@ def main(name: str, reps: int = 3) -> None:
         fn = {
             "quantize_per_tensor": lambda: ops.quantize_per_tensor(x2, out=q.view(x2.shape)),
             "quantize_with_scale": lambda: ops.quantize_with_scale(x, sc),
+            "quantize_f16": lambda: ops.quantize_with_scale(h, sc),
             "quantize_per_channel": lambda: ops.quantize_per_channel(x2),
             "dequantize": lambda: ops.dequantize_per_tensor(q, sc),
             "cast": lambda: ops.cast(x, torch.float16, out=h),

@@ -13,8 +13,9 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle.cpu_ref import RefLib  # noqa: E402  (test/measurement infrastructure)
 from paper_2407_02327_b200.profiler import (bert_graph, build_bundle, collect_tensor_stats,  # noqa: E402
-                                            graph_step_ms, measure_cast_samples, measure_fused_cast_samples,
-                                            measure_fused_costs, measure_op_costs, net_weight_casts)
+                                            graph_step_ms, measure_cast_samples, measure_comm_slots,
+                                            measure_fused_cast_samples, measure_fused_costs, measure_op_costs,
+                                            measured_op_trace, net_weight_casts)
 from paper_2407_02327_b200.qlinear import FP16, INT8  # noqa: E402
 from paper_2407_02327_b200.train_step import BertConfig, BertEncoderStack, mixed_plan, uniform_plan  # noqa: E402
 
@@ -40,9 +41,11 @@ def main():
     raw_costs = net_weight_casts(cfg, measure_fused_costs(cfg, args.batch, reps=5, calibrate=False), fused_casts)
     cal_costs = net_weight_casts(cfg, measure_fused_costs(cfg, args.batch, reps=5, calibrate=True), fused_casts)
     diag = measure_fused_costs.last_diag
+    # Measured gradient-exchange slots (C ABI NCCL all-reduce; one rank on this box).
+    comm = {"b200": measure_comm_slots(cfg, args.batch)}
     bundles = {
-        "fused": build_bundle(graph, cal_costs, fused_casts, stats, devices),
-        "fused_uncalibrated": build_bundle(graph, raw_costs, fused_casts, stats, devices),
+        "fused": build_bundle(graph, cal_costs, fused_casts, stats, devices, comm=comm),
+        "fused_uncalibrated": build_bundle(graph, raw_costs, fused_casts, stats, devices, comm=comm),
         "per_op": build_bundle(graph, measure_op_costs(cfg, args.batch, reps=10),
                                measure_cast_samples(reps=10), stats, devices),
     }
@@ -65,6 +68,33 @@ def main():
             print(kind, name, rows[name], flush=True)
         out["rows" if kind == "fused" else f"rows_{kind}_bundle"] = rows
     out["calibration"] = diag
+    out["comm_slots"] = comm["b200"]
+    # Measured vs predicted operator-level traces of the mixed plan, same event ids
+    # (replayer.cpp:126-148): the measured eager single-stream step against the
+    # uncalibrated fused bundle (built from the same eager regions).
+    import gzip
+    meas = measured_op_trace(cfg, args.batch, plans["mixed"], "b200")
+    pred = ref.replay_trace(args.bundle.replace(".json", "_fused_uncalibrated.json"),
+                            {"per_device": {"b200": plans["mixed"]}})
+    base = args.out[:-5] if args.out.endswith(".json") else args.out
+    for tag, tr in (("measured", meas), ("predicted", pred)):
+        with gzip.open(f"{base}_{tag}_mixed.trace.json.gz", "wt") as f:
+            json.dump(tr, f)
+
+    def by_id(tr):
+        d = {}
+        for e in tr["traceEvents"]:
+            d[e["name"]] = d.get(e["name"], 0.0) + e["dur"]
+        return d
+    m_id, p_id = by_id(meas), by_id(pred)
+    common = sorted(set(m_id) & set(p_id))
+    out["trace_diff_mixed"] = {
+        "ids_measured": len(m_id), "ids_predicted": len(p_id), "ids_common": len(common),
+        "only_measured": sorted(set(m_id) - set(p_id)), "only_predicted": sorted(set(p_id) - set(m_id)),
+        "sum_us_measured": sum(m_id[k] for k in common), "sum_us_predicted": sum(p_id[k] for k in common),
+        "worst": sorted(({"id": k, "measured_us": m_id[k], "predicted_us": p_id[k]} for k in common),
+                        key=lambda r: -abs(r["measured_us"] - r["predicted_us"]))[:10],
+    }
     with open(args.out, "w") as f:
         json.dump(out, f, indent=1)
 

@@ -29,7 +29,8 @@ ALG = {  # algorithmic flops (GEMM) or bytes (streaming) per launch
     "conv_dgrad": (2.0 * 64 * 28 * 28 * 128 * 9 * 128, "flops"),
     "quantize_with_scale": ((1 << 28) * 5, "bytes"), "quantize_per_channel": ((1 << 28) * 5, "bytes"),
     "absmax": ((1 << 28) * 4, "bytes"), "stats": ((1 << 28) * 4, "bytes"), "cast": ((1 << 28) * 6, "bytes"),
-    "dequantize": ((1 << 28) * 5, "bytes"),
+    "dequantize": ((1 << 28) * 5, "bytes"), "quantize_f16": ((1 << 28) * 3, "bytes"),
+    "quantize_per_tensor": ((1 << 28) * 5, "bytes"),
 }
 
 
