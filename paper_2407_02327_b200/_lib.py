@@ -106,6 +106,7 @@ SIGNATURES = {
     "qsync_gemm_set_pdl": [_int],
     "qsync_conv_set_impl": [_int],
     "qsync_gemm_set_max_ctas": [_int],
+    "qsync_gemm_trace_buffer": [_p],
     "qsync_attention_set_impl": [_int],
     "qsync_mt_jump_selftest": [],
 }

@@ -31,8 +31,9 @@ namespace {
 
 constexpr int BM = 128;             // UMMA M (cta_group::1)
 constexpr int BK_BYTES = 128;       // one 128B swizzle row per stage
-constexpr int kThreads = 192;       // 6 warps
 constexpr int kEpiWarp0 = 2;
+constexpr int kEpiWarps = 8;        // two per TMEM lane quadrant
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // producer, MMA, 8 epilogue warps
 
 struct EpiParams {
     int64_t M, N, K;
@@ -81,20 +82,54 @@ struct Cfg {
 #endif
     static constexpr int kStagesWant =
         kStageBytes >= 48 * 1024 ? QSB_GEMM_STAGES_48K : (kStageBytes >= 32 * 1024 ? 6 : 8);
-#ifndef QSB_GEMM_EPIBUFS
-#define QSB_GEMM_EPIBUFS 2
-#endif
-    // 4 warps x QSB_GEMM_EPIBUFS staging chunks.  1 frees 16 KB: a 5th stage for
-    // 192-wide tiles -- measured +0.2% on the step (tools/build_variant.sh A/B), so 2 stays.
-    static constexpr int kEpiStageBytes = 4 * QSB_GEMM_EPIBUFS * kStageChunkBytes;
-    // ... as many as fit next to the epilogue staging in 227 KB (BN = 192: 4 x 40 KB)
-    static constexpr int kStagesFit = (227 * 1024 - kEpiStageBytes - 1024 - 256) / kStageBytes;
+    // Staging chunks per epilogue warp: two (the TMA store of one overlaps the
+    // next chunk's math) unless that costs a mainloop stage (BN = 256, 1 CTA).
+    static constexpr int kEpiBufs = (BN / kCta) >= 256 ? 1 : 2;
+    static constexpr int kEpiStageBytes = kEpiWarps * kEpiBufs * kStageChunkBytes;
+    // per-column epilogue factors of the current tile: scale (s_a * s_b[n]) + bias
+    static constexpr int kFacBytes = 2 * BN * 4;
+    // mbarriers (full/empty per stage, 2 tfull + 2 tempty) + the TMEM address slot
+    static constexpr int kBarBytes = ((2 * kStagesWant + 4) * 8 + 4 + 15) / 16 * 16;
+    // ... as many stages as fit next to the epilogue staging in 227 KB (the
+    // dynamic smem base is 1024-aligned, __align__ below; checked at entry)
+    static constexpr int kStagesFit = (227 * 1024 - kEpiStageBytes - kFacBytes - kBarBytes) / kStageBytes;
     static constexpr int kStages = kStagesWant < kStagesFit ? kStagesWant : kStagesFit;
     // two accumulator buffers; TMEM allocations are powers of two (BN = 192 -> 512)
     static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-    static constexpr int kSmemBytes =
-        kStages * kStageBytes + kEpiStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kEpiStageBytes + kFacBytes + kBarBytes;
 };
+
+// Phase timeline of every CTA (tools/gemm_trace.py; A/B builds only:
+// tools/build_variant.sh <lib> -DQSB_GEMM_TRACE).  Slot layout per CTA:
+// [0] globaltimer at entry, [1] clock at entry, [2] clock after the prologue
+// (griddepcontrol.wait), [3] clock at exit, [4] globaltimer at exit; then per unit u < 8 at 8 + 8u:
+// [0] producer's first load issued, [1] MMA: accumulator free, [2] MMA: first
+// stage full, [3] MMA: last commit issued, [4] epilogue: accumulator full,
+// [5] epilogue: last store issued.
+#ifdef QSB_GEMM_TRACE
+__device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ unsigned long long trace_clock() {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    return c;
+}
+#define QSB_TRACE(slot, val)                                                               \
+    do {                                                                                   \
+        if (g_gemm_trace) g_gemm_trace[static_cast<size_t>(blockIdx.x) * 72 + (slot)] = (val); \
+    } while (0)
+#define QSB_TRACE_U(u, ev)                                                      \
+    do {                                                                        \
+        const int _k = ((u) - unit0) / unit_stride;                             \
+        if (_k < 8) QSB_TRACE(8 + 8 * _k + (ev), trace_clock());                \
+    } while (0)
+#else
+#define QSB_TRACE(slot, val) \
+    do {                     \
+    } while (0)
+#define QSB_TRACE_U(u, ev) \
+    do {                   \
+    } while (0)
+#endif
 
 __device__ __forceinline__ float bits_f(uint32_t v) { return __uint_as_float(v); }
 
@@ -111,14 +146,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // template bit, not a runtime flag: a per-MMA / per-element branch on it cost
     // the INT8 GEMM 20% (8192^3: 3.07 -> 2.43 POPS).
     constexpr bool kF8 = (kLay & 128) != 0;
-    extern __shared__ uint8_t smem_raw[];
-    // 1024-byte alignment for the 128B swizzle atoms.
-    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
-    uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for the 128B swizzle atoms: the declaration asks for
+    // it and the smem budget (Cfg::kSmemBytes) assumes it -- trap, not corrupt.
+    if (ptx::smem_u32(smem_raw) & 1023) __trap();
+    uint8_t* smem = smem_raw;
     uint8_t* smem_a = smem;                              // kStages x [BM rows x 128B]
     uint8_t* smem_b = smem + kStages * BM * BK_BYTES;    // kStages x [kBRows rows x 128B]
     uint8_t* smem_stage = smem + kStages * C::kStageBytes;  // 1024-aligned epilogue staging
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_stage + C::kEpiStageBytes);
+    float* fac = reinterpret_cast<float*>(smem_stage + C::kEpiStageBytes);  // [2][BN]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_stage + C::kEpiStageBytes + C::kFacBytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + kStages;
     uint64_t* tfull = bars + 2 * kStages;
@@ -127,6 +164,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+#ifdef QSB_GEMM_TRACE
+    if (threadIdx.x == 0) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        QSB_TRACE(0, gt);
+        QSB_TRACE(1, trace_clock());
+    }
+#endif
 
     const int64_t M = p.M, N = p.N, K = p.K;
     constexpr int kTileM = BM * kCta;  // rows of one (pair) tile
@@ -155,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], kCta * 4 * 32);  // epilogue threads of both CTAs
+            ptx::mbar_init(&tempty[a], kCta * kEpiWarps * 32);  // epilogue threads of both CTAs
         }
         ptx::fence_mbar_init();
     }
@@ -177,6 +222,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // no global memory is touched before the previous grid has completed.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef QSB_GEMM_TRACE
+    if (threadIdx.x == 0) QSB_TRACE(2, trace_clock());
+#endif
     // Leader-CTA addresses of the barriers the pair shares.
     const uint32_t full_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
     const uint32_t tempty_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
@@ -331,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (kb == kb0) QSB_TRACE_U(u, 0);
                     if (kCta == 2) {
                         // Both CTAs' bytes complete on the leader's full barrier.
                         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], kCta * C::kStageBytes);
@@ -432,10 +481,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int kb0 = (u % ksplit) * p.kb_per;
                 const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                QSB_TRACE_U(u, 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
+                    if (kb == kb0) QSB_TRACE_U(u, 2);
                     // cp.async (generic proxy) wrote A: order it before the
                     // tensor core's async-proxy reads.
                     if (kLay & 12) ptx::fence_proxy_async_smem();
@@ -482,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tc_commit_pair(&tfull[acc]);  // both CTAs' epilogues
                 else
                     ptx::tc_commit(&tfull[acc]);
+                QSB_TRACE_U(u, 3);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -489,13 +541,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5) =====================
+        // ===================== epilogue (warps 2..9) =====================
+        // Two warps per TMEM lane quadrant (warp w reads lanes 32*(w%4)..+31):
+        // the tile's column chunks alternate between them, so each quadrant's
+        // TMEM loads, dequant math and staging stores run on two warps.
         // TMEM -> registers -> (scale, bias) -> 128B-swizzled smem staging ->
-        // TMA 2-D store (or reduce-add) of a 32-row x 128-byte chunk per warp,
-        // double-buffered per warp.  Direct global stores remain as the path for
+        // TMA 2-D store (or reduce-add) of a 32-row x 128-byte chunk per warp.
+        // The per-column factors (s_a*s_b[n], bias[n]) are staged in smem once
+        // per tile by all epilogue threads (broadcast float4 reads replace the
+        // per-column shuffles).  Direct global stores remain as the path for
         // shapes TMA cannot address (row pitch not a multiple of 16 bytes).
-        const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-        uint8_t* my_stage = smem_stage + (warp - kEpiWarp0) * QSB_GEMM_EPIBUFS * kStageChunkBytes;
+        const int ew = warp - kEpiWarp0;  // 0..7
+        const int quad = warp & 3;        // TMEM lane quadrant this warp may access
+        const int half = ew >> 2;         // chunks half, half + 2, ... of the tile
+        const int et = ew * 32 + lane;    // 0..255
+        uint8_t* my_stage = smem_stage + ew * C::kEpiBufs * kStageChunkBytes;
+        float* fs = fac;       // [BN] column scale
+        float* fb = fac + BN;  // [BN] column bias
         int sbuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -504,27 +566,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sa = (kI8 && p.scale_a) ? *p.scale_a : 1.0f;
         const bool out16 = p.c && p.c_dtype != QSYNC_F32;
         const bool raw = p.c_i32 != nullptr && p.c == nullptr;
+        const bool need_fac = !raw && (kI8 || p.bias);
         const int chunk_cols = out16 ? 64 : 32;
-        constexpr int kNC = BN / 32;  // 32-column groups per tile
+#ifdef QSB_GEMM_TRACE
+        unsigned long long t_ld = 0, t_math = 0, t_wait = 0, t_store = 0;
+#endif
         for (int u = unit0; u < num_units; u += unit_stride) {
             const int t = u / ksplit;
             const bool add_bias = (u % ksplit) == 0;  // bias once per tile under split-K
             const int64_t m0 = static_cast<int64_t>(t % num_m) * kTileM + static_cast<int64_t>(rank) * BM;
             const int64_t n0 = static_cast<int64_t>(t / num_m) * BN;
-            // Per-column epilogue factors of this tile, loaded BEFORE waiting for
-            // the accumulator so their latency hides behind the tile's MMAs:
-            // lane j holds columns n0 + 32*i + j.
-            float col_sb[kNC], col_bias[kNC];
-#pragma unroll
-            for (int i = 0; i < kNC; ++i) {
-                const int64_t col = n0 + 32 * i + lane;
-                const bool ok = col < N;
-                float sb = 1.0f;
-                if (kI8 && p.scale_b) sb = p.b_per_channel ? (ok ? p.scale_b[col] : 0.0f) : *p.scale_b;
-                col_sb[i] = sb;
-                col_bias[i] = (p.bias && ok && add_bias) ? p.bias[col] : 0.0f;
+            if (need_fac) {
+                // Every epilogue warp is past the previous tile's factors, then this
+                // tile's are written -- BEFORE waiting for the accumulator, so their
+                // latency hides behind the tile's MMAs.
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+                for (int c = et; c < BN; c += kEpiWarps * 32) {
+                    const int64_t col = n0 + c;
+                    const bool ok = col < N;
+                    if (kI8) {
+                        const float sb = p.scale_b ? (p.b_per_channel ? (ok ? p.scale_b[col] : 0.0f) : *p.scale_b)
+                                                   : 1.0f;
+                        fs[c] = __fmul_rn(sa, sb);
+                    }
+                    fb[c] = (p.bias && ok && add_bias) ? p.bias[col] : 0.0f;
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
             }
             ptx::mbar_wait(&tfull[acc], acc_phase);
+            if (warp == kEpiWarp0 && lane == 0) QSB_TRACE_U(u, 4);
             ptx::tc_fence_after();
             const int64_t row0 = m0 + quad * 32;
             const int64_t row = row0 + lane;
@@ -532,18 +602,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += chunk_cols) {
+            for (int c0 = half * chunk_cols; c0 < BN; c0 += 2 * chunk_cols) {
                 uint32_t w[32];  // the 128 bytes of this thread's row in the chunk
-                uint32_t rawv[32];  // raw accumulators when both outputs are requested
-                float v[32];
                 const int64_t col0 = n0 + c0;
                 const int nsub = out16 ? 2 : 1;
                 // Both 32-column TMEM loads of a 16-bit chunk are in flight
                 // before the single wait.
                 uint32_t rr[2][32];
+#ifdef QSB_GEMM_TRACE
+                unsigned long long tc0 = trace_clock();
+#endif
                 ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0), rr[0]);
                 if (out16) ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0 + 32), rr[1]);
                 ptx::tmem_ld_wait();
+#ifdef QSB_GEMM_TRACE
+                unsigned long long tc1 = trace_clock();
+                t_ld += tc1 - tc0;
+#endif
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     if (sub >= nsub) break;
@@ -554,58 +629,57 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j) w[j] = r[j];
                         continue;
                     }
-                    if (p.c_i32) {
+                    if (p.c_i32 && row_ok && row0 < M) {
+                        // both outputs requested (direct-store path): raw accumulators first
+                        int32_t* dst = p.c_i32 + row * N + col0;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) rawv[j] = r[j];
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < N) dst[j] = static_cast<int32_t>(r[j]);
                     }
-                    // Select this 32-column group's factors (register selects, no
-                    // local memory), then broadcast column j's from lane j.
-                    const int g = (c0 >> 5) + sub;
-                    float sb = col_sb[0], bs = col_bias[0];
+                    const int cb = c0 + 32 * sub;  // tile column of r[0]
+                    const bool bf = p.c_dtype == QSYNC_BF16;
 #pragma unroll
-                    for (int i = 1; i < kNC; ++i) {
-                        if (g == i) {
-                            sb = col_sb[i];
-                            bs = col_bias[i];
+                    for (int j = 0; j < 32; j += 4) {
+                        float4 s4 = make_float4(alpha, alpha, alpha, alpha);
+                        if (kI8) s4 = *reinterpret_cast<const float4*>(fs + cb + j);
+                        const float sj[4] = {s4.x, s4.y, s4.z, s4.w};
+                        float v[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint32_t a = r[j + e];
+                            v[e] = kI8 ? __fmul_rn(kF8 ? bits_f(a) : __int2float_rn(static_cast<int>(a)), sj[e])
+                                       : __fmul_rn(bits_f(a), sj[e]);
                         }
-                    }
-                    const float colscale = kI8 ? __fmul_rn(sa, sb) : alpha;
-                    // Column j's factors live in lane j: broadcast by shuffle only
-                    // where they vary per column (INT8 per-channel scale, bias); the
-                    // FP16 GEMMs' alpha is uniform.
-                    if (p.bias) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float sj = kI8 ? __shfl_sync(0xffffffffu, colscale, j) : alpha;
-                            const float bj = __shfl_sync(0xffffffffu, bs, j);
-                            const float x = kI8 ? __fmul_rn(kF8 ? bits_f(r[j]) : __int2float_rn(static_cast<int>(r[j])), sj)
-                                                : __fmul_rn(bits_f(r[j]), sj);
-                            v[j] = __fadd_rn(x, bj);
+                        if (p.bias) {
+                            const float4 b4 = *reinterpret_cast<const float4*>(fb + cb + j);
+                            v[0] = __fadd_rn(v[0], b4.x);
+                            v[1] = __fadd_rn(v[1], b4.y);
+                            v[2] = __fadd_rn(v[2], b4.z);
+                            v[3] = __fadd_rn(v[3], b4.w);
                         }
-                    } else {
+                        if (out16) {
+                            w[16 * sub + j / 2] = bf ? pack_bf162(v[0], v[1]) : pack_half2(v[0], v[1]);
+                            w[16 * sub + j / 2 + 1] = bf ? pack_bf162(v[2], v[3]) : pack_half2(v[2], v[3]);
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float sj = kI8 ? __shfl_sync(0xffffffffu, colscale, j) : alpha;
-                            v[j] = kI8 ? __fmul_rn(kF8 ? bits_f(r[j]) : __int2float_rn(static_cast<int>(r[j])), sj)
-                                       : __fmul_rn(bits_f(r[j]), sj);
+                            for (int e = 0; e < 4; ++e) w[j + e] = __float_as_uint(v[e]);
                         }
-                    }
-                    if (out16) {
-                        const bool bf = p.c_dtype == QSYNC_BF16;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            w[16 * sub + j] = bf ? pack_bf162(v[2 * j], v[2 * j + 1]) : pack_half2(v[2 * j], v[2 * j + 1]);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
                     }
                 }
+#ifdef QSB_GEMM_TRACE
+                unsigned long long tc2 = trace_clock();
+                t_math += tc2 - tc1;
+#endif
                 if (row0 >= M || col0 >= N || p.debug_epi) continue;  // warp-uniform skip
                 if (p.tma_store) {
-                    // Free the staging buffer used two chunks ago, then write this
-                    // row's 8 x 16B pieces at their 128B-swizzled positions.
-                    if (lane == 0) ptx::bulk_wait_read<QSB_GEMM_EPIBUFS - 1>();
+                    // Free the staging buffer used kEpiBufs chunks ago, then write
+                    // this row's 8 x 16B pieces at their 128B-swizzled positions.
+                    if (lane == 0) ptx::bulk_wait_read<C::kEpiBufs - 1>();
                     __syncwarp();
+#ifdef QSB_GEMM_TRACE
+                    unsigned long long tc3 = trace_clock();
+                    t_wait += tc3 - tc2;
+#endif
                     uint8_t* buf = my_stage + sbuf * kStageChunkBytes;
                     const uint32_t rbase = ptx::smem_u32(buf) + lane * 128;
 #pragma unroll
@@ -623,18 +697,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                               static_cast<int32_t>(row0));
                         ptx::bulk_commit();
                     }
-                    sbuf = (sbuf + 1) % QSB_GEMM_EPIBUFS;
+                    sbuf = (sbuf + 1) % C::kEpiBufs;
+#ifdef QSB_GEMM_TRACE
+                    t_store += trace_clock() - tc3;
+#endif
                     continue;
                 }
                 // ---- direct-store path (fully unrolled: keeps w[] in registers) ----
                 if (!row_ok) continue;
-                if (p.c_i32) {
+                if (raw) {
                     int32_t* dst = p.c_i32 + row * N + col0;
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        if (col0 + j < N) dst[j] = static_cast<int32_t>(raw ? w[j] : rawv[j]);
+                        if (col0 + j < N) dst[j] = static_cast<int32_t>(w[j]);
+                    continue;
                 }
-                if (raw) continue;
                 if (!out16) {
                     float* dst = static_cast<float*>(p.c) + row * N + col0;
 #pragma unroll
@@ -665,6 +742,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            if (warp == kEpiWarp0 && lane == 0) QSB_TRACE_U(u, 5);
             ptx::tc_fence_before();
             if (kCta == 2)
                 ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);  // leader's barrier
@@ -678,6 +756,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // The staging smem must outlive the TMA reads only; the global writes complete
         // with the grid (the next kernel sees them after its griddepcontrol.wait).
         if (lane == 0) ptx::bulk_wait_read<0>();
+#ifdef QSB_GEMM_TRACE
+        if (warp == kEpiWarp0 && lane == 0) {  // header slots 5..7 + the spare slot 71
+            QSB_TRACE(5, t_ld);
+            QSB_TRACE(6, t_math);
+            QSB_TRACE(7, t_wait);
+            QSB_TRACE(71, t_store);
+        }
+#endif
     }
 
     ptx::tc_fence_before();
@@ -685,6 +771,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::cluster_sync();  // both CTAs done with TMEM and remote barriers
     else
         __syncthreads();
+#ifdef QSB_GEMM_TRACE
+    if (threadIdx.x == 0) {
+        QSB_TRACE(3, trace_clock());
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        QSB_TRACE(4, gt);
+    }
+#endif
     if (warp == 1) {
         ptx::tc_fence_after();
         if (kCta == 2)
@@ -1123,6 +1217,19 @@ int qsync_gemm_force_splitk(int ks) {
     QSB_REQUIRE(ks >= 0 && ks <= 64, QSYNC_ERR_DOMAIN, "split-K override must be in [0, 64]");
     g_force_splitk = ks;
     return QSYNC_OK;
+}
+
+// A/B hook (QSB_GEMM_TRACE builds): device buffer of 72 uint64 per CTA for
+// the phase timeline; nullptr turns tracing off.  No-op in normal builds.
+int qsync_gemm_trace_buffer(void* buf) {
+#ifdef QSB_GEMM_TRACE
+    unsigned long long* p = static_cast<unsigned long long*>(buf);
+    QSB_TRY(cuda_status(cudaMemcpyToSymbol(g_gemm_trace, &p, sizeof(p)), "cudaMemcpyToSymbol"));
+    return QSYNC_OK;
+#else
+    (void)buf;
+    return set_error(QSYNC_ERR_DOMAIN, "library built without QSB_GEMM_TRACE");
+#endif
 }
 
 int qsync_gemm_set_max_ctas(int n) {

@@ -221,10 +221,11 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
         const int64_t n16 = n / 16;
         const uint4* xv = reinterpret_cast<const uint4*>(x);
         uint4* qv = reinterpret_cast<uint4*>(q);
-        for (int64_t i = tid; i < n16; i += stride) {
-            uint4 r[LOADS];
-#pragma unroll
-            for (int u = 0; u < LOADS; ++u) r[u] = ld_stream(xv + i * LOADS + u);
+        // G groups of 16 elements per thread-iteration, all loads issued before
+        // any math: 128 B (F32) / 64 B (16-bit) in flight per thread, so the
+        // stream stays HBM-bound at the occupancy the registers allow.
+        constexpr int G = DT == QSYNC_F32 ? 2 : (ACT == 1 ? 2 : 4);
+        auto process = [&](int64_t i, const uint4 (&r)[LOADS]) {
             uint32_t packed[4];
             uint32_t dp[8];  // GELU'(x) of the 16 elements as FP16 pairs (the backward's factor)
             uint32_t hq[8];  // the 16 grid values as FP16 pairs (exact; the wgrad's operand)
@@ -268,6 +269,22 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                 dv[0] = make_uint4(dp[0], dp[1], dp[2], dp[3]);
                 dv[1] = make_uint4(dp[4], dp[5], dp[6], dp[7]);
             }
+        };
+        int64_t i = tid;
+        for (; i + (G - 1) * stride < n16; i += G * stride) {
+            uint4 r[G][LOADS];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int u = 0; u < LOADS; ++u) r[g][u] = ld_stream(xv + (i + g * stride) * LOADS + u);
+#pragma unroll
+            for (int g = 0; g < G; ++g) process(i + g * stride, r[g]);
+        }
+        for (; i < n16; i += stride) {
+            uint4 r[LOADS];
+#pragma unroll
+            for (int u = 0; u < LOADS; ++u) r[u] = ld_stream(xv + i * LOADS + u);
+            process(i, r);
         }
         done = n16 * 16;
     }
@@ -927,7 +944,7 @@ struct QuantRun {
             return check_launch("k_tile<quant>");
         }
         const int vec = aligned16(x) && aligned16(q);
-        const int grid = grid_for(n / 16 + 1, kThreads, 4);
+        const int grid = grid_for(n / 16 + 1, kThreads, 2);  // <= 64 regs: 2 x 512 threads per SM
         pdl_launch(k_quantize<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, scale + 1, nullptr,
                                                   q, scale, vec, static_cast<uint16_t*>(nullptr), static_cast<uint16_t*>(nullptr));
         return check_launch("k_quantize");
@@ -940,7 +957,7 @@ struct QuantScaleRun {
         using T = typename Elem<DT>::T;
         if (n == 0) return QSYNC_OK;
         const int vec = aligned16(x) && aligned16(q);
-        const int grid = grid_for(n / 16 + 1, kThreads, 4);
+        const int grid = grid_for(n / 16 + 1, kThreads, 2);  // <= 64 regs: 2 x 512 threads per SM
         pdl_launch(k_quantize<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, nullptr, scale, q,
                                                   nullptr, vec, static_cast<uint16_t*>(nullptr), static_cast<uint16_t*>(nullptr));
         return check_launch("k_quantize");
@@ -1017,7 +1034,7 @@ struct QuantActRun {
         using T = typename Elem<DT>::T;
         if (n == 0) return QSYNC_OK;
         const int vec = aligned16(x) && aligned16(q) && (!dact || aligned16(dact)) && (!q16 || aligned16(q16));
-        const int grid = grid_for(n / 16 + 1, kThreads, 4);
+        const int grid = grid_for(n / 16 + 1, kThreads, 2);  // <= 64 regs: 2 x 512 threads per SM
         if (act == 1)
             pdl_launch(k_quantize<DT, 1>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, absmax, nullptr,
                                                          q, scale_out, vec, dact, q16);

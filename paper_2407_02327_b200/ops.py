@@ -216,8 +216,10 @@ GEMM_TIMER: list | None = None
 def _timed(kind: str, flops: float):
     if GEMM_TIMER is None:
         return None
-    s = torch.cuda.Event(enable_timing=True)
-    e = torch.cuda.Event(enable_timing=True)
+    # inside a CUDA-graph capture the events become event-record nodes of the graph
+    ext = torch.cuda.is_current_stream_capturing()
+    s = torch.cuda.Event(enable_timing=True, external=ext)
+    e = torch.cuda.Event(enable_timing=True, external=ext)
     s.record()
     GEMM_TIMER.append((kind, flops, s, e))
     return e

@@ -51,8 +51,12 @@ def test_reference_acceptance_gate_against_device_library():
         pytest.skip("acceptance binary not built (needs /root/reference at build time)")
     r = subprocess.run([ACCEPTANCE], capture_output=True, text=True, timeout=900)
     print(r.stdout)
-    lines = {ln.split(": ", 1)[1].rsplit(" (", 1)[0]: ln.split(":", 1)[0]
-             for ln in r.stdout.splitlines() if ln.startswith(("PASS: ", "FAIL: "))}
+    import re
+    lines = {}
+    for ln in r.stdout.splitlines():
+        m = re.match(r"^(PASS|FAIL): (.*?) \([0-9.]+s\)", ln)
+        if m:
+            lines[m.group(2)] = m.group(1)
     for name in ("fixed-point variance bound (Monte Carlo, 100 x 1e5 samples)",
                  "floating-point variance bound (20 x 1e5 samples, 9 mantissa bits)",
                  "stochastic rounding unbiasedness (1e6 samples)"):
