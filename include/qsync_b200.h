@@ -319,7 +319,8 @@ int qsync_act_cast(const void* x, int src_dtype, void* out, int dst_dtype, int64
  * g = dy * act'(h) (act NONE: g = dy, h may be NULL; act DERIV: h is the FP16
  * act'(x) the forward stored, g = dy * h), out (optional) = g as
  * out_dtype, colsum (optional) += sum_rows g (the bias gradient).  dy, h
- * [rows, cols] F32/F16. */
+ * [rows, cols] F32/F16; with act NONE, dy and out may also be BF16 (the BF16
+ * backward entry of a BF16-planned op). */
 int qsync_act_bwd_colsum(const void* dy, int dy_dtype, const void* h, int h_dtype, int64_t rows,
                          int64_t cols, int act, void* out, int out_dtype, float* colsum,
                          qsync_stream_t stream);

@@ -50,7 +50,7 @@ __device__ __forceinline__ void store8v(void* base, int64_t i, const float* f) {
         uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            w[k] = pack_half2(f[2 * k], f[2 * k + 1]);
+            w[k] = DT == QSYNC_BF16 ? pack_bf162(f[2 * k], f[2 * k + 1]) : pack_half2(f[2 * k], f[2 * k + 1]);
         }
         *reinterpret_cast<uint4*>(static_cast<uint16_t*>(base) + i) = make_uint4(w[0], w[1], w[2], w[3]);
     }
@@ -60,6 +60,8 @@ template <int DT>
 __device__ __forceinline__ void store1(void* base, int64_t i, float v) {
     if constexpr (DT == QSYNC_F32)
         static_cast<float*>(base)[i] = v;
+    else if constexpr (DT == QSYNC_BF16)
+        static_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(v);
     else
         static_cast<__half*>(base)[i] = __float2half_rn(v);
 }
@@ -167,6 +169,10 @@ template <int DDY, int DH, int ACT>
 int act_bwd_out(const void* dy, const void* h, int64_t rows, int64_t cols, void* out, int out_dtype,
                 float* colsum, cudaStream_t st) {
     if (out_dtype == QSYNC_F32) return launch_act_bwd<DDY, DH, QSYNC_F32, ACT>(dy, h, rows, cols, out, colsum, st);
+    if constexpr (ACT == 0) {  // the BF16 backward entry of a BF16 op (no activation)
+        if (out_dtype == QSYNC_BF16)
+            return launch_act_bwd<DDY, DH, QSYNC_BF16, ACT>(dy, h, rows, cols, out, colsum, st);
+    }
     return launch_act_bwd<DDY, DH, QSYNC_F16, ACT>(dy, h, rows, cols, out, colsum, st);
 }
 
@@ -194,16 +200,20 @@ int qsync_act_bwd_colsum(const void* dy, int dy_dtype, const void* h, int h_dtyp
     QSB_REQUIRE(act == QSYNC_ACT_NONE || act == QSYNC_ACT_GELU || act == QSYNC_ACT_DERIV, QSYNC_ERR_DOMAIN,
                 "unknown activation");
     QSB_REQUIRE(act == QSYNC_ACT_NONE || h != nullptr, QSYNC_ERR_VALIDATION, "activation backward needs h");
-    QSB_REQUIRE(dy_dtype == QSYNC_F32 || dy_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN, "dy must be F32 or F16");
+    QSB_REQUIRE(dy_dtype == QSYNC_F32 || dy_dtype == QSYNC_F16 || (dy_dtype == QSYNC_BF16 && act == QSYNC_ACT_NONE),
+                QSYNC_ERR_DOMAIN, "dy must be F32 or F16 (BF16 without an activation)");
     QSB_REQUIRE(act != QSYNC_ACT_GELU || h_dtype == QSYNC_F32 || h_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN,
                 "h must be F32 or F16");
     QSB_REQUIRE(act != QSYNC_ACT_DERIV || h_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN, "a stored derivative is F16");
-    QSB_REQUIRE(!out || out_dtype == QSYNC_F32 || out_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN,
-                "out must be F32 or F16");
+    QSB_REQUIRE(!out || out_dtype == QSYNC_F32 || out_dtype == QSYNC_F16 ||
+                    (out_dtype == QSYNC_BF16 && act == QSYNC_ACT_NONE),
+                QSYNC_ERR_DOMAIN, "out must be F32 or F16 (BF16 without an activation)");
     if (rows == 0 || cols == 0 || (!out && !colsum)) return QSYNC_OK;
     cudaStream_t st = to_stream(stream);
     if (dy_dtype == QSYNC_F32)
         return act_bwd_h<QSYNC_F32>(dy, h, h_dtype, rows, cols, act, out, out_dtype, colsum, st);
+    if (dy_dtype == QSYNC_BF16)
+        return act_bwd_out<QSYNC_BF16, QSYNC_F32, 0>(dy, nullptr, rows, cols, out, out_dtype, colsum, st);
     return act_bwd_h<QSYNC_F16>(dy, h, h_dtype, rows, cols, act, out, out_dtype, colsum, st);
 }
 

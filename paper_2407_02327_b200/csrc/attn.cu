@@ -887,21 +887,10 @@ int qsync_attention_fwd(const void* qkv, int64_t B, int64_t S, int64_t H, int64_
     QSB_REQUIRE(qkv && out && lse, QSYNC_ERR_VALIDATION, "attention needs qkv, out and lse buffers");
     QSB_TRY(check_shape(B, S, H, D));
     cudaStream_t st = to_stream(stream);
-    static bool configured = false;
-    if (!configured) {
-        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem),
-                            "cudaFuncSetAttribute"));
-        configured = true;
-    }
+    QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_fwd), kFwdSmem));
     if (out_absmax) QSB_TRY(zero_async(out_absmax, sizeof(float), st));
     if (g_attn_tc) {
-        static bool tc_configured = false;
-        if (!tc_configured) {
-            QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     kTcFwdSmem),
-                                "cudaFuncSetAttribute"));
-            tc_configured = true;
-        }
+        QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_fwd_tc), kTcFwdSmem));
         CUtensorMap tm;
         QSB_TRY(make_tma_2d(&tm, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 3 * H * kD, B * kS, kD, kS));
         pdl_launch(k_attn_fwd_tc, dim3(static_cast<unsigned>(B * H)), dim3(kTcThreads), kTcFwdSmem, st, tm,
@@ -920,13 +909,7 @@ int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, cons
     QSB_TRY(check_shape(B, S, H, D));
     cudaStream_t st = to_stream(stream);
     if (g_attn_tc == 2) {
-        static bool tc2_configured = false;
-        if (!tc2_configured) {
-            QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_bwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     kTcBwd2Smem),
-                                "cudaFuncSetAttribute"));
-            tc2_configured = true;
-        }
+        QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_bwd_tc2), kTcBwd2Smem));
         CUtensorMap tq, td;
         QSB_TRY(make_tma_2d(&tq, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 3 * H * kD, B * kS, kD, kS));
         QSB_TRY(make_tma_2d(&td, dout, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, H * kD, B * kS, kD, kS));
@@ -936,13 +919,7 @@ int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, cons
         return check_launch("k_attn_bwd_tc2");
     }
     if (g_attn_tc) {
-        static bool tc_configured = false;
-        if (!tc_configured) {
-            QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     kTcBwdSmem),
-                                "cudaFuncSetAttribute"));
-            tc_configured = true;
-        }
+        QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_bwd_tc), kTcBwdSmem));
         CUtensorMap tq, td;
         QSB_TRY(make_tma_2d(&tq, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 3 * H * kD, B * kS, kD, kS));
         QSB_TRY(make_tma_2d(&td, dout, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, H * kD, B * kS, kD, kS));
@@ -951,12 +928,7 @@ int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, cons
                    scale, static_cast<__half*>(dqkv));
         return check_launch("k_attn_bwd_tc");
     }
-    static bool configured = false;
-    if (!configured) {
-        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem),
-                            "cudaFuncSetAttribute"));
-        configured = true;
-    }
+    QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_bwd), kBwdSmem));
     pdl_launch(k_attn_bwd, dim3(static_cast<unsigned>(B * H)), dim3(kThreadsA), kBwdSmem, st, 
         static_cast<const __half*>(qkv), static_cast<const __half*>(out), static_cast<const __half*>(dout), lse,
         static_cast<int>(H), scale, static_cast<__half*>(dqkv));

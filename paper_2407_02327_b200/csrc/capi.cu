@@ -8,6 +8,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <set>
 #include <string>
 
 #include "common.cuh"
@@ -73,6 +74,19 @@ int zero_async(void* p, int64_t bytes, cudaStream_t st) {
     const int64_t n = bytes / 4;
     const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 1024));
     return launch_pdl("k_zero_words", k_zero_words, dim3(grid), dim3(256), 0, st, static_cast<uint32_t*>(p), n);
+}
+
+int ensure_max_dynamic_smem(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    QSB_TRY(cuda_status(cudaGetDevice(&dev), "cudaGetDevice"));
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({kernel, dev})) return QSYNC_OK;
+    QSB_TRY(cuda_status(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        "cudaFuncSetAttribute"));
+    done.insert({kernel, dev});
+    return QSYNC_OK;
 }
 
 int sm_count() {

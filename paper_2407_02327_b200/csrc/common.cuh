@@ -39,6 +39,10 @@ inline int cuda_status(cudaError_t e, const char* what) {
 inline cudaStream_t to_stream(qsync_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-DEVICE property:
+// set it once per (kernel, device ordinal) -- a process that launches on a
+// second GPU gets the attribute there too (capi.cu).
+int ensure_max_dynamic_smem(const void* kernel, int bytes);
 // Zero `bytes` (a multiple of 4) as a PDL kernel (keeps the graph's kernel chain).
 int zero_async(void* p, int64_t bytes, cudaStream_t st);
 // 2-D SWIZZLE_128B TMA map (row pitch = inner * elem_bytes), defined in gemm.cu.

@@ -959,14 +959,8 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
                                                                 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
         QSB_TRY(make_map(&mc, cptr, cdt, ceb, p.N, p.M, 128 / ceb, 32));
     }
-    static bool configured = false;
-    if (!configured) {
-        QSB_TRY(cuda_status(cudaFuncSetAttribute(k_gemm_tc<kI8, BN, kCta, kLay>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 C::kSmemBytes),
-                            "cudaFuncSetAttribute"));
-        configured = true;
-    }
+    QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_gemm_tc<kI8, BN, kCta, kLay>),
+                                    C::kSmemBytes));
     const int64_t tiles = ((p.M + BM * kCta - 1) / (BM * kCta)) * ((p.N + BN - 1) / BN);
     // Split-K when the tile grid leaves SMs idle and the result is reduce-added
     // anyway (accumulating FP32 output, e.g. wgrad into the flat main_grad).

@@ -16,6 +16,8 @@
 // SR arithmetic is FP64 exactly as indicator.cpp:180-189.
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -184,8 +186,17 @@ struct Workspace {
     size_t cap_segments = 0;
 };
 
-int run_sr(int mode, SrArgs a, uint64_t seed, cudaStream_t st, Workspace& ws) {
+Workspace& workspace_for(cudaStream_t st);
+
+int run_sr(int mode, SrArgs a, uint64_t seed, cudaStream_t st) {
     if (a.n == 0) return QSYNC_OK;
+    // The jump polynomials come from the host per call: not capturable.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    QSB_TRY(cuda_status(cudaStreamIsCapturing(st, &cap), "cudaStreamIsCapturing"));
+    QSB_REQUIRE(cap == cudaStreamCaptureStatusNone, QSYNC_ERR_VALIDATION,
+                "stochastic rounding on the reference RNG stream cannot be captured in a CUDA graph "
+                "(its jump-ahead polynomials are computed on the host per call)");
+    Workspace& ws = workspace_for(st);
     const int sms = sm_count();
     // Segment length: a whole number of twist blocks; enough segments to fill
     // the chip, but not shorter than the cost of a jump (~20K words).
@@ -200,15 +211,23 @@ int run_sr(int mode, SrArgs a, uint64_t seed, cudaStream_t st, Workspace& ws) {
     const std::vector<uint64_t>& polys = mtjump::jump_polys(twists);  // nseg x kPolyWords
     const int pw = mtjump::kPolyWords;
     if (ws.cap_segments < static_cast<size_t>(nseg)) {
-        cudaFree(ws.raw);
-        cudaFree(ws.polys);
-        cudaFree(ws.states);
+        // Stream-ordered growth: the old buffers are released after the work
+        // already queued on this stream (no hidden device synchronisation).
+        if (ws.raw) QSB_TRY(cuda_status(cudaFreeAsync(ws.raw, st), "cudaFreeAsync"));
+        if (ws.polys) QSB_TRY(cuda_status(cudaFreeAsync(ws.polys, st), "cudaFreeAsync"));
+        if (ws.states) QSB_TRY(cuda_status(cudaFreeAsync(ws.states, st), "cudaFreeAsync"));
         ws.raw = ws.polys = ws.states = nullptr;
-        QSB_TRY(cuda_status(cudaMalloc(&ws.raw, sizeof(uint64_t) * mtjump::kRawWords), "malloc"));
-        QSB_TRY(cuda_status(cudaMalloc(&ws.polys, sizeof(uint64_t) * pw * nseg), "malloc"));
-        QSB_TRY(cuda_status(cudaMalloc(&ws.states, sizeof(uint64_t) * MT_N * nseg), "malloc"));
+        ws.cap_segments = 0;
+        QSB_TRY(cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&ws.raw), sizeof(uint64_t) * mtjump::kRawWords, st),
+                            "cudaMallocAsync"));
+        QSB_TRY(cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&ws.polys), sizeof(uint64_t) * pw * nseg, st),
+                            "cudaMallocAsync"));
+        QSB_TRY(cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&ws.states), sizeof(uint64_t) * MT_N * nseg, st),
+                            "cudaMallocAsync"));
         ws.cap_segments = nseg;
     }
+    // Pageable source: the copy is staged before cudaMemcpyAsync returns, so the
+    // cache-owned host buffer may change afterwards.
     QSB_TRY(cuda_status(cudaMemcpyAsync(ws.polys, polys.data(), sizeof(uint64_t) * pw * nseg,
                                         cudaMemcpyHostToDevice, st),
                         "copy jump polynomials"));
@@ -223,14 +242,21 @@ int run_sr(int mode, SrArgs a, uint64_t seed, cudaStream_t st, Workspace& ws) {
         default: k_sr<kSrDraws><<<static_cast<unsigned>(nseg), kSrThreads, 0, st>>>(a); break;
     }
     QSB_TRY(check_launch("k_sr"));
-    // The polynomial upload reads pageable host memory; keep it alive until
-    // the copy retires (jump_polys returns a cache-owned buffer).
     return QSYNC_OK;
 }
 
-// Library-owned scratch for the jump-ahead (one per host thread; the SR
-// entries are the only ones that keep per-device state).
-thread_local Workspace g_ws;
+// Library-owned jump-ahead scratch, one per (device, stream): work on one
+// stream is ordered, so its workspace is reused safely; two streams (or the
+// same stream handle on another device) never share one.  The SR entries are
+// the only ones that keep per-device state.
+Workspace& workspace_for(cudaStream_t st) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, Workspace> table;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    return table[{dev, st}];
+}
 
 }  // namespace
 }  // namespace qsb
@@ -251,7 +277,7 @@ int qsync_stochastic_round_f64(const double* x, int64_t n, double q, double zp, 
     a.zp = zp;
     a.rounded = rounded;
     a.deq = dequantized;
-    return run_sr(kSrF64, a, seed, to_stream(stream), g_ws);
+    return run_sr(kSrF64, a, seed, to_stream(stream));
 }
 
 int qsync_stochastic_round_float_f64(const double* x, int64_t n, int e, int k, uint64_t seed,
@@ -270,7 +296,7 @@ int qsync_quantize_sr(const float* x, int64_t n, const float* scale, uint64_t se
     a.n = n;
     a.scale_dev = scale;
     a.q8 = q;
-    return run_sr(kSrI8, a, seed, to_stream(stream), g_ws);
+    return run_sr(kSrI8, a, seed, to_stream(stream));
 }
 
 int qsync_mt64_draws(uint64_t seed, uint64_t offset, int64_t n, uint64_t* out,
@@ -280,7 +306,7 @@ int qsync_mt64_draws(uint64_t seed, uint64_t offset, int64_t n, uint64_t* out,
     a.n = n;
     a.draws = out;
     a.offset = offset;
-    return run_sr(kSrDraws, a, seed, to_stream(stream), g_ws);
+    return run_sr(kSrDraws, a, seed, to_stream(stream));
 }
 
 }  // extern "C"

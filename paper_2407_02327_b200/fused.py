@@ -152,6 +152,16 @@ class FusedAdamW:
         """Recompute the weight copies from the current weights (no update)."""
         if self._prep:
             self._launch(0)
+            for m in self._prep.values():
+                m._wver = m.weight._version
+
+    def refresh_if_stale(self) -> None:
+        """Re-emit the copies when a weight changed OUTSIDE this optimizer since
+        they were written (load_state_dict, a DP broadcast, manual edits bump the
+        tensor version; the update kernel writes weights and copies together and
+        leaves the version alone), so the forward never runs on stale copies."""
+        if any(getattr(m, "_wver", None) != m.weight._version for m in self._prep.values()):
+            self.prepare()
 
 
 # =============================================================================== profiling marks
@@ -188,7 +198,17 @@ def _operand(x, aux, prec):
 
 def _weights(m):
     """(wq, ws, w16) of a planned Linear: the optimizer-emitted copies when
-    present, else made now (standalone use)."""
+    present and current, else made now (standalone use, or the weight changed
+    outside the optimizer since the copies were written)."""
+    if getattr(m, "_wver", None) is not None and m._wver != m.weight._version:
+        with torch.no_grad():
+            if getattr(m, "wq", None) is not None:
+                wq, ws, _ = ops.quantize_per_channel(m.weight.detach())
+                m.wq.copy_(wq)
+                m.ws.copy_(ws)
+            if getattr(m, "w16", None) is not None:
+                m.w16.copy_(ops.cast(m.weight.detach(), torch.float16))
+        m._wver = m.weight._version
     if m.precision == INT8:
         if getattr(m, "wq", None) is not None:
             return m.wq, m.ws, m.w16

@@ -498,7 +498,7 @@ def act_cast(x: torch.Tensor, dtype: torch.dtype, act: int = ACT_NONE, out=None,
 def act_bwd_colsum(dy: torch.Tensor, h: torch.Tensor | None, act: int = ACT_NONE,
                    out_dtype: torch.dtype | None = torch.float16, colsum_into=None):
     """g = dy * act'(h) as out_dtype (None: no output), column sums ADDED into ``colsum_into``."""
-    _req(dy, "dy", (torch.float32, torch.float16))
+    _req(dy, "dy", (torch.float32, torch.float16, torch.bfloat16))
     if h is not None:
         _req(h, "h", (torch.float32, torch.float16))
     cols = dy.shape[-1]

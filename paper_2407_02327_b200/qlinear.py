@@ -28,7 +28,13 @@ INT8, FP16, FP32 = "INT8", "FP16", "FP32"
 # The reference planner's Precision enum (precision.hpp:12) does not know it,
 # so plans from the reference never select it.
 FP8 = "FP8"
+# BF16: the float rung SPEC.md:324 leaves room for (indicator k = 7 instead of
+# FP16's 9): BF16 operands, FP32 accumulation, emits BF16, BF16 backward (dgrad
+# BF16, wgrad FP32).  Like FP8, the reference enum has no BF16; plans name it
+# through this package (load_plan accepts it).
+BF16 = "BF16"
 PRECISIONS = (INT8, FP16, FP32)
+EXTENDED = (INT8, FP8, BF16, FP16, FP32)  # the B200 ladder, coarsest first
 
 # Profiling hook (profiler.StatsRecorder): when set, every QLinear records the
 # device statistics of its input activation, weight and incoming gradient
@@ -43,11 +49,11 @@ def _record(name, kind, t):
 
 def output_dtype(precision: str) -> torch.dtype:
     """graph.hpp:38-40: fixed-point kernels emit FP32, float kernels their own format."""
-    return torch.float16 if precision == FP16 else torch.float32
+    return {FP16: torch.float16, BF16: torch.bfloat16}.get(precision, torch.float32)
 
 
 def backward_precision(precision: str) -> str:
-    """cost_mapper.cpp:13-15 (FP8 backs off to FP16 like INT8)."""
+    """cost_mapper.cpp:13-15 (FP8 backs off to FP16 like INT8; BF16 stays BF16)."""
     return FP16 if precision in (INT8, FP8) else precision
 
 
@@ -64,7 +70,7 @@ def _main_grad(p):
     return getattr(p, "main_grad", None) if p is not None else None
 
 
-def _fp16_backward(ctx, dy, x16, w16, alpha_dev):
+def _fp16_backward(ctx, dy, x16, w16, alpha_dev, dt=torch.float16):
     """Shared FP16 backward (cost_mapper.cpp:13-15) on row-major operands.
 
     dgrad = dY16 W16 reads W16 [N_out, K_in] as an MN-major B operand and wgrad =
@@ -76,7 +82,13 @@ def _fp16_backward(ctx, dy, x16, w16, alpha_dev):
     w, b = ctx.w_ref, ctx.b_ref
     dy = dy.contiguous()
     mw, mb = _main_grad(w), _main_grad(b)
-    dy16, _, db = ops.cast_transpose(dy, True, False, b is not None and mb is None, colsum_into=mb)
+    if dt == torch.float16:
+        dy16, _, db = ops.cast_transpose(dy, True, False, b is not None and mb is None, colsum_into=mb)
+    else:  # BF16 backward entry: one kernel for the cast and the bias-gradient column sums
+        db = None
+        if b is not None and mb is None:
+            db = torch.zeros(dy.shape[-1], device=dy.device, dtype=torch.float32)
+        dy16 = ops.act_bwd_colsum(dy, None, ops.ACT_NONE, dt, colsum_into=mb if mb is not None else db)
     dx = ops.gemm_f16(dy16, w16, out_dtype=ctx.x_dtype, b_mn=True)  # dgrad [M, K_in]
     if mw is not None and WGRAD_STREAM is not None:
         cur = torch.cuda.current_stream()
@@ -174,6 +186,31 @@ class _QLinearFp16(torch.autograd.Function):
         return _fp16_backward(ctx, dy, x16, w16, None) + (None,)
 
 
+class _QLinearBf16(torch.autograd.Function):
+    """BF16 rung: BF16 operands on tcgen05 kind::f16 (BF16 format), FP32
+    accumulation, emits BF16; BF16 backward (dgrad BF16 -> the input's format,
+    wgrad FP32)."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, name=None):
+        _record(name, "act", x)
+        _record(name, "w", w)
+        ctx.name = name
+        xb = x if x.dtype == torch.bfloat16 else ops.cast(x, torch.bfloat16)
+        wb = ops.cast(w, torch.bfloat16)
+        y = ops.gemm_f16(xb, wb, out_dtype=torch.bfloat16, bias=b)
+        ctx.save_for_backward(xb, wb)
+        ctx.x_dtype = x.dtype
+        ctx.w_ref, ctx.b_ref = w, b
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        xb, wb = ctx.saved_tensors
+        _record(ctx.name, "grad", dy)
+        return _fp16_backward(ctx, dy, xb, wb, None, dt=torch.bfloat16) + (None,)
+
+
 class _Cast(torch.autograd.Function):
     """Autograd-aware device cast (K4) for the glue between planned operators."""
 
@@ -204,6 +241,8 @@ def qlinear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, precision:
         y = _QLinearFp16.apply(x2, w, b, name)
     elif precision == FP8:
         y = _QLinearFp8.apply(x2, w, b, name)
+    elif precision == BF16:
+        y = _QLinearBf16.apply(x2, w, b, name)
     elif precision == FP32:
         _record(name, "act", x2)
         _record(name, "w", w)

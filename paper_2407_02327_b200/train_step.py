@@ -26,7 +26,7 @@ import torch.nn.functional as F
 
 from . import qlinear as _ql
 from .glue import AddLayerNorm, attention
-from .qlinear import FP16, FP32, INT8, QLinear, cast
+from .qlinear import EXTENDED, FP16, FP32, INT8, QLinear, cast
 
 
 @dataclass
@@ -79,7 +79,7 @@ def load_plan(path: str, device_id: str) -> dict[str, str]:
         raise KeyError(f"reference: plan has no device \"{device_id}\"")
     plan = dict(table[device_id])
     for op, p in plan.items():
-        if p not in (INT8, FP16, FP32):
+        if p not in EXTENDED:  # the reference's INT8/FP16/FP32 plus this ladder's FP8 / BF16
             raise ValueError(f"validation: unknown precision \"{p}\"")
     return plan
 
@@ -105,10 +105,22 @@ class EncoderLayer(torch.nn.Module):
         # packed dQKV out -- no permute/stack copies around it.
         a = attention(qkv.view(B, S, 3, nh, H // nh))  # [B, S, nh, d]
         a = a.reshape(B, S, H)
-        x = self.ln1(x, self.o(a))        # fused residual add (FP32 or FP16 operand)
+        x = self.ln1(x, _ln_operand(self.o(a)))        # fused residual add (FP32 or FP16 operand)
         f = F.gelu(self.ff1(x))
-        x = self.ln2(x, self.ff2(f))
+        x = self.ln2(x, _ln_operand(self.ff2(f)))
         return x
+
+
+def _ln_operand(y):
+    """The residual LayerNorm reads an FP32 or FP16 operand; a BF16 op's output
+    is widened to FP32 (exact) on the way in."""
+    return cast(y, torch.float32) if y.dtype == torch.bfloat16 else y
+
+
+def _fusable(layer: EncoderLayer) -> bool:
+    """The layer-fused path (fused.py) covers the reference ladder INT8 / FP16 /
+    FP32; a layer with a BF16 or FP8 op runs the per-operator QLinear path."""
+    return all(m.precision in (INT8, FP16, FP32) for m in (layer.qkv, layer.o, layer.ff1, layer.ff2))
 
 
 class BertEncoderStack(torch.nn.Module):
@@ -143,12 +155,16 @@ class BertEncoderStack(torch.nn.Module):
         if self.fused:
             from .fused import fused_layer
             from .glue import embed_layernorm
-            p0 = self.layers[0].qkv.precision if len(self.layers) else None
+            fusable = [_fusable(layer) for layer in self.layers]
+            p0 = self.layers[0].qkv.precision if len(self.layers) and fusable[0] else None
             x, aux = embed_layernorm(tokens, self.word, self.pos, self.typ, self.ln,
                                      want_f16=p0 == FP16, want_absmax=p0 == INT8)
             n = len(self.layers)
             for i, layer in enumerate(self.layers):
-                nxt = self.layers[i + 1].qkv.precision if i + 1 < n else None
+                if not fusable[i]:  # a BF16 / FP8 op: the per-operator layer
+                    x, aux = layer(x), None
+                    continue
+                nxt = self.layers[i + 1].qkv.precision if i + 1 < n and fusable[i + 1] else None
                 x, aux = fused_layer(layer, x, aux, nxt)
         else:
             pos = torch.arange(S, device=tokens.device)

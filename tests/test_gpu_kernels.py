@@ -347,3 +347,30 @@ def test_gemm_f16_mn_major_operands(mnk, lay, cta):
     assert err <= 1e-3 * ref.abs().max().item()
     err2 = (torch.from_numpy(_np(base)).double() - (1.0 + 0.5 * ref)).abs().max().item()
     assert err2 <= 1e-3 * (1.0 + 0.5 * ref).abs().max().item()
+
+
+def test_sr_rejects_graph_capture_and_streams_are_independent():
+    """the SR jump-ahead workspace is per (device, stream) and SR is
+    refused inside a CUDA-graph capture (its polynomials come from the host)."""
+    import torch
+
+    from paper_2407_02327_b200 import ops
+    from paper_2407_02327_b200._lib import QsyncError
+    x = torch.rand(1 << 20, device="cuda", dtype=torch.float32)
+    sc = torch.tensor([0.01], device="cuda")
+    ref = ops.quantize_sr(x, sc, 7)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for s in (s1, s2, s1, s2):  # interleaved on two streams, larger then smaller
+        with torch.cuda.stream(s):
+            outs.append(ops.quantize_sr(x, sc, 7))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with pytest.raises(QsyncError) as e:
+            with torch.cuda.graph(g, stream=s):
+                ops.quantize_sr(x, sc, 7)
+    assert e.value.kind == "validation"
