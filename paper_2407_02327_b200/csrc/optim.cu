@@ -53,7 +53,10 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, con
     return p - c.step_size * (m / denom);
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_adamw(const qsync_adamw_seg* __restrict__ segs, int nseg,
+#ifndef QSB_ADAM_MINB
+#define QSB_ADAM_MINB 4  // 64 registers: 4 x 256 threads resident per SM (2 at 88 regs held HBM at 0.69)
+#endif
+__global__ void __launch_bounds__(kWarps * 32, QSB_ADAM_MINB) k_adamw(const qsync_adamw_seg* __restrict__ segs, int nseg,
                                                        const int64_t* seg_start, int64_t row_begin,
                                                        int64_t total_rows, const int64_t* __restrict__ step,
                                                        float lr, float b1, float b2, float eps, float wd,
