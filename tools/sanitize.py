@@ -1,0 +1,104 @@
+"""One small launch of every kernel family with tricky synchronisation, for
+compute-sanitizer (memcheck / racecheck / synccheck):
+
+    compute-sanitizer --tool memcheck python tools/sanitize.py [group ...]
+
+groups: gemm1 (1-CTA tcgen05 GEMM, INT8 + FP16, TMA store and reduce-add),
+gemm2 (CTA-pair cta_group::2), conv_tma / conv_gather (implicit conv, both
+operand loaders, fwd / dgrad / wgrad), attn1 / attn2 (tcgen05 attention, 1 and
+2 CTAs/SM backward), sr (mt19937_64 jump-ahead + SR), pdl (PDL zeroing kernel +
+atomic-max producer + quantizer chain), quant (streaming quantizers).
+Shapes are small: the sanitizers replay every access.
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2407_02327_b200 import _lib, ops  # noqa: E402
+
+
+def gemm(cta):
+    ops.force_cta(cta)
+    try:
+        M, N, K = 512, 512, 256
+        a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
+        b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
+        sa = torch.tensor([0.01], device="cuda")
+        sb = torch.rand(N, device="cuda") * 0.01
+        ops.gemm_s8(a, b, sa, sb, torch.randn(N, device="cuda"))
+        ah, bh = torch.randn(M, K, device="cuda").half(), torch.randn(N, K, device="cuda").half()
+        ops.gemm_f16(ah, bh, out_dtype=torch.float16)
+        if cta == 1:
+            acc = torch.zeros(M, N, device="cuda")
+            ops.gemm_f16(ah.t().contiguous(), bh.t().contiguous(), out=acc, accumulate=True, a_mn=True, b_mn=True)
+    finally:
+        ops.force_cta(0)
+
+
+def conv(tma):
+    ops.conv_set_impl(tma)
+    try:
+        N, H, C, Co = 2, 8, 128, 128
+        x = torch.randn(N, H, H, C, device="cuda").half()
+        w = (torch.randn(Co, 3, 3, C, device="cuda") * 0.03).half()
+        ops.conv_fwd_implicit(x, w.view(Co, -1), 3, 3, (1, 1), (1, 1), out_dtype=torch.float16)
+        dy = torch.randn(N, H, H, Co, device="cuda").half()
+        ops.conv_dgrad_implicit(dy, w, (N, H, H, C), (1, 1), (1, 1))
+        ops.conv_wgrad_implicit(x, dy.view(-1, Co), 3, 3, (1, 1), (1, 1))
+        xq = torch.randint(-127, 128, (N, H, H, C), dtype=torch.int8, device="cuda")
+        wq = torch.randint(-127, 128, (Co, 9 * C), dtype=torch.int8, device="cuda")
+        ops.conv_fwd_implicit(xq, wq, 3, 3, (1, 1), (1, 1), torch.tensor([0.01], device="cuda"),
+                              torch.rand(Co, device="cuda") * 0.01)
+    finally:
+        ops.conv_set_impl(1)
+
+
+def attn(impl):
+    _lib.call("qsync_attention_set_impl", impl)
+    try:
+        qkv = torch.randn(2, 128, 3, 2, 64, device="cuda").half()
+        out, lse, _ = ops.attention_fwd(qkv, want_absmax=True)
+        ops.attention_bwd(qkv, out, torch.randn_like(out), lse)
+    finally:
+        _lib.call("qsync_attention_set_impl", 2)
+
+
+def sr():
+    x = torch.rand(1 << 16, device="cuda")
+    ops.quantize_sr(x, torch.tensor([0.01], device="cuda"), 7)
+    ops.stochastic_round(x.double(), 0.01, 0.0, 3)
+
+
+def pdl():
+    x = torch.randn(4096, 768, device="cuda")
+    am = ops.absmax_act(x)
+    ops.quantize_act(x, am)
+    ops.quantize_per_tensor(x)
+
+
+def quant():
+    x = torch.randn(1 << 16, device="cuda")
+    ops.quantize_per_channel(x.view(64, -1))
+    ops.cast(x, torch.float16)
+    ops.tensor_stats(x)
+    q, s, _ = ops.quantize_per_tensor(x.view(1, -1))
+    ops.dequantize_per_tensor(q.view(-1), s[:1])
+
+
+GROUPS = {"gemm1": lambda: gemm(1), "gemm2": lambda: gemm(2), "conv_tma": lambda: conv(1),
+          "conv_gather": lambda: conv(0), "attn1": lambda: attn(1), "attn2": lambda: attn(2), "sr": sr,
+          "pdl": pdl, "quant": quant}
+
+
+def main():
+    names = sys.argv[1:] or list(GROUPS)
+    for n in names:
+        GROUPS[n]()
+        torch.cuda.synchronize()
+        print(f"ran {n}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
