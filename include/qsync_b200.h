@@ -201,6 +201,29 @@ int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_
                    int accumulate, int layout, qsync_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * FP32 operator kernel on the tensor cores (the training devices' plan: they
+ * stay FP32, replayer.cpp:96-101).  3xTF32: each FP32 operand is split into
+ * hi = rna_tf32(x) and lo = rna_tf32(x - hi) (|x - hi - lo| <= 2^-22 |x|), and
+ * one tcgen05 kind::tf32 GEMM over K' = 3K computes hi*hi + hi*lo + lo*hi with
+ * FP32 accumulation -- FP32-level accuracy (the dropped lo*lo term is 2^-22).
+ * Same operand convention, layouts (0 / 2 / 3), alpha / bias / accumulate as
+ * qsync_gemm_f16; FP32 output.  workspace: caller-owned device buffer of
+ * qsync_gemm_f32_workspace_bytes(m, n, k) bytes (the split operands).
+ * ------------------------------------------------------------------------- */
+size_t qsync_gemm_f32_workspace_bytes(int64_t m, int64_t n, int64_t k);
+int qsync_gemm_f32(const float* a, const float* b, int64_t m, int64_t n, int64_t k, float* c, float alpha,
+                   const float* alpha_dev, const float* bias, int accumulate, int layout, void* workspace,
+                   qsync_stream_t stream);
+/* The pieces: the split of x [rows, k] (transpose = 1: x stored [k, rows]) into
+ * out [rows, 3 kp] = (hi, hi, lo) (order 0, the A operand) or (hi, lo, hi)
+ * (order 1, B), each part zero-padded to kp = k rounded up to 4; and the
+ * K-major TF32 GEMM (operands read as TF32, K % 4 == 0). */
+int qsync_split_tf32x3(const float* x, int64_t rows, int64_t k, int transpose, int order, float* out,
+                       qsync_stream_t stream);
+int qsync_gemm_tf32(const float* a, const float* b, int64_t m, int64_t n, int64_t k, float* c, float alpha,
+                    const float* alpha_dev, const float* bias, int accumulate, qsync_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * K8  Conv2d as GEMM, NHWC.  The column matrix
  * A[(n,p,q), (r,s,c)] = x[n, p*sh-ph+r*dh, q*sw-pw+s*dw, c] (0 outside) is the
  * K-major operand of qsync_gemm_s8 / qsync_gemm_f16 (weights [Cout, R*S*C],

@@ -92,6 +92,10 @@ SIGNATURES = {
     "qsync_gemm_f8": [_p, _p, _i64, _i64, _i64, _p, _int, _p, _p, _int, _p, _p],
     "qsync_quantize_fp8": [_p, _int, _i64, _p, _p, _p, _p],
     "qsync_quantize_fp8_rows": [_p, _i64, _i64, _p, _p, _p],
+    "qsync_gemm_f32_workspace_bytes": [_i64, _i64, _i64],
+    "qsync_gemm_f32": [_p, _p, _i64, _i64, _i64, _p, _f32, _p, _p, _int, _int, _p, _p],
+    "qsync_split_tf32x3": [_p, _i64, _i64, _int, _int, _p, _p],
+    "qsync_gemm_tf32": [_p, _p, _i64, _i64, _i64, _p, _f32, _p, _p, _int, _p],
     "qsync_comm_unique_id": [_p],
     "qsync_comm_init": [_p, _int, _int, _p],
     "qsync_comm_destroy": [_p],
@@ -111,7 +115,7 @@ SIGNATURES = {
     "qsync_mt_jump_selftest": [],
 }
 _RESTYPES = {"qsync_last_error": C.c_char_p, "qsync_status_name": C.c_char_p,
-             "qsync_stats_workspace_bytes": C.c_size_t, "qsync_launch_count": C.c_ulonglong}
+             "qsync_stats_workspace_bytes": C.c_size_t, "qsync_gemm_f32_workspace_bytes": C.c_size_t, "qsync_launch_count": C.c_ulonglong}
 
 _lib = None
 

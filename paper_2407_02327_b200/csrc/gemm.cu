@@ -146,6 +146,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // template bit, not a runtime flag: a per-MMA / per-element branch on it cost
     // the INT8 GEMM 20% (8192^3: 3.07 -> 2.43 POPS).
     constexpr bool kF8 = (kLay & 128) != 0;
+    // kLay bit 8: TF32 operands (4-byte elements, kind::tf32, FP32 accumulators),
+    // K-major only -- the FP32 plan's 3xTF32 GEMM (qsync_gemm_f32).
+    constexpr bool kTF32 = (kLay & 256) != 0;
+    static_assert(!kTF32 || (!kI8 && (kLay & 255) == 0), "TF32 is a K-major FP-kind layout");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B swizzle atoms: the declaration asks for
     // it and the smem budget (Cfg::kSmemBytes) assumes it -- trap, not corrupt.
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Work units = (tile, K split); split-K partials are reduce-added by TMA.
     const int ksplit = p.ksplit > 1 ? p.ksplit : 1;
     const int num_units = num_tiles * ksplit;
-    const int bk_elems = kI8 ? BK_BYTES : BK_BYTES / 2;
+    const int bk_elems = kI8 ? BK_BYTES : (kTF32 ? BK_BYTES / 4 : BK_BYTES / 2);
     const int num_kb = static_cast<int>((K + bk_elems - 1) / bk_elems);
 
     if (warp == 0 && lane == 0) {
@@ -516,6 +520,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::mma_f8(d_tmem, da, db, p.idesc, accum);
                             else if (kI8)
                                 ptx::mma_i8(d_tmem, da, db, p.idesc, accum);
+                            else if (kTF32)
+                                ptx::mma_tf32(d_tmem, da, db, p.idesc, accum);
                             else
                                 ptx::mma_f16(d_tmem, da, db, p.idesc, accum);
                         }
@@ -896,13 +902,14 @@ int make_im2col_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, u
 
 // Instruction descriptor (tcgen05 "idesc"): c_format [4,6), a_format [7,10),
 // b_format [10,13), a/b major [15],[16] (0 = K-major), N>>3 [17,23), M>>4 [24,29).
-uint32_t make_idesc(bool i8, bool bf16, int n, int m, int lay = 0, bool fp8 = false) {
+uint32_t make_idesc(bool i8, bool bf16, int n, int m, int lay = 0, bool fp8 = false, bool tf32 = false) {
     uint32_t d = 0;
     d |= static_cast<uint32_t>(lay & 1) << 15;         // A MN-major
     d |= static_cast<uint32_t>((lay >> 1) & 1) << 16;  // B MN-major
     d |= (i8 && !fp8 ? 2u : 1u) << 4;                 // S32 / F32 accumulator
-    // kind::i8: signed = 1; kind::f16: F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0
-    const uint32_t fmt = fp8 ? 0u : (i8 ? 1u : (bf16 ? 1u : 0u));
+    // kind::i8: signed = 1; kind::f16: F16 = 0, BF16 = 1; kind::tf32: TF32 = 2;
+    // kind::f8f6f4: E4M3 = 0
+    const uint32_t fmt = fp8 ? 0u : (i8 ? 1u : (tf32 ? 2u : (bf16 ? 1u : 0u)));
     d |= fmt << 7;
     d |= fmt << 10;
     d |= static_cast<uint32_t>(n >> 3) << 17;
@@ -921,7 +928,7 @@ int g_conv_tma = 1;      // implicit conv operand loads: 1 = TMA im2col, 0 = cp.
 template <bool kI8, int BN, int kCta, int kLay>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
     using C = Cfg<BN, kCta>;
-    const uint32_t eb = kI8 ? 1 : 2;
+    const uint32_t eb = kI8 ? 1 : ((kLay & 256) ? 4 : 2);
     const uint32_t box_k = BK_BYTES / eb;
     CUtensorMap ma, mb, mc;
     if (kLay & 4)  // implicit conv: A is gathered by the producer lanes
@@ -1178,6 +1185,82 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
         }
     }
 }
+
+// TF32 (K-major) GEMM: single-CTA tiles by the same cost models (a 128-byte
+// K-slice is 32 TF32 elements, the MMA time per slice equals the FP16 one).
+int dispatch_tf32(const void* a, const void* b, EpiParams p, cudaStream_t st, int force_bn) {
+    const bool accumulating = p.accumulate && p.c_dtype == QSYNC_F32;
+    Shape sh = pick_shape(p.M, p.N, false);
+    if (accumulating && !force_bn && g_force_splitk == 0) {
+        const AccChoice c = choose_acc(p.M, p.N, (p.K + 31) / 32);
+        sh.bn = c.bn;
+        p.ksplit = c.ksplit;
+    } else if (accumulating) {
+        sh.bn = 256;
+    }
+    if (force_bn) sh.bn = force_bn;
+    p.idesc = make_idesc(false, false, sh.bn, BM, 0, false, true);
+    p.debug_epi = g_debug_epi;
+    const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    switch (sh.bn) {
+        case 256: return launch<false, 256, 1, 256>(a, b, dt, p, st);
+        case 192: return launch<false, 192, 1, 256>(a, b, dt, p, st);
+        case 128: return launch<false, 128, 1, 256>(a, b, dt, p, st);
+        default: return launch<false, 64, 1, 256>(a, b, dt, p, st);
+    }
+}
+
+// 3xTF32 operand split: x = hi + lo + r with hi = rna_tf32(x), lo =
+// rna_tf32(x - hi) (|r| <= 2^-22 |x|).  out [R, 3K] holds the parts along K in
+// the order (hi, hi, lo) for A or (hi, lo, hi) for B, so ONE TF32 GEMM over
+// K' = 3Kp computes hi_a hi_b + hi_a lo_b + lo_a hi_b -- FP32-level accuracy on
+// the tensor cores (each part zero-padded from K to Kp = K rounded up to 4).
+// transpose = 1 reads x as [K, R] (an MN-major source) and writes the K-major
+// parts through a 32 x 33 smem tile.
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__global__ void __launch_bounds__(256) k_split_tf32(const float* __restrict__ x, int64_t R, int64_t K, int64_t Kp,
+                                                    int transpose, int order, float* __restrict__ out) {
+    QSB_PDL_ENTER();
+    __shared__ float tile[32][33];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, k0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
+    float v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr = ty + 8 * i;
+        if (transpose) {  // x [K, R]: coalesced along R, stored transposed
+            const int64_t kk = k0 + rr, r = r0 + tx;
+            tile[rr][tx] = (kk < K && r < R) ? x[kk * R + r] : 0.0f;
+        } else {
+            const int64_t r = r0 + rr, kk = k0 + tx;
+            v[i] = (r < R && kk < K) ? x[r * K + kk] : 0.0f;
+        }
+    }
+    if (transpose) {
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = tile[tx][ty + 8 * i];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t r = r0 + ty + 8 * i, kk = k0 + tx;
+        if (r >= R || kk >= Kp) continue;  // columns K..Kp-1: zero padding of each part
+        const float hi = tf32_rna(v[i]);
+        const float lo = tf32_rna(v[i] - hi);
+        float* o = out + r * 3 * Kp + kk;
+        o[0] = hi;
+        o[Kp] = order ? lo : hi;
+        o[2 * Kp] = order ? hi : lo;
+    }
+}
+
+// Each split part is K padded to a multiple of 4 elements (16-byte TMA rows).
+inline int64_t tf32_part(int64_t k) { return (k + 3) / 4 * 4; }
 
 int g_force_bn = 0;  // test hook (qsync_gemm_force_tile_n)
 
@@ -1457,6 +1540,57 @@ int qsync_conv_wgrad_implicit(const void* x, int dtype, int64_t N, int64_t H, in
     const CUtensorMapDataType dt =
         dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     return dispatch<false>(dy, x, dt, p, to_stream(stream), 256, g_conv_tma ? 67 : 11);
+}
+
+int qsync_split_tf32x3(const float* x, int64_t rows, int64_t k, int transpose, int order, float* out,
+                       qsync_stream_t stream) {
+    QSB_REQUIRE(x && out, QSYNC_ERR_VALIDATION, "split needs x and out");
+    QSB_REQUIRE(rows >= 0 && k >= 0, QSYNC_ERR_DOMAIN, "negative extent");
+    QSB_REQUIRE(rows < (int64_t(1) << 31) && k < (int64_t(1) << 31), QSYNC_ERR_DOMAIN, "split extent too large");
+    if (rows == 0 || k == 0) return QSYNC_OK;
+    const int64_t kp = tf32_part(k);
+    dim3 grid(static_cast<unsigned>((kp + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+    QSB_REQUIRE(grid.y < 65536, QSYNC_ERR_DOMAIN, "too many rows for the split grid");
+    pdl_launch(k_split_tf32, grid, dim3(256), 0, to_stream(stream), x, rows, k, kp, transpose, order, out);
+    return check_launch("k_split_tf32");
+}
+
+int qsync_gemm_tf32(const float* a, const float* b, int64_t m, int64_t n, int64_t k, float* c, float alpha,
+                    const float* alpha_dev, const float* bias, int accumulate, qsync_stream_t stream) {
+    QSB_TRY(validate(a, b, m, n, k, 4));
+    QSB_REQUIRE(c != nullptr, QSYNC_ERR_VALIDATION, "GEMM needs an output");
+    EpiParams p{};
+    p.M = m;
+    p.N = n;
+    p.K = k;
+    p.c = c;
+    p.c_dtype = QSYNC_F32;
+    p.alpha = alpha;
+    p.alpha_dev = alpha_dev;
+    p.bias = bias;
+    p.accumulate = accumulate;
+    return dispatch_tf32(a, b, p, to_stream(stream), g_force_bn);
+}
+
+size_t qsync_gemm_f32_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+    const int64_t kp = tf32_part(k);
+    return static_cast<size_t>(3) * 4 * static_cast<size_t>(m * kp + n * kp) + 256;
+}
+
+int qsync_gemm_f32(const float* a, const float* b, int64_t m, int64_t n, int64_t k, float* c, float alpha,
+                   const float* alpha_dev, const float* bias, int accumulate, int layout, void* workspace,
+                   qsync_stream_t stream) {
+    QSB_REQUIRE(layout == 0 || layout == 2 || layout == 3, QSYNC_ERR_DOMAIN,
+                "operand layout must be 0 (K-major A/B), 2 (MN-major B) or 3 (MN-major A and B)");
+    QSB_REQUIRE(a && b && c && workspace, QSYNC_ERR_VALIDATION, "FP32 GEMM needs a, b, c and the workspace");
+    QSB_REQUIRE(m > 0 && n > 0 && k > 0, QSYNC_ERR_DOMAIN, "GEMM extents must be positive");
+    const int64_t kp = tf32_part(k);
+    float* a3 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(workspace) + 127) & ~uintptr_t(127));
+    float* b3 = a3 + ((3 * m * kp + 31) / 32) * 32;
+    cudaStream_t st = to_stream(stream);
+    QSB_TRY(qsync_split_tf32x3(a, m, k, (layout & 1) ? 1 : 0, 0, a3, st));
+    QSB_TRY(qsync_split_tf32x3(b, n, k, (layout & 2) ? 1 : 0, 1, b3, st));
+    return qsync_gemm_tf32(a3, b3, m, n, 3 * kp, c, alpha, alpha_dev, bias, accumulate, st);
 }
 
 int qsync_gemm_f16(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,

@@ -40,7 +40,6 @@ import ctypes as C
 
 import numpy as np
 import torch
-import torch.nn.functional as F
 
 from . import ops
 from . import qlinear as _ql
@@ -230,8 +229,8 @@ def _linear_fwd(m, opnd, out_dtype=None):
         y = ops.gemm_s8_ex(x, wq, s, ws, bias, out_dtype=out_dtype or torch.float32)
     elif kind == "f16":
         y = ops.gemm_f16(x, w16, out_dtype=torch.float16, bias=bias)
-    else:
-        y = F.linear(x, w.detach(), bias)
+    else:  # FP32 plan: tensor cores through the 3xTF32 split (FP32-level accuracy)
+        y = ops.gemm_f32(x, w.detach(), bias=bias)
     return y, w16
 
 
@@ -248,9 +247,6 @@ def _wgrad(m, dy16_or_32, opnd, side):
     """wgrad of one planned op into weight.main_grad (FP32, accumulate)."""
     kind, x, s = opnd[:3]
     mw = m.weight.main_grad
-    if kind == "f32":
-        mw.addmm_(dy16_or_32.float().t(), x)  # training-device FP32 path (cuBLAS), main stream
-        return
     if kind == "i8":  # FP16 copy of the INT8 grid values (exact), from the quantizer when it wrote one
         x16 = opnd[3] if len(opnd) > 3 else ops.cast(x, torch.float16)
     else:
@@ -260,7 +256,11 @@ def _wgrad(m, dy16_or_32, opnd, side):
         if side is not None and WGRAD_CTAS:
             _call_cap(WGRAD_CTAS)
         try:
-            ops.gemm_f16(dy16_or_32, x16, alpha_dev=s, out=mw, accumulate=True, a_mn=True, b_mn=True)
+            if kind == "f32":  # training-device FP32 wgrad: 3xTF32 on the tensor cores
+                ops.gemm_f32(dy16_or_32.float().contiguous(), x16, out=mw, accumulate=True, a_mn=True,
+                             b_mn=True)
+            else:
+                ops.gemm_f16(dy16_or_32, x16, alpha_dev=s, out=mw, accumulate=True, a_mn=True, b_mn=True)
         finally:
             if side is not None and WGRAD_CTAS:
                 _call_cap(0)
@@ -280,12 +280,12 @@ def _wgrad(m, dy16_or_32, opnd, side):
 def _dgrad(m, dy, w16, out_dtype, acc_into=None):
     """dgrad of one planned op: FP16 GEMM (INT8/FP16 ops) or FP32 (FP32 op);
     with ``acc_into`` the result is ADDED into that FP32 buffer."""
-    if m.precision == FP32:
-        d = dy.float() @ m.weight.detach()
+    if m.precision == FP32:  # 3xTF32 on the tensor cores (FP32-level accuracy)
+        dyf = dy.float().contiguous()
         if acc_into is not None:
-            acc_into.add_(d)
-            return acc_into
-        return d.to(out_dtype)
+            return ops.gemm_f32(dyf, m.weight.detach(), out=acc_into, accumulate=True, b_mn=True)
+        d = ops.gemm_f32(dyf, m.weight.detach(), b_mn=True)
+        return d if out_dtype == torch.float32 else d.to(out_dtype)
     if acc_into is not None:
         return ops.gemm_f16(dy, w16, out=acc_into, accumulate=True, b_mn=True)
     return ops.gemm_f16(dy, w16, out_dtype=out_dtype, b_mn=True)

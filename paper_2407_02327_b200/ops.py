@@ -267,6 +267,37 @@ def gemm_f16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32, alpha: f
     return c
 
 
+_f32_ws: dict = {}
+_f32_ws_retired: list = []
+
+
+def gemm_f32(a: torch.Tensor, b: torch.Tensor, alpha: float = 1.0, alpha_dev=None, bias=None, out=None,
+             accumulate: bool = False, a_mn: bool = False, b_mn: bool = False) -> torch.Tensor:
+    """C = alpha * A B^T in FP32 on the tensor cores (3xTF32 split, FP32-level
+    accuracy; qsync_gemm_f32).  Layouts as gemm_f16; FP32 output."""
+    _req(a, "a", (torch.float32,))
+    _req(b, "b", (torch.float32,))
+    if a_mn and not b_mn:
+        raise QsyncError(4, "domain: MN-major A requires MN-major B")
+    K, M = a.shape if a_mn else (a.shape[1], a.shape[0])
+    N = b.shape[1] if b_mn else b.shape[0]
+    c = out if out is not None else torch.empty((M, N), device=a.device, dtype=torch.float32)
+    nbytes = int(_lib.lib().qsync_gemm_f32_workspace_bytes(M, N, K))
+    key = (a.device, torch.cuda.current_stream().cuda_stream)
+    ws = _f32_ws.get(key)
+    if ws is None or ws.numel() < nbytes:
+        if ws is not None:  # kernels already enqueued (or captured) may still read it
+            _f32_ws_retired.append(ws)
+        ws = torch.empty(nbytes, device=a.device, dtype=torch.uint8)
+        _f32_ws[key] = ws
+    ev = _timed("gemm_f32", 2.0 * M * N * K)
+    call("qsync_gemm_f32", _ptr(a), _ptr(b), M, N, K, _ptr(c), float(alpha), _ptr(alpha_dev), _ptr(bias),
+         int(accumulate), (1 if a_mn else 0) | (2 if b_mn else 0), _ptr(ws), _stream())
+    if ev is not None:
+        ev.record()
+    return c
+
+
 # --------------------------------------------------------------------------- K8 conv
 def conv_out_size(H, W, R, S, stride, pad, dil=(1, 1)):
     import ctypes as C

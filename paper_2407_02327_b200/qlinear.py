@@ -6,7 +6,8 @@ Forward (Y = X W^T + b), per the plan's ``Precision`` (precision.hpp:12):
              and the dequant + bias epilogue fused; emits FP32
              (graph.hpp:38-40 ``output_precision``).
   * FP16  -- FP16 operands, FP32 accumulation, emits FP16.
-  * FP32  -- plain FP32 GEMM (cuBLAS library GEMM: training devices stay FP32,
+  * FP32  -- FP32 GEMMs on the tensor cores through the 3xTF32 split
+             (qsync_gemm_f32, FP32-level accuracy; training devices stay FP32,
              replayer.cpp:96-101).
 Backward of INT8 and FP16 ops runs in FP16 (cost_mapper.cpp:13-15
 ``backward_precision``): the incoming gradient is cast once to FP16 (plus its
@@ -17,7 +18,6 @@ epilogue) emitted in FP32 (cost_mapper.cpp:48-50).
 from __future__ import annotations
 
 import torch
-import torch.nn.functional as F
 
 from . import ops
 
@@ -211,6 +211,48 @@ class _QLinearBf16(torch.autograd.Function):
         return _fp16_backward(ctx, dy, xb, wb, None, dt=torch.bfloat16) + (None,)
 
 
+class _QLinearFp32(torch.autograd.Function):
+    """FP32 (the training devices' plan, replayer.cpp:96-101): FP32 in, FP32 out,
+    FP32 backward -- every GEMM on the tensor cores through the 3xTF32 split
+    (qsync_gemm_f32, FP32-level accuracy); the bias gradient is one column-sum
+    kernel."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, name=None):
+        _record(name, "act", x)
+        _record(name, "w", w)
+        ctx.name = name
+        xf = x if x.dtype == torch.float32 else ops.cast(x, torch.float32)
+        y = ops.gemm_f32(xf, w.detach(), bias=b.detach() if b is not None else None)
+        ctx.save_for_backward(xf)
+        ctx.x_dtype = x.dtype
+        ctx.w_ref, ctx.b_ref = w, b
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (xf,) = ctx.saved_tensors
+        _record(ctx.name, "grad", dy)
+        w, b = ctx.w_ref, ctx.b_ref
+        dy = dy.contiguous().float()
+        mw, mb = _main_grad(w), _main_grad(b)
+        dx = ops.gemm_f32(dy, w.detach(), b_mn=True)  # dgrad [M, K_in]
+        if dx.dtype != ctx.x_dtype:
+            dx = ops.cast(dx, ctx.x_dtype)
+        dw = db = None
+        if mw is not None:
+            ops.gemm_f32(dy, xf, out=mw, accumulate=True, a_mn=True, b_mn=True)
+        else:
+            dw = ops.gemm_f32(dy, xf, a_mn=True, b_mn=True)
+        if b is not None:
+            if mb is not None:
+                ops.act_bwd_colsum(dy, None, ops.ACT_NONE, None, colsum_into=mb)
+            else:
+                db = torch.zeros(dy.shape[-1], device=dy.device, dtype=torch.float32)
+                ops.act_bwd_colsum(dy, None, ops.ACT_NONE, None, colsum_into=db)
+        return dx, dw, db, None
+
+
 class _Cast(torch.autograd.Function):
     """Autograd-aware device cast (K4) for the glue between planned operators."""
 
@@ -244,11 +286,7 @@ def qlinear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, precision:
     elif precision == BF16:
         y = _QLinearBf16.apply(x2, w, b, name)
     elif precision == FP32:
-        _record(name, "act", x2)
-        _record(name, "w", w)
-        y = F.linear(x2.float(), w, b)
-        if STATS_RECORDER is not None and name is not None and y.requires_grad:
-            y.register_hook(lambda g, n=name: _record(n, "grad", g))
+        y = _QLinearFp32.apply(x2, w, b, name)
     else:
         raise ValueError(f"validation: unknown precision \"{precision}\"")
     return y.reshape(*shape[:-1], w.shape[0])
