@@ -104,8 +104,12 @@ def test_train_step_through_comm_matches(comm):
     _, m0b, l0b = _tiny_step(None)
     st1, m1, l1 = _tiny_step(comm)
     run_to_run = max(float((a - b).abs().max()) for a, b in zip(m0.parameters(), m0b.parameters()))
-    for x, y in zip(l0, l1):
-        assert abs(x - y) <= 1e-4 * abs(x)
+    # The first loss precedes any update (forward only: no atomics on its
+    # value path); the second follows one step whose split-K / column-sum
+    # atomics differ run to run, and INT8 re-rounding of the updated weights
+    # amplifies that -- bound it by the same step run twice without comm.
+    assert abs(l0[0] - l1[0]) <= 1e-6 * abs(l0[0])
+    assert abs(l0[1] - l1[1]) <= max(10 * abs(l0[1] - l0b[1]), 1e-3 * abs(l0[1]))
     for a, b in zip(m0.parameters(), m1.parameters()):
         assert float((a - b).abs().max()) <= max(10 * run_to_run, 1e-6)
     assert [b for b, _ in st1.grads.issue_log] == list(range(len(st1.grads.buckets)))
