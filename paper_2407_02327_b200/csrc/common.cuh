@@ -158,11 +158,29 @@ __device__ __forceinline__ float quot_rn(float x, QScale q) {
     const float t = __fmaf_rn(-y, q.s, x);
     return fabsf(y) < 256.0f ? __fmaf_rn(t, q.r, y) : y;
 }
-__device__ __forceinline__ int quant_rne(float x, QScale q) {
-    float r = rintf(quot_rn(x, q));
-    r = fminf(fmaxf(r, -127.0f), 127.0f);
-    return static_cast<int>(r);
+// The quantized value is produced as a "grid float": t = RN(clamp(x/s) + 1.5*2^23).
+// Every float in [2^23, 2^24) is an integer, so the add is the round-to-nearest-
+// even of the clamped quotient, t's bits are 0x4B400000 + q, and -- that
+// constant's low byte being 0 -- t's low byte IS the int8 two's-complement byte
+// of q.  No FRND / F2I / I2F (quarter-rate conversion pipe) on the path: the
+// quantizers were issue-bound on them.  Clamping before rounding equals
+// rounding then clamping on [-127, 127] (the bounds are integers); a NaN
+// quotient clamps to -127 either way (fmaxf returns the non-NaN operand).
+__device__ __forceinline__ float quant_rne_f(float x, QScale q) {
+    const float v = fminf(fmaxf(quot_rn(x, q), -127.0f), 127.0f);
+    return __fadd_rn(v, 12582912.0f);
 }
+__device__ __forceinline__ int quant_rne(float x, QScale q) {
+    return static_cast<int>(__float_as_uint(quant_rne_f(x, q))) - 0x4B400000;
+}
+// Four grid floats -> four packed int8 (their low bytes), lowest address first.
+__device__ __forceinline__ uint32_t pack_q4(float a, float b, float c, float d) {
+    const uint32_t ab = __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x0040);
+    const uint32_t cd = __byte_perm(__float_as_uint(c), __float_as_uint(d), 0x0040);
+    return __byte_perm(ab, cd, 0x5410);
+}
+// The grid value q of a grid float, exactly, as a float.
+__device__ __forceinline__ float grid_value(float t) { return __fsub_rn(t, 12582912.0f); }
 
 
 // Two floats -> packed 16-bit pair (one F2FP.PACK_AB instruction), low half first.

@@ -175,11 +175,8 @@ __global__ void __launch_bounds__(kWarps * 32, QSB_ADAM_MINB) k_adamw(const qsyn
                     reinterpret_cast<uint2*>(w16)[k] = h;
                 }
                 if (wq) {
-                    reinterpret_cast<uint32_t*>(wq)[k] =
-                        static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.x, qsc))) |
-                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.y, qsc))) << 8) |
-                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.z, qsc))) << 16) |
-                        (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(pv.w, qsc))) << 24);
+                    reinterpret_cast<uint32_t*>(wq)[k] = pack_q4(quant_rne_f(pv.x, qsc), quant_rne_f(pv.y, qsc),
+                                                                 quant_rne_f(pv.z, qsc), quant_rne_f(pv.w, qsc));
                 }
             }
         } else {

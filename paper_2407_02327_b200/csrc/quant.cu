@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256) k_absmax_rows(const typename Elem<DT>::T*
 // 4 (F32) or 2 (F16/BF16) 16B loads, one 16B store.  Block 0 publishes s.
 // ---------------------------------------------------------------------------
 template <int DT, int ACT = 0>
-__global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::T* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, 2) k_quantize(const typename Elem<DT>::T* __restrict__ x,
                                                        int64_t n, const float* __restrict__ absmax_in,
                                                        const float* __restrict__ scale_in,
                                                        int8_t* __restrict__ q,
@@ -249,13 +249,13 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
 #pragma unroll
                         for (int e = 0; e < 4; ++e) a[e] = act_f<ACT, DT>(f[j + e]);
                     }
-                    const int i0 = quant_rne(a[0], qs), i1 = quant_rne(a[1], qs);
-                    const int i2 = quant_rne(a[2], qs), i3 = quant_rne(a[3], qs);
-                    const uint32_t b0 = static_cast<uint8_t>(i0), b1 = static_cast<uint8_t>(i1);
-                    const uint32_t b2 = static_cast<uint8_t>(i2), b3 = static_cast<uint8_t>(i3);
-                    packed[(u * V::N + j) / 4] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
-                    hq[(u * V::N + j) / 2] = pack_half2(static_cast<float>(i0), static_cast<float>(i1));
-                    hq[(u * V::N + j) / 2 + 1] = pack_half2(static_cast<float>(i2), static_cast<float>(i3));
+                    const float t0 = quant_rne_f(a[0], qs), t1 = quant_rne_f(a[1], qs);
+                    const float t2 = quant_rne_f(a[2], qs), t3 = quant_rne_f(a[3], qs);
+                    packed[(u * V::N + j) / 4] = pack_q4(t0, t1, t2, t3);
+                    if (q16) {
+                        hq[(u * V::N + j) / 2] = pack_half2(grid_value(t0), grid_value(t1));
+                        hq[(u * V::N + j) / 2 + 1] = pack_half2(grid_value(t2), grid_value(t3));
+                    }
                 }
             }
             qv[i] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
@@ -270,21 +270,26 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename Elem<DT>::
                 dv[1] = make_uint4(dp[4], dp[5], dp[6], dp[7]);
             }
         };
+        // vec_ok bit 1: walk the groups from the end -- the second pass of the
+        // two-pass per-tensor quantizer then starts on what the absmax pass read
+        // last (still in L2) instead of on what it has already evicted.
+        const bool rev = (vec_ok & 2) != 0;
+        auto at = [&](int64_t j) { return rev ? n16 - 1 - j : j; };
         int64_t i = tid;
         for (; i + (G - 1) * stride < n16; i += G * stride) {
             uint4 r[G][LOADS];
 #pragma unroll
             for (int g = 0; g < G; ++g)
 #pragma unroll
-                for (int u = 0; u < LOADS; ++u) r[g][u] = ld_stream(xv + (i + g * stride) * LOADS + u);
+                for (int u = 0; u < LOADS; ++u) r[g][u] = ld_stream(xv + at(i + g * stride) * LOADS + u);
 #pragma unroll
-            for (int g = 0; g < G; ++g) process(i + g * stride, r[g]);
+            for (int g = 0; g < G; ++g) process(at(i + g * stride), r[g]);
         }
         for (; i < n16; i += stride) {
             uint4 r[LOADS];
 #pragma unroll
-            for (int u = 0; u < LOADS; ++u) r[u] = ld_stream(xv + i * LOADS + u);
-            process(i, r);
+            for (int u = 0; u < LOADS; ++u) r[u] = ld_stream(xv + at(i) * LOADS + u);
+            process(at(i), r);
         }
         done = n16 * 16;
     }
@@ -371,23 +376,19 @@ __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __rest
         }
         __half h[4];
         if (MODE == 0) {
-            int qi[4];
+            float t[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                qi[i] = quant_rne(f[i], qs);
-                h[i] = __int2half_rn(qi[i]);
+                t[i] = quant_rne_f(f[i], qs);
+                h[i] = __float2half_rn(grid_value(t[i]));
             }
             if (q && r < rows) {
                 if (full_cols) {
-                    const uint32_t pk = static_cast<uint32_t>(static_cast<uint8_t>(qi[0])) |
-                                        (static_cast<uint32_t>(static_cast<uint8_t>(qi[1])) << 8) |
-                                        (static_cast<uint32_t>(static_cast<uint8_t>(qi[2])) << 16) |
-                                        (static_cast<uint32_t>(static_cast<uint8_t>(qi[3])) << 24);
-                    *reinterpret_cast<uint32_t*>(q + r * cols + c) = pk;
+                    *reinterpret_cast<uint32_t*>(q + r * cols + c) = pack_q4(t[0], t[1], t[2], t[3]);
                 } else {
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
-                        if (c + i < cols) q[r * cols + c + i] = static_cast<int8_t>(qi[i]);
+                        if (c + i < cols) q[r * cols + c + i] = static_cast<int8_t>(__float_as_uint(t[i]) & 0xffu);
                 }
             }
         } else {
@@ -474,8 +475,11 @@ __global__ void __launch_bounds__(256) k_tile(const typename Elem<DT>::T* __rest
     }
 }
 
-// Per-channel quantize: one warp per row, absmax pass then quantize pass (the
-// second read of the row hits L1/L2).
+// Per-channel quantize: one warp per row.  Rows of up to 32 * 4 * kRowVec
+// floats stay in registers between the absmax and the quantize step (all of a
+// lane's 16-byte loads in flight at once, one HBM read per element); longer or
+// unaligned rows take two passes (the second read hits L1/L2).
+constexpr int kRowVec = 8;  // float4 per lane cached: rows of <= 1024 floats
 __global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w, int64_t rows,
                                                     int64_t cols, int8_t* __restrict__ q,
                                                     float* __restrict__ scales) {
@@ -485,11 +489,39 @@ __global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w,
     if (row >= rows) return;
     const float* wr = w + row * cols;
     int8_t* qr = q + row * cols;
-    const bool vec = (cols % 4 == 0) && aligned16(wr);
+    const bool vec = (cols % 4 == 0) && aligned16(wr) && (reinterpret_cast<uintptr_t>(qr) & 3u) == 0;
+    const int64_t n4 = cols / 4;
+    if (vec && n4 <= 32 * kRowVec) {
+        const float4* v = reinterpret_cast<const float4*>(wr);
+        float4 f[kRowVec];
+#pragma unroll
+        for (int i = 0; i < kRowVec; ++i) {
+            const int64_t c = lane + 32 * i;
+            f[i] = c < n4 ? __ldcs(v + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float m = 0.0f;
+#pragma unroll
+        for (int i = 0; i < kRowVec; ++i)
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(f[i].x), fabsf(f[i].y)), fmaxf(fabsf(f[i].z), fabsf(f[i].w))));
+        m = warp_max(m);
+        const float s = scale_from_absmax(m);
+        if (lane == 0) scales[row] = s;
+        const QScale qs = make_qscale(s);
+        uint32_t* qo = reinterpret_cast<uint32_t*>(qr);
+#pragma unroll
+        for (int i = 0; i < kRowVec; ++i) {
+            const int64_t c = lane + 32 * i;
+            if (c < n4)
+                qo[c] = pack_q4(quant_rne_f(f[i].x, qs), quant_rne_f(f[i].y, qs), quant_rne_f(f[i].z, qs),
+                                quant_rne_f(f[i].w, qs));
+        }
+        return;
+    }
     float m = 0.0f;
     if (vec) {
         const float4* v = reinterpret_cast<const float4*>(wr);
-        for (int64_t c = lane; c < cols / 4; c += 32) {
+#pragma unroll 4
+        for (int64_t c = lane; c < n4; c += 32) {
             float4 f = v[c];
             m = fmaxf(m, fmaxf(fmaxf(fabsf(f.x), fabsf(f.y)), fmaxf(fabsf(f.z), fabsf(f.w))));
         }
@@ -500,15 +532,13 @@ __global__ void __launch_bounds__(256) k_quant_rows(const float* __restrict__ w,
     const float s = scale_from_absmax(m);
     if (lane == 0) scales[row] = s;
     const QScale qs = make_qscale(s);
-    if (vec && (reinterpret_cast<uintptr_t>(qr) & 3u) == 0) {
+    if (vec) {
         const float4* v = reinterpret_cast<const float4*>(wr);
         uint32_t* qo = reinterpret_cast<uint32_t*>(qr);
-        for (int64_t c = lane; c < cols / 4; c += 32) {
+#pragma unroll 4
+        for (int64_t c = lane; c < n4; c += 32) {
             float4 f = v[c];
-            qo[c] = static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.x, qs))) |
-                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.y, qs))) << 8) |
-                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.z, qs))) << 16) |
-                    (static_cast<uint32_t>(static_cast<uint8_t>(quant_rne(f.w, qs))) << 24);
+            qo[c] = pack_q4(quant_rne_f(f.x, qs), quant_rne_f(f.y, qs), quant_rne_f(f.z, qs), quant_rne_f(f.w, qs));
         }
     } else {
         for (int64_t c = lane; c < cols; c += 32) qr[c] = static_cast<int8_t>(quant_rne(wr[c], qs));
@@ -821,7 +851,26 @@ __global__ void __launch_bounds__(kThreads) k_stats_partial(const typename Elem<
     if (vec_ok) {
         const int64_t nv = n / V::N;
         const uint4* xv = reinterpret_cast<const uint4*>(x);
-        for (int64_t i = tid; i < nv; i += stride) {
+        // 4 x 16 B loads in flight per thread (as k_absmax): one load per
+        // iteration left the smaller sweep sizes latency-bound (0.68 at 64 MB)
+        constexpr int U = 4;
+        int64_t i = tid;
+        for (; i + (U - 1) * stride < nv; i += U * stride) {
+            uint4 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) r[u] = ld_stream(xv + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float f[V::N];
+                V::unpack(r[u], f);
+#pragma unroll
+                for (int j = 0; j < V::N; ++j) {
+                    m = fmaxf(m, fabsf(f[j]));
+                    ss = fma(static_cast<double>(f[j]), static_cast<double>(f[j]), ss);
+                }
+            }
+        }
+        for (; i < nv; i += stride) {
             float f[V::N];
             V::unpack(ld_stream(xv + i), f);
 #pragma unroll
@@ -943,7 +992,7 @@ struct QuantRun {
                                                 t8 ? static_cast<int8_t*>(q_t) : nullptr);
             return check_launch("k_tile<quant>");
         }
-        const int vec = aligned16(x) && aligned16(q);
+        const int vec = (aligned16(x) && aligned16(q)) ? 3 : 0;  // bit 1: reverse walk (L2 reuse)
         const int grid = grid_for(n / 16 + 1, kThreads, 2);  // <= 64 regs: 2 x 512 threads per SM
         pdl_launch(k_quantize<DT>, dim3(grid), dim3(kThreads), 0, st, static_cast<const T*>(x), n, scale + 1, nullptr,
                                                   q, scale, vec, static_cast<uint16_t*>(nullptr), static_cast<uint16_t*>(nullptr));

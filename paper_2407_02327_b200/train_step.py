@@ -418,13 +418,13 @@ class TrainStep:
             # Side-stream wgrad GEMM grid cap (persistent kernels).  A 2/3-of-SMs
             # cap once paid (5.55 -> 5.25 ms); with 192-wide tiles and the FP16
             # wgrad operands written by the quantizer the uncapped grid is best
-            # (tools/ab_wgrad_cap.py: 5.09 ms uncapped vs 5.20 at 98 CTAs).
+            # (tools/ab_step.py wgrad_cap=0,98: 5.09 ms uncapped vs 5.20).
             from . import fused as _fz
             _fz.WGRAD_CTAS = 0
         # Bucket-wise optimizer (DP): each bucket's AdamW runs on the comm stream
         # right after its all-reduce, overlapping the remaining buckets' reductions
         # and the rest of the backward.  On one GPU it only contends with the
-        # backward for HBM (tools/ab_overlap_opt.py: 5.01 vs 4.97 ms), so it is off there.
+        # backward for HBM (tools/ab_step.py overlap_opt=0,1: 5.01 vs 4.97 ms), so it is off there.
         self.overlap_opt = fused and (world > 1 if overlap_opt is None else overlap_opt)
         self._hooked = (world > 1 or self.overlap_opt or comm is not None) and fused
         if self._hooked:

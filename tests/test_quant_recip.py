@@ -24,3 +24,7 @@ def test_reciprocal_fma_rounding_is_exact(tmp_path):
     r = subprocess.run([exe] + edge + rand, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout
     assert "mismatches 0" in r.stdout
+    # the grid-float rounding (clamp + 1.5*2^23 add) vs sat(rint(v)) over all non-NaN quotients
+    r = subprocess.run([exe, "grid"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout
+    assert "checked 4278190082 mismatches 0" in r.stdout

@@ -69,8 +69,16 @@ def cases():
 
 
 def main():
-    print(f"{'case':22s} {'GFLOP':>7s} {'ideal':>7s} {'us':>7s} {'noepi':>7s} {'nopdl':>7s}  TF/s")
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bn", type=int, default=0, help="force the tile width (0 = cost model)")
+    ap.add_argument("--only", default="", help="substring filter on the case name")
+    args = ap.parse_args()
+    _lib.call("qsync_gemm_force_tile_n", args.bn)
+    print(f"{'case':22s} {'GFLOP':>7s} {'ideal':>7s} {'us':>7s} {'noepi':>7s} {'nopdl':>7s}  TF/s  (bn={args.bn})")
     for name, fn, flops in cases():
+        if args.only and args.only not in name:
+            continue
         t = graph_time_us(fn)
         _lib.call("qsync_gemm_debug_epilogue", 1)
         t_ne = graph_time_us(fn)
