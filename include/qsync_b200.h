@@ -293,6 +293,16 @@ int qsync_layernorm_fwd_ex(const float* a, const void* b, int b_dtype, const flo
                            const float* beta, int64_t rows, int64_t cols, float eps, float* s_out,
                            float* y, float* mean, float* rstd, uint16_t* y16, float* y_absmax,
                            qsync_stream_t stream);
+/* LayerNorm forward fused with the per-tensor INT8 quantizer of y (the input of
+ * an INT8-planned Linear): y, s_out, mean, rstd as qsync_layernorm_fwd_ex, q =
+ * RNE int8 of y with s = absmax(y)/127, q16 (optional) = FP16(q), scale[0] = s,
+ * scale[1] = absmax -- bit-identical to qsync_layernorm_fwd_ex(.., y_absmax)
+ * followed by qsync_quantize_act_ex.  One kernel when one row per warp fits
+ * co-resident (the rows stay in registers across a grid barrier on absmax),
+ * else those two launches. */
+int qsync_layernorm_fwd_quant(const float* a, const void* b, int b_dtype, const float* gamma, const float* beta,
+                              int64_t rows, int64_t cols, float eps, float* s_out, float* y, float* mean,
+                              float* rstd, int8_t* q, uint16_t* q16, float* scale, qsync_stream_t stream);
 /* LayerNorm backward that also emits the incoming gradient of the Linear that
  * produced the residual branch: dx16 (optional) = FP16(dx), the FP16 backward
  * format (cost_mapper.cpp:13-15), and dcolsum (optional) += sum_rows dx, that
@@ -311,6 +321,12 @@ int qsync_embed_layernorm_fwd(const int64_t* tokens, int64_t rows, int64_t seq, 
                               const float* pos, const float* typ, const float* gamma, const float* beta,
                               int64_t cols, float eps, float* s_out, float* y, float* mean, float* rstd,
                               uint16_t* y16, float* y_absmax, qsync_stream_t stream);
+/* qsync_embed_layernorm_fwd fused with the INT8 quantizer of y, as
+ * qsync_layernorm_fwd_quant. */
+int qsync_embed_layernorm_fwd_quant(const int64_t* tokens, int64_t rows, int64_t seq, const float* word,
+                                    const float* pos, const float* typ, const float* gamma, const float* beta,
+                                    int64_t cols, float eps, float* s_out, float* y, float* mean, float* rstd,
+                                    int8_t* q, uint16_t* q16, float* scale, qsync_stream_t stream);
 int qsync_embed_layernorm_bwd(const float* dy, const float* s, const float* mean, const float* rstd,
                               const float* gamma, const int64_t* tokens, int64_t rows, int64_t seq, int64_t cols,
                               float* dgamma, float* dbeta, float* dword, float* dpos, float* dtyp,

@@ -68,6 +68,8 @@ SIGNATURES = {
     "qsync_im2col": [_p, _int, _i64, _i64, _i64, _i64] + [_int] * 8 + [_p, _i64, _p],
     "qsync_col2im": [_p, _int, _i64, _i64, _i64, _i64] + [_int] * 8 + [_i64, _p, _p],
     "qsync_layernorm_fwd_ex": [_p, _p, _int, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p, _p],
+    "qsync_layernorm_fwd_quant": [_p, _p, _int, _p, _p, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p, _p, _p],
+    "qsync_embed_layernorm_fwd_quant": [_p, _i64, _i64, _p, _p, _p, _p, _p, _i64, _f32] + [_p] * 8,
     "qsync_layernorm_bwd_ex": [_p, _p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p],
     "qsync_absmax_act": [_p, _int, _i64, _int, _p, _p],
     "qsync_quantize_act": [_p, _int, _i64, _int, _p, _p, _p, _p, _p],

@@ -14,6 +14,10 @@
 #include "common.cuh"
 #include "vec.cuh"
 
+#ifndef QSB_LN_FWD_MINB
+#define QSB_LN_FWD_MINB 4  // 4 x 256 threads per SM (<= 64 registers)
+#endif
+
 namespace qsb {
 namespace {
 
@@ -30,8 +34,44 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
                  : "memory");
 }
 
-template <int NV, int BDT>
-__global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
+// Fused per-tensor quantizer state (kQ): per-block absmax partials and a
+// self-resetting grid barrier, one slot per stream (slot = stream hash), in
+// statically allocated device memory -- nothing to allocate or zero per call.
+constexpr int kLnQSlots = 32;
+constexpr int kLnQMaxBlocks = 1024;
+__device__ float g_lnq_part[kLnQSlots][kLnQMaxBlocks];
+__device__ unsigned g_lnq_bar[kLnQSlots][2];  // [0] arrivals, [1] generation
+
+// Grid-wide barrier over co-resident blocks (the host checks residency): the
+// last arriving block resets the count and bumps the generation the others
+// spin on.  Each kernel uses its slot once, and launches on one stream are
+// ordered, so a slot is never shared by two live barriers.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g0 = *gen;  // read before arriving: it cannot move until every block arrived
+        __threadfence();           // this block's partial is visible before its arrival
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// kQ: LayerNorm + per-tensor INT8 quantizer of y in one kernel (the input of an
+// INT8-planned Linear).  One row per warp and every block co-resident: the
+// normalised row stays in shared memory across a grid barrier on absmax(y), then
+// is quantized with s = absmax/127 (quant_rne_f, bit-identical to
+// qsync_quantize_act_ex on the stored y) -- y is not read back and the
+// separate quantize launch is gone.  qs[0] = s, qs[1] = absmax.
+template <int NV, int BDT, bool kQ = false>
+__global__ void __launch_bounds__(256, QSB_LN_FWD_MINB) k_ln_fwd(const float* __restrict__ a,
                                                 const typename Elem<BDT>::T* __restrict__ b,
                                                 const float* __restrict__ gamma,
                                                 const float* __restrict__ beta, int64_t rows,
@@ -43,16 +83,32 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
                                                 const int64_t* __restrict__ tok = nullptr,
                                                 const float* __restrict__ pos = nullptr,
                                                 const float* __restrict__ typ = nullptr,
-                                                int seq = 1) {
-    QSB_PDL_ENTER();
+                                                int seq = 1, int8_t* __restrict__ q = nullptr,
+                                                uint16_t* __restrict__ q16 = nullptr,
+                                                float* __restrict__ qs = nullptr, int qslot = 0) {
+    if constexpr (kQ) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // dependents only after the barrier
+    } else {
+        QSB_PDL_ENTER();
+    }
     const int lane = threadIdx.x & 31;
     float amax = 0.0f;
+    int64_t keep_row = -1;
+    // kQ: this warp's normalised row, parked in shared memory across the barrier
+    __shared__ float4 s_keep[kQ ? 8 : 1][kQ ? NV : 1][32];
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    float4 g[NV], be[NV];
+    // gamma / beta are read at use (L1-resident, shared by all rows): holding
+    // them across the grid-stride rows cost 48 registers and held the kernel
+    // to one 256-thread block per SM; at <= 64 registers 4 blocks (one row per
+    // warp for BERT's 4096 rows, the fused quantizer's co-residency) fit.
+    constexpr bool kHold = false;
+    float4 g[kHold ? NV : 1], be[kHold ? NV : 1];
+    if constexpr (kHold) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        g[i] = reinterpret_cast<const float4*>(gamma)[lane + 32 * i];
-        be[i] = reinterpret_cast<const float4*>(beta)[lane + 32 * i];
+        for (int i = 0; i < NV; ++i) {
+            g[i] = reinterpret_cast<const float4*>(gamma)[lane + 32 * i];
+            be[i] = reinterpret_cast<const float4*>(beta)[lane + 32 * i];
+        }
     }
     const float inv_n = 1.0f / static_cast<float>(cols);
     for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
@@ -99,12 +155,15 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             const int64_t off = row * cols + 4 * (lane + 32 * i);
+            const float4 gi = kHold ? g[kHold ? i : 0] : __ldg(reinterpret_cast<const float4*>(gamma) + lane + 32 * i);
+            const float4 bi = kHold ? be[kHold ? i : 0] : __ldg(reinterpret_cast<const float4*>(beta) + lane + 32 * i);
             float4 o;
-            o.x = (v[i].x - mean) * rstd * g[i].x + be[i].x;
-            o.y = (v[i].y - mean) * rstd * g[i].y + be[i].y;
-            o.z = (v[i].z - mean) * rstd * g[i].z + be[i].z;
-            o.w = (v[i].w - mean) * rstd * g[i].w + be[i].w;
+            o.x = (v[i].x - mean) * rstd * gi.x + bi.x;
+            o.y = (v[i].y - mean) * rstd * gi.y + bi.y;
+            o.z = (v[i].z - mean) * rstd * gi.z + bi.z;
+            o.w = (v[i].w - mean) * rstd * gi.w + bi.w;
             *reinterpret_cast<float4*>(y + off) = o;
+            if constexpr (kQ) s_keep[threadIdx.x >> 5][i][lane] = o;
             if (y16) {
                 uint2 h;
                 h.x = pack_half2(o.x, o.y);
@@ -117,6 +176,56 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const float* __restrict__ a,
             mean_out[row] = mean;
             rstd_out[row] = rstd;
         }
+        if constexpr (kQ) keep_row = row;
+    }
+    if constexpr (kQ) {
+        __shared__ float wmax[8];
+        __shared__ float s_abs;
+        amax = warp_max(amax);
+        if (lane == 0) wmax[threadIdx.x >> 5] = amax;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            amax = warp_max(threadIdx.x < (blockDim.x >> 5) ? wmax[threadIdx.x] : 0.0f);
+            if (threadIdx.x == 0) g_lnq_part[qslot][blockIdx.x] = amax;
+        }
+        grid_barrier(g_lnq_bar[qslot], gridDim.x);
+        // every block reduces all partials (deterministic, no accumulator to zero)
+        float m = 0.0f;
+        for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x)
+            m = fmaxf(m, __ldcg(&g_lnq_part[qslot][i]));
+        m = warp_max(m);
+        if (lane == 0) wmax[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float t = 0.0f;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t = fmaxf(t, wmax[w]);
+            s_abs = t;
+        }
+        __syncthreads();
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        const float sc = scale_from_absmax(s_abs);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            qs[0] = sc;
+            qs[1] = s_abs;
+        }
+        const QScale qsc = make_qscale(sc);
+        if (keep_row >= 0) {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int64_t off = keep_row * cols + 4 * (lane + 32 * i);
+                const float4 o = s_keep[threadIdx.x >> 5][i][lane];
+                const float t0 = quant_rne_f(o.x, qsc), t1 = quant_rne_f(o.y, qsc);
+                const float t2 = quant_rne_f(o.z, qsc), t3 = quant_rne_f(o.w, qsc);
+                *reinterpret_cast<uint32_t*>(q + off) = pack_q4(t0, t1, t2, t3);
+                if (q16) {
+                    uint2 h;
+                    h.x = pack_half2(grid_value(t0), grid_value(t1));
+                    h.y = pack_half2(grid_value(t2), grid_value(t3));
+                    *reinterpret_cast<uint2*>(q16 + off) = h;
+                }
+            }
+        }
+        return;
     }
     if (y_absmax) {
         // absmax of y for the next INT8 op's per-tensor scale: warp max, block
@@ -359,14 +468,67 @@ int ln_fwd_nv(const float* a, const void* b, int b_dtype, const float* gamma, co
                                                       rows, cols, eps, s_out, y, mean, rstd,
                                                       reinterpret_cast<__half*>(y16),
                                                       reinterpret_cast<unsigned*>(y_absmax), nullptr, nullptr,
-                                                      nullptr, 1);
+                                                      nullptr, 1, static_cast<int8_t*>(nullptr),
+                                                      static_cast<uint16_t*>(nullptr), static_cast<float*>(nullptr), 0);
     else
         pdl_launch(k_ln_fwd<NV, QSYNC_F32>, dim3(grid), dim3(256), 0, st, a, static_cast<const float*>(b), gamma, beta,
                                                       rows, cols, eps, s_out, y, mean, rstd,
                                                       reinterpret_cast<__half*>(y16),
                                                       reinterpret_cast<unsigned*>(y_absmax), nullptr, nullptr,
-                                                      nullptr, 1);
+                                                      nullptr, 1, static_cast<int8_t*>(nullptr),
+                                                      static_cast<uint16_t*>(nullptr), static_cast<float*>(nullptr), 0);
     return check_launch("k_ln_fwd");
+}
+
+// LayerNorm (+ embedding gather when tok) fused with the per-tensor INT8
+// quantizer of y (k_ln_fwd<kQ>) when one row per warp fits co-resident;
+// otherwise LayerNorm with absmax, then the one-pass quantizer -- the same q,
+// q16 and qs either way.
+template <int NV, int BDT>
+int ln_fwd_quant_launch(const float* a, const void* b, const int64_t* tok, const float* pos, const float* typ,
+                        int seq, const float* gamma, const float* beta, int64_t rows, int cols, float eps,
+                        float* s_out, float* y, float* mean, float* rstd, int8_t* q, uint16_t* q16, float* qs,
+                        cudaStream_t st) {
+    using BT = typename Elem<BDT>::T;
+    const int64_t blocks = (rows + 7) / 8;
+    static int occ[16] = {0};
+    int dev = 0;
+    QSB_TRY(cuda_status(cudaGetDevice(&dev), "cudaGetDevice"));
+    if (dev < 16 && occ[dev] == 0) {
+        int n = 0;
+        QSB_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_ln_fwd<NV, BDT, true>, 256, 0),
+                            "cudaOccupancyMaxActiveBlocksPerMultiprocessor"));
+        occ[dev] = n > 0 ? n : -1;
+    }
+    const int per_sm = dev < 16 ? occ[dev] : 0;
+    if (per_sm > 0 && blocks <= kLnQMaxBlocks && blocks <= static_cast<int64_t>(per_sm) * sm_count()) {
+        const int slot = static_cast<int>((reinterpret_cast<uintptr_t>(st) >> 4) % kLnQSlots);
+        pdl_launch(k_ln_fwd<NV, BDT, true>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, a,
+                   static_cast<const BT*>(b), gamma, beta, rows, cols, eps, s_out, y, mean, rstd,
+                   static_cast<__half*>(nullptr), static_cast<unsigned*>(nullptr), tok, pos, typ, seq, q, q16, qs,
+                   slot);
+        return check_launch("k_ln_fwd<quant>");
+    }
+    QSB_TRY(zero_async(qs + 1, sizeof(float), st));
+    const int grid = static_cast<int>(std::min<int64_t>(blocks, sm_count() * 8LL));
+    pdl_launch(k_ln_fwd<NV, BDT>, dim3(grid), dim3(256), 0, st, a, static_cast<const BT*>(b), gamma, beta, rows, cols,
+               eps, s_out, y, mean, rstd, static_cast<__half*>(nullptr), reinterpret_cast<unsigned*>(qs + 1), tok, pos,
+               typ, seq, static_cast<int8_t*>(nullptr), static_cast<uint16_t*>(nullptr), static_cast<float*>(nullptr),
+               0);
+    QSB_TRY(check_launch("k_ln_fwd"));
+    return qsync_quantize_act_ex(y, QSYNC_F32, rows * cols, QSYNC_ACT_NONE, qs + 1, q, qs, nullptr, q16, st);
+}
+
+template <int NV>
+int ln_fwd_quant_nv(const float* a, const void* b, int b_dtype, const int64_t* tok, const float* pos,
+                    const float* typ, int seq, const float* gamma, const float* beta, int64_t rows, int cols,
+                    float eps, float* s_out, float* y, float* mean, float* rstd, int8_t* q, uint16_t* q16, float* qs,
+                    cudaStream_t st) {
+    if (b_dtype == QSYNC_F16)
+        return ln_fwd_quant_launch<NV, QSYNC_F16>(a, b, tok, pos, typ, seq, gamma, beta, rows, cols, eps, s_out, y,
+                                                  mean, rstd, q, q16, qs, st);
+    return ln_fwd_quant_launch<NV, QSYNC_F32>(a, b, tok, pos, typ, seq, gamma, beta, rows, cols, eps, s_out, y, mean,
+                                              rstd, q, q16, qs, st);
 }
 
 template <int NV>
@@ -396,7 +558,9 @@ int embed_ln_fwd_nv(const int64_t* tok, int64_t rows, int seq, const float* word
     const int grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, sm_count() * 8LL));
     pdl_launch(k_ln_fwd<NV, QSYNC_F32>, dim3(grid), dim3(256), 0, st, word, static_cast<const float*>(nullptr), gamma, beta, rows, cols, eps, s_out, y, mean,
                                                   rstd, reinterpret_cast<__half*>(y16),
-                                                  reinterpret_cast<unsigned*>(y_absmax), tok, pos, typ, seq);
+                                                  reinterpret_cast<unsigned*>(y_absmax), tok, pos, typ, seq,
+                                                  static_cast<int8_t*>(nullptr), static_cast<uint16_t*>(nullptr),
+                                                  static_cast<float*>(nullptr), 0);
     return check_launch("k_ln_fwd<embed>");
 }
 
@@ -441,6 +605,62 @@ int qsync_layernorm_fwd_ex(const float* a, const void* b, int b_dtype, const flo
         case 7: return ln_fwd_nv<7>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
         default: return ln_fwd_nv<8>(a, b, b_dtype, gamma, beta, rows, c, eps, s_out, y, mean, rstd, y16, y_absmax, st);
     }
+}
+
+int qsync_layernorm_fwd_quant(const float* a, const void* b, int b_dtype, const float* gamma, const float* beta,
+                              int64_t rows, int64_t cols, float eps, float* s_out, float* y, float* mean,
+                              float* rstd, int8_t* q, uint16_t* q16, float* scale, qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0, QSYNC_ERR_DOMAIN, "negative row count");
+    QSB_REQUIRE(cols % 128 == 0 && cols >= 128 && cols <= 1024, QSYNC_ERR_DOMAIN,
+                "layernorm supports 128 <= cols <= 1024, cols % 128 == 0");
+    QSB_REQUIRE(b_dtype == QSYNC_F32 || b_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN,
+                "residual operand must be F32 or F16");
+    QSB_REQUIRE(q != nullptr && scale != nullptr, QSYNC_ERR_VALIDATION, "q and scale (float[2]) are required");
+    if (rows == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int c = static_cast<int>(cols);
+#define QSB_LNQ(NV) \
+    return ln_fwd_quant_nv<NV>(a, b, b_dtype, nullptr, nullptr, nullptr, 1, gamma, beta, rows, c, eps, s_out, y, mean, \
+                               rstd, q, q16, scale, st)
+    switch (c / 128) {
+        case 1: QSB_LNQ(1);
+        case 2: QSB_LNQ(2);
+        case 3: QSB_LNQ(3);
+        case 4: QSB_LNQ(4);
+        case 5: QSB_LNQ(5);
+        case 6: QSB_LNQ(6);
+        case 7: QSB_LNQ(7);
+        default: QSB_LNQ(8);
+    }
+#undef QSB_LNQ
+}
+
+int qsync_embed_layernorm_fwd_quant(const int64_t* tokens, int64_t rows, int64_t seq, const float* word,
+                                    const float* pos, const float* typ, const float* gamma, const float* beta,
+                                    int64_t cols, float eps, float* s_out, float* y, float* mean, float* rstd,
+                                    int8_t* q, uint16_t* q16, float* scale, qsync_stream_t stream) {
+    QSB_REQUIRE(rows >= 0 && seq > 0, QSYNC_ERR_DOMAIN, "bad rows / seq");
+    QSB_REQUIRE(cols % 128 == 0 && cols >= 128 && cols <= 1024, QSYNC_ERR_DOMAIN,
+                "layernorm supports 128 <= cols <= 1024, cols % 128 == 0");
+    QSB_REQUIRE(tokens && word && pos && typ, QSYNC_ERR_VALIDATION, "tokens and embedding tables are required");
+    QSB_REQUIRE(q != nullptr && scale != nullptr, QSYNC_ERR_VALIDATION, "q and scale (float[2]) are required");
+    if (rows == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    const int c = static_cast<int>(cols);
+#define QSB_ELNQ(NV)                                                                                          \
+    return ln_fwd_quant_nv<NV>(word, nullptr, QSYNC_F32, tokens, pos, typ, static_cast<int>(seq), gamma, beta, rows, \
+                               c, eps, s_out, y, mean, rstd, q, q16, scale, st)
+    switch (c / 128) {
+        case 1: QSB_ELNQ(1);
+        case 2: QSB_ELNQ(2);
+        case 3: QSB_ELNQ(3);
+        case 4: QSB_ELNQ(4);
+        case 5: QSB_ELNQ(5);
+        case 6: QSB_ELNQ(6);
+        case 7: QSB_ELNQ(7);
+        default: QSB_ELNQ(8);
+    }
+#undef QSB_ELNQ
 }
 
 int qsync_layernorm_bwd_ex(const float* dy, const float* s, const float* mean, const float* rstd,

@@ -179,6 +179,9 @@ def _mark(kind: str, op: str) -> None:
 # =============================================================================== layer
 def _operand(x, aux, prec):
     """The planned op's input operand (and what its backward keeps)."""
+    if isinstance(aux, tuple):  # produced by the upstream kernel (LayerNorm + quantizer)
+        assert prec == INT8 and aux[0] == "i8"
+        return aux
     if prec == INT8:
         if aux is not None and aux.dtype == torch.float32 and aux.numel() == 1:
             # the quantizer also writes FP16(q) for the wgrad (no cast kernel there)
@@ -330,11 +333,17 @@ class _FusedLayerFn(torch.autograd.Function):
         yo, w16_o = _linear_fwd(L.o, op_o)
         f16, am = _need_aux(p1)
         _mark("fwd", pre + ".ln1")
-        x1, s1, mean1, rstd1, x1_16, x1_am = ops.layernorm_fwd_ex(
-            x0f, yo, L.ln1.weight.detach(), L.ln1.bias.detach(), L.ln1.eps, f16, am)
+        if am:  # INT8 FF1: LayerNorm and its per-tensor quantizer in one kernel
+            x1, s1, mean1, rstd1, q1, sc1, q1_16 = ops.layernorm_fwd_quant(
+                x0f, yo, L.ln1.weight.detach(), L.ln1.bias.detach(), L.ln1.eps)
+            aux1 = ("i8", q1, sc1[:1], q1_16)
+        else:
+            x1, s1, mean1, rstd1, x1_16, _ = ops.layernorm_fwd_ex(
+                x0f, yo, L.ln1.weight.detach(), L.ln1.bias.detach(), L.ln1.eps, f16, False)
+            aux1 = x1_16 if f16 else None
         # --- FF1 -> GELU folded into FF2's operand kernel
         _mark("cast", L.ff1.name)
-        op_1 = _operand(x1, x1_16 if f16 else x1_am, p1)
+        op_1 = _operand(x1, aux1, p1)
         _mark("fwd", L.ff1.name)
         h, w16_1 = _linear_fwd(L.ff1, op_1)
         # ... and the same pass stores GELU'(h) in FP16 for the backward, which
@@ -357,9 +366,15 @@ class _FusedLayerFn(torch.autograd.Function):
         f, w16_2 = _linear_fwd(L.ff2, op_2)
         f16n, amn = _need_aux(next_prec)
         _mark("fwd", pre + ".ln2")
-        x2, s2, mean2, rstd2, x2_16, x2_am = ops.layernorm_fwd_ex(
-            x1, f, L.ln2.weight.detach(), L.ln2.bias.detach(), L.ln2.eps, f16n, amn)
-        aux2 = x2_16 if f16n else (x2_am if amn else None)
+        none = torch.empty(0, device=x0.device)
+        if amn:  # the next layer's INT8 QKV operand straight out of LN2
+            x2, s2, mean2, rstd2, q2, sc2, q2_16 = ops.layernorm_fwd_quant(
+                x1, f, L.ln2.weight.detach(), L.ln2.bias.detach(), L.ln2.eps)
+            auxes = (q2, sc2, q2_16)
+        else:
+            x2, s2, mean2, rstd2, x2_16, _ = ops.layernorm_fwd_ex(
+                x1, f, L.ln2.weight.detach(), L.ln2.bias.detach(), L.ln2.eps, f16n, False)
+            auxes = (x2_16 if f16n else none, none, none)
 
         ctx.layer = L
         ctx.ops_ = (op_qkv, op_o, op_1, op_2)
@@ -369,14 +384,12 @@ class _FusedLayerFn(torch.autograd.Function):
         ctx.h = (h.dtype, gp)  # GELU'(h) is all the backward needs of h
         ctx.shape = (B, S, H)
         out = x2.view(B, S, H)
-        if aux2 is None:
-            aux2 = torch.empty(0, device=x0.device)
-        ctx.mark_non_differentiable(aux2)
-        ctx.set_materialize_grads(False)  # no zero-filled gradient for the aux output
-        return out, aux2
+        ctx.mark_non_differentiable(*auxes)
+        ctx.set_materialize_grads(False)  # no zero-filled gradient for the aux outputs
+        return (out,) + auxes
 
     @staticmethod
-    def backward(ctx, dx2, _daux):
+    def backward(ctx, dx2, _daux, _ds, _d16):
         L = ctx.layer
         B, S, H = ctx.shape
         M = B * S
@@ -449,5 +462,6 @@ class _FusedLayerFn(torch.autograd.Function):
 def fused_layer(layer, x, aux, next_prec):
     """Run one EncoderLayer through the layer-fused Function.  Returns (x, aux)
     where aux is the next planned op's operand hint (FP16 copy or absmax)."""
-    out, aux2 = _FusedLayerFn.apply(x, aux, layer, next_prec)
-    return out, (aux2 if aux2.numel() else None)
+    from .glue import pack_aux
+    out, aux2, s2, q16 = _FusedLayerFn.apply(x, aux, layer, next_prec)
+    return out, pack_aux(aux2, s2, q16)

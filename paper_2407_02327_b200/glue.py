@@ -75,21 +75,26 @@ class _EmbedLN(torch.autograd.Function):
     aux is the first planned op's operand hint (FP16 copy / absmax) or empty."""
 
     @staticmethod
-    def forward(ctx, tokens, word, pos, typ, gamma, beta, eps, want_f16, want_absmax):
+    def forward(ctx, tokens, word, pos, typ, gamma, beta, eps, want_f16, want_absmax, want_quant=False):
         from .fused import _mark
         _mark("fwd", "embed")
         B, S = tokens.shape
-        y, s, mean, rstd, y16, am = ops.embed_layernorm_fwd(tokens, word, pos, typ, gamma, beta, eps,
-                                                            want_f16, want_absmax)
+        none = torch.empty(0, device=word.device)
+        if want_quant:  # the first planned op is INT8: its operand comes out of the same kernel
+            y, s, mean, rstd, q, sc, q16 = ops.embed_layernorm_fwd_quant(tokens, word, pos, typ, gamma, beta, eps)
+            aux = (q, sc, q16)
+        else:
+            y, s, mean, rstd, y16, am = ops.embed_layernorm_fwd(tokens, word, pos, typ, gamma, beta, eps,
+                                                                want_f16, want_absmax)
+            aux = (y16 if want_f16 else (am if want_absmax else none), none, none)
         ctx.save_for_backward(tokens, s, mean, rstd)
         ctx.params = (word, pos, typ, gamma, beta)
-        aux = y16 if want_f16 else (am if want_absmax else torch.empty(0, device=y.device))
-        ctx.mark_non_differentiable(aux)
+        ctx.mark_non_differentiable(*aux)
         ctx.set_materialize_grads(False)
-        return y.view(B, S, -1), aux
+        return (y.view(B, S, -1),) + aux
 
     @staticmethod
-    def backward(ctx, dy, _daux):
+    def backward(ctx, dy, _daux, _ds, _d16):
         from .fused import _mark
         _mark("bwd", "embed")
         tokens, s, mean, rstd = ctx.saved_tensors
@@ -101,14 +106,23 @@ class _EmbedLN(torch.autograd.Function):
         dy = dy.reshape(-1, dy.shape[-1]).contiguous()
         ops.embed_layernorm_bwd(dy, s, mean, rstd, gamma.detach(), tokens, grads[3], grads[4], grads[0],
                                 grads[1], grads[2])
-        out = [None, None, None, None, None, None, None, None, None]
+        out = [None] * 10
         for i, p in enumerate((word, pos, typ, gamma, beta)):
             if getattr(p, "main_grad", None) is None:
                 out[1 + i] = grads[i]
         return tuple(out)
 
 
-def embed_layernorm(tokens, word, pos, typ, ln, want_f16=False, want_absmax=False):
-    y, aux = _EmbedLN.apply(tokens, word.weight, pos.weight, typ.weight, ln.weight, ln.bias, ln.eps,
-                            want_f16, want_absmax)
-    return y, (aux if aux.numel() else None)
+def pack_aux(aux, s, q16):
+    """The next planned op's operand hint carried between fused kernels: an
+    FP16 copy or absmax tensor, or (INT8) the quantized operand itself as the
+    tuple ("i8", q, s[1], FP16(q)); None when there is nothing to carry."""
+    if s.numel():
+        return ("i8", aux, s[:1], q16)
+    return aux if aux.numel() else None
+
+
+def embed_layernorm(tokens, word, pos, typ, ln, want_f16=False, want_absmax=False, want_quant=False):
+    y, aux, s, q16 = _EmbedLN.apply(tokens, word.weight, pos.weight, typ.weight, ln.weight, ln.bias, ln.eps,
+                                    want_f16, want_absmax, want_quant)
+    return y, pack_aux(aux, s, q16)

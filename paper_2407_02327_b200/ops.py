@@ -470,6 +470,29 @@ def layernorm_fwd_ex(a, b, gamma, beta, eps: float, want_f16: bool = False,
     return y, (s if s is not None else a), mean, rstd, y16, am
 
 
+def layernorm_fwd_quant(a, b, gamma, beta, eps: float, s_out: bool = True):
+    """LN forward fused with the per-tensor INT8 quantizer of y (the input of an
+    INT8-planned Linear).  Returns (y, s, mean, rstd, q, scale, q16): scale =
+    device float[2] (s = absmax/127, absmax), q16 = FP16(q) for the wgrad."""
+    _req(a, "a", (torch.float32,))
+    cols = a.shape[-1]
+    rows = a.numel() // cols
+    y = torch.empty_like(a)
+    s = torch.empty_like(a) if (b is not None and s_out) else None
+    mean = torch.empty(rows, device=a.device, dtype=torch.float32)
+    rstd = torch.empty(rows, device=a.device, dtype=torch.float32)
+    q = torch.empty(a.shape, device=a.device, dtype=torch.int8)
+    q16 = torch.empty(a.shape, device=a.device, dtype=torch.float16)
+    sc = torch.empty(2, device=a.device, dtype=torch.float32)
+    bd = F32
+    if b is not None:
+        _req(b, "b", (torch.float32, torch.float16))
+        bd = _DT[b.dtype]
+    call("qsync_layernorm_fwd_quant", _ptr(a), _ptr(b), bd, _ptr(gamma), _ptr(beta), rows, cols, float(eps),
+         _ptr(s), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(q), _ptr(q16), _ptr(sc), _stream())
+    return y, (s if s is not None else a), mean, rstd, q, sc, q16
+
+
 def layernorm_bwd_ex(dy, s, mean, rstd, gamma, dgamma, dbeta, want_f16: bool = False,
                      colsum_into=None, out=None):
     """LN backward; also FP16(dx) and dx's column sums ADDED into ``colsum_into``.
@@ -575,6 +598,27 @@ def embed_layernorm_fwd(tokens, word, pos, typ, gamma, beta, eps: float, want_f1
     call("qsync_embed_layernorm_fwd", _ptr(tokens), rows, S, _ptr(word), _ptr(pos), _ptr(typ), _ptr(gamma),
          _ptr(beta), H, float(eps), _ptr(s), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(y16), _ptr(am), _stream())
     return y, s, mean, rstd, y16, am
+
+
+def embed_layernorm_fwd_quant(tokens, word, pos, typ, gamma, beta, eps: float):
+    """embed_layernorm_fwd fused with the INT8 quantizer of y (layernorm_fwd_quant).
+    Returns (y [B*S, H], s, mean, rstd, q, scale float[2], q16)."""
+    _req(tokens, "tokens", (torch.int64,))
+    B, S = tokens.shape
+    H = word.shape[1]
+    rows = B * S
+    dev = word.device
+    y = torch.empty((rows, H), device=dev, dtype=torch.float32)
+    s = torch.empty_like(y)
+    mean = torch.empty(rows, device=dev, dtype=torch.float32)
+    rstd = torch.empty(rows, device=dev, dtype=torch.float32)
+    q = torch.empty((rows, H), device=dev, dtype=torch.int8)
+    q16 = torch.empty((rows, H), device=dev, dtype=torch.float16)
+    sc = torch.empty(2, device=dev, dtype=torch.float32)
+    call("qsync_embed_layernorm_fwd_quant", _ptr(tokens), rows, S, _ptr(word), _ptr(pos), _ptr(typ), _ptr(gamma),
+         _ptr(beta), H, float(eps), _ptr(s), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(q), _ptr(q16), _ptr(sc),
+         _stream())
+    return y, s, mean, rstd, q, sc, q16
 
 
 def embed_layernorm_bwd(dy, s, mean, rstd, gamma, tokens, dgamma, dbeta, dword, dpos, dtyp) -> None:

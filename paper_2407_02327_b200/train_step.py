@@ -158,7 +158,7 @@ class BertEncoderStack(torch.nn.Module):
             fusable = [_fusable(layer) for layer in self.layers]
             p0 = self.layers[0].qkv.precision if len(self.layers) and fusable[0] else None
             x, aux = embed_layernorm(tokens, self.word, self.pos, self.typ, self.ln,
-                                     want_f16=p0 == FP16, want_absmax=p0 == INT8)
+                                     want_f16=p0 == FP16, want_quant=p0 == INT8)
             n = len(self.layers)
             for i, layer in enumerate(self.layers):
                 if not fusable[i]:  # a BF16 / FP8 op: the per-operator layer

@@ -33,9 +33,10 @@ def graph_us(fns, streams, n=20, reps=5):
     with torch.cuda.graph(g):
         cur = torch.cuda.current_stream()
         for _ in range(n):
+            if any(streams):  # fork before either GEMM is enqueued: the two run concurrently
+                side.wait_stream(cur)
             for f, s in zip(fns, streams):
                 if s:
-                    side.wait_stream(cur)
                     with torch.cuda.stream(side):
                         f()
                 else:
