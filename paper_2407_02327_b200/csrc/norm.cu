@@ -15,7 +15,7 @@
 #include "vec.cuh"
 
 #ifndef QSB_LN_FWD_MINB
-#define QSB_LN_FWD_MINB 4  // 4 x 256 threads per SM (<= 64 registers)
+#define QSB_LN_FWD_MINB 1  // A/B (tools/ab_step.py lib=): 1, 2 and 4 blocks / SM within 0.2%
 #endif
 
 namespace qsb {
@@ -71,7 +71,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
 // qsync_quantize_act_ex on the stored y) -- y is not read back and the
 // separate quantize launch is gone.  qs[0] = s, qs[1] = absmax.
 template <int NV, int BDT, bool kQ = false>
-__global__ void __launch_bounds__(256, QSB_LN_FWD_MINB) k_ln_fwd(const float* __restrict__ a,
+__global__ void __launch_bounds__(256, kQ ? 4 : QSB_LN_FWD_MINB) k_ln_fwd(const float* __restrict__ a,
                                                 const typename Elem<BDT>::T* __restrict__ b,
                                                 const float* __restrict__ gamma,
                                                 const float* __restrict__ beta, int64_t rows,
@@ -97,10 +97,10 @@ __global__ void __launch_bounds__(256, QSB_LN_FWD_MINB) k_ln_fwd(const float* __
     // kQ: this warp's normalised row, parked in shared memory across the barrier
     __shared__ float4 s_keep[kQ ? 8 : 1][kQ ? NV : 1][32];
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    // gamma / beta are read at use (L1-resident, shared by all rows): holding
-    // them across the grid-stride rows cost 48 registers and held the kernel
-    // to one 256-thread block per SM; at <= 64 registers 4 blocks (one row per
-    // warp for BERT's 4096 rows, the fused quantizer's co-residency) fit.
+    // gamma / beta are read at use (L1-resident, shared by all rows) rather than
+    // held across the grid-stride rows: 48 registers less, which the fused
+    // quantizer needs (<= 64 registers: 4 blocks / SM, one row per warp for
+    // BERT's 4096 rows co-resident).
     constexpr bool kHold = false;
     float4 g[kHold ? NV : 1], be[kHold ? NV : 1];
     if constexpr (kHold) {
