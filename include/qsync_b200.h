@@ -372,6 +372,20 @@ int qsync_gemm_s8_ex(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int
                      int c_dtype, const float* scale_a, const float* scale_b, int b_per_channel,
                      const float* bias, qsync_stream_t stream);
 
+/* An encoder layer's FF1 with the GELU that follows it in the GEMM epilogue
+ * (the work of the FF2 operand kernels qsync_act_cast / qsync_gelu_absmax_store,
+ * minus the quantization, which needs the finished absmax).  ab_dtype I8: the
+ * qsync_gemm_s8_ex dequant epilogue (scale_a, scale_b, bias) gives y in FP32;
+ * F16/BF16: y = the qsync_gemm_f16 value rounded to FP16 (what the FP16 op
+ * stores).  Then g = gelu(y) (erf form), rounded to y's dtype and stored as
+ * g_dtype (F32 or F16); dact [m, n] FP16 = gelu'(y) (for the backward); and
+ * *absmax (device float, overwritten) = max |g| -- the FF2 quantizer's input.
+ * Bit-identical to the unfused GEMM followed by those kernels.  n % 8 == 0,
+ * g and dact 16-byte aligned. */
+int qsync_gemm_gelu(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,
+                    const float* scale_a, const float* scale_b, int b_per_channel, const float* bias, void* g,
+                    int g_dtype, uint16_t* dact, float* absmax, qsync_stream_t stream);
+
 /* Attention core softmax(Q K^T scale) V of an encoder layer (stays
  * floating point), in the planned projections' formats: qkv packed
  * [B, S, 3, H, D] FP16 (the QKV projection's output), out [B, S, H, D] FP16,

@@ -63,6 +63,11 @@ struct EpiParams {
     const uint8_t* cx;  // NHWC input (elements of the GEMM operand type)
     int cN, cH, cW, cC, cP, cQ, cR, cS, csh, csw, cph, cpw;
     int ctap, cdvh, cdvw;
+    // kLay bit 9: GELU epilogue (an encoder layer's FF1 with the activation that
+    // follows it): c = g = gelu(y), dact = FP16(gelu'(y)) through tm_d, and
+    // act_absmax = max |g| (float bits, atomicMax; the caller zeroes it).
+    uint16_t* dact;
+    unsigned* act_absmax;
     // kLay bits 5 / 6: the same operands loaded by TMA in im2col mode instead
     // (A for fwd / stride-1 dgrad -- the dgrad as a conv of dY with pad k-1-p and
     // flipped taps; B for wgrad); one elected thread, no gather lanes.
@@ -138,7 +143,8 @@ __device__ __forceinline__ float bits_f(uint32_t v) { return __uint_as_float(v);
 template <bool kI8, int BN, int kCta, int kLay>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-              const __grid_constant__ CUtensorMap tm_c, const EpiParams p) {
+              const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_d,
+              const EpiParams p) {
     using C = Cfg<BN, kCta>;
     constexpr int kBRows = C::kBRows;
     constexpr int kStages = C::kStages;
@@ -150,6 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // K-major only -- the FP32 plan's 3xTF32 GEMM (qsync_gemm_f32).
     constexpr bool kTF32 = (kLay & 256) != 0;
     static_assert(!kTF32 || (!kI8 && (kLay & 255) == 0), "TF32 is a K-major FP-kind layout");
+    constexpr bool kGelu = (kLay & 512) != 0;
+    static_assert(!kGelu || (kCta == 1 && (kLay & 511) == 0), "GELU epilogue: single-CTA K-major tiles");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B swizzle atoms: the declaration asks for
     // it and the smem budget (Cfg::kSmemBytes) assumes it -- trap, not corrupt.
@@ -197,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!(kLay & 4)) ptx::tma_prefetch(&tm_a);
         if (!(kLay & 8)) ptx::tma_prefetch(&tm_b);
         if (p.tma_store) ptx::tma_prefetch(&tm_c);
+        if (kGelu) ptx::tma_prefetch(&tm_d);
         for (int s = 0; s < kStages; ++s) {
             // implicit conv: + one cp.async completion arrival per producer lane
             ptx::mbar_init(&full[s], (kLay & 12) ? 33 : 1);
@@ -382,6 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int kb0 = (u % ksplit) * p.kb_per;
                 const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
                 for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef QSB_GEMM_TRACE
+                    if (p.debug_epi & 2) break;  // isolation: MMA-only (no operand loads)
+#endif
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (kb == kb0) QSB_TRACE_U(u, 0);
                     if (kCta == 2) {
@@ -489,7 +501,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
                 for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef QSB_GEMM_TRACE
+                    // isolation modes: 2 = MMA-only (no full wait), 4 = loads only (no MMAs)
+                    if (!(p.debug_epi & 2)) ptx::mbar_wait(&full[stage], phase);
+                    if (p.debug_epi & 4) {
+                        if (kb == kb0) QSB_TRACE_U(u, 2);
+                        ptx::mbar_arrive(&empty[stage]);
+                        if (++stage == kStages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
+#else
                     ptx::mbar_wait(&full[stage], phase);
+#endif
                     if (kb == kb0) QSB_TRACE_U(u, 2);
                     // cp.async (generic proxy) wrote A: order it before the
                     // tensor core's async-proxy reads.
@@ -508,6 +534,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                 ? ptx::sw128_mnmajor_desc(b_addr + k * 16 * 128, bk_elems * 128)
                                                 : ptx::sw128_kmajor_desc(b_addr + k * 32);
                         const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+#ifdef QSB_GEMM_TRACE
+                        // isolation mode 8: odd K-steps into the other accumulator
+                        // buffer (wrong sums; times two independent MMA chains)
+                        const uint32_t d_tmem_k = ((p.debug_epi & 8) && (k & 1))
+                                                      ? tmem_base + static_cast<uint32_t>((acc ^ 1) * BN)
+                                                      : d_tmem;
+#define d_tmem d_tmem_k
+#endif
                         if (kCta == 2) {
                             if (kI8 && kF8)
                                 ptx::mma_f8_pair(d_tmem, da, db, p.idesc, accum);
@@ -525,6 +559,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             else
                                 ptx::mma_f16(d_tmem, da, db, p.idesc, accum);
                         }
+#ifdef QSB_GEMM_TRACE
+#undef d_tmem
+#endif
                     }
                     if (kCta == 2)
                         ptx::tc_commit_pair(&empty[stage]);  // frees the stage in both CTAs
@@ -607,6 +644,73 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool row_ok = row < M;
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
+            if constexpr (kGelu) {
+                // 64-column chunks: y exactly as the plain GEMM would store it (FP32
+                // for INT8; the FP16 GEMM's value rounded to FP16), then the FF2
+                // operand kernel's math (qsync_act_cast / gelu_absmax_store):
+                // g = gelu(y) rounded as those kernels round it (to y's dtype, then to
+                // c_dtype), FP16 gelu'(y), max |g| over the valid rows and columns.
+                const bool g16 = p.c_dtype == QSYNC_F16;
+                float amax = 0.0f;
+                // one staged 32-row x 128-byte piece -> TMA store at (col, row0)
+                auto emit = [&](const uint32_t (&wv)[32], const CUtensorMap* map, int64_t col) {
+                    if (lane == 0) ptx::bulk_wait_read<C::kEpiBufs - 1>();
+                    __syncwarp();
+                    uint8_t* buf = my_stage + sbuf * kStageChunkBytes;
+                    const uint32_t rbase = ptx::smem_u32(buf) + lane * 128;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        ptx::st_shared_v4(rbase + ((c ^ (lane & 7)) << 4), wv[4 * c], wv[4 * c + 1], wv[4 * c + 2],
+                                          wv[4 * c + 3]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d(map, buf, static_cast<int32_t>(col), static_cast<int32_t>(row0));
+                        ptx::bulk_commit();
+                    }
+                    sbuf = (sbuf + 1) % C::kEpiBufs;
+                };
+#pragma unroll 1
+                for (int c0 = half * 64; c0 < BN; c0 += 128) {
+                    const int64_t col0 = n0 + c0;
+                    uint32_t rr[2][32];
+                    ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0), rr[0]);
+                    ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0 + 32), rr[1]);
+                    ptx::tmem_ld_wait();
+                    if (row0 >= M || col0 >= N) continue;  // warp-uniform
+                    uint32_t wg[32], wd[32];  // FP16 g (64 cols), FP16 gelu' (64 cols)
+#pragma unroll
+                    for (int sub = 0; sub < 2; ++sub) {
+                        const int cb = c0 + 32 * sub;
+                        uint32_t wf[32];  // FP32 g of these 32 columns
+#pragma unroll
+                        for (int j = 0; j < 32; j += 2) {
+                            float gv[2], dv[2];
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const uint32_t a = rr[sub][j + e];
+                                float v = kI8 ? __fmul_rn(__int2float_rn(static_cast<int>(a)), fs[cb + j + e])
+                                              : __fmul_rn(bits_f(a), alpha);
+                                if (p.bias) v = __fadd_rn(v, fb[cb + j + e]);
+                                if (!kI8) v = __half2float(__float2half_rn(v));  // the FP16 GEMM's stored h
+                                gelu_and_grad(v, gv[e], dv[e]);
+                                // round_to<h dtype> as the FF2 operand kernels do (FP16 for an
+                                // FP16 GEMM's h), and the stored dtype
+                                if (g16 || !kI8) gv[e] = __half2float(__float2half_rn(gv[e]));
+                                if (row_ok && col0 + 32 * sub + j + e < N) amax = fmaxf(amax, fabsf(gv[e]));
+                                wf[j + e] = __float_as_uint(gv[e]);
+                            }
+                            wg[16 * sub + j / 2] = pack_half2(gv[0], gv[1]);
+                            wd[16 * sub + j / 2] = pack_half2(dv[0], dv[1]);
+                        }
+                        if (!g16) emit(wf, &tm_c, col0 + 32 * sub);
+                    }
+                    if (g16) emit(wg, &tm_c, col0);
+                    emit(wd, &tm_d, col0);
+                }
+                amax = warp_max(amax);
+                if (lane == 0 && amax > 0.0f) atomicMax(p.act_absmax, __float_as_uint(amax));
+            } else
 #pragma unroll 1
             for (int c0 = half * chunk_cols; c0 < BN; c0 += 2 * chunk_cols) {
                 uint32_t w[32];  // the 128 bytes of this thread's row in the chunk
@@ -930,7 +1034,10 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     using C = Cfg<BN, kCta>;
     const uint32_t eb = kI8 ? 1 : ((kLay & 256) ? 4 : 2);
     const uint32_t box_k = BK_BYTES / eb;
-    CUtensorMap ma, mb, mc;
+    CUtensorMap ma, mb, mc, md;
+    std::memset(&md, 0, sizeof(md));
+    if (kLay & 512)  // GELU epilogue: FP16 gelu'(y) [M, N], 64-column x 32-row boxes
+        QSB_TRY(make_map(&md, p.dact, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, p.N, p.M, 64, 32));
     if (kLay & 4)  // implicit conv: A is gathered by the producer lanes
         std::memset(&ma, 0, sizeof(ma));
     else if (kLay & 32)  // A = im2col view of the NHWC input, 128 pixels x 128 bytes
@@ -1025,7 +1132,7 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    QSB_TRY(cuda_status(cudaLaunchKernelEx(&cfg, k_gemm_tc<kI8, BN, kCta, kLay>, ma, mb, mc, p),
+    QSB_TRY(cuda_status(cudaLaunchKernelEx(&cfg, k_gemm_tc<kI8, BN, kCta, kLay>, ma, mb, mc, md, p),
                         "cudaLaunchKernelEx(k_gemm_tc)"));
     return check_launch("k_gemm_tc");
 }
@@ -1064,12 +1171,18 @@ Shape pick_shape(int64_t M, int64_t N, bool allow_pair) {
     return best;
 }
 
-// Tile width and split-K of an accumulating FP32 GEMM (wgrad into main_grad),
-// chosen together: a unit (tile, K range) costs its k-blocks x max(MMA, L2
-// feed) cycles plus a fixed pipeline fill + reduce-add epilogue; the GEMM costs
-// waves x that.  E.g. wgrad QKV 2304x768x4096 -> 192-wide tiles split 2 ways =
-// 144 units, one wave; wgrad FF1/FF2 -> 256-wide split 2 ways (not 4: two
-// waves of half-length units).
+// Tile width and split-K of an accumulating FP32 GEMM (wgrad into main_grad,
+// dgrad reduce-added into the residual gradient), chosen together: a unit
+// (tile, K range) costs its k-blocks x the measured per-k-block time plus a
+// fixed pipeline fill + reduce-add epilogue; the GEMM costs waves x that.
+// Per k-block (4 MMAs of K = 32 bytes): tcgen05.mma at M = 128 takes >= ~116
+// cycles per instruction whatever N <= 192 (isolation runs of the trace build,
+// MMA-only: 463-467 cycles per k-block at N = 64, 128, 192 and for CTA pairs),
+// + ~12% when the operand loads run beside it; N = 256 runs at its own rate
+// (128 / MMA) and, with an MN-major B, ~86% of it.  The fixed cost is fitted to
+// tools/acc_sweep.py.  E.g. wgrad QKV 2304x768x4096 -> 192-wide tiles split 2
+// ways = 144 units, one wave; wgrad FF1/FF2 -> 256-wide split 2 ways; dgrad
+// QKV / FF1 (4096x768, K 2304 / 3072) -> 192-wide, no split (128 tiles).
 struct AccChoice {
     int bn, ksplit;
 };
@@ -1080,8 +1193,8 @@ AccChoice choose_acc(int64_t M, int64_t N, int64_t num_kb) {
     double best_cost = 1e300;
     for (int bn : {256, 192, 128}) {
         const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-        const double kb_cost = std::max(4.0 * BM * bn / 256.0, (BM + bn) * 128.0 / 64.0);
-        const double fixed = 1500.0 + 8.0 * bn;
+        const double kb_cost = bn >= 256 ? 600.0 : 520.0;
+        const double fixed = 6000.0;
         for (int ks = 1; ks <= 16; ++ks) {
             const int64_t per = (num_kb + ks - 1) / ks;
             if (ks > 1 && per < 4) break;
@@ -1104,6 +1217,11 @@ int dispatch_shape(const void* a, const void* b, CUtensorMapDataType dt, EpiPara
         switch (sh.bn) {
             case 256: return launch<kI8, 256, 2, kLay>(a, b, dt, p, st);
             case 128: return launch<kI8, 128, 2, kLay>(a, b, dt, p, st);
+            case 192:
+                // 96 B rows per CTA: one 96-row TMA box when B is K-major; the
+                // MN-major B loads come in 64-wide blocks, so no 192-wide pair there.
+                if constexpr (!(kLay & 2)) return launch<kI8, 192, 2, kLay>(a, b, dt, p, st);
+                break;
             default: break;
         }
     }
@@ -1134,7 +1252,8 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     }
     if (force_bn) sh.bn = force_bn;
     if (g_force_cta) sh.cta = g_force_cta;
-    if (sh.cta == 2 && (sh.bn == 64 || sh.bn == 192)) sh.cta = 1;  // pairs: BN/2 a multiple of 64
+    // pairs: BN/2 a multiple of 64, or 96 with a K-major B
+    if (sh.cta == 2 && (sh.bn == 64 || (sh.bn == 192 && (layout & 2)))) sh.cta = 1;
     p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout, p.fp8);
     p.debug_epi = g_debug_epi;
     if (layout & 108) {  // implicit conv (fwd 4/32, dgrad 22/50, wgrad 11/67): single-CTA tiles
@@ -1173,6 +1292,15 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
         if (layout == 11) return launch<false, 256, 1, 11>(a, b, dt, p, st);
         if (layout == 67) return launch<false, 256, 1, 67>(a, b, dt, p, st);
         return set_error(QSYNC_ERR_DOMAIN, "unsupported implicit conv layout " + std::to_string(layout));
+    }
+    if (layout == 512) {  // GELU epilogue (FF1): single-CTA 128..256-wide K-major tiles
+        if (sh.bn == 64) sh.bn = 128;
+        p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM, 0, false);
+        switch (sh.bn) {
+            case 256: return launch<kI8, 256, 1, 512>(a, b, dt, p, st);
+            case 192: return launch<kI8, 192, 1, 512>(a, b, dt, p, st);
+            default: return launch<kI8, 128, 1, 512>(a, b, dt, p, st);
+        }
     }
     if constexpr (kI8) {
         return p.fp8 ? dispatch_shape<true, 128>(a, b, dt, p, st, sh) : dispatch_shape<true, 0>(a, b, dt, p, st, sh);
@@ -1387,6 +1515,39 @@ int qsync_gemm_s8_ex(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int
     p.bias = bias;
     p.alpha = 1.0f;
     return dispatch<true>(a, b, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, to_stream(stream), g_force_bn);
+}
+
+int qsync_gemm_gelu(const void* a, const void* b, int ab_dtype, int64_t m, int64_t n, int64_t k,
+                    const float* scale_a, const float* scale_b, int b_per_channel, const float* bias, void* g,
+                    int g_dtype, uint16_t* dact, float* absmax, qsync_stream_t stream) {
+    QSB_REQUIRE(ab_dtype == QSYNC_I8 || ab_dtype == QSYNC_F16 || ab_dtype == QSYNC_BF16, QSYNC_ERR_DOMAIN,
+                "GELU GEMM operands must be I8, F16 or BF16");
+    const bool i8 = ab_dtype == QSYNC_I8;
+    QSB_TRY(validate(a, b, m, n, k, i8 ? 16 : 8));
+    QSB_REQUIRE(g && dact && absmax, QSYNC_ERR_VALIDATION, "GELU GEMM needs g, dact and absmax");
+    QSB_REQUIRE(g_dtype == QSYNC_F32 || g_dtype == QSYNC_F16, QSYNC_ERR_DOMAIN, "GELU GEMM output must be F32 or F16");
+    QSB_REQUIRE(n % 8 == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(dact) & 15) == 0,
+                QSYNC_ERR_DOMAIN, "GELU GEMM needs N % 8 == 0 and 16-byte aligned outputs (TMA stores)");
+    QSB_REQUIRE(!i8 || (scale_a && scale_b), QSYNC_ERR_VALIDATION, "the dequant epilogue needs scale_a and scale_b");
+    EpiParams p{};
+    p.M = m;
+    p.N = n;
+    p.K = k;
+    p.c = g;
+    p.c_dtype = g_dtype;
+    p.scale_a = i8 ? scale_a : nullptr;
+    p.scale_b = i8 ? scale_b : nullptr;
+    p.b_per_channel = b_per_channel;
+    p.bias = bias;
+    p.alpha = 1.0f;
+    p.dact = dact;
+    p.act_absmax = reinterpret_cast<unsigned*>(absmax);
+    QSB_TRY(zero_async(absmax, sizeof(float), to_stream(stream)));
+    if (i8) return dispatch<true>(a, b, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, to_stream(stream), g_force_bn, 512);
+    const CUtensorMapDataType dt =
+        ab_dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    return dispatch<false>(a, b, dt, p, to_stream(stream), g_force_bn, 512);
 }
 
 int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k,

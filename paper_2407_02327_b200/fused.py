@@ -237,6 +237,28 @@ def _linear_fwd(m, opnd, out_dtype=None):
     return y, w16
 
 
+# GELU in FF1's GEMM epilogue (qsync_gemm_gelu) instead of the GELU-applying FF2
+# operand kernel after a plain GEMM.  Off: measured SLOWER (tools/ab_step.py
+# ff1gelu=1,0 on one B200: int8 plan 5.48 vs 5.00 ms, fp16 4.99 vs 4.66, mixed
+# 5.27 vs 4.87; 128/192-wide tiles no better).  The erf GELU + GELU' is ~45
+# instructions per element; in the epilogue it runs on 8 warps per SM and stalls
+# the tile pipeline, where the standalone kernel spreads it over full occupancy.
+FF1_GELU_EPILOGUE = False
+
+
+def _ff1_gelu(m, opnd, g_dtype):
+    """FF1 (INT8 / FP16 operand) with GELU in the GEMM epilogue: (absmax(g), g,
+    GELU'(h) FP16, w16) -- ops.gemm_gelu."""
+    kind, x, s = opnd[:3]
+    bias = m.bias.detach() if m.bias is not None else None
+    wq, ws, w16 = _weights(m)
+    if kind == "i8":
+        am, g, gp = ops.gemm_gelu(x, wq, s, ws, bias, g_dtype=g_dtype)
+    else:
+        am, g, gp = ops.gemm_gelu(x, w16, bias=bias, g_dtype=g_dtype)
+    return am, g, gp, w16
+
+
 # Persistent-grid cap for the side-stream wgrad GEMMs (0 = all SMs): leaves SMs
 # to the critical-path chain on the main stream.  Set by TrainStep / tools.
 WGRAD_CTAS = 0
@@ -341,27 +363,39 @@ class _FusedLayerFn(torch.autograd.Function):
             x1, s1, mean1, rstd1, x1_16, _ = ops.layernorm_fwd_ex(
                 x0f, yo, L.ln1.weight.detach(), L.ln1.bias.detach(), L.ln1.eps, f16, False)
             aux1 = x1_16 if f16 else None
-        # --- FF1 -> GELU folded into FF2's operand kernel
+        # --- FF1 -> GELU: in FF1's GEMM epilogue (INT8 / FP16 FF1), else folded
+        # into FF2's operand kernel; either way GELU'(h) is stored in FP16 for the
+        # backward, which then needs no transcendental (dh = dg * GELU'(h)).
         _mark("cast", L.ff1.name)
         op_1 = _operand(x1, aux1, p1)
         _mark("fwd", L.ff1.name)
-        h, w16_1 = _linear_fwd(L.ff1, op_1)
-        # ... and the same pass stores GELU'(h) in FP16 for the backward, which
-        # then needs no transcendental (dh = dg * GELU'(h)).
+        h = None
+        if FF1_GELU_EPILOGUE and op_1[0] in ("i8", "f16") and L.ff1.weight.shape[0] % 8 == 0:
+            # g in the dtype the FF2 operand kernel reads, GELU'(h) and absmax(g),
+            # bit-identical to the GEMM + operand kernel below; h is never stored.
+            h_dtype = torch.float32 if op_1[0] == "i8" else torch.float16
+            gdt = h_dtype if p2 == INT8 else (torch.float16 if p2 == FP16 else torch.float32)
+            gam, g_act, gp, w16_1 = _ff1_gelu(L.ff1, op_1, gdt)
+        else:
+            h, w16_1 = _linear_fwd(L.ff1, op_1)
+            h_dtype = h.dtype
         _mark("fwd", pre + ".gelu")
         if p2 == INT8:
-            # one GELU evaluation: g (and GELU') stored with the absmax pass, the
-            # quantizer then a pure streaming pass over g (bit-identical q, s)
-            gam, g_act, gp = ops.gelu_absmax_store(h)
+            if h is not None:
+                # one GELU evaluation: g (and GELU') stored with the absmax pass
+                gam, g_act, gp = ops.gelu_absmax_store(h)
+            # the quantizer is then a pure streaming pass over g (bit-identical q, s)
             gq, gs, g16 = ops.quantize_act(g_act, gam, want_q16=True)
             del g_act
             op_2 = ("i8", gq, gs, g16)
         elif p2 == FP16:
-            g16, gp = ops.act_cast(h, torch.float16, ops.ACT_GELU, want_dact=True)
-            op_2 = ("f16", g16, None)
+            if h is not None:
+                g_act, gp = ops.act_cast(h, torch.float16, ops.ACT_GELU, want_dact=True)
+            op_2 = ("f16", g_act, None)
         else:
-            g32, gp = ops.act_cast(h, torch.float32, ops.ACT_GELU, want_dact=True)
-            op_2 = ("f32", g32, None)
+            if h is not None:
+                g_act, gp = ops.act_cast(h, torch.float32, ops.ACT_GELU, want_dact=True)
+            op_2 = ("f32", g_act, None)
         _mark("fwd", L.ff2.name)
         f, w16_2 = _linear_fwd(L.ff2, op_2)
         f16n, amn = _need_aux(next_prec)
@@ -381,7 +415,7 @@ class _FusedLayerFn(torch.autograd.Function):
         ctx.w16 = (w16_qkv, w16_o, w16_1, w16_2)
         ctx.attn = (qkv5, a, lse, scale)
         ctx.ln = (s1, mean1, rstd1, s2, mean2, rstd2)
-        ctx.h = (h.dtype, gp)  # GELU'(h) is all the backward needs of h
+        ctx.h = (h_dtype, gp)  # GELU'(h) is all the backward needs of h
         ctx.shape = (B, S, H)
         out = x2.view(B, S, H)
         ctx.mark_non_differentiable(*auxes)

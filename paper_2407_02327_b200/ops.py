@@ -580,6 +580,27 @@ def gemm_s8_ex(a: torch.Tensor, b: torch.Tensor, scale_a, scale_b, bias=None,
     return c
 
 
+def gemm_gelu(a: torch.Tensor, b: torch.Tensor, scale_a=None, scale_b=None, bias=None,
+              g_dtype=torch.float32, b_per_channel: bool = True):
+    """FF1 with its GELU in the epilogue: (absmax[1], g = GELU(y) as g_dtype,
+    GELU'(y) FP16) where y is what gemm_s8_ex (INT8 a/b, FP32 y) or gemm_f16
+    (FP16 a/b, FP16 y) would return -- bit-identical to that GEMM followed by
+    gelu_absmax_store / act_cast(ACT_GELU, want_dact=True)."""
+    _req(a, "a", (torch.int8, torch.float16, torch.bfloat16))
+    _req(b, "b", (a.dtype,))
+    M, K = a.shape
+    N = b.shape[0]
+    g = torch.empty((M, N), device=a.device, dtype=g_dtype)
+    d = torch.empty((M, N), device=a.device, dtype=torch.float16)
+    am = torch.empty(1, device=a.device, dtype=torch.float32)
+    ev = _timed("gemm_s8" if a.dtype == torch.int8 else "gemm_f16", 2.0 * M * N * K)
+    call("qsync_gemm_gelu", _ptr(a), _ptr(b), _DT_CAST[a.dtype], M, N, K, _ptr(scale_a), _ptr(scale_b),
+         int(b_per_channel), _ptr(bias), _ptr(g), _DT[g_dtype], _ptr(d), _ptr(am), _stream())
+    if ev is not None:
+        ev.record()
+    return am, g, d
+
+
 def embed_layernorm_fwd(tokens, word, pos, typ, gamma, beta, eps: float, want_f16: bool = False,
                         want_absmax: bool = False):
     """y = LN(word[tok] + pos[s] + typ[0]) for tokens [B, S] (int64).

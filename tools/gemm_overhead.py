@@ -1,6 +1,8 @@
 """Per-launch time of the tcgen05 GEMMs at the BERT-base step shapes, launched
 back-to-back inside a CUDA graph (as in the train step), with the epilogue
-math/stores on or skipped and programmatic dependent launch on or off.  The
+math/stores on or skipped and programmatic dependent launch on or off, next to
+cuBLAS / cuBLASLt on the same operands (torch.mm FP16 out; torch._int_mm int32
+out with no epilogue, FP16 wgrad without the FP32 accumulate).  The
 difference to the MMA-only bound is the fixed cost (prologue, pipeline fill,
 exposed epilogue) the small GEMMs of the step pay.
 
@@ -46,7 +48,10 @@ def cases():
         a = torch.randn((K, M) if lay == 3 else (M, K), device="cuda").half()
         b = torch.randn((K, N) if lay & 2 else (N, K), device="cuda").half()
         out = torch.zeros(M, N, device="cuda", dtype=torch.float16 if out16 and not acc else torch.float32)
-        return (lambda: ops.gemm_f16(a, b, out=out, accumulate=acc, a_mn=lay == 3, b_mn=bool(lay & 2))), 2.0 * M * N * K
+        am = a.t() if lay == 3 else a
+        bm = b if lay & 2 else b.t()
+        ref = (lambda: torch.mm(am, bm)) if not acc else (lambda: torch.mm(am, bm))
+        return (lambda: ops.gemm_f16(a, b, out=out, accumulate=acc, a_mn=lay == 3, b_mn=bool(lay & 2))), 2.0 * M * N * K, ref
 
     def s8(M, N, K):
         a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
@@ -55,7 +60,8 @@ def cases():
         sb = torch.rand(N, device="cuda")
         bias = torch.randn(N, device="cuda")
         out = torch.empty(M, N, device="cuda")
-        return (lambda: ops.gemm_s8(a, b, sa, sb, bias, out=out)), 2.0 * M * N * K
+        bt = b.t()
+        return (lambda: ops.gemm_s8(a, b, sa, sb, bias, out=out)), 2.0 * M * N * K, (lambda: torch._int_mm(a, bt))
 
     yield "big  f16 8192^3", *f16(8192, 8192, 8192, out16=False)
     yield "big  s8  8192^3", *s8(8192, 8192, 8192)
@@ -75,8 +81,8 @@ def main():
     ap.add_argument("--only", default="", help="substring filter on the case name")
     args = ap.parse_args()
     _lib.call("qsync_gemm_force_tile_n", args.bn)
-    print(f"{'case':22s} {'GFLOP':>7s} {'ideal':>7s} {'us':>7s} {'noepi':>7s} {'nopdl':>7s}  TF/s  (bn={args.bn})")
-    for name, fn, flops in cases():
+    print(f"{'case':22s} {'GFLOP':>7s} {'ideal':>7s} {'us':>7s} {'noepi':>7s} {'nopdl':>7s} {'cublas':>7s}  TF/s  (bn={args.bn})")
+    for name, fn, flops, ref in cases():
         if args.only and args.only not in name:
             continue
         t = graph_time_us(fn)
@@ -86,8 +92,9 @@ def main():
         _lib.call("qsync_gemm_set_pdl", 0)
         t_np = graph_time_us(fn)
         _lib.call("qsync_gemm_set_pdl", 1)
+        t_ref = graph_time_us(ref)
         ideal = flops / PEAK_F16 * 1e6 / (2 if "s8" in name else 1)
-        print(f"{name:22s} {flops / 1e9:7.2f} {ideal:7.1f} {t:7.1f} {t_ne:7.1f} {t_np:7.1f}  {flops / t / 1e6:6.0f}",
+        print(f"{name:22s} {flops / 1e9:7.2f} {ideal:7.1f} {t:7.1f} {t_ne:7.1f} {t_np:7.1f} {t_ref:7.1f}  {flops / t / 1e6:6.0f}",
               flush=True)
 
 

@@ -43,6 +43,12 @@ def cases():
     dw = torch.zeros(F, H, device="cuda")
     out["f16_ff1_wgrad"] = (lambda: ops.gemm_f16(dy, a, out=dw, accumulate=True, a_mn=True, b_mn=True),
                             2.0 * T * F * H)
+    aq = torch.randn(T, H, device="cuda").half()
+    wq = torch.randn(3 * H, H, device="cuda").half()
+    cq = torch.empty(T, 3 * H, device="cuda", dtype=torch.float16)
+    out["f16_qkv_fwd"] = (lambda: ops.gemm_f16(aq, wq, out=cq), 2.0 * T * 3 * H * H)
+    dyq = torch.randn(T, 3 * H, device="cuda").half()
+    out["f16_qkv_dgrad"] = (lambda: ops.gemm_f16(dyq, wq, out=aq, b_mn=True), 2.0 * T * 3 * H * H)
     return out
 
 
@@ -85,14 +91,22 @@ def analyse(buf: torch.Tensor, grid: int) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--json", default=None)
+    ap.add_argument("--modes", default="0", help="comma list of isolation modes (trace build): 0 full, "
+                    "1 no epilogue math/stores, 2 MMA only (no loads), 4 loads only (no MMAs, single CTA)")
+    ap.add_argument("--only", default="")
     ap.add_argument("--variants", default="0:0", help="comma list of cta:tile_n overrides, e.g. 0:0,2:256,2:128")
     args = ap.parse_args()
     buf = torch.zeros(1024 * 72, dtype=torch.int64, device="cuda")
     out = {}
     variants = [tuple(int(x) for x in v.split(":")) for v in args.variants.split(",")]
-    todo = [(f"{name}[cta{c},bn{b}]" if (c, b) != (0, 0) else name, fn, flops, c, b)
-            for name, (fn, flops) in cases().items() for c, b in variants]
-    for name, fn, flops, cta, bn in todo:
+    modes = [int(m) for m in args.modes.split(",")]
+    todo = [(f"{name}[cta{c},bn{b}]" if (c, b) != (0, 0) else name, fn, flops, c, b, m)
+            for name, (fn, flops) in cases().items() for c, b in variants for m in modes
+            if args.only in name]
+    for name, fn, flops, cta, bn, mode in todo:
+        if mode:
+            name += f"[mode{mode}]"
+        _lib.call("qsync_gemm_debug_epilogue", mode)
         ops.force_cta(cta)
         ops.force_tile_n(bn)
         for _ in range(3):
@@ -112,6 +126,7 @@ def main():
         r = analyse(buf, 1024)
         ops.force_cta(0)
         ops.force_tile_n(0)
+        _lib.call("qsync_gemm_debug_epilogue", 0)
         r["event_us"] = plain_us
         r["tflops_event"] = flops / (plain_us * 1e-6) / 1e12
         out[name] = r
