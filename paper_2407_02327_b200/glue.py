@@ -34,6 +34,37 @@ class _AddLayerNorm(torch.autograd.Function):
         return dx, grad_b, (None if mg is not None else dg), (None if mb is not None else db), None
 
 
+class _Gelu(torch.autograd.Function):
+    """GELU (erf form) on this package's kernel, the one the fused layer uses
+    (common.cuh gelu_and_grad): y in x's dtype; the backward multiplies by the
+    FP16 GELU'(x) the forward stored (the fused layer's backward does the same)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        x = x.contiguous()
+        # a BF16 op's output: GELU in FP32, rounded once to BF16 (as torch's bf16 GELU)
+        if x.dtype == torch.bfloat16:
+            y, d = ops.act_cast(ops.cast(x, torch.float32), torch.float32, ops.ACT_GELU, want_dact=True)
+            y = ops.cast(y, torch.bfloat16)
+        else:
+            y, d = ops.act_cast(x, x.dtype, ops.ACT_GELU, want_dact=True)
+        ctx.save_for_backward(d)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (d,) = ctx.saved_tensors
+        if dy.dtype == torch.bfloat16:
+            g = ops.act_bwd_colsum(ops.cast(dy.contiguous(), torch.float32), d, ops.ACT_DERIV,
+                                   out_dtype=torch.float32)
+            return ops.cast(g, torch.bfloat16)
+        return ops.act_bwd_colsum(dy.contiguous(), d, ops.ACT_DERIV, out_dtype=dy.dtype)
+
+
+def gelu(x: torch.Tensor) -> torch.Tensor:
+    return _Gelu.apply(x)
+
+
 class AddLayerNorm(torch.nn.Module):
     """y = LayerNorm(a + b) with FP32 statistics; b may be FP32 or FP16."""
 

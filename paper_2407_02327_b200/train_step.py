@@ -25,7 +25,7 @@ import torch
 import torch.nn.functional as F
 
 from . import qlinear as _ql
-from .glue import AddLayerNorm, attention
+from .glue import AddLayerNorm, attention, gelu
 from .qlinear import EXTENDED, FP16, FP32, INT8, QLinear, cast
 
 
@@ -106,7 +106,7 @@ class EncoderLayer(torch.nn.Module):
         a = attention(qkv.view(B, S, 3, nh, H // nh))  # [B, S, nh, d]
         a = a.reshape(B, S, H)
         x = self.ln1(x, _ln_operand(self.o(a)))        # fused residual add (FP32 or FP16 operand)
-        f = F.gelu(self.ff1(x))
+        f = gelu(self.ff1(x))
         x = self.ln2(x, _ln_operand(self.ff2(f)))
         return x
 
