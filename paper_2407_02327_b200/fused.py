@@ -237,6 +237,13 @@ def _linear_fwd(m, opnd, out_dtype=None):
     return y, w16
 
 
+# INT8 FF2 operand from h: absmax(gelu(h)) then quantize(gelu(h)) with GELU'
+# (GELU evaluated twice, g never stored: 162 MB moved at [4096, 3072] FP32 h)
+# instead of gelu_absmax_store + a quantize of the stored g (212 MB).  Off:
+# measured slower even with the one-exponential GELU (tools/ab_step.py
+# ff2recompute=1,0: int8 plan 5.19 vs 5.03 ms, mixed 4.95 vs 4.87).
+FF2_INT8_RECOMPUTE = False
+
 # GELU in FF1's GEMM epilogue (qsync_gemm_gelu) instead of the GELU-applying FF2
 # operand kernel after a plain GEMM.  Off: measured SLOWER (tools/ab_step.py
 # ff1gelu=1,0 on one B200: int8 plan 5.48 vs 5.00 ms, fp16 4.99 vs 4.66, mixed
@@ -381,12 +388,18 @@ class _FusedLayerFn(torch.autograd.Function):
             h_dtype = h.dtype
         _mark("fwd", pre + ".gelu")
         if p2 == INT8:
-            if h is not None:
-                # one GELU evaluation: g (and GELU') stored with the absmax pass
-                gam, g_act, gp = ops.gelu_absmax_store(h)
-            # the quantizer is then a pure streaming pass over g (bit-identical q, s)
-            gq, gs, g16 = ops.quantize_act(g_act, gam, want_q16=True)
-            del g_act
+            if h is not None and FF2_INT8_RECOMPUTE:
+                # two reads of h, GELU evaluated in both (absmax, then quantize +
+                # GELU' + FP16 q): g is never stored (bit-identical q, s, GELU')
+                gam = ops.absmax_act(h, ops.ACT_GELU)
+                gq, gs, gp, g16 = ops.quantize_act(h, gam, ops.ACT_GELU, want_dact=True, want_q16=True)
+            else:
+                if h is not None:
+                    # one GELU evaluation: g (and GELU') stored with the absmax pass
+                    gam, g_act, gp = ops.gelu_absmax_store(h)
+                # the quantizer is then a pure streaming pass over g (bit-identical q, s)
+                gq, gs, g16 = ops.quantize_act(g_act, gam, want_q16=True)
+                del g_act
             op_2 = ("i8", gq, gs, g16)
         elif p2 == FP16:
             if h is not None:

@@ -40,7 +40,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="launch without programmatic dependent launch, so each kernel's traced duration "
+                         "is its own (with PDL a kernel starts early and waits in griddepcontrol.wait)")
     args = ap.parse_args()
+    if args.no_pdl:
+        from paper_2407_02327_b200 import _lib
+        _lib.call("qsync_gemm_set_pdl", 0)
     cfg = BertConfig()
     torch.manual_seed(0)
     m = BertEncoderStack(cfg).cuda()
