@@ -20,6 +20,7 @@
 // PAPER.md:588-592).
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -52,6 +53,16 @@ struct EpiParams {
     int debug_epi;  // bench hook: 1 = skip epilogue math+stores (TMEM read only)
     int ksplit;     // split-K factor (>1 only with accumulate: partials reduce-add)
     int kb_per;     // k-blocks per split
+    // Stream-K (streamk = 1): the tiles x k-blocks iteration space is cut into
+    // one contiguous range per CTA.  A CTA's first unit may start inside a tile
+    // (a "contributor": its raw accumulators go to sk_ws slot blockIdx.x and it
+    // bumps sk_flags[tile]); a unit that starts a tile but ends inside it (the
+    // "owner") waits for that tile's contributors, adds their partials in CTA
+    // order and runs the epilogue; the owner resets the flag.  Accumulating
+    // outputs need no fixup: every unit reduce-adds, bias from the k = 0 unit.
+    int streamk;
+    uint32_t* sk_ws;   // [gridDim.x][BN / 4][BM][4] raw 32-bit accumulators
+    int* sk_flags;     // [tiles], zero between launches
     // Implicit-GEMM convolution (kLay bit 2): A[(n,p,q), (r,s,c)] is gathered from
     // the NHWC input on the fly -- never materialised.
     int fp8;            // byte operands are FP8 E4M3 (host side; the kernel sees kLay bit 7)
@@ -138,6 +149,42 @@ __device__ __forceinline__ unsigned long long trace_clock() {
 
 __device__ __forceinline__ float bits_f(uint32_t v) { return __uint_as_float(v); }
 
+// Work unit i of a CTA: tile t, k-blocks [kb0, kb1), and its stream-K role
+// (0 plain / split-K part / accumulating, 1 contributor, 2 owner).  The
+// classic schedule strides units u = cta + i * ncta over tiles x ksplit.
+enum { kUnitPlain = 0, kUnitContrib = 1, kUnitOwner = 2 };
+template <bool kSK>
+__device__ __forceinline__ bool unit_at(const EpiParams& p, int i, int cta, int ncta, int num_tiles, int ksplit,
+                                        int num_kb, int& t, int& kb0, int& kb1, int& role) {
+    if (!kSK || !p.streamk) {
+        const int u = cta + i * ncta;
+        if (u >= num_tiles * ksplit) return false;
+        t = u / ksplit;
+        kb0 = (u % ksplit) * p.kb_per;
+        kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
+        role = kUnitPlain;
+        return true;
+    } else {
+    const int64_t total = static_cast<int64_t>(num_tiles) * num_kb;
+    int64_t pos = total * cta / ncta;
+    const int64_t end = total * (cta + 1) / ncta;
+    for (int j = 0;; ++j) {
+        if (pos >= end) return false;
+        const int64_t tt = pos / num_kb;
+        const int k0 = static_cast<int>(pos - tt * num_kb);
+        const int k1 = static_cast<int>(min(static_cast<int64_t>(num_kb), end - tt * num_kb));
+        if (j == i) {
+            t = static_cast<int>(tt);
+            kb0 = k0;
+            kb1 = k1;
+            role = p.accumulate ? kUnitPlain : (k0 > 0 ? kUnitContrib : (k1 < num_kb ? kUnitOwner : kUnitPlain));
+            return true;
+        }
+        pos = tt * num_kb + k1;
+    }
+    }
+}
+
 // kLay bit 0: A is MN-major (stored [K, M]); bit 1: B is MN-major ([K, N]).
 // MN-major tiles are loaded as 64-element-wide (128 B) blocks of bk K-rows.
 template <bool kI8, int BN, int kCta, int kLay>
@@ -157,6 +204,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr bool kTF32 = (kLay & 256) != 0;
     static_assert(!kTF32 || (!kI8 && (kLay & 255) == 0), "TF32 is a K-major FP-kind layout");
     constexpr bool kGelu = (kLay & 512) != 0;
+    // kLay bit 10: stream-K schedule (EpiParams::streamk; 256-wide single-CTA tiles)
+    constexpr bool kSK = (kLay & 1024) != 0;
+    static_assert(!kSK || (kCta == 1 && BN == 256 && (kLay & 0x3fc) == 0), "stream-K: plain 256-wide single-CTA");
     static_assert(!kGelu || (kCta == 1 && (kLay & 511) == 0), "GELU epilogue: single-CTA K-major tiles");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B swizzle atoms: the declaration asks for
@@ -197,7 +247,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_tiles = num_m * num_n;
     // Work units = (tile, K split); split-K partials are reduce-added by TMA.
     const int ksplit = p.ksplit > 1 ? p.ksplit : 1;
-    const int num_units = num_tiles * ksplit;
     const int bk_elems = kI8 ? BK_BYTES : (kTF32 ? BK_BYTES / 4 : BK_BYTES / 2);
     const int num_kb = static_cast<int>((K + bk_elems - 1) / bk_elems);
 
@@ -259,8 +308,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int eb = kI8 ? 1 : 2;
         const int rowbytes = p.cC * eb;
         const int64_t img = static_cast<int64_t>(p.cH) * p.cW * rowbytes;
-        for (int u = unit0; u < num_units; u += unit_stride) {
-            const int t = u / ksplit;
+        for (int ui = 0;; ++ui) {
+            int t, kb0, kb1, role;
+            if (!unit_at<kSK>(p, ui, unit0, unit_stride, num_tiles, ksplit, num_kb, t, kb0, kb1, role)) break;
             const int m0 = (t % num_m) * kTileM;
             const int n0 = (t / num_m) * BN;
             int hb[4], wb[4];
@@ -278,8 +328,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pix[i] = p.cx + static_cast<int64_t>(n) * img;
                 }
             }
-            const int kb0 = (u % ksplit) * p.kb_per;
-            const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
             for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem_a + stage * BM * BK_BYTES;
@@ -384,12 +432,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = unit0; u < num_units; u += unit_stride) {
-                const int t = u / ksplit;
+            for (int ui = 0;; ++ui) {
+                int t, kb0, kb1, role;
+                if (!unit_at<kSK>(p, ui, unit0, unit_stride, num_tiles, ksplit, num_kb, t, kb0, kb1, role)) break;
+                const int u = unit0 + ui * unit_stride;  // (trace slot)
+                (void)u;
                 const int m0 = (t % num_m) * kTileM + static_cast<int>(rank) * BM;
                 const int n0 = (t / num_m) * BN + static_cast<int>(rank) * kBRows;
-                const int kb0 = (u % ksplit) * p.kb_per;
-                const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
                 for (int kb = kb0; kb < kb1; ++kb) {
 #ifdef QSB_GEMM_TRACE
                     if (p.debug_epi & 2) break;  // isolation: MMA-only (no operand loads)
@@ -493,9 +542,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int u = unit0; u < num_units; u += unit_stride) {
-                const int kb0 = (u % ksplit) * p.kb_per;
-                const int kb1 = ksplit > 1 ? min(num_kb, kb0 + p.kb_per) : num_kb;
+            for (int ui = 0;; ++ui) {
+                int t, kb0, kb1, role;
+                if (!unit_at<kSK>(p, ui, unit0, unit_stride, num_tiles, ksplit, num_kb, t, kb0, kb1, role)) break;
+                const int u = unit0 + ui * unit_stride;  // (trace slot)
+                (void)u;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 QSB_TRACE_U(u, 1);
                 ptx::tc_fence_after();
@@ -614,9 +665,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef QSB_GEMM_TRACE
         unsigned long long t_ld = 0, t_math = 0, t_wait = 0, t_store = 0;
 #endif
-        for (int u = unit0; u < num_units; u += unit_stride) {
-            const int t = u / ksplit;
-            const bool add_bias = (u % ksplit) == 0;  // bias once per tile under split-K
+        for (int ui = 0;; ++ui) {
+            int t, kb0, kb1, role;
+            if (!unit_at<kSK>(p, ui, unit0, unit_stride, num_tiles, ksplit, num_kb, t, kb0, kb1, role)) break;
+            const int u = unit0 + ui * unit_stride;  // (trace slot)
+            (void)u;
+            const bool add_bias = kb0 == 0;  // bias once per tile under split-K / stream-K
             const int64_t m0 = static_cast<int64_t>(t % num_m) * kTileM + static_cast<int64_t>(rank) * BM;
             const int64_t n0 = static_cast<int64_t>(t / num_m) * BN;
             if (need_fac) {
@@ -644,6 +698,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool row_ok = row < M;
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
+            // Stream-K owner: the contributors are the next CTAs whose ranges start
+            // inside tile t; wait until all of them have published their partials.
+            int sk_c0 = 0, sk_nc = 0;
+            if (kSK && role == kUnitOwner) {
+                const int64_t total = static_cast<int64_t>(num_tiles) * num_kb;
+                const int64_t tile_end = static_cast<int64_t>(t + 1) * num_kb;
+                sk_c0 = static_cast<int>(blockIdx.x) + 1;
+                for (int c = sk_c0; c < static_cast<int>(gridDim.x) && total * c / gridDim.x < tile_end; ++c) ++sk_nc;
+                if (et == 0) {
+                    uint32_t spins = 0;
+                    while (ptx::ld_acquire_gpu(p.sk_flags + t) < sk_nc)
+                        if (++spins == 0x40000000u) __trap();
+                    p.sk_flags[t] = 0;  // every contributor has arrived: ready for the next launch
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+                __threadfence();
+            }
             if constexpr (kGelu) {
                 // 64-column chunks: y exactly as the plain GEMM would store it (FP32
                 // for INT8; the FP16 GEMM's value rounded to FP16), then the FF2
@@ -729,6 +800,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                 unsigned long long tc1 = trace_clock();
                 t_ld += tc1 - tc0;
 #endif
+                if (kSK && role != kUnitPlain) {
+                    // stream-K partials: raw 32-bit accumulators of the tile in 16-byte
+                    // pieces [slot][column quad][row], so a warp's 32 rows of one quad
+                    // are 512 contiguous bytes (coalesced; a row-major slot made every
+                    // lane's 16 bytes a separate transaction: 7 us per partial tile).
+                    const int row_l = quad * 32 + lane;
+                    if (role == kUnitContrib) {
+                        uint32_t* dst = p.sk_ws + static_cast<size_t>(blockIdx.x) * BM * BN + row_l * 4;
+#pragma unroll
+                        for (int sub = 0; sub < 2; ++sub) {
+                            if (sub >= nsub) break;
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                __stcg(reinterpret_cast<uint4*>(dst + ((c0 + 32 * sub + j) >> 2) * (BM * 4)),
+                                       make_uint4(rr[sub][j], rr[sub][j + 1], rr[sub][j + 2], rr[sub][j + 3]));
+                        }
+                        continue;
+                    }
+                    for (int c = sk_c0; c < sk_c0 + sk_nc; ++c) {  // owner: add in CTA order
+                        const uint32_t* src = p.sk_ws + static_cast<size_t>(c) * BM * BN + row_l * 4;
+#pragma unroll
+                        for (int sub = 0; sub < 2; ++sub) {
+                            if (sub >= nsub) break;
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                const uint4 v =
+                                    __ldcg(reinterpret_cast<const uint4*>(src + ((c0 + 32 * sub + j) >> 2) * (BM * 4)));
+                                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    if constexpr (kI8 && !kF8)
+                                        rr[sub][j + e] = static_cast<uint32_t>(static_cast<int>(rr[sub][j + e]) +
+                                                                               static_cast<int>(w4[e]));
+                                    else
+                                        rr[sub][j + e] = __float_as_uint(__fadd_rn(bits_f(rr[sub][j + e]), bits_f(w4[e])));
+                                }
+                            }
+                        }
+                    }
+                }
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     if (sub >= nsub) break;
@@ -851,6 +962,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+            }
+            if (kSK && role == kUnitContrib) {  // publish this CTA's partial of tile t
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+                if (et == 0) atomicAdd(p.sk_flags + t, 1);
             }
             if (warp == kEpiWarp0 && lane == 0) QSB_TRACE_U(u, 5);
             ptx::tc_fence_before();
@@ -1028,6 +1144,49 @@ int g_debug_epi = 0;     // bench hook (qsync_gemm_debug_epilogue)
 int g_pdl = 1;           // programmatic dependent launch (qsync_gemm_set_pdl)
 int g_max_ctas = 0;      // cap on the persistent grid (qsync_gemm_set_max_ctas), 0 = all SMs
 int g_conv_tma = 1;      // implicit conv operand loads: 1 = TMA im2col, 0 = cp.async gather lanes
+// Stream-K (qsync_gemm_set_streamk): -1 = never (default), 0 = cost model,
+// 1 = wherever eligible.  Off by default: graph-timed at every BERT step shape
+// it lost to the tile schedule -- accumulating dgrad / wgrad 18.6 vs 16.8 us
+// (QKV dgrad), 13.3 vs 9.7 (O wgrad), 21.8 vs 18.7 (FF2 wgrad); with a plain
+// output the partial-tile fixup made it 2-3x slower (tools/acc_sweep.py,
+// tools/gemm_overhead.py --streamk).  The 256-wide tiles it needs run the
+// MN-major B operand at ~86% of their MMA rate and each CTA's range crosses
+// tile boundaries, each crossing a pipeline drain + an accumulator switch.
+int g_streamk = -1;
+
+// Stream-K scratch, one per (device, stream) and never freed (a captured graph
+// keeps pointing at it): partial accumulators of at most one unit per CTA
+// ([CTAs][128][256] 32-bit) + one arrival counter per tile (zeroed once; the
+// tile's owner resets it).  Allocated on first use outside a graph capture; a
+// GEMM captured on a stream that has none keeps the tile schedule.
+constexpr int kSkMaxTiles = 1 << 16;
+struct SkWorkspace {
+    uint32_t* ws = nullptr;
+    int* flags = nullptr;
+};
+int sk_workspace(cudaStream_t st, SkWorkspace& out) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, SkWorkspace> table;
+    int dev = 0;
+    QSB_TRY(cuda_status(cudaGetDevice(&dev), "cudaGetDevice"));
+    std::lock_guard<std::mutex> lock(mu);
+    SkWorkspace& w = table[{dev, st}];
+    if (!w.ws) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        QSB_TRY(cuda_status(cudaStreamIsCapturing(st, &cap), "cudaStreamIsCapturing"));
+        if (cap != cudaStreamCaptureStatusNone) {
+            out = SkWorkspace{};
+            return QSYNC_OK;
+        }
+        const size_t bytes = static_cast<size_t>(sm_count()) * BM * 256 * 4;
+        QSB_TRY(cuda_status(cudaMalloc(reinterpret_cast<void**>(&w.ws), bytes), "cudaMalloc(stream-K partials)"));
+        QSB_TRY(cuda_status(cudaMalloc(reinterpret_cast<void**>(&w.flags), sizeof(int) * kSkMaxTiles),
+                            "cudaMalloc(stream-K flags)"));
+        QSB_TRY(cuda_status(cudaMemsetAsync(w.flags, 0, sizeof(int) * kSkMaxTiles, st), "cudaMemsetAsync"));
+    }
+    out = w;
+    return QSYNC_OK;
+}
 
 template <bool kI8, int BN, int kCta, int kLay>
 int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cudaStream_t st) {
@@ -1107,7 +1266,21 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
             p.ksplit = static_cast<int>((num_kb + per - 1) / per);
         }
     }
-    const int64_t units = tiles * p.ksplit;
+    if (!(kLay & 1024)) p.streamk = 0;
+    if (p.streamk) {
+        SkWorkspace w;
+        QSB_TRY(sk_workspace(st, w));
+        if (kCta != 1 || g_max_ctas > 0 || tiles > kSkMaxTiles || (!p.accumulate && !w.ws) || BN > 256 ||
+            (p.accumulate && !p.tma_store)) {
+            p.streamk = 0;
+        } else {
+            p.sk_ws = w.ws;
+            p.sk_flags = w.flags;
+            p.ksplit = 1;
+            p.kb_per = static_cast<int>(num_kb);
+        }
+    }
+    const int64_t units = p.streamk ? std::min<int64_t>(tiles * num_kb, slots) : tiles * p.ksplit;
     int64_t cap = slots;
     if (g_max_ctas > 0) cap = std::max<int64_t>(1, std::min<int64_t>(slots, g_max_ctas / kCta));
     const int grid = static_cast<int>(std::min<int64_t>(units, cap)) * kCta;
@@ -1193,8 +1366,13 @@ AccChoice choose_acc(int64_t M, int64_t N, int64_t num_kb) {
     double best_cost = 1e300;
     for (int bn : {256, 192, 128}) {
         const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+#ifdef QSB_ACC_MODEL_R1
+        const double kb_cost = std::max(4.0 * BM * bn / 256.0, (BM + bn) * 128.0 / 64.0);
+        const double fixed = 1500.0 + 8.0 * bn;
+#else
         const double kb_cost = bn >= 256 ? 600.0 : 520.0;
         const double fixed = 6000.0;
+#endif
         for (int ks = 1; ks <= 16; ++ks) {
             const int64_t per = (num_kb + ks - 1) / ks;
             if (ks > 1 && per < 4) break;
@@ -1252,10 +1430,54 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     }
     if (force_bn) sh.bn = force_bn;
     if (g_force_cta) sh.cta = g_force_cta;
+    // Stream-K candidate (plain operand layouts): 256-wide single-CTA tiles --
+    // the only width at which tcgen05.mma runs at its rate (116-cycle floor per
+    // instruction below it) -- with the tiles x k-blocks space spread evenly over
+    // all SMs, so N = 768 GEMMs (96 such tiles at M = 4096) use the whole chip.
+    // Costs in cycles per k-block as choose_acc, + a partial write/read fixup.
+    const bool sk_layout = layout == 0 || layout == 2 || layout == 3;
+    // The cost model only takes accumulating FP32 outputs, where every unit
+    // reduce-adds its partial.  With a plain output the fixup (a 128 KB partial
+    // tile written, then read back by the tile's owner) cost more than the even
+    // split saved at every step shape (tools/gemm_overhead.py --streamk 1: O
+    // 8.3 -> 22 us, FF2 19.5 -> 30 us); qsync_gemm_set_streamk(1) still forces
+    // it (tested bit-exact for INT8).
+    const bool sk_acc = p.c != nullptr && p.c_i32 == nullptr && p.accumulate && !kI8 && p.c_dtype == QSYNC_F32;
+    const bool sk_plain = p.c != nullptr && p.c_i32 == nullptr && !p.accumulate;
+    const bool sk_out = g_streamk == 1 ? (sk_acc || sk_plain) : sk_acc;
+    if (g_streamk >= 0 && sk_layout && sk_out && !force_bn && !g_force_cta && g_force_splitk == 0 &&
+        g_max_ctas == 0) {
+        const int sms = sm_count();
+        const int64_t bk = kI8 ? BK_BYTES : BK_BYTES / 2;
+        const int64_t kb = (p.K + bk - 1) / bk;
+        const int64_t mt = (p.M + BM - 1) / BM;
+        const double kb256 = (layout & 2) ? 600.0 : 560.0;
+        const double sk_cost = static_cast<double>((mt * ((p.N + 255) / 256) * kb + sms - 1) / sms) * kb256 +
+                               (p.accumulate ? 0.0 : 3000.0) + 6000.0;
+        const int64_t ks = std::max(1, p.ksplit);
+        const int64_t units = ((p.M + BM * sh.cta - 1) / (BM * sh.cta)) * ((p.N + sh.bn - 1) / sh.bn) * ks;
+        const int64_t slots = sms / sh.cta;
+        const double kbc = sh.bn >= 256 ? (sh.cta == 2 ? 540.0 : kb256) : 520.0;
+        const double cl_cost =
+            static_cast<double>((units + slots - 1) / slots) * (static_cast<double>((kb + ks - 1) / ks) * kbc + 6000.0);
+        if (g_streamk == 1 || sk_cost < 0.9 * cl_cost) {
+            sh = Shape{256, 1};
+            p.streamk = 1;
+            p.ksplit = 0;
+        }
+    }
     // pairs: BN/2 a multiple of 64, or 96 with a K-major B
     if (sh.cta == 2 && (sh.bn == 64 || (sh.bn == 192 && (layout & 2)))) sh.cta = 1;
     p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout, p.fp8);
     p.debug_epi = g_debug_epi;
+    if (p.streamk && !p.fp8) {  // the stream-K instantiations (kLay bit 10)
+        if (layout == 0) return launch<kI8, 256, 1, 1024>(a, b, dt, p, st);
+        if constexpr (!kI8) {
+            if (layout == 2) return launch<false, 256, 1, 1026>(a, b, dt, p, st);
+            if (layout == 3) return launch<false, 256, 1, 1027>(a, b, dt, p, st);
+        }
+    }
+    p.streamk = 0;
     if (layout & 108) {  // implicit conv (fwd 4/32, dgrad 22/50, wgrad 11/67): single-CTA tiles
         sh.cta = 1;
         if (sh.bn == 192) sh.bn = 256;  // (no 192-wide conv instantiations)
@@ -1456,6 +1678,12 @@ int qsync_gemm_set_pdl(int on) {
 
 int qsync_gemm_debug_epilogue(int v) {
     g_debug_epi = v;
+    return QSYNC_OK;
+}
+
+int qsync_gemm_set_streamk(int mode) {
+    QSB_REQUIRE(mode >= -1 && mode <= 1, QSYNC_ERR_DOMAIN, "stream-K mode must be -1 (never), 0 (cost model) or 1");
+    g_streamk = mode;
     return QSYNC_OK;
 }
 

@@ -38,6 +38,11 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+    return v;
+}
 // Spin with a watchdog: a protocol bug traps (a launch error the host sees)
 // instead of hanging the GPU.  ~2^31 polls is tens of seconds.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -726,6 +726,13 @@ def force_splitk(ks: int) -> None:
     call("qsync_gemm_force_splitk", int(ks))
 
 
+def set_streamk(mode: int) -> None:
+    """Stream-K scheduling of the plain GEMMs: -1 = never (the tile schedule,
+    default: measured faster at the step shapes), 0 = cost model, 1 = wherever
+    eligible."""
+    call("qsync_gemm_set_streamk", int(mode))
+
+
 def force_cta(cta: int) -> None:
     """Test hook: 1 = single-CTA tiles, 2 = CTA-pair (cta_group::2) tiles, 0 = cost model."""
     call("qsync_gemm_force_cta", int(cta))

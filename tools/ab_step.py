@@ -78,7 +78,8 @@ def main():
                 env = dict(os.environ)
                 if v != "default":
                     env["QSYNC_B200_LIB"] = os.path.abspath(v)
-                r = subprocess.run([sys.executable, __file__, "--one=plan:mixed"], env=env, capture_output=True,
+                plan = os.environ.get("QSB_AB_PLAN", "mixed")
+                r = subprocess.run([sys.executable, __file__, f"--one=plan:{plan}"], env=env, capture_output=True,
                                    text=True)
                 ms = float(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else float("nan")
             else:

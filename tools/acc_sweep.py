@@ -27,7 +27,13 @@ def main():
         b = torch.randn((K, N) if bmn else (N, K), device="cuda").half()
         out = torch.zeros(M, N, device="cuda")
         fn = lambda: ops.gemm_f16(a, b, out=out, accumulate=True, a_mn=amn, b_mn=bmn)  # noqa: E731
+        ops.set_streamk(-1)
         res = {"model": graph_time_us(fn)}
+        ops.set_streamk(1)
+        res["streamk"] = graph_time_us(fn)
+        ops.set_streamk(0)
+        res["model+sk"] = graph_time_us(fn)
+        ops.set_streamk(-1)
         for bn in (128, 192, 256):
             for ks in (1, 2, 3, 4, 6):
                 ops.force_tile_n(bn)
@@ -35,9 +41,11 @@ def main():
                 res[f"{bn}/{ks}"] = graph_time_us(fn)
         ops.force_tile_n(0)
         ops.force_splitk(0)
+        ops.set_streamk(-1)
         best = min(res, key=res.get)
-        print(f"{name:10s} model {res['model']:6.1f} us | best {best} {res[best]:6.1f} | " +
-              " ".join(f"{k}:{v:.1f}" for k, v in res.items() if k != "model"), flush=True)
+        print(f"{name:10s} tiles {res['model']:6.1f} sk {res['streamk']:6.1f} model+sk {res['model+sk']:6.1f} us"
+              f" | best {best} {res[best]:6.1f} | " +
+              " ".join(f"{k}:{v:.1f}" for k, v in res.items() if "/" in k), flush=True)
 
 
 if __name__ == "__main__":

@@ -67,6 +67,8 @@ def cases():
     yield "big  s8  8192^3", *s8(8192, 8192, 8192)
     yield "tiny f16 128x256x64", *f16(128, 256, 64)
     yield "tiny f16 128x256x768", *f16(128, 256, 768)
+    for nm, (M, N, K) in {"qkv": (T, H, 3 * H), "ff1": (T, H, F)}.items():
+        yield f"dgac f16 {nm}", *f16(M, N, K, lay=2, acc=True)
     for nm, (M, N, K) in {"qkv": (T, 3 * H, H), "o": (T, H, H), "ff1": (T, F, H), "ff2": (T, H, F)}.items():
         yield f"fwd  f16 {nm}", *f16(M, N, K)
         yield f"fwd  s8  {nm}", *s8(M, N, K)
@@ -79,7 +81,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bn", type=int, default=0, help="force the tile width (0 = cost model)")
     ap.add_argument("--only", default="", help="substring filter on the case name")
+    ap.add_argument("--streamk", type=int, default=-1, help="-1 never (default), 0 cost model, 1 always")
     args = ap.parse_args()
+    ops.set_streamk(args.streamk)
     _lib.call("qsync_gemm_force_tile_n", args.bn)
     print(f"{'case':22s} {'GFLOP':>7s} {'ideal':>7s} {'us':>7s} {'noepi':>7s} {'nopdl':>7s} {'cublas':>7s}  TF/s  (bn={args.bn})")
     for name, fn, flops, ref in cases():

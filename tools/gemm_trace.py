@@ -94,8 +94,10 @@ def main():
     ap.add_argument("--modes", default="0", help="comma list of isolation modes (trace build): 0 full, "
                     "1 no epilogue math/stores, 2 MMA only (no loads), 4 loads only (no MMAs, single CTA)")
     ap.add_argument("--only", default="")
+    ap.add_argument("--streamk", type=int, default=-1, help="-1 never (default), 0 cost model, 1 always")
     ap.add_argument("--variants", default="0:0", help="comma list of cta:tile_n overrides, e.g. 0:0,2:256,2:128")
     args = ap.parse_args()
+    ops.set_streamk(args.streamk)
     buf = torch.zeros(1024 * 72, dtype=torch.int64, device="cuda")
     out = {}
     variants = [tuple(int(x) for x in v.split(":")) for v in args.variants.split(",")]
