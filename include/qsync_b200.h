@@ -386,6 +386,25 @@ int qsync_gemm_gelu(const void* a, const void* b, int ab_dtype, int64_t m, int64
                     const float* scale_a, const float* scale_b, int b_per_channel, const float* bias, void* g,
                     int g_dtype, uint16_t* dact, float* absmax, qsync_stream_t stream);
 
+/* The classification head around the encoder stack (FP32 ops; train_step.py:
+ * pooler = tanh(x[:, 0] Wp^T + bp), logits = pooled Wc^T + bc, loss = mean
+ * cross entropy), so the graphed step launches only this library's kernels.
+ * x [B, S, H] FP32; Wp [H, H], Wc [C, H]; labels [B] int64.  Forward writes
+ * pooled [B, H], probs [B, C] (softmax, kept for the backward) and *loss.
+ * Backward (dloss a device scalar) ADDS into dwp / dbp / dwc / dbc (the flat
+ * FP32 gradient buffer), uses dpre [B, H] as scratch and writes all of
+ * dx [B, S, H] (zero except token 0).  Deterministic (fixed reduction order). */
+int qsync_cls_head_fwd(const float* x, int64_t B, int64_t S, int64_t H, const float* wp, const float* bp,
+                       const float* wc, const float* bc, int64_t C, const int64_t* labels, float* pooled,
+                       float* probs, float* loss, qsync_stream_t stream);
+int qsync_cls_head_bwd(const float* x, int64_t B, int64_t S, int64_t H, const float* wp, const float* wc, int64_t C,
+                       const int64_t* labels, const float* pooled, const float* probs, const float* dloss,
+                       float* dwp, float* dbp, float* dwc, float* dbc, float* dpre, float* dx,
+                       qsync_stream_t stream);
+/* Zero `bytes` bytes (16-byte vector stores when aligned), as a PDL kernel: the
+ * per-step gradient-buffer reset inside the graphed step. */
+int qsync_zero(void* p, int64_t bytes, qsync_stream_t stream);
+
 /* Attention core softmax(Q K^T scale) V of an encoder layer (stays
  * floating point), in the planned projections' formats: qkv packed
  * [B, S, 3, H, D] FP16 (the QKV projection's output), out [B, S, H, D] FP16,

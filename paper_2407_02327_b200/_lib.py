@@ -79,6 +79,9 @@ SIGNATURES = {
     "qsync_act_bwd_colsum": [_p, _int, _p, _int, _i64, _i64, _int, _p, _int, _p, _p],
     "qsync_gemm_s8_ex": [_p, _p, _i64, _i64, _i64, _p, _int, _p, _p, _int, _p, _p],
     "qsync_gemm_gelu": [_p, _p, _int, _i64, _i64, _i64, _p, _p, _int, _p, _p, _int, _p, _p, _p],
+    "qsync_cls_head_fwd": [_p, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p],
+    "qsync_cls_head_bwd": [_p, _i64, _i64, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
+    "qsync_zero": [_p, _i64, _p],
     "qsync_adamw_step": [_p, _int, _p, _i64, _p, _f32, _f32, _f32, _f32, _f32, _int, _p],
     "qsync_adamw_step_range": [_p, _int, _p, _i64, _i64, _p, _f32, _f32, _f32, _f32, _f32, _int, _p],
     "qsync_adamw_advance": [_p, _p],

@@ -65,6 +65,41 @@ def gelu(x: torch.Tensor) -> torch.Tensor:
     return _Gelu.apply(x)
 
 
+class _ClsHead(torch.autograd.Function):
+    """Pooler (tanh) + classifier + mean cross entropy on this package's
+    kernels (csrc/head.cu).  The weight gradients are ADDED into each
+    parameter's ``main_grad`` when it has one (the flat buffer), and reported
+    final through qlinear.GRAD_READY as the fused layers do."""
+
+    @staticmethod
+    def forward(ctx, x, wp, bp, wc, bc, labels):
+        x = x.contiguous()
+        loss, pooled, probs = ops.cls_head_fwd(x, wp, bp, wc, bc, labels)
+        ctx.save_for_backward(x, pooled, probs, labels)
+        ctx.params = (wp, bp, wc, bc)
+        return loss.reshape(())
+
+    @staticmethod
+    def backward(ctx, dloss):
+        from . import qlinear as _ql
+        from .fused import _mark
+        _mark("bwd", "loss")
+        x, pooled, probs, labels = ctx.saved_tensors
+        params = ctx.params
+        outs = [getattr(p, "main_grad", None) for p in params]
+        bufs = [o if o is not None else torch.zeros_like(p) for o, p in zip(outs, params)]
+        wp, _, wc, _ = params
+        dx = ops.cls_head_bwd(x, wp, wc, labels, pooled, probs, dloss.reshape(1).contiguous(), *bufs)
+        if _ql.GRAD_READY is not None:
+            _ql.GRAD_READY([p for p, o in zip(params, outs) if o is not None])
+        return (dx,) + tuple(None if o is not None else b for o, b in zip(outs, bufs)) + (None,)
+
+
+def cls_head(x: torch.Tensor, pooler, cls, labels: torch.Tensor) -> torch.Tensor:
+    """Mean cross-entropy loss of cls(tanh(pooler(x[:, 0]))) -- FP32 pooler."""
+    return _ClsHead.apply(x, pooler.weight, pooler.bias, cls.weight, cls.bias, labels)
+
+
 class AddLayerNorm(torch.nn.Module):
     """y = LayerNorm(a + b) with FP32 statistics; b may be FP32 or FP16."""
 

@@ -601,6 +601,37 @@ def gemm_gelu(a: torch.Tensor, b: torch.Tensor, scale_a=None, scale_b=None, bias
     return am, g, d
 
 
+def zero_(t: torch.Tensor) -> torch.Tensor:
+    """t.zero_() on this library's kernel (16-byte stores)."""
+    if t.numel():
+        call("qsync_zero", _ptr(t), t.numel() * t.element_size(), _stream())
+    return t
+
+
+def cls_head_fwd(x: torch.Tensor, wp, bp, wc, bc, labels):
+    """(loss[1], pooled [B, H], probs [B, C]) of the pooler + classifier + mean CE
+    on x [B, S, H] FP32 (qsync_cls_head_fwd)."""
+    _req(x, "x", (torch.float32,))
+    B, S, H = x.shape
+    C = wc.shape[0]
+    pooled = torch.empty((B, H), device=x.device, dtype=torch.float32)
+    probs = torch.empty((B, C), device=x.device, dtype=torch.float32)
+    loss = torch.empty(1, device=x.device, dtype=torch.float32)
+    call("qsync_cls_head_fwd", _ptr(x), B, S, H, _ptr(wp), _ptr(bp), _ptr(wc), _ptr(bc), C, _ptr(labels),
+         _ptr(pooled), _ptr(probs), _ptr(loss), _stream())
+    return loss, pooled, probs
+
+
+def cls_head_bwd(x, wp, wc, labels, pooled, probs, dloss, dwp, dbp, dwc, dbc):
+    """dx [B, S, H]; ADDS the weight / bias gradients into dwp, dbp, dwc, dbc."""
+    B, S, H = x.shape
+    dpre = torch.empty((B, H), device=x.device, dtype=torch.float32)
+    dx = torch.empty_like(x)
+    call("qsync_cls_head_bwd", _ptr(x), B, S, H, _ptr(wp), _ptr(wc), wc.shape[0], _ptr(labels), _ptr(pooled),
+         _ptr(probs), _ptr(dloss), _ptr(dwp), _ptr(dbp), _ptr(dwc), _ptr(dbc), _ptr(dpre), _ptr(dx), _stream())
+    return dx
+
+
 def embed_layernorm_fwd(tokens, word, pos, typ, gamma, beta, eps: float, want_f16: bool = False,
                         want_absmax: bool = False):
     """y = LN(word[tok] + pos[s] + typ[0]) for tokens [B, S] (int64).

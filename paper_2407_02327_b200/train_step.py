@@ -123,6 +123,10 @@ def _fusable(layer: EncoderLayer) -> bool:
     return all(m.precision in (INT8, FP16, FP32) for m in (layer.qkv, layer.o, layer.ff1, layer.ff2))
 
 
+# Fused path: pooler + classifier + CE on csrc/head.cu (A/B: tools/ab_step.py head=1,0).
+HEAD_KERNELS = True
+
+
 class BertEncoderStack(torch.nn.Module):
     """BERT-base: embeddings + 12 encoder layers + pooler + classifier."""
 
@@ -174,6 +178,13 @@ class BertEncoderStack(torch.nn.Module):
                 x = layer(x)
         if self.fused:
             from .fused import _mark
+            if HEAD_KERNELS and self.pooler.precision == FP32 and x.dtype == torch.float32 and x.is_cuda:
+                # pooler + classifier + CE on the library's head kernels (csrc/head.cu);
+                # profiling charges the head to "loss" (the pooler op is costed from
+                # its own kernels, profiler.measure_linear)
+                from .glue import cls_head
+                _mark("fwd", "loss")
+                return cls_head(x, self.pooler, self.cls, labels)
             _mark("fwd", "pooler")
         pooled = torch.tanh(cast(self.pooler(x[:, 0].contiguous()), torch.float32))
         if self.fused:
@@ -260,7 +271,11 @@ class FlatGrads:
         self._slot_events: list[tuple] = []
 
     def zero(self) -> None:
-        self.flat.zero_()
+        if self.flat.is_cuda:
+            from . import ops
+            ops.zero_(self.flat)  # the library's PDL kernel, not a framework memset
+        else:  # host-logic tests (gloo, world 2, CPU)
+            self.flat.zero_()
 
     # ---- overlapped, in-order bucket all-reduce (Eq. 6 slots, replayer.cpp:48-62)
     def begin(self, world: int, side_stream=None, on_final=None) -> None:

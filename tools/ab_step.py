@@ -12,6 +12,7 @@ repetitions shows.
     python tools/ab_step.py lib=default,/tmp/x.so library build (fresh process each)
     python tools/ab_step.py ff1gelu=1,0           GELU in FF1's GEMM epilogue vs the operand kernel
     python tools/ab_step.py ff2recompute=1,0      INT8 FF2 operand: GELU twice vs stored GELU(h)
+    python tools/ab_step.py head=1,0              classification head on csrc/head.cu vs torch
     QSB_AB_PLAN=int8 python tools/ab_step.py ...  plan for the non-plan knobs (default mixed)
 """
 import os
@@ -34,7 +35,9 @@ def step_ms(knob: str, val: str, steps: int = 40) -> float:
     m = BertEncoderStack(cfg).cuda()
     plan = val if knob == "plan" else os.environ.get("QSB_AB_PLAN", "mixed")
     fused.FF1_GELU_EPILOGUE = knob == "ff1gelu" and val == "1"
-    fused.FF2_INT8_RECOMPUTE = not (knob == "ff2recompute" and val == "0")
+    fused.FF2_INT8_RECOMPUTE = knob == "ff2recompute" and val == "1"
+    import paper_2407_02327_b200.train_step as _ts
+    _ts.HEAD_KERNELS = not (knob == "head" and val == "0")
     m.apply_plan({"mixed": mixed_plan(cfg), "int8": uniform_plan(cfg, INT8), "fp16": uniform_plan(cfg, FP16)}[plan])
     kw = {}
     if knob == "overlap":
