@@ -400,6 +400,8 @@ class TrainStep:
         dev = next(model.parameters()).device
         self.tokens = torch.zeros((batch, cfg.seq), dtype=torch.long, device=dev)
         self.labels = torch.zeros((batch,), dtype=torch.long, device=dev)
+        # d(loss)/d(loss) = 1, allocated once: backward() would fill a new one per step
+        self._one = torch.ones((), dtype=torch.float32, device=dev)
         self.params = [p for p in model.parameters() if p.requires_grad]
         self.grads = FlatGrads(self.params)
         # C1: the gradient buckets go through this library's NCCL entry points
@@ -472,7 +474,7 @@ class TrainStep:
                          on_final=self._opt_bucket if self.overlap_opt else None)
         _ql.GRAD_READY = self.grads.params_ready if self._hooked else None
         try:
-            loss.backward()
+            loss.backward(self._one)
         finally:
             _ql.WGRAD_STREAM = None
             _ql.GRAD_READY = None
