@@ -42,7 +42,10 @@ def flush_l2():
 
 
 def time_ms(fn, iters=20, warmup=3, flush=False) -> float:
-    """Mean device time of fn() over iters (flushing L2 before each if asked)."""
+    """Mean device time of fn() over iters (flushing L2 before each if asked).
+    The stream is held behind a ~100 us device spin while the host enqueues
+    the start event, fn's launches and the end event, so the events bracket
+    the kernels only -- not the host launch latency of the ctypes calls."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -51,6 +54,7 @@ def time_ms(fn, iters=20, warmup=3, flush=False) -> float:
         if flush:
             flush_l2()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200_000)
         s.record()
         fn()
         e.record()
