@@ -413,6 +413,13 @@ int qsync_zero(void* p, int64_t bytes, qsync_stream_t stream);
  * Backward: dqkv packed like qkv from dout [B, S, H, D].  S = 128, D = 64. */
 int qsync_attention_fwd(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t D, float scale, void* out,
                         float* lse, float* out_absmax, qsync_stream_t stream);
+/* Attention forward for an INT8 O projection: also quantizes out per tensor --
+ * q [B, S, H, D] int8, q16 (optional) = FP16 of the grid values (the wgrad
+ * operand), qscale[0] = scale, qscale[1] = absmax(out).  One kernel (a grid
+ * barrier over the co-resident (batch, head) blocks) when they all fit, else
+ * qsync_attention_fwd + qsync_quantize_act_ex; the same bits either way. */
+int qsync_attention_fwd_quant(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t D, float scale, void* out,
+                              float* lse, int8_t* q, uint16_t* q16, float* qscale, qsync_stream_t stream);
 int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, int64_t B,
                         int64_t S, int64_t H, int64_t D, float scale, void* dqkv, qsync_stream_t stream);
 

@@ -9,14 +9,17 @@
 //
 // Sequence length 128, head dim 64 (BERT-base): one CTA owns one (batch, head),
 // the whole sequence fits on chip, so there is no online softmax and no
-// atomics.  8 warps; the tensor-core work is mma.sync m16n8k16 (FP16 x FP16 ->
-// FP32) on ldmatrix fragments of 128B-row tiles whose 16-byte chunks are
-// XOR-swizzled by row (conflict-free ldmatrix).  Forward: warp w owns query
-// rows 16w..16w+15.  Backward: phase 1 warp w owns key rows 16w.. and computes
-// S^T, P^T, dP^T, dS^T for all queries, accumulating dV = P^T dO and
-// dK = dS^T Q; dS^T goes to shared memory; phase 2 warp w owns query rows and
-// computes dQ = dS K.  HBM traffic per (b, h): fwd 3 x 16 KB in, 16 KB out;
-// bwd 5 x 16 KB in (Q, K, V, O, dO), 48 KB out.
+// atomics.  Three implementations (qsync_attention_set_impl):
+//   impl 2 (default): tcgen05 -- TMA-loaded Q/K/V, S and O accumulated in TMEM,
+//     thread-per-row softmax, P written in the K-major UMMA layout; the backward
+//     (k_attn_bwd_tc2) runs five UMMA GEMMs at 2 CTAs/SM with P^T kept in TMEM;
+//   impl 1: the same forward, a 1-CTA/SM tcgen05 backward (k_attn_bwd_tc);
+//   impl 0: the first version, mma.sync m16n8k16 on ldmatrix fragments of
+//     XOR-swizzled 128B-row tiles (8 warps; forward warp w owns query rows
+//     16w..; backward phase 1 per key rows -> dV, dK, dS^T in smem; phase 2 per
+//     query rows -> dQ), kept selectable for A/B and tested like the others.
+// HBM traffic per (b, h): fwd 3 x 16 KB in, 16 KB out; bwd 5 x 16 KB in
+// (Q, K, V, O, dO), 48 KB out.
 #include <algorithm>
 
 #include "common.cuh"
@@ -395,11 +398,48 @@ __device__ __forceinline__ uint32_t idesc_f16_f32(int n, int m, bool b_mn) {
     return d;
 }
 
+// kQ: the O projection is INT8 -- the forward also quantizes O per tensor (its
+// INT8 operand + the FP16 copy of the grid values for its wgrad): per-block
+// absmax partials, a grid barrier over the co-resident (batch, head) blocks,
+// then each thread quantizes the O row it still holds in registers.  Same q,
+// q16 and scale as qsync_attention_fwd + qsync_quantize_act_ex.
+constexpr int kAttQSlots = 32;
+constexpr int kAttQMaxBlocks = 4096;
+__device__ float g_attq_part[kAttQSlots][kAttQMaxBlocks];
+__device__ unsigned g_attq_bar[kAttQSlots][2];  // [0] arrivals, [1] generation
+
+__device__ __forceinline__ void attq_grid_barrier(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g0 = *gen;  // cannot move before every block has arrived
+        __threadfence();           // this block's partial before its arrival
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <bool kQ>
 __global__ void __launch_bounds__(kTcThreads) k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, int H,
                                                             float scale, __half* __restrict__ out,
                                                             float* __restrict__ lse,
-                                                            unsigned* __restrict__ out_absmax) {
-    QSB_PDL_ENTER();
+                                                            unsigned* __restrict__ out_absmax, int8_t* __restrict__ q,
+                                                            uint16_t* __restrict__ q16, float* __restrict__ qs,
+                                                            int qslot) {
+    if constexpr (kQ) {
+        // dependents may launch only after the grid barrier: a dependent grid's
+        // blocks must not take the SMs this grid's unscheduled blocks still need
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    } else {
+        QSB_PDL_ENTER();
+    }
     extern __shared__ uint8_t sm_raw[];
     const uint32_t raw = ptx::smem_u32(sm_raw);
     uint8_t* sm = sm_raw + ((1024 - (raw & 1023)) & 1023);
@@ -501,7 +541,7 @@ __global__ void __launch_bounds__(kTcThreads) k_attn_fwd_tc(const __grid_constan
     for (int q = 0; q < 8; ++q)
         reinterpret_cast<uint4*>(orow)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
     lse[static_cast<int64_t>(bh) * kS + t] = mx * scale + logf(sum);
-    if (out_absmax) {
+    if (kQ || out_absmax) {
         float amax = 0.f;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -509,7 +549,61 @@ __global__ void __launch_bounds__(kTcThreads) k_attn_fwd_tc(const __grid_constan
             amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
         }
         amax = warp_max(amax);
-        if (lane == 0 && amax > 0.f) atomicMax(out_absmax, __float_as_uint(amax));
+        if constexpr (kQ) {
+            __shared__ float wmax[kTcThreads / 32];
+            __shared__ float s_abs;
+            if (lane == 0) wmax[warp] = amax;
+            __syncthreads();
+            if (t == 0) {
+                float m = 0.f;
+                for (int i = 0; i < kTcThreads / 32; ++i) m = fmaxf(m, wmax[i]);
+                g_attq_part[qslot][blockIdx.x] = m;
+            }
+            attq_grid_barrier(g_attq_bar[qslot], gridDim.x);
+            // every block reduces all partials (deterministic, nothing to zero)
+            float m = 0.f;
+            for (int i = t; i < static_cast<int>(gridDim.x); i += kTcThreads)
+                m = fmaxf(m, __ldcg(&g_attq_part[qslot][i]));
+            m = warp_max(m);
+            if (lane == 0) wmax[warp] = m;
+            __syncthreads();
+            if (t == 0) {
+                float a2 = 0.f;
+                for (int i = 0; i < kTcThreads / 32; ++i) a2 = fmaxf(a2, wmax[i]);
+                s_abs = a2;
+            }
+            __syncthreads();
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+            const float sc = scale_from_absmax(s_abs);
+            if (blockIdx.x == 0 && t == 0) {
+                qs[0] = sc;
+                qs[1] = s_abs;
+            }
+            const QScale qsc = make_qscale(sc);
+            const int64_t off = (static_cast<int64_t>(b * kS + t) * H + h) * kD;  // this thread's O row
+            uint32_t qw[16], hw[32];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&w[2 * j]));
+                const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&w[2 * j + 1]));
+                const float t0 = quant_rne_f(f0.x, qsc), t1 = quant_rne_f(f0.y, qsc);
+                const float t2 = quant_rne_f(f1.x, qsc), t3 = quant_rne_f(f1.y, qsc);
+                qw[j] = pack_q4(t0, t1, t2, t3);
+                hw[2 * j] = pack_half2(grid_value(t0), grid_value(t1));
+                hw[2 * j + 1] = pack_half2(grid_value(t2), grid_value(t3));
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                reinterpret_cast<uint4*>(q + off)[i] = make_uint4(qw[4 * i], qw[4 * i + 1], qw[4 * i + 2], qw[4 * i + 3]);
+            if (q16) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    reinterpret_cast<uint4*>(q16 + off)[i] =
+                        make_uint4(hw[4 * i], hw[4 * i + 1], hw[4 * i + 2], hw[4 * i + 3]);
+            }
+        } else {
+            if (lane == 0 && amax > 0.f) atomicMax(out_absmax, __float_as_uint(amax));
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -890,17 +984,56 @@ int qsync_attention_fwd(const void* qkv, int64_t B, int64_t S, int64_t H, int64_
     QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_fwd), kFwdSmem));
     if (out_absmax) QSB_TRY(zero_async(out_absmax, sizeof(float), st));
     if (g_attn_tc) {
-        QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_fwd_tc), kTcFwdSmem));
+        QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_fwd_tc<false>), kTcFwdSmem));
         CUtensorMap tm;
         QSB_TRY(make_tma_2d(&tm, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 3 * H * kD, B * kS, kD, kS));
-        pdl_launch(k_attn_fwd_tc, dim3(static_cast<unsigned>(B * H)), dim3(kTcThreads), kTcFwdSmem, st, tm,
-                   static_cast<int>(H), scale, static_cast<__half*>(out), lse, reinterpret_cast<unsigned*>(out_absmax));
+        pdl_launch(k_attn_fwd_tc<false>, dim3(static_cast<unsigned>(B * H)), dim3(kTcThreads), kTcFwdSmem, st, tm,
+                   static_cast<int>(H), scale, static_cast<__half*>(out), lse, reinterpret_cast<unsigned*>(out_absmax),
+                   static_cast<int8_t*>(nullptr), static_cast<uint16_t*>(nullptr), static_cast<float*>(nullptr), 0);
         return check_launch("k_attn_fwd_tc");
     }
     pdl_launch(k_attn_fwd, dim3(static_cast<unsigned>(B * H)), dim3(kThreadsA), kFwdSmem, st, 
         static_cast<const __half*>(qkv), static_cast<int>(H), scale, static_cast<__half*>(out), lse,
         reinterpret_cast<unsigned*>(out_absmax));
     return check_launch("k_attn_fwd");
+}
+
+int qsync_attention_fwd_quant(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t D, float scale, void* out,
+                              float* lse, int8_t* q, uint16_t* q16, float* qscale, qsync_stream_t stream) {
+    QSB_REQUIRE(qkv && out && lse && q && qscale, QSYNC_ERR_VALIDATION,
+                "attention + quantize needs qkv, out, lse, q and qscale (float[2]) buffers");
+    QSB_TRY(check_shape(B, S, H, D));
+    cudaStream_t st = to_stream(stream);
+    const int64_t blocks = B * H;
+    bool fused = g_attn_tc != 0 && blocks <= kAttQMaxBlocks;
+    if (fused) {
+        // every block must be co-resident for the grid barrier (TMEM: 128 columns each)
+        static int occ[16] = {0};
+        int dev = 0;
+        QSB_TRY(cuda_status(cudaGetDevice(&dev), "cudaGetDevice"));
+        QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_fwd_tc<true>), kTcFwdSmem));
+        if (dev < 16 && occ[dev] == 0) {
+            int n = 0;
+            QSB_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_attn_fwd_tc<true>, kTcThreads,
+                                                                              kTcFwdSmem),
+                                "cudaOccupancyMaxActiveBlocksPerMultiprocessor"));
+            occ[dev] = n > 0 ? std::min(n, 512 / 128) : -1;
+        }
+        const int per_sm = dev < 16 ? occ[dev] : 0;
+        fused = per_sm > 0 && blocks <= static_cast<int64_t>(per_sm) * sm_count();
+    }
+    if (!fused) {  // attention with absmax, then the one-pass quantizer: the same q, q16, scale
+        QSB_TRY(qsync_attention_fwd(qkv, B, S, H, D, scale, out, lse, qscale + 1, stream));
+        return qsync_quantize_act_ex(out, QSYNC_F16, B * S * H * D, QSYNC_ACT_NONE, qscale + 1, q, qscale, nullptr,
+                                     q16, stream);
+    }
+    CUtensorMap tm;
+    QSB_TRY(make_tma_2d(&tm, qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 3 * H * kD, B * kS, kD, kS));
+    const int slot = static_cast<int>((reinterpret_cast<uintptr_t>(st) >> 4) % kAttQSlots);
+    pdl_launch(k_attn_fwd_tc<true>, dim3(static_cast<unsigned>(blocks)), dim3(kTcThreads), kTcFwdSmem, st, tm,
+               static_cast<int>(H), scale, static_cast<__half*>(out), lse, static_cast<unsigned*>(nullptr), q, q16,
+               qscale, slot);
+    return check_launch("k_attn_fwd_tc<quant>");
 }
 
 int qsync_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, int64_t B,

@@ -237,6 +237,10 @@ def _linear_fwd(m, opnd, out_dtype=None):
     return y, w16
 
 
+# INT8 O projection: its operand quantized inside the attention kernel
+# (qsync_attention_fwd_quant) instead of a quantize_act pass over the output.
+ATTN_QUANT = True
+
 # INT8 FF2 operand from h: absmax(gelu(h)) then quantize(gelu(h)) with GELU'
 # (GELU evaluated twice, g never stored: 162 MB moved at [4096, 3072] FP32 h)
 # instead of gelu_absmax_store + a quantize of the stored g (212 MB).  Off:
@@ -353,11 +357,19 @@ class _FusedLayerFn(torch.autograd.Function):
         # Attention core (FP16, csrc/attn.cu); it also emits absmax(out) when the
         # O projection is INT8, so that op's quantizer is one pass.
         _mark("fwd", pre + ".attn")
-        a, lse, a_am = ops.attention_fwd(qkv5, scale, want_absmax=po == INT8)
-        a2 = a.reshape(M, H)
-        # --- output projection + residual LayerNorm (emits FF1's operand)
-        _mark("cast", L.o.name)
-        op_o = _operand(a2, a_am, po)
+        if po == INT8 and ATTN_QUANT:
+            # the attention kernel also quantizes its output for the INT8 O
+            # projection (grid barrier on absmax): no separate quantizer pass
+            a, lse, aq, as_, aq16 = ops.attention_fwd_quant(qkv5, scale)
+            a2 = a.reshape(M, H)
+            _mark("cast", L.o.name)
+            op_o = ("i8", aq, as_, aq16)
+        else:
+            a, lse, a_am = ops.attention_fwd(qkv5, scale, want_absmax=po == INT8)
+            a2 = a.reshape(M, H)
+            # --- output projection + residual LayerNorm (emits FF1's operand)
+            _mark("cast", L.o.name)
+            op_o = _operand(a2, a_am, po)
         _mark("fwd", L.o.name)
         yo, w16_o = _linear_fwd(L.o, op_o)
         f16, am = _need_aux(p1)

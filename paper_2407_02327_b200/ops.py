@@ -694,6 +694,23 @@ def attention_fwd(qkv: torch.Tensor, scale: float | None = None, want_absmax: bo
     return out, lse, am
 
 
+def attention_fwd_quant(qkv: torch.Tensor, scale: float | None = None, want_q16: bool = True):
+    """Attention core for an INT8 O projection: (out, lse, q [B*S, H*D] int8,
+    s[1] scale, q16 FP16 grid values or None) -- out / lse as attention_fwd, q /
+    s / q16 as quantize_act(out, absmax(out)), from one kernel when it fits."""
+    _req(qkv, "qkv", (torch.float16,))
+    B, S, _, H, D = qkv.shape
+    scale = D ** -0.5 if scale is None else scale
+    out = torch.empty((B, S, H, D), device=qkv.device, dtype=torch.float16)
+    lse = torch.empty((B, H, S), device=qkv.device, dtype=torch.float32)
+    q = torch.empty((B * S, H * D), device=qkv.device, dtype=torch.int8)
+    q16 = torch.empty((B * S, H * D), device=qkv.device, dtype=torch.float16) if want_q16 else None
+    qs = torch.empty(2, device=qkv.device, dtype=torch.float32)
+    call("qsync_attention_fwd_quant", _ptr(qkv), B, S, H, D, float(scale), _ptr(out), _ptr(lse), _ptr(q), _ptr(q16),
+         _ptr(qs), _stream())
+    return out, lse, q, qs[:1], q16
+
+
 def attention_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor,
                   scale: float | None = None) -> torch.Tensor:
     """dQKV (packed like qkv) of the attention core."""

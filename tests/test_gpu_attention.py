@@ -92,3 +92,20 @@ def test_attention_bwd_tmem_p_matches_smem_p():
         call("qsync_attention_set_impl", 2)
     d2 = ops.attention_bwd(qkv, out, dout, lse)
     assert _rel(d2, d1) < 1e-3
+
+
+@pytest.mark.parametrize("B,H", [(32, 12), (2, 3), (600, 12)])
+def test_attention_fwd_quant_bit_identical(B, H):
+    """qsync_attention_fwd_quant (one kernel with a grid barrier when the blocks
+    fit, B = 600 x 12 falls back) == attention_fwd + absmax + quantize_act."""
+    from paper_2407_02327_b200 import ops
+    torch.manual_seed(B)
+    qkv = (torch.randn(B, 128, 3, H, 64, device="cuda") * 0.5).half()
+    out, lse, q, s, q16 = ops.attention_fwd_quant(qkv)
+    out0, lse0, am = ops.attention_fwd(qkv, want_absmax=True)
+    q0, s0, h0 = ops.quantize_act(out0.view(B * 128, H * 64), am, want_q16=True)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out0) and torch.equal(lse, lse0)
+    assert torch.equal(q, q0) and torch.equal(s, s0) and torch.equal(q16, h0)
+    out2, _, q2, s2, _ = ops.attention_fwd_quant(qkv)  # barrier slot reuse
+    assert torch.equal(q2, q0) and torch.equal(s2, s0)

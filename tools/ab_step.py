@@ -13,6 +13,7 @@ repetitions shows.
     python tools/ab_step.py ff1gelu=1,0           GELU in FF1's GEMM epilogue vs the operand kernel
     python tools/ab_step.py ff2recompute=1,0      INT8 FF2 operand: GELU twice vs stored GELU(h)
     python tools/ab_step.py head=1,0              classification head on csrc/head.cu vs torch
+    python tools/ab_step.py attnq=1,0             INT8 O operand quantized in the attention kernel
     QSB_AB_PLAN=int8 python tools/ab_step.py ...  plan for the non-plan knobs (default mixed)
 """
 import os
@@ -38,6 +39,7 @@ def step_ms(knob: str, val: str, steps: int = 40) -> float:
     fused.FF2_INT8_RECOMPUTE = knob == "ff2recompute" and val == "1"
     import paper_2407_02327_b200.train_step as _ts
     _ts.HEAD_KERNELS = not (knob == "head" and val == "0")
+    fused.ATTN_QUANT = not (knob == "attnq" and val == "0")
     m.apply_plan({"mixed": mixed_plan(cfg), "int8": uniform_plan(cfg, INT8), "fp16": uniform_plan(cfg, FP16)}[plan])
     kw = {}
     if knob == "overlap":
