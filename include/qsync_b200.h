@@ -392,7 +392,7 @@ int qsync_gemm_gelu(const void* a, const void* b, int ab_dtype, int64_t m, int64
  * x [B, S, H] FP32; Wp [H, H], Wc [C, H]; labels [B] int64.  Forward writes
  * pooled [B, H], probs [B, C] (softmax, kept for the backward) and *loss.
  * Backward (dloss a device scalar) ADDS into dwp / dbp / dwc / dbc (the flat
- * FP32 gradient buffer), uses dpre [B, H] as scratch and writes all of
+ * FP32 gradient buffer), uses dpre [9 * B * H] floats as scratch and writes all of
  * dx [B, S, H] (zero except token 0).  Deterministic (fixed reduction order). */
 int qsync_cls_head_fwd(const float* x, int64_t B, int64_t S, int64_t H, const float* wp, const float* bp,
                        const float* wc, const float* bc, int64_t C, const int64_t* labels, float* pooled,

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(256) k_head_bwd_w(const float* __restrict__ x,
     }
     for (int h = threadIdx.x; h < H; h += blockDim.x) {
         float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 8
         for (int b = 0; b < B; ++b) {
             const float xv = x[b * SH + h];
 #pragma unroll
@@ -172,29 +173,56 @@ __global__ void __launch_bounds__(256) k_head_bwd_w(const float* __restrict__ x,
     }
 }
 
-// dx for sequences 8*blockIdx.y.. (+8): row 0 = dpre[b] Wp, rows 1..S-1 = 0;
-// each Wp element is read once per 8 sequences.
-__global__ void __launch_bounds__(256) k_head_dx(const float* __restrict__ dpre, int B, int S, int H,
-                                                 const float* __restrict__ wp, float* __restrict__ dx) {
+// dx row 0 = dpre Wp ([B, H] x [H, H]) in two deterministic steps: k_head_dx_part
+// splits the j range over blockIdx.z (kDxSplit parts) for parallelism -- block =
+// 256 columns h x 8 sequences, the 8 dpre rows of its j range staged in shared
+// memory, Wp rows read coalesced -- into part[split][b][h]; k_head_dx sums the
+// parts in split order and writes all of dx (rows 1..S-1 zero).  One block per
+// 8 sequences over the whole j range had left 12 blocks doing 768 serial loads.
+constexpr int kDxSplit = 8;
+__global__ void __launch_bounds__(256) k_head_dx_part(const float* __restrict__ dpre, int B, int H,
+                                                      const float* __restrict__ wp, float* __restrict__ part) {
     QSB_PDL_ENTER();
-    extern __shared__ float rows[];  // [8][H] = dpre[b0 .. b0+7, :]
+    __shared__ float rows[8][128];  // dpre[b0 .. b0+7, j0 .. j0+127]
     const int b0 = blockIdx.y * 8;
     const int nb = min(8, B - b0);
-    for (int i = threadIdx.x; i < nb * H; i += blockDim.x) rows[i] = dpre[static_cast<int64_t>(b0) * H + i];
-    __syncthreads();
+    const int per = (H + kDxSplit - 1) / kDxSplit;
+    const int ja = blockIdx.z * per, jb = min(H, ja + per);
+    const int h = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    for (int j0 = ja; j0 < jb; j0 += 128) {
+        const int nj = min(128, jb - j0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < 8 * 128; i += blockDim.x) {
+            const int bi = i / 128, jj = i % 128;
+            rows[bi][jj] = (bi < nb && jj < nj) ? dpre[static_cast<int64_t>(b0 + bi) * H + j0 + jj] : 0.0f;
+        }
+        __syncthreads();
+        if (h < H) {
+#pragma unroll 4
+            for (int jj = 0; jj < nj; ++jj) {
+                const float wv = wp[static_cast<int64_t>(j0 + jj) * H + h];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] = fmaf(rows[i][jj], wv, acc[i]);
+            }
+        }
+    }
+    if (h >= H) return;
+    for (int i = 0; i < nb; ++i) part[(static_cast<int64_t>(blockIdx.z) * B + b0 + i) * H + h] = acc[i];
+}
+
+__global__ void __launch_bounds__(256) k_head_dx(const float* __restrict__ part, int B, int S, int H,
+                                                 float* __restrict__ dx) {
+    QSB_PDL_ENTER();
+    const int b = blockIdx.y;
     const int h = blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= H) return;
-    float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-    for (int j = 0; j < H; ++j) {
-        const float wv = wp[static_cast<int64_t>(j) * H + h];
+    float s = 0.0f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fmaf(rows[i * H + j], wv, acc[i]);
-    }
-    for (int i = 0; i < nb; ++i) {
-        float* out = dx + static_cast<int64_t>(b0 + i) * S * H + h;
-        out[0] = acc[i];
-        for (int t = 1; t < S; ++t) out[static_cast<int64_t>(t) * H] = 0.0f;
-    }
+    for (int k = 0; k < kDxSplit; ++k) s += part[(static_cast<int64_t>(k) * B + b) * H + h];
+    float* out = dx + static_cast<int64_t>(b) * S * H + h;
+    out[0] = s;
+    for (int t = 1; t < S; ++t) out[static_cast<int64_t>(t) * H] = 0.0f;
 }
 
 // 16-byte stores over the aligned body, single bytes for the unaligned head
@@ -259,10 +287,12 @@ int qsync_cls_head_bwd(const float* x, int64_t B, int64_t S, int64_t H, const fl
                        sizeof(float) * B * C, st, pooled, Bi, Hi, wc, Ci, labels, probs, dloss, dwc, dbc, dpre));
     QSB_TRY(launch_pdl("k_head_bwd_w", k_head_bwd_w, dim3(static_cast<unsigned>((H + 7) / 8)), dim3(256),
                        sizeof(float) * B * 8, st, x, Bi, S * H, Hi, static_cast<const float*>(dpre), dwp, dbp));
-    QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_head_dx), kHeadSmemMax));
-    return launch_pdl("k_head_dx", k_head_dx,
-                      dim3(static_cast<unsigned>((H + 255) / 256), static_cast<unsigned>((B + 7) / 8)), dim3(256),
-                      sizeof(float) * 8 * H, st, static_cast<const float*>(dpre), Bi, static_cast<int>(S), Hi, wp, dx);
+    float* part = dpre + B * H;  // the scratch holds dpre [B, H] then the split partials [kDxSplit, B, H]
+    QSB_TRY(launch_pdl("k_head_dx_part", k_head_dx_part,
+                       dim3(static_cast<unsigned>((H + 255) / 256), static_cast<unsigned>((B + 7) / 8), kDxSplit),
+                       dim3(256), 0, st, static_cast<const float*>(dpre), Bi, Hi, wp, part));
+    return launch_pdl("k_head_dx", k_head_dx, dim3(static_cast<unsigned>((H + 255) / 256), static_cast<unsigned>(B)),
+                      dim3(256), 0, st, static_cast<const float*>(part), Bi, static_cast<int>(S), Hi, dx);
 }
 
 }  // extern "C"

@@ -625,7 +625,7 @@ def cls_head_fwd(x: torch.Tensor, wp, bp, wc, bc, labels):
 def cls_head_bwd(x, wp, wc, labels, pooled, probs, dloss, dwp, dbp, dwc, dbc):
     """dx [B, S, H]; ADDS the weight / bias gradients into dwp, dbp, dwc, dbc."""
     B, S, H = x.shape
-    dpre = torch.empty((B, H), device=x.device, dtype=torch.float32)
+    dpre = torch.empty((9, B, H), device=x.device, dtype=torch.float32)  # dpre + 8 split partials
     dx = torch.empty_like(x)
     call("qsync_cls_head_bwd", _ptr(x), B, S, H, _ptr(wp), _ptr(wc), wc.shape[0], _ptr(labels), _ptr(pooled),
          _ptr(probs), _ptr(dloss), _ptr(dwp), _ptr(dbp), _ptr(dwc), _ptr(dbc), _ptr(dpre), _ptr(dx), _stream())
