@@ -26,9 +26,10 @@ def _launch_rows(path):
 
 def launches(path, out):
     rows = _launch_rows(path)
-    # One step starts with the memset of the flat gradient buffer (the largest
-    # FillFunctor) and ends with the optimizer; take the last complete step.
-    fills = [i for i, (k, v) in enumerate(rows) if "FillFunctor" in k and v > 20e3]
+    # One step starts with the reset of the flat gradient buffer (k_zero16 of
+    # qsync_zero; a framework FillFunctor before round 2) and ends with the
+    # optimizer; take the last complete step.
+    fills = [i for i, (k, v) in enumerate(rows) if ("FillFunctor" in k or "k_zero16" in k) and v > 20e3]
     seg = rows
     for a, b in zip(fills[-2::-1], fills[:0:-1]):
         if any("multi_tensor_apply" in k or "k_adamw" in k for k, _ in rows[a:b]):
