@@ -114,6 +114,7 @@ SIGNATURES = {
     "qsync_gemm_force_splitk": [_int],
     "qsync_gemm_force_cta": [_int],
     "qsync_gemm_set_streamk": [_int],
+    "qsync_gemm_set_dual": [_int],
     "qsync_gemm_debug_epilogue": [_int],
     "qsync_gemm_set_pdl": [_int],
     "qsync_conv_set_impl": [_int],

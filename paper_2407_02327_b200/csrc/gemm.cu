@@ -206,6 +206,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr bool kGelu = (kLay & 512) != 0;
     // kLay bit 10: stream-K schedule (EpiParams::streamk; 256-wide single-CTA tiles)
     constexpr bool kSK = (kLay & 1024) != 0;
+    // kLay bit 11: two MMA issuers on ONE work unit per CTA, alternate k-blocks
+    // into the two accumulator buffers, summed by the epilogue.  One issuing
+    // thread cannot keep the tensor pipe busy below N = 256 (>= ~116 cycles
+    // per tcgen05.mma); two can (trace build, isolation mode 18: 2x the MMAs
+    // of a 192-wide tile in 1.63x the time, 128-wide in 1.2x).
+    constexpr bool kDual = (kLay & 2048) != 0;
+    static_assert(!kDual || (kCta == 1 && (kLay & 0x7fc) == 0), "dual issue: plain single-CTA tiles");
     static_assert(!kSK || (kCta == 1 && BN == 256 && (kLay & 0x3fc) == 0), "stream-K: plain 256-wide single-CTA");
     static_assert(!kGelu || (kCta == 1 && (kLay & 511) == 0), "GELU epilogue: single-CTA K-major tiles");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tfull[a], (kDual && a == 0) ? 2 : 1);  // dual: both issuers commit
             ptx::mbar_init(&tempty[a], kCta * kEpiWarps * 32);  // epilogue threads of both CTAs
         }
         ptx::fence_mbar_init();
@@ -290,6 +297,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Leader-CTA addresses of the barriers the pair shares.
     const uint32_t full_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : 0u;
     const uint32_t tempty_leader0 = kCta == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
+
+    // kDual: issuer `parity` takes the k-blocks kb0 + parity, kb0 + parity + 2, ...
+    // of the CTA's single unit into accumulator buffer `parity`, frees each
+    // stage it consumed and commits once to tfull[0] (count 2).
+    auto dual_issue = [&](int parity) {
+        int t, kb0, kb1, role;
+        if (!unit_at<kSK>(p, 0, unit0, unit_stride, num_tiles, ksplit, num_kb, t, kb0, kb1, role)) return;
+        const uint32_t d = tmem_base + static_cast<uint32_t>(parity * BN);
+        for (int kb = kb0 + parity; kb < kb1; kb += 2) {
+            const int j = kb - kb0;
+            const int stage = j % kStages;
+            ptx::mbar_wait(&full[stage], static_cast<uint32_t>((j / kStages) & 1));
+            ptx::tc_fence_after();
+            const uint32_t a_addr = ptx::smem_u32(smem_a + stage * BM * BK_BYTES);
+            const uint32_t b_addr = ptx::smem_u32(smem_b + stage * kBRows * BK_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK_BYTES / 32; ++k) {
+                const uint64_t da = (kLay & 1) ? ptx::sw128_mnmajor_desc(a_addr + k * 16 * 128, bk_elems * 128)
+                                               : ptx::sw128_kmajor_desc(a_addr + k * 32);
+                const uint64_t db = (kLay & 2) ? ptx::sw128_mnmajor_desc(b_addr + k * 16 * 128, bk_elems * 128)
+                                               : ptx::sw128_kmajor_desc(b_addr + k * 32);
+                const uint32_t accum = (kb != kb0 + parity || k != 0) ? 1u : 0u;
+                if (kI8)
+                    ptx::mma_i8(d, da, db, p.idesc, accum);
+                else
+                    ptx::mma_f16(d, da, db, p.idesc, accum);
+            }
+            ptx::tc_commit(&empty[stage]);
+        }
+        ptx::tc_commit(&tfull[0]);
+    };
 
     if (warp == 0 && (kLay & 12)) {
         // ============ implicit-GEMM conv producer (all 32 lanes) ============
@@ -429,6 +467,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 0) {
         // ===================== TMA producer =====================
+#ifdef QSB_GEMM_TRACE
+        // isolation mode 16 (with 2, MMA-only): this warp issues a SECOND MMA
+        // stream of the same shape into the other accumulator buffer -- two
+        // issuing threads on one SM's tensor pipe (wrong sums; timing only)
+        if ((p.debug_epi & 18) == 18 && kCta == 1 && lane == 0) {
+            for (int ui = 0;; ++ui) {
+                int t, kb0, kb1, role;
+                if (!unit_at<kSK>(p, ui, unit0, unit_stride, num_tiles, ksplit, num_kb, t, kb0, kb1, role)) break;
+                const uint32_t d2 = tmem_base + static_cast<uint32_t>(((ui & 1) ^ 1) * BN);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    const uint32_t a_addr = ptx::smem_u32(smem_a);
+                    const uint32_t b_addr = ptx::smem_u32(smem_b);
+#pragma unroll
+                    for (int k = 0; k < BK_BYTES / 32; ++k) {
+                        const uint64_t da = ptx::sw128_kmajor_desc(a_addr + k * 32);
+                        const uint64_t db = ptx::sw128_kmajor_desc(b_addr + k * 32);
+                        if (kI8)
+                            ptx::mma_i8(d2, da, db, p.idesc, 1u);
+                        else
+                            ptx::mma_f16(d2, da, db, p.idesc, 1u);
+                    }
+                }
+            }
+            ptx::tc_commit(&full[0]);
+            ptx::mbar_wait(&full[0], 0);
+        } else
+#endif
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
@@ -537,7 +602,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA of a pair) =====================
-        if (lane == 0 && leader) {
+        if (kDual) {
+            if (lane == 0) dual_issue(0);
+        } else if (lane == 0 && leader) {
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -636,6 +703,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ===================== epilogue (warps 2..9) =====================
+        if (kDual) {  // the second MMA issuer, then this warp's epilogue share
+            if (warp == kEpiWarp0 && lane == 0) dual_issue(1);
+            __syncwarp();
+        }
         // Two warps per TMEM lane quadrant (warp w reads lanes 32*(w%4)..+31):
         // the tile's column chunks alternate between them, so each quadrant's
         // TMEM loads, dequant math and staging stores run on two warps.
@@ -796,6 +867,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0), rr[0]);
                 if (out16) ptx::tmem_ld32(tbase + static_cast<uint32_t>(c0 + 32), rr[1]);
                 ptx::tmem_ld_wait();
+                if constexpr (kDual) {  // + the odd k-blocks' accumulator (buffer 1)
+#pragma unroll
+                    for (int sub = 0; sub < 2; ++sub) {
+                        if (sub >= nsub) break;
+                        uint32_t r2[32];
+                        ptx::tmem_ld32(tbase + static_cast<uint32_t>(BN + c0 + 32 * sub), r2);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            if constexpr (kI8 && !kF8)
+                                rr[sub][j] = static_cast<uint32_t>(static_cast<int>(rr[sub][j]) + static_cast<int>(r2[j]));
+                            else
+                                rr[sub][j] = __float_as_uint(__fadd_rn(bits_f(rr[sub][j]), bits_f(r2[j])));
+                        }
+                    }
+                }
 #ifdef QSB_GEMM_TRACE
                 unsigned long long tc1 = trace_clock();
                 t_ld += tc1 - tc0;
@@ -1153,6 +1240,9 @@ int g_conv_tma = 1;      // implicit conv operand loads: 1 = TMA im2col, 0 = cp.
 // MN-major B operand at ~86% of their MMA rate and each CTA's range crosses
 // tile boundaries, each crossing a pipeline drain + an accumulator switch.
 int g_streamk = -1;
+// Two MMA issuers (kLay bit 11) for 192-wide single-CTA tiles when every CTA
+// owns exactly one work unit of >= 4 k-blocks (qsync_gemm_set_dual; 1 = on).
+int g_dual = 1;
 
 // Stream-K scratch, one per (device, stream) and never freed (a captured graph
 // keeps pointing at it): partial accumulators of at most one unit per CTA
@@ -1257,7 +1347,7 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
             p.kb_per = static_cast<int>(per);
             p.ksplit = static_cast<int>((num_kb + per - 1) / per);
         }
-    } else if (can_split && tiles < slots) {
+    } else if (can_split && tiles < slots && !(kLay & 2048)) {  // (dual issue: the split is dispatch's)
         int64_t want = std::max<int64_t>(1, (2 * slots) / tiles);         // ~2 units per slot
         want = std::min<int64_t>(want, std::max<int64_t>(1, num_kb / 8));  // >= 8 k-blocks each
         if (want > 1) {
@@ -1283,6 +1373,8 @@ int launch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, cu
     const int64_t units = p.streamk ? std::min<int64_t>(tiles * num_kb, slots) : tiles * p.ksplit;
     int64_t cap = slots;
     if (g_max_ctas > 0) cap = std::max<int64_t>(1, std::min<int64_t>(slots, g_max_ctas / kCta));
+    QSB_REQUIRE(!(kLay & 2048) || (units <= cap && p.kb_per >= 2), QSYNC_ERR_INTERNAL,
+                "dual-issue GEMM needs one work unit of >= 2 k-blocks per CTA");
     const int grid = static_cast<int>(std::min<int64_t>(units, cap)) * kCta;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid, 1, 1);
@@ -1470,6 +1562,21 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
     if (sh.cta == 2 && (sh.bn == 64 || (sh.bn == 192 && (layout & 2)))) sh.cta = 1;
     p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM * sh.cta, layout, p.fp8);
     p.debug_epi = g_debug_epi;
+    if (!p.streamk && g_dual && !p.fp8 && sh.cta == 1 && sh.bn == 192 && g_max_ctas == 0 &&
+        (layout == 0 || layout == 2 || layout == 3)) {
+        // dual issue: one unit per CTA (tiles x K-splits <= SMs), >= 4 k-blocks each
+        const int64_t bk = kI8 ? BK_BYTES : BK_BYTES / 2;
+        const int64_t kb = (p.K + bk - 1) / bk;
+        const int64_t ks = std::max(1, p.ksplit);
+        const int64_t units = ((p.M + BM - 1) / BM) * ((p.N + 191) / 192) * ks;
+        if (units <= sm_count() && (kb + ks - 1) / ks >= 4) {
+            if (layout == 0) return launch<kI8, 192, 1, 2048>(a, b, dt, p, st);
+            if constexpr (!kI8) {
+                if (layout == 2) return launch<false, 192, 1, 2050>(a, b, dt, p, st);
+                if (layout == 3) return launch<false, 192, 1, 2051>(a, b, dt, p, st);
+            }
+        }
+    }
     if (p.streamk && !p.fp8) {  // the stream-K instantiations (kLay bit 10)
         if (layout == 0) return launch<kI8, 256, 1, 1024>(a, b, dt, p, st);
         if constexpr (!kI8) {
@@ -1684,6 +1791,11 @@ int qsync_gemm_debug_epilogue(int v) {
 int qsync_gemm_set_streamk(int mode) {
     QSB_REQUIRE(mode >= -1 && mode <= 1, QSYNC_ERR_DOMAIN, "stream-K mode must be -1 (never), 0 (cost model) or 1");
     g_streamk = mode;
+    return QSYNC_OK;
+}
+
+int qsync_gemm_set_dual(int on) {
+    g_dual = on ? 1 : 0;
     return QSYNC_OK;
 }
 

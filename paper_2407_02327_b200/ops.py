@@ -781,6 +781,11 @@ def set_streamk(mode: int) -> None:
     call("qsync_gemm_set_streamk", int(mode))
 
 
+def set_dual_issue(on: bool) -> None:
+    """Two MMA issuers for 192-wide single-unit-per-CTA GEMMs (default on)."""
+    call("qsync_gemm_set_dual", int(bool(on)))
+
+
 def force_cta(cta: int) -> None:
     """Test hook: 1 = single-CTA tiles, 2 = CTA-pair (cta_group::2) tiles, 0 = cost model."""
     call("qsync_gemm_force_cta", int(cta))

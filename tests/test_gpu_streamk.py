@@ -71,3 +71,52 @@ def test_streamk_accumulate(M, N, K):
     scale = want.abs().max().item()
     for y in (ref, y1, y2):
         assert (y.double() - want).abs().max().item() <= 1e-5 * scale
+
+
+def _dual_pair(fn):
+    try:
+        ops.set_dual_issue(False)
+        ref = fn()
+        ops.set_dual_issue(True)
+        got = fn()
+        torch.cuda.synchronize()
+    finally:
+        ops.set_dual_issue(True)
+    return ref, got
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 768, 768), (4096, 768, 3072), (1000, 768, 528), (4096, 768, 512)])
+def test_dual_issue_int8_bit_exact(M, N, K):
+    """Two MMA issuers splitting the k-blocks into two accumulators (kLay bit
+    11): int32 partial sums are exact, so the INT8 output is bit-identical."""
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda", generator=g)
+    b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda", generator=g)
+    sa = torch.tensor([0.02], device="cuda")
+    sb = torch.rand(N, device="cuda", generator=g) * 0.01
+    bias = torch.randn(N, device="cuda", generator=g)
+    for dt in (torch.float32, torch.float16):
+        ref, got = _dual_pair(lambda: ops.gemm_s8_ex(a, b, sa, sb, bias, out_dtype=dt))
+        assert torch.equal(ref, got)
+
+
+@pytest.mark.parametrize("M,N,K,lay", [(4096, 768, 768, 0), (4096, 768, 2304, 2), (4096, 768, 3072, 2),
+                                       (2304, 768, 4096, 3), (768, 768, 4096, 3)])
+def test_dual_issue_f16(M, N, K, lay):
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * K)
+    a = torch.randn((K, M) if lay == 3 else (M, K), device="cuda", generator=g).half()
+    b = torch.randn((K, N) if lay & 2 else (N, K), device="cuda", generator=g).half()
+    acc = lay != 0
+    base = torch.randn(M, N, device="cuda", generator=g)
+
+    def run():
+        out = base.clone() if acc else torch.empty(M, N, device="cuda")
+        ops.gemm_f16(a, b, out=out, accumulate=acc, a_mn=lay == 3, b_mn=bool(lay & 2))
+        return out
+    ref, got = _dual_pair(run)
+    A = a.double().t() if lay == 3 else a.double()
+    B = b.double() if lay & 2 else b.double().t()
+    want = (base.double() if acc else 0) + A @ B
+    scale = want.abs().max().item()
+    for y in (ref, got):
+        assert (y.double() - want).abs().max().item() <= 1e-5 * scale
