@@ -213,8 +213,13 @@ int qsync_adamw_step_range(const qsync_adamw_seg* segs, int nseg, const int64_t*
         static_cast<int>(std::min<int64_t>((row_end - row_begin + kWarps - 1) / kWarps, sm_count() * 16LL));
     const size_t smem = sizeof(int64_t) * (static_cast<size_t>(nseg) + 1);
     QSB_REQUIRE(smem <= 48 * 1024, QSYNC_ERR_DOMAIN, "too many parameter segments");
-    pdl_launch(k_adamw, dim3(grid), dim3(kWarps * 32), smem, st, segs, nseg, seg_row_start, row_begin, row_end, step, lr, beta1,
-                                             beta2, eps, weight_decay, update);
+    // A plain launch, not PDL: the optimizer follows the join of the wgrad side
+    // stream, and launched programmatically (its 4-wave grid becoming resident
+    // behind the last backward kernels) it ran ~770 us in the graphed step
+    // against ~570 us alone; plain, the step went 4.73 -> 4.53 ms (A/B of the
+    // two library builds, tools/ab_step.py lib=...).
+    k_adamw<<<grid, kWarps * 32, smem, st>>>(segs, nseg, seg_row_start, row_begin, row_end, step, lr, beta1, beta2,
+                                              eps, weight_decay, update);
     return check_launch("k_adamw");
 }
 

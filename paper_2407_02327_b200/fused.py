@@ -270,6 +270,10 @@ def _ff1_gelu(m, opnd, g_dtype):
     return am, g, gp, w16
 
 
+# Side-stream wgrad GEMMs launched with programmatic dependent launch (each
+# follows an event wait on the main stream).  A/B: tools/ab_step.py wgradpdl=1,0.
+WGRAD_PDL = True
+
 # Persistent-grid cap for the side-stream wgrad GEMMs (0 = all SMs): leaves SMs
 # to the critical-path chain on the main stream.  Set by TrainStep / tools.
 WGRAD_CTAS = 0
@@ -291,6 +295,8 @@ def _wgrad(m, dy16_or_32, opnd, side):
     def run():
         if side is not None and WGRAD_CTAS:
             _call_cap(WGRAD_CTAS)
+        if side is not None and not WGRAD_PDL:
+            call("qsync_gemm_set_pdl", 0)
         try:
             if kind == "f32":  # training-device FP32 wgrad: 3xTF32 on the tensor cores
                 ops.gemm_f32(dy16_or_32.float().contiguous(), x16, out=mw, accumulate=True, a_mn=True,
@@ -300,6 +306,8 @@ def _wgrad(m, dy16_or_32, opnd, side):
         finally:
             if side is not None and WGRAD_CTAS:
                 _call_cap(0)
+            if side is not None and not WGRAD_PDL:
+                call("qsync_gemm_set_pdl", 1)
 
     if side is not None:
         cur = torch.cuda.current_stream()

@@ -15,6 +15,7 @@ repetitions shows.
     python tools/ab_step.py head=1,0              classification head on csrc/head.cu vs torch
     python tools/ab_step.py attnq=1,0             INT8 O operand quantized in the attention kernel
     python tools/ab_step.py dual=1,0              two MMA issuers on 192-wide single-unit GEMMs
+    python tools/ab_step.py wgradpdl=1,0          side-stream wgrad GEMMs launched with PDL
     QSB_AB_PLAN=int8 python tools/ab_step.py ...  plan for the non-plan knobs (default mixed)
 """
 import os
@@ -41,6 +42,7 @@ def step_ms(knob: str, val: str, steps: int = 40) -> float:
     import paper_2407_02327_b200.train_step as _ts
     _ts.HEAD_KERNELS = not (knob == "head" and val == "0")
     fused.ATTN_QUANT = not (knob == "attnq" and val == "0")
+    fused.WGRAD_PDL = not (knob == "wgradpdl" and val == "0")
     from paper_2407_02327_b200 import ops as _ops
     _ops.set_dual_issue(not (knob == "dual" and val == "0"))
     m.apply_plan({"mixed": mixed_plan(cfg), "int8": uniform_plan(cfg, INT8), "fp16": uniform_plan(cfg, FP16)}[plan])
