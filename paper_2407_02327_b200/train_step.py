@@ -125,6 +125,9 @@ def _fusable(layer: EncoderLayer) -> bool:
 
 # Fused path: pooler + classifier + CE on csrc/head.cu (A/B: tools/ab_step.py head=1,0).
 HEAD_KERNELS = True
+# Gradient-buffer reset on the wgrad side stream, overlapping the forward pass
+# (A/B: tools/ab_step.py zero=1,0).
+ZERO_OVERLAP = True
 
 
 class BertEncoderStack(torch.nn.Module):
@@ -462,10 +465,20 @@ class TrainStep:
         if self.fused:
             from .fused import _mark
             _mark("opt", "zero")
-        self.grads.zero()
+        overlap_zero = ZERO_OVERLAP and self.wgrad_stream is not None and self.grads.timing is False
+        if overlap_zero:
+            # reset the gradient buffer on the side stream, under the forward pass
+            # (which writes no gradient); joined before the backward starts
+            self.wgrad_stream.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(self.wgrad_stream):
+                self.grads.zero()
+        else:
+            self.grads.zero()
         loss = self.model(self.tokens, self.labels)
         _ql.WGRAD_STREAM = self.wgrad_stream
         if self.wgrad_stream is not None:
+            if overlap_zero:
+                torch.cuda.current_stream().wait_stream(self.wgrad_stream)  # gradients zeroed
             self.wgrad_stream.wait_stream(torch.cuda.current_stream())  # after the zeroing
         # Buckets are all-reduced while the backward continues: a fused layer
         # reports its parameters final when its backward is enqueued, autograd

@@ -16,6 +16,7 @@ repetitions shows.
     python tools/ab_step.py attnq=1,0             INT8 O operand quantized in the attention kernel
     python tools/ab_step.py dual=1,0              two MMA issuers on 192-wide single-unit GEMMs
     python tools/ab_step.py wgradpdl=1,0          side-stream wgrad GEMMs launched with PDL
+    python tools/ab_step.py zero=1,0              gradient reset overlapping the forward
     QSB_AB_PLAN=int8 python tools/ab_step.py ...  plan for the non-plan knobs (default mixed)
 """
 import os
@@ -41,6 +42,7 @@ def step_ms(knob: str, val: str, steps: int = 40) -> float:
     fused.FF2_INT8_RECOMPUTE = knob == "ff2recompute" and val == "1"
     import paper_2407_02327_b200.train_step as _ts
     _ts.HEAD_KERNELS = not (knob == "head" and val == "0")
+    _ts.ZERO_OVERLAP = not (knob == "zero" and val == "0")
     fused.ATTN_QUANT = not (knob == "attnq" and val == "0")
     fused.WGRAD_PDL = not (knob == "wgradpdl" and val == "0")
     from paper_2407_02327_b200 import ops as _ops
