@@ -76,7 +76,7 @@ __device__ __forceinline__ void act_row8(const void* __restrict__ dy, const void
             float hv[8];
             load8v<DH>(h, off, hv);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) g[j] = __fmul_rn(g[j], gelu_erf_grad(hv[j]));
+            for (int j = 0; j < 8; ++j) g[j] = __fmul_rn(g[j], gelu_erf_grad<DH != QSYNC_F32>(hv[j]));
         } else if constexpr (ACT == 2) {  // h holds act'(x) (FP16), stored by the forward
             float hv[8];
             load8v<QSYNC_F16>(h, off, hv);
@@ -90,7 +90,7 @@ __device__ __forceinline__ void act_row8(const void* __restrict__ dy, const void
             g[j] = 0.0f;
             if (c + j < cols) {
                 g[j] = load1<DDY>(dy, off + j);
-                if constexpr (ACT == 1) g[j] = __fmul_rn(g[j], gelu_erf_grad(load1<DH>(h, off + j)));
+                if constexpr (ACT == 1) g[j] = __fmul_rn(g[j], gelu_erf_grad<DH != QSYNC_F32>(load1<DH>(h, off + j)));
                 if constexpr (ACT == 2) g[j] = __fmul_rn(g[j], load1<QSYNC_F16>(h, off + j));
                 if (out) store1<DO>(out, off + j, g[j]);
             }

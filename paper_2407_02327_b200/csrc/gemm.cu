@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                               : __fmul_rn(bits_f(a), alpha);
                                 if (p.bias) v = __fadd_rn(v, fb[cb + j + e]);
                                 if (!kI8) v = __half2float(__float2half_rn(v));  // the FP16 GEMM's stored h
-                                gelu_and_grad(v, gv[e], dv[e]);
+                                gelu_pair<!kI8>(v, gv[e], dv[e]);  // FP16 GEMM: h is an FP16 value
                                 // round_to<h dtype> as the FF2 operand kernels do (FP16 for an
                                 // FP16 GEMM's h), and the stored dtype
                                 if (g16 || !kI8) gv[e] = __half2float(__float2half_rn(gv[e]));

@@ -34,7 +34,7 @@ __device__ __forceinline__ float round_to(float g) {
 template <int ACT, int DT = QSYNC_F32>
 __device__ __forceinline__ float act_f(float v) {
     if constexpr (ACT == 1) {
-        const float g = gelu_erf(v);
+        const float g = gelu_erf<DT != QSYNC_F32>(v);
         if constexpr (DT == QSYNC_F16) return __half2float(__float2half_rn(g));
         if constexpr (DT == QSYNC_BF16) return __bfloat162float(__float2bfloat16_rn(g));
         return g;
@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(kThreads) k_gelu_absmax_store(const typename E
 #pragma unroll
             for (int j = 0; j < 8; j += 2) {
                 float d0, d1;
-                gelu_and_grad(f[j], g[j], d0);
-                gelu_and_grad(f[j + 1], g[j + 1], d1);
+                gelu_pair<DT != QSYNC_F32>(f[j], g[j], d0);
+                gelu_pair<DT != QSYNC_F32>(f[j + 1], g[j + 1], d1);
                 g[j] = round_to<DT>(g[j]);
                 g[j + 1] = round_to<DT>(g[j + 1]);
                 m = fmaxf(m, fmaxf(fabsf(g[j]), fabsf(g[j + 1])));
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_gelu_absmax_store(const typename E
     }
     for (int64_t i = done + tid; i < n; i += stride) {
         float g, d;
-        gelu_and_grad(Elem<DT>::f(x[i]), g, d);
+        gelu_pair<DT != QSYNC_F32>(Elem<DT>::f(x[i]), g, d);
         g = round_to<DT>(g);
         m = fmaxf(m, fabsf(g));
         if constexpr (DT == QSYNC_F32)
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_quantize(const typename Elem<DT
                         float d[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            gelu_and_grad(f[j + e], a[e], d[e]);
+                            gelu_pair<DT != QSYNC_F32>(f[j + e], a[e], d[e]);
                             a[e] = round_to<DT>(a[e]);
                         }
                         dp[(u * V::N + j) / 2] = pack_half2(d[0], d[1]);
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_quantize(const typename Elem<DT
         const int qi = quant_rne(act_f<ACT, DT>(xv), qs);
         q[i] = static_cast<int8_t>(qi);
         if (q16) q16[i] = __half_as_ushort(__int2half_rn(qi));
-        if (ACT == 1 && dact) dact[i] = __half_as_ushort(__float2half_rn(gelu_erf_grad(xv)));
+        if (ACT == 1 && dact) dact[i] = __half_as_ushort(__float2half_rn(gelu_erf_grad<DT != QSYNC_F32>(xv)));
     }
 }
 
@@ -782,8 +782,8 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
                 float d0[8], d1[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    gelu_and_grad(f0[j], f0[j], d0[j]);
-                    gelu_and_grad(f1[j], f1[j], d1[j]);
+                    gelu_pair<SD != QSYNC_F32>(f0[j], f0[j], d0[j]);
+                    gelu_pair<SD != QSYNC_F32>(f1[j], f1[j], d1[j]);
                     f0[j] = round_to<SD>(f0[j]);
                     f1[j] = round_to<SD>(f1[j]);
                 }
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
                 float d0[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    gelu_and_grad(f0[j], f0[j], d0[j]);
+                    gelu_pair<SD != QSYNC_F32>(f0[j], f0[j], d0[j]);
                     f0[j] = round_to<SD>(f0[j]);
                 }
                 reinterpret_cast<uint4*>(dact)[i] =
@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(kThreads) k_cast(const typename Elem<SD>::T* _
     for (int64_t i = done + tid; i < n; i += stride) {
         const float xv = Elem<SD>::f(x[i]);
         out[i] = Store<SD, DD>::cvt(act_f<ACT, SD>(xv));
-        if (ACT == 1 && dact) dact[i] = __half_as_ushort(__float2half_rn(gelu_erf_grad(xv)));
+        if (ACT == 1 && dact) dact[i] = __half_as_ushort(__float2half_rn(gelu_erf_grad<SD != QSYNC_F32>(xv)));
     }
 }
 
