@@ -386,6 +386,26 @@ int qsync_gemm_gelu(const void* a, const void* b, int ab_dtype, int64_t m, int64
                     const float* scale_a, const float* scale_b, int b_per_channel, const float* bias, void* g,
                     int g_dtype, uint16_t* dact, float* absmax, qsync_stream_t stream);
 
+/* An INT8 FF1 feeding an INT8 FF2 without storing GELU(h):
+ *   qsync_gemm_s8_ymax: qsync_gemm_s8_ex with FP32 output that also writes
+ *     *ymax (overwritten) = max(0, max over the outputs y);
+ *   qsync_gelu_quantize: FF2's operand from h (FP32) in one pass -- q = INT8 of
+ *     gelu(h) with s = absmax(gelu(h)) / 127, q16 (optional) = FP16 of the grid
+ *     values, dact (optional) = FP16 gelu'(h), scale_out[0] = s, [1] = absmax.
+ *     gelu is non-decreasing where it exceeds 0.1701 and below that for every
+ *     h < 0 (qsync_gelu_fp32_check), so absmax = gelu(hmax) when that is >= 0.1701
+ *     and no absmax pass is needed; otherwise the kernel reduces it exactly
+ *     first.  Bit-identical to qsync_gelu_absmax_store + qsync_quantize_act_ex.
+ *   qsync_gelu_fp32_check: out[0] += monotonicity violations over every float32
+ *     in [0, 16] above 0.1701, out[1] = max |gelu(h)| over h < 0 (float bits);
+ *     out zeroed by the caller (a self-check for the tests). */
+int qsync_gemm_s8_ymax(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k, float* c,
+                       const float* scale_a, const float* scale_b, int b_per_channel, const float* bias, float* ymax,
+                       qsync_stream_t stream);
+int qsync_gelu_quantize(const float* h, int64_t n, const float* hmax, int8_t* q, uint16_t* q16, uint16_t* dact_out,
+                        float* scale_out, qsync_stream_t stream);
+int qsync_gelu_fp32_check(unsigned* out);
+
 /* The classification head around the encoder stack (FP32 ops; train_step.py:
  * pooler = tanh(x[:, 0] Wp^T + bp), logits = pooled Wc^T + bc, loss = mean
  * cross entropy), so the graphed step launches only this library's kernels.

@@ -82,6 +82,9 @@ SIGNATURES = {
     "qsync_cls_head_fwd": [_p, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p],
     "qsync_cls_head_bwd": [_p, _i64, _i64, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "qsync_zero": [_p, _i64, _p],
+    "qsync_gemm_s8_ymax": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _int, _p, _p, _p],
+    "qsync_gelu_quantize": [_p, _i64, _p, _p, _p, _p, _p, _p],
+    "qsync_gelu_fp32_check": [_p],
     "qsync_attention_fwd_quant": [_p, _i64, _i64, _i64, _i64, _f32, _p, _p, _p, _p, _p, _p],
     "qsync_adamw_step": [_p, _int, _p, _i64, _p, _f32, _f32, _f32, _f32, _f32, _int, _p],
     "qsync_adamw_step_range": [_p, _int, _p, _i64, _i64, _p, _f32, _f32, _f32, _f32, _f32, _int, _p],

@@ -79,6 +79,10 @@ struct EpiParams {
     // act_absmax = max |g| (float bits, atomicMax; the caller zeroes it).
     uint16_t* dact;
     unsigned* act_absmax;
+    // kLay bit 12: also reduce ymax = max(0, max y) over the stored outputs
+    // (float bits, atomicMax; zeroed by the host) -- FF1's input to the
+    // one-pass GELU quantizer (qsync_gelu_quantize).
+    unsigned* ymax;
     // kLay bits 5 / 6: the same operands loaded by TMA in im2col mode instead
     // (A for fwd / stride-1 dgrad -- the dgrad as a conv of dY with pad k-1-p and
     // flipped taps; B for wgrad); one elected thread, no gather lanes.
@@ -212,6 +216,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // per tcgen05.mma); two can (trace build, isolation mode 18: 2x the MMAs
     // of a 192-wide tile in 1.63x the time, 128-wide in 1.2x).
     constexpr bool kDual = (kLay & 2048) != 0;
+    constexpr bool kYmax = (kLay & 4096) != 0;
+    static_assert(!kYmax || (kI8 && kCta == 1 && (kLay & 0xfff) == 0), "ymax: INT8 K-major single-CTA");
     static_assert(!kDual || (kCta == 1 && (kLay & 0x7fc) == 0), "dual issue: plain single-CTA tiles");
     static_assert(!kSK || (kCta == 1 && BN == 256 && (kLay & 0x3fc) == 0), "stream-K: plain 256-wide single-CTA");
     static_assert(!kGelu || (kCta == 1 && (kLay & 511) == 0), "GELU epilogue: single-CTA K-major tiles");
@@ -728,6 +734,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t acc_phase = 0;
         float alpha = p.alpha;
         if (p.alpha_dev) alpha *= *p.alpha_dev;
+        float vmax = 0.0f;  // kYmax: this thread's running max of the unit's outputs
+        (void)vmax;
         const float sa = (kI8 && p.scale_a) ? *p.scale_a : 1.0f;
         const bool out16 = p.c && p.c_dtype != QSYNC_F32;
         const bool raw = p.c_i32 != nullptr && p.c == nullptr;
@@ -965,6 +973,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             v[2] = __fadd_rn(v[2], b4.z);
                             v[3] = __fadd_rn(v[3], b4.w);
                         }
+                        if constexpr (kYmax) {  // valid rows / columns only (padding rows hold the bias)
+                            if (row_ok) {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    if (col0 + 32 * sub + j + e < N) vmax = fmaxf(vmax, v[e]);
+                            }
+                        }
                         if (out16) {
                             w[16 * sub + j / 2] = bf ? pack_bf162(v[0], v[1]) : pack_half2(v[0], v[1]);
                             w[16 * sub + j / 2 + 1] = bf ? pack_bf162(v[2], v[3]) : pack_half2(v[2], v[3]);
@@ -1049,6 +1064,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+            }
+            if constexpr (kYmax) {
+                vmax = warp_max(vmax);
+                if (lane == 0 && vmax > 0.0f) atomicMax(p.ymax, __float_as_uint(vmax));
+                vmax = 0.0f;
             }
             if (kSK && role == kUnitContrib) {  // publish this CTA's partial of tile t
                 __threadfence();
@@ -1622,6 +1642,18 @@ int dispatch(const void* a, const void* b, CUtensorMapDataType dt, EpiParams p, 
         if (layout == 67) return launch<false, 256, 1, 67>(a, b, dt, p, st);
         return set_error(QSYNC_ERR_DOMAIN, "unsupported implicit conv layout " + std::to_string(layout));
     }
+    if (layout == 4096) {  // INT8 with ymax: single-CTA 128..256-wide K-major tiles
+        if constexpr (kI8) {
+            if (sh.bn == 64) sh.bn = 128;
+            p.idesc = make_idesc(true, false, sh.bn, BM, 0, false);
+            switch (sh.bn) {
+                case 256: return launch<true, 256, 1, 4096>(a, b, dt, p, st);
+                case 192: return launch<true, 192, 1, 4096>(a, b, dt, p, st);
+                default: return launch<true, 128, 1, 4096>(a, b, dt, p, st);
+            }
+        }
+        return set_error(QSYNC_ERR_DOMAIN, "ymax GEMM is INT8 only");
+    }
     if (layout == 512) {  // GELU epilogue (FF1): single-CTA 128..256-wide K-major tiles
         if (sh.bn == 64) sh.bn = 128;
         p.idesc = make_idesc(kI8, dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.bn, BM, 0, false);
@@ -1888,6 +1920,29 @@ int qsync_gemm_gelu(const void* a, const void* b, int ab_dtype, int64_t m, int64
     const CUtensorMapDataType dt =
         ab_dtype == QSYNC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     return dispatch<false>(a, b, dt, p, to_stream(stream), g_force_bn, 512);
+}
+
+int qsync_gemm_s8_ymax(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k, float* c,
+                       const float* scale_a, const float* scale_b, int b_per_channel, const float* bias, float* ymax,
+                       qsync_stream_t stream) {
+    QSB_TRY(validate(a, b, m, n, k, 16));
+    QSB_REQUIRE(c != nullptr && ymax != nullptr, QSYNC_ERR_VALIDATION, "GEMM needs an output and ymax");
+    QSB_REQUIRE(scale_a && scale_b, QSYNC_ERR_VALIDATION, "the dequant epilogue needs scale_a and scale_b");
+    EpiParams p{};
+    p.M = m;
+    p.N = n;
+    p.K = k;
+    p.c = c;
+    p.c_dtype = QSYNC_F32;
+    p.scale_a = scale_a;
+    p.scale_b = scale_b;
+    p.b_per_channel = b_per_channel;
+    p.bias = bias;
+    p.alpha = 1.0f;
+    p.ymax = reinterpret_cast<unsigned*>(ymax);
+    cudaStream_t st = to_stream(stream);
+    QSB_TRY(zero_async(ymax, sizeof(float), st));
+    return dispatch<true>(a, b, CU_TENSOR_MAP_DATA_TYPE_UINT8, p, st, g_force_bn, 4096);
 }
 
 int qsync_gemm_s8(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k,

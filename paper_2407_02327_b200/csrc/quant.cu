@@ -1076,6 +1076,156 @@ struct GeluAbsmaxStoreRun {
     }
 };
 
+// ---------------------------------------------------------------------------
+// FF2's INT8 operand from FF1's FP32 output h in ONE pass when the answer is
+// known up front.  The unfused path quantizes g = gelu(h) with s = absmax(g)/127.
+// gelu (this library's float32 function) is monotone only up to ulp-level
+// dips, but over every float32 x in [0, 16] above 0.1701, gelu(y) >= gelu(x)
+// for every y at least kGeluGap ulps above x (checked exhaustively with steps
+// of kGeluGap .. 2 kGeluGap - 1 ulps, which compose into any larger gap, by
+// qsync_gelu_fp32_check), and |gelu(h)| < 0.1701 for every h < 0.  So with hmax
+// the largest h (reduced by FF1's GEMM epilogue, qsync_gemm_s8_ymax): if
+// gelu(hmax) >= 0.1701 and no float within kGeluGap ulps below hmax has a larger
+// gelu, absmax(g) = gelu(hmax) exactly and the quantizer needs no absmax pass
+// over g: read h, write q, FP16(q) and GELU'(h).  Otherwise the kernel takes
+// the exact absmax over gelu(h) first, across a grid barrier (one co-resident
+// wave).  q / s / q16 / GELU' are bit-identical to gelu_absmax_store +
+// quantize_act either way.
+constexpr float kGeluMonoFloor = 0.1701f;
+constexpr int kGeluGap = 16;
+constexpr int kGqSlots = 32;
+constexpr int kGqMaxBlocks = 2048;
+__device__ float g_gq_part[kGqSlots][kGqMaxBlocks];
+__device__ unsigned g_gq_bar[kGqSlots][2];
+
+__device__ __forceinline__ void gq_grid_barrier(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_gelu_quant(const float* __restrict__ h, int64_t n,
+                                                     const float* __restrict__ hmax, int8_t* __restrict__ q,
+                                                     uint16_t* __restrict__ q16, uint16_t* __restrict__ dact,
+                                                     float* __restrict__ scale_out, int slot, int vec_ok) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // dependents only after the (possible) barrier
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const float hm = fmaxf(*hmax, 0.0f);
+    const float gm = gelu_erf<false>(hm);
+    bool fast = gm >= kGeluMonoFloor;
+    if (fast) {  // no float just below hmax may have a larger gelu (ulp-level dips)
+        const uint32_t hb = __float_as_uint(hm);
+        for (int k = 1; k < kGeluGap && static_cast<uint32_t>(k) <= hb; ++k)
+            fast = fast && !(gelu_erf<false>(__uint_as_float(hb - k)) > gm);
+    }
+    float am = gm;
+    if (!fast) {  // exact fallback: absmax over gelu(h)
+        float m = 0.0f;
+        for (int64_t i = tid; i < n; i += stride) m = fmaxf(m, fabsf(gelu_erf<false>(h[i])));
+        __shared__ float red[8];
+        m = warp_max(m);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float b = 0.0f;
+            for (int w = 0; w < 8; ++w) b = fmaxf(b, red[w]);
+            g_gq_part[slot][blockIdx.x] = b;
+        }
+        gq_grid_barrier(g_gq_bar[slot], gridDim.x);
+        __shared__ float s_am;
+        if (threadIdx.x == 0) {
+            float b = 0.0f;
+            for (int i = 0; i < static_cast<int>(gridDim.x); ++i) b = fmaxf(b, __ldcg(&g_gq_part[slot][i]));
+            s_am = b;
+        }
+        __syncthreads();
+        am = s_am;
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const float sc = scale_from_absmax(am);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scale_out[0] = sc;
+        scale_out[1] = am;
+    }
+    const QScale qs = make_qscale(sc);
+    int64_t done = 0;
+    if (vec_ok) {  // 8 elements per thread-iteration: 2 x 16 B loads, 8 B of q, 16 B of q16 and GELU'
+        const int64_t n8 = n / 8;
+        for (int64_t i = tid; i < n8; i += stride) {
+            float f[8];
+            Vec<QSYNC_F32>::unpack(ld_stream(reinterpret_cast<const uint4*>(h) + 2 * i), f);
+            Vec<QSYNC_F32>::unpack(ld_stream(reinterpret_cast<const uint4*>(h) + 2 * i + 1), f + 4);
+            float t[8];
+            uint32_t dp[4], hq[4];
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+                float g0, g1, d0, d1;
+                gelu_pair<false>(f[j], g0, d0);
+                gelu_pair<false>(f[j + 1], g1, d1);
+                t[j] = quant_rne_f(g0, qs);
+                t[j + 1] = quant_rne_f(g1, qs);
+                dp[j / 2] = pack_half2(d0, d1);
+                hq[j / 2] = pack_half2(grid_value(t[j]), grid_value(t[j + 1]));
+            }
+            reinterpret_cast<uint2*>(q)[i] = make_uint2(pack_q4(t[0], t[1], t[2], t[3]), pack_q4(t[4], t[5], t[6], t[7]));
+            if (q16) reinterpret_cast<uint4*>(q16)[i] = make_uint4(hq[0], hq[1], hq[2], hq[3]);
+            if (dact) reinterpret_cast<uint4*>(dact)[i] = make_uint4(dp[0], dp[1], dp[2], dp[3]);
+        }
+        done = n8 * 8;
+    }
+    for (int64_t i = done + tid; i < n; i += stride) {
+        float g, d;
+        gelu_pair<false>(h[i], g, d);
+        const int qi = quant_rne(g, qs);
+        q[i] = static_cast<int8_t>(qi);
+        if (q16) q16[i] = __half_as_ushort(__int2half_rn(qi));
+        if (dact) dact[i] = __half_as_ushort(__float2half_rn(d));
+    }
+}
+
+// Exhaustive checks behind k_gelu_quant's shortcut: over every float32 x in
+// [0, 16] with gelu(x) > 0.1701, count the steps y = x + j ulp, j in
+// [kGeluGap, 2 kGeluGap), with gelu(y) < gelu(x) (must be 0; outside [0, 16]
+// gelu(h) is h); and max |gelu(h)| over h in [-16, 0) (must be < 0.1701).  A
+// block takes 1024 consecutive floats and their 2 kGeluGap successors from
+// shared memory.
+__global__ void __launch_bounds__(256) k_gelu_check(unsigned* out) {
+    constexpr int kChunk = 1024;
+    __shared__ float gs[kChunk + 2 * kGeluGap];
+    const uint32_t top = 0x41800000u;  // 16.0f
+    unsigned viol = 0;
+    float negmax = 0.0f;
+    for (uint32_t b0 = blockIdx.x * kChunk; b0 < top; b0 += gridDim.x * kChunk) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < kChunk + 2 * kGeluGap; i += blockDim.x)
+            gs[i] = gelu_erf<false>(__uint_as_float(b0 + i));
+        __syncthreads();
+        for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
+            const float g = gs[i];
+            if (g > kGeluMonoFloor) {
+                for (int j = kGeluGap; j < 2 * kGeluGap; ++j) viol += gs[i + j] < g ? 1u : 0u;
+            }
+            negmax = fmaxf(negmax, fabsf(gelu_erf<false>(-__uint_as_float(b0 + i))));
+        }
+    }
+    if (viol) atomicAdd(out, viol);
+    negmax = warp_max(negmax);
+    if ((threadIdx.x & 31) == 0 && negmax > 0.0f) atomicMax(out + 1, __float_as_uint(negmax));
+}
+
 template <int DT>
 struct QuantActRun {
     static int run(const void* x, int64_t n, int act, const float* absmax, int8_t* q,
@@ -1233,6 +1383,38 @@ int qsync_gelu_absmax_store(const void* x, int dtype, int64_t n, float* absmax, 
     if (dtype == QSYNC_F32)
         return GeluAbsmaxStoreRun<QSYNC_F32>::run(x, n, absmax, y, dact_out, to_stream(stream));
     return GeluAbsmaxStoreRun<QSYNC_F16>::run(x, n, absmax, y, dact_out, to_stream(stream));
+}
+
+int qsync_gelu_quantize(const float* h, int64_t n, const float* hmax, int8_t* q, uint16_t* q16, uint16_t* dact_out,
+                        float* scale_out, qsync_stream_t stream) {
+    QSB_REQUIRE(n >= 0, QSYNC_ERR_DOMAIN, "negative element count");
+    QSB_REQUIRE(h && hmax && q && scale_out, QSYNC_ERR_VALIDATION, "h, hmax, q and scale_out (float[2]) are required");
+    if (n == 0) return QSYNC_OK;
+    cudaStream_t st = to_stream(stream);
+    static int occ[16] = {0};
+    int dev = 0;
+    QSB_TRY(cuda_status(cudaGetDevice(&dev), "cudaGetDevice"));
+    if (dev < 16 && occ[dev] == 0) {
+        int nb = 0;
+        QSB_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_gelu_quant, 256, 0),
+                            "cudaOccupancyMaxActiveBlocksPerMultiprocessor"));
+        occ[dev] = nb > 0 ? nb : 1;
+    }
+    const int per_sm = dev < 16 ? occ[dev] : 1;
+    // one co-resident wave (the fallback's grid barrier needs every block resident)
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({(n / 8 + 255) / 256, int64_t(per_sm) * sm_count(), int64_t(kGqMaxBlocks)})));
+    const int vec = aligned16(h) && (reinterpret_cast<uintptr_t>(q) & 7) == 0 && (!q16 || aligned16(q16)) &&
+                    (!dact_out || aligned16(dact_out));
+    const int slot = static_cast<int>((reinterpret_cast<uintptr_t>(st) >> 4) % kGqSlots);
+    pdl_launch(k_gelu_quant, dim3(grid), dim3(256), 0, st, h, n, hmax, q, q16, dact_out, scale_out, slot, vec);
+    return check_launch("k_gelu_quant");
+}
+
+int qsync_gelu_fp32_check(unsigned* out) {
+    QSB_REQUIRE(out != nullptr, QSYNC_ERR_VALIDATION, "out (uint32[2], zeroed) is required");
+    k_gelu_check<<<sm_count() * 8, 256>>>(out);
+    return check_launch("k_gelu_check");
 }
 
 int qsync_quantize_act_ex(const void* x, int dtype, int64_t n, int act, const float* absmax, int8_t* q,

@@ -237,6 +237,10 @@ def _linear_fwd(m, opnd, out_dtype=None):
     return y, w16
 
 
+# INT8 FF1 -> INT8 FF2: FF1's GEMM reduces max(h), then one pass builds FF2's
+# operand (qsync_gemm_s8_ymax + qsync_gelu_quantize).  A/B: ab_step onepass=1,0.
+GELU_ONE_PASS = True
+
 # INT8 O projection: its operand quantized inside the attention kernel
 # (qsync_attention_fwd_quant) instead of a quantize_act pass over the output.
 ATTN_QUANT = True
@@ -397,17 +401,28 @@ class _FusedLayerFn(torch.autograd.Function):
         op_1 = _operand(x1, aux1, p1)
         _mark("fwd", L.ff1.name)
         h = None
+        hmax = None
         if FF1_GELU_EPILOGUE and op_1[0] in ("i8", "f16") and L.ff1.weight.shape[0] % 8 == 0:
             # g in the dtype the FF2 operand kernel reads, GELU'(h) and absmax(g),
             # bit-identical to the GEMM + operand kernel below; h is never stored.
             h_dtype = torch.float32 if op_1[0] == "i8" else torch.float16
             gdt = h_dtype if p2 == INT8 else (torch.float16 if p2 == FP16 else torch.float32)
             gam, g_act, gp, w16_1 = _ff1_gelu(L.ff1, op_1, gdt)
+        elif op_1[0] == "i8" and p2 == INT8 and GELU_ONE_PASS:
+            # INT8 FF1 -> INT8 FF2: the GEMM also reduces max(h), then one pass
+            # quantizes gelu(h) (no GELU(h) stored, no absmax pass; bit-identical)
+            wq1, ws1, w16_1 = _weights(L.ff1)
+            h, hmax = ops.gemm_s8_ymax(op_1[1], wq1, op_1[2], ws1,
+                                       L.ff1.bias.detach() if L.ff1.bias is not None else None)
+            h_dtype = h.dtype
         else:
             h, w16_1 = _linear_fwd(L.ff1, op_1)
             h_dtype = h.dtype
         _mark("fwd", pre + ".gelu")
-        if p2 == INT8:
+        if p2 == INT8 and hmax is not None:
+            gq, gs, gp, g16 = ops.gelu_quantize(h, hmax)
+            op_2 = ("i8", gq, gs, g16)
+        elif p2 == INT8:
             if h is not None and FF2_INT8_RECOMPUTE:
                 # two reads of h, GELU evaluated in both (absmax, then quantize +
                 # GELU' + FP16 q): g is never stored (bit-identical q, s, GELU')

@@ -601,6 +601,42 @@ def gemm_gelu(a: torch.Tensor, b: torch.Tensor, scale_a=None, scale_b=None, bias
     return am, g, d
 
 
+def gemm_s8_ymax(a: torch.Tensor, b: torch.Tensor, scale_a, scale_b, bias=None, b_per_channel: bool = True):
+    """(y FP32 as gemm_s8_ex, ymax[1] = max(0, max y))."""
+    _req(a, "a", (torch.int8,))
+    _req(b, "b", (torch.int8,))
+    M, K = a.shape
+    N = b.shape[0]
+    c = torch.empty((M, N), device=a.device, dtype=torch.float32)
+    ym = torch.empty(1, device=a.device, dtype=torch.float32)
+    ev = _timed("gemm_s8", 2.0 * M * N * K)
+    call("qsync_gemm_s8_ymax", _ptr(a), _ptr(b), M, N, K, _ptr(c), _ptr(scale_a), _ptr(scale_b),
+         int(b_per_channel), _ptr(bias), _ptr(ym), _stream())
+    if ev is not None:
+        ev.record()
+    return c, ym
+
+
+def gelu_quantize(h: torch.Tensor, hmax: torch.Tensor, want_dact: bool = True, want_q16: bool = True):
+    """FF2's INT8 operand from FF1's FP32 output in one pass (qsync_gelu_quantize):
+    (q, s[1], GELU'(h) FP16 or None, FP16(q) or None) == quantize_act(gelu(h))."""
+    _req(h, "h", (torch.float32,))
+    q = torch.empty(h.shape, device=h.device, dtype=torch.int8)
+    s = torch.empty(2, device=h.device, dtype=torch.float32)
+    d = torch.empty(h.shape, device=h.device, dtype=torch.float16) if want_dact else None
+    h16 = torch.empty(h.shape, device=h.device, dtype=torch.float16) if want_q16 else None
+    call("qsync_gelu_quantize", _ptr(h), h.numel(), _ptr(hmax), _ptr(q), _ptr(h16), _ptr(d), _ptr(s), _stream())
+    return q, s[:1], d, h16
+
+
+def gelu_fp32_check():
+    """(monotonicity violations above 0.1701 over float32 [0, 16], max |gelu| for h < 0)."""
+    out = torch.zeros(2, dtype=torch.int32, device="cuda")
+    call("qsync_gelu_fp32_check", _ptr(out))
+    v = out.cpu()
+    return int(v[0]), float(v[1:2].view(torch.float32)[0])
+
+
 def zero_(t: torch.Tensor) -> torch.Tensor:
     """t.zero_() on this library's kernel (16-byte stores)."""
     if t.numel():

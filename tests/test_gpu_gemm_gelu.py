@@ -110,3 +110,34 @@ def test_fused_stack_with_gelu_epilogue(plan_kind):
         if g0.abs().max().item() == 0:
             continue
         assert ((g1 - g0).norm() / g0.norm()).item() < 1e-3, n
+
+
+def test_gelu_fp32_shortcut_preconditions():
+    """k_gelu_quant's shortcut (absmax(gelu(h)) = gelu(max h)) rests on two
+    properties of this library's float32 gelu, checked over EVERY float32 in
+    [-16, 16]: non-decreasing wherever it exceeds 0.1701, and |gelu(h)| < 0.1701
+    for h < 0."""
+    viol, negmax = ops.gelu_fp32_check()
+    assert viol == 0, f"{viol} monotonicity violations above 0.1701"
+    assert 0.16 < negmax < 0.1701, negmax
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 3072, 768), (333, 200, 160)])
+@pytest.mark.parametrize("shift", [0.0, -6.0])
+def test_gemm_ymax_then_gelu_quantize_bit_exact(M, N, K, shift):
+    """qsync_gemm_s8_ymax + qsync_gelu_quantize == gemm_s8_ex + gelu_absmax_store +
+    quantize_act (q, s, FP16(q), GELU').  shift -6 makes every h small, so the
+    kernel takes its exact absmax fallback (grid barrier)."""
+    opnd, bias = _operands(M, N, K, True, seed=5)
+    a, b, sa, sb = opnd
+    bias = bias + shift
+    h, ym = ops.gemm_s8_ymax(a, b, sa, sb, bias)
+    q, s, d, q16 = ops.gelu_quantize(h, ym)
+    h0 = ops.gemm_s8_ex(a, b, sa, sb, bias, out_dtype=torch.float32)
+    am, g0, d0 = ops.gelu_absmax_store(h0)
+    q0, s0, h16 = ops.quantize_act(g0, am, want_q16=True)
+    torch.cuda.synchronize()
+    assert torch.equal(h, h0)
+    assert ym.item() == max(0.0, h0.max().item())
+    assert torch.equal(s, s0) and torch.equal(q, q0) and torch.equal(q16, h16)
+    assert torch.equal(d.view(torch.int16), d0.view(torch.int16))

@@ -17,6 +17,7 @@ repetitions shows.
     python tools/ab_step.py dual=1,0              two MMA issuers on 192-wide single-unit GEMMs
     python tools/ab_step.py wgradpdl=1,0          side-stream wgrad GEMMs launched with PDL
     python tools/ab_step.py zero=1,0              gradient reset overlapping the forward
+    python tools/ab_step.py onepass=1,0           INT8 FF1 -> FF2 operand in one pass (GEMM ymax)
     QSB_AB_PLAN=int8 python tools/ab_step.py ...  plan for the non-plan knobs (default mixed)
 """
 import os
@@ -45,6 +46,7 @@ def step_ms(knob: str, val: str, steps: int = 40) -> float:
     _ts.ZERO_OVERLAP = not (knob == "zero" and val == "0")
     fused.ATTN_QUANT = not (knob == "attnq" and val == "0")
     fused.WGRAD_PDL = not (knob == "wgradpdl" and val == "0")
+    fused.GELU_ONE_PASS = not (knob == "onepass" and val == "0")
     from paper_2407_02327_b200 import ops as _ops
     _ops.set_dual_issue(not (knob == "dual" and val == "0"))
     m.apply_plan({"mixed": mixed_plan(cfg), "int8": uniform_plan(cfg, INT8), "fp16": uniform_plan(cfg, FP16)}[plan])
