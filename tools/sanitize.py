@@ -7,7 +7,11 @@ groups: gemm1 (1-CTA tcgen05 GEMM, INT8 + FP16, TMA store and reduce-add),
 gemm2 (CTA-pair cta_group::2), conv_tma / conv_gather (implicit conv, both
 operand loaders, fwd / dgrad / wgrad), attn1 / attn2 (tcgen05 attention, 1 and
 2 CTAs/SM backward), sr (mt19937_64 jump-ahead + SR), pdl (PDL zeroing kernel +
-atomic-max producer + quantizer chain), quant (streaming quantizers).
+atomic-max producer + quantizer chain), quant (streaming quantizers); round 2:
+dual (two MMA issuers per CTA), streamk (stream-K fixup through the workspace +
+arrival counters), gelu1 (FF1 GEMM with max(h) + the one-pass GELU quantizer,
+shortcut and grid-barrier fallback), attnq (attention + quantizer behind a grid
+barrier), head (classification head + the vector zero kernel).
 Shapes are small: the sanitizers replay every access.
 """
 import os
@@ -87,9 +91,61 @@ def quant():
     ops.dequantize_per_tensor(q.view(-1), s[:1])
 
 
+def dual():
+    ops.set_dual_issue(True)
+    M, N, K = 512, 384, 512  # 4 x 2 tiles of 128 x 192 <= SMs: one unit per CTA
+    a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
+    b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
+    ops.gemm_s8_ex(a, b, torch.tensor([0.01], device="cuda"), torch.rand(N, device="cuda") * 0.01)
+    ah, bh = torch.randn(M, K, device="cuda").half(), torch.randn(K, N, device="cuda").half()
+    ops.gemm_f16(ah, bh, b_mn=True)
+
+
+def streamk():
+    ops.set_streamk(1)
+    try:
+        M, N, K = 384, 512, 1024
+        a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
+        b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
+        ops.gemm_s8_ex(a, b, torch.tensor([0.01], device="cuda"), torch.rand(N, device="cuda") * 0.01)
+        acc = torch.zeros(M, N, device="cuda")
+        ah, bh = torch.randn(K, M, device="cuda").half(), torch.randn(K, N, device="cuda").half()
+        ops.gemm_f16(ah, bh, out=acc, accumulate=True, a_mn=True, b_mn=True)
+    finally:
+        ops.set_streamk(-1)
+
+
+def gelu1():
+    M, N, K = 256, 512, 256
+    a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
+    b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
+    sb = torch.rand(N, device="cuda") * 0.01
+    for shift in (0.0, -50.0):  # shortcut, then the grid-barrier fallback
+        h, ym = ops.gemm_s8_ymax(a, b, torch.tensor([0.01], device="cuda"), sb,
+                                 torch.full((N,), shift, device="cuda"))
+        ops.gelu_quantize(h, ym)
+
+
+def attnq():
+    qkv = torch.randn(2, 128, 3, 2, 64, device="cuda").half()
+    ops.attention_fwd_quant(qkv)
+
+
+def head():
+    x = torch.randn(4, 16, 256, device="cuda")
+    wp, bp = torch.randn(256, 256, device="cuda") * 0.05, torch.zeros(256, device="cuda")
+    wc, bc = torch.randn(3, 256, device="cuda") * 0.05, torch.zeros(3, device="cuda")
+    labels = torch.randint(0, 3, (4,), device="cuda")
+    loss, pooled, probs = ops.cls_head_fwd(x, wp, bp, wc, bc, labels)
+    grads = [torch.zeros_like(t) for t in (wp, bp, wc, bc)]
+    ops.cls_head_bwd(x, wp, wc, labels, pooled, probs, torch.ones(1, device="cuda"), *grads)
+    ops.zero_(torch.randn(1001, device="cuda")[1:])
+
+
 GROUPS = {"gemm1": lambda: gemm(1), "gemm2": lambda: gemm(2), "conv_tma": lambda: conv(1),
           "conv_gather": lambda: conv(0), "attn1": lambda: attn(1), "attn2": lambda: attn(2), "sr": sr,
-          "pdl": pdl, "quant": quant}
+          "pdl": pdl, "quant": quant, "dual": dual, "streamk": streamk, "gelu1": gelu1, "attnq": attnq,
+          "head": head}
 
 
 def main():
