@@ -101,6 +101,39 @@ def graph_step_ms(cfg: BertConfig, batch: int, plan: dict, steps: int = 20) -> f
     return ms
 
 
+def graph_fwd_ms(cfg: BertConfig, batch: int, plan: dict, steps: int = 20) -> float:
+    """The forward pass of the fused train step alone, as one CUDA graph (the
+    forward has no side-stream overlap; used to calibrate forward and backward
+    regions separately)."""
+    from .train_step import TrainStep
+    torch.manual_seed(0)
+    m = BertEncoderStack(cfg).cuda()
+    m.apply_plan(plan)
+    st = TrainStep(m, batch=batch, graph=False)  # fused layers + the optimizer's prepared weight copies
+    tok, lab = st.tokens.random_(0, cfg.vocab), st.labels
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            m(tok, lab)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        m(tok, lab)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del g, st, m
+    torch.cuda.empty_cache()
+    return ms
+
+
 # ----------------------------------------------------------------------------- graph
 def bert_graph(cfg: BertConfig, batch: int) -> dict:
     T, H, Fh = batch * cfg.seq, cfg.hidden, cfg.ffn
@@ -349,11 +382,20 @@ def measure_fused_costs(cfg: BertConfig, batch: int, reps: int = 5, calibrate: b
         torch.cuda.empty_cache()
     diag = {}
     for p in (INT8, FP16, FP32):
+        # Forward and backward calibrated separately: only the backward overlaps
+        # (wgrad side stream) -- one factor over-shrank the forward regions and
+        # over-predicted the backward ones.  fwd + cast regions -> the graphed
+        # forward; bwd + opt regions -> the rest of the graphed step.
+        plan = uniform_plan(cfg, p) if p != FP32 else {}
         tot = sum(per[p].values())
-        graph_ns = graph_step_ms(cfg, batch, uniform_plan(cfg, p) if p != FP32 else {}) * 1e6
-        scale = graph_ns / tot if calibrate else 1.0
-        diag[p] = {"eager_regions_ms": tot / 1e6, "graph_step_ms": graph_ns / 1e6, "scale": scale}
-        per[p] = {k: v * scale for k, v in per[p].items()}
+        tot_f = sum(v for (k, _), v in per[p].items() if k in ("fwd", "cast"))
+        graph_ns = graph_step_ms(cfg, batch, plan) * 1e6
+        fwd_ns = graph_fwd_ms(cfg, batch, plan) * 1e6
+        sf = fwd_ns / tot_f if calibrate and tot_f > 0 else 1.0
+        sb = (graph_ns - fwd_ns) / (tot - tot_f) if calibrate and tot > tot_f else 1.0
+        diag[p] = {"eager_regions_ms": tot / 1e6, "graph_step_ms": graph_ns / 1e6, "graph_fwd_ms": fwd_ns / 1e6,
+                   "scale_fwd": sf, "scale_bwd": sb, "scale": graph_ns / tot if tot else 1.0}
+        per[p] = {k: v * (sf if k[0] in ("fwd", "cast") else sb) for k, v in per[p].items()}
     measure_fused_costs.last_diag = diag
     for p in per:  # the pooler is costed from its kernels (measure_linear); its autograd
         # backward region stays with the head's, as before the head had marks
@@ -382,13 +424,18 @@ def measure_fused_costs(cfg: BertConfig, batch: int, reps: int = 5, calibrate: b
     med = statistics.median
 
     def fixed(op, mem):
-        es = [entry(op, p, mem) for p in (INT8, FP16, FP32)]
-        tot = int(med(e["pure_cost_ns"] for e in es))
-        return {FP32: {"pure_cost_ns": tot, "fwd_fraction": med(e["fwd_fraction"] for e in es),
-                       "memory_bytes": mem}}
+        # The FP32 plan's region: in the INT8 / FP16 plans a fixed op's region
+        # also holds the conversion of its output for the next planned op
+        # (LayerNorm + quantizer / FP16 copy, attention + quantizer), which the
+        # cast model charges at that precision boundary.
+        e = entry(op, FP32, mem)
+        return {FP32: {"pure_cost_ns": e["pure_cost_ns"], "fwd_fraction": e["fwd_fraction"], "memory_bytes": mem}}
 
     costs["embed"] = fixed("embed", cfg.vocab * H * 4 * 4 + T * H * 4)
-    costs["loss"] = fixed("loss", H * cfg.num_labels * 16 + batch * H * 4)
+    loss = fixed("loss", H * cfg.num_labels * 16 + batch * H * 4)
+    # the head's regions also hold the pooler's kernels, costed above from its own
+    loss[FP32]["pure_cost_ns"] = max(1, loss[FP32]["pure_cost_ns"] - pooler[FP32]["pure_cost_ns"])
+    costs["loss"] = loss
     for i in range(cfg.layers):
         L = f"layer{i}"
         for k, (M, N, K) in shapes.items():
