@@ -1013,11 +1013,28 @@ int qsync_attention_fwd_quant(const void* qkv, int64_t B, int64_t S, int64_t H, 
         QSB_TRY(cuda_status(cudaGetDevice(&dev), "cudaGetDevice"));
         QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_attn_fwd_tc<true>), kTcFwdSmem));
         if (dev < 16 && occ[dev] == 0) {
-            int n = 0;
-            QSB_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_attn_fwd_tc<true>, kTcThreads,
-                                                                              kTcFwdSmem),
-                                "cudaOccupancyMaxActiveBlocksPerMultiprocessor"));
-            occ[dev] = n > 0 ? std::min(n, 512 / 128) : -1;
+            // cudaOccupancyMaxActiveBlocksPerMultiprocessor answers 1 for ANY kernel that
+            // executes tcgen05.alloc (it cannot see the column count); the hardware keeps
+            // 4 of these blocks per SM resident (measured: a 4 x 148-block grid of
+            // 128-thread, 50 KB, 128-column blocks all pass a barrier). So count the
+            // per-SM limits here: shared memory, registers (per warp, 256-register
+            // granules), threads, and TMEM columns.
+            cudaFuncAttributes fa{};
+            QSB_TRY(cuda_status(cudaFuncGetAttributes(&fa, k_attn_fwd_tc<true>), "cudaFuncGetAttributes"));
+            int smem_sm = 0, regs_sm = 0, thr_sm = 0, resv = 0;
+            QSB_TRY(cuda_status(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev),
+                                "cudaDeviceGetAttribute"));
+            QSB_TRY(cuda_status(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev),
+                                "cudaDeviceGetAttribute"));
+            QSB_TRY(cuda_status(cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev),
+                                "cudaDeviceGetAttribute"));
+            QSB_TRY(cuda_status(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev),
+                                "cudaDeviceGetAttribute"));
+            const int smem_blk = ((kTcFwdSmem + static_cast<int>(fa.sharedSizeBytes) + resv + 1023) / 1024) * 1024;
+            const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+            const int n = std::min({smem_sm / smem_blk, regs_sm / (regs_warp * (kTcThreads / 32)),
+                                    thr_sm / kTcThreads, 512 / 128});
+            occ[dev] = n > 0 ? n : -1;
         }
         const int per_sm = dev < 16 ? occ[dev] : 0;
         fused = per_sm > 0 && blocks <= static_cast<int64_t>(per_sm) * sm_count();

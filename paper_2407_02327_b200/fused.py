@@ -243,7 +243,11 @@ GELU_ONE_PASS = True
 
 # INT8 O projection: its operand quantized inside the attention kernel
 # (qsync_attention_fwd_quant) instead of a quantize_act pass over the output.
-ATTN_QUANT = True
+# Off: bit-identical but ~2 us per layer slower (the grid barrier waits for the
+# slowest (batch, head) block and holds the dependents' launch; the separate
+# one-pass quantizer reads the 3 MB output from L2 under PDL).  ab_step attnq=1,0:
+# int8 plan 4.71 vs 4.69 ms, mixed 4.52 vs 4.49.
+ATTN_QUANT = False
 
 # INT8 FF2 operand from h: absmax(gelu(h)) then quantize(gelu(h)) with GELU'
 # (GELU evaluated twice, g never stored: 162 MB moved at [4096, 3072] FP32 h)
