@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "ptx.cuh"
 #include "vec.cuh"
 
 #ifndef QSB_LN_FWD_MINB
@@ -335,7 +336,11 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy,
 #ifndef QSB_LN_BWD_MINB
 #define QSB_LN_BWD_MINB 2
 #endif
-template <int NV>
+// ST > 0: each pair's rows of dy and s are staged in shared memory by 1-D bulk
+// copies issued ST rows ahead (mbarrier per stage), so a pair keeps ST rows of
+// loads in flight through its reductions and stores; ST = 0 loads straight into
+// registers.
+template <int NV, int ST>
 __global__ void __launch_bounds__(256, QSB_LN_BWD_MINB) k_ln_bwd2(const float* __restrict__ dy,
                                                     const float* __restrict__ s,
                                                     const float* __restrict__ mean_in,
@@ -366,15 +371,55 @@ __global__ void __launch_bounds__(256, QSB_LN_BWD_MINB) k_ln_bwd2(const float* _
     }
     const float inv_n = 1.0f / static_cast<float>(cols);
     int parity = 0;
-    for (int64_t row = blockIdx.x * (int64_t)4 + pair; row < rows; row += pairs) {
-        const float mean = mean_in[row], rstd = rstd_in[row];
+    const int64_t row0 = blockIdx.x * (int64_t)4 + pair;
+    extern __shared__ __align__(16) float lnb_stage[];
+    __shared__ __align__(8) uint64_t lnb_bar[4][ST > 0 ? ST : 1];
+    float* stage = lnb_stage + static_cast<size_t>(pair) * (ST > 0 ? ST : 1) * 2 * cols;
+    const bool issuer = half == 0 && lane == 0;
+    const uint32_t row_bytes = static_cast<uint32_t>(cols) * 4u;
+    if constexpr (ST > 0) {
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < 4 * ST; ++i) ptx::mbar_init(&lnb_bar[i / ST][i % ST], 1);
+            ptx::fence_mbar_init();
+        }
+        __syncthreads();
+        if (issuer) {
+#pragma unroll
+            for (int k = 0; k < ST; ++k) {
+                const int64_t r = row0 + k * pairs;
+                if (r < rows) {
+                    ptx::mbar_arrive_expect_tx(&lnb_bar[pair][k], 2 * row_bytes);
+                    ptx::bulk_load_1d(stage + k * 2 * cols, dy + r * cols, row_bytes, &lnb_bar[pair][k]);
+                    ptx::bulk_load_1d(stage + k * 2 * cols + cols, s + r * cols, row_bytes, &lnb_bar[pair][k]);
+                }
+            }
+        }
+    }
+    float mean_n = 0.f, rstd_n = 0.f;
+    if (row0 < rows) {
+        mean_n = mean_in[row0];
+        rstd_n = rstd_in[row0];
+    }
+    int it = 0;
+    for (int64_t row = row0; row < rows; row += pairs, ++it) {
+        const float mean = mean_n, rstd = rstd_n;
+        if (row + pairs < rows) {  // next row's statistics in flight under this row
+            mean_n = mean_in[row + pairs];
+            rstd_n = rstd_in[row + pairs];
+        }
+        const float* dyr = dy + row * cols + cbase;
+        const float* sr = s + row * cols + cbase;
+        if constexpr (ST > 0) {
+            ptx::mbar_wait(&lnb_bar[pair][it % ST], static_cast<uint32_t>(it / ST) & 1u);
+            dyr = stage + (it % ST) * 2 * cols + cbase;
+            sr = dyr + cols;
+        }
         float4 xh[NH], gy[NH];
         float s1 = 0.0f, s2 = 0.0f;
 #pragma unroll
         for (int i = 0; i < NH; ++i) {
-            const int64_t off = row * cols + cbase + 4 * (lane + 32 * i);
-            const float4 d = *reinterpret_cast<const float4*>(dy + off);
-            const float4 x = *reinterpret_cast<const float4*>(s + off);
+            const float4 d = reinterpret_cast<const float4*>(dyr)[lane + 32 * i];
+            const float4 x = reinterpret_cast<const float4*>(sr)[lane + 32 * i];
             xh[i] = make_float4((x.x - mean) * rstd, (x.y - mean) * rstd, (x.z - mean) * rstd,
                                 (x.w - mean) * rstd);
             gy[i] = make_float4(d.x * g[i].x, d.y * g[i].y, d.z * g[i].z, d.w * g[i].w);
@@ -396,6 +441,17 @@ __global__ void __launch_bounds__(256, QSB_LN_BWD_MINB) k_ln_bwd2(const float* _
         s1 += xb[parity][pair][half ^ 1][0];
         s2 += xb[parity][pair][half ^ 1][1];
         parity ^= 1;
+        if constexpr (ST > 0) {
+            // both warps of the pair have read this stage (the named barrier above):
+            // refill it with the row ST iterations ahead
+            const int64_t r = row + ST * pairs;
+            if (issuer && r < rows) {
+                const int k = it % ST;
+                ptx::mbar_arrive_expect_tx(&lnb_bar[pair][k], 2 * row_bytes);
+                ptx::bulk_load_1d(stage + k * 2 * cols, dy + r * cols, row_bytes, &lnb_bar[pair][k]);
+                ptx::bulk_load_1d(stage + k * 2 * cols + cols, s + r * cols, row_bytes, &lnb_bar[pair][k]);
+            }
+        }
         const float m1 = s1 * inv_n;
         const float m2 = s2 * inv_n;
 #pragma unroll
@@ -531,6 +587,17 @@ int ln_fwd_quant_nv(const float* a, const void* b, int b_dtype, const int64_t* t
                                               rstd, q, q16, qs, st);
 }
 
+// Bulk-staged LN backward (k_ln_bwd2<NV, ST > 0>): stage depth by row width so
+// two blocks per SM fit (4 pairs x ST stages x 2 rows x cols floats each).
+#ifndef QSB_LN_BWD_ST
+#define QSB_LN_BWD_ST 3
+#endif
+constexpr int ln_bwd_stages(int nv) { return QSB_LN_BWD_ST <= 0 ? 0 : (nv * 128 * 96 <= 90000 ? QSB_LN_BWD_ST : 2); }
+constexpr int ln_bwd_smem(int nv, int st) { return 4 * st * 2 * nv * 128 * 4; }
+inline bool ln_bwd_staged(const float* dy, const float* s) {
+    return QSB_LN_BWD_ST > 0 && aligned16(dy) && aligned16(s);
+}
+
 template <int NV>
 int ln_bwd_nv(const float* dy, const float* s, const float* mean, const float* rstd,
               const float* gamma, int64_t rows, int cols, float* dx, float* dgamma, float* dbeta,
@@ -540,7 +607,15 @@ int ln_bwd_nv(const float* dy, const float* s, const float* mean, const float* r
         // its column-partial reduction over as many rows as possible
         const int grid = static_cast<int>(std::min<int64_t>((rows + 3) / 4, sm_count() * int64_t(QSB_LN_BWD_MINB)));
         const int red4 = aligned16(dgamma) && aligned16(dbeta) && aligned16(dcol);
-        pdl_launch(k_ln_bwd2<NV>, dim3(grid), dim3(256), 0, st, dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
+        if (ln_bwd_staged(dy, s)) {
+            constexpr int ST = ln_bwd_stages(NV);
+            const int smem = ln_bwd_smem(NV, ST);
+            QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_ln_bwd2<NV, ST>), smem));
+            pdl_launch(k_ln_bwd2<NV, ST>, dim3(grid), dim3(256), smem, st, dy, s, mean, rstd, gamma, rows, cols, dx,
+                       dgamma, dbeta, reinterpret_cast<__half*>(dx16), dcol, red4, nullptr, nullptr, nullptr, 1);
+            return check_launch("k_ln_bwd<staged>");
+        }
+        pdl_launch(k_ln_bwd2<NV, 0>, dim3(grid), dim3(256), 0, st, dy, s, mean, rstd, gamma, rows, cols, dx, dgamma, dbeta,
                                              reinterpret_cast<__half*>(dx16), dcol, red4, nullptr, nullptr, nullptr, 1);
         return check_launch("k_ln_bwd");
     }
@@ -569,10 +644,18 @@ int embed_ln_bwd_nv(const float* dy, const float* s, const float* mean, const fl
                     const int64_t* tok, int64_t rows, int seq, int cols, float* dgamma, float* dbeta,
                     float* dword, float* dpos, float* dtyp, cudaStream_t st) {
     const int grid = static_cast<int>(std::min<int64_t>((rows + 3) / 4, sm_count() * int64_t(QSB_LN_BWD_MINB)));
-    pdl_launch(k_ln_bwd2<NV>, dim3(grid), dim3(256), 0, st, dy, s, mean, rstd, gamma, rows, cols, static_cast<float*>(nullptr), dgamma, dbeta,
-                                         static_cast<__half*>(nullptr), dtyp,
-                                         static_cast<int>(aligned16(dgamma) && aligned16(dbeta) && aligned16(dtyp)),
-                                         tok, dword, dpos, seq);
+    const int red4 = static_cast<int>(aligned16(dgamma) && aligned16(dbeta) && aligned16(dtyp));
+    if (ln_bwd_staged(dy, s)) {
+        constexpr int ST = ln_bwd_stages(NV);
+        const int smem = ln_bwd_smem(NV, ST);
+        QSB_TRY(ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_ln_bwd2<NV, ST>), smem));
+        pdl_launch(k_ln_bwd2<NV, ST>, dim3(grid), dim3(256), smem, st, dy, s, mean, rstd, gamma, rows, cols,
+                   static_cast<float*>(nullptr), dgamma, dbeta, static_cast<__half*>(nullptr), dtyp, red4, tok, dword,
+                   dpos, seq);
+        return check_launch("k_ln_bwd<embed, staged>");
+    }
+    pdl_launch(k_ln_bwd2<NV, 0>, dim3(grid), dim3(256), 0, st, dy, s, mean, rstd, gamma, rows, cols, static_cast<float*>(nullptr), dgamma, dbeta,
+                                         static_cast<__half*>(nullptr), dtyp, red4, tok, dword, dpos, seq);
     return check_launch("k_ln_bwd<embed>");
 }
 

@@ -247,6 +247,14 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const 
         "r"(smem_u32(src)), "r"(x), "r"(y)
         : "memory");
 }
+// 1-D bulk copy global -> shared (16-byte aligned, bytes % 16 == 0), completing
+// on an mbarrier's transaction count.
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {

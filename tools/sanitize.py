@@ -11,7 +11,8 @@ atomic-max producer + quantizer chain), quant (streaming quantizers); round 2:
 dual (two MMA issuers per CTA), streamk (stream-K fixup through the workspace +
 arrival counters), gelu1 (FF1 GEMM with max(h) + the one-pass GELU quantizer,
 shortcut and grid-barrier fallback), attnq (attention + quantizer behind a grid
-barrier), head (classification head + the vector zero kernel).
+barrier), head (classification head + the vector zero kernel), ln (LayerNorm
+backward with bulk-copied row stages, plain and embedding scatter).
 Shapes are small: the sanitizers replay every access.
 """
 import os
@@ -142,10 +143,24 @@ def head():
     ops.zero_(torch.randn(1001, device="cuda")[1:])
 
 
+def ln():
+    T, H, V = 300, 768, 50  # rows not a multiple of the 4 rows per block
+    a, b = torch.randn(T, H, device="cuda"), torch.randn(T, H, device="cuda")
+    g, be = torch.rand(H, device="cuda") + 0.5, torch.randn(H, device="cuda")
+    y, s, m, r = ops.layernorm_fwd(a, b, g, be, 1e-12)
+    dg, db, col = (torch.zeros(H, device="cuda") for _ in range(3))
+    ops.layernorm_bwd_ex(torch.randn(T, H, device="cuda"), s, m, r, g, dg, db, True, col)
+    tok = torch.randint(0, V, (3, T // 3), device="cuda")
+    word, pos, typ = torch.randn(V, H, device="cuda"), torch.randn(T // 3, H, device="cuda"), torch.randn(2, H, device="cuda")
+    y, s, m, r = ops.embed_layernorm_fwd(tok, word, pos, typ, g, be, 1e-12)[:4]
+    ops.embed_layernorm_bwd(torch.randn(T, H, device="cuda"), s, m, r, g, tok, dg, db, torch.zeros_like(word),
+                            torch.zeros_like(pos), torch.zeros(H, device="cuda"))
+
+
 GROUPS = {"gemm1": lambda: gemm(1), "gemm2": lambda: gemm(2), "conv_tma": lambda: conv(1),
           "conv_gather": lambda: conv(0), "attn1": lambda: attn(1), "attn2": lambda: attn(2), "sr": sr,
           "pdl": pdl, "quant": quant, "dual": dual, "streamk": streamk, "gelu1": gelu1, "attnq": attnq,
-          "head": head}
+          "head": head, "ln": ln}
 
 
 def main():
