@@ -1126,10 +1126,14 @@ __global__ void __launch_bounds__(256) k_gelu_quant(const float* __restrict__ h,
     const float hm = fmaxf(*hmax, 0.0f);
     const float gm = gelu_erf<false>(hm);
     bool fast = gm >= kGeluMonoFloor;
-    if (fast) {  // no float just below hmax may have a larger gelu (ulp-level dips)
+    if (fast) {  // no float just below hmax may have a larger gelu (ulp-level dips):
+        // lane k-1 of every warp checks hmax - k ulps, k = 1 .. kGeluGap-1
+        static_assert(kGeluGap <= 32, "one candidate per lane");
         const uint32_t hb = __float_as_uint(hm);
-        for (int k = 1; k < kGeluGap && static_cast<uint32_t>(k) <= hb; ++k)
-            fast = fast && !(gelu_erf<false>(__uint_as_float(hb - k)) > gm);
+        const uint32_t k = (threadIdx.x & 31) + 1;
+        const bool dip = k < static_cast<uint32_t>(kGeluGap) && k <= hb &&
+                         gelu_erf<false>(__uint_as_float(hb - k)) > gm;
+        fast = !__any_sync(0xffffffffu, dip);
     }
     float am = gm;
     if (!fast) {  // exact fallback: absmax over gelu(h)
