@@ -589,10 +589,14 @@ int ln_fwd_quant_nv(const float* a, const void* b, int b_dtype, const int64_t* t
 
 // Bulk-staged LN backward (k_ln_bwd2<NV, ST > 0>): stage depth by row width so
 // two blocks per SM fit (4 pairs x ST stages x 2 rows x cols floats each).
+// Two stages measured best in the step (ab_step lib=: 4.466 ms vs 4.48 with 1
+// or 3; the side-stream GEMMs co-schedule better next to smaller blocks).
 #ifndef QSB_LN_BWD_ST
-#define QSB_LN_BWD_ST 3
+#define QSB_LN_BWD_ST 2
 #endif
-constexpr int ln_bwd_stages(int nv) { return QSB_LN_BWD_ST <= 0 ? 0 : (nv * 128 * 96 <= 90000 ? QSB_LN_BWD_ST : 2); }
+constexpr int ln_bwd_stages(int nv) {
+    return QSB_LN_BWD_ST <= 0 ? 0 : (32 * QSB_LN_BWD_ST * nv * 128 <= 90000 ? QSB_LN_BWD_ST : 1);
+}
 constexpr int ln_bwd_smem(int nv, int st) { return 4 * st * 2 * nv * 128 * 4; }
 inline bool ln_bwd_staged(const float* dy, const float* s) {
     return QSB_LN_BWD_ST > 0 && aligned16(dy) && aligned16(s);
