@@ -10,7 +10,8 @@ producer warp gathers it tile by tile from the NHWC input (implicit GEMM,
             tensor, per-channel weight scales, tcgen05 kind::i8 GEMM with the fused
             dequant + bias epilogue -> FP32 NHWC output (graph.hpp:38-40).
   * FP16 -- FP16 im2col, tcgen05 kind::f16 GEMM -> FP16 NHWC output.
-  * FP32 -- cuDNN-free FP32 path via torch (training devices stay FP32).
+  * FP32 -- im2col (in place for 1x1/s1) + the tcgen05 3xTF32 GEMM (training
+            devices stay FP32, replayer.cpp:96-101).
 Backward of INT8/FP16 runs in FP16 (cost_mapper.cpp:13-15): dgrad = the implicit
 GEMM over dY taps (`qsync_conv_dgrad_implicit`, Cout % 64 == 0) or col2im(dY16 W16),
 FP32 out; wgrad = dY16^T A16 (times s_x for INT8) in FP32 (cost_mapper.cpp:48-50),
@@ -21,7 +22,6 @@ and widens it there (the paper's backward casting cost).
 from __future__ import annotations
 
 import torch
-import torch.nn.functional as F
 
 from . import ops
 from .qlinear import FP16, FP32, INT8
@@ -117,12 +117,66 @@ class _QConv(torch.autograd.Function):
         return dx, dw, db, None, None
 
 
+def _cols32(x, R, S, stride, pad, kp):
+    """FP32 column matrix [N*P*Q, kp]: a 1x1/stride-1 conv reads x in place; otherwise
+    the byte-exact im2col runs over x viewed as FP16 pairs (each tap's channel run is
+    contiguous, so C FP32 channels are 2C 16-bit lanes; zero padding is 0.0f)."""
+    N, H, W, C = x.shape
+    if R == 1 and S == 1 and tuple(stride) == (1, 1) and tuple(pad) == (0, 0) and kp == C:
+        return x.reshape(N * H * W, C), (H, W)
+    A, pq = ops.im2col(x.view(torch.float16), R, S, stride, pad, ld=2 * kp)
+    return A.view(torch.float32), pq
+
+
+class _QConv32(torch.autograd.Function):
+    """FP32 Conv2d (training devices stay FP32, replayer.cpp:96-101) on the library's
+    tcgen05 3xTF32 GEMM (qsync_gemm_f32, FP32-level accuracy): y = cols(x) W^T,
+    dgrad = col2im(dY W) (1x1/s1: dY W itself), wgrad = dY^T cols(x)."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, geom):
+        R, S, stride, pad = geom
+        N, H, W, C = x.shape
+        cout = w.shape[0]
+        K = R * S * C
+        kp = (K + 3) // 4 * 4
+        w2 = _pad_k(w.reshape(cout, K), kp)
+        A, (P, Q) = _cols32(x, R, S, stride, pad, kp)
+        y = ops.gemm_f32(A, w2, bias=b)
+        ctx.save_for_backward(x, w2)
+        ctx.geom, ctx.kp, ctx.has_bias, ctx.shapes = geom, kp, b is not None, (N, H, W, C, cout, P, Q, K)
+        return y.view(N, P, Q, cout)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, w2 = ctx.saved_tensors
+        R, S, stride, pad = ctx.geom
+        N, H, W, C, cout, P, Q, K = ctx.shapes
+        dy2 = dy.reshape(N * P * Q, cout).float().contiguous()
+        dx = dw = db = None
+        if ctx.needs_input_grad[0]:
+            dcol = ops.gemm_f32(dy2, w2, b_mn=True)  # [NPQ, kp]
+            if R == 1 and S == 1 and tuple(stride) == (1, 1) and tuple(pad) == (0, 0) and ctx.kp == C:
+                dx = dcol.view(N, H, W, C)
+            else:
+                dx = ops.col2im(dcol, (N, H, W, C), R, S, stride, pad)
+        if ctx.needs_input_grad[1]:
+            A, _ = _cols32(x, R, S, stride, pad, ctx.kp)
+            # K of this GEMM is the pixel count (802,816 for conv1 at batch 64) while
+            # M x N is tiny: accumulating into a zeroed buffer lets it split K over the SMs
+            dw2 = torch.zeros((cout, ctx.kp), device=dy.device, dtype=torch.float32)
+            ops.gemm_f32(dy2, A, out=dw2, accumulate=True, a_mn=True, b_mn=True)
+            dw = dw2[:, :K].reshape(cout, R, S, C)
+        if ctx.has_bias and ctx.needs_input_grad[2]:
+            db = dy2.sum(0)
+        return dx, dw, db, None
+
+
 def qconv2d(x, w, b, stride=(1, 1), pad=(0, 0), precision=FP32):
     """x NHWC [N,H,W,C], w KRSC [Cout,R,S,C] -> y NHWC [N,P,Q,Cout]."""
     cout, R, S, C = w.shape
     if precision == FP32:
-        y = F.conv2d(x.permute(0, 3, 1, 2).float(), w.permute(0, 3, 1, 2), b, stride, pad)
-        return y.permute(0, 2, 3, 1)
+        return _QConv32.apply(x.float().contiguous(), w, b, (R, S, tuple(stride), tuple(pad)))
     if precision not in (INT8, FP16):
         raise ValueError(f"validation: unknown precision \"{precision}\"")
     return _QConv.apply(x.contiguous(), w, b, (R, S, tuple(stride), tuple(pad)), precision)

@@ -70,3 +70,30 @@ def test_fp32_qlinear_on_tensor_cores():
     assert _nrel(x.grad, dy.double() @ w64) < 1e-4
     assert _nrel(w.grad, dy.double().t() @ x64) < 1e-4
     assert _nrel(b.grad, dy.double().sum(0)) < 1e-6
+
+
+@pytest.mark.parametrize("geom", [
+    # (N, H, C, Cout, R, stride, pad): the ResNet-50 kinds -- 7x7/2 stem (C = 3),
+    # 1x1/1 (read in place), 3x3/1, 3x3/2, 1x1/2 downsample, odd channel counts
+    (2, 32, 3, 64, 7, 2, 3), (2, 14, 64, 256, 1, 1, 0), (2, 14, 64, 64, 3, 1, 1),
+    (2, 15, 128, 128, 3, 2, 1), (2, 14, 256, 512, 1, 2, 0), (1, 9, 5, 7, 3, 1, 1)])
+def test_fp32_conv_on_tensor_cores(geom):
+    """FP32-planned Conv2d (im2col + 3xTF32 GEMM, col2im dgrad, GEMM wgrad) against
+    float64 autograd: forward, dgrad and wgrad within 1e-5 of the norm."""
+    import torch.nn.functional as F
+
+    from paper_2407_02327_b200.qconv import qconv2d
+    N, H, C, Co, R, st, pd = geom
+    g = torch.Generator(device="cuda").manual_seed(sum(geom))
+    x = torch.randn(N, H, H, C, device="cuda", generator=g, requires_grad=True)
+    w = (torch.randn(Co, R, R, C, device="cuda", generator=g) / (R * R * C) ** 0.5).requires_grad_(True)
+    b = torch.randn(Co, device="cuda", generator=g, requires_grad=True)
+    y = qconv2d(x, w, b, (st, st), (pd, pd), "FP32")
+    gy = torch.randn(y.shape, device="cuda", generator=g)
+    dx, dw, db = torch.autograd.grad(y, (x, w, b), gy)
+    xd, wd, bd = (t.detach().double().requires_grad_(True) for t in (x, w, b))
+    yr = F.conv2d(xd.permute(0, 3, 1, 2), wd.permute(0, 3, 1, 2), bd, st, pd).permute(0, 2, 3, 1)
+    dxr, dwr, dbr = torch.autograd.grad(yr, (xd, wd, bd), gy.double())
+    assert y.dtype == torch.float32 and y.shape == yr.shape
+    for got, ref in ((y, yr), (dx, dxr), (dw, dwr), (db, dbr)):
+        assert _nrel(got, ref) < 1e-5

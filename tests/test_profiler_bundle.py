@@ -212,3 +212,44 @@ def test_fused_bundle_closes_the_loop(tmp_path, reflib):
     pred_ms = reflib.replay_bundle(str(path), plan) / 1e6
     meas_ms = graph_step_ms(cfg, batch, plan["per_device"]["infer"])
     assert abs(pred_ms - meas_ms) / meas_ms < 0.25
+
+
+def test_resnet50_bundle_accepted_by_reference_planner(tmp_path, reflib):
+    """The conv model's graph (53 adjustable convs, fixed BN/add, fc) with conv op
+    costs goes through the unmodified reference score / solve / replay."""
+    from paper_2407_02327_b200.profiler_resnet import conv_memory_bytes, resnet50_graph
+    from paper_2407_02327_b200.resnet import conv_specs
+    batch = 8
+    g = resnet50_graph(batch)
+    adj = [n["id"] for n in g["nodes"] if n["kind"] == "adjustable"]
+    assert len(adj) == 54 and "fc" in adj  # 53 convs + classifier
+    specs = {s[0]: s for s in conv_specs(batch)}
+    speed = {INT8: 0.5, FP16: 0.7, FP32: 1.0}
+    costs = {}
+    for n in g["nodes"]:
+        costs[n["id"]] = {}
+        for p in n["supported_precisions"]:
+            if n["id"] in specs:
+                _, nb, h, _, c, cout, r, _, _, _ = specs[n["id"]]
+                mem = conv_memory_bytes(p, nb, h, c, cout, r)
+            else:
+                mem = n["output_numel"] * 4 + n["weight_numel"] * 16
+            costs[n["id"]][p] = {"pure_cost_ns": max(1, int(n["output_numel"] * speed[p] * 0.01)),
+                                 "fwd_fraction": 1.0 / 3.0, "memory_bytes": int(mem)}
+    stats = []
+    for s in range(2):
+        stats.append({op: {"norm_w_sq": 10.0, "norm_act_sq": 4e4, "norm_grad_act_sq": 1e-5,
+                           "d_act": 1e5, "d_w": 4e4, "d_grad": 1e5, "q_act": 0.03 + 0.01 * s,
+                           "q_w": 0.002, "e_act": 1, "e_w": -4, "e_grad": -14} for op in adj})
+    cap = default_cap(g, costs)
+    devices = [{"id": "trainer", "is_inference": False, "mem_capacity_bytes": 10**12},
+               {"id": "infer", "is_inference": True, "mem_capacity_bytes": cap}]
+    path = tmp_path / "rn50.json"
+    path.write_text(json.dumps(build_bundle(g, costs, _fake_casts(), stats, devices)))
+    omegas = {(op, p): w for op, p, w in reflib.score_bundle(str(path), 0, batch)}
+    assert omegas[("res3.0.b", "INT8")] > omegas[("res3.0.b", "FP16")] > 0
+    rep = reflib.plan_bundle(str(path), 0, batch, 50, "infer", cap)
+    assert rep["memory_ok"]
+    assert all(p == FP32 for p in rep["devices"]["trainer"].values())
+    assert any(rep["devices"]["infer"][op] != FP32 for op in adj)
+    assert reflib.replay_bundle(str(path), {"per_device": rep["devices"]}) > 0
