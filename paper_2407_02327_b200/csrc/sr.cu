@@ -33,6 +33,9 @@ constexpr uint64_t UPPER = 0xFFFFFFFF80000000ULL;
 constexpr uint64_t LOWER = 0x000000007FFFFFFFULL;
 constexpr uint64_t MATA = 0xB5026F5AA96619E9ULL;
 constexpr int kSrThreads = 320;  // 312 state words, 10 warps
+// The jump-ahead of a segment is split into kJumpParts partial sums (k_mt_jump).
+constexpr int kJumpParts = 8;
+constexpr int kJumpChunk = (mtjump::kPolyWords + kJumpParts - 1) / kJumpParts;  // poly words per part
 
 __device__ __forceinline__ uint64_t temper(uint64_t y) {
     y ^= (y >> 29) & 0x5555555555555555ULL;
@@ -95,7 +98,12 @@ __global__ void __launch_bounds__(kSrThreads) k_sr(const SrArgs a) {
     const int64_t first = static_cast<int64_t>(blockIdx.x) * a.seg_len;
     const int64_t last = min(a.n, first + a.seg_len);
     if (first >= last) return;
-    if (i < MT_N) st[i] = a.states[static_cast<int64_t>(blockIdx.x) * MT_N + i];
+    if (i < MT_N) {
+        uint64_t v = 0;
+        for (int y = 0; y < kJumpParts; ++y)
+            v ^= a.states[(static_cast<int64_t>(y) * gridDim.x + blockIdx.x) * MT_N + i];
+        st[i] = v;
+    }
     double q = a.q;
     if (MODE == kSrI8) q = static_cast<double>(*a.scale_dev);
     // Absolute draw index of element e is offset + e; its twist block is
@@ -134,23 +142,74 @@ __global__ void __launch_bounds__(kSrThreads) k_sr(const SrArgs a) {
 // Device jump-ahead: out state (312 words) for each segment b = sum over the
 // set bits i of poly_b of raw_window_i, where raw_window_i = raw[i .. i+312)
 // is the word window of the seed's raw recurrence sequence (raw[0..312) = the
-// seeded state, raw[312+t] = t-th generated word).  One CTA per segment.
+// seeded state, raw[312+t] = t-th generated word).  Grid (segment, part): part y
+// covers poly words [y*kJumpChunk, (y+1)*kJumpChunk) and writes its partial sum
+// to out[(y*nseg + b)*312 ..); k_sr XORs the parts.  The raw words that chunk
+// touches sit in shared memory, and the set bits are consumed four at a time
+// (independent loads into four accumulators) -- the loop was L2-latency bound
+// at one dependent load per bit.
 __global__ void __launch_bounds__(kSrThreads) k_mt_jump(const uint64_t* __restrict__ raw,
                                                         const uint64_t* __restrict__ polys,
                                                         int poly_words, uint64_t* __restrict__ out) {
+    __shared__ uint64_t sraw[kJumpChunk * 64 + MT_N];
+    __shared__ uint64_t spoly[kJumpChunk];
     const int i = threadIdx.x;
-    if (i >= MT_N) return;
+    const int w0 = blockIdx.y * kJumpChunk;
+    const int w1 = min(poly_words, w0 + kJumpChunk);
     const uint64_t* poly = polys + static_cast<int64_t>(blockIdx.x) * poly_words;
-    uint64_t acc = 0;
-    for (int w = 0; w < poly_words; ++w) {
-        uint64_t bits = poly[w];
+    const int nraw = max(0, (w1 - w0) * 64 + MT_N);
+    for (int j = i; j < nraw; j += blockDim.x) {
+        const int64_t g = static_cast<int64_t>(w0) * 64 + j;
+        sraw[j] = g < mtjump::kRawWords ? raw[g] : 0ull;
+    }
+    for (int j = i; j < w1 - w0; j += blockDim.x) spoly[j] = poly[w0 + j];
+    __syncthreads();
+    if (i >= MT_N) return;
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int w = 0; w < w1 - w0; ++w) {
+        uint64_t bits = spoly[w];  // uniform across the CTA
+        const uint64_t* base = sraw + w * 64 + i;
+#if QSB_JUMP_SETBITS
+        while (__popcll(bits) >= 4) {
+            const int b0 = __ffsll(static_cast<long long>(bits)) - 1;
+            bits &= bits - 1;
+            const int b1 = __ffsll(static_cast<long long>(bits)) - 1;
+            bits &= bits - 1;
+            const int b2 = __ffsll(static_cast<long long>(bits)) - 1;
+            bits &= bits - 1;
+            const int b3 = __ffsll(static_cast<long long>(bits)) - 1;
+            bits &= bits - 1;
+            a0 ^= base[b0];
+            a1 ^= base[b1];
+            a2 ^= base[b2];
+            a3 ^= base[b3];
+        }
         while (bits) {
             const int b = __ffsll(static_cast<long long>(bits)) - 1;
             bits &= bits - 1;
-            acc ^= raw[w * 64 + b + i];
+            a0 ^= base[b];
         }
+#else
+        // all 64 positions unrolled: constant smem offsets, predicated loads
+        // (the predicate is uniform across the CTA), no bit-scan per set bit
+        const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
+#pragma unroll
+        for (int b = 0; b < 32; b += 4) {
+            if (lo & (1u << b)) a0 ^= base[b];
+            if (lo & (2u << b)) a1 ^= base[b + 1];
+            if (lo & (4u << b)) a2 ^= base[b + 2];
+            if (lo & (8u << b)) a3 ^= base[b + 3];
+        }
+#pragma unroll
+        for (int b = 0; b < 32; b += 4) {
+            if (hi & (1u << b)) a0 ^= base[32 + b];
+            if (hi & (2u << b)) a1 ^= base[33 + b];
+            if (hi & (4u << b)) a2 ^= base[34 + b];
+            if (hi & (8u << b)) a3 ^= base[35 + b];
+        }
+#endif
     }
-    out[static_cast<int64_t>(blockIdx.x) * MT_N + i] = acc;
+    out[(static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * MT_N + i] = a0 ^ a1 ^ a2 ^ a3;
 }
 
 // Raw recurrence sequence of a seed: raw[0..312) = seeded state, then words
@@ -222,7 +281,7 @@ int run_sr(int mode, SrArgs a, uint64_t seed, cudaStream_t st) {
                             "cudaMallocAsync"));
         QSB_TRY(cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&ws.polys), sizeof(uint64_t) * pw * nseg, st),
                             "cudaMallocAsync"));
-        QSB_TRY(cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&ws.states), sizeof(uint64_t) * MT_N * nseg, st),
+        QSB_TRY(cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&ws.states), sizeof(uint64_t) * MT_N * nseg * kJumpParts, st),
                             "cudaMallocAsync"));
         ws.cap_segments = nseg;
     }
@@ -233,7 +292,7 @@ int run_sr(int mode, SrArgs a, uint64_t seed, cudaStream_t st) {
                         "copy jump polynomials"));
     k_mt_raw<<<1, kSrThreads, 0, st>>>(seed, mtjump::kRawWords, ws.raw);
     QSB_TRY(check_launch("k_mt_raw"));
-    k_mt_jump<<<static_cast<unsigned>(nseg), kSrThreads, 0, st>>>(ws.raw, ws.polys, pw, ws.states);
+    k_mt_jump<<<dim3(static_cast<unsigned>(nseg), kJumpParts), kSrThreads, 0, st>>>(ws.raw, ws.polys, pw, ws.states);
     QSB_TRY(check_launch("k_mt_jump"));
     a.states = ws.states;
     switch (mode) {
