@@ -110,8 +110,18 @@ __global__ void __launch_bounds__(kSrThreads) k_sr(const SrArgs a) {
     // (offset+e)/312 and position (offset+e)%312.
     const uint64_t abs_first = a.offset + static_cast<uint64_t>(first);
     int64_t block_base = static_cast<int64_t>(abs_first / MT_N) * MT_N;  // absolute
+    // The next block's input is loaded before this block's twist, so the HBM
+    // latency overlaps the twist and the FP64 work (one block per iteration).
+    const auto fetch = [&](int64_t base) -> double {
+        const int64_t e = base + i - static_cast<int64_t>(a.offset);
+        if (MODE == kSrDraws || i >= MT_N || e < first || e >= last) return 0.0;
+        return MODE == kSrF64 ? a.x64[e] : static_cast<double>(a.x32[e]);
+    };
+    double xnext = fetch(block_base);
     __syncthreads();
     while (true) {
+        const double xcur = xnext;
+        xnext = fetch(block_base + MT_N);
         twist(st);
         const int64_t e = block_base + i - static_cast<int64_t>(a.offset);  // element index
         if (i < MT_N && e >= first && e < last) {
@@ -119,14 +129,14 @@ __global__ void __launch_bounds__(kSrThreads) k_sr(const SrArgs a) {
             if (MODE == kSrDraws) {
                 a.draws[e] = d;
             } else if (MODE == kSrF64) {
-                const double xbar = __ddiv_rn(__dsub_rn(a.x64[e], a.zp), q);
+                const double xbar = __ddiv_rn(__dsub_rn(xcur, a.zp), q);
                 const double lo = floor(xbar);
                 const double frac = __dsub_rn(xbar, lo);
                 const int64_t r = static_cast<int64_t>(lo) + (u01(d) < frac ? 1 : 0);
                 if (a.rounded) a.rounded[e] = r;
                 if (a.deq) a.deq[e] = __dadd_rn(__dmul_rn(q, static_cast<double>(r)), a.zp);
             } else {
-                const double xbar = __ddiv_rn(static_cast<double>(a.x32[e]), q);
+                const double xbar = __ddiv_rn(xcur, q);
                 const double lo = floor(xbar);
                 const double frac = __dsub_rn(xbar, lo);
                 int64_t r = static_cast<int64_t>(lo) + (u01(d) < frac ? 1 : 0);
