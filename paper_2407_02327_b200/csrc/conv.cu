@@ -22,6 +22,38 @@ struct ConvGeom {
     int64_t ld;  // row pitch of the column matrix (>= R*S*C)
 };
 
+// One thread per 16-byte chunk of the column matrix (C a multiple of the
+// vector width, fewer than 2^31 chunks): consecutive threads write consecutive
+// chunks, so every store is a full coalesced line whatever the row length.  The
+// warp-per-row kernel below leaves lanes idle when a row is not a multiple of
+// 32 chunks (C = 64 INT8 3x3: 36 chunks per row, 1.2 TB/s).
+template <typename T>
+__global__ void __launch_bounds__(256) k_im2col_chunks(const T* __restrict__ x, ConvGeom g,
+                                                       T* __restrict__ out, int items) {
+    constexpr int V = 16 / sizeof(T);
+    const int C = static_cast<int>(g.C), CV = C / V;
+    const int K = g.R * g.S * C;
+    const int nch = static_cast<int>(g.ld / V);
+    const int P = static_cast<int>(g.P), Q = static_cast<int>(g.Q);
+    const int H = static_cast<int>(g.H), W = static_cast<int>(g.W);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < items; i += gridDim.x * blockDim.x) {
+        const int row = i / nch;
+        const int j = i - row * nch;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (j * V < K) {
+            const int tap = j / CV;
+            const int c = (j - tap * CV) * V;
+            const int r = tap / g.S, ss = tap - r * g.S;
+            const int q = row % Q, t = row / Q;
+            const int p = t % P, n = t / P;
+            const int h = p * g.sh - g.ph + r * g.dh, w = q * g.sw - g.pw + ss * g.dw;
+            if (h >= 0 && h < H && w >= 0 && w < W)
+                v = *reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + h) * W + w) * C + c);
+        }
+        *reinterpret_cast<uint4*>(out + static_cast<int64_t>(row) * g.ld + static_cast<int64_t>(j) * V) = v;
+    }
+}
+
 // One warp per column row (n,p,q): the row's coordinates are decoded once, the
 // lanes stride over its 16-byte chunks (tap = chunk / (C/V), 32-bit math).
 // Scalar fallback (C not a multiple of the vector width) keeps one element per lane.
@@ -301,7 +333,11 @@ int qsync_im2col(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int6
                         : (g.ld % 16 == 0 && al(out))                          ? 2
                                                                                : 0;
         const int64_t work = g.N * g.P * g.Q;
-        if (vec == 2)
+        const int64_t chunks = work * (g.ld / 16);
+        if (vec == 1 && chunks < (int64_t(1) << 31))
+            k_im2col_chunks<int8_t><<<grid_of(chunks / 32 + 1), 256, 0, st>>>(
+                static_cast<const int8_t*>(x), g, static_cast<int8_t*>(out), static_cast<int>(chunks));
+        else if (vec == 2)
             k_im2col_narrow<int8_t><<<grid_of(work * (g.ld / 16) / 32 + 1), 256, 0, st>>>(
                 static_cast<const int8_t*>(x), g, static_cast<int8_t*>(out));
         else
@@ -312,7 +348,11 @@ int qsync_im2col(const void* x, int dtype, int64_t N, int64_t H, int64_t W, int6
                         : (g.ld % 8 == 0 && al(out))                         ? 2
                                                                              : 0;
         const int64_t work = g.N * g.P * g.Q;
-        if (vec == 2)
+        const int64_t chunks = work * (g.ld / 8);
+        if (vec == 1 && chunks < (int64_t(1) << 31))
+            k_im2col_chunks<uint16_t><<<grid_of(chunks / 32 + 1), 256, 0, st>>>(
+                static_cast<const uint16_t*>(x), g, static_cast<uint16_t*>(out), static_cast<int>(chunks));
+        else if (vec == 2)
             k_im2col_narrow<uint16_t><<<grid_of(work * (g.ld / 8) / 32 + 1), 256, 0, st>>>(
                 static_cast<const uint16_t*>(x), g, static_cast<uint16_t*>(out));
         else

@@ -35,6 +35,11 @@ def _pad_k(w2: torch.Tensor, kp: int) -> torch.Tensor:
     return out
 
 
+def _pointwise(R, S, stride, pad, kp, C) -> bool:
+    """1x1, stride 1, no padding, no K padding: the NHWC input is the column matrix."""
+    return R == 1 and S == 1 and tuple(stride) == (1, 1) and tuple(pad) == (0, 0) and kp == C
+
+
 class _QConv(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, b, geom, precision):
@@ -52,6 +57,10 @@ class _QConv(torch.autograd.Function):
             if ops.implicit_conv_ok(C, torch.int8):
                 # implicit GEMM: the producer warp gathers the column tiles from xq
                 y, (P, Q) = ops.conv_fwd_implicit(xq, wq, R, S, stride, pad, xs, ws, b)
+            elif _pointwise(R, S, stride, pad, kp, C):
+                # 1x1 / stride 1: the NHWC int8 tensor IS the column matrix
+                _, y = ops.gemm_s8(xq.view(N * H * W, C), wq, xs, ws, b)
+                P, Q = H, W
             else:
                 A, (P, Q) = ops.im2col(xq, R, S, stride, pad, ld=kp)
                 _, y = ops.gemm_s8(A, wq, xs, ws, b)
@@ -62,6 +71,9 @@ class _QConv(torch.autograd.Function):
             if ops.implicit_conv_ok(C, torch.float16):
                 y, (P, Q) = ops.conv_fwd_implicit(x16, w16, R, S, stride, pad, bias=b,
                                                   out_dtype=torch.float16)
+            elif _pointwise(R, S, stride, pad, kp, C):
+                y = ops.gemm_f16(x16.reshape(N * H * W, C), w16, out_dtype=torch.float16, bias=b)
+                P, Q = H, W
             else:
                 A, (P, Q) = ops.im2col(x16, R, S, stride, pad, ld=kp)
                 y = ops.gemm_f16(A, w16, out_dtype=torch.float16, bias=b)
@@ -122,7 +134,7 @@ def _cols32(x, R, S, stride, pad, kp):
     the byte-exact im2col runs over x viewed as FP16 pairs (each tap's channel run is
     contiguous, so C FP32 channels are 2C 16-bit lanes; zero padding is 0.0f)."""
     N, H, W, C = x.shape
-    if R == 1 and S == 1 and tuple(stride) == (1, 1) and tuple(pad) == (0, 0) and kp == C:
+    if _pointwise(R, S, stride, pad, kp, C):
         return x.reshape(N * H * W, C), (H, W)
     A, pq = ops.im2col(x.view(torch.float16), R, S, stride, pad, ld=2 * kp)
     return A.view(torch.float32), pq
@@ -156,7 +168,7 @@ class _QConv32(torch.autograd.Function):
         dx = dw = db = None
         if ctx.needs_input_grad[0]:
             dcol = ops.gemm_f32(dy2, w2, b_mn=True)  # [NPQ, kp]
-            if R == 1 and S == 1 and tuple(stride) == (1, 1) and tuple(pad) == (0, 0) and ctx.kp == C:
+            if _pointwise(R, S, stride, pad, ctx.kp, C):
                 dx = dcol.view(N, H, W, C)
             else:
                 dx = ops.col2im(dcol, (N, H, W, C), R, S, stride, pad)
