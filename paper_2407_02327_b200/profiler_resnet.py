@@ -12,8 +12,9 @@ the conv model on B200 numbers, as `profiler.profile_bert` does for BERT-base.
                    op's forward and forward+backward kernels (launches queued behind a
                    device spin, CUDA events, median). The operator is fed the format
                    its producer hands it at that precision (FP16 conv: FP16 input), and
-                   the INT8 conv's input quantizer -- a cast the cost mapper charges
-                   separately (cost_mapper.cpp:36-40) -- is measured and netted out.
+                   the conversions the cost mapper charges itself (cost_mapper.cpp:36-50:
+                   the forward weight cast; for INT8 also the input quantizer and the
+                   FP32 -> FP16 cast of the incoming gradient) are measured and netted out.
 * ``cast_samples`` / ``devices`` -- as for BERT (profiler.measure_cast_samples).
 * ``tensor_stats`` -- K5 device statistics of every conv's input, weight and
                    incoming gradient over FP32 training steps of `resnet.ResNet50`.
@@ -130,9 +131,24 @@ def measure_conv(n, h, c, cout, r, stride, pad, precision: str, reps: int = 5) -
         torch.autograd.grad(qconv2d(xg, w, None, st, pd, precision), wrt, gy)
 
     f, t = _spin_ns(fwd, reps), _spin_ns(fwd_bwd, reps)
-    if precision == INT8:  # the input quantizer is the cost mapper's cast, not the op's
-        qt = _spin_ns(lambda: ops.quantize_per_tensor(x32.view(1, -1)), reps)
-        f, t = max(1, f - qt), max(2, t - qt)
+    # Conversions the cost mapper charges itself (cost_mapper.cpp:36-50) are netted
+    # out of the op: the forward weight cast (both precisions), and for INT8 the
+    # input quantizer and the FP32 -> FP16 cast of the incoming gradient.
+    w2 = w.detach().reshape(cout, -1).contiguous()
+    if precision == INT8:
+        k = w2.shape[1]
+        w2p = torch.zeros(cout, (k + 15) // 16 * 16, device="cuda") if k % 16 else w2
+        if k % 16:
+            w2p[:, :k] = w2
+        fc = _spin_ns(lambda: ops.quantize_per_tensor(x32.view(1, -1)), reps) + \
+            _spin_ns(lambda: ops.quantize_per_channel(w2p), reps)
+        g2 = gy.reshape(-1, cout).contiguous()
+        bc = _spin_ns(lambda: ops.cast_transpose(g2, True, False, False), reps)
+    elif precision == FP16:
+        fc, bc = _spin_ns(lambda: ops.cast(w2, torch.float16), reps), 0
+    else:
+        fc = bc = 0
+    f, t = max(1, f - fc), max(2, t - fc - bc)
     t = max(t, f + 1)
     return {"pure_cost_ns": t, "fwd_fraction": min(1.0, f / t),
             "memory_bytes": conv_memory_bytes(precision, n, h, c, cout, r)}
