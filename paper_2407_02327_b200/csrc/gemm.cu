@@ -399,16 +399,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (kLay & 4) {
-                    const int kbyte = kb * BK_BYTES;  // byte offset along K = (tap, c)
+                    // A 64-byte channel run (INT8 C = 64) fills half a K-slice: the slice
+                    // then holds two taps, four 16-byte chunks each (taps past R*S and
+                    // rows past M are zero-filled).
+                    const int halves = (rowbytes & (BK_BYTES - 1)) ? 2 : 1;
+                    const uint32_t sbase = ptx::smem_u32(sa);
+                    for (int hf = 0; hf < halves; ++hf) {
+                    const int kbyte = kb * BK_BYTES + hf * 64;  // byte offset along K = (tap, c)
                     const int tap = kbyte / rowbytes;
                     const int cbyte = kbyte - tap * rowbytes;
                     const int r = tap / p.cS, sx = tap - r * p.cS;
-                    const uint32_t sbase = ptx::smem_u32(sa);
+                    const bool tap_ok = tap < p.cR * p.cS;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int row = lane + 32 * i;
                         int h = hb[i] + p.ctap * r, w = wb[i] + p.ctap * sx;
-                        bool ok = rok[i];
+                        bool ok = rok[i] && tap_ok;
                         if (p.cdvh > 1) {  // dgrad of a strided conv: only taps on the stride grid
                             ok = ok && h >= 0 && h % p.cdvh == 0;
                             h /= p.cdvh;
@@ -421,10 +427,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint8_t* src =
                             ok ? pix[i] + (static_cast<int64_t>(h) * p.cW + w) * rowbytes + cbyte : p.cx;
                         const uint32_t nbytes = ok ? 16u : 0u;
+                        if (halves == 1) {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            ptx::cp_async16_zfill(sbase + row * 128 + ((j ^ (row & 7)) << 4), src + 16 * j,
-                                                  nbytes);
+                            for (int j = 0; j < 8; ++j)
+                                ptx::cp_async16_zfill(sbase + row * 128 + ((j ^ (row & 7)) << 4), src + 16 * j,
+                                                      nbytes);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                ptx::cp_async16_zfill(sbase + row * 128 + (((hf * 4 + j) ^ (row & 7)) << 4),
+                                                      src + 16 * j, nbytes);
+                        }
+                    }
                     }
                 } else {
                     constexpr int kRows = kI8 ? 4 : 2;  // K-rows (pixels) per lane per stage
@@ -1977,8 +1991,8 @@ int qsync_conv_fwd_implicit(const void* x, int dtype, int64_t N, int64_t H, int6
     const int eb = dtype == QSYNC_I8 ? 1 : 2;
     QSB_REQUIRE(N > 0 && H > 0 && W > 0 && C > 0 && R > 0 && S > 0 && sh > 0 && sw > 0 && ph >= 0 && pw >= 0,
                 QSYNC_ERR_DOMAIN, "bad conv geometry");
-    QSB_REQUIRE((C * eb) % BK_BYTES == 0, QSYNC_ERR_DOMAIN,
-                "implicit conv needs C * element size to be a multiple of 128 bytes (use im2col)");
+    QSB_REQUIRE((C * eb) % 64 == 0, QSYNC_ERR_DOMAIN,
+                "implicit conv needs C * element size to be a multiple of 64 bytes (use im2col)");
     const int64_t P = (H + 2 * ph - R) / sh + 1, Q = (W + 2 * pw - S) / sw + 1;
     QSB_REQUIRE(P > 0 && Q > 0, QSYNC_ERR_DOMAIN, "conv output would be empty");
     const int64_t M = N * P * Q, K = static_cast<int64_t>(R) * S * C;
@@ -2001,7 +2015,8 @@ int qsync_conv_fwd_implicit(const void* x, int dtype, int64_t N, int64_t H, int6
     p.cC = static_cast<int>(C); p.cP = static_cast<int>(P); p.cQ = static_cast<int>(Q);
     p.cR = R; p.cS = S; p.csh = sh; p.csw = sw; p.cph = ph; p.cpw = pw;
     p.ctap = 1; p.cdvh = 1; p.cdvw = 1;
-    const int lay = g_conv_tma ? 32 : 4;
+    // 64-byte channel runs go through the gather lanes (two taps per 128-byte K-slice)
+    const int lay = (g_conv_tma && (C * eb) % BK_BYTES == 0) ? 32 : 4;
     if (dtype == QSYNC_I8) {
         QSB_REQUIRE(scale_a && scale_b, QSYNC_ERR_VALIDATION, "the dequant epilogue needs scale_a and scale_b");
         p.scale_a = scale_a;

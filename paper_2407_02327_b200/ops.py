@@ -322,9 +322,10 @@ def im2col(x: torch.Tensor, R: int, S: int, stride, pad, dil=(1, 1), ld: int | N
 
 
 def implicit_conv_ok(C: int, dtype: torch.dtype) -> bool:
-    """Whether the implicit-GEMM forward applies: each (r,s) tap's channel run
-    must be a whole number of 128-byte K-slices."""
-    return (C * (1 if dtype == torch.int8 else 2)) % 128 == 0
+    """Whether the implicit-GEMM forward applies: each (r,s) tap's channel run must
+    be a whole number of 128-byte K-slices, or exactly half of one (64 bytes: two
+    taps per slice, gathered by the cp.async lanes)."""
+    return (C * (1 if dtype == torch.int8 else 2)) % 64 == 0
 
 
 def conv_fwd_implicit(x: torch.Tensor, w2: torch.Tensor, R: int, S: int, stride, pad, scale_a=None,

@@ -2,10 +2,11 @@
 
 Forward is a GEMM over the column matrix A [N*P*Q, R*S*C] and the KRSC weight
 W [Cout, R*S*C] (below-16-bit convolutions are channels-last).  When
-each (r,s) tap's channel run is a whole number of 128-byte K-slices (C % 128 INT8,
-C % 64 FP16: every ResNet-50 conv but conv1) A is never materialised: the GEMM's
-producer warp gathers it tile by tile from the NHWC input (implicit GEMM,
-`qsync_conv_fwd_implicit`); otherwise im2col builds it.
+each (r,s) tap's channel run is a whole number of 128-byte K-slices or half of one
+(C % 64 INT8, C % 32 FP16: every ResNet-50 conv but conv1) A is never materialised:
+the GEMM's producer warp gathers it tile by tile from the NHWC input (implicit GEMM,
+`qsync_conv_fwd_implicit`); a 1x1/stride-1 conv reads the NHWC tensor itself as A;
+otherwise im2col builds it.
   * INT8 -- x quantized once per tensor (1 B/elem NHWC), im2col of the int8
             tensor, per-channel weight scales, tcgen05 kind::i8 GEMM with the fused
             dequant + bias epilogue -> FP32 NHWC output (graph.hpp:38-40).
@@ -54,13 +55,16 @@ class _QConv(torch.autograd.Function):
             xq, xs, _ = ops.quantize_per_tensor(x.reshape(1, -1))
             xq = xq.view(N, H, W, C)
             wq, ws, _ = ops.quantize_per_channel(w2)
-            if ops.implicit_conv_ok(C, torch.int8):
-                # implicit GEMM: the producer warp gathers the column tiles from xq
-                y, (P, Q) = ops.conv_fwd_implicit(xq, wq, R, S, stride, pad, xs, ws, b)
-            elif _pointwise(R, S, stride, pad, kp, C):
+            # Order measured on the ResNet-50 shapes: the TMA-im2col implicit GEMM
+            # (whole 128-byte runs) beats a plain GEMM over the NHWC tensor for 1x1
+            # convs at M = 200k; the plain GEMM beats the cp.async gather (64-byte runs).
+            if C % 128 and _pointwise(R, S, stride, pad, kp, C):
                 # 1x1 / stride 1: the NHWC int8 tensor IS the column matrix
                 _, y = ops.gemm_s8(xq.view(N * H * W, C), wq, xs, ws, b)
                 P, Q = H, W
+            elif ops.implicit_conv_ok(C, torch.int8):
+                # implicit GEMM: the producer warp gathers the column tiles from xq
+                y, (P, Q) = ops.conv_fwd_implicit(xq, wq, R, S, stride, pad, xs, ws, b)
             else:
                 A, (P, Q) = ops.im2col(xq, R, S, stride, pad, ld=kp)
                 _, y = ops.gemm_s8(A, wq, xs, ws, b)
@@ -68,12 +72,12 @@ class _QConv(torch.autograd.Function):
         else:
             x16 = x if x.dtype == torch.float16 else ops.cast(x.contiguous(), torch.float16)
             w16 = ops.cast(w2, torch.float16)
-            if ops.implicit_conv_ok(C, torch.float16):
-                y, (P, Q) = ops.conv_fwd_implicit(x16, w16, R, S, stride, pad, bias=b,
-                                                  out_dtype=torch.float16)
-            elif _pointwise(R, S, stride, pad, kp, C):
+            if C % 64 and _pointwise(R, S, stride, pad, kp, C):
                 y = ops.gemm_f16(x16.reshape(N * H * W, C), w16, out_dtype=torch.float16, bias=b)
                 P, Q = H, W
+            elif ops.implicit_conv_ok(C, torch.float16):
+                y, (P, Q) = ops.conv_fwd_implicit(x16, w16, R, S, stride, pad, bias=b,
+                                                  out_dtype=torch.float16)
             else:
                 A, (P, Q) = ops.im2col(x16, R, S, stride, pad, ld=kp)
                 y = ops.gemm_f16(A, w16, out_dtype=torch.float16, bias=b)

@@ -117,7 +117,11 @@ def test_fp16_conv_vs_torch_fp32(case):
 
 @pytest.mark.parametrize("geom", [(2, 14, 14, 128, 256, 3, 1, 1), (2, 15, 15, 128, 128, 3, 2, 1),
                                   (3, 7, 7, 256, 512, 1, 1, 0), (1, 28, 28, 128, 64, 1, 2, 0),
-                                  (2, 9, 11, 128, 200, 3, 1, 1)])
+                                  (2, 9, 11, 128, 200, 3, 1, 1),
+                                  # 64-byte channel runs: two taps per 128-byte K-slice
+                                  (2, 14, 14, 64, 64, 3, 1, 1), (2, 15, 15, 64, 128, 3, 2, 1),
+                                  (3, 9, 9, 64, 256, 1, 1, 0), (2, 12, 12, 64, 96, 1, 2, 0),
+                                  (1, 11, 7, 192, 64, 3, 1, 1)])
 def test_implicit_conv_int8_bit_exact_vs_im2col(geom, conv_impl):
     """Implicit-GEMM forward (A gathered by the producer warp) == im2col + GEMM:
     same int8 operands, same K order -> identical int32 accumulators and epilogue."""
@@ -137,7 +141,7 @@ def test_implicit_conv_int8_bit_exact_vs_im2col(geom, conv_impl):
 
 
 @pytest.mark.parametrize("geom", [(2, 14, 14, 64, 256, 3, 1, 1), (2, 28, 28, 128, 128, 3, 2, 1),
-                                  (4, 7, 7, 64, 96, 1, 1, 0)])
+                                  (4, 7, 7, 64, 96, 1, 1, 0), (2, 10, 10, 32, 64, 3, 1, 1)])
 def test_implicit_conv_fp16_matches_im2col(geom, conv_impl):
     N, H, W, C, Co, R, st, pd = geom
     torch.manual_seed(sum(geom))
@@ -176,7 +180,7 @@ def test_implicit_conv_asymmetric_geometry(geom, conv_impl):
 def test_implicit_conv_rejects_narrow_channels():
     x = torch.zeros(1, 8, 8, 3, dtype=torch.int8, device=DEV)
     w2 = torch.zeros(16, 27, dtype=torch.int8, device=DEV)
-    with pytest.raises(Exception, match="128 bytes"):
+    with pytest.raises(Exception, match="64 bytes"):
         ops.conv_fwd_implicit(x, w2, 3, 3, (1, 1), (1, 1), torch.ones(1, device=DEV), torch.ones(16, device=DEV))
 
 
